@@ -1,0 +1,184 @@
+/*
+ * volpot_b200.h -- C ABI of the B200-native FMM-step library
+ * (paper_2203_05933_b200/libvolpot_b200.so, sm_100a only).
+ *
+ * This is the drop-in boundary for the hot path of the arxiv 2203.05933
+ * volume-potential artifact (/root/reference/proj):
+ *
+ *   reference symbol                                  replaced by
+ *   ------------------------------------------------  ---------------------------
+ *   SummationPlan::SummationPlan  (summation.hpp:36-37,
+ *                                  summation.cpp:551-591)  vpg_plan_create
+ *   SummationPlan::apply          (summation.hpp:42,
+ *                                  summation.cpp:610-643)  vpg_plan_apply
+ *   SummationPlan::num_sources/num_targets/levels/
+ *                  expansion_order (summation.hpp:44-50)   vpg_plan_info
+ *   SummationPlan::~SummationPlan (summation.hpp:38)       vpg_plan_destroy
+ *   direct_sum                    (summation.hpp:22-23,
+ *                                  summation.cpp:501-540)  vpg_direct_sum
+ *   accelerated_sum               (summation.hpp:58-61)    create+apply+destroy
+ *   bessel_k0                     (kernel.hpp:11)          vpg_bessel_k0 (device)
+ *   correction loop of VolumePotentialOperator::apply
+ *                                 (potential.cpp:446-462)  vpg_corr_create/apply
+ *   build_charges                 (potential.cpp:397-412)  vpg_charges_create/apply
+ *
+ * Conventions
+ *   - Point arrays are interleaved xy float64 (the reference Vec2 is a
+ *     16-byte POD, common.hpp:13-14), so a std::vector<Vec2>::data() can be
+ *     passed zero-copy.
+ *   - Every entry point returns a vpg_status; on failure vpg_last_error()
+ *     returns a thread-local message using the reference's wording where the
+ *     reference throws (e.g. "SummationPlan::apply: charge count N does not
+ *     match source count M", summation.cpp:613-617).
+ *   - apply is const: a plan is immutable after creation and may be applied
+ *     concurrently from several host threads with distinct charge vectors
+ *     (summation.hpp:32-33).  Scratch is stream-ordered per call.
+ *   - Results are run-to-run bit-identical: no floating-point atomics, every
+ *     sum is reduced in a fixed order.
+ *   - There is no CPU fallback: without a usable sm_100 device every compute
+ *     entry point fails with VPG_ERR_CUDA.
+ */
+#ifndef VOLPOT_B200_H
+#define VOLPOT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VPG_ABI_VERSION 1
+
+typedef enum {
+    VPG_OK = 0,
+    VPG_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+    VPG_ERR_COINCIDENT = 2,       /* direct_sum coincidence (summation.cpp:535-538) */
+    VPG_ERR_DOMAIN = 3,           /* std::domain_error (kernel.cpp:169) */
+    VPG_ERR_CUDA = 4,
+    VPG_ERR_OUT_OF_MEMORY = 5
+} vpg_status;
+
+typedef enum { VPG_LAPLACE = 0, VPG_MODIFIED_HELMHOLTZ = 1 } vpg_family;
+
+/* Tree policy.  REFERENCE reproduces the reference plan bit-exactly (same
+ * bounding box, depth clamp(ceil(log4(max(ns,nt)/32)),2,7), same P, same
+ * pairwise threshold ns*nt <= 4e6), so trees and interaction lists can be
+ * compared entry by entry.  NATIVE lifts the depth cap (leaf target
+ * VPG_NATIVE_LEAF points) and never falls back to pairwise above 4e6 pairs;
+ * parity against the reference is then to the requested tolerance. */
+typedef enum { VPG_MODE_REFERENCE = 0, VPG_MODE_NATIVE = 1 } vpg_mode;
+
+/* vpg_plan_apply flags */
+#define VPG_DEVICE_POINTERS 1u /* q and out are device pointers (no copies) */
+#define VPG_NO_SYNC 2u         /* return without synchronising the stream */
+
+typedef struct vpg_plan vpg_plan;
+typedef struct vpg_corr vpg_corr;
+typedef struct vpg_charges vpg_charges;
+
+typedef struct {
+    int64_t num_sources, num_targets;
+    int32_t levels;          /* 0 = pairwise (summation.hpp:46-47) */
+    int32_t expansion_order; /* P, or max Chebyshev m (summation.hpp:48-50) */
+    int32_t family, mode, device;
+    double epsilon;          /* clamped to [1e-12, 1e-3] (summation.cpp:557) */
+    double x0, y0, side;     /* root box */
+    int64_t m2l_pairs;       /* (target box, source box) translations */
+    int64_t p2p_pairs;       /* enumerated near-field pairs, self included */
+    int64_t m2m_children, l2l_children;
+    int64_t device_bytes;    /* resident plan footprint */
+} vpg_plan_info_t;
+
+/* Phase timings of the most recent apply on a plan with profiling on, in
+ * milliseconds (CUDA events on the apply stream). */
+typedef enum {
+    VPG_PHASE_UPLOAD = 0,  /* H2D of charges (host-pointer apply only) */
+    VPG_PHASE_GATHER,      /* charges into Morton order */
+    VPG_PHASE_P2M,
+    VPG_PHASE_M2M,
+    VPG_PHASE_M2L,
+    VPG_PHASE_L2L,
+    VPG_PHASE_P2P,         /* fused L2P + near field (or pairwise / treecode) */
+    VPG_PHASE_DOWNLOAD,    /* D2H of potentials */
+    VPG_PHASE_COUNT
+} vpg_phase;
+
+const char* vpg_last_error(void);
+int vpg_abi_version(void);
+/* Number of visible devices usable by this library (sm_100). */
+int vpg_device_count(int* count);
+
+int vpg_plan_create(int family, double lambda, const double* src_xy,
+                    int64_t ns, const double* tgt_xy, int64_t nt,
+                    double epsilon, int mode, int device, vpg_plan** plan);
+/* q: ns charges; out: nt potentials in original target order.  Host
+ * pointers unless VPG_DEVICE_POINTERS.  stream: cudaStream_t or NULL for a
+ * library-owned per-call stream. */
+int vpg_plan_apply(const vpg_plan* plan, const double* q, int64_t nq,
+                   double* out, unsigned flags, void* stream);
+int vpg_plan_info(const vpg_plan* plan, vpg_plan_info_t* info);
+int vpg_plan_set_profiling(vpg_plan* plan, int on);
+int vpg_plan_phase_times(const vpg_plan* plan, float* ms /* VPG_PHASE_COUNT */);
+/* Kernel launches issued by the most recent apply. */
+int vpg_plan_last_launches(const vpg_plan* plan, int64_t* launches);
+/* Copies the device tree back for the bit-exact check.
+ * src_off/tgt_off: 4^L + 1 ints, src_ids: ns, tgt_ids: nt,
+ * src_cnt/tgt_cnt: sum_{l<=L} 4^l ints (levels concatenated, level l at
+ * (4^l-1)/3).  Any pointer may be NULL.  Fails for pairwise plans. */
+int vpg_plan_dump_tree(const vpg_plan* plan, int32_t* src_off,
+                       int32_t* src_ids, int32_t* tgt_off, int32_t* tgt_ids,
+                       int32_t* src_cnt, int32_t* tgt_cnt);
+/* M2L interaction list of one level in the reference enumeration order
+ * (summation.cpp:271-303): *ntbox target boxes (tbox, toff CSR of ntbox+1)
+ * and *nent entries (src box, offset index (dx+3)+7*(dy+3)).  Call with NULL
+ * arrays to get the sizes. */
+int vpg_plan_dump_m2l(const vpg_plan* plan, int level, int32_t* ntbox,
+                      int64_t* nent, int32_t* tbox, int32_t* toff,
+                      int32_t* src, int32_t* oidx);
+int vpg_plan_destroy(vpg_plan* plan);
+
+/* direct_sum (summation.cpp:501-540).  skip_coincident = 0: reference
+ * semantics, returns VPG_ERR_COINCIDENT and the smallest (i, j) when a
+ * target coincides with a source; 1: pairwise-mode semantics, r^2 == 0
+ * pairs are skipped (summation.cpp:630).  Host pointers unless
+ * VPG_DEVICE_POINTERS. */
+int vpg_direct_sum(int family, double lambda, const double* src_xy,
+                   const double* q, int64_t ns, const double* tgt_xy,
+                   int64_t nt, double* out, int skip_coincident,
+                   int64_t* clash_i, int64_t* clash_j, int device,
+                   unsigned flags, void* stream);
+
+/* K0 on the device (kernel.cpp:167-172); x <= 0 -> VPG_ERR_DOMAIN with the
+ * reference message.  Host arrays. */
+int vpg_bessel_k0(const double* x, int64_t n, double* out, int device);
+
+/* Correction map (potential.cpp:92-110, 446-462): out[t] += sum over blocks
+ * k in [blk_off[t], blk_off[t+1]) of pool_row(blk_pool[k]) . f[node_off[cell]
+ * ..]. Rows are a flat pool with pool_off CSR (shared box-lattice rows are
+ * stored once). */
+int vpg_corr_create(int64_t nt, const int32_t* blk_off, int64_t nblocks,
+                    const int32_t* blk_cell, const int32_t* blk_pool,
+                    int64_t npool, const int64_t* pool_off,
+                    const double* pool_vals, int64_t ncell,
+                    const int32_t* node_off, int device, vpg_corr** corr);
+/* f: ndofs samples, out: nt values accumulated into (out += C f). */
+int vpg_corr_apply(const vpg_corr* corr, const double* f, int64_t nf,
+                   double* out, unsigned flags, void* stream);
+int vpg_corr_destroy(vpg_corr* corr);
+
+/* build_charges (potential.cpp:397-412): charges[src_off[c] + s] =
+ * src_wj[...] * sum_i O_type(c)[s][i] f[node_off[c] + i].  Two cell types
+ * (0 = box, 1 = triangle), O row-major nq x np. */
+int vpg_charges_create(int64_t ncell, const int32_t* cell_type,
+                       const int32_t* node_off, const int32_t* src_off,
+                       const double* over0, int np0, int nq0,
+                       const double* over1, int np1, int nq1,
+                       const double* src_wj, int device, vpg_charges** ch);
+int vpg_charges_apply(const vpg_charges* ch, const double* f, int64_t nf,
+                      double* charges, unsigned flags, void* stream);
+int vpg_charges_destroy(vpg_charges* ch);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VOLPOT_B200_H */

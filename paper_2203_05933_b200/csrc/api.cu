@@ -1,0 +1,474 @@
+// api.cu -- the extern "C" boundary (include/volpot_b200.h): argument
+// checks with the reference's error semantics, device selection, per-device
+// tables, stream handling and host<->device staging around the kernels.
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <set>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "k0.cuh"
+#include "plan.cuh"
+
+struct vpg_plan {
+    vpg::Plan impl;
+};
+
+namespace vpg {
+
+namespace {
+thread_local std::string t_err;
+std::mutex g_mu;
+struct DeviceTables {
+    double2* log_tab = nullptr;
+    double* k0_tab = nullptr;
+};
+std::map<int, DeviceTables> g_tables;
+std::set<std::pair<const void*, int>> g_optin;
+std::set<int> g_ready;
+}  // namespace
+
+void set_error(const std::string& msg) { t_err = msg; }
+const char* get_error() { return t_err.c_str(); }
+
+void use_device(int device) {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        (void)cudaGetLastError();
+        throw Error{VPG_ERR_CUDA, std::string("no CUDA device available: ") +
+                                      (e == cudaSuccess ? "device count 0" : cudaGetErrorString(e))};
+    }
+    if (device < 0 || device >= count)
+        throw Error{VPG_ERR_INVALID_ARGUMENT, "device " + std::to_string(device) + " out of range"};
+    VPG_CUDA(cudaSetDevice(device));
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g_ready.count(device)) return;
+    cudaDeviceProp prop;
+    VPG_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        throw Error{VPG_ERR_CUDA, std::string("libvolpot_b200 is built for sm_100a; device is ") +
+                                      prop.name + " sm_" + std::to_string(prop.major) +
+                                      std::to_string(prop.minor)};
+    // Keep stream-ordered scratch in the pool between applies.
+    cudaMemPool_t pool;
+    VPG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = ~uint64_t(0);
+    VPG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    g_ready.insert(device);
+}
+
+static DeviceTables& tables_locked(int dev) {
+    DeviceTables& t = g_tables[dev];
+    if (!t.log_tab) {
+        // (RN(1/c), -ln RN(1/c)) at the centres c = 1 + i/256, i = 0..256
+        std::vector<double2> h(kLogTableSize);
+        for (int i = 0; i < kLogTableSize; ++i) {
+            const long double c = 1.0L + (long double)i / (kLogTableSize - 1);
+            const double inv = double(1.0L / c);
+            h[size_t(i)] = make_double2(inv, double(-std::log((long double)inv)));
+        }
+        VPG_CUDA(cudaMalloc(&t.log_tab, sizeof(double2) * h.size()));
+        VPG_CUDA(cudaMemcpy(t.log_tab, h.data(), sizeof(double2) * h.size(), cudaMemcpyHostToDevice));
+    }
+    if (!t.k0_tab) {
+        std::vector<double> h(size_t(kK0Intervals) * kK0Coeffs);
+        k0_fit_host(h.data());
+        VPG_CUDA(cudaMalloc(&t.k0_tab, sizeof(double) * h.size()));
+        VPG_CUDA(cudaMemcpy(t.k0_tab, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
+    }
+    return t;
+}
+
+const double2* log_table_dev() {
+    int dev = 0;
+    VPG_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_mu);
+    return tables_locked(dev).log_tab;
+}
+const double* k0_table_dev() {
+    int dev = 0;
+    VPG_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_mu);
+    return tables_locked(dev).k0_tab;
+}
+
+void smem_optin(const void* func, int bytes) {
+    int dev = 0;
+    VPG_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g_optin.count({func, dev})) return;
+    VPG_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    g_optin.insert({func, dev});
+}
+
+int64_t Plan::device_bytes() const {
+    return int64_t(src.bytes() + tgt.bytes() + src_sorted.bytes() + tgt_sorted.bytes() +
+                   src_off.bytes() + src_ids.bytes() + tgt_off.bytes() + tgt_ids.bytes() +
+                   src_cnt.bytes() + tgt_cnt.bytes() + m2l_tbox.bytes() + m2l_toff.bytes() +
+                   m2l_src.bytes() + m2l_oidx.bytes() + m2l_batches.bytes() + m2m_ops.bytes() +
+                   l2l_ops.bytes() + h_t.bytes() + dpow.bytes() + logmd.bytes() +
+                   p2p_chunks.bytes() + p2m_leaves.bytes() + updown_boxes.bytes() +
+                   helm_nodes.bytes() + helm_bw.bytes() + exp_off_dev.bytes());
+}
+
+// Runs f, mapping exceptions to status codes + thread-local message.
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return VPG_OK;
+    } catch (const Error& e) {
+        set_error(e.msg);
+        return e.status;
+    } catch (const std::bad_alloc&) {
+        set_error("host allocation failed");
+        return VPG_ERR_OUT_OF_MEMORY;
+    } catch (const std::exception& e) {
+        set_error(e.what());
+        return VPG_ERR_CUDA;
+    }
+}
+
+// Stream to run on: the caller's, or a private one for this call.
+struct CallStream {
+    cudaStream_t s = nullptr;
+    bool owned = false;
+    explicit CallStream(void* user) {
+        if (user) {
+            s = static_cast<cudaStream_t>(user);
+        } else {
+            VPG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+            owned = true;
+        }
+    }
+    ~CallStream() {
+        if (owned) cudaStreamDestroy(s);
+    }
+};
+
+template <typename T>
+struct Scratch {  // stream-ordered device scratch
+    T* p = nullptr;
+    cudaStream_t s;
+    Scratch(size_t n, cudaStream_t st) : s(st) {
+        if (n) VPG_CUDA(cudaMallocAsync(&p, n * sizeof(T), st));
+    }
+    ~Scratch() {
+        if (p) cudaFreeAsync(p, s);
+    }
+};
+
+}  // namespace vpg
+
+using namespace vpg;
+
+extern "C" {
+
+const char* vpg_last_error(void) { return get_error(); }
+int vpg_abi_version(void) { return VPG_ABI_VERSION; }
+
+int vpg_device_count(int* count) {
+    return guarded([&] {
+        if (!count) throw Error{VPG_ERR_INVALID_ARGUMENT, "count is NULL"};
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess) {
+            (void)cudaGetLastError();
+            n = 0;
+        }
+        int usable = 0;
+        for (int d = 0; d < n; ++d) {
+            cudaDeviceProp p;
+            if (cudaGetDeviceProperties(&p, d) == cudaSuccess && p.major == 10) ++usable;
+        }
+        *count = usable;
+    });
+}
+
+int vpg_plan_create(int family, double lambda, const double* src_xy, int64_t ns,
+                    const double* tgt_xy, int64_t nt, double epsilon, int mode,
+                    int device, vpg_plan** plan) {
+    return guarded([&] {
+        if (!plan) throw Error{VPG_ERR_INVALID_ARGUMENT, "plan is NULL"};
+        *plan = nullptr;
+        if (family != VPG_LAPLACE && family != VPG_MODIFIED_HELMHOLTZ)
+            throw Error{VPG_ERR_INVALID_ARGUMENT, "unknown kernel family"};
+        if (family == VPG_MODIFIED_HELMHOLTZ && !(lambda > 0.0))  // kernel.cpp:195-196
+            throw Error{VPG_ERR_INVALID_ARGUMENT, "make_kernel: modified Helmholtz needs lambda > 0"};
+        if (ns < 0 || nt < 0 || (ns > 0 && !src_xy) || (nt > 0 && !tgt_xy))
+            throw Error{VPG_ERR_INVALID_ARGUMENT, "bad point arrays"};
+        if (ns > INT32_MAX || nt > INT32_MAX)
+            throw Error{VPG_ERR_INVALID_ARGUMENT, "point count exceeds int32 indexing"};
+        if (mode != VPG_MODE_REFERENCE && mode != VPG_MODE_NATIVE)
+            throw Error{VPG_ERR_INVALID_ARGUMENT, "unknown tree mode"};
+        use_device(device);
+        auto holder = std::make_unique<vpg_plan>();
+        Plan& pl = holder->impl;
+        pl.device = device;
+        VPG_CUDA(cudaDeviceGetAttribute(&pl.sm_count, cudaDevAttrMultiProcessorCount, device));
+        pl.family = family;
+        pl.lambda = family == VPG_LAPLACE ? 0.0 : lambda;
+        pl.mode = mode;
+        pl.eps = std::min(std::max(epsilon, 1e-12), 1e-3);  // summation.cpp:557
+        if (std::isnan(epsilon)) pl.eps = 1e-12;
+        pl.ns = ns;
+        pl.nt = nt;
+        pl.src.alloc(size_t(ns));
+        pl.tgt.alloc(size_t(nt));
+        if (ns) VPG_CUDA(cudaMemcpy(pl.src.p, src_xy, sizeof(double2) * size_t(ns), cudaMemcpyHostToDevice));
+        if (nt) VPG_CUDA(cudaMemcpy(pl.tgt.p, tgt_xy, sizeof(double2) * size_t(nt), cudaMemcpyHostToDevice));
+        build_tree(pl);
+        if (!pl.direct) {
+            if (family == VPG_LAPLACE) build_laplace_ops(pl);
+            else build_helm_ops(pl);
+        }
+        (void)log_table_dev();
+        (void)k0_table_dev();
+        VPG_CUDA(cudaDeviceSynchronize());
+        *plan = holder.release();
+    });
+}
+
+int vpg_plan_apply(const vpg_plan* plan, const double* q, int64_t nq, double* out,
+                   unsigned flags, void* stream) {
+    return guarded([&] {
+        if (!plan) throw Error{VPG_ERR_INVALID_ARGUMENT, "plan is NULL"};
+        const Plan& pl = plan->impl;
+        if (nq != pl.ns)  // summation.cpp:613-617
+            throw Error{VPG_ERR_INVALID_ARGUMENT,
+                        "SummationPlan::apply: charge count " + std::to_string(nq) +
+                            " does not match source count " + std::to_string(pl.ns)};
+        if ((pl.ns > 0 && !q) || (pl.nt > 0 && !out))
+            throw Error{VPG_ERR_INVALID_ARGUMENT, "NULL charge or output array"};
+        VPG_CUDA(cudaSetDevice(pl.device));
+        CallStream cs(stream);
+        cudaStream_t st = cs.s;
+        const bool dev = flags & VPG_DEVICE_POINTERS;
+        Scratch<double> qd(dev ? 0 : size_t(pl.ns), st), od(dev ? 0 : size_t(pl.nt), st);
+        const double* q_dev = dev ? q : qd.p;
+        double* out_dev = dev ? out : od.p;
+
+        const bool prof = pl.profiling;
+        cudaEvent_t ev[VPG_PHASE_COUNT + 1] = {};
+        if (prof)
+            for (auto& e : ev) VPG_CUDA(cudaEventCreate(&e));
+        struct EvGuard {
+            cudaEvent_t* e;
+            bool on;
+            ~EvGuard() {
+                if (on)
+                    for (int i = 0; i <= VPG_PHASE_COUNT; ++i) cudaEventDestroy(e[i]);
+            }
+        } eg{ev, prof};
+        // event i marks the start of phase i; ev[PHASE_COUNT] the end
+        if (prof) VPG_CUDA(cudaEventRecord(ev[VPG_PHASE_UPLOAD], st));
+        if (!dev && pl.ns)
+            VPG_CUDA(cudaMemcpyAsync(qd.p, q, sizeof(double) * size_t(pl.ns), cudaMemcpyHostToDevice, st));
+        int64_t launches = 0;
+        cudaEvent_t* inner = prof ? ev + 1 : nullptr;  // GATHER .. DOWNLOAD
+        if (pl.direct) {
+            if (prof)
+                for (int i = 0; i < 6; ++i) VPG_CUDA(cudaEventRecord(inner[i], st));
+            pairwise_apply(pl, q_dev, out_dev, st, launches);
+            if (prof) VPG_CUDA(cudaEventRecord(inner[6], st));
+        } else if (pl.family == VPG_LAPLACE) {
+            laplace_apply(pl, q_dev, out_dev, st, inner, launches);
+        } else {
+            helm_apply(pl, q_dev, out_dev, st, inner, launches);
+        }
+        if (!dev && pl.nt)
+            VPG_CUDA(cudaMemcpyAsync(out, od.p, sizeof(double) * size_t(pl.nt), cudaMemcpyDeviceToHost, st));
+        if (prof) VPG_CUDA(cudaEventRecord(ev[VPG_PHASE_COUNT], st));
+        const bool sync = !(flags & VPG_NO_SYNC) || cs.owned || prof;
+        if (sync) VPG_CUDA(cudaStreamSynchronize(st));
+        if (prof) {
+            std::lock_guard<std::mutex> lk(pl.prof_mu);
+            for (int i = 0; i < VPG_PHASE_COUNT; ++i)
+                VPG_CUDA(cudaEventElapsedTime(&pl.phase_ms[i], ev[i], ev[i + 1]));
+        }
+        pl.last_launches = launches;
+    });
+}
+
+int vpg_plan_info(const vpg_plan* plan, vpg_plan_info_t* info) {
+    return guarded([&] {
+        if (!plan || !info) throw Error{VPG_ERR_INVALID_ARGUMENT, "NULL argument"};
+        const Plan& pl = plan->impl;
+        vpg_plan_info_t r{};
+        r.num_sources = pl.ns;
+        r.num_targets = pl.nt;
+        r.levels = pl.direct ? 0 : pl.L;
+        r.expansion_order = pl.direct ? 0 : pl.P;
+        r.family = pl.family;
+        r.mode = pl.mode;
+        r.device = pl.device;
+        r.epsilon = pl.eps;
+        r.x0 = pl.x0;
+        r.y0 = pl.y0;
+        r.side = pl.side;
+        r.m2l_pairs = pl.direct ? 0 : pl.n_m2l;
+        r.p2p_pairs = pl.direct ? pl.ns * pl.nt : pl.p2p_pairs;
+        r.m2m_children = pl.m2m_children;
+        r.l2l_children = pl.l2l_children;
+        r.device_bytes = pl.device_bytes();
+        *info = r;
+    });
+}
+
+int vpg_plan_set_profiling(vpg_plan* plan, int on) {
+    return guarded([&] {
+        if (!plan) throw Error{VPG_ERR_INVALID_ARGUMENT, "plan is NULL"};
+        plan->impl.profiling = on != 0;
+    });
+}
+
+int vpg_plan_phase_times(const vpg_plan* plan, float* ms) {
+    return guarded([&] {
+        if (!plan || !ms) throw Error{VPG_ERR_INVALID_ARGUMENT, "NULL argument"};
+        std::lock_guard<std::mutex> lk(plan->impl.prof_mu);
+        std::memcpy(ms, plan->impl.phase_ms, sizeof(float) * VPG_PHASE_COUNT);
+    });
+}
+
+int vpg_plan_last_launches(const vpg_plan* plan, int64_t* launches) {
+    return guarded([&] {
+        if (!plan || !launches) throw Error{VPG_ERR_INVALID_ARGUMENT, "NULL argument"};
+        *launches = plan->impl.last_launches;
+    });
+}
+
+int vpg_plan_dump_tree(const vpg_plan* plan, int32_t* src_off, int32_t* src_ids,
+                       int32_t* tgt_off, int32_t* tgt_ids, int32_t* src_cnt,
+                       int32_t* tgt_cnt) {
+    return guarded([&] {
+        if (!plan) throw Error{VPG_ERR_INVALID_ARGUMENT, "plan is NULL"};
+        const Plan& pl = plan->impl;
+        if (pl.direct) throw Error{VPG_ERR_INVALID_ARGUMENT, "pairwise plan has no tree"};
+        VPG_CUDA(cudaSetDevice(pl.device));
+        auto cp = [](int32_t* dst, const DBuf<int32_t>& s, size_t n) {
+            if (dst && n) VPG_CUDA(cudaMemcpy(dst, s.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        };
+        const size_t nleaf = size_t(1) << (2 * pl.L);
+        cp(src_off, pl.src_off, nleaf + 1);
+        cp(tgt_off, pl.tgt_off, nleaf + 1);
+        cp(src_ids, pl.src_ids, size_t(pl.ns));
+        cp(tgt_ids, pl.tgt_ids, size_t(pl.nt));
+        cp(src_cnt, pl.src_cnt, size_t(lvl_base(pl.L + 1)));
+        cp(tgt_cnt, pl.tgt_cnt, size_t(lvl_base(pl.L + 1)));
+    });
+}
+
+int vpg_plan_dump_m2l(const vpg_plan* plan, int level, int32_t* ntbox, int64_t* nent,
+                      int32_t* tbox, int32_t* toff, int32_t* src, int32_t* oidx) {
+    return guarded([&] {
+        if (!plan) throw Error{VPG_ERR_INVALID_ARGUMENT, "plan is NULL"};
+        const Plan& pl = plan->impl;
+        if (pl.direct || level < 2 || level > pl.L)
+            throw Error{VPG_ERR_INVALID_ARGUMENT, "level out of range"};
+        VPG_CUDA(cudaSetDevice(pl.device));
+        const int64_t t0 = pl.lvl_tfirst[size_t(level)], t1 = pl.lvl_tfirst[size_t(level + 1)];
+        std::vector<int32_t> off(size_t(t1 - t0 + 1));
+        VPG_CUDA(cudaMemcpy(off.data(), pl.m2l_toff.p + t0, off.size() * sizeof(int32_t),
+                            cudaMemcpyDeviceToHost));
+        const int64_t e0 = off.front(), e1 = off.back();
+        if (ntbox) *ntbox = int32_t(t1 - t0);
+        if (nent) *nent = e1 - e0;
+        if (tbox && t1 > t0)
+            VPG_CUDA(cudaMemcpy(tbox, pl.m2l_tbox.p + t0, size_t(t1 - t0) * sizeof(int32_t),
+                                cudaMemcpyDeviceToHost));
+        if (toff)
+            for (size_t i = 0; i < off.size(); ++i) toff[i] = int32_t(off[i] - e0);
+        if (src && e1 > e0)
+            VPG_CUDA(cudaMemcpy(src, pl.m2l_src.p + e0, size_t(e1 - e0) * sizeof(int32_t),
+                                cudaMemcpyDeviceToHost));
+        if (oidx && e1 > e0)
+            VPG_CUDA(cudaMemcpy(oidx, pl.m2l_oidx.p + e0, size_t(e1 - e0) * sizeof(int32_t),
+                                cudaMemcpyDeviceToHost));
+    });
+}
+
+int vpg_plan_destroy(vpg_plan* plan) {
+    return guarded([&] {
+        if (!plan) return;
+        cudaSetDevice(plan->impl.device);
+        delete plan;
+    });
+}
+
+int vpg_direct_sum(int family, double lambda, const double* src_xy, const double* q,
+                   int64_t ns, const double* tgt_xy, int64_t nt, double* out,
+                   int skip_coincident, int64_t* clash_i, int64_t* clash_j, int device,
+                   unsigned flags, void* stream) {
+    return guarded([&] {
+        if (family != VPG_LAPLACE && family != VPG_MODIFIED_HELMHOLTZ)
+            throw Error{VPG_ERR_INVALID_ARGUMENT, "unknown kernel family"};
+        if (family == VPG_MODIFIED_HELMHOLTZ && !(lambda > 0.0))
+            throw Error{VPG_ERR_INVALID_ARGUMENT, "make_kernel: modified Helmholtz needs lambda > 0"};
+        if (ns < 0 || nt < 0 || (ns && (!src_xy || !q)) || (nt && (!tgt_xy || !out)))
+            throw Error{VPG_ERR_INVALID_ARGUMENT, "direct_sum: points/charges size mismatch"};
+        if (ns > INT32_MAX || nt > INT32_MAX)
+            throw Error{VPG_ERR_INVALID_ARGUMENT, "point count exceeds int32 indexing"};
+        if (clash_i) *clash_i = -1;
+        if (clash_j) *clash_j = -1;
+        use_device(device);
+        CallStream cs(stream);
+        cudaStream_t st = cs.s;
+        const bool dev = flags & VPG_DEVICE_POINTERS;
+        Scratch<double2> sd(dev ? 0 : size_t(ns), st), td(dev ? 0 : size_t(nt), st);
+        Scratch<double> qd(dev ? 0 : size_t(ns), st), od(dev ? 0 : size_t(nt), st);
+        Scratch<unsigned long long> clash(1, st);
+        const double2* s_p = dev ? reinterpret_cast<const double2*>(src_xy) : sd.p;
+        const double2* t_p = dev ? reinterpret_cast<const double2*>(tgt_xy) : td.p;
+        const double* q_p = dev ? q : qd.p;
+        double* o_p = dev ? out : od.p;
+        if (!dev) {
+            if (ns) {
+                VPG_CUDA(cudaMemcpyAsync(sd.p, src_xy, sizeof(double2) * size_t(ns), cudaMemcpyHostToDevice, st));
+                VPG_CUDA(cudaMemcpyAsync(qd.p, q, sizeof(double) * size_t(ns), cudaMemcpyHostToDevice, st));
+            }
+            if (nt) VPG_CUDA(cudaMemcpyAsync(td.p, tgt_xy, sizeof(double2) * size_t(nt), cudaMemcpyHostToDevice, st));
+        }
+        VPG_CUDA(cudaMemsetAsync(clash.p, 0xFF, sizeof(unsigned long long), st));
+        if (nt) {
+            if (ns)
+                direct_sum_device(family, lambda, s_p, q_p, ns, t_p, nt, o_p,
+                                  skip_coincident != 0, clash.p, st);
+            else
+                VPG_CUDA(cudaMemsetAsync(o_p, 0, sizeof(double) * size_t(nt), st));
+        }
+        unsigned long long key = ~0ull;
+        VPG_CUDA(cudaMemcpyAsync(&key, clash.p, sizeof(key), cudaMemcpyDeviceToHost, st));
+        if (!dev && nt)
+            VPG_CUDA(cudaMemcpyAsync(out, od.p, sizeof(double) * size_t(nt), cudaMemcpyDeviceToHost, st));
+        VPG_CUDA(cudaStreamSynchronize(st));
+        if (!skip_coincident && key != ~0ull) {  // summation.cpp:533-538
+            const int64_t i = int64_t(key >> 32), j = int64_t(key & 0xFFFFFFFFull);
+            if (clash_i) *clash_i = i;
+            if (clash_j) *clash_j = j;
+            throw Error{VPG_ERR_COINCIDENT, "direct_sum: target " + std::to_string(i) +
+                                                " coincides with source " + std::to_string(j)};
+        }
+    });
+}
+
+int vpg_bessel_k0(const double* x, int64_t n, double* out, int device) {
+    return guarded([&] {
+        if (n < 0 || (n && (!x || !out))) throw Error{VPG_ERR_INVALID_ARGUMENT, "bad arrays"};
+        for (int64_t i = 0; i < n; ++i)
+            if (!(x[i] > 0.0))  // kernel.cpp:169
+                throw Error{VPG_ERR_DOMAIN, "bessel_k0: argument must be positive"};
+        use_device(device);
+        CallStream cs(nullptr);
+        Scratch<double> xd(size_t(n), cs.s), od(size_t(n), cs.s);
+        if (n) VPG_CUDA(cudaMemcpyAsync(xd.p, x, sizeof(double) * size_t(n), cudaMemcpyHostToDevice, cs.s));
+        k0_device(xd.p, n, od.p, cs.s);
+        if (n) VPG_CUDA(cudaMemcpyAsync(out, od.p, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, cs.s));
+        VPG_CUDA(cudaStreamSynchronize(cs.s));
+    });
+}
+
+}  // extern "C"

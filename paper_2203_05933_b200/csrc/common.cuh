@@ -1,0 +1,131 @@
+// common.cuh -- shared device/host helpers for libvolpot_b200.so (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "volpot_b200.h"
+
+namespace vpg {
+
+// ---------------------------------------------------------------- errors --
+// Thread-local message behind vpg_last_error().
+void set_error(const std::string& msg);
+const char* get_error();
+
+struct Error {
+    int status;
+    std::string msg;
+};
+
+#define VPG_CUDA(call)                                                       \
+    do {                                                                     \
+        cudaError_t e_ = (call);                                             \
+        if (e_ != cudaSuccess) {                                             \
+            (void)cudaGetLastError();                                        \
+            throw ::vpg::Error{e_ == cudaErrorMemoryAllocation               \
+                                   ? VPG_ERR_OUT_OF_MEMORY                   \
+                                   : VPG_ERR_CUDA,                           \
+                               std::string(#call) + ": " +                   \
+                                   cudaGetErrorString(e_)};                  \
+        }                                                                    \
+    } while (0)
+
+#define VPG_LAUNCH_CHECK() VPG_CUDA(cudaGetLastError())
+
+// Verifies that `device` is a usable sm_100 device and makes it current.
+void use_device(int device);
+
+// ------------------------------------------------------------- constants --
+constexpr double kInv2Pi = 0.15915494309189533577;   // summation.cpp:15
+constexpr double kInv4Pi = 0.07957747154594766788;   // 0.25/pi, kernel.cpp:183
+constexpr double kLn2Hi = 6.93147180369123816490e-01;  // ln2 split, hi has
+constexpr double kLn2Lo = 1.90821492927058770002e-10;  // 21 trailing zeros
+
+// ------------------------------------------------------------ Morton ids --
+// Bit interleave of the reference (summation.cpp:45-62): x in even bits.
+__host__ __device__ inline uint32_t spread2(uint32_t v) {
+    v = (v | (v << 8)) & 0x00FF00FFu;
+    v = (v | (v << 4)) & 0x0F0F0F0Fu;
+    v = (v | (v << 2)) & 0x33333333u;
+    v = (v | (v << 1)) & 0x55555555u;
+    return v;
+}
+__host__ __device__ inline uint32_t mort(uint32_t ix, uint32_t iy) {
+    return spread2(ix) | (spread2(iy) << 1);
+}
+__host__ __device__ inline uint32_t squash2(uint32_t v) {
+    v &= 0x55555555u;
+    v = (v | (v >> 1)) & 0x33333333u;
+    v = (v | (v >> 2)) & 0x0F0F0F0Fu;
+    v = (v | (v >> 4)) & 0x00FF00FFu;
+    v = (v | (v >> 8)) & 0x0000FFFFu;
+    return v;
+}
+// Offset of level l in the concatenated per-level box arrays.
+__host__ __device__ inline int64_t lvl_base(int l) {
+    return ((int64_t(1) << (2 * l)) - 1) / 3;
+}
+
+// --------------------------------------------------------------- complex --
+struct cplx {
+    double re, im;
+};
+__host__ __device__ inline cplx cmul(cplx a, cplx b) {
+    return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re};
+}
+__host__ __device__ inline cplx cadd(cplx a, cplx b) {
+    return {a.re + b.re, a.im + b.im};
+}
+
+// ------------------------------------------------------------ fast log --
+// Natural log for the P2P inner loop, split as ln(x) = e*ln2 + t so the
+// caller can accumulate sum(q*t) and sum(q*e) separately and apply ln2 once
+// (hi/lo split) per target.  x = 2^e * m, m in [1,2); m is rounded to the
+// nearest centre c = 1 + i/256 (i = 0..256, from the top mantissa bits) and
+// ln(m) = -ln(1/c) + log1p(m * RN(1/c) - 1) with |m/c - 1| <= 2^-9; log1p by
+// a degree-5 polynomial (truncation 2^-54/6 < 1e-17 absolute).  Centre i = 0
+// is c = 1 exactly (RN(1/c) = 1, ln = 0), so ln(1) and ln(2^k) come out
+// exact.  The table (RN(1/c), -ln RN(1/c)) lives in shared memory replicated
+// 8x so the eight lanes of every quarter-warp 128-bit access hit distinct
+// bank groups whatever the indices (conflict-free).
+constexpr int kLogTableBits = 8;
+constexpr int kLogTableSize = (1 << kLogTableBits) + 1;
+constexpr int kLogTableCopies = 8;
+constexpr int kLogTableBytes = kLogTableSize * kLogTableCopies * 16;
+
+// Host-built table (inv_c, -ln(inv_c)) in global memory (one per device,
+// see log_table_dev()), replicated into shared memory by each CTA.
+__device__ inline void log_table_to_smem(double2* sm, const double2* gtab) {
+    for (int i = threadIdx.x; i < kLogTableSize * kLogTableCopies; i += blockDim.x)
+        sm[i] = gtab[i / kLogTableCopies];
+}
+
+// Returns t with ln(x) = ed*ln2 + t; ed = exponent as a double.
+__device__ __forceinline__ double fast_log_split(double x, const double2* tab,
+                                                 int lane8, double& ed) {
+    const int hi = __double2hiint(x);
+    const int lo = __double2loint(x);
+    const int idx = ((hi & 0x000FFFFF) + (1 << (19 - kLogTableBits))) >> (20 - kLogTableBits);
+    const double m = __hiloint2double((hi & 0x000FFFFF) | 0x3FF00000, lo);
+    // exponent field e_b in [0, 2047]: ed = (2^52 + e_b) - (2^52 + 1023)
+    ed = __hiloint2double(0x43300000, hi >> 20) - 4503599627371519.0;
+    const double2 tc = tab[idx * kLogTableCopies + lane8];
+    const double r = fma(m, tc.x, -1.0);
+    double p = fma(r, 0.2, -0.25);
+    p = fma(r, p, 0.33333333333333333333);
+    p = fma(r, p, -0.5);
+    const double r2 = r * r;
+    return tc.y + fma(r2, p, r);
+}
+
+// Per-device constant tables, built on first use (api.cu).
+const double2* log_table_dev();  // kLogTableSize entries (inv_c, -ln inv_c)
+const double* k0_table_dev();    // K0 Chebyshev fits, see k0.cuh
+
+// Opt a kernel into > 48 KB dynamic shared memory once per device.
+void smem_optin(const void* func, int bytes);
+
+}  // namespace vpg

@@ -1,0 +1,90 @@
+// k0.cuh -- modified Bessel K0 on the device, for the modified-Helmholtz
+// kernel G = (1/2pi) K0(lambda r) (kernel.cpp:181-186).
+//
+// Same split as the reference bessel_k0 (kernel.cpp:167-172):
+//   x <= 2: K0 = -(ln(x/2) + gamma) I0(x) + sum_k q^k H_k / (k!)^2,
+//           q = x^2/4 (kernel.cpp:17-31).  Here both series are evaluated
+//           as fixed degree-16 polynomials in q by Horner (the reference
+//           loop stops once a term drops below 1e-19 I0; the omitted tail is
+//           below 1e-26 for q <= 1), which keeps the warp converged.
+//   x > 2:  K0 = g(x) e^-x / sqrt(x) with g a 25-coefficient Chebyshev fit of
+//           K0(x) e^x sqrt(x) on the dyadic intervals [2,4], ..., [512,1024]
+//           (kernel.cpp:93-163).  The fit is computed on the host in long
+//           double (k0_fit.cu) and lives in global memory.
+//   exp(-x) underflow (x > ~745) returns 0 like kernel.cpp:158-161.
+#pragma once
+
+#include "common.cuh"
+
+namespace vpg {
+
+constexpr int kK0Intervals = 9;
+constexpr int kK0Coeffs = 25;
+
+__device__ __forceinline__ double k0_small(double x) {
+    // 1/(k!)^2 and H_k/(k!)^2, k = 0..16
+    constexpr double c[17] = {
+        1.0, 1.0, 0.25, 0.027777777777777776, 0.001736111111111111,
+        6.944444444444444e-05, 1.9290123456790124e-06, 3.936759889140842e-08,
+        6.151187326782565e-10, 7.594058428126624e-12, 7.594058428126623e-14,
+        6.276081345559193e-16, 4.358389823304995e-18, 2.5789288895295828e-20,
+        1.3157800456783586e-22, 5.8479113141260385e-25, 2.2843403570804838e-27};
+    constexpr double d[17] = {
+        0.0, 1.0, 0.375, 0.05092592592592592, 0.003616898148148148,
+        0.0001585648148148148, 4.72608024691358e-06, 1.0207455998272325e-07,
+        1.6718048413148328e-09, 2.1483350211950277e-11, 2.224275605476294e-13,
+        1.895299587006153e-15, 1.3525001839484812e-17, 8.201338813682637e-20,
+        4.278340826570208e-22, 1.9404708872364884e-24, 7.722735675585063e-27};
+    const double q = 0.25 * x * x;
+    double i0 = c[16], s = d[16];
+#pragma unroll
+    for (int k = 15; k >= 0; --k) {
+        i0 = fma(i0, q, c[k]);
+        s = fma(s, q, d[k]);
+    }
+    constexpr double kGamma = 0.57721566490153286061;
+    return -(log(0.5 * x) + kGamma) * i0 + s;
+}
+
+__device__ __forceinline__ double k0_large(double x, const double* tab) {
+    const double ex = exp(-x);
+    if (ex == 0.0) return 0.0;
+    // Interval iv covers (2^(iv+1), 2^(iv+2)] like the reference search
+    // (kernel.cpp:139-146); x beyond 1024 extrapolates on the last one.
+    const int e = ilogb(x);
+    int iv = (x == ldexp(1.0, e)) ? e - 2 : e - 1;
+    iv = max(0, min(iv, kK0Intervals - 1));
+    // u = (2x - (lo+hi)) / (hi-lo) with lo = 2^(iv+1): exact power-of-two
+    // scaling, one rounding, same value as the reference expression.
+    const double u = fma(x, ldexp(1.0, -iv), -3.0);
+    const double* c = tab + iv * kK0Coeffs;
+    const double u2 = 2.0 * u;
+    double b1 = 0.0, b2 = 0.0;
+#pragma unroll
+    for (int k = kK0Coeffs - 1; k >= 1; --k) {
+        const double b0 = fma(u2, b1, c[k] - b2);
+        b2 = b1;
+        b1 = b0;
+    }
+    const double g = fma(u, b1, 0.5 * c[0] - b2);
+    return g * ex * rsqrt(x);
+}
+
+__device__ __forceinline__ double k0_dev(double x, const double* tab) {
+    return x <= 2.0 ? k0_small(x) : k0_large(x, tab);
+}
+
+// q * K0(lambda r) for one pair, r^2 == 0 skipped (summation.cpp:486, 630).
+__device__ __forceinline__ double k0_pair(double tx, double ty, double sx,
+                                          double sy, double q, double lambda,
+                                          const double* tab) {
+    const double dx = tx - sx, dy = ty - sy;
+    const double r2 = fma(dy, dy, dx * dx);
+    if (r2 == 0.0) return 0.0;
+    return q * k0_dev(lambda * sqrt(r2), tab);
+}
+
+// Host: builds the Chebyshev table (kK0Intervals x kK0Coeffs doubles).
+void k0_fit_host(double* out);
+
+}  // namespace vpg

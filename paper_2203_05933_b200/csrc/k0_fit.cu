@@ -1,0 +1,82 @@
+// k0_fit.cu -- host construction of the K0 Chebyshev table used by
+// k0_large() (k0.cuh).  The reference fits g(x) = K0(x) e^x sqrt(x) by
+// 25-point Chebyshev interpolation on the dyadic intervals [2,4] .. [512,1024]
+// from long-double quadrature of the integral representation
+// K0(x) = int_0^inf exp(-x cosh t) dt (kernel.cpp:51-163).  This is an
+// independent implementation of the same construction: Gauss-Legendre
+// nodes by Newton iteration, composite panels doubled to convergence.
+#include <cmath>
+#include <vector>
+
+#include "k0.cuh"
+
+namespace vpg {
+namespace {
+
+struct GL {
+    std::vector<long double> x, w;
+    explicit GL(int n) : x(size_t(n)), w(size_t(n)) {
+        const long double pi = 3.141592653589793238462643383279502884L;
+        for (int i = 0; i < n; ++i) {
+            long double z = std::cos(pi * (i + 0.75L) / (n + 0.5L));
+            long double dp = 0;
+            for (int it = 0; it < 100; ++it) {
+                long double p0 = 1, p1 = z;
+                for (int k = 2; k <= n; ++k) {
+                    const long double p2 = ((2 * k - 1) * z * p1 - (k - 1) * p0) / k;
+                    p0 = p1;
+                    p1 = p2;
+                }
+                dp = n * (z * p1 - p0) / (z * z - 1);
+                const long double dz = p1 / dp;
+                z -= dz;
+                if (std::fabs(dz) < 1e-21L) break;
+            }
+            x[size_t(i)] = z;
+            w[size_t(i)] = 2 / ((1 - z * z) * dp * dp);
+        }
+    }
+};
+
+// e^x K0(x) for x >= 2.
+long double scaled_k0(long double x, const GL& g) {
+    const long double T = std::acosh(1.0L + 64.0L / x);  // integrand ~ e^-64
+    long double prev = 0;
+    for (int panels = 4; panels <= 4096; panels *= 2) {
+        const long double h = T / panels;
+        long double sum = 0;
+        for (int p = 0; p < panels; ++p)
+            for (size_t i = 0; i < g.x.size(); ++i) {
+                const long double t = h * (p + 0.5L * (g.x[i] + 1));
+                sum += g.w[i] * std::exp(-x * (std::cosh(t) - 1));
+            }
+        sum *= 0.5L * h;
+        if (panels > 4 && std::fabs(sum - prev) <= 1e-20L * sum) return sum;
+        prev = sum;
+    }
+    return prev;
+}
+
+}  // namespace
+
+void k0_fit_host(double* out) {
+    const GL g(20);
+    const long double pi = 3.141592653589793238462643383279502884L;
+    const int N = kK0Coeffs;
+    for (int iv = 0; iv < kK0Intervals; ++iv) {
+        const long double lo = std::ldexp(1.0L, iv + 1), hi = 2 * lo;
+        long double f[kK0Coeffs];
+        for (int j = 0; j < N; ++j) {
+            const long double th = pi * (j + 0.5L) / N;
+            const long double xj = 0.5L * (lo + hi) + 0.5L * (hi - lo) * std::cos(th);
+            f[j] = scaled_k0(xj, g) * std::sqrt(xj);
+        }
+        for (int k = 0; k < N; ++k) {
+            long double s = 0;
+            for (int j = 0; j < N; ++j) s += f[j] * std::cos(k * pi * (j + 0.5L) / N);
+            out[iv * N + k] = double(2 * s / N);
+        }
+    }
+}
+
+}  // namespace vpg

@@ -1,0 +1,143 @@
+// plan.cuh -- device-resident SummationPlan state (the pimpl behind the
+// C ABI; the reference keeps the same information in SummationPlan::Impl,
+// summation.cpp:542-549).
+#pragma once
+
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+
+namespace vpg {
+
+// Owning device buffer (cudaMalloc at plan build; plans are immutable).
+template <typename T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() { release(); }
+    void alloc(size_t count) {
+        release();
+        n = count;
+        if (count) VPG_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    size_t bytes() const { return n * sizeof(T); }
+};
+
+// M2L work unit: a run of consecutive non-empty target boxes (one level)
+// whose interaction lists together hold <= kM2LPairs entries.
+struct M2LBatch {
+    int32_t level;
+    int32_t tfirst;  // index into the concatenated target-box list
+    int32_t tcount;
+    int32_t efirst;  // first list entry
+    int32_t ecount;
+};
+constexpr int kM2LPairs = 128;  // columns = 2 * pairs (re | im)
+
+// P2P work unit: up to chunk targets of one leaf (Morton-sorted order).
+struct P2PChunk {
+    int32_t leaf;
+    int32_t tbegin;
+    int32_t tcount;
+    int32_t pad;
+};
+
+struct Plan {
+    int device = 0;
+    int sm_count = 148;
+    int family = VPG_LAPLACE;
+    int mode = VPG_MODE_REFERENCE;
+    double lambda = 0.0, eps = 1e-12;
+    int64_t ns = 0, nt = 0;
+    bool direct = true;
+    int L = 0, P = 0;
+    double x0 = 0, y0 = 0, side = 1;
+
+    // Original-order points (pairwise mode) and Morton-sorted points.
+    DBuf<double2> src, tgt;
+    DBuf<double2> src_sorted, tgt_sorted;
+    DBuf<int32_t> src_off, src_ids, tgt_off, tgt_ids;  // leaf CSR
+    DBuf<int32_t> src_cnt, tgt_cnt;                    // all levels
+
+    // M2L lists (levels 2..L concatenated): target boxes and entries.
+    std::vector<int64_t> lvl_tfirst;  // per level: first target-box index
+    DBuf<int32_t> m2l_tbox, m2l_toff, m2l_src, m2l_oidx;
+    int64_t n_tbox = 0, n_m2l = 0;
+    DBuf<M2LBatch> m2l_batches;
+    int64_t n_m2l_batches = 0;
+
+    // Laplace operators (summation.cpp:150-222), uploaded once.
+    DBuf<double> m2m_ops, l2l_ops;  // 4 x (P+1)^2 complex, transposed
+    DBuf<double> h_t;               // H^T: P x RP (k-major), real
+    DBuf<double2> dpow;             // 49 x (2P+1): d^-j per offset
+    DBuf<double2> logmd;            // 49: log(-d)
+    int RP = 0;                     // rows padded to a multiple of 8
+
+    // Upward/downward expansion level sizes.
+    std::vector<int64_t> exp_off;  // per level offset (in complex) into scratch
+    DBuf<int64_t> exp_off_dev;
+    int64_t exp_total = 0;         // complex count for one of mult/loc
+
+    // P2P schedule.
+    int p2p_tpt = 1;
+    DBuf<P2PChunk> p2p_chunks;
+    int64_t n_p2p_chunks = 0;
+    int64_t p2p_pairs = 0;
+    int64_t m2m_children = 0, l2l_children = 0;
+
+    // Leaf ids with src_cnt > 0 (P2M work list) and parents per level for
+    // M2M (src_cnt > 0) / L2L (tgt_cnt > 0).
+    DBuf<int32_t> p2m_leaves;
+    int64_t n_p2m_leaves = 0;
+    std::vector<int64_t> m2m_first, m2m_count;  // into updown_boxes, per level
+    std::vector<int64_t> l2l_first, l2l_count;
+    DBuf<int32_t> updown_boxes;
+
+    // Modified Helmholtz (treecode) state.
+    int helm_min_level = 2;
+    double helm_skip_x = 40.0;
+    std::vector<int> helm_m;          // per level
+    DBuf<double> helm_nodes;          // per level, 32 slots
+    DBuf<double> helm_bw;             // per level, 32 slots
+    std::vector<int64_t> helm_w_off;  // per level offset into proxy weights
+    int64_t helm_w_total = 0;
+
+    // Profiling.
+    bool profiling = false;
+    mutable std::mutex prof_mu;
+    mutable float phase_ms[VPG_PHASE_COUNT] = {};
+    mutable int64_t last_launches = 0;
+
+    int64_t device_bytes() const;
+};
+
+// tree.cu
+void build_tree(Plan& pl);
+// fmm.cu
+void build_laplace_ops(Plan& pl);
+void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
+                   cudaStream_t st, cudaEvent_t* ev, int64_t& launches);
+// direct.cu
+void pairwise_apply(const Plan& pl, const double* q_dev, double* out_dev,
+                    cudaStream_t st, int64_t& launches);
+void direct_sum_device(int family, double lambda, const double2* src,
+                       const double* q, int64_t ns, const double2* tgt,
+                       int64_t nt, double* out, bool skip,
+                       unsigned long long* clash, cudaStream_t st);
+// helm.cu
+void build_helm_ops(Plan& pl);
+void helm_apply(const Plan& pl, const double* q_dev, double* out_dev,
+                cudaStream_t st, cudaEvent_t* ev, int64_t& launches);
+void k0_device(const double* x, int64_t n, double* out, cudaStream_t st);
+void ensure_k0_table();
+
+}  // namespace vpg

@@ -1,0 +1,441 @@
+// tree.cu -- on-device quadtree build: bounding box, Morton leaf keys,
+// stable radix sort into leaf CSR, per-level occupancy and explicit M2L
+// interaction lists.  Reproduces the reference tree bit for bit in
+// VPG_MODE_REFERENCE (summation.cpp:81-129, 271-303, 551-591).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+
+#include "plan.cuh"
+
+namespace vpg {
+namespace {
+
+// ---------------------------------------------------------------- bbox --
+// Exact min/max (order-independent) in two passes: per-block partials, then
+// one block folds them.  summation.cpp:560-575.
+constexpr int kBoxThreads = 256;
+
+__global__ void bbox_partial(const double2* a, int64_t na, const double2* b,
+                             int64_t nb, double4* part) {
+    double xlo = INFINITY, xhi = -INFINITY, ylo = INFINITY, yhi = -INFINITY;
+    const int64_t n = na + nb;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const double2 p = i < na ? a[i] : b[i - na];
+        xlo = fmin(xlo, p.x);
+        xhi = fmax(xhi, p.x);
+        ylo = fmin(ylo, p.y);
+        yhi = fmax(yhi, p.y);
+    }
+    __shared__ double4 red[kBoxThreads];
+    red[threadIdx.x] = make_double4(xlo, xhi, ylo, yhi);
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) {
+            double4 u = red[threadIdx.x], v = red[threadIdx.x + s];
+            red[threadIdx.x] = make_double4(fmin(u.x, v.x), fmax(u.y, v.y),
+                                            fmin(u.z, v.z), fmax(u.w, v.w));
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+__global__ void bbox_final(const double4* part, int n, double4* out) {
+    __shared__ double4 red[kBoxThreads];
+    double4 acc = make_double4(INFINITY, -INFINITY, INFINITY, -INFINITY);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double4 v = part[i];
+        acc = make_double4(fmin(acc.x, v.x), fmax(acc.y, v.y), fmin(acc.z, v.z),
+                           fmax(acc.w, v.w));
+    }
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) {
+            double4 u = red[threadIdx.x], v = red[threadIdx.x + s];
+            red[threadIdx.x] = make_double4(fmin(u.x, v.x), fmax(u.y, v.y),
+                                            fmin(u.z, v.z), fmax(u.w, v.w));
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = red[0];
+}
+
+// ------------------------------------------------------------ leaf keys --
+// ix = clamp(int((x - x0) / side * n), 0, n-1) -- summation.cpp:85-92.  The
+// expression has no multiply-add pair, so no contraction can change it.
+__global__ void leaf_keys(const double2* pts, int64_t n, double x0, double y0,
+                          double side, int L, uint32_t* keys, int32_t* ids) {
+    const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (j >= n) return;
+    const int nb = 1 << L;
+    const double2 p = pts[j];
+    int ix = __double2int_rz(__dmul_rn(__ddiv_rn(__dsub_rn(p.x, x0), side), double(nb)));
+    int iy = __double2int_rz(__dmul_rn(__ddiv_rn(__dsub_rn(p.y, y0), side), double(nb)));
+    ix = min(max(ix, 0), nb - 1);
+    iy = min(max(iy, 0), nb - 1);
+    keys[j] = mort(uint32_t(ix), uint32_t(iy));
+    ids[j] = int32_t(j);
+}
+
+// off[b] = first sorted position with key >= b, b in [0, 4^L].
+__global__ void leaf_offsets(const uint32_t* skeys, int64_t n, int64_t nbox,
+                             int32_t* off) {
+    const int64_t b = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (b > nbox) return;
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (skeys[mid] < uint32_t(b)) lo = mid + 1; else hi = mid;
+    }
+    off[b] = int32_t(lo);
+}
+
+// cnt[l][b] = number of points in the Morton leaf range of box b: the
+// closed form of count_levels' child sums (summation.cpp:102-115).
+__global__ void level_counts(const int32_t* off, int L, int64_t total,
+                             int32_t* cnt) {
+    const int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (g >= total) return;
+    int l = 0;
+    while (lvl_base(l + 1) <= g) ++l;
+    const int64_t b = g - lvl_base(l);
+    const int sh = 2 * (L - l);
+    cnt[g] = off[(b + 1) << sh] - off[b << sh];
+}
+
+__global__ void gather_points(const double2* pts, const int32_t* ids,
+                              int64_t n, double2* out) {
+    const int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (e < n) out[e] = pts[ids[e]];
+}
+
+// ----------------------------------------------------- M2L interaction --
+// Children of the parent's 3x3 neighbours that are not neighbours of the
+// box, with a non-empty source box (summation.cpp:271-303).  Boxes of
+// levels 2..L are addressed by g = lvl_base(l) + b - lvl_base(2).
+__device__ inline int box_level(int64_t g, int lmin) {
+    int l = lmin;
+    while (lvl_base(l + 1) - lvl_base(lmin) <= g) ++l;
+    return l;
+}
+
+template <bool kFill>
+__global__ void m2l_list_kernel(const int32_t* src_cnt, const int32_t* tgt_cnt,
+                                int64_t nbox, const int64_t* tpos,
+                                const int64_t* epos, int32_t* ecount,
+                                int32_t* tflag, int32_t* tbox, int32_t* toff,
+                                int32_t* esrc, int32_t* eoidx) {
+    const int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (g >= nbox) return;
+    const int l = box_level(g, 2);
+    const int64_t b = g + lvl_base(2) - lvl_base(l);
+    const bool active = tgt_cnt[lvl_base(l) + b] > 0;
+    if (!kFill) {
+        tflag[g] = active ? 1 : 0;
+        if (!active) {
+            ecount[g] = 0;
+            return;
+        }
+    } else if (!active) {
+        return;
+    }
+    const int nb = 1 << l;
+    const int ix = int(squash2(uint32_t(b))), iy = int(squash2(uint32_t(b) >> 1));
+    const int px = ix >> 1, py = iy >> 1;
+    const int32_t* sc = src_cnt + lvl_base(l);
+    int cnt = 0;
+    int64_t e = kFill ? epos[g] : 0;
+    for (int qy = py - 1; qy <= py + 1; ++qy) {
+        if (qy < 0 || qy > (nb >> 1) - 1) continue;
+        for (int qx = px - 1; qx <= px + 1; ++qx) {
+            if (qx < 0 || qx > (nb >> 1) - 1) continue;
+            for (int c = 0; c < 4; ++c) {
+                const int jx = 2 * qx + (c & 1), jy = 2 * qy + ((c & 2) >> 1);
+                const int dx = jx - ix, dy = jy - iy;
+                if (max(abs(dx), abs(dy)) < 2) continue;
+                const uint32_t sid = mort(uint32_t(jx), uint32_t(jy));
+                if (sc[sid] == 0) continue;
+                if (kFill) {
+                    esrc[e] = int32_t(sid);
+                    eoidx[e] = (dx + 3) + 7 * (dy + 3);
+                    ++e;
+                } else {
+                    ++cnt;
+                }
+            }
+        }
+    }
+    if (!kFill) {
+        ecount[g] = cnt;
+    } else {
+        const int64_t t = tpos[g];
+        tbox[t] = int32_t(b);
+        toff[t] = int32_t(epos[g]);
+    }
+}
+
+inline unsigned blocks_for(int64_t n, int t) { return unsigned((n + t - 1) / t); }
+
+// Stable (key, index) sort of one point set into leaf CSR.
+void sort_points(const double2* pts, int64_t n, const Plan& pl, int32_t* off,
+                 int32_t* ids_out, double2* sorted, cudaStream_t st) {
+    const int64_t nbox = int64_t(1) << (2 * pl.L);
+    DBuf<uint32_t> keys, skeys;
+    DBuf<int32_t> ids;
+    keys.alloc(size_t(std::max<int64_t>(n, 1)));
+    skeys.alloc(size_t(std::max<int64_t>(n, 1)));
+    ids.alloc(size_t(std::max<int64_t>(n, 1)));
+    if (n > 0) {
+        leaf_keys<<<blocks_for(n, 256), 256, 0, st>>>(pts, n, pl.x0, pl.y0, pl.side,
+                                                      pl.L, keys.p, ids.p);
+        VPG_LAUNCH_CHECK();
+        size_t tmp_bytes = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys.p, skeys.p, ids.p,
+                                        ids_out, int(n), 0, 2 * pl.L, st);
+        DBuf<unsigned char> tmp;
+        tmp.alloc(std::max<size_t>(tmp_bytes, 1));
+        VPG_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, keys.p, skeys.p,
+                                                 ids.p, ids_out, int(n), 0, 2 * pl.L,
+                                                 st));
+        gather_points<<<blocks_for(n, 256), 256, 0, st>>>(pts, ids_out, n, sorted);
+        VPG_LAUNCH_CHECK();
+    }
+    leaf_offsets<<<blocks_for(nbox + 1, 256), 256, 0, st>>>(skeys.p, n, nbox, off);
+    VPG_LAUNCH_CHECK();
+    VPG_CUDA(cudaStreamSynchronize(st));
+}
+
+template <typename T>
+std::vector<T> to_host(const DBuf<T>& d, cudaStream_t st) {
+    std::vector<T> h(d.n);
+    if (d.n) VPG_CUDA(cudaMemcpyAsync(h.data(), d.p, d.bytes(), cudaMemcpyDeviceToHost, st));
+    VPG_CUDA(cudaStreamSynchronize(st));
+    return h;
+}
+template <typename T>
+void to_device(DBuf<T>& d, const std::vector<T>& h, cudaStream_t st) {
+    d.alloc(h.size());
+    if (!h.empty())
+        VPG_CUDA(cudaMemcpyAsync(d.p, h.data(), d.bytes(), cudaMemcpyHostToDevice, st));
+    VPG_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace
+
+void build_tree(Plan& pl) {
+    cudaStream_t st;
+    VPG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct StreamGuard {
+        cudaStream_t s;
+        ~StreamGuard() { cudaStreamDestroy(s); }
+    } guard{st};
+
+    // ---- bounding box over sources and targets (summation.cpp:560-576)
+    const int64_t ntot = pl.ns + pl.nt;
+    double4 bb = make_double4(0, 0, 0, 0);
+    if (ntot > 0) {
+        const int nblk = int(std::min<int64_t>(blocks_for(ntot, kBoxThreads), 1184));
+        DBuf<double4> part, fin;
+        part.alloc(size_t(nblk));
+        fin.alloc(1);
+        bbox_partial<<<nblk, kBoxThreads, 0, st>>>(pl.src.p, pl.ns, pl.tgt.p, pl.nt, part.p);
+        VPG_LAUNCH_CHECK();
+        bbox_final<<<1, kBoxThreads, 0, st>>>(part.p, nblk, fin.p);
+        VPG_LAUNCH_CHECK();
+        VPG_CUDA(cudaMemcpyAsync(&bb, fin.p, sizeof(bb), cudaMemcpyDeviceToHost, st));
+        VPG_CUDA(cudaStreamSynchronize(st));
+    }
+    const double side = std::max(bb.y - bb.x, bb.w - bb.z);
+    // Pairwise threshold (summation.cpp:578).  NATIVE mode keeps the same
+    // threshold: below 4e6 pairs one all-pairs launch beats any tree.
+    pl.direct = (ntot == 0) || side <= 0.0 || double(pl.ns) * double(pl.nt) <= 4e6;
+    if (pl.direct) return;
+
+    const double big = double(std::max(pl.ns, pl.nt));
+    if (pl.mode == VPG_MODE_REFERENCE) {
+        pl.L = std::clamp(int(std::ceil(std::log(big / 32.0) / std::log(4.0))), 2, 7);
+    } else {
+        // NATIVE: same leaf-size target, depth cap lifted to 9 levels.
+        pl.L = std::clamp(int(std::ceil(std::log(big / 32.0) / std::log(4.0))), 2, 9);
+    }
+    pl.x0 = bb.x;
+    pl.y0 = bb.z;
+    pl.side = side * (1.0 + 1e-12);
+    const int L = pl.L;
+    const int64_t nleaf = int64_t(1) << (2 * L);
+    const int64_t nall = lvl_base(L + 1);
+
+    // ---- leaf CSR for sources and targets (summation.cpp:81-100, 124-125)
+    pl.src_off.alloc(size_t(nleaf + 1));
+    pl.tgt_off.alloc(size_t(nleaf + 1));
+    pl.src_ids.alloc(size_t(std::max<int64_t>(pl.ns, 1)));
+    pl.tgt_ids.alloc(size_t(std::max<int64_t>(pl.nt, 1)));
+    pl.src_sorted.alloc(size_t(std::max<int64_t>(pl.ns, 1)));
+    pl.tgt_sorted.alloc(size_t(std::max<int64_t>(pl.nt, 1)));
+    sort_points(pl.src.p, pl.ns, pl, pl.src_off.p, pl.src_ids.p, pl.src_sorted.p, st);
+    sort_points(pl.tgt.p, pl.nt, pl, pl.tgt_off.p, pl.tgt_ids.p, pl.tgt_sorted.p, st);
+
+    // ---- per-level occupancy (summation.cpp:102-115, 126-127)
+    pl.src_cnt.alloc(size_t(nall));
+    pl.tgt_cnt.alloc(size_t(nall));
+    level_counts<<<blocks_for(nall, 256), 256, 0, st>>>(pl.src_off.p, L, nall, pl.src_cnt.p);
+    VPG_LAUNCH_CHECK();
+    level_counts<<<blocks_for(nall, 256), 256, 0, st>>>(pl.tgt_off.p, L, nall, pl.tgt_cnt.p);
+    VPG_LAUNCH_CHECK();
+
+    // ---- explicit M2L lists for levels 2..L (summation.cpp:271-303)
+    const int64_t nbox = nall - lvl_base(2);
+    {
+        DBuf<int32_t> ecount, tflag;
+        DBuf<int64_t> epos, tpos;
+        ecount.alloc(size_t(nbox));
+        tflag.alloc(size_t(nbox));
+        epos.alloc(size_t(nbox + 1));
+        tpos.alloc(size_t(nbox + 1));
+        m2l_list_kernel<false><<<blocks_for(nbox, 128), 128, 0, st>>>(
+            pl.src_cnt.p, pl.tgt_cnt.p, nbox, nullptr, nullptr, ecount.p, tflag.p,
+            nullptr, nullptr, nullptr, nullptr);
+        VPG_LAUNCH_CHECK();
+        size_t tb1 = 0, tb2 = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb1, ecount.p, epos.p, int(nbox), st);
+        cub::DeviceScan::ExclusiveSum(nullptr, tb2, tflag.p, tpos.p, int(nbox), st);
+        DBuf<unsigned char> tmp;
+        tmp.alloc(std::max<size_t>(std::max(tb1, tb2), 1));
+        VPG_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb1, ecount.p, epos.p, int(nbox), st));
+        VPG_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb2, tflag.p, tpos.p, int(nbox), st));
+        std::vector<int32_t> h_ecount = to_host(ecount, st);
+        std::vector<int32_t> h_tflag = to_host(tflag, st);
+        std::vector<int64_t> h_epos = to_host(epos, st);
+        std::vector<int64_t> h_tpos = to_host(tpos, st);
+        pl.n_m2l = h_epos[size_t(nbox - 1)] + h_ecount[size_t(nbox - 1)];
+        pl.n_tbox = h_tpos[size_t(nbox - 1)] + h_tflag[size_t(nbox - 1)];
+        if (pl.n_m2l > INT32_MAX) throw Error{VPG_ERR_INVALID_ARGUMENT, "M2L list too large"};
+        pl.m2l_tbox.alloc(size_t(std::max<int64_t>(pl.n_tbox, 1)));
+        pl.m2l_toff.alloc(size_t(pl.n_tbox + 1));
+        pl.m2l_src.alloc(size_t(std::max<int64_t>(pl.n_m2l, 1)));
+        pl.m2l_oidx.alloc(size_t(std::max<int64_t>(pl.n_m2l, 1)));
+        m2l_list_kernel<true><<<blocks_for(nbox, 128), 128, 0, st>>>(
+            pl.src_cnt.p, pl.tgt_cnt.p, nbox, tpos.p, epos.p, nullptr, nullptr,
+            pl.m2l_tbox.p, pl.m2l_toff.p, pl.m2l_src.p, pl.m2l_oidx.p);
+        VPG_LAUNCH_CHECK();
+        const int32_t total = int32_t(pl.n_m2l);
+        VPG_CUDA(cudaMemcpyAsync(pl.m2l_toff.p + pl.n_tbox, &total, sizeof(total),
+                                 cudaMemcpyHostToDevice, st));
+        VPG_CUDA(cudaStreamSynchronize(st));
+
+        // Per-level first target-box index, and M2L batches of <= kM2LPairs
+        // entries that never split a target box (so each target's local
+        // expansion is reduced by one CTA in a fixed order).
+        pl.lvl_tfirst.assign(size_t(L + 2), 0);
+        for (int l = 2; l <= L + 1; ++l) {
+            const int64_t g = lvl_base(l) - lvl_base(2);
+            pl.lvl_tfirst[size_t(l)] = g < nbox ? h_tpos[size_t(g)] : pl.n_tbox;
+        }
+        std::vector<M2LBatch> batches;
+        {
+            M2LBatch cur{};
+            bool open = false;
+            int cur_level = -1;
+            for (int64_t g = 0; g < nbox; ++g) {
+                if (!h_tflag[size_t(g)]) continue;
+                const int l = [&] {
+                    int ll = 2;
+                    while (lvl_base(ll + 1) - lvl_base(2) <= g) ++ll;
+                    return ll;
+                }();
+                const int32_t ne = h_ecount[size_t(g)];
+                if (open && (l != cur_level || cur.ecount + ne > kM2LPairs)) {
+                    batches.push_back(cur);
+                    open = false;
+                }
+                if (!open) {
+                    cur = M2LBatch{l, int32_t(h_tpos[size_t(g)]), 0, int32_t(h_epos[size_t(g)]), 0};
+                    cur_level = l;
+                    open = true;
+                }
+                cur.tcount += 1;
+                cur.ecount += ne;
+            }
+            if (open) batches.push_back(cur);
+        }
+        pl.n_m2l_batches = int64_t(batches.size());
+        to_device(pl.m2l_batches, batches, st);
+    }
+
+    // ---- work lists: P2M leaves, M2M/L2L parents, P2P target chunks
+    std::vector<int32_t> h_scnt = to_host(pl.src_cnt, st);
+    std::vector<int32_t> h_tcnt = to_host(pl.tgt_cnt, st);
+    {
+        std::vector<int32_t> leaves;
+        for (int64_t b = 0; b < nleaf; ++b)
+            if (h_scnt[size_t(lvl_base(L) + b)] > 0) leaves.push_back(int32_t(b));
+        pl.n_p2m_leaves = int64_t(leaves.size());
+        to_device(pl.p2m_leaves, leaves, st);
+    }
+    {
+        std::vector<int32_t> boxes;
+        pl.m2m_first.assign(size_t(L + 1), 0);
+        pl.m2m_count.assign(size_t(L + 1), 0);
+        pl.l2l_first.assign(size_t(L + 1), 0);
+        pl.l2l_count.assign(size_t(L + 1), 0);
+        pl.m2m_children = pl.l2l_children = 0;
+        for (int l = 2; l < L; ++l) {
+            // M2M: parents at level l with src_cnt > 0 (summation.cpp:257-267)
+            pl.m2m_first[size_t(l)] = int64_t(boxes.size());
+            for (int64_t b = 0; b < (int64_t(1) << (2 * l)); ++b)
+                if (h_scnt[size_t(lvl_base(l) + b)] > 0) {
+                    boxes.push_back(int32_t(b));
+                    for (int c = 0; c < 4; ++c)
+                        pl.m2m_children += h_scnt[size_t(lvl_base(l + 1) + (b << 2) + c)] > 0;
+                }
+            pl.m2m_count[size_t(l)] = int64_t(boxes.size()) - pl.m2m_first[size_t(l)];
+        }
+        for (int l = 2; l < L; ++l) {
+            // L2L: parents at level l having a child with tgt_cnt > 0
+            // (summation.cpp:305-312); parent tgt_cnt > 0 is equivalent.
+            pl.l2l_first[size_t(l)] = int64_t(boxes.size());
+            for (int64_t b = 0; b < (int64_t(1) << (2 * l)); ++b)
+                if (h_tcnt[size_t(lvl_base(l) + b)] > 0) {
+                    boxes.push_back(int32_t(b));
+                    for (int c = 0; c < 4; ++c)
+                        pl.l2l_children += h_tcnt[size_t(lvl_base(l + 1) + (b << 2) + c)] > 0;
+                }
+            pl.l2l_count[size_t(l)] = int64_t(boxes.size()) - pl.l2l_first[size_t(l)];
+        }
+        to_device(pl.updown_boxes, boxes, st);
+    }
+    {
+        std::vector<int32_t> h_soff = to_host(pl.src_off, st);
+        std::vector<int32_t> h_toff = to_host(pl.tgt_off, st);
+        const int nb = 1 << L;
+        int64_t occupied = 0;
+        for (int64_t b = 0; b < nleaf; ++b) occupied += h_toff[size_t(b) + 1] > h_toff[size_t(b)];
+        const double avg = occupied ? double(pl.nt) / double(occupied) : 0.0;
+        pl.p2p_tpt = avg > 48.0 ? 2 : 1;
+        const int chunk = 32 * pl.p2p_tpt;
+        std::vector<P2PChunk> chunks;
+        pl.p2p_pairs = 0;
+        for (int64_t b = 0; b < nleaf; ++b) {
+            const int32_t t0 = h_toff[size_t(b)], t1 = h_toff[size_t(b) + 1];
+            if (t1 == t0) continue;
+            const int ix = int(squash2(uint32_t(b))), iy = int(squash2(uint32_t(b) >> 1));
+            int64_t nsrc = 0;
+            for (int jy = std::max(0, iy - 1); jy <= std::min(nb - 1, iy + 1); ++jy)
+                for (int jx = std::max(0, ix - 1); jx <= std::min(nb - 1, ix + 1); ++jx) {
+                    const uint32_t sid = mort(uint32_t(jx), uint32_t(jy));
+                    nsrc += h_soff[sid + 1] - h_soff[sid];
+                }
+            pl.p2p_pairs += int64_t(t1 - t0) * nsrc;
+            for (int32_t t = t0; t < t1; t += chunk)
+                chunks.push_back(P2PChunk{int32_t(b), t, std::min(chunk, t1 - t), 0});
+        }
+        pl.n_p2p_chunks = int64_t(chunks.size());
+        to_device(pl.p2p_chunks, chunks, st);
+    }
+}
+
+}  // namespace vpg

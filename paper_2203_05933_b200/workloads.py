@@ -1,0 +1,273 @@
+"""Seeded synthetic inputs for the BASELINE.json configurations.
+
+The reference measures nothing public; BASELINE.json defines five synthetic
+node sets (quadrature nodes, weights, densities).  These generators build
+them deterministically (numpy PCG64 with fixed seeds).  The FMM step only
+sees (points, charges), so the node rule (8x8 Gauss-Legendre here, tensor
+Chebyshev/Fejer in the reference operator, basis.cpp:143-180) does not affect
+summation parity.
+
+Each generator returns a :class:`Workload` with sources (points, charges =
+weight * f) and targets.  Where a config names tolerances, ``eps`` holds them.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_GL_X, _GL_W = np.polynomial.legendre.leggauss(8)
+
+
+@dataclass
+class Workload:
+    name: str
+    src: np.ndarray            # (ns, 2)
+    q: np.ndarray              # (ns,) charges = weight * f(node)
+    tgt: np.ndarray            # (nt, 2)
+    kernel: str = "laplace"    # or "helmholtz"
+    lam: float = 0.0
+    eps: tuple = (1e-12,)
+    notes: dict = field(default_factory=dict)
+
+    @property
+    def ns(self):
+        return len(self.src)
+
+    @property
+    def nt(self):
+        return len(self.tgt)
+
+
+def box_nodes(cx, cy, h):
+    """8x8 tensor GL nodes and box-scaled weights of boxes centred (cx, cy), side h.
+
+    Returns (n_box*64, 2) points and weights; per box, y index outer, x inner.
+    """
+    cx = np.atleast_1d(np.asarray(cx, float))
+    cy = np.atleast_1d(np.asarray(cy, float))
+    h = np.broadcast_to(np.asarray(h, float), cx.shape)
+    gx, gy = np.meshgrid(_GL_X, _GL_X)          # gy rows (outer), gx cols (inner)
+    wx, wy = np.meshgrid(_GL_W, _GL_W)
+    px = cx[:, None] + 0.5 * h[:, None] * gx.ravel()[None, :]
+    py = cy[:, None] + 0.5 * h[:, None] * gy.ravel()[None, :]
+    w = (0.5 * h[:, None]) ** 2 * (wx * wy).ravel()[None, :]
+    return np.stack([px.ravel(), py.ravel()], axis=1), w.ravel()
+
+
+def gaussian(p, c, alpha):
+    d = p - np.asarray(c)[None, :]
+    return np.exp(-alpha * (d[:, 0] ** 2 + d[:, 1] ** 2))
+
+
+def star_radius(theta):
+    return 1.0 + 0.3 * np.cos(5.0 * theta)
+
+
+def _polar(p):
+    return np.hypot(p[:, 0], p[:, 1]), np.arctan2(p[:, 1], p[:, 0])
+
+
+def uniform_grid(nbox_side, lo=-1.0, hi=1.0):
+    h = (hi - lo) / nbox_side
+    iy, ix = np.meshgrid(np.arange(nbox_side), np.arange(nbox_side), indexing="ij")
+    cx = lo + (ix.ravel() + 0.5) * h
+    cy = lo + (iy.ravel() + 0.5) * h
+    return cx, cy, h
+
+
+def cfg1():
+    """[-1,1]^2, 16x16 boxes x 8x8 GL (16,384 nodes); f = exp(-50|r-c|^2), c=(0.1,-0.2)."""
+    cx, cy, h = uniform_grid(16)
+    p, w = box_nodes(cx, cy, h)
+    q = w * gaussian(p, (0.1, -0.2), 50.0)
+    return Workload("cfg1", p, q, p.copy(), notes={"boxes": 256, "h": h})
+
+
+def _star_boxes(n_side, strip=0.05):
+    lo, hi = -1.3, 1.3
+    cx, cy, h = uniform_grid(n_side, lo, hi)
+    keep = np.ones(cx.shape, bool)
+    for sx in (-0.5, 0.5):
+        for sy in (-0.5, 0.5):
+            r, th = _polar(np.stack([cx + sx * h, cy + sy * h], 1))
+            keep &= r < star_radius(th) - strip
+    return cx[keep], cy[keep], h
+
+
+def _strip_triangles(ntri, strip=0.05):
+    """ntri curved triangles covering r(theta)-strip <= rho <= r(theta).
+
+    The strip is cut into ntri/2 angular segments; each (theta, s) quad,
+    rho = r(theta) - strip (1 - s), splits into two triangles mapped by the
+    polar blending map.  64-node collapsed (Duffy) 8x8 GL rule per triangle.
+    """
+    nseg = ntri // 2
+    t0 = np.arange(nseg) * (2 * np.pi / nseg)
+    t1 = t0 + 2 * np.pi / nseg
+    # triangle vertices in (theta, s): A, B, C
+    A = np.concatenate([np.stack([t0, 0 * t0], 1), np.stack([t1, 0 * t1], 1)])
+    B = np.concatenate([np.stack([t1, 0 * t1], 1), np.stack([t1, 1 + 0 * t1], 1)])
+    Cv = np.concatenate([np.stack([t0, 1 + 0 * t0], 1), np.stack([t0, 1 + 0 * t0], 1)])
+    u = 0.5 * (_GL_X + 1.0)
+    wu = 0.5 * _GL_W
+    U, V = np.meshgrid(u, u, indexing="ij")      # u outer, v inner
+    WU, WV = np.meshgrid(wu, wu, indexing="ij")
+    U, V, WUV = U.ravel(), V.ravel(), (WU * WV).ravel()
+    # Duffy: X = A + u (B - A) + u v (C - B), jacobian u |det(B-A, C-B)|
+    pa = A[:, None, :] + U[None, :, None] * (B - A)[:, None, :] + \
+        (U * V)[None, :, None] * (Cv - B)[:, None, :]
+    e1, e2 = B - A, Cv - B
+    det = np.abs(e1[:, 0] * e2[:, 1] - e1[:, 1] * e2[:, 0])
+    th, s = pa[..., 0], pa[..., 1]
+    rho = star_radius(th) - strip * (1.0 - s)
+    pts = np.stack([rho * np.cos(th), rho * np.sin(th)], -1).reshape(-1, 2)
+    # d(x,y)/d(theta,s): |det| = rho * d rho/ds = rho * strip
+    w = (WUV[None, :] * U[None, :] * det[:, None] * rho * strip).ravel()
+    return pts, w
+
+
+def cfg2(seed=2):
+    """Star domain r=1+0.3cos5t: 64x64 clipped box grid + 2,000 strip triangles.
+
+    f = 3 seeded Gaussians (alpha in [20,80]); targets = all nodes + 10,000
+    seeded interior points; Laplace FMM at 1e-12.
+    """
+    rng = np.random.default_rng(seed)
+    cx, cy, h = _star_boxes(64)
+    pb, wb = box_nodes(cx, cy, h)
+    pt, wt = _strip_triangles(2000)
+    p = np.concatenate([pb, pt])
+    w = np.concatenate([wb, wt])
+    cen = rng.uniform(-0.6, 0.6, size=(3, 2))
+    alpha = rng.uniform(20, 80, size=3)
+    f = sum(gaussian(p, cen[k], alpha[k]) for k in range(3))
+    extra = []
+    while sum(len(e) for e in extra) < 10_000:
+        c = rng.uniform(-1.3, 1.3, size=(20_000, 2))
+        r, th = _polar(c)
+        extra.append(c[r < star_radius(th)])
+    extra = np.concatenate(extra)[:10_000]
+    tgt = np.concatenate([p, extra])
+    return Workload("cfg2", p, w * f, tgt, notes={"boxes": len(cx), "triangles": 2000, "h": h})
+
+
+def adaptive_leaves(c, lmin=4, lmax=10, radius=0.14):
+    """Quadtree on [-1,1]^2 refined from level lmin to lmax around c.
+
+    Rule (builder-defined): split a box while its level is
+    below lmax and the distance from c to the box is below ``radius``.
+    Returns leaf centres and sides in depth-first (Morton) order.
+    """
+    out_c, out_h = [], []
+
+    def rec(x0, y0, s, lev):
+        dx = max(x0 - c[0], 0.0, c[0] - (x0 + s))
+        dy = max(y0 - c[1], 0.0, c[1] - (y0 + s))
+        if lev < lmax and (lev < lmin or np.hypot(dx, dy) < radius):
+            hs = 0.5 * s
+            for (ox, oy) in ((0, 0), (1, 0), (0, 1), (1, 1)):
+                rec(x0 + ox * hs, y0 + oy * hs, hs, lev + 1)
+        else:
+            out_c.append((x0 + 0.5 * s, y0 + 0.5 * s))
+            out_h.append(s)
+
+    rec(-1.0, -1.0, 2.0, 0)
+    return np.array(out_c), np.array(out_h)
+
+
+def cfg3(seed=3):
+    """Adaptive quadtree (level 4 -> 10) around a sharp source f=exp(-1000|r-c|^2)."""
+    rng = np.random.default_rng(seed)
+    c = rng.uniform(-0.5, 0.5, size=2)
+    cen, hs = adaptive_leaves(c)
+    p, w = box_nodes(cen[:, 0], cen[:, 1], hs)
+    q = w * gaussian(p, c, 1000.0)
+    return Workload("cfg3", p, q, p.copy(), notes={"leaves": len(hs), "centre": c.tolist()})
+
+
+def cfg4(seed=4, nbox_side=256):
+    """256x256 boxes x 8x8 GL on [-1,1]^2 (4,194,304 nodes), 16 seeded Gaussians."""
+    rng = np.random.default_rng(seed)
+    cx, cy, h = uniform_grid(nbox_side)
+    p, w = box_nodes(cx, cy, h)
+    cen = rng.uniform(-1, 1, size=(16, 2))
+    alpha = rng.uniform(10, 200, size=16)
+    f = np.zeros(len(p))
+    for k in range(16):
+        f += gaussian(p, cen[k], alpha[k])
+    return Workload("cfg4", p, w * f, p, eps=(1e-6, 1e-9, 1e-12), notes={"h": h})
+
+
+def cfg5(seed=5, n_side=192, ntri=2000):
+    """Modified Helmholtz (lambda=10) on the star domain refined to ~1M nodes.
+
+    Also returns (in notes) a synthetic correction CSR: per target its cell
+    (self) plus the existing 8-neighbour box cells (<= 9 blocks x 64), rows
+    shared per (offset, local node) for boxes (potential.cpp:256-267) and
+    private for triangle self blocks; row values seeded.
+    """
+    rng = np.random.default_rng(seed)
+    cx, cy, h = _star_boxes(n_side)
+    pb, wb = box_nodes(cx, cy, h)
+    pt, wt = _strip_triangles(ntri)
+    p = np.concatenate([pb, pt])
+    w = np.concatenate([wb, wt])
+    cen = rng.uniform(-0.6, 0.6, size=(3, 2))
+    alpha = rng.uniform(20, 80, size=3)
+    f = sum(gaussian(p, cen[k], alpha[k]) for k in range(3))
+    wl = Workload("cfg5", p, w * f, p.copy(), kernel="helmholtz", lam=10.0,
+                  notes={"boxes": len(cx), "triangles": ntri, "h": h, "f": f})
+    return wl
+
+
+def correction_csr(nbox_cells, box_ij, ntri_cells, seed=55, np_box=64, np_tri=64):
+    """Synthetic correction map for a mesh of ``nbox_cells`` grid boxes
+    (integer grid coordinates ``box_ij``) followed by ``ntri_cells`` triangles.
+
+    Targets are the mesh nodes in order.  Box node t of cell c gets the self
+    block plus every existing box among the 8 grid neighbours (<= 9 blocks);
+    box rows are shared per (offset, local node) like the reference lattice
+    table (potential.cpp:256-267); triangle nodes get one private self row.
+    """
+    rng = np.random.default_rng(seed)
+    ncell = nbox_cells + ntri_cells
+    node_off = np.zeros(ncell + 1, np.int64)
+    node_off[1:nbox_cells + 1] = np.arange(1, nbox_cells + 1) * np_box
+    node_off[nbox_cells + 1:] = nbox_cells * np_box + np.arange(1, ntri_cells + 1) * np_tri
+    index = {tuple(ij): k for k, ij in enumerate(map(tuple, box_ij))}
+    offsets = [(0, 0)] + [(dx, dy) for dy in (-1, 0, 1) for dx in (-1, 0, 1) if (dx, dy) != (0, 0)]
+    # shared lattice rows: 9 offsets x np_box local nodes
+    lattice = rng.standard_normal((len(offsets), np_box, np_box)) * 1e-3
+    blk_cell, blk_pool, blk_off = [], [], [0]
+    pool_rows = [lattice.reshape(-1, np_box)]
+    npool = len(offsets) * np_box
+    for c, (i, j) in enumerate(map(tuple, box_ij)):
+        nbrs = [(o, index.get((i + o[0], j + o[1]))) for o in offsets]
+        nbrs = [(k, cell) for k, (o, cell) in enumerate(nbrs) if cell is not None]
+        for t in range(np_box):
+            for k, cell in nbrs:
+                blk_cell.append(cell)
+                blk_pool.append(k * np_box + t)
+            blk_off.append(len(blk_cell))
+    tri_rows = rng.standard_normal((ntri_cells * np_tri, np_tri)) * 1e-3
+    for c in range(ntri_cells):
+        for t in range(np_tri):
+            blk_cell.append(nbox_cells + c)
+            blk_pool.append(npool + c * np_tri + t)
+            blk_off.append(len(blk_cell))
+    pool_rows.append(tri_rows)
+    vals = np.concatenate([r.reshape(-1) for r in pool_rows])
+    lens = np.concatenate([np.full(len(offsets) * np_box, np_box), np.full(ntri_cells * np_tri, np_tri)])
+    pool_off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    return {"blk_off": np.array(blk_off, np.int32), "blk_cell": np.array(blk_cell, np.int32),
+            "blk_pool": np.array(blk_pool, np.int32), "pool_off": pool_off, "pool_vals": vals,
+            "node_off": node_off.astype(np.int32)}
+
+
+CONFIGS = {"cfg1": cfg1, "cfg2": cfg2, "cfg3": cfg3, "cfg4": cfg4, "cfg5": cfg5}
+
+
+def random_points(n, seed, lo=0.0, hi=1.0):
+    rng = np.random.default_rng(seed)
+    return rng.uniform(lo, hi, size=(n, 2))

@@ -1,0 +1,52 @@
+"""Correction apply (potential.cpp:446-462) and build_charges
+(potential.cpp:397-412) on the GPU vs the restatement."""
+import numpy as np
+import pytest
+
+from conftest import rel_l2
+from paper_2203_05933_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+def _mesh(n=24):
+    ij = np.array([(i, j) for j in range(n) for i in range(n) if (i - n / 2) ** 2 + (j - n / 2) ** 2 < (n / 2) ** 2])
+    return ij
+
+
+def test_correction_apply_matches_restatement(vp, rest):
+    ij = _mesh()
+    csr = W.correction_csr(len(ij), ij, ntri_cells=50)
+    ndofs = int(csr["node_off"][-1])
+    rng = np.random.default_rng(3)
+    f = rng.standard_normal(ndofs)
+    out0 = rng.standard_normal(ndofs)
+    cm = vp.CorrectionMap(csr["blk_off"], csr["blk_cell"], csr["blk_pool"], csr["pool_off"],
+                          csr["pool_vals"], csr["node_off"])
+    gpu = cm.apply(f, out0.copy())
+    cpu = rest.correction_apply(csr["blk_off"], csr["blk_cell"], csr["blk_pool"], csr["pool_off"],
+                                csr["pool_vals"], csr["node_off"], f, out0)
+    assert rel_l2(gpu - out0, cpu - out0) <= 1e-14
+    assert np.max(csr["blk_off"][1:] - csr["blk_off"][:-1]) <= 9
+    # f == 0 adds nothing
+    assert np.array_equal(cm.apply(np.zeros(ndofs), out0.copy()), out0)
+    with pytest.raises(vp.InvalidArgument, match="apply: expected"):
+        cm.apply(np.zeros(ndofs + 1), out0.copy())
+
+
+def test_build_charges_matches_restatement(vp, rest):
+    rng = np.random.default_rng(5)
+    ncell = 300
+    ct = rng.integers(0, 2, ncell).astype(np.int32)
+    npn = np.where(ct == 0, 64, 36)
+    nqn = np.where(ct == 0, 256, 81)
+    node_off = np.concatenate([[0], np.cumsum(npn)]).astype(np.int32)
+    src_off = np.concatenate([[0], np.cumsum(nqn)]).astype(np.int32)
+    over0 = rng.standard_normal((256, 64))
+    over1 = rng.standard_normal((81, 36))
+    wj = rng.uniform(0.1, 1.0, src_off[-1])
+    f = rng.standard_normal(node_off[-1])
+    ch = vp.ChargeMap(ct, node_off, src_off, over0, over1, wj)
+    gpu = ch.apply(f)
+    cpu = rest.build_charges(ct, node_off, src_off, over0, over1, wj, f)
+    assert rel_l2(gpu, cpu) <= 1e-14

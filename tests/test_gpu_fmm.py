@@ -1,0 +1,132 @@
+"""Laplace FMM on the GPU vs the reference SummationPlan (oracle/_ref), the
+restatement and long-double direct sums (summation.cpp:224-348, 610-643)."""
+import numpy as np
+import pytest
+
+from conftest import rel_l2
+from paper_2203_05933_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+def lap(vp):
+    return vp.make_kernel(vp.KernelFamily.Laplace)
+
+
+def test_cfg1_fmm_vs_reference(vp, ref, rest):
+    w = W.cfg1()
+    with vp.SummationPlan(lap(vp), w.src, w.tgt, 1e-12) as plan:
+        assert plan.levels() == 5 and plan.expansion_order() == 50
+        gpu = plan.apply(w.q)
+        again = plan.apply(w.q)
+    assert np.array_equal(gpu, again)  # run-to-run bit identical
+    rp = ref.plan(0, 0.0, w.src, w.tgt, 1e-12)
+    cpu = rp.apply(w.q)
+    assert rel_l2(gpu, cpu) <= 1e-13
+    ld = rest.pairwise_ld(0, 0.0, w.src, w.q, w.tgt)
+    assert rel_l2(gpu, ld) <= 1e-12
+
+
+def test_cfg2_fmm_vs_reference(vp, rest):
+    w = W.cfg2()
+    with vp.SummationPlan(lap(vp), w.src, w.tgt, 1e-12) as plan:
+        assert plan.levels() == 7
+        gpu = plan.apply(w.q)
+    cpu = rest.plan_sum(0, 0.0, w.src, w.q, w.tgt, 1e-12)
+    assert rel_l2(gpu, cpu) <= 1e-13
+    idx = np.random.default_rng(0).choice(w.nt, 2000, replace=False)
+    ld = rest.pairwise_ld(0, 0.0, w.src, w.q, w.tgt[idx])
+    assert rel_l2(gpu[idx], ld) <= 1e-12
+
+
+@pytest.mark.parametrize("eps", [1e-6, 1e-9])
+def test_tolerances(vp, rest, eps):
+    w = W.cfg1()
+    with vp.SummationPlan(lap(vp), w.src, w.tgt, eps) as plan:
+        gpu = plan.apply(w.q)
+    cpu = rest.plan_sum(0, 0.0, w.src, w.q, w.tgt, eps)
+    ld = rest.pairwise_ld(0, 0.0, w.src, w.q, w.tgt)
+    assert rel_l2(gpu, cpu) <= 1e-13
+    assert rel_l2(gpu, ld) <= eps
+
+
+def test_spec_acceptance8_random_1e4(vp, rest):
+    """1e4 random points, eps=1e-10 -> rel l2 <= 1e-10 vs direct."""
+    rng = np.random.default_rng(8)
+    pts = rng.uniform(0, 1, (10_000, 2))
+    q = rng.standard_normal(10_000)
+    gpu = None
+    with vp.SummationPlan(lap(vp), pts, pts, 1e-10) as plan:
+        assert plan.levels() > 0
+        gpu = plan.apply(q)
+    ld = rest.pairwise_ld(0, 0.0, pts, q, pts)
+    assert rel_l2(gpu, ld) <= 1e-10
+
+
+def test_zero_charges_and_linearity(vp):
+    rng = np.random.default_rng(9)
+    pts = rng.uniform(-1, 1, (20_000, 2))
+    tg = rng.uniform(-1, 1, (15_000, 2))
+    with vp.SummationPlan(lap(vp), pts, tg, 1e-12) as plan:
+        assert np.all(plan.apply(np.zeros(20_000)) == 0.0)
+        q1 = rng.choice([-1.0, 1.0], 20_000)  # Rademacher
+        q2 = rng.standard_normal(20_000)
+        a, b, ab = plan.apply(q1), plan.apply(q2), plan.apply(q1 + q2)
+    assert rel_l2(ab, a + b) <= 10 * 1e-12
+
+
+def test_single_source(vp, rest):
+    rng = np.random.default_rng(10)
+    tg = rng.uniform(-1, 1, (5000, 2))
+    src = np.concatenate([[[0.3, -0.2]], rng.uniform(-1, 1, (999, 2))])
+    q = np.zeros(1000)
+    q[0] = 1.0
+    with vp.SummationPlan(lap(vp), src, tg, 1e-12) as plan:
+        gpu = plan.apply(q)
+    d = tg - src[0]
+    exact = -0.25 / np.pi * np.log(d[:, 0] ** 2 + d[:, 1] ** 2)
+    assert rel_l2(gpu, exact) <= 1e-13
+
+
+def test_apply_size_mismatch_message(vp):
+    pts = np.random.default_rng(1).uniform(0, 1, (3000, 2))
+    with vp.SummationPlan(lap(vp), pts, pts, 1e-12) as plan:
+        with pytest.raises(vp.InvalidArgument,
+                           match="SummationPlan::apply: charge count 5 does not match source count 3000"):
+            plan.apply(np.ones(5))
+
+
+def test_pairwise_mode(vp, rest):
+    rng = np.random.default_rng(12)
+    src = rng.uniform(0, 1, (1500, 2))
+    tgt = np.concatenate([src[:500], rng.uniform(0, 1, (1000, 2))])  # coincident -> skipped
+    q = rng.standard_normal(1500)
+    with vp.SummationPlan(lap(vp), src, tgt, 1e-12) as plan:
+        assert plan.levels() == 0 and plan.expansion_order() == 0
+        gpu = plan.apply(q)
+    cpu = rest.plan_sum(0, 0.0, src, q, tgt, 1e-12)
+    assert rel_l2(gpu, cpu) <= 1e-14
+
+
+def test_native_mode_deeper_tree(vp, rest):
+    w = W.cfg3()
+    sub = slice(0, None, 4)
+    src, q = w.src[sub], w.q[sub]
+    with vp.SummationPlan(lap(vp), src, src, 1e-12, mode="native") as plan:
+        gpu = plan.apply(q)
+    idx = np.random.default_rng(5).choice(len(src), 1500, replace=False)
+    ld = rest.pairwise_ld(0, 0.0, src, q, src[idx])
+    assert rel_l2(gpu[idx], ld) <= 1e-12
+
+
+def test_device_pointer_apply(vp):
+    torch = pytest.importorskip("torch")
+    w = W.cfg1()
+    with vp.SummationPlan(lap(vp), w.src, w.tgt, 1e-12) as plan:
+        host = plan.apply(w.q)
+        qd = torch.tensor(w.q, device="cuda")
+        od = torch.empty(w.nt, dtype=torch.float64, device="cuda")
+        s = torch.cuda.current_stream()
+        plan.apply_device(qd.data_ptr(), od.data_ptr(), s.cuda_stream)
+        torch.cuda.synchronize()
+        assert np.array_equal(od.cpu().numpy(), host)

@@ -1,0 +1,48 @@
+"""Modified Helmholtz (lambda = 10): GPU treecode vs the reference treecode
+(oracle/_ref, summation.cpp:350-497), the restatement and direct K0 sums."""
+import numpy as np
+import pytest
+
+from conftest import rel_l2
+from paper_2203_05933_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+def mh(vp, lam=10.0):
+    return vp.make_kernel(vp.KernelFamily.ModifiedHelmholtz, lam)
+
+
+def test_make_kernel_rejects_nonpositive_lambda(vp):
+    with pytest.raises(vp.InvalidArgument, match="needs lambda > 0"):
+        vp.make_kernel(vp.KernelFamily.ModifiedHelmholtz, 0.0)
+
+
+def test_treecode_vs_reference_random(vp, ref, rest):
+    rng = np.random.default_rng(21)
+    pts = rng.uniform(-1.3, 1.3, (12_000, 2))
+    q = rng.standard_normal(12_000)
+    with vp.SummationPlan(mh(vp), pts, pts, 1e-12) as plan:
+        assert plan.levels() > 0
+        gpu = plan.apply(q)
+        rp = ref.plan(1, 10.0, pts, pts, 1e-12)
+        assert plan.levels() == rp.levels()
+        assert plan.expansion_order() == rp.expansion_order()
+    cpu = rp.apply(q)
+    assert rel_l2(gpu, cpu) <= 1e-13
+    direct = rest.plan_sum(1, 10.0, pts[:1], q[:1], pts[:1])  # smoke of the oracle path
+    assert np.isfinite(direct).all()
+    idx = rng.choice(12_000, 600, replace=False)
+    ld = rest.pairwise_ld(1, 10.0, pts, q, pts[idx])
+    assert rel_l2(gpu[idx], ld) <= 1e-12
+
+
+def test_cfg5_subset_vs_direct(vp, rest):
+    """cfg5 accuracy oracle: direct K0 P2P on a 65,536-node subset."""
+    w = W.cfg5(n_side=96, ntri=1000)
+    src, q = w.src, w.q
+    with vp.SummationPlan(mh(vp), src, src, 1e-12) as plan:
+        gpu = plan.apply(q)
+    idx = np.random.default_rng(4).choice(len(src), 2000, replace=False)
+    ld = rest.pairwise_ld(1, 10.0, src, q, src[idx])
+    assert rel_l2(gpu[idx], ld) <= 1e-12
