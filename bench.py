@@ -1,0 +1,373 @@
+#!/usr/bin/env python
+"""FMM-step benchmark (BASELINE.json metric: source-target interactions/s, FP64).
+
+A step is one SummationPlan::apply (summation.cpp:610-643) of the workload:
+charges in -> potentials out at every target.  Throughput is counted as
+all-pairs-equivalent interactions, ns * nt per step (what a direct sum would
+evaluate); the per-kernel numbers (P2P pairs/s, M2L flop/s, fraction of the
+measured FP64 peak) explain it.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2]
+    python bench.py --impl reference ...   # the reference CPU code (oracle/_ref)
+
+N > 1 runs under torchrun: every rank owns a Morton-contiguous shard of the
+target leaves (balanced by near-field pair count), the upward pass is
+replicated, there is no data-path collective inside the step (results stay
+sharded), and the timing is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "source-target interactions/s (FP64) for the FMM step"
+FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peak_r01.json")
+DEFAULT_WORKLOAD = "cfg2"  # BASELINE.json configs[1]
+
+THROTTLE_BITS = {
+    0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+    0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+    0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+    0x100: "display_clock_setting",
+}
+
+
+def fp64_peak_tflops():
+    with open(FP64_PEAK_FILE) as f:
+        rows = [json.loads(x) for x in f if x.strip()]
+    return max(r["fp64_dfma_tflops_best"] for r in rows)
+
+
+def hbm_peak_gbs():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f).get("hbm_gbs", 6650.0), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (the recipe's clocks line)."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 3:
+                try:
+                    self.rows.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                except ValueError:
+                    pass
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [r[0] for r in self.rows]
+        mask = 0
+        for r in self.rows:
+            mask |= r[2]
+        reasons = [n for b, n in THROTTLE_BITS.items() if mask & b and n != "gpu_idle"]
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def load_workload(name):
+    from paper_2203_05933_b200 import workloads as W
+    return W.CONFIGS[name]()
+
+
+def kernel_for(wl):
+    import paper_2203_05933_b200 as vp
+    if wl.kernel == "helmholtz":
+        return vp.make_kernel(vp.KernelFamily.ModifiedHelmholtz, wl.lam)
+    return vp.make_kernel(vp.KernelFamily.Laplace)
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ----------------------------------------------------------------- reference arm
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+    wl = load_workload(args.workload)
+    ref = oracle.reference()
+    cores = os.cpu_count() or 1
+    ref.set_threads(cores)
+    fam = 1 if wl.kernel == "helmholtz" else 0
+    eps = min(wl.eps)
+    plan = ref.plan(fam, wl.lam, wl.src, wl.tgt, eps)
+    for _ in range(args.warmup):
+        plan.apply(wl.q)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        plan.apply(wl.q)
+        times.append(time.perf_counter() - t0)
+    t = float(np.mean(times))
+    inter = float(wl.ns) * float(wl.nt)
+    v = inter / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "interactions/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, BASELINE.json shapes)",
+        "config": {"workload": args.workload, "ns": wl.ns, "nt": wl.nt, "epsilon": eps,
+                   "levels": plan.levels(), "order": plan.expansion_order(),
+                   "tree": "reference uniform quadtree"},
+        "cpu_baseline": {"value": v, "unit": "interactions/s", "cores": cores, "kind": "reference",
+                         "sample": f"{args.steps} full SummationPlan::apply of {args.workload} "
+                                   f"(oracle/_ref = unmodified proj/src/summation.cpp, g++ -O3 "
+                                   f"-march=native, set_thread_count({cores}))"},
+        "e2e": {"value": v, "unit": "interactions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------- GPU arm
+def cpu_baseline_sample(wl, budget_s=20.0):
+    """oracle/_ref on the host cores: full applies, bounded to ~budget_s."""
+    import oracle
+    try:
+        ref = oracle.reference()
+    except Exception as e:  # pragma: no cover
+        return {"value": None, "unit": "interactions/s", "cores": 0, "kind": "reference",
+                "sample": f"unavailable: {e}"}
+    cores = os.cpu_count() or 1
+    ref.set_threads(cores)
+    fam = 1 if wl.kernel == "helmholtz" else 0
+    plan = ref.plan(fam, wl.lam, wl.src, wl.tgt, min(wl.eps))
+    t0 = time.perf_counter()
+    plan.apply(wl.q)
+    first = time.perf_counter() - t0
+    n = max(1, min(5, int(budget_s / max(first, 1e-3))))
+    times = []
+    for _ in range(n):
+        t0 = time.perf_counter()
+        plan.apply(wl.q)
+        times.append(time.perf_counter() - t0)
+    t = float(np.median(times))
+    return {"value": float(wl.ns) * wl.nt / t, "unit": "interactions/s", "cores": cores,
+            "kind": "reference", "ms_per_step": t * 1e3,
+            "sample": f"median of {n} full SummationPlan::apply of the workload after 1 warm-up "
+                      f"(oracle/_ref, set_thread_count({cores}))"}
+
+
+def run_gpu(args):
+    import torch
+
+    import paper_2203_05933_b200 as vp
+    from paper_2203_05933_b200 import multigpu
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    wl = load_workload(args.workload)
+    kern = kernel_for(wl)
+    eps = min(wl.eps)
+    plan = vp.SummationPlan(kern, wl.src, wl.tgt, eps, mode=args.mode, device=local)
+    shard = None
+    if world > 1:
+        shard = multigpu.shard_plan(plan, rank, world)
+    info = plan.info()
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+    q_d = torch.from_numpy(wl.q).to("cuda")
+    out_d = torch.empty(wl.nt, dtype=torch.float64, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # 256 MB > L2
+
+    def step():
+        plan.apply_device(q_d.data_ptr(), out_d.data_ptr(), sh)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K device-resident steps, L2 flushed between steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    ms = float(np.sum(step_ms)) / args.steps
+    launches_per_step = plan.last_launches()
+    if dist:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # ---- phase split (profiled pass, same protocol, events inside the library)
+    plan.set_profiling(True)
+    phases = {k: 0.0 for k in ("gather", "p2m", "m2m", "m2l", "l2l", "p2p")}
+    for _ in range(args.steps):
+        flush.zero_()
+        plan.apply_device(q_d.data_ptr(), out_d.data_ptr(), sh)
+        pt = plan.phase_times()
+        for k in phases:
+            phases[k] += pt[k] / args.steps
+    plan.set_profiling(False)
+
+    # ---- end to end through the C ABI with pinned HOST buffers (H2D + D2H inside)
+    q_h = torch.from_numpy(wl.q.copy()).pin_memory()
+    out_h = torch.empty(wl.nt, dtype=torch.float64).pin_memory()
+    for _ in range(max(1, args.warmup)):
+        plan.apply_host_ptr(q_h.data_ptr(), out_h.data_ptr(), sh, sync=True)
+    e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+    if dist:
+        dist.barrier()
+    for i in range(args.steps):
+        flush.zero_()
+        e2e_ev[i][0].record(stream)
+        plan.apply_host_ptr(q_h.data_ptr(), out_h.data_ptr(), sh, sync=False)
+        e2e_ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = float(np.sum([a.elapsed_time(b) for a, b in e2e_ev])) / args.steps
+    if dist:
+        t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    # parity spot check of this very run against the device-resident result
+    host_res = out_h.numpy()
+    dev_res = out_d.cpu().numpy()
+    if shard is None and not np.array_equal(host_res, dev_res):
+        raise RuntimeError("host-pointer and device-pointer applies differ")
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return 0
+
+    inter = float(wl.ns) * float(wl.nt)
+    value = inter / (ms * 1e-3)
+    P = info["expansion_order"]
+    peak = fp64_peak_tflops()
+    kern_stats = {}
+    if info["levels"] > 0 and wl.kernel == "laplace":
+        m2l_flops = info["m2l_pairs"] * (4.0 * P * (P + 1) + 8.0 * (P + 1) + 6.0 * P)
+        m2l_dense = info["m2l_pairs"] * 8.0 * (P + 1) ** 2
+        p2p_flops = info["p2p_pairs"] * 27.0
+        kern_stats["m2l"] = {"ms": phases["m2l"], "pairs": info["m2l_pairs"],
+                             "tflops_executed": m2l_flops / (phases["m2l"] * 1e-3) / 1e12 if phases["m2l"] else None,
+                             "tflops_dense_equiv": m2l_dense / (phases["m2l"] * 1e-3) / 1e12 if phases["m2l"] else None}
+        kern_stats["p2p"] = {"ms": phases["p2p"], "pairs": info["p2p_pairs"],
+                             "pairs_per_s": info["p2p_pairs"] / (phases["p2p"] * 1e-3) if phases["p2p"] else None,
+                             "tflops_27": p2p_flops / (phases["p2p"] * 1e-3) / 1e12 if phases["p2p"] else None}
+        dom = "m2l" if phases["m2l"] >= phases["p2p"] else "p2p"
+        flops = m2l_flops if dom == "m2l" else p2p_flops
+        achieved = flops / (phases[dom] * 1e-3) / 1e12
+        roofline = {"bound": "fp64", "kernel": "m2l_kernel" if dom == "m2l" else "l2p_p2p_kernel",
+                    "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                    "traffic": None,
+                    "peak_source": "measured DFMA microbenchmark (tools/fp64_peak.cu, profiles/fp64_peak_r01.json); "
+                                   "MEASURED_PEAKS.json has no FP64 entry",
+                    "flops_per_unit": ("4P(P+1)+8(P+1)+6P executed per M2L pair" if dom == "m2l"
+                                       else "27 per near-field pair (SURVEY.md 8d convention)")}
+    else:
+        dom = "p2p"
+        roofline = {"bound": "fp64", "kernel": "traverse_kernel" if wl.kernel == "helmholtz" else "allpairs_kernel",
+                    "achieved": None, "peak": peak, "unit": "TFLOP/s", "frac": None, "traffic": None}
+    line = {
+        "metric": METRIC, "value": value, "unit": "interactions/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json shapes)",
+        "config": {"workload": args.workload, "ns": wl.ns, "nt": wl.nt, "epsilon": eps,
+                   "levels": info["levels"], "order": P, "mode": args.mode,
+                   "parallelism": f"target-shard{world}" if world > 1 else "single",
+                   "l2": "flushed (256 MB write) before every timed step"},
+        "e2e": {"value": inter / (e2e_ms * 1e-3), "unit": "interactions/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": 8 * wl.ns, "d2h_bytes_per_step": 8 * wl.nt,
+                "path": "vpg_plan_apply with pinned host buffers"},
+        "gpu_launches": int(launches_per_step * args.steps),
+        "phases_ms": phases,
+        "kernels": kern_stats,
+        "roofline": roofline,
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_sample(wl)
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--mode", default="reference", choices=["reference", "native"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

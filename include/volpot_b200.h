@@ -135,6 +135,14 @@ int vpg_plan_dump_tree(const vpg_plan* plan, int32_t* src_off,
 int vpg_plan_dump_m2l(const vpg_plan* plan, int level, int32_t* ntbox,
                       int64_t* nent, int32_t* tbox, int32_t* toff,
                       int32_t* src, int32_t* oidx);
+/* Multi-GPU target sharding (one process per GPU): restricts
+ * the target side of later applies (M2L, L2L, L2P+P2P) to the target leaves
+ * of Morton range [leaf_begin, leaf_end); the upward pass stays complete.
+ * Outputs of targets outside the range are written as 0.0, so summing the
+ * shards' outputs (one all-reduce) reproduces the unsharded plan bit for
+ * bit.  Not to be called concurrently with apply.  [0, 4^levels) restores
+ * the full plan. */
+int vpg_plan_set_shard(vpg_plan* plan, int64_t leaf_begin, int64_t leaf_end);
 int vpg_plan_destroy(vpg_plan* plan);
 
 /* direct_sum (summation.cpp:501-540).  skip_coincident = 0: reference

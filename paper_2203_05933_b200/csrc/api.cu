@@ -270,6 +270,8 @@ int vpg_plan_apply(const vpg_plan* plan, const double* q, int64_t nq, double* ou
             VPG_CUDA(cudaMemcpyAsync(qd.p, q, sizeof(double) * size_t(pl.ns), cudaMemcpyHostToDevice, st));
         int64_t launches = 0;
         cudaEvent_t* inner = prof ? ev + 1 : nullptr;  // GATHER .. DOWNLOAD
+        if (!pl.direct && (pl.shard_lb != 0 || pl.shard_le != (int64_t(1) << (2 * pl.L))) && pl.nt)
+            VPG_CUDA(cudaMemsetAsync(out_dev, 0, sizeof(double) * size_t(pl.nt), st));
         if (pl.direct) {
             if (prof)
                 for (int i = 0; i < 6; ++i) VPG_CUDA(cudaEventRecord(inner[i], st));
@@ -310,7 +312,7 @@ int vpg_plan_info(const vpg_plan* plan, vpg_plan_info_t* info) {
         r.x0 = pl.x0;
         r.y0 = pl.y0;
         r.side = pl.side;
-        r.m2l_pairs = pl.direct ? 0 : pl.n_m2l;
+        r.m2l_pairs = pl.direct ? 0 : pl.shard_m2l;
         r.p2p_pairs = pl.direct ? pl.ns * pl.nt : pl.p2p_pairs;
         r.m2m_children = pl.m2m_children;
         r.l2l_children = pl.l2l_children;
@@ -388,6 +390,19 @@ int vpg_plan_dump_m2l(const vpg_plan* plan, int level, int32_t* ntbox, int64_t* 
         if (oidx && e1 > e0)
             VPG_CUDA(cudaMemcpy(oidx, pl.m2l_oidx.p + e0, size_t(e1 - e0) * sizeof(int32_t),
                                 cudaMemcpyDeviceToHost));
+    });
+}
+
+int vpg_plan_set_shard(vpg_plan* plan, int64_t leaf_begin, int64_t leaf_end) {
+    return guarded([&] {
+        if (!plan) throw Error{VPG_ERR_INVALID_ARGUMENT, "plan is NULL"};
+        Plan& pl = plan->impl;
+        if (pl.direct) throw Error{VPG_ERR_INVALID_ARGUMENT, "pairwise plan cannot be sharded"};
+        const int64_t nleaf = int64_t(1) << (2 * pl.L);
+        if (leaf_begin < 0 || leaf_end > nleaf || leaf_begin > leaf_end)
+            throw Error{VPG_ERR_INVALID_ARGUMENT, "shard leaf range out of bounds"};
+        VPG_CUDA(cudaSetDevice(pl.device));
+        build_schedules(pl, leaf_begin, leaf_end);
     });
 }
 

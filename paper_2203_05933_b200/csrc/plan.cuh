@@ -111,6 +111,12 @@ struct Plan {
     std::vector<int64_t> helm_w_off;  // per level offset into proxy weights
     int64_t helm_w_total = 0;
 
+    // Host copies used to (re)build the schedules (tree.cu build_schedules).
+    std::vector<int32_t> h_tflag, h_ecount;   // per box of levels 2..L
+    std::vector<int64_t> h_epos, h_tpos;
+    std::vector<int32_t> h_scnt, h_tcnt, h_soff, h_toff;
+    int64_t shard_lb = 0, shard_le = 0, shard_m2l = 0;
+
     // Profiling.
     bool profiling = false;
     mutable std::mutex prof_mu;
@@ -122,6 +128,7 @@ struct Plan {
 
 // tree.cu
 void build_tree(Plan& pl);
+void build_schedules(Plan& pl, int64_t leaf_begin, int64_t leaf_end);
 // fmm.cu
 void build_laplace_ops(Plan& pl);
 void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,

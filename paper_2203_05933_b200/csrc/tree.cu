@@ -327,54 +327,78 @@ void build_tree(Plan& pl) {
                                  cudaMemcpyHostToDevice, st));
         VPG_CUDA(cudaStreamSynchronize(st));
 
-        // Per-level first target-box index, and M2L batches of <= kM2LPairs
-        // entries that never split a target box (so each target's local
-        // expansion is reduced by one CTA in a fixed order).
         pl.lvl_tfirst.assign(size_t(L + 2), 0);
         for (int l = 2; l <= L + 1; ++l) {
             const int64_t g = lvl_base(l) - lvl_base(2);
             pl.lvl_tfirst[size_t(l)] = g < nbox ? h_tpos[size_t(g)] : pl.n_tbox;
         }
-        std::vector<M2LBatch> batches;
-        {
-            M2LBatch cur{};
-            bool open = false;
-            int cur_level = -1;
-            for (int64_t g = 0; g < nbox; ++g) {
-                if (!h_tflag[size_t(g)]) continue;
-                const int l = [&] {
-                    int ll = 2;
-                    while (lvl_base(ll + 1) - lvl_base(2) <= g) ++ll;
-                    return ll;
-                }();
-                const int32_t ne = h_ecount[size_t(g)];
-                if (open && (l != cur_level || cur.ecount + ne > kM2LPairs)) {
-                    batches.push_back(cur);
-                    open = false;
-                }
-                if (!open) {
-                    cur = M2LBatch{l, int32_t(h_tpos[size_t(g)]), 0, int32_t(h_epos[size_t(g)]), 0};
-                    cur_level = l;
-                    open = true;
-                }
-                cur.tcount += 1;
-                cur.ecount += ne;
-            }
-            if (open) batches.push_back(cur);
-        }
-        pl.n_m2l_batches = int64_t(batches.size());
-        to_device(pl.m2l_batches, batches, st);
+        pl.h_tflag = std::move(h_tflag);
+        pl.h_ecount = std::move(h_ecount);
+        pl.h_epos = std::move(h_epos);
+        pl.h_tpos = std::move(h_tpos);
     }
-
-    // ---- work lists: P2M leaves, M2M/L2L parents, P2P target chunks
-    std::vector<int32_t> h_scnt = to_host(pl.src_cnt, st);
-    std::vector<int32_t> h_tcnt = to_host(pl.tgt_cnt, st);
+    pl.h_scnt = to_host(pl.src_cnt, st);
+    pl.h_tcnt = to_host(pl.tgt_cnt, st);
+    pl.h_soff = to_host(pl.src_off, st);
+    pl.h_toff = to_host(pl.tgt_off, st);
     {
         std::vector<int32_t> leaves;
         for (int64_t b = 0; b < nleaf; ++b)
-            if (h_scnt[size_t(lvl_base(L) + b)] > 0) leaves.push_back(int32_t(b));
+            if (pl.h_scnt[size_t(lvl_base(L) + b)] > 0) leaves.push_back(int32_t(b));
         pl.n_p2m_leaves = int64_t(leaves.size());
         to_device(pl.p2m_leaves, leaves, st);
+    }
+    build_schedules(pl, 0, nleaf);
+}
+
+// Target-side schedules restricted to the Morton leaf range [lb, le): M2L
+// batches and L2L parents of every box overlapping the range, P2P chunks of
+// the leaves inside it.  The upward pass (P2M, M2M) always covers the whole
+// tree.  [0, 4^L) is the single-GPU plan; a proper sub-range is one shard of
+// a multi-GPU run (vpg_plan_set_shard).
+void build_schedules(Plan& pl, int64_t lb, int64_t le) {
+    const int L = pl.L;
+    const int64_t nleaf = int64_t(1) << (2 * L);
+    const int64_t nbox = lvl_base(L + 1) - lvl_base(2);
+    cudaStream_t st = 0;
+    auto overlaps = [&](int l, int64_t b) {
+        const int sh = 2 * (L - l);
+        return (b << sh) < le && ((b + 1) << sh) > lb;
+    };
+    pl.shard_lb = lb;
+    pl.shard_le = le;
+    {
+        // M2L batches of <= kM2LPairs entries that never split a target box
+        // (each target's local expansion is reduced by one CTA, fixed order).
+        std::vector<M2LBatch> batches;
+        M2LBatch cur{};
+        bool open = false;
+        int cur_level = -1;
+        int l = 2;
+        for (int64_t g = 0; g < nbox; ++g) {
+            while (lvl_base(l + 1) - lvl_base(2) <= g) ++l;
+            const bool take = pl.h_tflag[size_t(g)] && overlaps(l, g + lvl_base(2) - lvl_base(l));
+            if (!take) {
+                if (open) batches.push_back(cur);
+                open = false;
+                continue;
+            }
+            const int32_t ne = pl.h_ecount[size_t(g)];
+            if (open && (l != cur_level || cur.ecount + ne > kM2LPairs)) {
+                batches.push_back(cur);
+                open = false;
+            }
+            if (!open) {
+                cur = M2LBatch{l, int32_t(pl.h_tpos[size_t(g)]), 0, int32_t(pl.h_epos[size_t(g)]), 0};
+                cur_level = l;
+                open = true;
+            }
+            cur.tcount += 1;
+            cur.ecount += ne;
+        }
+        if (open) batches.push_back(cur);
+        pl.n_m2l_batches = int64_t(batches.size());
+        to_device(pl.m2l_batches, batches, st);
     }
     {
         std::vector<int32_t> boxes;
@@ -387,10 +411,10 @@ void build_tree(Plan& pl) {
             // M2M: parents at level l with src_cnt > 0 (summation.cpp:257-267)
             pl.m2m_first[size_t(l)] = int64_t(boxes.size());
             for (int64_t b = 0; b < (int64_t(1) << (2 * l)); ++b)
-                if (h_scnt[size_t(lvl_base(l) + b)] > 0) {
+                if (pl.h_scnt[size_t(lvl_base(l) + b)] > 0) {
                     boxes.push_back(int32_t(b));
                     for (int c = 0; c < 4; ++c)
-                        pl.m2m_children += h_scnt[size_t(lvl_base(l + 1) + (b << 2) + c)] > 0;
+                        pl.m2m_children += pl.h_scnt[size_t(lvl_base(l + 1) + (b << 2) + c)] > 0;
                 }
             pl.m2m_count[size_t(l)] = int64_t(boxes.size()) - pl.m2m_first[size_t(l)];
         }
@@ -399,18 +423,18 @@ void build_tree(Plan& pl) {
             // (summation.cpp:305-312); parent tgt_cnt > 0 is equivalent.
             pl.l2l_first[size_t(l)] = int64_t(boxes.size());
             for (int64_t b = 0; b < (int64_t(1) << (2 * l)); ++b)
-                if (h_tcnt[size_t(lvl_base(l) + b)] > 0) {
+                if (pl.h_tcnt[size_t(lvl_base(l) + b)] > 0 && overlaps(l, b)) {
                     boxes.push_back(int32_t(b));
                     for (int c = 0; c < 4; ++c)
-                        pl.l2l_children += h_tcnt[size_t(lvl_base(l + 1) + (b << 2) + c)] > 0;
+                        pl.l2l_children += pl.h_tcnt[size_t(lvl_base(l + 1) + (b << 2) + c)] > 0;
                 }
             pl.l2l_count[size_t(l)] = int64_t(boxes.size()) - pl.l2l_first[size_t(l)];
         }
         to_device(pl.updown_boxes, boxes, st);
     }
     {
-        std::vector<int32_t> h_soff = to_host(pl.src_off, st);
-        std::vector<int32_t> h_toff = to_host(pl.tgt_off, st);
+        const std::vector<int32_t>& h_soff = pl.h_soff;
+        const std::vector<int32_t>& h_toff = pl.h_toff;
         const int nb = 1 << L;
         int64_t occupied = 0;
         for (int64_t b = 0; b < nleaf; ++b) occupied += h_toff[size_t(b) + 1] > h_toff[size_t(b)];
@@ -419,7 +443,7 @@ void build_tree(Plan& pl) {
         const int chunk = 32 * pl.p2p_tpt;
         std::vector<P2PChunk> chunks;
         pl.p2p_pairs = 0;
-        for (int64_t b = 0; b < nleaf; ++b) {
+        for (int64_t b = lb; b < le; ++b) {
             const int32_t t0 = h_toff[size_t(b)], t1 = h_toff[size_t(b) + 1];
             if (t1 == t0) continue;
             const int ix = int(squash2(uint32_t(b))), iy = int(squash2(uint32_t(b) >> 1));
@@ -435,6 +459,16 @@ void build_tree(Plan& pl) {
         }
         pl.n_p2p_chunks = int64_t(chunks.size());
         to_device(pl.p2p_chunks, chunks, st);
+    }
+    {
+        int64_t m2l = 0;
+        int l = 2;
+        for (int64_t g = 0; g < nbox; ++g) {
+            while (lvl_base(l + 1) - lvl_base(2) <= g) ++l;
+            if (pl.h_tflag[size_t(g)] && overlaps(l, g + lvl_base(2) - lvl_base(l)))
+                m2l += pl.h_ecount[size_t(g)];
+        }
+        pl.shard_m2l = m2l;
     }
 }
 

@@ -202,6 +202,11 @@ class SummationPlan:
         L.check(L.lib().vpg_plan_apply(self._h, q_ptr, self._info.num_sources, out_ptr, flags,
                                        stream or None), "SummationPlan::apply")
 
+    def set_shard(self, leaf_begin: int, leaf_end: int) -> None:
+        """Restrict the target side to Morton leaves [leaf_begin, leaf_end)."""
+        L.check(L.lib().vpg_plan_set_shard(self._h, int(leaf_begin), int(leaf_end)), "set_shard")
+        self._info = self._read_info()
+
     def _read_info(self) -> L.PlanInfo:
         info = L.PlanInfo()
         L.check(L.lib().vpg_plan_info(self._h, C.byref(info)), "plan_info")

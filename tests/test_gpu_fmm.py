@@ -130,3 +130,30 @@ def test_device_pointer_apply(vp):
         plan.apply_device(qd.data_ptr(), od.data_ptr(), s.cuda_stream)
         torch.cuda.synchronize()
         assert np.array_equal(od.cpu().numpy(), host)
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_target_shards_assemble_bit_exact(vp, world):
+    """Multi-GPU sharding emulated shard by shard on one GPU: the sum of the
+    shards' outputs equals the single-plan result bit for bit."""
+    from paper_2203_05933_b200 import multigpu
+    w = W.cfg2()
+    with vp.SummationPlan(lap(vp), w.src, w.tgt, 1e-12) as plan:
+        full = plan.apply(w.q)
+        total = np.zeros_like(full)
+        seen = np.zeros(w.nt, bool)
+        t = plan.dump_tree()
+        for r in range(world):
+            lo, hi = multigpu.shard_plan(plan, r, world)
+            part = plan.apply(w.q)
+            own = multigpu.owned_targets(t["tgt_off"], t["tgt_ids"], (lo, hi))
+            mask = np.ones(w.nt, bool)
+            mask[own] = False
+            assert np.all(part[mask] == 0.0)
+            assert not seen[own].any()
+            seen[own] = True
+            total += part
+        plan.set_shard(0, 4 ** plan.levels())
+        assert seen.all()
+        assert np.array_equal(total, full)
+        assert np.array_equal(plan.apply(w.q), full)
