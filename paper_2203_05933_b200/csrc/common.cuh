@@ -103,22 +103,99 @@ __device__ inline void log_table_to_smem(double2* sm, const double2* gtab) {
         sm[i] = gtab[i / kLogTableCopies];
 }
 
+// Polynomial coefficients live in constant memory so every DFMA takes them
+// as a c[][] operand (no register materialisation inside the hot loop).
+static __constant__ double c_log1p5[4] = {0.2, -0.25, 0.33333333333333333333, -0.5};
+static __constant__ double c_magic_bias = 4503599627371519.0;  // 2^52 + 1023
+
+__device__ __forceinline__ double2 lds_f64x2(uint32_t saddr) {
+    double2 v;
+    asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(saddr));
+    return v;
+}
+
+// Shared-window byte address of this lane's copy of table entry 0.
+__device__ __forceinline__ uint32_t log_table_lane_addr(const double2* tab, int lane8) {
+    return uint32_t(__cvta_generic_to_shared(tab)) + uint32_t(lane8) * 16u;
+}
+
 // Returns t with ln(x) = ed*ln2 + t; ed = exponent as a double.
-__device__ __forceinline__ double fast_log_split(double x, const double2* tab,
-                                                 int lane8, double& ed) {
+__device__ __forceinline__ double fast_log_split(double x, uint32_t tab_lane, double& ed) {
     const int hi = __double2hiint(x);
     const int lo = __double2loint(x);
-    const int idx = ((hi & 0x000FFFFF) + (1 << (19 - kLogTableBits))) >> (20 - kLogTableBits);
+    const uint32_t idx = (uint32_t(hi & 0x000FFFFF) + (1u << (19 - kLogTableBits))) >> (20 - kLogTableBits);
     const double m = __hiloint2double((hi & 0x000FFFFF) | 0x3FF00000, lo);
     // exponent field e_b in [0, 2047]: ed = (2^52 + e_b) - (2^52 + 1023)
-    ed = __hiloint2double(0x43300000, hi >> 20) - 4503599627371519.0;
-    const double2 tc = tab[idx * kLogTableCopies + lane8];
+    ed = __hiloint2double(0x43300000, hi >> 20) - c_magic_bias;
+    const double2 tc = lds_f64x2(tab_lane + idx * uint32_t(16 * kLogTableCopies));
     const double r = fma(m, tc.x, -1.0);
-    double p = fma(r, 0.2, -0.25);
-    p = fma(r, p, 0.33333333333333333333);
-    p = fma(r, p, -0.5);
+    double p = fma(r, c_log1p5[0], c_log1p5[1]);
+    p = fma(r, p, c_log1p5[2]);
+    p = fma(r, p, c_log1p5[3]);
     const double r2 = r * r;
     return tc.y + fma(r2, p, r);
+}
+
+// ----------------------------------------------- programmatic launches --
+// Kernels of one apply are chained with programmatic dependent launch: the
+// next grid may start (and stage its constant operators / tables) while the
+// previous one drains; it calls pdl_wait() before touching the
+// predecessor's outputs.  pdl_trigger() lets the successor launch early.
+__device__ __forceinline__ void pdl_wait() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    VPG_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+}
+
+// ------------------------------------------------ TMA bulk copies (1-D) --
+// cp.async.bulk global -> shared with mbarrier completion (sm_90+ async
+// proxy).  Sizes and addresses must be multiples of 16 bytes.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return uint32_t(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src_gmem, uint32_t bytes,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst_smem)),
+        "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
 }
 
 // Per-device constant tables, built on first use (api.cu).

@@ -31,7 +31,7 @@ allpairs_kernel(const double2* src, const double* q, int64_t ns,
     double2* tab = smd;
     double2* tile = smd + (kFamily == VPG_LAPLACE ? kLogTableSize * kLogTableCopies : 0);
     if (kFamily == VPG_LAPLACE) log_table_to_smem(tab, gtab);
-    const int lane8 = threadIdx.x & 7;
+    const uint32_t tab_lane = log_table_lane_addr(tab, threadIdx.x & 7);
     const int64_t j0 = int64_t(blockIdx.y) * slice;
     const int64_t j1 = min(ns, j0 + slice);
 
@@ -70,7 +70,7 @@ allpairs_kernel(const double2* src, const double* q, int64_t ns,
                     }
                 }
                 if (kFamily == VPG_LAPLACE)
-                    lap_pair(tx[u], ty[u], sp.x, sp.y, qj, tab, lane8, acc[u]);
+                    lap_pair(tx[u], ty[u], sp.x, sp.y, qj, tab_lane, acc[u]);
                 else
                     kacc[u] += k0_pair(tx[u], ty[u], sp.x, sp.y, qj, lambda, k0tab);
             }

@@ -43,6 +43,8 @@ p2m_kernel(const int32_t* leaves, const int32_t* soff, const double2* sxy,
            const double* q, int P, double x0, double y0, double s,
            double2* mult_leaf) {
     extern __shared__ double2 panel[];  // [32][P+1]
+    pdl_trigger();
+    pdl_wait();
     const int n = P + 1;
     const uint32_t b = uint32_t(leaves[blockIdx.x]);
     double cx, cy;
@@ -82,87 +84,75 @@ p2m_kernel(const int32_t* leaves, const int32_t* soff, const double2* sxy,
 }
 
 // ------------------------------------------------------------ M2M / L2L --
-// Shared-operator batched matvec.  A CTA takes kShiftGroup parents of one
-// level; for each child index c it stages the (P+1)^2 complex operator
-// (transposed, 41.6 KB at P=50) in smem and applies it to every parent of
-// the group.  Upward (M2M, summation.cpp:257-267): parent = sum_c
-// m2m[c] * child_c over children with src_cnt > 0, reduced in c order.
-// Downward (L2L, summation.cpp:305-312): child += l2l[c] * parent for
-// children with tgt_cnt > 0.  Each output vector is owned by one thread
-// row, so there are no atomics.
-constexpr int kShiftGroup = 8;
-constexpr int kShiftThreads = 64;
+// All four child operators (transposed, 4 x (P+1)^2 complex = 166 KB at
+// P=50) are staged in smem once per CTA -- before pdl_wait(), so the copy
+// overlaps the previous pass -- and every thread owns one output row of one
+// box: thread (g, r) of a CTA handles parent g, coefficient r.
+//   Upward (M2M, summation.cpp:257-267): parent[r] = sum_c (m2m[c] child_c)[r]
+//     over children with src_cnt > 0, reduced in c order.
+//   Downward (L2L, summation.cpp:305-312): child_c[r] += (l2l[c] parent)[r]
+//     for children with tgt_cnt > 0.
+// Each output element has exactly one writer: no atomics, fixed order.
+constexpr int kRowSlots = 64;  // threads per box (>= P+1)
+constexpr int kUpGroup = 8;    // parents per CTA, M2M
+constexpr int kDownGroup = 16; // parents per CTA, L2L
 
-template <bool kUp>
-__global__ void __launch_bounds__(kShiftThreads)
+template <bool kUp, int G>
+__global__ void __launch_bounds__(G * kRowSlots)
 shift_kernel(const int32_t* parents, int64_t nparents, const double2* ops_t,
              const int32_t* cnt_child, const double2* in_level,
-             double2* out_level, double2* child_level_out, int P) {
+             double2* out_level, int P) {
     extern __shared__ double2 sm[];
     const int n = P + 1;
-    double2* op = sm;                  // [k][r]
-    double2* vec = sm + n * n;         // [g][k]
-    const int64_t g0 = int64_t(blockIdx.x) * kShiftGroup;
-    const int ng = int(min(int64_t(kShiftGroup), nparents - g0));
-    const int r = threadIdx.x;
-    double2 acc[kShiftGroup];
-#pragma unroll
-    for (int g = 0; g < kShiftGroup; ++g) acc[g] = make_double2(0.0, 0.0);
-
-    if (!kUp) {
-        // parents' local expansions are the input for every c
+    const int nn = n * n;
+    double2* op = sm;              // [c][k][r]
+    double2* vec = sm + 4 * nn;    // up: [g][c][k]; down: [g][k]
+    for (int i = threadIdx.x; i < 4 * nn; i += blockDim.x) op[i] = ops_t[i];
+    pdl_trigger();
+    pdl_wait();
+    const int64_t g0 = int64_t(blockIdx.x) * G;
+    const int ng = int(min(int64_t(G), nparents - g0));
+    if (kUp) {
+        for (int i = threadIdx.x; i < ng * 4 * n; i += blockDim.x) {
+            const int g = i / (4 * n), rem = i % (4 * n), c = rem / n, kk = rem % n;
+            const int64_t child = (int64_t(parents[g0 + g]) << 2) | c;
+            vec[i] = cnt_child[child] > 0 ? in_level[child * n + kk] : make_double2(0.0, 0.0);
+        }
+    } else {
         for (int i = threadIdx.x; i < ng * n; i += blockDim.x) {
             const int g = i / n, kk = i % n;
-            vec[g * n + kk] = in_level[int64_t(parents[g0 + g]) * n + kk];
+            vec[i] = in_level[int64_t(parents[g0 + g]) * n + kk];
         }
     }
+    __syncthreads();
+    const int g = threadIdx.x / kRowSlots, r = threadIdx.x % kRowSlots;
+    if (g >= ng || r > P) return;
+    const int64_t parent = parents[g0 + g];
+    double ar = 0.0, ai = 0.0;
     for (int c = 0; c < 4; ++c) {
-        __syncthreads();
-        for (int i = threadIdx.x; i < n * n; i += blockDim.x) op[i] = ops_t[int64_t(c) * n * n + i];
-        if (kUp) {
-            for (int i = threadIdx.x; i < ng * n; i += blockDim.x) {
-                const int g = i / n, kk = i % n;
-                const int64_t child = (int64_t(parents[g0 + g]) << 2) | c;
-                vec[g * n + kk] = cnt_child[child] > 0 ? in_level[child * n + kk]
-                                                       : make_double2(0.0, 0.0);
-            }
+        const int64_t child = (parent << 2) | c;
+        if (cnt_child[child] == 0) continue;
+        const double2* oc = op + c * nn + r;
+        const double2* x = kUp ? vec + (g * 4 + c) * n : vec + g * n;
+        double yr = 0.0, yi = 0.0;
+        for (int kk = 0; kk <= P; ++kk) {
+            const double2 m = oc[kk * n];
+            const double2 v = x[kk];
+            yr = fma(m.x, v.x, fma(-m.y, v.y, yr));
+            yi = fma(m.x, v.y, fma(m.y, v.x, yi));
         }
-        __syncthreads();
-        if (r <= P) {
-            double2 y[kShiftGroup];
-#pragma unroll
-            for (int g = 0; g < kShiftGroup; ++g) y[g] = make_double2(0.0, 0.0);
-            for (int kk = 0; kk <= P; ++kk) {
-                const double2 m = op[kk * n + r];
-#pragma unroll
-                for (int g = 0; g < kShiftGroup; ++g) {
-                    const double2 x = vec[g * n + kk];
-                    y[g].x = fma(m.x, x.x, fma(-m.y, x.y, y[g].x));
-                    y[g].y = fma(m.x, x.y, fma(m.y, x.x, y[g].y));
-                }
-            }
-            if (kUp) {
-#pragma unroll
-                for (int g = 0; g < kShiftGroup; ++g) {
-                    acc[g].x += y[g].x;
-                    acc[g].y += y[g].y;
-                }
-            } else {
-                for (int g = 0; g < ng; ++g) {
-                    const int64_t child = (int64_t(parents[g0 + g]) << 2) | c;
-                    if (cnt_child[child] > 0) {
-                        double2* dst = child_level_out + child * n + r;
-                        double2 v = *dst;
-                        v.x += y[g].x;
-                        v.y += y[g].y;
-                        *dst = v;
-                    }
-                }
-            }
+        if (kUp) {
+            ar += yr;
+            ai += yi;
+        } else {
+            double2* dst = out_level + child * n + r;
+            double2 d = *dst;
+            d.x += yr;
+            d.y += yi;
+            *dst = d;
         }
     }
-    if (kUp && r <= P)
-        for (int g = 0; g < ng; ++g) out_level[int64_t(parents[g0 + g]) * n + r] = acc[g];
+    if (kUp) out_level[parent * n + r] = make_double2(ar, ai);
 }
 
 // ------------------------------------------------------------------ M2L --
@@ -175,211 +165,373 @@ shift_kernel(const int32_t* parents, int64_t nparents, const double2* ops_t,
 //   y = H a~,  b_0 = y_0 + log(-d) a_0,  b_l = d^-l (y_l - a_0 / l).
 // A batch (<= kM2LPairs list entries of consecutive target boxes of one
 // level) becomes ONE dense real GEMM Y[RP x 2*pairs] = H[RP x P] X[P x
-// 2*pairs] (re and im columns), with H^T and X staged in smem and an 8x8
-// register micro-tile per thread.  The epilogue applies the d^-l scaling
-// and reduces each target's entries in list order, then adds the monopole
-// shift qsum*log(s_l) (summation.cpp:297-301).  Executed flops per pair:
-// 4 P (P+1) for the GEMM + O(P) epilogue, half of the dense 8 (P+1)^2.
-constexpr int kM2LCols = 2 * kM2LPairs;  // 256
-constexpr int kM2LColGroups = 32;        // 8 columns each, interleaved
+// 2*pairs] (re and im columns).  Persistent CTAs (one per SM) keep H^T and
+// the offset power table d^-j (j <= P) resident in smem; per batch:
+//   1. X build: warp per list entry, lane per coefficient (coalesced rows);
+//   2. GEMM: 8x4 register micro-tile per thread, H rows broadcast, X
+//      columns interleaved (conflict-free);
+//   3. epilogue in two passes: b = D'(y ...) per (entry, l) in place, then
+//      each target box sums its entries in list order and adds the monopole
+//      shift qsum*log(s_l) (summation.cpp:297-301).
+// Executed flops per pair: 4 P (P+1) for the GEMM + O(P), half the dense
+// 8 (P+1)^2 of the reference matvec.
+constexpr int kM2LCols = 2 * kM2LPairs;  // 108
+constexpr int kM2LColGroups = kM2LCols / 4;      // 27 groups of 4 columns, interleaved
+constexpr int kM2LGemmThreads = 7 * kM2LColGroups;  // 189; RP <= 56
+constexpr int kM2LThreads = 192;                     // whole warps for the warp loops
 
-__global__ void __launch_bounds__(7 * kM2LColGroups)
-m2l_kernel(const M2LBatch* batches, const int32_t* tbox, const int32_t* toff,
-           const int32_t* esrc, const int32_t* eoidx, const double* h_t,
-           const double2* dpow, const double2* logmd, const double2* mult,
-           double2* loc, const int64_t* exp_off, int P, int RP, double side) {
-    extern __shared__ double smd[];
-    const int n = P + 1;
-    const int dp_stride = 2 * P + 1;
-    double* hs = smd;                        // [P][RP]
-    double* xy = hs + P * RP;                // [n][kM2LCols]
-    double2* a0s = reinterpret_cast<double2*>(xy + n * kM2LCols);  // [pairs]
-    int* os = reinterpret_cast<int*>(a0s + kM2LPairs);             // [pairs]
+// Batch staging: source multipole rows of the NEXT batch are fetched with 1-D
+// TMA bulk copies (one 16(P+1)-byte row per list entry, mbarrier
+// completion) while the current batch runs its GEMM and epilogue.
+struct M2LStage {
+    int32_t src[kM2LPairs];
+    int32_t oidx[kM2LPairs];
+};
 
-    const M2LBatch bt = batches[blockIdx.x];
-    const int level = bt.level;
-    const double2* mlev = mult + exp_off[level];
-    double2* llev = loc + exp_off[level];
-    const int tid = threadIdx.x;
-    const int nthr = blockDim.x;
-
-    for (int i = tid; i < P * RP; i += nthr) hs[i] = h_t[i];
-    // X[k-1][2p | 2p+1] = (-1)^k d^-k a_k  (k = 1..P)
-    for (int i = tid; i < bt.ecount * n; i += nthr) {
-        const int p = i / n, k = i % n;
+__device__ __forceinline__ void m2l_issue(const M2LBatch& bt, const int32_t* esrc,
+                                          const int32_t* eoidx, const double2* mult,
+                                          const int64_t* exp_off, int n, M2LStage* stg,
+                                          double2* raw, uint64_t* bar) {
+    // called by all threads; thread p < ecount owns entry p
+    const int p = threadIdx.x;
+    const double2* mlev = mult + exp_off[bt.level];
+    if (p == 0) mbar_arrive_expect_tx(bar, uint32_t(bt.ecount) * uint32_t(n) * 16u);
+    if (p < bt.ecount) {
         const int64_t e = int64_t(bt.efirst) + p;
         const int sid = esrc[e];
-        const int o = eoidx[e];
-        const double2 a = mlev[int64_t(sid) * n + k];
-        if (k == 0) {
-            a0s[p] = a;
-            os[p] = o;
-        } else {
-            double2 sg = dpow[o * dp_stride + k];
-            if (k & 1) {
-                sg.x = -sg.x;
-                sg.y = -sg.y;
-            }
-            xy[(k - 1) * kM2LCols + 2 * p] = a.x * sg.x - a.y * sg.y;
-            xy[(k - 1) * kM2LCols + 2 * p + 1] = a.x * sg.y + a.y * sg.x;
-        }
-    }
-    __syncthreads();
-
-    // GEMM: thread (rg, cg) owns rows rg*8..rg*8+7, columns cg + 32 j.
-    const int rg = tid / kM2LColGroups, cg = tid % kM2LColGroups;
-    const bool active_rows = rg * 8 < RP;
-    double acc[8][8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
-    if (active_rows) {
-        for (int k = 0; k < P; ++k) {
-            const double* hrow = hs + k * RP + rg * 8;
-            const double2 h01 = *reinterpret_cast<const double2*>(hrow);
-            const double2 h23 = *reinterpret_cast<const double2*>(hrow + 2);
-            const double2 h45 = *reinterpret_cast<const double2*>(hrow + 4);
-            const double2 h67 = *reinterpret_cast<const double2*>(hrow + 6);
-            const double h[8] = {h01.x, h01.y, h23.x, h23.y, h45.x, h45.y, h67.x, h67.y};
-            const double* xrow = xy + k * kM2LCols + cg;
-            double x[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) x[j] = xrow[32 * j];
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-#pragma unroll
-                for (int j = 0; j < 8; ++j) acc[i][j] = fma(h[i], x[j], acc[i][j]);
-        }
-    }
-    __syncthreads();
-    if (active_rows) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int l = rg * 8 + i;
-            if (l < n)
-#pragma unroll
-                for (int j = 0; j < 8; ++j) xy[l * kM2LCols + cg + 32 * j] = acc[i][j];
-        }
-    }
-    __syncthreads();
-
-    // Epilogue: thread -> (target t, coefficient l); t fastest so the smem
-    // reads of one warp fall on different columns.
-    const double logs = log(side / double(1 << level));
-    for (int i = tid; i < bt.tcount * n; i += nthr) {
-        const int t = i % bt.tcount, l = i / bt.tcount;
-        const int64_t tg = int64_t(bt.tfirst) + t;
-        const int p0 = toff[tg] - bt.efirst, p1 = toff[tg + 1] - bt.efirst;
-        double sr = 0.0, si = 0.0, qsum = 0.0;
-        const double inv_l = l > 0 ? c_neg_inv_k[l] : 0.0;  // -1/l
-        for (int p = p0; p < p1; ++p) {
-            const double yr = xy[l * kM2LCols + 2 * p];
-            const double yi = xy[l * kM2LCols + 2 * p + 1];
-            const double2 a0 = a0s[p];
-            const int o = os[p];
-            if (l == 0) {
-                const double2 lg = logmd[o];
-                sr += yr + (lg.x * a0.x - lg.y * a0.y);
-                si += yi + (lg.x * a0.y + lg.y * a0.x);
-                qsum += a0.x;
-            } else {
-                const double zr = fma(inv_l, a0.x, yr), zi = fma(inv_l, a0.y, yi);
-                const double2 dl = dpow[o * dp_stride + l];
-                sr += dl.x * zr - dl.y * zi;
-                si += dl.x * zi + dl.y * zr;
-            }
-        }
-        if (l == 0) sr += qsum * logs;
-        llev[int64_t(tbox[tg]) * n + l] = make_double2(sr, si);
+        stg->src[p] = sid;
+        stg->oidx[p] = eoidx[e];
+        tma_load_1d(raw + p * n, mlev + int64_t(sid) * n, uint32_t(n) * 16u, bar);
     }
 }
 
-// -------------------------------------------------- L2P + near-field P2P --
-// A persistent grid of warps walks the target chunks (<= 32*TPT targets of
-// one leaf).  Per chunk: each lane evaluates the local expansion of its
-// targets by Horner in u = (t-c)/s (summation.cpp:326-329), then sums the
-// 3x3 neighbour leaves (summation.cpp:330-344) in the reference order,
-// staging 32 sources at a time in a per-warp smem slot (one coalesced load
-// per lane, then warp-broadcast reads).  Output is scattered to the
-// original target order (summation.cpp:345).
-constexpr int kP2PWarps = 8;
-
-template <int TPT>
-__global__ void __launch_bounds__(kP2PWarps * 32)
-l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, const int32_t* soff,
-               const double2* sxy, const double* q, const double2* txy,
-               const int32_t* tids, const double2* loc_leaf, int P, int L,
-               double x0, double y0, double s, const double2* gtab, double* out) {
-    extern __shared__ double2 smp[];
-    double2* tab = smp;                                     // log table
-    double2* sbuf = smp + kLogTableSize * kLogTableCopies;  // [warps][32][2]
-    log_table_to_smem(tab, gtab);
-    __syncthreads();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int lane8 = lane & 7;
-    double2* my = sbuf + warp * 64;
-    const int nb = 1 << L;
+__global__ void __launch_bounds__(kM2LThreads, 2)
+m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
+           const int32_t* toff, const int32_t* esrc, const int32_t* eoidx,
+           const double* h_t, const double2* dpow, const double2* logmd,
+           const double2* mult, double2* loc, const int64_t* exp_off, int P, int RP,
+           double side) {
+    extern __shared__ __align__(16) double smd[];
     const int n = P + 1;
-    const double inv_s = 1.0 / s;
+    const int dp_stride = 2 * P + 1;
+    double* hs = smd;                                        // [P][RP]
+    double2* raw = reinterpret_cast<double2*>(hs + P * RP);  // [pairs][n] TMA landing
+    double* xy = reinterpret_cast<double*>(raw + kM2LPairs * n);  // [n][cols]
+    double2* a0s = reinterpret_cast<double2*>(xy + n * kM2LCols);  // [pairs]
+    M2LStage* stg = reinterpret_cast<M2LStage*>(a0s + kM2LPairs);  // [2]
+    __shared__ __align__(8) uint64_t bar;
 
-    for (int64_t ch = int64_t(blockIdx.x) * kP2PWarps + warp; ch < nchunks;
-         ch += int64_t(gridDim.x) * kP2PWarps) {
-        const P2PChunk c = chunks[ch];
-        const uint32_t b = uint32_t(c.leaf);
-        double cx, cy;
-        box_center(x0, y0, s, b, cx, cy);
-        double tx[TPT], ty[TPT], pot[TPT];
-        LapAcc acc[TPT];
-#pragma unroll
-        for (int u = 0; u < TPT; ++u) {
-            const int li = min(lane + 32 * u, c.tcount - 1);
-            const double2 t = txy[c.tbegin + li];
-            tx[u] = t.x;
-            ty[u] = t.y;
-            // L2P (summation.cpp:326-329)
-            const double ur = (t.x - cx) * inv_s, ui = (t.y - cy) * inv_s;
-            const double2* ab = loc_leaf + int64_t(b) * n;
-            double vr = ab[P].x, vi = ab[P].y;
-            for (int l = P - 1; l >= 0; --l) {
-                const double2 a = ab[l];
-                const double nr = fma(vr, ur, fma(-vi, ui, a.x));
-                const double ni = fma(vr, ui, fma(vi, ur, a.y));
-                vr = nr;
-                vi = ni;
-            }
-            pot[u] = -kInv2Pi * vr;
-        }
-        const int ix = int(squash2(b)), iy = int(squash2(b >> 1));
-        for (int jy = max(0, iy - 1); jy <= min(nb - 1, iy + 1); ++jy) {
-            for (int jx = max(0, ix - 1); jx <= min(nb - 1, ix + 1); ++jx) {
-                const uint32_t sid = mort(uint32_t(jx), uint32_t(jy));
-                const int f0 = soff[sid], f1 = soff[sid + 1];
-                for (int base = f0; base < f1; base += 32) {
-                    const int cnt = min(32, f1 - base);
-                    __syncwarp();
-                    if (lane < cnt) {
-                        my[2 * lane] = sxy[base + lane];
-                        my[2 * lane + 1] = make_double2(q[base + lane], 0.0);
+    const int tid = threadIdx.x;
+    const int nthr = blockDim.x;
+    const int lane = tid & 31, warp = tid >> 5, nwarp = (nthr + 31) >> 5;
+    for (int i = tid; i < P * RP; i += nthr) hs[i] = h_t[i];
+    if (tid == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    pdl_trigger();
+    pdl_wait();
+
+    const int rg = tid / kM2LColGroups, cg = tid % kM2LColGroups;
+    const bool active_rows = rg * 8 < RP && tid < kM2LGemmThreads;
+    uint32_t phase = 0;
+    int cur = 0;
+    int64_t bi = blockIdx.x;
+    if (bi < nbatch) m2l_issue(batches[bi], esrc, eoidx, mult, exp_off, n, &stg[0], raw, &bar);
+
+    for (; bi < nbatch; bi += gridDim.x) {
+        const M2LBatch bt = batches[bi];
+        double2* llev = loc + exp_off[bt.level];
+        const M2LStage& sg = stg[cur];
+        mbar_wait(&bar, phase);
+        phase ^= 1u;
+        // 1. X[k-1][2p | 2p+1] = (-1)^k d^-k a_k from the landed rows
+        //    (d^-j table in global memory, L1-resident: 49 x (2P+1));
+        //    warp per entry, lane per coefficient.
+        for (int p = warp; p < bt.ecount; p += nwarp) {
+            const double2* rr = raw + p * n;
+            const double2* dr = dpow + sg.oidx[p] * dp_stride;
+            for (int k = lane; k <= P; k += 32) {
+                const double2 a = rr[k];
+                if (k == 0) {
+                    a0s[p] = a;
+                } else {
+                    double2 d = __ldg(dr + k);
+                    if (k & 1) {
+                        d.x = -d.x;
+                        d.y = -d.y;
                     }
-                    __syncwarp();
-                    for (int j = 0; j < cnt; ++j) {
-                        const double2 sp = my[2 * j];
-                        const double qj = my[2 * j + 1].x;
-#pragma unroll
-                        for (int u = 0; u < TPT; ++u)
-                            lap_pair(tx[u], ty[u], sp.x, sp.y, qj, tab, lane8, acc[u]);
-                    }
+                    xy[(k - 1) * kM2LCols + 2 * p] = a.x * d.x - a.y * d.y;
+                    xy[(k - 1) * kM2LCols + 2 * p + 1] = a.x * d.y + a.y * d.x;
                 }
             }
         }
+        __syncthreads();
+        // raw[] is free: start the next batch's copies under this GEMM
+        // (generic-proxy reads of raw[] above must precede the async writes)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const int64_t bn = bi + gridDim.x;
+        if (bn < nbatch) m2l_issue(batches[bn], esrc, eoidx, mult, exp_off, n, &stg[cur ^ 1], raw, &bar);
+
+        // 2. GEMM: thread (rg, cg) owns rows rg*8..rg*8+7, columns cg + 27 j.
+        double acc[8][4];
 #pragma unroll
-        for (int u = 0; u < TPT; ++u) {
-            const int li = lane + 32 * u;
-            if (li < c.tcount) {
-                const double v = pot[u] - kInv4Pi * lap_total(acc[u]);
-                out[tids[c.tbegin + li]] = v;
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+        if (active_rows) {
+            const double* hcol = hs + rg * 8;
+            const double* xcol = xy + cg;
+#pragma unroll 2
+            for (int k = 0; k < P; ++k) {
+                const double2 h01 = *reinterpret_cast<const double2*>(hcol + k * RP);
+                const double2 h23 = *reinterpret_cast<const double2*>(hcol + k * RP + 2);
+                const double2 h45 = *reinterpret_cast<const double2*>(hcol + k * RP + 4);
+                const double2 h67 = *reinterpret_cast<const double2*>(hcol + k * RP + 6);
+                const double h[8] = {h01.x, h01.y, h23.x, h23.y, h45.x, h45.y, h67.x, h67.y};
+                double x[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) x[j] = xcol[k * kM2LCols + kM2LColGroups * j];
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[i][j] = fma(h[i], x[j], acc[i][j]);
             }
+        }
+        __syncthreads();  // everyone done reading X
+        // 3a. Y to smem, then per (entry p, row l): b_0 = y_0 + log(-d) a_0,
+        //     b_l = d^-l (y_l - a_0 / l), in place.
+        if (active_rows) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int l = rg * 8 + i;
+                if (l < n)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) xy[l * kM2LCols + cg + kM2LColGroups * j] = acc[i][j];
+            }
+        }
+        __syncthreads();
+        for (int l = warp; l <= P; l += nwarp) {
+            const double inv_l = l > 0 ? c_neg_inv_k[l] : 0.0;  // -1/l
+            double* yrow = xy + l * kM2LCols;
+            for (int p = lane; p < bt.ecount; p += 32) {
+                const double yr = yrow[2 * p], yi = yrow[2 * p + 1];
+                const double2 a0 = a0s[p];
+                const int o = sg.oidx[p];
+                double br, bim;
+                if (l == 0) {
+                    const double2 lg = logmd[o];
+                    br = yr + (lg.x * a0.x - lg.y * a0.y);
+                    bim = yi + (lg.x * a0.y + lg.y * a0.x);
+                } else {
+                    const double zr = fma(inv_l, a0.x, yr), zi = fma(inv_l, a0.y, yi);
+                    const double2 dl = __ldg(dpow + o * dp_stride + l);
+                    br = dl.x * zr - dl.y * zi;
+                    bim = dl.x * zi + dl.y * zr;
+                }
+                yrow[2 * p] = br;
+                yrow[2 * p + 1] = bim;
+            }
+        }
+        __syncthreads();
+        // 3b. per (target t, row l): sum the entries in list order, add the
+        // monopole shift (summation.cpp:297-301)
+        const double logs = log(side / double(1 << bt.level));
+        {
+            const int l = tid & 63;
+            if (l <= P)
+                for (int t = tid >> 6; t < bt.tcount; t += (nthr + 63) >> 6) {
+                    const int64_t tg = int64_t(bt.tfirst) + t;
+                    const int p0 = toff[tg] - bt.efirst, p1 = toff[tg + 1] - bt.efirst;
+                    const double* yrow = xy + l * kM2LCols;
+                    double sr = 0.0, si = 0.0, qsum = 0.0;
+#pragma unroll 4
+                    for (int p = p0; p < p1; ++p) {
+                        sr += yrow[2 * p];
+                        si += yrow[2 * p + 1];
+                        if (l == 0) qsum += a0s[p].x;
+                    }
+                    if (l == 0) sr += qsum * logs;
+                    llev[int64_t(tbox[tg]) * n + l] = make_double2(sr, si);
+                }
+        }
+        cur ^= 1;
+        __syncthreads();  // xy / a0s reused by the next batch
+    }
+}
+
+// ------------------------------------------------------------------ L2P --
+// One thread per (Morton-sorted) target: Horner of the leaf's local
+// expansion in u = (t-c)/s, pot = -(1/2pi) Re (summation.cpp:323-329).
+// Threads of one leaf read the same coefficients (L1 broadcast).  The
+// near-field kernel adds its sum on top (fixed order: far, then near).
+__global__ void __launch_bounds__(256)
+l2p_kernel(const int32_t* tleaf, int64_t t0, int64_t t1, const double2* txy,
+           const double2* loc_leaf, int P, double x0, double y0, double s, double* pot_far,
+           int* ticket) {
+    pdl_trigger();
+    pdl_wait();
+    const int64_t e = t0 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (e == t0) *ticket = 0;  // near-field work counter for l2p_p2p_kernel
+    if (e >= t1) return;
+    const uint32_t b = uint32_t(tleaf[e]);
+    double cx, cy;
+    box_center(x0, y0, s, b, cx, cy);
+    const double inv_s = 1.0 / s;
+    const double2 t = txy[e];
+    const double ur = (t.x - cx) * inv_s, ui = (t.y - cy) * inv_s;
+    const double2* ab = loc_leaf + int64_t(b) * (P + 1);
+    double vr = ab[P].x, vi = ab[P].y;
+    for (int l = P - 1; l >= 0; --l) {
+        const double2 a = ab[l];
+        const double nr = fma(vr, ur, fma(-vi, ui, a.x));
+        const double ni = fma(vr, ui, fma(vi, ur, a.y));
+        vr = nr;
+        vi = ni;
+    }
+    pot_far[e] = -kInv2Pi * vr;
+}
+
+// ------------------------------------------------------- near-field P2P --
+// A persistent grid of warps walks the target chunks (<= 64 targets of one
+// leaf).  Per chunk the warp
+//   1. picks up the far-field value of its targets (l2p_kernel);
+//   2. flattens the 3x3 neighbour leaves (summation.cpp:330-334, reference
+//      order: jy outer, jx inner) into one virtual source list -- lanes 0..8
+//      own one neighbour range each, a shuffle scan gives the flat offsets;
+//   3. streams that list through a per-warp smem slot, kP2PBatch sources at
+//      a time (coalesced loads, then broadcast reads); every lane holds two
+//      targets, so one source fetch feeds two pair evaluations (p2p.cuh);
+//   4. undoes the r^2 == 0 pairs (coincident points share a leaf, so only the
+//      centre leaf is rescanned) -- the hot loop itself has no zero test.
+// Small leaves (cfg1/cfg2: ~15 targets) would idle most of the warp, so the
+// warp splits into S = 32 / ceil(nT/2) groups taking every S-th source; the
+// S partial sums are added in group order (fixed order: results are
+// run-to-run identical).  Output is scattered to the original target order
+// (summation.cpp:345).
+constexpr int kP2PWarps = 8;
+constexpr int kP2PBatch = 64;
+constexpr int kP2PChunk = 64;
+
+__global__ void __launch_bounds__(kP2PWarps * 32)
+l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, const int32_t* soff,
+               const double2* sxy, const double* q, const double2* txy,
+               const int32_t* tids, const double* pot_far, int L,
+               const double2* gtab, int* ticket, double* out) {
+    extern __shared__ double2 smp[];
+    double2* tab = smp;                                                  // log table
+    double2* sbuf = smp + kLogTableSize * kLogTableCopies;               // [warps][batch] xy
+    double* qbuf = reinterpret_cast<double*>(sbuf + kP2PWarps * kP2PBatch);  // [warps][batch]
+    log_table_to_smem(tab, gtab);
+    pdl_trigger();
+    pdl_wait();
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t tab_lane = log_table_lane_addr(tab, lane & 7);
+    double2* mxy = sbuf + warp * kP2PBatch;
+    double* mq = qbuf + warp * kP2PBatch;
+    const int nb = 1 << L;
+
+    // Dynamic schedule: chunks are sorted costliest first (tree.cu); each
+    // warp takes the next one from a ticket counter zeroed by l2p_kernel.
+    for (;;) {
+        int ch = 0;
+        if (lane == 0) ch = atomicAdd(ticket, 1);
+        ch = __shfl_sync(0xffffffffu, ch, 0);
+        if (ch >= nchunks) break;
+        const P2PChunk c = chunks[ch];
+        const uint32_t b = uint32_t(c.leaf);
+        const int nT = c.tcount;
+        const int nTh = (nT + 1) >> 1;
+        const int S = max(1, 32 / nTh);
+        const int tl = lane % nTh;  // target slot: targets tl and tl + nTh
+        const int grp = lane / nTh; // source group
+        const bool active = grp < S;
+        double tx[2], ty[2], pot[2];
+        LapAcc acc[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int li = min(tl + nTh * u, nT - 1);
+            const double2 t = txy[c.tbegin + li];
+            tx[u] = t.x;
+            ty[u] = t.y;
+            pot[u] = grp == 0 ? pot_far[c.tbegin + li] : 0.0;
+        }
+        // neighbour ranges: lane i < 9 owns (jy, jx) = (iy-1 + i/3, ix-1 + i%3)
+        const int ix = int(squash2(b)), iy = int(squash2(b >> 1));
+        int rs = 0, rl = 0;
+        if (lane < 9) {
+            const int jx = ix - 1 + lane % 3, jy = iy - 1 + lane / 3;
+            if (jx >= 0 && jx < nb && jy >= 0 && jy < nb) {
+                const uint32_t sid = mort(uint32_t(jx), uint32_t(jy));
+                rs = soff[sid];
+                rl = soff[sid + 1] - rs;
+            }
+        }
+        int incl = rl;
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 8);
+        int pre[9], st[9];
+#pragma unroll
+        for (int i = 0; i < 9; ++i) {
+            pre[i] = __shfl_sync(0xffffffffu, incl - rl, i);
+            st[i] = __shfl_sync(0xffffffffu, rs, i);
+        }
+        for (int base = 0; base < total; base += kP2PBatch) {
+            const int cnt = min(kP2PBatch, total - base);
+            __syncwarp();
+#pragma unroll
+            for (int h = 0; h < kP2PBatch / 32; ++h) {
+                const int f = h * 32 + lane;
+                if (f < cnt) {
+                    const int ff = base + f;
+                    int src = st[0] + ff;
+#pragma unroll
+                    for (int i = 1; i < 9; ++i)
+                        if (ff >= pre[i]) src = st[i] + (ff - pre[i]);
+                    mxy[f] = sxy[src];
+                    mq[f] = q[src];
+                }
+            }
+            __syncwarp();
+            if (active) {
+                // source f of the flat list goes to group f mod S
+                int j = grp - base % S;
+                if (j < 0) j += S;
+#pragma unroll 2
+                for (; j < cnt; j += S) {
+                    const double2 sp = mxy[j];
+                    const double qj = mq[j];
+                    lap_pair_fast(tx[0], ty[0], sp.x, sp.y, qj, tab_lane, acc[0]);
+                    lap_pair_fast(tx[1], ty[1], sp.x, sp.y, qj, tab_lane, acc[1]);
+                }
+            }
+        }
+        // coincident points share the leaf: rescan the centre range only
+        if (active) {
+            const int f0 = pre[4], f1 = pre[5];
+            int ff = f0 + (grp - f0 % S);
+            if (ff < f0) ff += S;
+            for (; ff < f1; ff += S) {
+                const int src = st[4] + (ff - f0);
+                const double2 sp = sxy[src];
+                const double qj = q[src];
+                lap_pair_fixup(tx[0], ty[0], sp.x, sp.y, qj, tab_lane, acc[0]);
+                lap_pair_fixup(tx[1], ty[1], sp.x, sp.y, qj, tab_lane, acc[1]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            double v = active ? pot[u] - kInv4Pi * lap_total(acc[u]) : 0.0;
+            // add the other groups' partials in group order
+            for (int g2 = 1; g2 < S; ++g2) {
+                const double w = __shfl_sync(0xffffffffu, v, min(31, tl + g2 * nTh));
+                if (grp == 0) v += w;
+            }
+            const int li = tl + nTh * u;
+            if (grp == 0 && li < nT) out[tids[c.tbegin + li]] = v;
         }
     }
 }
@@ -487,11 +639,10 @@ void build_laplace_ops(Plan& pl) {
     VPG_CUDA(cudaMemcpy(pl.exp_off_dev.p, pl.exp_off.data(), pl.exp_off_dev.bytes(),
                         cudaMemcpyHostToDevice));
 
-    smem_optin((const void*)m2l_kernel, 200 * 1024);
-    smem_optin((const void*)shift_kernel<true>, 100 * 1024);
-    smem_optin((const void*)shift_kernel<false>, 100 * 1024);
-    smem_optin((const void*)l2p_p2p_kernel<1>, 64 * 1024);
-    smem_optin((const void*)l2p_p2p_kernel<2>, 64 * 1024);
+    smem_optin((const void*)m2l_kernel, 220 * 1024);
+    smem_optin((const void*)shift_kernel<true, kUpGroup>, 220 * 1024);
+    smem_optin((const void*)shift_kernel<false, kDownGroup>, 220 * 1024);
+    smem_optin((const void*)l2p_p2p_kernel, 64 * 1024);
 }
 
 // ----------------------------------------------------------------- apply --
@@ -505,17 +656,21 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
     double* qs = nullptr;
     double2* mult = nullptr;
     double2* loc = nullptr;
+    double* pot_far = nullptr;
+    int* ticket = nullptr;
     VPG_CUDA(cudaMallocAsync(&qs, sizeof(double) * size_t(std::max<int64_t>(pl.ns, 1)), st));
+    VPG_CUDA(cudaMallocAsync(&ticket, sizeof(int) * 32, st));
+    VPG_CUDA(cudaMallocAsync(&pot_far, sizeof(double) * size_t(std::max<int64_t>(pl.nt, 1)), st));
     VPG_CUDA(cudaMallocAsync(&mult, sizeof(double2) * size_t(pl.exp_total), st));
     VPG_CUDA(cudaMallocAsync(&loc, sizeof(double2) * size_t(pl.exp_total), st));
     struct Free {
-        void* p[3];
+        void* p[5];
         cudaStream_t s;
         ~Free() {
             for (void* x : p)
                 if (x) cudaFreeAsync(x, s);
         }
-    } fr{{qs, mult, loc}, st};
+    } fr{{qs, mult, loc, pot_far, ticket}, st};
     const int64_t* exp_off_d = pl.exp_off_dev.p;
 
     mark(0);
@@ -526,65 +681,70 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
 
     const double sL = pl.side / double(1 << L);
     if (pl.n_p2m_leaves > 0) {
-        p2m_kernel<<<unsigned(pl.n_p2m_leaves), kP2MThreads, 32 * n * sizeof(double2), st>>>(
-            pl.p2m_leaves.p, pl.src_off.p, pl.src_sorted.p, qs, P, pl.x0, pl.y0, sL,
-            mult + pl.exp_off[size_t(L)]);
-        VPG_LAUNCH_CHECK();
+        launch_pdl(p2m_kernel, dim3(unsigned(pl.n_p2m_leaves)), dim3(kP2MThreads),
+                   32 * n * sizeof(double2), st, (const int32_t*)pl.p2m_leaves.p,
+                   (const int32_t*)pl.src_off.p, (const double2*)pl.src_sorted.p, (const double*)qs, P,
+                   pl.x0, pl.y0, sL, mult + pl.exp_off[size_t(L)]);
         ++launches;
     }
     mark(2);
-    const size_t shift_smem = sizeof(double2) * size_t(n * n + kShiftGroup * n);
+    const size_t up_smem = sizeof(double2) * size_t(4 * n * n + kUpGroup * 4 * n);
+    const size_t down_smem = sizeof(double2) * size_t(4 * n * n + kDownGroup * n);
+    const double2* m2m_ops = reinterpret_cast<const double2*>(pl.m2m_ops.p);
+    const double2* l2l_ops = reinterpret_cast<const double2*>(pl.l2l_ops.p);
     for (int l = L - 1; l >= 2; --l) {
         const int64_t np = pl.m2m_count[size_t(l)];
         if (!np) continue;
-        shift_kernel<true><<<nblk(np, kShiftGroup), kShiftThreads, shift_smem, st>>>(
-            pl.updown_boxes.p + pl.m2m_first[size_t(l)], np,
-            reinterpret_cast<const double2*>(pl.m2m_ops.p),
-            pl.src_cnt.p + lvl_base(l + 1), mult + pl.exp_off[size_t(l + 1)],
-            mult + pl.exp_off[size_t(l)], nullptr, P);
-        VPG_LAUNCH_CHECK();
+        launch_pdl(shift_kernel<true, kUpGroup>, dim3(nblk(np, kUpGroup)), dim3(kUpGroup * kRowSlots),
+                   up_smem, st, pl.updown_boxes.p + pl.m2m_first[size_t(l)], np, m2m_ops,
+                   pl.src_cnt.p + lvl_base(l + 1), (const double2*)(mult + pl.exp_off[size_t(l + 1)]),
+                   mult + pl.exp_off[size_t(l)], P);
         ++launches;
     }
     mark(3);
     if (pl.n_m2l_batches > 0) {
         const size_t smem = sizeof(double) * (size_t(P) * pl.RP + size_t(n) * kM2LCols) +
-                            sizeof(double2) * kM2LPairs + sizeof(int) * kM2LPairs;
-        const int threads = (pl.RP / 8) * kM2LColGroups;
-        m2l_kernel<<<unsigned(pl.n_m2l_batches), threads, smem, st>>>(
-            pl.m2l_batches.p, pl.m2l_tbox.p, pl.m2l_toff.p, pl.m2l_src.p, pl.m2l_oidx.p,
-            pl.h_t.p, pl.dpow.p, pl.logmd.p, mult, loc, exp_off_d, P, pl.RP, pl.side);
-        VPG_LAUNCH_CHECK();
+                            sizeof(double2) * (size_t(kM2LPairs) * n + kM2LPairs) + 2 * sizeof(M2LStage);
+        int per_sm = 1;
+        VPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, m2l_kernel, kM2LThreads, smem));
+        const unsigned grid =
+            unsigned(std::min<int64_t>(pl.n_m2l_batches, int64_t(pl.sm_count) * std::max(per_sm, 1)));
+        launch_pdl(m2l_kernel, dim3(grid), dim3(kM2LThreads), smem, st,
+                   (const M2LBatch*)pl.m2l_batches.p, pl.n_m2l_batches, (const int32_t*)pl.m2l_tbox.p,
+                   (const int32_t*)pl.m2l_toff.p, (const int32_t*)pl.m2l_src.p,
+                   (const int32_t*)pl.m2l_oidx.p, (const double*)pl.h_t.p, (const double2*)pl.dpow.p,
+                   (const double2*)pl.logmd.p, (const double2*)mult, loc, exp_off_d, P, pl.RP, pl.side);
         ++launches;
     }
     mark(4);
     for (int l = 2; l < L; ++l) {
         const int64_t np = pl.l2l_count[size_t(l)];
         if (!np) continue;
-        shift_kernel<false><<<nblk(np, kShiftGroup), kShiftThreads, shift_smem, st>>>(
-            pl.updown_boxes.p + pl.l2l_first[size_t(l)], np,
-            reinterpret_cast<const double2*>(pl.l2l_ops.p),
-            pl.tgt_cnt.p + lvl_base(l + 1), loc + pl.exp_off[size_t(l)], nullptr,
-            loc + pl.exp_off[size_t(l + 1)], P);
-        VPG_LAUNCH_CHECK();
+        launch_pdl(shift_kernel<false, kDownGroup>, dim3(nblk(np, kDownGroup)),
+                   dim3(kDownGroup * kRowSlots), down_smem, st,
+                   pl.updown_boxes.p + pl.l2l_first[size_t(l)], np, l2l_ops,
+                   pl.tgt_cnt.p + lvl_base(l + 1), (const double2*)(loc + pl.exp_off[size_t(l)]),
+                   loc + pl.exp_off[size_t(l + 1)], P);
         ++launches;
     }
     mark(5);
+    if (pl.shard_t1 > pl.shard_t0) {
+        launch_pdl(l2p_kernel, dim3(nblk(pl.shard_t1 - pl.shard_t0, 256)), dim3(256), 0, st,
+                   (const int32_t*)pl.tgt_leaf.p, pl.shard_t0, pl.shard_t1, (const double2*)pl.tgt_sorted.p, (const double2*)(loc + pl.exp_off[size_t(L)]),
+                   P, pl.x0, pl.y0, sL, pot_far, ticket);
+        ++launches;
+    }
     if (pl.n_p2p_chunks > 0) {
-        const size_t smem = size_t(kLogTableBytes) + sizeof(double2) * 64 * kP2PWarps;
-        const int per_sm = 2;
+        const size_t smem = size_t(kLogTableBytes) + (sizeof(double2) + sizeof(double)) * kP2PBatch * kP2PWarps;
+        int per_sm = 1;
+        VPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, l2p_p2p_kernel, kP2PWarps * 32, smem));
         const int64_t want = (pl.n_p2p_chunks + kP2PWarps - 1) / kP2PWarps;
-        const unsigned grid = unsigned(std::min<int64_t>(want, int64_t(pl.sm_count) * per_sm));
-        if (pl.p2p_tpt == 2)
-            l2p_p2p_kernel<2><<<grid, kP2PWarps * 32, smem, st>>>(
-                pl.p2p_chunks.p, pl.n_p2p_chunks, pl.src_off.p, pl.src_sorted.p, qs,
-                pl.tgt_sorted.p, pl.tgt_ids.p, loc + pl.exp_off[size_t(L)], P, L, pl.x0,
-                pl.y0, sL, log_table_dev(), out_dev);
-        else
-            l2p_p2p_kernel<1><<<grid, kP2PWarps * 32, smem, st>>>(
-                pl.p2p_chunks.p, pl.n_p2p_chunks, pl.src_off.p, pl.src_sorted.p, qs,
-                pl.tgt_sorted.p, pl.tgt_ids.p, loc + pl.exp_off[size_t(L)], P, L, pl.x0,
-                pl.y0, sL, log_table_dev(), out_dev);
-        VPG_LAUNCH_CHECK();
+        const unsigned grid = unsigned(std::min<int64_t>(want, int64_t(pl.sm_count) * std::max(per_sm, 1)));
+        launch_pdl(l2p_p2p_kernel, dim3(grid), dim3(kP2PWarps * 32), smem, st,
+                   (const P2PChunk*)pl.p2p_chunks.p, pl.n_p2p_chunks, (const int32_t*)pl.src_off.p,
+                   (const double2*)pl.src_sorted.p, (const double*)qs, (const double2*)pl.tgt_sorted.p,
+                   (const int32_t*)pl.tgt_ids.p, (const double*)pot_far, L, log_table_dev(), ticket,
+                   out_dev);
         ++launches;
     }
     mark(6);

@@ -41,14 +41,14 @@ struct M2LBatch {
     int32_t efirst;  // first list entry
     int32_t ecount;
 };
-constexpr int kM2LPairs = 128;  // columns = 2 * pairs (re | im)
+constexpr int kM2LPairs = 54;  // two interior target boxes (27 each); 2 * pairs columns
 
 // P2P work unit: up to chunk targets of one leaf (Morton-sorted order).
 struct P2PChunk {
     int32_t leaf;
     int32_t tbegin;
     int32_t tcount;
-    int32_t pad;
+    int32_t pad;  // neighbourhood source count (schedule cost estimate)
 };
 
 struct Plan {
@@ -67,6 +67,7 @@ struct Plan {
     DBuf<double2> src_sorted, tgt_sorted;
     DBuf<int32_t> src_off, src_ids, tgt_off, tgt_ids;  // leaf CSR
     DBuf<int32_t> src_cnt, tgt_cnt;                    // all levels
+    DBuf<int32_t> tgt_leaf;  // leaf id of every Morton-sorted target
 
     // M2L lists (levels 2..L concatenated): target boxes and entries.
     std::vector<int64_t> lvl_tfirst;  // per level: first target-box index
@@ -116,6 +117,7 @@ struct Plan {
     std::vector<int64_t> h_epos, h_tpos;
     std::vector<int32_t> h_scnt, h_tcnt, h_soff, h_toff;
     int64_t shard_lb = 0, shard_le = 0, shard_m2l = 0;
+    int64_t shard_t0 = 0, shard_t1 = 0;  // Morton-sorted target range of the shard
 
     // Profiling.
     bool profiling = false;

@@ -342,6 +342,12 @@ void build_tree(Plan& pl) {
     pl.h_soff = to_host(pl.src_off, st);
     pl.h_toff = to_host(pl.tgt_off, st);
     {
+        std::vector<int32_t> tl(size_t(std::max<int64_t>(pl.nt, 1)), 0);
+        for (int64_t b = 0; b < nleaf; ++b)
+            for (int32_t e = pl.h_toff[size_t(b)]; e < pl.h_toff[size_t(b) + 1]; ++e) tl[size_t(e)] = int32_t(b);
+        to_device(pl.tgt_leaf, tl, st);
+    }
+    {
         std::vector<int32_t> leaves;
         for (int64_t b = 0; b < nleaf; ++b)
             if (pl.h_scnt[size_t(lvl_base(L) + b)] > 0) leaves.push_back(int32_t(b));
@@ -367,6 +373,8 @@ void build_schedules(Plan& pl, int64_t lb, int64_t le) {
     };
     pl.shard_lb = lb;
     pl.shard_le = le;
+    pl.shard_t0 = pl.h_toff[size_t(lb)];
+    pl.shard_t1 = pl.h_toff[size_t(le)];
     {
         // M2L batches of <= kM2LPairs entries that never split a target box
         // (each target's local expansion is reduced by one CTA, fixed order).
@@ -438,9 +446,9 @@ void build_schedules(Plan& pl, int64_t lb, int64_t le) {
         const int nb = 1 << L;
         int64_t occupied = 0;
         for (int64_t b = 0; b < nleaf; ++b) occupied += h_toff[size_t(b) + 1] > h_toff[size_t(b)];
-        const double avg = occupied ? double(pl.nt) / double(occupied) : 0.0;
-        pl.p2p_tpt = avg > 48.0 ? 2 : 1;
-        const int chunk = 32 * pl.p2p_tpt;
+        (void)occupied;
+        pl.p2p_tpt = 2;
+        const int chunk = 64;  // kP2PChunk: two targets per lane
         std::vector<P2PChunk> chunks;
         pl.p2p_pairs = 0;
         for (int64_t b = lb; b < le; ++b) {
@@ -455,8 +463,17 @@ void build_schedules(Plan& pl, int64_t lb, int64_t le) {
                 }
             pl.p2p_pairs += int64_t(t1 - t0) * nsrc;
             for (int32_t t = t0; t < t1; t += chunk)
-                chunks.push_back(P2PChunk{int32_t(b), t, std::min(chunk, t1 - t), 0});
+                chunks.push_back(P2PChunk{int32_t(b), t, std::min(chunk, t1 - t), int32_t(std::min<int64_t>(nsrc, INT32_MAX))});
         }
+        // Costliest chunks first (pairs ~ ceil(targets/2) * sources per lane
+        // group): the persistent grid deals them round-robin, so the long
+        // ones start early and the tail is short.  Stable, so equal-cost
+        // chunks keep Morton order.
+        std::stable_sort(chunks.begin(), chunks.end(), [](const P2PChunk& a, const P2PChunk& b) {
+            const int64_t ca = int64_t(a.pad) * ((a.tcount + 1) / 2) / std::max(1, 32 / ((a.tcount + 1) / 2));
+            const int64_t cb = int64_t(b.pad) * ((b.tcount + 1) / 2) / std::max(1, 32 / ((b.tcount + 1) / 2));
+            return ca > cb;
+        });
         pl.n_p2p_chunks = int64_t(chunks.size());
         to_device(pl.p2p_chunks, chunks, st);
     }
