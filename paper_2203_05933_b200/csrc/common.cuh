@@ -198,6 +198,22 @@ __device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src_gmem
         : "memory");
 }
 
+// Whole-CTA staging of a contiguous global block into smem with 1-D bulk
+// copies (one issuing thread, <= 32 KB per copy) -- replaces the dependent
+// load/store loops whose L2 latency dominated the small per-level kernels.
+// Must be called by every thread of the CTA; bar is a __shared__ word.
+__device__ __forceinline__ void bulk_stage(void* dst, const void* src, uint32_t bytes,
+                                           uint64_t* bar, uint32_t phase) {
+    if (threadIdx.x == 0) {
+        mbar_arrive_expect_tx(bar, bytes);
+        for (uint32_t off = 0; off < bytes; off += 32768u) {
+            const uint32_t len = bytes - off < 32768u ? bytes - off : 32768u;
+            tma_load_1d(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, len, bar);
+        }
+    }
+    mbar_wait(bar, phase);
+}
+
 // Per-device constant tables, built on first use (api.cu).
 const double2* log_table_dev();  // kLogTableSize entries (inv_c, -ln inv_c)
 const double* k0_table_dev();    // K0 Chebyshev fits, see k0.cuh

@@ -30,57 +30,87 @@ __device__ inline void box_center(double x0, double y0, double s, uint32_t id,
 }
 
 // ------------------------------------------------------------------ P2M --
-// One CTA (64 threads) per non-empty source leaf.  Sources are processed 32
-// at a time: lane t forms the running powers q*w^k of its source
-// (summation.cpp:247-254) into a [32][P+1] smem panel; thread k then sums
-// column k in source order, so each coefficient is reduced in the same
-// order as the reference loop.  Row stride P+1 complex keeps the 128-bit
-// panel accesses of each quarter-warp on distinct banks for odd P+1.
-constexpr int kP2MThreads = 64;
+// One warp per non-empty source leaf, two lanes per source: lane (j, h)
+// forms the running powers q w^k of source j (summation.cpp:247-254) for
+// the half k in (h*kh, (h+1)*kh], the upper half starting from w^kh by
+// binary powering, so the dependent multiply chain is half as long.  The
+// scaled powers -q w^k / k land in a per-warp [16][P+1] smem panel; lane k
+// then sums column k in source order.  16 sources per pass.
+constexpr int kP2MWarps = 4;
+constexpr int kP2MSrc = 16;
 
-__global__ void __launch_bounds__(kP2MThreads)
-p2m_kernel(const int32_t* leaves, const int32_t* soff, const double2* sxy,
-           const double* q, int P, double x0, double y0, double s,
-           double2* mult_leaf) {
-    extern __shared__ double2 panel[];  // [32][P+1]
+__global__ void __launch_bounds__(kP2MWarps * 32)
+p2m_kernel(const int32_t* leaves, int64_t nleaves, const int32_t* soff, const double2* sxy,
+           const double* q, int P, double x0, double y0, double s, double2* mult_leaf) {
+    extern __shared__ double2 panels[];
     pdl_trigger();
     pdl_wait();
     const int n = P + 1;
-    const uint32_t b = uint32_t(leaves[blockIdx.x]);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t li = int64_t(blockIdx.x) * kP2MWarps + warp;
+    if (li >= nleaves) return;
+    double2* panel = panels + warp * kP2MSrc * n;
+    const uint32_t b = uint32_t(leaves[li]);
     double cx, cy;
     box_center(x0, y0, s, b, cx, cy);
     const double inv_s = 1.0 / s;
     const int e0 = soff[b], e1 = soff[b + 1];
-    const int k = threadIdx.x;
-    double2 acc = make_double2(0.0, 0.0);
-    for (int base = e0; base < e1; base += 32) {
-        const int cnt = min(32, e1 - base);
-        if (k < cnt) {
-            const double2 p = sxy[base + k];
+    const int j = lane & (kP2MSrc - 1), h = lane >> 4;
+    const int kh = (P + 1) >> 1;
+    double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
+    for (int base = e0; base < e1; base += kP2MSrc) {
+        const int cnt = min(kP2MSrc, e1 - base);
+        if (j < cnt) {
+            const double2 p = sxy[base + j];
             const double wr = (p.x - cx) * inv_s, wi = (p.y - cy) * inv_s;
-            const double qj = q[base + k];
-            double2* row = panel + k * n;
-            row[0] = make_double2(qj, 0.0);
+            const double qj = q[base + j];
+            double2* row = panel + j * n;
             double pr = qj, pi = 0.0;
-            for (int j = 1; j <= P; ++j) {
+            int k0 = 1, k1 = kh;
+            if (h == 0) {
+                row[0] = make_double2(qj, 0.0);
+            } else {
+                // q w^kh by binary powering
+                double br = wr, bi = wi;
+                for (int e = kh; e; e >>= 1) {
+                    if (e & 1) {
+                        const double nr = pr * br - pi * bi;
+                        pi = pr * bi + pi * br;
+                        pr = nr;
+                    }
+                    const double sr = br * br - bi * bi;
+                    bi = 2.0 * br * bi;
+                    br = sr;
+                }
+                k0 = kh + 1;
+                k1 = P;
+            }
+            for (int k = k0; k <= k1; ++k) {
                 const double nr = pr * wr - pi * wi;
                 const double ni = pr * wi + pi * wr;
                 pr = nr;
                 pi = ni;
-                const double f = c_neg_inv_k[j];
-                row[j] = make_double2(f * pr, f * pi);
+                const double f = c_neg_inv_k[k];
+                row[k] = make_double2(f * pr, f * pi);
             }
         }
-        __syncthreads();
-        if (k <= P)
-            for (int t = 0; t < cnt; ++t) {
-                const double2 v = panel[t * n + k];
-                acc.x += v.x;
-                acc.y += v.y;
+        __syncwarp();
+        for (int t = 0; t < cnt; ++t) {
+            if (lane <= P) {
+                const double2 v0 = panel[t * n + lane];
+                acc0.x += v0.x;
+                acc0.y += v0.y;
             }
-        __syncthreads();
+            if (lane + 32 <= P) {
+                const double2 v1 = panel[t * n + lane + 32];
+                acc1.x += v1.x;
+                acc1.y += v1.y;
+            }
+        }
+        __syncwarp();
     }
-    if (k <= P) mult_leaf[int64_t(b) * n + k] = acc;
+    if (lane <= P) mult_leaf[int64_t(b) * n + lane] = acc0;
+    if (lane + 32 <= P) mult_leaf[int64_t(b) * n + lane + 32] = acc1;
 }
 
 // ------------------------------------------------------------ M2M / L2L --
@@ -102,12 +132,15 @@ __global__ void __launch_bounds__(G * kRowSlots)
 shift_kernel(const int32_t* parents, int64_t nparents, const double2* ops_t,
              const int32_t* cnt_child, const double2* in_level,
              double2* out_level, int P) {
-    extern __shared__ double2 sm[];
+    extern __shared__ __align__(16) double2 sm[];
+    __shared__ __align__(8) uint64_t bar;
     const int n = P + 1;
     const int nn = n * n;
     double2* op = sm;              // [c][k][r]
     double2* vec = sm + 4 * nn;    // up: [g][c][k]; down: [g][k]
-    for (int i = threadIdx.x; i < 4 * nn; i += blockDim.x) op[i] = ops_t[i];
+    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    bulk_stage(op, ops_t, uint32_t(4 * nn) * 16u, &bar, 0);
     pdl_trigger();
     pdl_wait();
     const int64_t g0 = int64_t(blockIdx.x) * G;
@@ -128,31 +161,40 @@ shift_kernel(const int32_t* parents, int64_t nparents, const double2* ops_t,
     const int g = threadIdx.x / kRowSlots, r = threadIdx.x % kRowSlots;
     if (g >= ng || r > P) return;
     const int64_t parent = parents[g0 + g];
-    double ar = 0.0, ai = 0.0;
-    for (int c = 0; c < 4; ++c) {
-        const int64_t child = (parent << 2) | c;
-        if (cnt_child[child] == 0) continue;
-        const double2* oc = op + c * nn + r;
-        const double2* x = kUp ? vec + (g * 4 + c) * n : vec + g * n;
-        double yr = 0.0, yi = 0.0;
-        for (int kk = 0; kk <= P; ++kk) {
-            const double2 m = oc[kk * n];
-            const double2 v = x[kk];
-            yr = fma(m.x, v.x, fma(-m.y, v.y, yr));
-            yi = fma(m.x, v.y, fma(m.y, v.x, yi));
+    // all four children at once: eight independent FMA chains per thread
+    double yr[4] = {0.0, 0.0, 0.0, 0.0}, yi[4] = {0.0, 0.0, 0.0, 0.0};
+    const double2* x0v = kUp ? vec + (g * 4) * n : vec + g * n;
+#pragma unroll 2
+    for (int kk = 0; kk <= P; ++kk) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const double2 m = op[c * nn + kk * n + r];
+            const double2 v = kUp ? x0v[c * n + kk] : x0v[kk];
+            yr[c] = fma(m.x, v.x, fma(-m.y, v.y, yr[c]));
+            yi[c] = fma(m.x, v.y, fma(m.y, v.x, yi[c]));
         }
-        if (kUp) {
-            ar += yr;
-            ai += yi;
-        } else {
+    }
+    if (kUp) {
+        // children with src_cnt == 0 were staged as zeros; sum in c order
+        double ar = 0.0, ai = 0.0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            ar += yr[c];
+            ai += yi[c];
+        }
+        out_level[parent * n + r] = make_double2(ar, ai);
+    } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int64_t child = (parent << 2) | c;
+            if (cnt_child[child] == 0) continue;
             double2* dst = out_level + child * n + r;
             double2 d = *dst;
-            d.x += yr;
-            d.y += yi;
+            d.x += yr[c];
+            d.y += yi[c];
             *dst = d;
         }
     }
-    if (kUp) out_level[parent * n + r] = make_double2(ar, ai);
 }
 
 // ------------------------------------------------------------------ M2L --
@@ -224,15 +266,15 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
     const int tid = threadIdx.x;
     const int nthr = blockDim.x;
     const int lane = tid & 31, warp = tid >> 5, nwarp = (nthr + 31) >> 5;
-    for (int i = tid; i < P * RP; i += nthr) hs[i] = h_t[i];
     if (tid == 0) mbar_init(&bar, 1);
     __syncthreads();
+    bulk_stage(hs, h_t, uint32_t(P * RP) * 8u, &bar, 0);
     pdl_trigger();
     pdl_wait();
 
     const int rg = tid / kM2LColGroups, cg = tid % kM2LColGroups;
     const bool active_rows = rg * 8 < RP && tid < kM2LGemmThreads;
-    uint32_t phase = 0;
+    uint32_t phase = 1;  // phase 0 was the H^T staging
     int cur = 0;
     int64_t bi = blockIdx.x;
     if (bi < nbatch) m2l_issue(batches[bi], esrc, eoidx, mult, exp_off, n, &stg[0], raw, &bar);
@@ -420,7 +462,13 @@ l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, const int32_t* soff,
     double2* tab = smp;                                                  // log table
     double2* sbuf = smp + kLogTableSize * kLogTableCopies;               // [warps][batch] xy
     double* qbuf = reinterpret_cast<double*>(sbuf + kP2PWarps * kP2PBatch);  // [warps][batch]
-    log_table_to_smem(tab, gtab);
+    __shared__ __align__(8) uint64_t bar;
+    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    // one bulk copy of the 257-entry table into the (still unused) source
+    // slots, then replicate 8x (log_table_to_smem)
+    bulk_stage(sbuf, gtab, uint32_t(kLogTableSize) * 16u, &bar, 0);
+    log_table_to_smem(tab, sbuf);
     pdl_trigger();
     pdl_wait();
     __syncthreads();
@@ -640,6 +688,7 @@ void build_laplace_ops(Plan& pl) {
                         cudaMemcpyHostToDevice));
 
     smem_optin((const void*)m2l_kernel, 220 * 1024);
+    smem_optin((const void*)p2m_kernel, 100 * 1024);
     smem_optin((const void*)shift_kernel<true, kUpGroup>, 220 * 1024);
     smem_optin((const void*)shift_kernel<false, kDownGroup>, 220 * 1024);
     smem_optin((const void*)l2p_p2p_kernel, 64 * 1024);
@@ -681,9 +730,9 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
 
     const double sL = pl.side / double(1 << L);
     if (pl.n_p2m_leaves > 0) {
-        launch_pdl(p2m_kernel, dim3(unsigned(pl.n_p2m_leaves)), dim3(kP2MThreads),
-                   32 * n * sizeof(double2), st, (const int32_t*)pl.p2m_leaves.p,
-                   (const int32_t*)pl.src_off.p, (const double2*)pl.src_sorted.p, (const double*)qs, P,
+        launch_pdl(p2m_kernel, dim3(nblk(pl.n_p2m_leaves, kP2MWarps)), dim3(kP2MWarps * 32),
+                   size_t(kP2MWarps) * kP2MSrc * n * sizeof(double2), st, (const int32_t*)pl.p2m_leaves.p,
+                   pl.n_p2m_leaves, (const int32_t*)pl.src_off.p, (const double2*)pl.src_sorted.p, (const double*)qs, P,
                    pl.x0, pl.y0, sL, mult + pl.exp_off[size_t(L)]);
         ++launches;
     }
