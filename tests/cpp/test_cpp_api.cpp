@@ -1,0 +1,60 @@
+// C++ mirror smoke/parity program (include/volpot_b200/summation.hpp).
+// Reads: n_src n_tgt, then src xy, q, tgt xy (float64) from argv[1];
+// writes: fmm potentials, direct potentials (skip semantics checked via
+// error path) to argv[2].  Exit 0 on success.
+#include <cstdio>
+#include <fstream>
+#include <iostream>
+#include <stdexcept>
+
+#include "volpot_b200/summation.hpp"
+
+using namespace volpot_b200;
+
+int main(int argc, char** argv) {
+    if (argc < 3) return 2;
+    std::ifstream in(argv[1], std::ios::binary);
+    int64_t ns = 0, nt = 0;
+    in.read(reinterpret_cast<char*>(&ns), 8);
+    in.read(reinterpret_cast<char*>(&nt), 8);
+    std::vector<Vec2> src(static_cast<size_t>(ns)), tgt(static_cast<size_t>(nt));
+    std::vector<double> q(static_cast<size_t>(ns));
+    in.read(reinterpret_cast<char*>(src.data()), 16 * ns);
+    in.read(reinterpret_cast<char*>(q.data()), 8 * ns);
+    in.read(reinterpret_cast<char*>(tgt.data()), 16 * nt);
+    const Kernel k = make_kernel(KernelFamily::Laplace);
+    SummationPlan plan(k, src, tgt, 1e-12);
+    std::vector<double> a = plan.apply(q);
+    std::vector<double> b = accelerated_sum(k, SourceSet{src, q}, tgt);
+    // reference error semantics
+    int errors = 0;
+    try {
+        plan.apply(std::vector<double>(3, 1.0));
+    } catch (const std::invalid_argument& e) {
+        errors += std::string(e.what()).find("does not match source count") != std::string::npos;
+    }
+    try {
+        make_kernel(KernelFamily::ModifiedHelmholtz, 0.0);
+    } catch (const std::invalid_argument&) {
+        ++errors;
+    }
+    try {
+        direct_sum(k, SourceSet{{Vec2{0, 0}}, {1.0}}, {Vec2{0, 0}});
+    } catch (const std::invalid_argument& e) {
+        errors += std::string(e.what()).find("coincides") != std::string::npos;
+    }
+    try {
+        bessel_k0(-1.0);
+    } catch (const std::domain_error&) {
+        ++errors;
+    }
+    SummationPlan moved = std::move(plan);
+    std::vector<double> c = moved.apply(q);
+    std::ofstream out(argv[2], std::ios::binary);
+    out.write(reinterpret_cast<const char*>(a.data()), 8 * nt);
+    out.write(reinterpret_cast<const char*>(b.data()), 8 * nt);
+    out.write(reinterpret_cast<const char*>(c.data()), 8 * nt);
+    std::printf("{\"levels\": %d, \"order\": %d, \"errors_ok\": %d}\n", moved.levels(),
+                moved.expansion_order(), errors);
+    return errors == 4 ? 0 : 1;
+}

@@ -1,0 +1,57 @@
+"""C++ boundary on the GPU: the header-only mirror (include/volpot_b200/
+summation.hpp) and the drop-in replacement of proj/src/summation.cpp
+(integration/volpot_summation_b200.cpp, built against the reference's own
+headers) must give the oracle's potentials and the reference's exceptions."""
+import json
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import rel_l2
+from paper_2203_05933_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BUILD = os.path.join(ROOT, "tests", "cpp", "build")
+
+
+def _run(binary, w, tmp_path):
+    inp = tmp_path / "in.bin"
+    outp = tmp_path / "out.bin"
+    with open(inp, "wb") as f:
+        np.array([w.ns, w.nt], np.int64).tofile(f)
+        w.src.astype(np.float64).tofile(f)
+        w.q.astype(np.float64).tofile(f)
+        w.tgt.astype(np.float64).tofile(f)
+    r = subprocess.run([binary, str(inp), str(outp)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    meta = json.loads(r.stdout.strip().splitlines()[-1])
+    out = np.fromfile(outp, np.float64).reshape(3, w.nt)
+    return meta, out
+
+
+def test_cpp_mirror(rest, tmp_path):
+    exe = os.path.join(BUILD, "test_cpp_api")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-C", os.path.join(ROOT, "tests", "cpp"), "api"], check=True)
+    w = W.cfg1()
+    meta, out = _run(exe, w, tmp_path)
+    assert meta["levels"] == 5 and meta["order"] == 50 and meta["errors_ok"] == 4
+    cpu = rest.plan_sum(0, 0.0, w.src, w.q, w.tgt, 1e-12)
+    for row in out:
+        assert rel_l2(row, cpu) <= 1e-13
+    assert np.array_equal(out[0], out[1]) and np.array_equal(out[0], out[2])
+
+
+def test_reference_header_dropin(rest, tmp_path):
+    exe = os.path.join(BUILD, "test_dropin")
+    if not os.path.exists(exe):
+        pytest.skip("test_dropin is built only where /root/reference exists (build())")
+    w = W.cfg2()
+    meta, out = _run(exe, w, tmp_path)
+    assert meta["levels"] == 7 and meta["order"] == 50 and meta["errors_ok"] == 2
+    cpu = rest.plan_sum(0, 0.0, w.src, w.q, w.tgt, 1e-12)
+    assert rel_l2(out[0], cpu) <= 1e-13
+    assert np.array_equal(out[0], out[1])
