@@ -45,7 +45,7 @@ THROTTLE_BITS = {
 def fp64_peak_tflops():
     with open(FP64_PEAK_FILE) as f:
         rows = [json.loads(x) for x in f if x.strip()]
-    return max(r["fp64_dfma_tflops_best"] for r in rows)
+    return max(max(r.get("fp64_dfma_tflops_best", 0.0), r.get("fp64_dmma_tflops_best", 0.0)) for r in rows)
 
 
 def hbm_peak_gbs():
@@ -320,7 +320,8 @@ def run_gpu(args):
         roofline = {"bound": "fp64", "kernel": "m2l_kernel" if dom == "m2l" else "l2p_p2p_kernel",
                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                     "traffic": None,
-                    "peak_source": "measured DFMA microbenchmark (tools/fp64_peak.cu, profiles/fp64_peak_r01.json); "
+                    "peak_source": "measured FP64 peak, max of DFMA (tools/fp64_peak.cu) and DMMA "
+                                   "(tools/dmma_peak.cu) microbenchmarks, profiles/fp64_peak_r01.json; "
                                    "MEASURED_PEAKS.json has no FP64 entry",
                     "flops_per_unit": ("4P(P+1)+8(P+1)+6P executed per M2L pair" if dom == "m2l"
                                        else "27 per near-field pair (SURVEY.md 8d convention)")}

@@ -217,155 +217,222 @@ shift_kernel(const int32_t* parents, int64_t nparents, const double2* ops_t,
 //      shift qsum*log(s_l) (summation.cpp:297-301).
 // Executed flops per pair: 4 P (P+1) for the GEMM + O(P), half the dense
 // 8 (P+1)^2 of the reference matvec.
-constexpr int kM2LCols = 2 * kM2LPairs;  // 108
-constexpr int kM2LColGroups = kM2LCols / 4;      // 27 groups of 4 columns, interleaved
-constexpr int kM2LGemmThreads = 7 * kM2LColGroups;  // 189; RP <= 56
-constexpr int kM2LThreads = 192;                     // whole warps for the warp loops
+constexpr int kM2LCols = 2 * kM2LPairs;          // 108 used columns
+constexpr int kM2LNTiles = (kM2LCols + 7) / 8;   // 14 DMMA column tiles
+constexpr int kM2LXS = 116;                      // X/Y row stride (== 4 mod 16: conflict-free fragments)
+constexpr int kM2LHS = 60;                       // H^T row stride (== 12 mod 16)
+constexpr int kM2LGroupThreads = 192;            // six warps per batch group
+constexpr int kM2LGroupWarps = kM2LGroupThreads / 32;
+constexpr int kM2LGroups = 2;                    // two batches in flight per CTA
+constexpr int kM2LThreads = kM2LGroups * kM2LGroupThreads;
+constexpr int kM2LCanon = 7;                     // offsets up to the square's symmetry
+constexpr int kM2LMaxMT = 7;                     // RP <= 56
+constexpr int kM2LNTPerWarp = (kM2LNTiles + kM2LGroupWarps - 1) / kM2LGroupWarps;  // 3
 
-// Batch staging: source multipole rows of the NEXT batch are fetched with 1-D
-// TMA bulk copies (one 16(P+1)-byte row per list entry, mbarrier
-// completion) while the current batch runs its GEMM and epilogue.
+// Offset powers through the symmetry of the square: every interaction offset
+// d is u * conj^s(c) for a canonical c in {(2,0),(2,1),(2,2),(3,0),(3,1),
+// (3,2),(3,3)} and u = i^m', so d^-j = i^(m j) conj^s(c^-j) (m = -m' mod 4).
+// The table c^-j (7 x (P+1) complex, 5.7 KB at P=50) lives in smem; the
+// conjugation and the quarter turn i^r are sign flips and a swap done on
+// the integer words (no FP64 instructions).
+__device__ __forceinline__ double2 turn(double2 v, int r, int sconj) {
+    int xh = __double2hiint(v.x), xl = __double2loint(v.x);
+    int yh = __double2hiint(v.y) ^ (sconj << 31), yl = __double2loint(v.y);
+    const bool sw = r & 1;
+    int ah = sw ? yh : xh, al = sw ? yl : xl;
+    int bh = sw ? xh : yh, bl = sw ? xl : yl;
+    ah ^= ((r + 1) & 2) << 30;  // new re negated for r = 1, 2
+    bh ^= (r & 2) << 30;        // new im negated for r = 2, 3
+    return make_double2(__hiloint2double(ah, al), __hiloint2double(bh, bl));
+}
+
 struct M2LStage {
     int32_t src[kM2LPairs];
+    int32_t omap[kM2LPairs];
     int32_t oidx[kM2LPairs];
 };
 
+__device__ __forceinline__ void group_sync(int g) {
+    asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(kM2LGroupThreads) : "memory");
+}
+
+__device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
 __device__ __forceinline__ void m2l_issue(const M2LBatch& bt, const int32_t* esrc,
-                                          const int32_t* eoidx, const double2* mult,
-                                          const int64_t* exp_off, int n, M2LStage* stg,
-                                          double2* raw, uint64_t* bar) {
-    // called by all threads; thread p < ecount owns entry p
-    const int p = threadIdx.x;
+                                          const int32_t* eoidx, const int32_t* omap_s,
+                                          const double2* mult, const int64_t* exp_off, int n,
+                                          M2LStage* stg, double2* raw, uint64_t* bar, int gtid) {
     const double2* mlev = mult + exp_off[bt.level];
-    if (p == 0) mbar_arrive_expect_tx(bar, uint32_t(bt.ecount) * uint32_t(n) * 16u);
-    if (p < bt.ecount) {
-        const int64_t e = int64_t(bt.efirst) + p;
+    if (gtid == 0) mbar_arrive_expect_tx(bar, uint32_t(bt.ecount) * uint32_t(n) * 16u);
+    if (gtid < bt.ecount) {
+        const int64_t e = int64_t(bt.efirst) + gtid;
         const int sid = esrc[e];
-        stg->src[p] = sid;
-        stg->oidx[p] = eoidx[e];
-        tma_load_1d(raw + p * n, mlev + int64_t(sid) * n, uint32_t(n) * 16u, bar);
+        const int o = eoidx[e];
+        stg->src[gtid] = sid;
+        stg->oidx[gtid] = o;
+        stg->omap[gtid] = omap_s[o];
+        tma_load_1d(raw + gtid * n, mlev + int64_t(sid) * n, uint32_t(n) * 16u, bar);
     }
 }
 
-__global__ void __launch_bounds__(kM2LThreads, 2)
+// Factorised M2L (see the block comment above): per batch one dense real
+// GEMM Y = H X on the FP64 tensor cores (mma.sync m8n8k4, DMMA: 256 FMA per
+// warp instruction, measured 36.9 TFLOP/s on this B200 vs 34.2 for DFMA).
+// A CTA runs two independent batch groups of 192 threads (named barriers)
+// that share H^T, the canonical offset-power table and log(-d); each group
+// double-buffers its source rows with 1-D TMA bulk copies (mbarrier
+// completion) so the next batch lands while the current one computes.
+__global__ void __launch_bounds__(kM2LThreads, 1)
 m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
            const int32_t* toff, const int32_t* esrc, const int32_t* eoidx,
-           const double* h_t, const double2* dpow, const double2* logmd,
-           const double2* mult, double2* loc, const int64_t* exp_off, int P, int RP,
-           double side) {
+           const double* h_t, const double2* canon_g, const int32_t* omap_g,
+           const double2* logmd_g, const double2* mult, double2* loc, const int64_t* exp_off,
+           int P, int RP, int KP, double side) {
     extern __shared__ __align__(16) double smd[];
     const int n = P + 1;
-    const int dp_stride = 2 * P + 1;
-    double* hs = smd;                                        // [P][RP]
-    double2* raw = reinterpret_cast<double2*>(hs + P * RP);  // [pairs][n] TMA landing
-    double* xy = reinterpret_cast<double*>(raw + kM2LPairs * n);  // [n][cols]
-    double2* a0s = reinterpret_cast<double2*>(xy + n * kM2LCols);  // [pairs]
-    M2LStage* stg = reinterpret_cast<M2LStage*>(a0s + kM2LPairs);  // [2]
-    __shared__ __align__(8) uint64_t bar;
+    const int XR = max(KP, n);                                  // X/Y rows
+    double* hs = smd;                                           // [KP][kM2LHS]
+    double2* canon = reinterpret_cast<double2*>(hs + KP * kM2LHS);  // [7][n]
+    double2* logmd = canon + kM2LCanon * n;                     // [49]
+    int32_t* omap_s = reinterpret_cast<int32_t*>(logmd + 49);   // [49] (+pad)
+    char* gbase = reinterpret_cast<char*>(omap_s + 52);
+    const size_t gbytes = sizeof(double2) * (size_t(kM2LPairs) * n + kM2LPairs) +
+                          sizeof(double) * size_t(XR) * kM2LXS + 2 * sizeof(M2LStage);
+    __shared__ __align__(8) uint64_t bars[1 + kM2LGroups];
 
     const int tid = threadIdx.x;
-    const int nthr = blockDim.x;
-    const int lane = tid & 31, warp = tid >> 5, nwarp = (nthr + 31) >> 5;
-    if (tid == 0) mbar_init(&bar, 1);
+    const int g = tid / kM2LGroupThreads, gtid = tid % kM2LGroupThreads;
+    const int lane = gtid & 31, warp = gtid >> 5;
+    char* gp = gbase + size_t(g) * gbytes;
+    double2* raw = reinterpret_cast<double2*>(gp);
+    double* xy = reinterpret_cast<double*>(raw + kM2LPairs * n);
+    double2* a0s = reinterpret_cast<double2*>(xy + XR * kM2LXS);
+    M2LStage* stg = reinterpret_cast<M2LStage*>(a0s + kM2LPairs);
+    if (tid == 0)
+        for (int i = 0; i <= kM2LGroups; ++i) mbar_init(&bars[i], 1);
+    for (int i = tid; i < kM2LCanon * n; i += blockDim.x) canon[i] = canon_g[i];
+    for (int i = tid; i < 49; i += blockDim.x) {
+        logmd[i] = logmd_g[i];
+        omap_s[i] = omap_g[i];
+    }
     __syncthreads();
-    bulk_stage(hs, h_t, uint32_t(P * RP) * 8u, &bar, 0);
+    bulk_stage(hs, h_t, uint32_t(KP * kM2LHS) * 8u, &bars[0], 0);
+    __syncthreads();
     pdl_trigger();
     pdl_wait();
 
-    const int rg = tid / kM2LColGroups, cg = tid % kM2LColGroups;
-    const bool active_rows = rg * 8 < RP && tid < kM2LGemmThreads;
-    uint32_t phase = 1;  // phase 0 was the H^T staging
+    uint64_t* bar = &bars[1 + g];
+    const int MT = RP / 8;
+    uint32_t phase = 0;
     int cur = 0;
-    int64_t bi = blockIdx.x;
-    if (bi < nbatch) m2l_issue(batches[bi], esrc, eoidx, mult, exp_off, n, &stg[0], raw, &bar);
+    const int64_t stride = int64_t(gridDim.x) * kM2LGroups;
+    int64_t bi = int64_t(blockIdx.x) * kM2LGroups + g;
+    if (bi < nbatch)
+        m2l_issue(batches[bi], esrc, eoidx, omap_s, mult, exp_off, n, &stg[0], raw, bar, gtid);
 
-    for (; bi < nbatch; bi += gridDim.x) {
+    for (; bi < nbatch; bi += stride) {
         const M2LBatch bt = batches[bi];
         double2* llev = loc + exp_off[bt.level];
         const M2LStage& sg = stg[cur];
-        mbar_wait(&bar, phase);
+        mbar_wait(bar, phase);
         phase ^= 1u;
-        // 1. X[k-1][2p | 2p+1] = (-1)^k d^-k a_k from the landed rows
-        //    (d^-j table in global memory, L1-resident: 49 x (2P+1));
-        //    warp per entry, lane per coefficient.
-        for (int p = warp; p < bt.ecount; p += nwarp) {
+        // 1. X[k-1][2p | 2p+1] = (-1)^k d^-k a_k (warp per entry, lane per k);
+        //    (-1)^k d^-k = i^((m+2)k) conj^s(c^-k)
+        for (int p = warp; p < bt.ecount; p += kM2LGroupWarps) {
             const double2* rr = raw + p * n;
-            const double2* dr = dpow + sg.oidx[p] * dp_stride;
+            const int om = sg.omap[p];
+            const int ci = om & 7, sc = (om >> 3) & 1, m2 = ((om >> 4) & 3) + 2;
+            const double2* crow = canon + ci * n;
             for (int k = lane; k <= P; k += 32) {
                 const double2 a = rr[k];
                 if (k == 0) {
                     a0s[p] = a;
                 } else {
-                    double2 d = __ldg(dr + k);
-                    if (k & 1) {
-                        d.x = -d.x;
-                        d.y = -d.y;
-                    }
-                    xy[(k - 1) * kM2LCols + 2 * p] = a.x * d.x - a.y * d.y;
-                    xy[(k - 1) * kM2LCols + 2 * p + 1] = a.x * d.y + a.y * d.x;
+                    const double2 d = turn(crow[k], (m2 * k) & 3, sc);
+                    double* xr = xy + (k - 1) * kM2LXS + 2 * p;
+                    xr[0] = a.x * d.x - a.y * d.y;
+                    xr[1] = a.x * d.y + a.y * d.x;
                 }
             }
         }
-        __syncthreads();
+        for (int i = gtid; i < (KP - P) * kM2LXS; i += kM2LGroupThreads) xy[P * kM2LXS + i] = 0.0;
+        group_sync(g);
         // raw[] is free: start the next batch's copies under this GEMM
-        // (generic-proxy reads of raw[] above must precede the async writes)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        const int64_t bn = bi + gridDim.x;
-        if (bn < nbatch) m2l_issue(batches[bn], esrc, eoidx, mult, exp_off, n, &stg[cur ^ 1], raw, &bar);
+        const int64_t bn = bi + stride;
+        if (bn < nbatch)
+            m2l_issue(batches[bn], esrc, eoidx, omap_s, mult, exp_off, n, &stg[cur ^ 1], raw, bar,
+                      gtid);
 
-        // 2. GEMM: thread (rg, cg) owns rows rg*8..rg*8+7, columns cg + 27 j.
-        double acc[8][4];
+        // 2. DMMA GEMM: warp w owns column tiles w, w+6, w+12 and all row tiles
+        double acc[kM2LMaxMT][kM2LNTPerWarp][2];
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+        for (int i = 0; i < kM2LMaxMT; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-        if (active_rows) {
-            const double* hcol = hs + rg * 8;
-            const double* xcol = xy + cg;
-#pragma unroll 2
-            for (int k = 0; k < P; ++k) {
-                const double2 h01 = *reinterpret_cast<const double2*>(hcol + k * RP);
-                const double2 h23 = *reinterpret_cast<const double2*>(hcol + k * RP + 2);
-                const double2 h45 = *reinterpret_cast<const double2*>(hcol + k * RP + 4);
-                const double2 h67 = *reinterpret_cast<const double2*>(hcol + k * RP + 6);
-                const double h[8] = {h01.x, h01.y, h23.x, h23.y, h45.x, h45.y, h67.x, h67.y};
-                double x[4];
+            for (int j = 0; j < kM2LNTPerWarp; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        {
+            const int kq = lane & 3, rq = lane >> 2;
+            const double* hcol = hs + kq * kM2LHS + rq;
+            const double* xcol = xy + kq * kM2LXS + rq;
+            for (int k4 = 0; k4 < KP; k4 += 4) {
+                double bfr[kM2LNTPerWarp];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) x[j] = xcol[k * kM2LCols + kM2LColGroups * j];
+                for (int j = 0; j < kM2LNTPerWarp; ++j) {
+                    const int nt = warp + kM2LGroupWarps * j;
+                    bfr[j] = nt < kM2LNTiles ? xcol[k4 * kM2LXS + 8 * nt] : 0.0;
+                }
 #pragma unroll
-                for (int i = 0; i < 8; ++i)
+                for (int i = 0; i < kM2LMaxMT; ++i) {
+                    if (i < MT) {
+                        const double afr = hcol[k4 * kM2LHS + 8 * i];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) acc[i][j] = fma(h[i], x[j], acc[i][j]);
+                        for (int j = 0; j < kM2LNTPerWarp; ++j)
+                            if (warp + kM2LGroupWarps * j < kM2LNTiles)
+                                dmma_884(acc[i][j][0], acc[i][j][1], afr, bfr[j]);
+                    }
+                }
             }
         }
-        __syncthreads();  // everyone done reading X
-        // 3a. Y to smem, then per (entry p, row l): b_0 = y_0 + log(-d) a_0,
-        //     b_l = d^-l (y_l - a_0 / l), in place.
-        if (active_rows) {
+        group_sync(g);  // everyone done reading X
+        {
+            const int r0 = lane >> 2, c0 = 2 * (lane & 3);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int l = rg * 8 + i;
-                if (l < n)
+            for (int i = 0; i < kM2LMaxMT; ++i) {
+                const int l = 8 * i + r0;
+                if (i < MT && l <= P)
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) xy[l * kM2LCols + cg + kM2LColGroups * j] = acc[i][j];
+                    for (int j = 0; j < kM2LNTPerWarp; ++j) {
+                        const int nt = warp + kM2LGroupWarps * j;
+                        if (nt < kM2LNTiles) {
+                            double* y = xy + l * kM2LXS + 8 * nt + c0;
+                            y[0] = acc[i][j][0];
+                            y[1] = acc[i][j][1];
+                        }
+                    }
             }
         }
-        __syncthreads();
-        for (int l = warp; l <= P; l += nwarp) {
+        group_sync(g);
+        // 3a. per (row l, entry p): b_0 = y_0 + log(-d) a_0,
+        //     b_l = d^-l (y_l - a_0 / l), in place
+        for (int l = warp; l <= P; l += kM2LGroupWarps) {
             const double inv_l = l > 0 ? c_neg_inv_k[l] : 0.0;  // -1/l
-            double* yrow = xy + l * kM2LCols;
+            double* yrow = xy + l * kM2LXS;
             for (int p = lane; p < bt.ecount; p += 32) {
                 const double yr = yrow[2 * p], yi = yrow[2 * p + 1];
                 const double2 a0 = a0s[p];
-                const int o = sg.oidx[p];
+                const int om = sg.omap[p];
                 double br, bim;
                 if (l == 0) {
-                    const double2 lg = logmd[o];
+                    const double2 lg = logmd[sg.oidx[p]];
                     br = yr + (lg.x * a0.x - lg.y * a0.y);
                     bim = yi + (lg.x * a0.y + lg.y * a0.x);
                 } else {
                     const double zr = fma(inv_l, a0.x, yr), zi = fma(inv_l, a0.y, yi);
-                    const double2 dl = __ldg(dpow + o * dp_stride + l);
+                    const double2 dl = turn(canon[(om & 7) * n + l], (((om >> 4) & 3) * l) & 3, (om >> 3) & 1);
                     br = dl.x * zr - dl.y * zi;
                     bim = dl.x * zi + dl.y * zr;
                 }
@@ -373,17 +440,17 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
                 yrow[2 * p + 1] = bim;
             }
         }
-        __syncthreads();
-        // 3b. per (target t, row l): sum the entries in list order, add the
-        // monopole shift (summation.cpp:297-301)
+        group_sync(g);
+        // 3b. per (target t, row l): sum the entries in list order and add
+        //     the monopole shift (summation.cpp:297-301)
         const double logs = log(side / double(1 << bt.level));
         {
-            const int l = tid & 63;
+            const int l = gtid & 63;
             if (l <= P)
-                for (int t = tid >> 6; t < bt.tcount; t += (nthr + 63) >> 6) {
+                for (int t = gtid >> 6; t < bt.tcount; t += kM2LGroupThreads >> 6) {
                     const int64_t tg = int64_t(bt.tfirst) + t;
                     const int p0 = toff[tg] - bt.efirst, p1 = toff[tg + 1] - bt.efirst;
-                    const double* yrow = xy + l * kM2LCols;
+                    const double* yrow = xy + l * kM2LXS;
                     double sr = 0.0, si = 0.0, qsum = 0.0;
 #pragma unroll 4
                     for (int p = p0; p < p1; ++p) {
@@ -396,7 +463,7 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
                 }
         }
         cur ^= 1;
-        __syncthreads();  // xy / a0s reused by the next batch
+        group_sync(g);  // xy / a0s reused by the next batch
     }
 }
 
@@ -641,9 +708,10 @@ void build_laplace_ops(Plan& pl) {
 
     // M2L factors: H^T[k-1][l] = C(l+k-1, k-1); d^-j and log(-d) per offset
     // (summation.cpp:199-220).
-    std::vector<double> ht(size_t(P) * pl.RP, 0.0);
+    pl.KP = ((P + 3) / 4) * 4;  // DMMA k-steps of 4
+    std::vector<double> ht(size_t(pl.KP) * kM2LHS, 0.0);
     for (int k = 1; k <= P; ++k)
-        for (int l = 0; l <= P; ++l) ht[size_t(k - 1) * pl.RP + l] = B(l + k - 1, k - 1);
+        for (int l = 0; l <= P; ++l) ht[size_t(k - 1) * kM2LHS + l] = B(l + k - 1, k - 1);
     const int dps = 2 * P + 1;
     std::vector<cplx> dpw(size_t(49) * dps, cplx{0, 0});
     std::vector<cplx> lg(49, cplx{0, 0});
@@ -659,7 +727,49 @@ void build_laplace_ops(Plan& pl) {
             lg[size_t(o)] = {0.5 * std::log(m2), std::atan2(double(-dy), double(-dx))};
         }
 
+    // canonical offsets and the map offset -> (canonical, conj, quarter turns)
+    const int canon_xy[kM2LCanon][2] = {{2, 0}, {2, 1}, {2, 2}, {3, 0}, {3, 1}, {3, 2}, {3, 3}};
+    std::vector<cplx> canon(size_t(kM2LCanon) * n, cplx{0, 0});
+    for (int ci = 0; ci < kM2LCanon; ++ci) {
+        const double cx = canon_xy[ci][0], cy = canon_xy[ci][1];
+        const double m2 = cx * cx + cy * cy;
+        const cplx cinv{cx / m2, -cy / m2};
+        cplx* row = canon.data() + size_t(ci) * n;
+        row[0] = {1.0, 0.0};
+        for (int j = 1; j <= P; ++j) row[j] = cmul(row[j - 1], cinv);
+    }
+    std::vector<int32_t> omap(49, 0);
+    for (int dy = -3; dy <= 3; ++dy)
+        for (int dx = -3; dx <= 3; ++dx) {
+            if (std::max(std::abs(dx), std::abs(dy)) < 2) continue;
+            const int o = (dx + 3) + 7 * (dy + 3);
+            bool found = false;
+            for (int sc = 0; sc < 2 && !found; ++sc)
+                for (int mq = 0; mq < 4 && !found; ++mq) {
+                    // cand = conj^sc(d * i^-mq)
+                    int ax = dx, ay = dy;
+                    for (int r = 0; r < mq; ++r) {  // multiply by -i: (x, y) -> (y, -x)
+                        const int t = ax;
+                        ax = ay;
+                        ay = -t;
+                    }
+                    if (sc) ay = -ay;
+                    for (int ci = 0; ci < kM2LCanon; ++ci)
+                        if (ax == canon_xy[ci][0] && ay == canon_xy[ci][1]) {
+                            // d = i^mq conj^sc(c)  =>  d^-j = i^(-mq j) conj^sc(c^-j)
+                            omap[size_t(o)] = ci | (sc << 3) | (((4 - mq) & 3) << 4);
+                            found = true;
+                            break;
+                        }
+                }
+            if (!found) throw Error{VPG_ERR_CUDA, "offset symmetry map incomplete"};
+        }
+
     cudaStream_t st = 0;
+    pl.m2l_canon.alloc(canon.size());
+    pl.m2l_omap.alloc(omap.size());
+    VPG_CUDA(cudaMemcpyAsync(pl.m2l_canon.p, canon.data(), pl.m2l_canon.bytes(), cudaMemcpyHostToDevice, st));
+    VPG_CUDA(cudaMemcpyAsync(pl.m2l_omap.p, omap.data(), pl.m2l_omap.bytes(), cudaMemcpyHostToDevice, st));
     pl.m2m_ops.alloc(size_t(4) * n * n * 2);
     pl.l2l_ops.alloc(size_t(4) * n * n * 2);
     pl.h_t.alloc(ht.size());
@@ -687,7 +797,7 @@ void build_laplace_ops(Plan& pl) {
     VPG_CUDA(cudaMemcpy(pl.exp_off_dev.p, pl.exp_off.data(), pl.exp_off_dev.bytes(),
                         cudaMemcpyHostToDevice));
 
-    smem_optin((const void*)m2l_kernel, 220 * 1024);
+    smem_optin((const void*)m2l_kernel, 225 * 1024);
     smem_optin((const void*)p2m_kernel, 100 * 1024);
     smem_optin((const void*)shift_kernel<true, kUpGroup>, 220 * 1024);
     smem_optin((const void*)shift_kernel<false, kDownGroup>, 220 * 1024);
@@ -752,17 +862,21 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
     }
     mark(3);
     if (pl.n_m2l_batches > 0) {
-        const size_t smem = sizeof(double) * (size_t(P) * pl.RP + size_t(n) * kM2LCols) +
-                            sizeof(double2) * (size_t(kM2LPairs) * n + kM2LPairs) + 2 * sizeof(M2LStage);
-        int per_sm = 1;
-        VPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, m2l_kernel, kM2LThreads, smem));
-        const unsigned grid =
-            unsigned(std::min<int64_t>(pl.n_m2l_batches, int64_t(pl.sm_count) * std::max(per_sm, 1)));
+        const int XR = std::max(pl.KP, n);
+        const size_t gbytes = sizeof(double2) * (size_t(kM2LPairs) * n + kM2LPairs) +
+                              sizeof(double) * size_t(XR) * kM2LXS + 2 * sizeof(M2LStage);
+        const size_t smem = sizeof(double) * size_t(pl.KP) * kM2LHS +
+                            sizeof(double2) * (size_t(kM2LCanon) * n + 49) + sizeof(int32_t) * 52 +
+                            kM2LGroups * gbytes;
+        const unsigned grid = unsigned(std::min<int64_t>((pl.n_m2l_batches + kM2LGroups - 1) / kM2LGroups,
+                                                         int64_t(pl.sm_count)));
         launch_pdl(m2l_kernel, dim3(grid), dim3(kM2LThreads), smem, st,
                    (const M2LBatch*)pl.m2l_batches.p, pl.n_m2l_batches, (const int32_t*)pl.m2l_tbox.p,
                    (const int32_t*)pl.m2l_toff.p, (const int32_t*)pl.m2l_src.p,
-                   (const int32_t*)pl.m2l_oidx.p, (const double*)pl.h_t.p, (const double2*)pl.dpow.p,
-                   (const double2*)pl.logmd.p, (const double2*)mult, loc, exp_off_d, P, pl.RP, pl.side);
+                   (const int32_t*)pl.m2l_oidx.p, (const double*)pl.h_t.p,
+                   (const double2*)pl.m2l_canon.p, (const int32_t*)pl.m2l_omap.p,
+                   (const double2*)pl.logmd.p, (const double2*)mult, loc, exp_off_d, P, pl.RP, pl.KP,
+                   pl.side);
         ++launches;
     }
     mark(4);

@@ -81,7 +81,10 @@ struct Plan {
     DBuf<double> h_t;               // H^T: P x RP (k-major), real
     DBuf<double2> dpow;             // 49 x (2P+1): d^-j per offset
     DBuf<double2> logmd;            // 49: log(-d)
+    DBuf<double2> m2l_canon;        // 7 x (P+1): c^-j for the canonical offsets
+    DBuf<int32_t> m2l_omap;         // 49: offset -> canonical | conj<<3 | quarter turns<<4
     int RP = 0;                     // rows padded to a multiple of 8
+    int KP = 0;                     // P padded to a multiple of 4 (DMMA k-steps)
 
     // Upward/downward expansion level sizes.
     std::vector<int64_t> exp_off;  // per level offset (in complex) into scratch
