@@ -479,7 +479,10 @@ l2p_kernel(const int32_t* tleaf, int64_t t0, int64_t t1, const double2* txy,
     pdl_trigger();
     pdl_wait();
     const int64_t e = t0 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-    if (e == t0) *ticket = 0;  // near-field work counter for l2p_p2p_kernel
+    if (e == t0) {  // near-field work counters for l2p_p2p_kernel
+        ticket[0] = 0;
+        ticket[1] = 0;
+    }
     if (e >= t1) return;
     const uint32_t b = uint32_t(tleaf[e]);
     double cx, cy;
@@ -500,28 +503,111 @@ l2p_kernel(const int32_t* tleaf, int64_t t0, int64_t t1, const double2* txy,
 }
 
 // ------------------------------------------------------- near-field P2P --
-// A persistent grid of warps walks the target chunks (<= 64 targets of one
-// leaf).  Per chunk the warp
-//   1. picks up the far-field value of its targets (l2p_kernel);
-//   2. flattens the 3x3 neighbour leaves (summation.cpp:330-334, reference
-//      order: jy outer, jx inner) into one virtual source list -- lanes 0..8
-//      own one neighbour range each, a shuffle scan gives the flat offsets;
-//   3. streams that list through a per-warp smem slot, kP2PBatch sources at
-//      a time (coalesced loads, then broadcast reads); every lane holds two
-//      targets, so one source fetch feeds two pair evaluations (p2p.cuh);
-//   4. undoes the r^2 == 0 pairs (coincident points share a leaf, so only the
-//      centre leaf is rescanned) -- the hot loop itself has no zero test.
-// Small leaves (cfg1/cfg2: ~15 targets) would idle most of the warp, so the
-// warp splits into S = 32 / ceil(nT/2) groups taking every S-th source; the
-// S partial sums are added in group order (fixed order: results are
-// run-to-run identical).  Output is scattered to the original target order
+// Persistent CTAs over target chunks (<= 64 targets of one leaf, sorted
+// costliest first at plan time).  For a chunk, the 3x3 neighbour leaves
+// (summation.cpp:330-334, reference order jy outer, jx inner) are flattened
+// into one virtual source list -- lanes 0..8 own one neighbour range each, a
+// shuffle scan gives the flat offsets -- and streamed through a per-warp
+// smem slot kP2PBatch sources at a time (coalesced loads, broadcast reads).
+// Every lane holds two targets, so one source fetch feeds two pairs.  The
+// hot loop has no zero test: pairs of the centre leaf (the only place equal
+// coordinates can meet) are undone and redone with the reference skip rule
+// right after their batch (lap_pair_fixup).
+//   Heavy chunks (>= kP2PCoopSources sources) are processed by the whole CTA:
+//   warp w takes batches w, w+8, ...; the eight partial sums per target are
+//   added in warp order through smem.
+//   Light chunks (small leaves, cfg1/cfg2 interior) are taken by single
+//   warps; to keep lanes busy with ~15-target leaves the warp splits into
+//   S = 32 / ceil(nT/2) groups taking every S-th source, partials added in
+//   group order.
+// Both phases draw from ticket counters zeroed by l2p_kernel; every sum has
+// a fixed order, so results are run-to-run identical.  Output: far field
+// (l2p_kernel) + near field, scattered to the original target order
 // (summation.cpp:345).
 constexpr int kP2PWarps = 8;
 constexpr int kP2PBatch = 64;
 constexpr int kP2PChunk = 64;
 
+struct NearList {
+    int total;
+    int pre[9], st[9];
+};
+
+__device__ __forceinline__ NearList near_list(uint32_t b, int nb, const int32_t* soff, int lane) {
+    const int ix = int(squash2(b)), iy = int(squash2(b >> 1));
+    int rs = 0, rl = 0;
+    if (lane < 9) {
+        const int jx = ix - 1 + lane % 3, jy = iy - 1 + lane / 3;
+        if (jx >= 0 && jx < nb && jy >= 0 && jy < nb) {
+            const uint32_t sid = mort(uint32_t(jx), uint32_t(jy));
+            rs = soff[sid];
+            rl = soff[sid + 1] - rs;
+        }
+    }
+    int incl = rl;
+#pragma unroll
+    for (int o = 1; o < 16; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    NearList nl;
+    nl.total = __shfl_sync(0xffffffffu, incl, 8);
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+        nl.pre[i] = __shfl_sync(0xffffffffu, incl - rl, i);
+        nl.st[i] = __shfl_sync(0xffffffffu, rs, i);
+    }
+    return nl;
+}
+
+// One batch [base, base+cnt) of the flat list: stage, evaluate (sources
+// f == grp mod S), then fix up the centre-leaf pairs of the batch.
+__device__ __forceinline__ void near_batch(const NearList& nl, int base, int cnt, int grp, int S,
+                                           bool active, int lane, const double2* sxy,
+                                           const double* q, double2* mxy, double* mq,
+                                           uint32_t tab_lane, const double (&tx)[2],
+                                           const double (&ty)[2], LapAcc (&acc)[2]) {
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < kP2PBatch / 32; ++h) {
+        const int f = h * 32 + lane;
+        if (f < cnt) {
+            const int ff = base + f;
+            int src = nl.st[0] + ff;
+#pragma unroll
+            for (int i = 1; i < 9; ++i)
+                if (ff >= nl.pre[i]) src = nl.st[i] + (ff - nl.pre[i]);
+            mxy[f] = sxy[src];
+            mq[f] = q[src];
+        }
+    }
+    __syncwarp();
+    if (!active) return;
+    int j = grp - base % S;
+    if (j < 0) j += S;
+#pragma unroll 2
+    for (; j < cnt; j += S) {
+        const double2 sp = mxy[j];
+        const double qj = mq[j];
+        lap_pair_fast(tx[0], ty[0], sp.x, sp.y, qj, tab_lane, acc[0]);
+        lap_pair_fast(tx[1], ty[1], sp.x, sp.y, qj, tab_lane, acc[1]);
+    }
+    // centre leaf = neighbour 4 (it always exists): flat range [pre4, pre5)
+    const int c0 = max(nl.pre[4], base), c1 = min(nl.pre[5], base + cnt);
+    if (c0 < c1) {
+        int f = c0 + (grp - c0 % S);
+        if (f < c0) f += S;
+        for (; f < c1; f += S) {
+            const double2 sp = mxy[f - base];
+            const double qj = mq[f - base];
+            lap_pair_fixup(tx[0], ty[0], sp.x, sp.y, qj, tab_lane, acc[0]);
+            lap_pair_fixup(tx[1], ty[1], sp.x, sp.y, qj, tab_lane, acc[1]);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kP2PWarps * 32)
-l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, const int32_t* soff,
+l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, int64_t nheavy, const int32_t* soff,
                const double2* sxy, const double* q, const double2* txy,
                const int32_t* tids, const double* pot_far, int L,
                const double2* gtab, int* ticket, double* out) {
@@ -529,7 +615,9 @@ l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, const int32_t* soff,
     double2* tab = smp;                                                  // log table
     double2* sbuf = smp + kLogTableSize * kLogTableCopies;               // [warps][batch] xy
     double* qbuf = reinterpret_cast<double*>(sbuf + kP2PWarps * kP2PBatch);  // [warps][batch]
+    double* red = qbuf + kP2PWarps * kP2PBatch;                          // [warps][64]
     __shared__ __align__(8) uint64_t bar;
+    __shared__ int s_ch;
     if (threadIdx.x == 0) mbar_init(&bar, 1);
     __syncthreads();
     // one bulk copy of the 257-entry table into the (still unused) source
@@ -545,108 +633,75 @@ l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, const int32_t* soff,
     double* mq = qbuf + warp * kP2PBatch;
     const int nb = 1 << L;
 
-    // Dynamic schedule: chunks are sorted costliest first (tree.cu); each
-    // warp takes the next one from a ticket counter zeroed by l2p_kernel.
+    // ---- phase 1: heavy chunks, the whole CTA per chunk
     for (;;) {
-        int ch = 0;
-        if (lane == 0) ch = atomicAdd(ticket, 1);
-        ch = __shfl_sync(0xffffffffu, ch, 0);
+        if (threadIdx.x == 0) s_ch = atomicAdd(&ticket[0], 1);
+        __syncthreads();
+        const int64_t ch = s_ch;
+        __syncthreads();
+        if (ch >= nheavy) break;
+        const P2PChunk c = chunks[ch];
+        const int nT = c.tcount;
+        double tx[2], ty[2];
+        LapAcc acc[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const double2 t = txy[c.tbegin + min(lane + 32 * u, nT - 1)];
+            tx[u] = t.x;
+            ty[u] = t.y;
+        }
+        const NearList nl = near_list(uint32_t(c.leaf), nb, soff, lane);
+        for (int base = warp * kP2PBatch; base < nl.total; base += kP2PWarps * kP2PBatch)
+            near_batch(nl, base, min(kP2PBatch, nl.total - base), 0, 1, true, lane, sxy, q, mxy, mq,
+                       tab_lane, tx, ty, acc);
+        red[warp * 64 + lane] = lap_total(acc[0]);
+        red[warp * 64 + lane + 32] = lap_total(acc[1]);
+        __syncthreads();
+        if (threadIdx.x < nT) {
+            double sum = 0.0;
+#pragma unroll
+            for (int w = 0; w < kP2PWarps; ++w) sum += red[w * 64 + threadIdx.x];
+            const int e = c.tbegin + threadIdx.x;
+            out[tids[e]] = pot_far[e] - kInv4Pi * sum;
+        }
+        __syncthreads();
+    }
+
+    // ---- phase 2: light chunks, one warp each
+    for (;;) {
+        int k = 0;
+        if (lane == 0) k = atomicAdd(&ticket[1], 1);
+        const int64_t ch = nheavy + __shfl_sync(0xffffffffu, k, 0);
         if (ch >= nchunks) break;
         const P2PChunk c = chunks[ch];
-        const uint32_t b = uint32_t(c.leaf);
         const int nT = c.tcount;
         const int nTh = (nT + 1) >> 1;
         const int S = max(1, 32 / nTh);
         const int tl = lane % nTh;  // target slot: targets tl and tl + nTh
         const int grp = lane / nTh; // source group
         const bool active = grp < S;
-        double tx[2], ty[2], pot[2];
+        double tx[2], ty[2];
         LapAcc acc[2];
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-            const int li = min(tl + nTh * u, nT - 1);
-            const double2 t = txy[c.tbegin + li];
+            const double2 t = txy[c.tbegin + min(tl + nTh * u, nT - 1)];
             tx[u] = t.x;
             ty[u] = t.y;
-            pot[u] = grp == 0 ? pot_far[c.tbegin + li] : 0.0;
         }
-        // neighbour ranges: lane i < 9 owns (jy, jx) = (iy-1 + i/3, ix-1 + i%3)
-        const int ix = int(squash2(b)), iy = int(squash2(b >> 1));
-        int rs = 0, rl = 0;
-        if (lane < 9) {
-            const int jx = ix - 1 + lane % 3, jy = iy - 1 + lane / 3;
-            if (jx >= 0 && jx < nb && jy >= 0 && jy < nb) {
-                const uint32_t sid = mort(uint32_t(jx), uint32_t(jy));
-                rs = soff[sid];
-                rl = soff[sid + 1] - rs;
-            }
-        }
-        int incl = rl;
-#pragma unroll
-        for (int o = 1; o < 16; o <<= 1) {
-            const int v = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += v;
-        }
-        const int total = __shfl_sync(0xffffffffu, incl, 8);
-        int pre[9], st[9];
-#pragma unroll
-        for (int i = 0; i < 9; ++i) {
-            pre[i] = __shfl_sync(0xffffffffu, incl - rl, i);
-            st[i] = __shfl_sync(0xffffffffu, rs, i);
-        }
-        for (int base = 0; base < total; base += kP2PBatch) {
-            const int cnt = min(kP2PBatch, total - base);
-            __syncwarp();
-#pragma unroll
-            for (int h = 0; h < kP2PBatch / 32; ++h) {
-                const int f = h * 32 + lane;
-                if (f < cnt) {
-                    const int ff = base + f;
-                    int src = st[0] + ff;
-#pragma unroll
-                    for (int i = 1; i < 9; ++i)
-                        if (ff >= pre[i]) src = st[i] + (ff - pre[i]);
-                    mxy[f] = sxy[src];
-                    mq[f] = q[src];
-                }
-            }
-            __syncwarp();
-            if (active) {
-                // source f of the flat list goes to group f mod S
-                int j = grp - base % S;
-                if (j < 0) j += S;
-#pragma unroll 2
-                for (; j < cnt; j += S) {
-                    const double2 sp = mxy[j];
-                    const double qj = mq[j];
-                    lap_pair_fast(tx[0], ty[0], sp.x, sp.y, qj, tab_lane, acc[0]);
-                    lap_pair_fast(tx[1], ty[1], sp.x, sp.y, qj, tab_lane, acc[1]);
-                }
-            }
-        }
-        // coincident points share the leaf: rescan the centre range only
-        if (active) {
-            const int f0 = pre[4], f1 = pre[5];
-            int ff = f0 + (grp - f0 % S);
-            if (ff < f0) ff += S;
-            for (; ff < f1; ff += S) {
-                const int src = st[4] + (ff - f0);
-                const double2 sp = sxy[src];
-                const double qj = q[src];
-                lap_pair_fixup(tx[0], ty[0], sp.x, sp.y, qj, tab_lane, acc[0]);
-                lap_pair_fixup(tx[1], ty[1], sp.x, sp.y, qj, tab_lane, acc[1]);
-            }
-        }
+        const NearList nl = near_list(uint32_t(c.leaf), nb, soff, lane);
+        for (int base = 0; base < nl.total; base += kP2PBatch)
+            near_batch(nl, base, min(kP2PBatch, nl.total - base), grp, S, active, lane, sxy, q, mxy,
+                       mq, tab_lane, tx, ty, acc);
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-            double v = active ? pot[u] - kInv4Pi * lap_total(acc[u]) : 0.0;
+            double v = active ? lap_total(acc[u]) : 0.0;
             // add the other groups' partials in group order
             for (int g2 = 1; g2 < S; ++g2) {
                 const double w = __shfl_sync(0xffffffffu, v, min(31, tl + g2 * nTh));
                 if (grp == 0) v += w;
             }
             const int li = tl + nTh * u;
-            if (grp == 0 && li < nT) out[tids[c.tbegin + li]] = v;
+            if (grp == 0 && li < nT) out[tids[c.tbegin + li]] = pot_far[c.tbegin + li] - kInv4Pi * v;
         }
     }
 }
@@ -898,16 +953,18 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
         ++launches;
     }
     if (pl.n_p2p_chunks > 0) {
-        const size_t smem = size_t(kLogTableBytes) + (sizeof(double2) + sizeof(double)) * kP2PBatch * kP2PWarps;
+        const size_t smem = size_t(kLogTableBytes) +
+                            (sizeof(double2) + sizeof(double)) * kP2PBatch * kP2PWarps +
+                            sizeof(double) * 64 * kP2PWarps;
         int per_sm = 1;
         VPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, l2p_p2p_kernel, kP2PWarps * 32, smem));
         const int64_t want = (pl.n_p2p_chunks + kP2PWarps - 1) / kP2PWarps;
         const unsigned grid = unsigned(std::min<int64_t>(want, int64_t(pl.sm_count) * std::max(per_sm, 1)));
         launch_pdl(l2p_p2p_kernel, dim3(grid), dim3(kP2PWarps * 32), smem, st,
-                   (const P2PChunk*)pl.p2p_chunks.p, pl.n_p2p_chunks, (const int32_t*)pl.src_off.p,
-                   (const double2*)pl.src_sorted.p, (const double*)qs, (const double2*)pl.tgt_sorted.p,
-                   (const int32_t*)pl.tgt_ids.p, (const double*)pot_far, L, log_table_dev(), ticket,
-                   out_dev);
+                   (const P2PChunk*)pl.p2p_chunks.p, pl.n_p2p_chunks, pl.n_p2p_heavy,
+                   (const int32_t*)pl.src_off.p, (const double2*)pl.src_sorted.p, (const double*)qs,
+                   (const double2*)pl.tgt_sorted.p, (const int32_t*)pl.tgt_ids.p, (const double*)pot_far, L,
+                   log_table_dev(), ticket, out_dev);
         ++launches;
     }
     mark(6);

@@ -41,6 +41,7 @@ struct M2LBatch {
     int32_t efirst;  // first list entry
     int32_t ecount;
 };
+constexpr int kP2PCoopSources = 768;  // neighbourhood size for CTA-cooperative chunks
 constexpr int kM2LPairs = 54;  // two interior target boxes (27 each); 2 * pairs columns
 
 // P2P work unit: up to chunk targets of one leaf (Morton-sorted order).
@@ -95,6 +96,7 @@ struct Plan {
     int p2p_tpt = 1;
     DBuf<P2PChunk> p2p_chunks;
     int64_t n_p2p_chunks = 0;
+    int64_t n_p2p_heavy = 0;  // leading chunks handled by a whole CTA
     int64_t p2p_pairs = 0;
     int64_t m2m_children = 0, l2l_children = 0;
 

@@ -465,15 +465,22 @@ void build_schedules(Plan& pl, int64_t lb, int64_t le) {
             for (int32_t t = t0; t < t1; t += chunk)
                 chunks.push_back(P2PChunk{int32_t(b), t, std::min(chunk, t1 - t), int32_t(std::min<int64_t>(nsrc, INT32_MAX))});
         }
-        // Costliest chunks first (pairs ~ ceil(targets/2) * sources per lane
-        // group): the persistent grid deals them round-robin, so the long
-        // ones start early and the tail is short.  Stable, so equal-cost
-        // chunks keep Morton order.
-        std::stable_sort(chunks.begin(), chunks.end(), [](const P2PChunk& a, const P2PChunk& b) {
-            const int64_t ca = int64_t(a.pad) * ((a.tcount + 1) / 2) / std::max(1, 32 / ((a.tcount + 1) / 2));
-            const int64_t cb = int64_t(b.pad) * ((b.tcount + 1) / 2) / std::max(1, 32 / ((b.tcount + 1) / 2));
-            return ca > cb;
-        });
+        // Heavy chunks (large neighbourhoods, > 32 targets) first -- a whole
+        // CTA processes each (l2p_p2p_kernel phase 1) -- then the light ones
+        // for single warps; costliest first within each part, so the
+        // dynamic ticket schedule starts the long work early.  Stable:
+        // equal-cost chunks keep Morton order.
+        auto heavy = [](const P2PChunk& c) { return c.pad >= kP2PCoopSources && c.tcount > 32; };
+        auto cost = [](const P2PChunk& c) {
+            const int nth = (c.tcount + 1) / 2;
+            return int64_t(c.pad) * nth / std::max(1, 32 / nth);
+        };
+        auto mid = std::stable_partition(chunks.begin(), chunks.end(), heavy);
+        std::stable_sort(chunks.begin(), mid,
+                         [&](const P2PChunk& x, const P2PChunk& y) { return cost(x) > cost(y); });
+        std::stable_sort(mid, chunks.end(),
+                         [&](const P2PChunk& x, const P2PChunk& y) { return cost(x) > cost(y); });
+        pl.n_p2p_heavy = int64_t(mid - chunks.begin());
         pl.n_p2p_chunks = int64_t(chunks.size());
         to_device(pl.p2p_chunks, chunks, st);
     }
