@@ -527,6 +527,10 @@ l2p_kernel(const int32_t* tleaf, int64_t t0, int64_t t1, const double2* txy,
 constexpr int kP2PWarps = 8;
 constexpr int kP2PBatch = 64;
 constexpr int kP2PChunk = 64;
+#ifndef VPG_P2P_MIN_BLOCKS
+#define VPG_P2P_MIN_BLOCKS 2
+#endif
+constexpr int kP2PMinBlocks = VPG_P2P_MIN_BLOCKS;
 
 struct NearList {
     int total;
@@ -606,7 +610,7 @@ __device__ __forceinline__ void near_batch(const NearList& nl, int base, int cnt
     }
 }
 
-__global__ void __launch_bounds__(kP2PWarps * 32)
+__global__ void __launch_bounds__(kP2PWarps * 32, kP2PMinBlocks)
 l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, int64_t nheavy, const int32_t* soff,
                const double2* sxy, const double* q, const double2* txy,
                const int32_t* tids, const double* pot_far, int L,
@@ -651,8 +655,11 @@ l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, int64_t nheavy, const in
             ty[u] = t.y;
         }
         const NearList nl = near_list(uint32_t(c.leaf), nb, soff, lane);
-        for (int base = warp * kP2PBatch; base < nl.total; base += kP2PWarps * kP2PBatch)
-            near_batch(nl, base, min(kP2PBatch, nl.total - base), 0, 1, true, lane, sxy, q, mxy, mq,
+        // warp w takes the w-th eighth of the flat source list
+        const int f0 = int(int64_t(nl.total) * warp / kP2PWarps);
+        const int f1 = int(int64_t(nl.total) * (warp + 1) / kP2PWarps);
+        for (int base = f0; base < f1; base += kP2PBatch)
+            near_batch(nl, base, min(kP2PBatch, f1 - base), 0, 1, true, lane, sxy, q, mxy, mq,
                        tab_lane, tx, ty, acc);
         red[warp * 64 + lane] = lap_total(acc[0]);
         red[warp * 64 + lane + 32] = lap_total(acc[1]);

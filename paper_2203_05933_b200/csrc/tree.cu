@@ -470,7 +470,13 @@ void build_schedules(Plan& pl, int64_t lb, int64_t le) {
         // for single warps; costliest first within each part, so the
         // dynamic ticket schedule starts the long work early.  Stable:
         // equal-cost chunks keep Morton order.
-        auto heavy = [](const P2PChunk& c) { return c.pad >= kP2PCoopSources && c.tcount > 32; };
+        // "heavy" = a chunk worth more than half a warp's fair share of the
+        // near field (~24 resident warps per SM); uniform grids (cfg4) have
+        // none and run barrier-free, the dense strip of cfg2 has many.
+        const double fair = double(pl.p2p_pairs) / (double(pl.sm_count) * 24.0);
+        auto heavy = [&](const P2PChunk& c) {
+            return c.pad >= kP2PCoopSources && c.tcount > 32 && double(c.pad) * c.tcount >= 0.5 * fair;
+        };
         auto cost = [](const P2PChunk& c) {
             const int nth = (c.tcount + 1) / 2;
             return int64_t(c.pad) * nth / std::max(1, 32 / nth);
