@@ -120,14 +120,21 @@ __device__ __forceinline__ uint32_t log_table_lane_addr(const double2* tab, int 
 }
 
 // Returns t with ln(x) = ed*ln2 + t; ed = exponent as a double.
+// Integer side: v = (hi + 2^11) >> 12 = 256 e_b + idx (the carry of the
+// rounding add lands in the exponent field), so the table byte offset is
+// 128 v - 32768 e_b; the exponent is converted by I2F.F64 (conversion pipe,
+// not the FP64 pipe); the mantissa word is one 3-input LOP3.
 __device__ __forceinline__ double fast_log_split(double x, uint32_t tab_lane, double& ed) {
     const int hi = __double2hiint(x);
     const int lo = __double2loint(x);
-    const uint32_t idx = (uint32_t(hi & 0x000FFFFF) + (1u << (19 - kLogTableBits))) >> (20 - kLogTableBits);
-    const double m = __hiloint2double((hi & 0x000FFFFF) | 0x3FF00000, lo);
-    // exponent field e_b in [0, 2047]: ed = (2^52 + e_b) - (2^52 + 1023)
-    ed = __hiloint2double(0x43300000, hi >> 20) - c_magic_bias;
-    const double2 tc = lds_f64x2(tab_lane + idx * uint32_t(16 * kLogTableCopies));
+    const int eb = hi >> 20;  // biased exponent (x >= 0)
+    const uint32_t v = uint32_t(hi + (1 << (19 - kLogTableBits))) >> (20 - kLogTableBits);
+    const uint32_t off = v * uint32_t(16 * kLogTableCopies) - uint32_t(eb) * uint32_t(16 * kLogTableCopies * 256);
+    int mhi;
+    asm("lop3.b32 %0, %1, 0x000FFFFF, %2, 0xEA;" : "=r"(mhi) : "r"(hi), "r"(0x3FF00000));
+    const double m = __hiloint2double(mhi, lo);
+    ed = __int2double_rn(eb - 1023);
+    const double2 tc = lds_f64x2(tab_lane + off);
     const double r = fma(m, tc.x, -1.0);
     double p = fma(r, c_log1p5[0], c_log1p5[1]);
     p = fma(r, p, c_log1p5[2]);
