@@ -221,6 +221,23 @@ __device__ __forceinline__ void bulk_stage(void* dst, const void* src, uint32_t 
     mbar_wait(bar, phase);
 }
 
+// Cooperative launch (all CTAs co-resident: grid-wide barriers allowed).
+template <typename... KArgs, typename... Args>
+void launch_coop(void (*kern)(KArgs...), int grid, dim3 block, size_t smem, cudaStream_t st,
+                 Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(grid));
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    VPG_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+}
+
 // Per-device constant tables, built on first use (api.cu).
 const double2* log_table_dev();  // kLogTableSize entries (inv_c, -ln inv_c)
 const double* k0_table_dev();    // K0 Chebyshev fits, see k0.cuh

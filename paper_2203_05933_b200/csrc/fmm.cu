@@ -114,24 +114,54 @@ p2m_kernel(const int32_t* leaves, int64_t nleaves, const int32_t* soff, const do
 }
 
 // ------------------------------------------------------------ M2M / L2L --
-// All four child operators (transposed, 4 x (P+1)^2 complex = 166 KB at
-// P=50) are staged in smem once per CTA -- before pdl_wait(), so the copy
-// overlaps the previous pass -- and every thread owns one output row of one
-// box: thread (g, r) of a CTA handles parent g, coefficient r.
+// One cooperative launch per pass (all levels): the four child operators
+// (transposed, 4 x (P+1)^2 complex = 166 KB at P=50) are bulk-copied into
+// smem once per CTA; then for each level (bottom-up for M2M, top-down for
+// L2L) the grid splits that level's parents, four threads per output row
+// (each sums a quarter of k for all four children, a fixed xor-shuffle
+// combines the quarters), and a grid-wide barrier separates the levels.
+// The per-level separate launches this replaces were latency-bound at
+// ~20 us each.
 //   Upward (M2M, summation.cpp:257-267): parent[r] = sum_c (m2m[c] child_c)[r]
 //     over children with src_cnt > 0, reduced in c order.
 //   Downward (L2L, summation.cpp:305-312): child_c[r] += (l2l[c] parent)[r]
 //     for children with tgt_cnt > 0.
-// Each output element has exactly one writer: no atomics, fixed order.
-constexpr int kRowSlots = 64;  // threads per box (>= P+1)
-constexpr int kUpGroup = 8;    // parents per CTA, M2M
-constexpr int kDownGroup = 16; // parents per CTA, L2L
+// Each output element has exactly one writer: no atomics on values, fixed
+// order.  Cross-level reads use ld.global.cg (L2), never a stale L1 line.
+constexpr int kRowSlots = 64;  // rows per box (>= P+1)
+constexpr int kKSplit = 4;     // threads per row
+constexpr int kShiftGroup = 4; // boxes per CTA round (4 x 64 x 4 = 1024 threads)
+constexpr int kMaxShiftLevels = 16;
 
-template <bool kUp, int G>
-__global__ void __launch_bounds__(G * kRowSlots)
-shift_kernel(const int32_t* parents, int64_t nparents, const double2* ops_t,
-             const int32_t* cnt_child, const double2* in_level,
-             double2* out_level, int P) {
+struct ShiftLevels {
+    int nlev;                          // levels processed, in order
+    const int32_t* parents[kMaxShiftLevels];
+    int64_t nparents[kMaxShiftLevels];
+    const int32_t* cnt_child[kMaxShiftLevels];
+    const double2* in_level[kMaxShiftLevels];
+    double2* out_level[kMaxShiftLevels];
+};
+
+// Grid-wide barrier for a cooperative launch (all CTAs co-resident):
+// monotonic arrival counter, zeroed by the previous kernel of the apply.
+__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned& target) {
+    __syncthreads();
+    target += gridDim.x;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(count, 1u);
+        unsigned v;
+        do {
+            asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(count) : "memory");
+            if (v < target) __nanosleep(64);
+        } while (v < target);
+    }
+    __syncthreads();
+}
+
+template <bool kUp>
+__global__ void __launch_bounds__(kShiftGroup * kRowSlots * kKSplit)
+shift_kernel(ShiftLevels lv, const double2* ops_t, int P, unsigned* gbar) {
     extern __shared__ __align__(16) double2 sm[];
     __shared__ __align__(8) uint64_t bar;
     const int n = P + 1;
@@ -143,57 +173,84 @@ shift_kernel(const int32_t* parents, int64_t nparents, const double2* ops_t,
     bulk_stage(op, ops_t, uint32_t(4 * nn) * 16u, &bar, 0);
     pdl_trigger();
     pdl_wait();
-    const int64_t g0 = int64_t(blockIdx.x) * G;
-    const int ng = int(min(int64_t(G), nparents - g0));
-    if (kUp) {
-        for (int i = threadIdx.x; i < ng * 4 * n; i += blockDim.x) {
-            const int g = i / (4 * n), rem = i % (4 * n), c = rem / n, kk = rem % n;
-            const int64_t child = (int64_t(parents[g0 + g]) << 2) | c;
-            vec[i] = cnt_child[child] > 0 ? in_level[child * n + kk] : make_double2(0.0, 0.0);
-        }
-    } else {
-        for (int i = threadIdx.x; i < ng * n; i += blockDim.x) {
-            const int g = i / n, kk = i % n;
-            vec[i] = in_level[int64_t(parents[g0 + g]) * n + kk];
-        }
-    }
-    __syncthreads();
-    const int g = threadIdx.x / kRowSlots, r = threadIdx.x % kRowSlots;
-    if (g >= ng || r > P) return;
-    const int64_t parent = parents[g0 + g];
-    // all four children at once: eight independent FMA chains per thread
-    double yr[4] = {0.0, 0.0, 0.0, 0.0}, yi[4] = {0.0, 0.0, 0.0, 0.0};
-    const double2* x0v = kUp ? vec + (g * 4) * n : vec + g * n;
+    const int ks = threadIdx.x & (kKSplit - 1);
+    const int r = (threadIdx.x / kKSplit) % kRowSlots;
+    const int g = threadIdx.x / (kKSplit * kRowSlots);
+    const int kspan = (n + kKSplit - 1) / kKSplit;
+    const int k0 = ks * kspan, k1 = min(n, k0 + kspan);
+    unsigned target = 0;
+    for (int li = 0; li < lv.nlev; ++li) {
+        const int32_t* parents = lv.parents[li];
+        const int64_t np = lv.nparents[li];
+        const int32_t* cnt_child = lv.cnt_child[li];
+        const double2* in_level = lv.in_level[li];
+        double2* out_level = lv.out_level[li];
+        for (int64_t g0 = int64_t(blockIdx.x) * kShiftGroup; g0 < np; g0 += int64_t(gridDim.x) * kShiftGroup) {
+            const int ng = int(min(int64_t(kShiftGroup), np - g0));
+            __syncthreads();  // vec reuse
+            if (kUp) {
+                for (int i = threadIdx.x; i < ng * 4 * n; i += blockDim.x) {
+                    const int gg = i / (4 * n), rem = i % (4 * n), c = rem / n, kk = rem % n;
+                    const int64_t child = (int64_t(parents[g0 + gg]) << 2) | c;
+                    vec[i] = cnt_child[child] > 0 ? __ldcg(in_level + child * n + kk) : make_double2(0.0, 0.0);
+                }
+            } else {
+                for (int i = threadIdx.x; i < ng * n; i += blockDim.x) {
+                    const int gg = i / n, kk = i % n;
+                    vec[i] = __ldcg(in_level + int64_t(parents[g0 + gg]) * n + kk);
+                }
+            }
+            __syncthreads();
+            const bool live = g < ng && r <= P;
+            double yr[4] = {0.0, 0.0, 0.0, 0.0}, yi[4] = {0.0, 0.0, 0.0, 0.0};
+            if (live) {
+                const double2* x0v = kUp ? vec + (g * 4) * n : vec + g * n;
 #pragma unroll 2
-    for (int kk = 0; kk <= P; ++kk) {
+                for (int kk = k0; kk < k1; ++kk) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            const double2 m = op[c * nn + kk * n + r];
-            const double2 v = kUp ? x0v[c * n + kk] : x0v[kk];
-            yr[c] = fma(m.x, v.x, fma(-m.y, v.y, yr[c]));
-            yi[c] = fma(m.x, v.y, fma(m.y, v.x, yi[c]));
-        }
-    }
-    if (kUp) {
-        // children with src_cnt == 0 were staged as zeros; sum in c order
-        double ar = 0.0, ai = 0.0;
+                    for (int c = 0; c < 4; ++c) {
+                        const double2 m = op[c * nn + kk * n + r];
+                        const double2 v = kUp ? x0v[c * n + kk] : x0v[kk];
+                        yr[c] = fma(m.x, v.x, fma(-m.y, v.y, yr[c]));
+                        yi[c] = fma(m.x, v.y, fma(m.y, v.x, yi[c]));
+                    }
+                }
+            }
+            // combine the k quarters: fixed butterfly, identical on all four lanes
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            ar += yr[c];
-            ai += yi[c];
-        }
-        out_level[parent * n + r] = make_double2(ar, ai);
-    } else {
+            for (int c = 0; c < 4; ++c) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            const int64_t child = (parent << 2) | c;
-            if (cnt_child[child] == 0) continue;
-            double2* dst = out_level + child * n + r;
-            double2 d = *dst;
-            d.x += yr[c];
-            d.y += yi[c];
-            *dst = d;
+                for (int o = 1; o < kKSplit; o <<= 1) {
+                    yr[c] += __shfl_xor_sync(0xffffffffu, yr[c], o);
+                    yi[c] += __shfl_xor_sync(0xffffffffu, yi[c], o);
+                }
+            }
+            if (live && ks == 0) {
+                const int64_t parent = parents[g0 + g];
+                if (kUp) {
+                    // children with src_cnt == 0 were staged as zeros; sum in c order
+                    double ar = 0.0, ai = 0.0;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        ar += yr[c];
+                        ai += yi[c];
+                    }
+                    out_level[parent * n + r] = make_double2(ar, ai);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const int64_t child = (parent << 2) | c;
+                        if (cnt_child[child] == 0) continue;
+                        double2* dst = out_level + child * n + r;
+                        double2 d = __ldcg(dst);
+                        d.x += yr[c];
+                        d.y += yi[c];
+                        *dst = d;
+                    }
+                }
+            }
         }
+        if (li + 1 < lv.nlev) grid_barrier(gbar, target);
     }
 }
 
@@ -713,8 +770,9 @@ l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, int64_t nheavy, const in
     }
 }
 
-__global__ void gather_q(const double* q, const int32_t* ids, int64_t n, double* qs) {
+__global__ void gather_q(const double* q, const int32_t* ids, int64_t n, double* qs, unsigned* gbar) {
     const int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (e < 2) gbar[e] = 0u;
     if (e < n) qs[e] = q[ids[e]];
 }
 
@@ -861,8 +919,16 @@ void build_laplace_ops(Plan& pl) {
 
     smem_optin((const void*)m2l_kernel, 225 * 1024);
     smem_optin((const void*)p2m_kernel, 100 * 1024);
-    smem_optin((const void*)shift_kernel<true, kUpGroup>, 220 * 1024);
-    smem_optin((const void*)shift_kernel<false, kDownGroup>, 220 * 1024);
+    smem_optin((const void*)shift_kernel<true>, 220 * 1024);
+    smem_optin((const void*)shift_kernel<false>, 220 * 1024);
+    {
+        // co-resident CTAs for the cooperative shift passes
+        const size_t up_smem = sizeof(double2) * size_t(4 * n * n + kShiftGroup * 4 * n);
+        int per_sm = 0;
+        VPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, shift_kernel<true>, kShiftGroup * kRowSlots * kKSplit, up_smem));
+        pl.shift_grid = std::max(1, per_sm) * pl.sm_count;
+    }
     smem_optin((const void*)l2p_p2p_kernel, 64 * 1024);
 }
 
@@ -893,9 +959,10 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
         }
     } fr{{qs, mult, loc, pot_far, ticket}, st};
     const int64_t* exp_off_d = pl.exp_off_dev.p;
+    unsigned* gbar = reinterpret_cast<unsigned*>(ticket) + 8;  // grid barriers of the shift passes
 
     mark(0);
-    gather_q<<<nblk(pl.ns, 256), 256, 0, st>>>(q_dev, pl.src_ids.p, pl.ns, qs);
+    gather_q<<<nblk(pl.ns, 256), 256, 0, st>>>(q_dev, pl.src_ids.p, pl.ns, qs, gbar);
     VPG_LAUNCH_CHECK();
     ++launches;
     mark(1);
@@ -909,18 +976,27 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
         ++launches;
     }
     mark(2);
-    const size_t up_smem = sizeof(double2) * size_t(4 * n * n + kUpGroup * 4 * n);
-    const size_t down_smem = sizeof(double2) * size_t(4 * n * n + kDownGroup * n);
+    const size_t up_smem = sizeof(double2) * size_t(4 * n * n + kShiftGroup * 4 * n);
+    const size_t down_smem = sizeof(double2) * size_t(4 * n * n + kShiftGroup * n);
     const double2* m2m_ops = reinterpret_cast<const double2*>(pl.m2m_ops.p);
     const double2* l2l_ops = reinterpret_cast<const double2*>(pl.l2l_ops.p);
-    for (int l = L - 1; l >= 2; --l) {
-        const int64_t np = pl.m2m_count[size_t(l)];
-        if (!np) continue;
-        launch_pdl(shift_kernel<true, kUpGroup>, dim3(nblk(np, kUpGroup)), dim3(kUpGroup * kRowSlots),
-                   up_smem, st, pl.updown_boxes.p + pl.m2m_first[size_t(l)], np, m2m_ops,
-                   pl.src_cnt.p + lvl_base(l + 1), (const double2*)(mult + pl.exp_off[size_t(l + 1)]),
-                   mult + pl.exp_off[size_t(l)], P);
-        ++launches;
+    {
+        ShiftLevels lv{};
+        for (int l = L - 1; l >= 2; --l) {
+            const int64_t np = pl.m2m_count[size_t(l)];
+            if (!np) continue;
+            lv.parents[lv.nlev] = pl.updown_boxes.p + pl.m2m_first[size_t(l)];
+            lv.nparents[lv.nlev] = np;
+            lv.cnt_child[lv.nlev] = pl.src_cnt.p + lvl_base(l + 1);
+            lv.in_level[lv.nlev] = mult + pl.exp_off[size_t(l + 1)];
+            lv.out_level[lv.nlev] = mult + pl.exp_off[size_t(l)];
+            ++lv.nlev;
+        }
+        if (lv.nlev) {
+            launch_coop(shift_kernel<true>, pl.shift_grid, dim3(kShiftGroup * kRowSlots * kKSplit), up_smem, st,
+                        lv, m2m_ops, P, gbar + 0);
+            ++launches;
+        }
     }
     mark(3);
     if (pl.n_m2l_batches > 0) {
@@ -942,15 +1018,23 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
         ++launches;
     }
     mark(4);
-    for (int l = 2; l < L; ++l) {
-        const int64_t np = pl.l2l_count[size_t(l)];
-        if (!np) continue;
-        launch_pdl(shift_kernel<false, kDownGroup>, dim3(nblk(np, kDownGroup)),
-                   dim3(kDownGroup * kRowSlots), down_smem, st,
-                   pl.updown_boxes.p + pl.l2l_first[size_t(l)], np, l2l_ops,
-                   pl.tgt_cnt.p + lvl_base(l + 1), (const double2*)(loc + pl.exp_off[size_t(l)]),
-                   loc + pl.exp_off[size_t(l + 1)], P);
-        ++launches;
+    {
+        ShiftLevels lv{};
+        for (int l = 2; l < L; ++l) {
+            const int64_t np = pl.l2l_count[size_t(l)];
+            if (!np) continue;
+            lv.parents[lv.nlev] = pl.updown_boxes.p + pl.l2l_first[size_t(l)];
+            lv.nparents[lv.nlev] = np;
+            lv.cnt_child[lv.nlev] = pl.tgt_cnt.p + lvl_base(l + 1);
+            lv.in_level[lv.nlev] = loc + pl.exp_off[size_t(l)];
+            lv.out_level[lv.nlev] = loc + pl.exp_off[size_t(l + 1)];
+            ++lv.nlev;
+        }
+        if (lv.nlev) {
+            launch_coop(shift_kernel<false>, pl.shift_grid, dim3(kShiftGroup * kRowSlots * kKSplit), down_smem,
+                        st, lv, l2l_ops, P, gbar + 1);
+            ++launches;
+        }
     }
     mark(5);
     if (pl.shard_t1 > pl.shard_t0) {

@@ -55,6 +55,7 @@ struct P2PChunk {
 struct Plan {
     int device = 0;
     int sm_count = 148;
+    int shift_grid = 148;  // co-resident CTAs of the cooperative M2M/L2L passes
     int family = VPG_LAPLACE;
     int mode = VPG_MODE_REFERENCE;
     double lambda = 0.0, eps = 1e-12;
