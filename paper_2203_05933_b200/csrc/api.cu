@@ -112,7 +112,7 @@ int64_t Plan::device_bytes() const {
                    src_cnt.bytes() + tgt_cnt.bytes() + m2l_tbox.bytes() + m2l_toff.bytes() +
                    m2l_src.bytes() + m2l_oidx.bytes() + m2l_batches.bytes() + m2m_ops.bytes() +
                    l2l_ops.bytes() + h_t.bytes() + dpow.bytes() + logmd.bytes() +
-                   p2p_chunks.bytes() + p2m_leaves.bytes() + updown_boxes.bytes() +
+                   p2p_chunks.bytes() + p2m_items.bytes() + p2m_splits.bytes() + updown_boxes.bytes() +
                    helm_nodes.bytes() + helm_bw.bytes() + exp_off_dev.bytes());
 }
 

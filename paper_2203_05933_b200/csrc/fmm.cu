@@ -30,31 +30,37 @@ __device__ inline void box_center(double x0, double y0, double s, uint32_t id,
 }
 
 // ------------------------------------------------------------------ P2M --
-// One warp per non-empty source leaf, two lanes per source: lane (j, h)
-// forms the running powers q w^k of source j (summation.cpp:247-254) for
-// the half k in (h*kh, (h+1)*kh], the upper half starting from w^kh by
-// binary powering, so the dependent multiply chain is half as long.  The
-// scaled powers -q w^k / k land in a per-warp [16][P+1] smem panel; lane k
-// then sums column k in source order.  16 sources per pass.
+// One warp per work item = (level, box, source range): two lanes per source,
+// lane (j, h) forms the running powers q w^k of source j
+// (summation.cpp:247-254) for the half k in (h*kh, (h+1)*kh], the upper half
+// starting from w^kh by binary powering, so the dependent multiply chain is
+// half as long.  The scaled powers -q w^k / k land in a per-warp [16][P+1]
+// smem panel; lane k then sums column k in source order.  Leaf items cover
+// the reference P2M; in the multilevel upward pass (small problems, see
+// laplace_apply) every level's boxes are items too and boxes split into
+// several items are summed in item order by p2m_reduce_kernel.
 constexpr int kP2MWarps = 4;
 constexpr int kP2MSrc = 16;
 
 __global__ void __launch_bounds__(kP2MWarps * 32)
-p2m_kernel(const int32_t* leaves, int64_t nleaves, const int32_t* soff, const double2* sxy,
-           const double* q, int P, double x0, double y0, double s, double2* mult_leaf) {
+p2m_kernel(const P2MItem* items, int64_t nitems, const int32_t* sorted_unused,
+           const double2* sxy, const double* q, int P, double x0, double y0, double side,
+           double2* mult, const int64_t* exp_off, double2* partial) {
     extern __shared__ double2 panels[];
     pdl_trigger();
     pdl_wait();
+    (void)sorted_unused;
     const int n = P + 1;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t li = int64_t(blockIdx.x) * kP2MWarps + warp;
-    if (li >= nleaves) return;
+    if (li >= nitems) return;
     double2* panel = panels + warp * kP2MSrc * n;
-    const uint32_t b = uint32_t(leaves[li]);
+    const P2MItem it = items[li];
+    const double s = side / double(1 << it.level);
     double cx, cy;
-    box_center(x0, y0, s, b, cx, cy);
+    box_center(x0, y0, s, uint32_t(it.box), cx, cy);
     const double inv_s = 1.0 / s;
-    const int e0 = soff[b], e1 = soff[b + 1];
+    const int e0 = it.e0, e1 = it.e1;
     const int j = lane & (kP2MSrc - 1), h = lane >> 4;
     const int kh = (P + 1) >> 1;
     double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
@@ -109,8 +115,29 @@ p2m_kernel(const int32_t* leaves, int64_t nleaves, const int32_t* soff, const do
         }
         __syncwarp();
     }
-    if (lane <= P) mult_leaf[int64_t(b) * n + lane] = acc0;
-    if (lane + 32 <= P) mult_leaf[int64_t(b) * n + lane + 32] = acc1;
+    double2* dst = it.direct ? mult + exp_off[it.level] + int64_t(it.box) * n : partial + li * n;
+    if (lane <= P) dst[lane] = acc0;
+    if (lane + 32 <= P) dst[lane + 32] = acc1;
+}
+
+// Boxes split over several P2M items: sum the item partials in item order.
+__global__ void p2m_reduce_kernel(const P2MSplit* splits, int64_t nsplit, const double2* partial,
+                                  int P, double2* mult, const int64_t* exp_off) {
+    pdl_trigger();
+    pdl_wait();
+    const int n = P + 1;
+    const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (i >= nsplit * n) return;
+    const int64_t sp = i / n;
+    const int k = int(i - sp * n);
+    const P2MSplit b = splits[sp];
+    double2 acc = make_double2(0.0, 0.0);
+    for (int t = 0; t < b.count; ++t) {
+        const double2 v = partial[int64_t(b.first + t) * n + k];
+        acc.x += v.x;
+        acc.y += v.y;
+    }
+    mult[exp_off[b.level] + int64_t(b.box) * n + k] = acc;
 }
 
 // ------------------------------------------------------------ M2M / L2L --
@@ -531,8 +558,8 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
 // near-field kernel adds its sum on top (fixed order: far, then near).
 __global__ void __launch_bounds__(256)
 l2p_kernel(const int32_t* tleaf, int64_t t0, int64_t t1, const double2* txy,
-           const double2* loc_leaf, int P, double x0, double y0, double s, double* pot_far,
-           int* ticket) {
+           const double2* loc, const int64_t* exp_off, int lmin, int L, int P, double x0,
+           double y0, double side, double* pot_far, int* ticket) {
     pdl_trigger();
     pdl_wait();
     const int64_t e = t0 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
@@ -541,22 +568,31 @@ l2p_kernel(const int32_t* tleaf, int64_t t0, int64_t t1, const double2* txy,
         ticket[1] = 0;
     }
     if (e >= t1) return;
-    const uint32_t b = uint32_t(tleaf[e]);
-    double cx, cy;
-    box_center(x0, y0, s, b, cx, cy);
-    const double inv_s = 1.0 / s;
+    const uint32_t bL = uint32_t(tleaf[e]);
     const double2 t = txy[e];
-    const double ur = (t.x - cx) * inv_s, ui = (t.y - cy) * inv_s;
-    const double2* ab = loc_leaf + int64_t(b) * (P + 1);
-    double vr = ab[P].x, vi = ab[P].y;
-    for (int l = P - 1; l >= 0; --l) {
-        const double2 a = ab[l];
-        const double nr = fma(vr, ur, fma(-vi, ui, a.x));
-        const double ni = fma(vr, ui, fma(vi, ur, a.y));
-        vr = nr;
-        vi = ni;
+    // levels lmin..L: lmin == L is the reference L2P after the L2L chain;
+    // lmin == 2 evaluates every ancestor's local expansion (multilevel
+    // downward pass, no L2L), summed coarse to fine.
+    double sum = 0.0;
+    for (int l = lmin; l <= L; ++l) {
+        const uint32_t b = bL >> (2 * (L - l));
+        const double s = side / double(1 << l);
+        double cx, cy;
+        box_center(x0, y0, s, b, cx, cy);
+        const double inv_s = 1.0 / s;
+        const double ur = (t.x - cx) * inv_s, ui = (t.y - cy) * inv_s;
+        const double2* ab = loc + exp_off[l] + int64_t(b) * (P + 1);
+        double vr = ab[P].x, vi = ab[P].y;
+        for (int k = P - 1; k >= 0; --k) {
+            const double2 a = ab[k];
+            const double nr = fma(vr, ur, fma(-vi, ui, a.x));
+            const double ni = fma(vr, ui, fma(vi, ur, a.y));
+            vr = nr;
+            vi = ni;
+        }
+        sum += vr;
     }
-    pot_far[e] = -kInv2Pi * vr;
+    pot_far[e] = -kInv2Pi * sum;
 }
 
 // ------------------------------------------------------- near-field P2P --
@@ -967,20 +1003,29 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
     ++launches;
     mark(1);
 
-    const double sL = pl.side / double(1 << L);
-    if (pl.n_p2m_leaves > 0) {
-        launch_pdl(p2m_kernel, dim3(nblk(pl.n_p2m_leaves, kP2MWarps)), dim3(kP2MWarps * 32),
-                   size_t(kP2MWarps) * kP2MSrc * n * sizeof(double2), st, (const int32_t*)pl.p2m_leaves.p,
-                   pl.n_p2m_leaves, (const int32_t*)pl.src_off.p, (const double2*)pl.src_sorted.p, (const double*)qs, P,
-                   pl.x0, pl.y0, sL, mult + pl.exp_off[size_t(L)]);
+    double2* partial = nullptr;
+    if (pl.n_p2m_splits > 0)
+        VPG_CUDA(cudaMallocAsync(&partial, sizeof(double2) * size_t(pl.n_p2m_items) * n, st));
+    if (pl.n_p2m_items > 0) {
+        launch_pdl(p2m_kernel, dim3(nblk(pl.n_p2m_items, kP2MWarps)), dim3(kP2MWarps * 32),
+                   size_t(kP2MWarps) * kP2MSrc * n * sizeof(double2), st, (const P2MItem*)pl.p2m_items.p,
+                   pl.n_p2m_items, (const int32_t*)nullptr, (const double2*)pl.src_sorted.p, (const double*)qs,
+                   P, pl.x0, pl.y0, pl.side, mult, exp_off_d, partial);
         ++launches;
+    }
+    if (pl.n_p2m_splits > 0) {
+        launch_pdl(p2m_reduce_kernel, dim3(nblk(pl.n_p2m_splits * n, 256)), dim3(256), 0, st,
+                   (const P2MSplit*)pl.p2m_splits.p, pl.n_p2m_splits, (const double2*)partial, P, mult,
+                   exp_off_d);
+        ++launches;
+        VPG_CUDA(cudaFreeAsync(partial, st));
     }
     mark(2);
     const size_t up_smem = sizeof(double2) * size_t(4 * n * n + kShiftGroup * 4 * n);
     const size_t down_smem = sizeof(double2) * size_t(4 * n * n + kShiftGroup * n);
     const double2* m2m_ops = reinterpret_cast<const double2*>(pl.m2m_ops.p);
     const double2* l2l_ops = reinterpret_cast<const double2*>(pl.l2l_ops.p);
-    {
+    if (!pl.multilevel_up) {
         ShiftLevels lv{};
         for (int l = L - 1; l >= 2; --l) {
             const int64_t np = pl.m2m_count[size_t(l)];
@@ -1018,7 +1063,7 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
         ++launches;
     }
     mark(4);
-    {
+    if (!pl.multilevel_down) {
         ShiftLevels lv{};
         for (int l = 2; l < L; ++l) {
             const int64_t np = pl.l2l_count[size_t(l)];
@@ -1039,8 +1084,9 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
     mark(5);
     if (pl.shard_t1 > pl.shard_t0) {
         launch_pdl(l2p_kernel, dim3(nblk(pl.shard_t1 - pl.shard_t0, 256)), dim3(256), 0, st,
-                   (const int32_t*)pl.tgt_leaf.p, pl.shard_t0, pl.shard_t1, (const double2*)pl.tgt_sorted.p, (const double2*)(loc + pl.exp_off[size_t(L)]),
-                   P, pl.x0, pl.y0, sL, pot_far, ticket);
+                   (const int32_t*)pl.tgt_leaf.p, pl.shard_t0, pl.shard_t1, (const double2*)pl.tgt_sorted.p,
+                   (const double2*)loc, exp_off_d, pl.multilevel_down ? 2 : L, L, P, pl.x0, pl.y0, pl.side,
+                   pot_far, ticket);
         ++launches;
     }
     if (pl.n_p2p_chunks > 0) {

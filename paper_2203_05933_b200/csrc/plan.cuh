@@ -44,6 +44,23 @@ struct M2LBatch {
 constexpr int kP2PCoopSources = 768;  // neighbourhood size for CTA-cooperative chunks
 constexpr int kM2LPairs = 54;  // two interior target boxes (27 each); 2 * pairs columns
 
+// P2M work unit: the sources [e0, e1) (Morton-sorted) of one box at one
+// level; direct = the box is a single item (write the expansion in place).
+struct P2MItem {
+    int32_t level;
+    int32_t box;
+    int32_t e0, e1;
+    int32_t direct;
+};
+// A box whose sources span several items: partials summed in item order.
+struct P2MSplit {
+    int32_t level;
+    int32_t box;
+    int32_t first;
+    int32_t count;
+};
+constexpr int kP2MItemCap = 256;  // sources per P2M item
+
 // P2P work unit: up to chunk targets of one leaf (Morton-sorted order).
 struct P2PChunk {
     int32_t leaf;
@@ -103,8 +120,14 @@ struct Plan {
 
     // Leaf ids with src_cnt > 0 (P2M work list) and parents per level for
     // M2M (src_cnt > 0) / L2L (tgt_cnt > 0).
-    DBuf<int32_t> p2m_leaves;
-    int64_t n_p2m_leaves = 0;
+    DBuf<P2MItem> p2m_items;
+    int64_t n_p2m_items = 0;
+    DBuf<P2MSplit> p2m_splits;
+    int64_t n_p2m_splits = 0;
+    // Multilevel passes (small problems): P2M at every level instead of the
+    // M2M chain, L2P of every ancestor instead of the L2L chain -- one
+    // launch each instead of one per level (tree.cu, choose_passes).
+    bool multilevel_up = false, multilevel_down = false;
     std::vector<int64_t> m2m_first, m2m_count;  // into updown_boxes, per level
     std::vector<int64_t> l2l_first, l2l_count;
     DBuf<int32_t> updown_boxes;
@@ -137,6 +160,7 @@ struct Plan {
 // tree.cu
 void build_tree(Plan& pl);
 void build_schedules(Plan& pl, int64_t leaf_begin, int64_t leaf_end);
+void choose_passes(Plan& pl);
 // fmm.cu
 void build_laplace_ops(Plan& pl);
 void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "plan.cuh"
 
@@ -347,14 +348,47 @@ void build_tree(Plan& pl) {
             for (int32_t e = pl.h_toff[size_t(b)]; e < pl.h_toff[size_t(b) + 1]; ++e) tl[size_t(e)] = int32_t(b);
         to_device(pl.tgt_leaf, tl, st);
     }
+    choose_passes(pl);
     {
-        std::vector<int32_t> leaves;
-        for (int64_t b = 0; b < nleaf; ++b)
-            if (pl.h_scnt[size_t(lvl_base(L) + b)] > 0) leaves.push_back(int32_t(b));
-        pl.n_p2m_leaves = int64_t(leaves.size());
-        to_device(pl.p2m_leaves, leaves, st);
+        // P2M items: leaves only for the M2M chain, every level otherwise
+        std::vector<P2MItem> items;
+        std::vector<P2MSplit> splits;
+        for (int l = pl.multilevel_up ? 2 : L; l <= L; ++l) {
+            const int sh = 2 * (L - l);
+            for (int64_t b = 0; b < (int64_t(1) << (2 * l)); ++b) {
+                if (pl.h_scnt[size_t(lvl_base(l) + b)] == 0) continue;
+                const int32_t e0 = pl.h_soff[size_t(b << sh)], e1 = pl.h_soff[size_t((b + 1) << sh)];
+                const int32_t pieces = (e1 - e0 + kP2MItemCap - 1) / kP2MItemCap;
+                if (pieces > 1)
+                    splits.push_back(P2MSplit{l, int32_t(b), int32_t(items.size()), pieces});
+                for (int32_t e = e0; e < e1; e += kP2MItemCap)
+                    items.push_back(P2MItem{l, int32_t(b), e, std::min(e1, e + kP2MItemCap), pieces == 1 ? 1 : 0});
+            }
+        }
+        pl.n_p2m_items = int64_t(items.size());
+        pl.n_p2m_splits = int64_t(splits.size());
+        to_device(pl.p2m_items, items, st);
+        to_device(pl.p2m_splits, splits, st);
     }
     build_schedules(pl, 0, nleaf);
+}
+
+// Small problems pay more for the level-by-level M2M / L2L chains (~20 us
+// of latency per level, measured) than for evaluating every level directly:
+// P2M costs ~6 (L-1) P flops per source and L2P ~8 (L-1) P per target.
+// VPG_MULTILEVEL=0/1 forces the choice (tests cover both).
+void choose_passes(Plan& pl) {
+    const char* env = std::getenv("VPG_MULTILEVEL");
+    if (env && (env[0] == '0' || env[0] == '1')) {
+        pl.multilevel_up = pl.multilevel_down = env[0] == '1';
+        return;
+    }
+    const double chain_s = 20e-6 * double(std::max(0, pl.L - 2));
+    const double rate = 15e12;  // sustained FP64 flop/s of these passes
+    const double up_s = double(pl.ns) * (pl.L - 1) * 6.0 * 50.0 / rate;
+    const double down_s = double(pl.nt) * (pl.L - 1) * 8.0 * 51.0 / rate;
+    pl.multilevel_up = up_s < chain_s;
+    pl.multilevel_down = down_s < chain_s;
 }
 
 // Target-side schedules restricted to the Morton leaf range [lb, le): M2L

@@ -157,3 +157,16 @@ def test_target_shards_assemble_bit_exact(vp, world):
         assert seen.all()
         assert np.array_equal(total, full)
         assert np.array_equal(plan.apply(w.q), full)
+
+
+@pytest.mark.parametrize("multilevel", ["0", "1"])
+def test_chain_and_multilevel_passes(vp, rest, monkeypatch, multilevel):
+    """Upward/downward passes as level chains (M2M/L2L, the reference
+    structure) or as direct per-level P2M/L2P (small problems) agree with the
+    oracle to the same tolerance."""
+    monkeypatch.setenv("VPG_MULTILEVEL", multilevel)
+    w = W.cfg2()
+    with vp.SummationPlan(lap(vp), w.src, w.tgt, 1e-12) as plan:
+        gpu = plan.apply(w.q)
+    cpu = rest.plan_sum(0, 0.0, w.src, w.q, w.tgt, 1e-12)
+    assert rel_l2(gpu, cpu) <= 1e-13
