@@ -112,7 +112,8 @@ int64_t Plan::device_bytes() const {
                    src_cnt.bytes() + tgt_cnt.bytes() + m2l_tbox.bytes() + m2l_toff.bytes() +
                    m2l_src.bytes() + m2l_oidx.bytes() + m2l_batches.bytes() + m2m_ops.bytes() +
                    l2l_ops.bytes() + h_t.bytes() + dpow.bytes() + logmd.bytes() +
-                   p2p_chunks.bytes() + p2m_items.bytes() + p2m_splits.bytes() + updown_boxes.bytes() +
+                   p2p_chunks.bytes() + near_ranges.bytes() + row_level.bytes() + row_morton.bytes() +
+                   row_parent.bytes() + tgt_row.bytes() + p2m_items.bytes() + p2m_splits.bytes() + updown_boxes.bytes() +
                    helm_nodes.bytes() + helm_bw.bytes() + exp_off_dev.bytes());
 }
 
@@ -379,14 +380,20 @@ int vpg_plan_dump_m2l(const vpg_plan* plan, int level, int32_t* ntbox, int64_t* 
         const int64_t e0 = off.front(), e1 = off.back();
         if (ntbox) *ntbox = int32_t(t1 - t0);
         if (nent) *nent = e1 - e0;
-        if (tbox && t1 > t0)
+        // lists hold expansion rows; report Morton ids of the level
+        const int32_t rowbase = int32_t(lvl_base(level) - lvl_base(2));
+        if (tbox && t1 > t0) {
             VPG_CUDA(cudaMemcpy(tbox, pl.m2l_tbox.p + t0, size_t(t1 - t0) * sizeof(int32_t),
                                 cudaMemcpyDeviceToHost));
+            for (int64_t i = 0; i < t1 - t0; ++i) tbox[i] -= rowbase;
+        }
         if (toff)
             for (size_t i = 0; i < off.size(); ++i) toff[i] = int32_t(off[i] - e0);
-        if (src && e1 > e0)
+        if (src && e1 > e0) {
             VPG_CUDA(cudaMemcpy(src, pl.m2l_src.p + e0, size_t(e1 - e0) * sizeof(int32_t),
                                 cudaMemcpyDeviceToHost));
+            for (int64_t i = 0; i < e1 - e0; ++i) src[i] -= rowbase;
+        }
         if (oidx && e1 > e0)
             VPG_CUDA(cudaMemcpy(oidx, pl.m2l_oidx.p + e0, size_t(e1 - e0) * sizeof(int32_t),
                                 cudaMemcpyDeviceToHost));

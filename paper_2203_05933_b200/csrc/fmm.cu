@@ -45,7 +45,7 @@ constexpr int kP2MSrc = 16;
 __global__ void __launch_bounds__(kP2MWarps * 32)
 p2m_kernel(const P2MItem* items, int64_t nitems, const int32_t* sorted_unused,
            const double2* sxy, const double* q, int P, double x0, double y0, double side,
-           double2* mult, const int64_t* exp_off, double2* partial) {
+           double2* mult, double2* partial) {
     extern __shared__ double2 panels[];
     pdl_trigger();
     pdl_wait();
@@ -115,14 +115,14 @@ p2m_kernel(const P2MItem* items, int64_t nitems, const int32_t* sorted_unused,
         }
         __syncwarp();
     }
-    double2* dst = it.direct ? mult + exp_off[it.level] + int64_t(it.box) * n : partial + li * n;
+    double2* dst = it.direct ? mult + int64_t(it.row) * n : partial + li * n;
     if (lane <= P) dst[lane] = acc0;
     if (lane + 32 <= P) dst[lane + 32] = acc1;
 }
 
 // Boxes split over several P2M items: sum the item partials in item order.
 __global__ void p2m_reduce_kernel(const P2MSplit* splits, int64_t nsplit, const double2* partial,
-                                  int P, double2* mult, const int64_t* exp_off) {
+                                  int P, double2* mult) {
     pdl_trigger();
     pdl_wait();
     const int n = P + 1;
@@ -137,7 +137,7 @@ __global__ void p2m_reduce_kernel(const P2MSplit* splits, int64_t nsplit, const 
         acc.x += v.x;
         acc.y += v.y;
     }
-    mult[exp_off[b.level] + int64_t(b.box) * n + k] = acc;
+    mult[int64_t(b.row) * n + k] = acc;
 }
 
 // ------------------------------------------------------------ M2M / L2L --
@@ -348,9 +348,9 @@ __device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, doubl
 
 __device__ __forceinline__ void m2l_issue(const M2LBatch& bt, const int32_t* esrc,
                                           const int32_t* eoidx, const int32_t* omap_s,
-                                          const double2* mult, const int64_t* exp_off, int n,
-                                          M2LStage* stg, double2* raw, uint64_t* bar, int gtid) {
-    const double2* mlev = mult + exp_off[bt.level];
+                                          const double2* mult, int n, M2LStage* stg, double2* raw,
+                                          uint64_t* bar, int gtid) {
+    const double2* mlev = mult;  // list entries are expansion rows
     if (gtid == 0) mbar_arrive_expect_tx(bar, uint32_t(bt.ecount) * uint32_t(n) * 16u);
     if (gtid < bt.ecount) {
         const int64_t e = int64_t(bt.efirst) + gtid;
@@ -374,8 +374,8 @@ __global__ void __launch_bounds__(kM2LThreads, 1)
 m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
            const int32_t* toff, const int32_t* esrc, const int32_t* eoidx,
            const double* h_t, const double2* canon_g, const int32_t* omap_g,
-           const double2* logmd_g, const double2* mult, double2* loc, const int64_t* exp_off,
-           int P, int RP, int KP, double side) {
+           const double2* logmd_g, const double2* mult, double2* loc, int P, int RP, int KP,
+           double side) {
     extern __shared__ __align__(16) double smd[];
     const int n = P + 1;
     const int XR = max(KP, n);                                  // X/Y rows
@@ -416,11 +416,11 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
     const int64_t stride = int64_t(gridDim.x) * kM2LGroups;
     int64_t bi = int64_t(blockIdx.x) * kM2LGroups + g;
     if (bi < nbatch)
-        m2l_issue(batches[bi], esrc, eoidx, omap_s, mult, exp_off, n, &stg[0], raw, bar, gtid);
+        m2l_issue(batches[bi], esrc, eoidx, omap_s, mult, n, &stg[0], raw, bar, gtid);
 
     for (; bi < nbatch; bi += stride) {
         const M2LBatch bt = batches[bi];
-        double2* llev = loc + exp_off[bt.level];
+        double2* llev = loc;  // target entries are expansion rows
         const M2LStage& sg = stg[cur];
         mbar_wait(bar, phase);
         phase ^= 1u;
@@ -449,8 +449,7 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         const int64_t bn = bi + stride;
         if (bn < nbatch)
-            m2l_issue(batches[bn], esrc, eoidx, omap_s, mult, exp_off, n, &stg[cur ^ 1], raw, bar,
-                      gtid);
+            m2l_issue(batches[bn], esrc, eoidx, omap_s, mult, n, &stg[cur ^ 1], raw, bar, gtid);
 
         // 2. DMMA GEMM: warp w owns column tiles w, w+6, w+12 and all row tiles
         double acc[kM2LMaxMT][kM2LNTPerWarp][2];
@@ -557,9 +556,9 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
 // Threads of one leaf read the same coefficients (L1 broadcast).  The
 // near-field kernel adds its sum on top (fixed order: far, then near).
 __global__ void __launch_bounds__(256)
-l2p_kernel(const int32_t* tleaf, int64_t t0, int64_t t1, const double2* txy,
-           const double2* loc, const int64_t* exp_off, int lmin, int L, int P, double x0,
-           double y0, double side, double* pot_far, int* ticket) {
+l2p_kernel(const int32_t* trow, int64_t t0, int64_t t1, const double2* txy, const double2* loc,
+           const int32_t* row_level, const int32_t* row_morton, const int32_t* row_parent,
+           int multilevel, int P, double x0, double y0, double side, double* pot_far, int* ticket) {
     pdl_trigger();
     pdl_wait();
     const int64_t e = t0 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
@@ -568,20 +567,19 @@ l2p_kernel(const int32_t* tleaf, int64_t t0, int64_t t1, const double2* txy,
         ticket[1] = 0;
     }
     if (e >= t1) return;
-    const uint32_t bL = uint32_t(tleaf[e]);
     const double2 t = txy[e];
-    // levels lmin..L: lmin == L is the reference L2P after the L2L chain;
-    // lmin == 2 evaluates every ancestor's local expansion (multilevel
-    // downward pass, no L2L), summed coarse to fine.
+    // The leaf's local expansion (after the L2L chain: summation.cpp:323-329)
+    // or, in the multilevel downward pass, the leaf's and every ancestor's
+    // (M2L / P2L contributions per level, no L2L), summed fine to coarse.
     double sum = 0.0;
-    for (int l = lmin; l <= L; ++l) {
-        const uint32_t b = bL >> (2 * (L - l));
+    for (int r = trow[e]; r >= 0; r = multilevel ? row_parent[r] : -1) {
+        const int l = row_level[r];
         const double s = side / double(1 << l);
         double cx, cy;
-        box_center(x0, y0, s, b, cx, cy);
+        box_center(x0, y0, s, uint32_t(row_morton[r]), cx, cy);
         const double inv_s = 1.0 / s;
         const double ur = (t.x - cx) * inv_s, ui = (t.y - cy) * inv_s;
-        const double2* ab = loc + exp_off[l] + int64_t(b) * (P + 1);
+        const double2* ab = loc + int64_t(r) * (P + 1);
         double vr = ab[P].x, vi = ab[P].y;
         for (int k = P - 1; k >= 0; --k) {
             const double2 a = ab[k];
@@ -625,40 +623,52 @@ constexpr int kP2PChunk = 64;
 #endif
 constexpr int kP2PMinBlocks = VPG_P2P_MIN_BLOCKS;
 
+// The near sources of a chunk: up to kMaxNearRanges leaf ranges (the 3x3
+// neighbourhood in uniform trees, the U list in adaptive ones) flattened
+// into one virtual list.  Range starts and prefix offsets live in a per-warp
+// smem slot; a flat index maps to its source by binary search.
 struct NearList {
     int total;
-    int pre[9], st[9];
+    int nr;
+    int self0, self1;   // flat range of the target leaf's own sources
+    const int* pre;     // [nr] prefix offsets (smem)
+    const int* st;      // [nr] first sorted source (smem)
 };
 
-__device__ __forceinline__ NearList near_list(uint32_t b, int nb, const int32_t* soff, int lane) {
-    const int ix = int(squash2(b)), iy = int(squash2(b >> 1));
-    int rs = 0, rl = 0;
-    if (lane < 9) {
-        const int jx = ix - 1 + lane % 3, jy = iy - 1 + lane / 3;
-        if (jx >= 0 && jx < nb && jy >= 0 && jy < nb) {
-            const uint32_t sid = mort(uint32_t(jx), uint32_t(jy));
-            rs = soff[sid];
-            rl = soff[sid + 1] - rs;
+__device__ __forceinline__ NearList near_list(const int2* ranges, int rfirst, int rcount, int rself,
+                                              int lane, int* pre_s, int* st_s) {
+    __syncwarp();
+    int2 r0 = make_int2(0, 0), r1 = make_int2(0, 0);
+    if (lane < rcount) r0 = ranges[rfirst + lane];
+    if (lane + 32 < rcount) r1 = ranges[rfirst + lane + 32];
+    int i0 = r0.y, i1 = r1.y;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v0 = __shfl_up_sync(0xffffffffu, i0, o);
+        const int v1 = __shfl_up_sync(0xffffffffu, i1, o);
+        if (lane >= o) {
+            i0 += v0;
+            i1 += v1;
         }
     }
-    int incl = rl;
-#pragma unroll
-    for (int o = 1; o < 16; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-    }
+    const int tot0 = __shfl_sync(0xffffffffu, i0, 31);
+    pre_s[lane] = i0 - r0.y;
+    st_s[lane] = r0.x;
+    pre_s[lane + 32] = tot0 + i1 - r1.y;
+    st_s[lane + 32] = r1.x;
     NearList nl;
-    nl.total = __shfl_sync(0xffffffffu, incl, 8);
-#pragma unroll
-    for (int i = 0; i < 9; ++i) {
-        nl.pre[i] = __shfl_sync(0xffffffffu, incl - rl, i);
-        nl.st[i] = __shfl_sync(0xffffffffu, rs, i);
-    }
+    nl.total = tot0 + __shfl_sync(0xffffffffu, i1, 31);
+    nl.nr = rcount;
+    __syncwarp();
+    nl.self0 = pre_s[rself];
+    nl.self1 = rself + 1 < rcount ? pre_s[rself + 1] : nl.total;
+    nl.pre = pre_s;
+    nl.st = st_s;
     return nl;
 }
 
 // One batch [base, base+cnt) of the flat list: stage, evaluate (sources
-// f == grp mod S), then fix up the centre-leaf pairs of the batch.
+// f == grp mod S), then fix up the pairs with the target leaf's own sources.
 __device__ __forceinline__ void near_batch(const NearList& nl, int base, int cnt, int grp, int S,
                                            bool active, int lane, const double2* sxy,
                                            const double* q, double2* mxy, double* mq,
@@ -670,10 +680,13 @@ __device__ __forceinline__ void near_batch(const NearList& nl, int base, int cnt
         const int f = h * 32 + lane;
         if (f < cnt) {
             const int ff = base + f;
-            int src = nl.st[0] + ff;
-#pragma unroll
-            for (int i = 1; i < 9; ++i)
-                if (ff >= nl.pre[i]) src = nl.st[i] + (ff - nl.pre[i]);
+            // last range with pre <= ff (empty ranges share the next start)
+            int lo = 0, hi = nl.nr - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (nl.pre[mid] <= ff) lo = mid; else hi = mid - 1;
+            }
+            const int src = nl.st[lo] + (ff - nl.pre[lo]);
             mxy[f] = sxy[src];
             mq[f] = q[src];
         }
@@ -689,8 +702,7 @@ __device__ __forceinline__ void near_batch(const NearList& nl, int base, int cnt
         lap_pair_fast(tx[0], ty[0], sp.x, sp.y, qj, tab_lane, acc[0]);
         lap_pair_fast(tx[1], ty[1], sp.x, sp.y, qj, tab_lane, acc[1]);
     }
-    // centre leaf = neighbour 4 (it always exists): flat range [pre4, pre5)
-    const int c0 = max(nl.pre[4], base), c1 = min(nl.pre[5], base + cnt);
+    const int c0 = max(nl.self0, base), c1 = min(nl.self1, base + cnt);
     if (c0 < c1) {
         int f = c0 + (grp - c0 % S);
         if (f < c0) f += S;
@@ -704,15 +716,16 @@ __device__ __forceinline__ void near_batch(const NearList& nl, int base, int cnt
 }
 
 __global__ void __launch_bounds__(kP2PWarps * 32, kP2PMinBlocks)
-l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, int64_t nheavy, const int32_t* soff,
+l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, int64_t nheavy, const int2* ranges,
                const double2* sxy, const double* q, const double2* txy,
-               const int32_t* tids, const double* pot_far, int L,
+               const int32_t* tids, const double* pot_far,
                const double2* gtab, int* ticket, double* out) {
     extern __shared__ double2 smp[];
     double2* tab = smp;                                                  // log table
     double2* sbuf = smp + kLogTableSize * kLogTableCopies;               // [warps][batch] xy
     double* qbuf = reinterpret_cast<double*>(sbuf + kP2PWarps * kP2PBatch);  // [warps][batch]
     double* red = qbuf + kP2PWarps * kP2PBatch;                          // [warps][64]
+    int* rbuf = reinterpret_cast<int*>(red + kP2PWarps * 64);            // [warps][2][64]
     __shared__ __align__(8) uint64_t bar;
     __shared__ int s_ch;
     if (threadIdx.x == 0) mbar_init(&bar, 1);
@@ -728,7 +741,8 @@ l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, int64_t nheavy, const in
     const uint32_t tab_lane = log_table_lane_addr(tab, lane & 7);
     double2* mxy = sbuf + warp * kP2PBatch;
     double* mq = qbuf + warp * kP2PBatch;
-    const int nb = 1 << L;
+    int* pre_s = rbuf + warp * 2 * kMaxNearRanges;
+    int* st_s = pre_s + kMaxNearRanges;
 
     // ---- phase 1: heavy chunks, the whole CTA per chunk
     for (;;) {
@@ -747,7 +761,7 @@ l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, int64_t nheavy, const in
             tx[u] = t.x;
             ty[u] = t.y;
         }
-        const NearList nl = near_list(uint32_t(c.leaf), nb, soff, lane);
+        const NearList nl = near_list(ranges, c.rfirst, c.rcount, c.rself, lane, pre_s, st_s);
         // warp w takes the w-th eighth of the flat source list
         const int f0 = int(int64_t(nl.total) * warp / kP2PWarps);
         const int f1 = int(int64_t(nl.total) * (warp + 1) / kP2PWarps);
@@ -788,7 +802,7 @@ l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, int64_t nheavy, const in
             tx[u] = t.x;
             ty[u] = t.y;
         }
-        const NearList nl = near_list(uint32_t(c.leaf), nb, soff, lane);
+        const NearList nl = near_list(ranges, c.rfirst, c.rcount, c.rself, lane, pre_s, st_s);
         for (int base = 0; base < nl.total; base += kP2PBatch)
             near_batch(nl, base, min(kP2PBatch, nl.total - base), grp, S, active, lane, sxy, q, mxy,
                        mq, tab_lane, tx, ty, acc);
@@ -1010,13 +1024,12 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
         launch_pdl(p2m_kernel, dim3(nblk(pl.n_p2m_items, kP2MWarps)), dim3(kP2MWarps * 32),
                    size_t(kP2MWarps) * kP2MSrc * n * sizeof(double2), st, (const P2MItem*)pl.p2m_items.p,
                    pl.n_p2m_items, (const int32_t*)nullptr, (const double2*)pl.src_sorted.p, (const double*)qs,
-                   P, pl.x0, pl.y0, pl.side, mult, exp_off_d, partial);
+                   P, pl.x0, pl.y0, pl.side, mult, partial);
         ++launches;
     }
     if (pl.n_p2m_splits > 0) {
         launch_pdl(p2m_reduce_kernel, dim3(nblk(pl.n_p2m_splits * n, 256)), dim3(256), 0, st,
-                   (const P2MSplit*)pl.p2m_splits.p, pl.n_p2m_splits, (const double2*)partial, P, mult,
-                   exp_off_d);
+                   (const P2MSplit*)pl.p2m_splits.p, pl.n_p2m_splits, (const double2*)partial, P, mult);
         ++launches;
         VPG_CUDA(cudaFreeAsync(partial, st));
     }
@@ -1058,8 +1071,7 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
                    (const int32_t*)pl.m2l_toff.p, (const int32_t*)pl.m2l_src.p,
                    (const int32_t*)pl.m2l_oidx.p, (const double*)pl.h_t.p,
                    (const double2*)pl.m2l_canon.p, (const int32_t*)pl.m2l_omap.p,
-                   (const double2*)pl.logmd.p, (const double2*)mult, loc, exp_off_d, P, pl.RP, pl.KP,
-                   pl.side);
+                   (const double2*)pl.logmd.p, (const double2*)mult, loc, P, pl.RP, pl.KP, pl.side);
         ++launches;
     }
     mark(4);
@@ -1084,23 +1096,24 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
     mark(5);
     if (pl.shard_t1 > pl.shard_t0) {
         launch_pdl(l2p_kernel, dim3(nblk(pl.shard_t1 - pl.shard_t0, 256)), dim3(256), 0, st,
-                   (const int32_t*)pl.tgt_leaf.p, pl.shard_t0, pl.shard_t1, (const double2*)pl.tgt_sorted.p,
-                   (const double2*)loc, exp_off_d, pl.multilevel_down ? 2 : L, L, P, pl.x0, pl.y0, pl.side,
+                   (const int32_t*)pl.tgt_row.p, pl.shard_t0, pl.shard_t1, (const double2*)pl.tgt_sorted.p,
+                   (const double2*)loc, (const int32_t*)pl.row_level.p, (const int32_t*)pl.row_morton.p,
+                   (const int32_t*)pl.row_parent.p, pl.multilevel_down ? 1 : 0, P, pl.x0, pl.y0, pl.side,
                    pot_far, ticket);
         ++launches;
     }
     if (pl.n_p2p_chunks > 0) {
         const size_t smem = size_t(kLogTableBytes) +
                             (sizeof(double2) + sizeof(double)) * kP2PBatch * kP2PWarps +
-                            sizeof(double) * 64 * kP2PWarps;
+                            sizeof(double) * 64 * kP2PWarps + sizeof(int) * 2 * kMaxNearRanges * kP2PWarps;
         int per_sm = 1;
         VPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, l2p_p2p_kernel, kP2PWarps * 32, smem));
         const int64_t want = (pl.n_p2p_chunks + kP2PWarps - 1) / kP2PWarps;
         const unsigned grid = unsigned(std::min<int64_t>(want, int64_t(pl.sm_count) * std::max(per_sm, 1)));
         launch_pdl(l2p_p2p_kernel, dim3(grid), dim3(kP2PWarps * 32), smem, st,
                    (const P2PChunk*)pl.p2p_chunks.p, pl.n_p2p_chunks, pl.n_p2p_heavy,
-                   (const int32_t*)pl.src_off.p, (const double2*)pl.src_sorted.p, (const double*)qs,
-                   (const double2*)pl.tgt_sorted.p, (const int32_t*)pl.tgt_ids.p, (const double*)pot_far, L,
+                   (const int2*)pl.near_ranges.p, (const double2*)pl.src_sorted.p, (const double*)qs,
+                   (const double2*)pl.tgt_sorted.p, (const int32_t*)pl.tgt_ids.p, (const double*)pot_far,
                    log_table_dev(), ticket, out_dev);
         ++launches;
     }

@@ -48,14 +48,14 @@ constexpr int kM2LPairs = 54;  // two interior target boxes (27 each); 2 * pairs
 // level; direct = the box is a single item (write the expansion in place).
 struct P2MItem {
     int32_t level;
-    int32_t box;
+    int32_t box;    // Morton id at `level` (centre)
+    int32_t row;    // expansion row (mult + row * (P+1))
     int32_t e0, e1;
     int32_t direct;
 };
 // A box whose sources span several items: partials summed in item order.
 struct P2MSplit {
-    int32_t level;
-    int32_t box;
+    int32_t row;
     int32_t first;
     int32_t count;
 };
@@ -63,11 +63,14 @@ constexpr int kP2MItemCap = 256;  // sources per P2M item
 
 // P2P work unit: up to chunk targets of one leaf (Morton-sorted order).
 struct P2PChunk {
-    int32_t leaf;
     int32_t tbegin;
     int32_t tcount;
-    int32_t pad;  // neighbourhood source count (schedule cost estimate)
+    int32_t pad;     // neighbourhood source count (schedule cost estimate)
+    int32_t rfirst;  // near source ranges [rfirst, rfirst + rcount) in near_ranges
+    int32_t rcount;  // <= kMaxNearRanges
+    int32_t rself;   // index (within the list) of the target's own leaf
 };
+constexpr int kMaxNearRanges = 64;
 
 struct Plan {
     int device = 0;
@@ -86,7 +89,12 @@ struct Plan {
     DBuf<double2> src_sorted, tgt_sorted;
     DBuf<int32_t> src_off, src_ids, tgt_off, tgt_ids;  // leaf CSR
     DBuf<int32_t> src_cnt, tgt_cnt;                    // all levels
-    DBuf<int32_t> tgt_leaf;  // leaf id of every Morton-sorted target
+    // Expansion rows: every box that carries an expansion has a row
+    // (mult/loc + row * (P+1)).  Uniform trees: levels 2..L dense, row =
+    // exp_off[l]/(P+1) + Morton id.  Adaptive trees: one row per box.
+    DBuf<int32_t> row_level, row_morton, row_parent;  // parent = -1 above level 2
+    int64_t n_rows = 0;
+    DBuf<int32_t> tgt_row;  // leaf row of every Morton-sorted target
 
     // M2L lists (levels 2..L concatenated): target boxes and entries.
     std::vector<int64_t> lvl_tfirst;  // per level: first target-box index
@@ -113,6 +121,7 @@ struct Plan {
     // P2P schedule.
     int p2p_tpt = 1;
     DBuf<P2PChunk> p2p_chunks;
+    DBuf<int2> near_ranges;  // (first sorted source, count) per near leaf
     int64_t n_p2p_chunks = 0;
     int64_t n_p2p_heavy = 0;  // leading chunks handled by a whole CTA
     int64_t p2p_pairs = 0;

@@ -161,7 +161,8 @@ __global__ void m2l_list_kernel(const int32_t* src_cnt, const int32_t* tgt_cnt,
                 const uint32_t sid = mort(uint32_t(jx), uint32_t(jy));
                 if (sc[sid] == 0) continue;
                 if (kFill) {
-                    esrc[e] = int32_t(sid);
+                    // expansion row of the source box (levels 2..L dense)
+                    esrc[e] = int32_t(lvl_base(l) - lvl_base(2) + sid);
                     eoidx[e] = (dx + 3) + 7 * (dy + 3);
                     ++e;
                 } else {
@@ -174,7 +175,7 @@ __global__ void m2l_list_kernel(const int32_t* src_cnt, const int32_t* tgt_cnt,
         ecount[g] = cnt;
     } else {
         const int64_t t = tpos[g];
-        tbox[t] = int32_t(b);
+        tbox[t] = int32_t(g);  // expansion row of the target box
         toff[t] = int32_t(epos[g]);
     }
 }
@@ -343,10 +344,25 @@ void build_tree(Plan& pl) {
     pl.h_soff = to_host(pl.src_off, st);
     pl.h_toff = to_host(pl.tgt_off, st);
     {
+        // expansion rows: levels 2..L dense, row = lvl_base(l) - lvl_base(2) + Morton
+        const int64_t rb2 = lvl_base(2);
+        pl.n_rows = lvl_base(L + 1) - rb2;
+        std::vector<int32_t> rl(size_t(pl.n_rows)), rm(size_t(pl.n_rows)), rp(size_t(pl.n_rows));
+        for (int l = 2; l <= L; ++l)
+            for (int64_t b = 0; b < (int64_t(1) << (2 * l)); ++b) {
+                const int64_t r = lvl_base(l) - rb2 + b;
+                rl[size_t(r)] = l;
+                rm[size_t(r)] = int32_t(b);
+                rp[size_t(r)] = l > 2 ? int32_t(lvl_base(l - 1) - rb2 + (b >> 2)) : -1;
+            }
+        to_device(pl.row_level, rl, st);
+        to_device(pl.row_morton, rm, st);
+        to_device(pl.row_parent, rp, st);
         std::vector<int32_t> tl(size_t(std::max<int64_t>(pl.nt, 1)), 0);
         for (int64_t b = 0; b < nleaf; ++b)
-            for (int32_t e = pl.h_toff[size_t(b)]; e < pl.h_toff[size_t(b) + 1]; ++e) tl[size_t(e)] = int32_t(b);
-        to_device(pl.tgt_leaf, tl, st);
+            for (int32_t e = pl.h_toff[size_t(b)]; e < pl.h_toff[size_t(b) + 1]; ++e)
+                tl[size_t(e)] = int32_t(lvl_base(L) - rb2 + b);
+        to_device(pl.tgt_row, tl, st);
     }
     choose_passes(pl);
     {
@@ -359,10 +375,10 @@ void build_tree(Plan& pl) {
                 if (pl.h_scnt[size_t(lvl_base(l) + b)] == 0) continue;
                 const int32_t e0 = pl.h_soff[size_t(b << sh)], e1 = pl.h_soff[size_t((b + 1) << sh)];
                 const int32_t pieces = (e1 - e0 + kP2MItemCap - 1) / kP2MItemCap;
-                if (pieces > 1)
-                    splits.push_back(P2MSplit{l, int32_t(b), int32_t(items.size()), pieces});
+                const int32_t row = int32_t(lvl_base(l) - lvl_base(2) + b);
+                if (pieces > 1) splits.push_back(P2MSplit{row, int32_t(items.size()), pieces});
                 for (int32_t e = e0; e < e1; e += kP2MItemCap)
-                    items.push_back(P2MItem{l, int32_t(b), e, std::min(e1, e + kP2MItemCap), pieces == 1 ? 1 : 0});
+                    items.push_back(P2MItem{l, int32_t(b), row, e, std::min(e1, e + kP2MItemCap), pieces == 1 ? 1 : 0});
             }
         }
         pl.n_p2m_items = int64_t(items.size());
@@ -484,21 +500,30 @@ void build_schedules(Plan& pl, int64_t lb, int64_t le) {
         pl.p2p_tpt = 2;
         const int chunk = 64;  // kP2PChunk: two targets per lane
         std::vector<P2PChunk> chunks;
+        std::vector<int2> ranges;
         pl.p2p_pairs = 0;
         for (int64_t b = lb; b < le; ++b) {
             const int32_t t0 = h_toff[size_t(b)], t1 = h_toff[size_t(b) + 1];
             if (t1 == t0) continue;
             const int ix = int(squash2(uint32_t(b))), iy = int(squash2(uint32_t(b) >> 1));
+            // 3x3 neighbour leaves in the reference order (summation.cpp:330-334)
+            const int32_t rfirst = int32_t(ranges.size());
+            int32_t rself = 0;
             int64_t nsrc = 0;
             for (int jy = std::max(0, iy - 1); jy <= std::min(nb - 1, iy + 1); ++jy)
                 for (int jx = std::max(0, ix - 1); jx <= std::min(nb - 1, ix + 1); ++jx) {
                     const uint32_t sid = mort(uint32_t(jx), uint32_t(jy));
+                    if (jx == ix && jy == iy) rself = int32_t(ranges.size()) - rfirst;
+                    ranges.push_back(make_int2(h_soff[sid], h_soff[sid + 1] - h_soff[sid]));
                     nsrc += h_soff[sid + 1] - h_soff[sid];
                 }
+            const int32_t rcount = int32_t(ranges.size()) - rfirst;
             pl.p2p_pairs += int64_t(t1 - t0) * nsrc;
             for (int32_t t = t0; t < t1; t += chunk)
-                chunks.push_back(P2PChunk{int32_t(b), t, std::min(chunk, t1 - t), int32_t(std::min<int64_t>(nsrc, INT32_MAX))});
+                chunks.push_back(P2PChunk{t, std::min(chunk, t1 - t), int32_t(std::min<int64_t>(nsrc, INT32_MAX)),
+                                          rfirst, rcount, rself});
         }
+        to_device(pl.near_ranges, ranges, st);
         // Heavy chunks (large neighbourhoods, > 32 targets) first -- a whole
         // CTA processes each (l2p_p2p_kernel phase 1) -- then the light ones
         // for single warps; costliest first within each part, so the
