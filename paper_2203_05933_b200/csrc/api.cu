@@ -271,7 +271,7 @@ int vpg_plan_apply(const vpg_plan* plan, const double* q, int64_t nq, double* ou
             VPG_CUDA(cudaMemcpyAsync(qd.p, q, sizeof(double) * size_t(pl.ns), cudaMemcpyHostToDevice, st));
         int64_t launches = 0;
         cudaEvent_t* inner = prof ? ev + 1 : nullptr;  // GATHER .. DOWNLOAD
-        if (!pl.direct && (pl.shard_lb != 0 || pl.shard_le != (int64_t(1) << (2 * pl.L))) && pl.nt)
+        if (!pl.direct && !pl.adaptive && (pl.shard_lb != 0 || pl.shard_le != (int64_t(1) << (2 * pl.L))) && pl.nt)
             VPG_CUDA(cudaMemsetAsync(out_dev, 0, sizeof(double) * size_t(pl.nt), st));
         if (pl.direct) {
             if (prof)
@@ -351,6 +351,8 @@ int vpg_plan_dump_tree(const vpg_plan* plan, int32_t* src_off, int32_t* src_ids,
         if (!plan) throw Error{VPG_ERR_INVALID_ARGUMENT, "plan is NULL"};
         const Plan& pl = plan->impl;
         if (pl.direct) throw Error{VPG_ERR_INVALID_ARGUMENT, "pairwise plan has no tree"};
+        if (pl.adaptive)
+            throw Error{VPG_ERR_INVALID_ARGUMENT, "adaptive (native) plan has no uniform leaf table"};
         VPG_CUDA(cudaSetDevice(pl.device));
         auto cp = [](int32_t* dst, const DBuf<int32_t>& s, size_t n) {
             if (dst && n) VPG_CUDA(cudaMemcpy(dst, s.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost));
@@ -372,6 +374,8 @@ int vpg_plan_dump_m2l(const vpg_plan* plan, int level, int32_t* ntbox, int64_t* 
         const Plan& pl = plan->impl;
         if (pl.direct || level < 2 || level > pl.L)
             throw Error{VPG_ERR_INVALID_ARGUMENT, "level out of range"};
+        if (pl.adaptive)
+            throw Error{VPG_ERR_INVALID_ARGUMENT, "adaptive (native) plan has no per-level M2L table"};
         VPG_CUDA(cudaSetDevice(pl.device));
         const int64_t t0 = pl.lvl_tfirst[size_t(level)], t1 = pl.lvl_tfirst[size_t(level + 1)];
         std::vector<int32_t> off(size_t(t1 - t0 + 1));
@@ -405,6 +409,8 @@ int vpg_plan_set_shard(vpg_plan* plan, int64_t leaf_begin, int64_t leaf_end) {
         if (!plan) throw Error{VPG_ERR_INVALID_ARGUMENT, "plan is NULL"};
         Plan& pl = plan->impl;
         if (pl.direct) throw Error{VPG_ERR_INVALID_ARGUMENT, "pairwise plan cannot be sharded"};
+        if (pl.adaptive)
+            throw Error{VPG_ERR_INVALID_ARGUMENT, "adaptive (native) plan cannot be leaf-sharded"};
         const int64_t nleaf = int64_t(1) << (2 * pl.L);
         if (leaf_begin < 0 || leaf_end > nleaf || leaf_begin > leaf_end)
             throw Error{VPG_ERR_INVALID_ARGUMENT, "shard leaf range out of bounds"};

@@ -820,6 +820,155 @@ l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, int64_t nheavy, const in
     }
 }
 
+// ------------------------------------------------------ adaptive: M2P / P2L --
+// M2P (W lists of adaptive trees): a box's multipole evaluated directly at a
+// leaf's targets.  With a_0 = sum q and a_k = -(1/k) sum q w^k,
+// w = (z - c)/s (P2M above), sum_j q_j log(t - z_j) = a_0 log(t - c)
+// + sum_k a_k (s/(t - c))^k, so per target u = s/(t - c), Horner over k, plus
+// a_0 log|t - c| (a_0 is real: real charges).  Warp per (leaf, 32 targets),
+// W entries in list order, coefficients staged per warp in smem.
+constexpr int kM2PWarps = 4;
+
+__global__ void __launch_bounds__(kM2PWarps * 32)
+m2p_kernel(const int4* work, int64_t nwork, const int32_t* wrows, const double2* txy,
+           const double2* mult, const int32_t* row_level, const int32_t* row_morton, int P,
+           double x0, double y0, double side, double* pot_far) {
+    extern __shared__ double2 coef[];
+    pdl_trigger();
+    pdl_wait();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t wi = int64_t(blockIdx.x) * kM2PWarps + warp;
+    if (wi >= nwork) return;
+    const int n = P + 1;
+    double2* cw = coef + warp * n;
+    const int4 w = work[wi];
+    const int e = w.x + min(lane, w.y - 1);
+    const double2 t = txy[e];
+    double acc = 0.0;
+    for (int k = 0; k < w.w; ++k) {
+        const int r = wrows[w.z + k];
+        __syncwarp();
+        for (int i = lane; i < n; i += 32) cw[i] = mult[int64_t(r) * n + i];
+        __syncwarp();
+        const double s = side / double(1 << row_level[r]);
+        double cx, cy;
+        box_center(x0, y0, s, uint32_t(row_morton[r]), cx, cy);
+        const double dx = t.x - cx, dy = t.y - cy;
+        const double d2 = fma(dy, dy, dx * dx);
+        const double inv = s / d2;
+        const double ur = dx * inv, ui = -dy * inv;  // s / (t - c)
+        double vr = cw[P].x, vi = cw[P].y;
+        for (int j = P - 1; j >= 1; --j) {
+            const double2 a = cw[j];
+            const double nr = fma(vr, ur, fma(-vi, ui, a.x));
+            const double ni = fma(vr, ui, fma(vi, ur, a.y));
+            vr = nr;
+            vi = ni;
+        }
+        const double re = vr * ur - vi * ui;  // times u once more: sum_{k>=1} a_k u^k
+        acc += re + cw[0].x * 0.5 * log(d2);
+    }
+    if (lane < w.y) pot_far[e] += -kInv2Pi * acc;
+}
+
+// P2L (X lists of adaptive trees): a coarser leaf's sources straight into a
+// box's local expansion.  For |z - c| < |z_j - c|, log(z - z_j) =
+// log(c - z_j) - sum_l (1/l) u^l v_j^l with u = (z - c)/s, v_j = s/(z_j - c):
+// b_0 += q log|z_j - c| (only the real part is ever used), b_l += -q v^l / l.
+// Warp per receiving box, the panel scheme of P2M (two lanes per source,
+// half the powers each), X ranges in list order; loc += result (the box's
+// only writer after M2L).
+__global__ void __launch_bounds__(kP2MWarps * 32)
+p2l_kernel(const int4* work, int64_t nwork, const int2* ranges, const double2* sxy,
+           const double* q, const int32_t* row_level, const int32_t* row_morton, int P,
+           double x0, double y0, double side, double2* loc) {
+    extern __shared__ double2 panels[];
+    pdl_trigger();
+    pdl_wait();
+    const int n = P + 1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t wi = int64_t(blockIdx.x) * kP2MWarps + warp;
+    if (wi >= nwork) return;
+    double2* panel = panels + warp * kP2MSrc * n;
+    const int4 w = work[wi];
+    const int r = w.x;
+    const double s = side / double(1 << row_level[r]);
+    double cx, cy;
+    box_center(x0, y0, s, uint32_t(row_morton[r]), cx, cy);
+    const int j = lane & (kP2MSrc - 1), h = lane >> 4;
+    const int kh = (P + 1) >> 1;
+    double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
+    for (int ri = 0; ri < w.z; ++ri) {
+        const int2 rg = ranges[w.y + ri];
+        for (int base = rg.x; base < rg.x + rg.y; base += kP2MSrc) {
+            const int cnt = min(kP2MSrc, rg.x + rg.y - base);
+            if (j < cnt) {
+                const double2 p = sxy[base + j];
+                const double dx = p.x - cx, dy = p.y - cy;
+                const double d2 = fma(dy, dy, dx * dx);
+                const double inv = s / d2;
+                const double vr = dx * inv, vi = -dy * inv;  // s / (z_j - c)
+                const double qj = q[base + j];
+                double2* row = panel + j * n;
+                double pr = qj, pi = 0.0;
+                int k0 = 1, k1 = kh;
+                if (h == 0) {
+                    row[0] = make_double2(qj * 0.5 * log(d2), 0.0);
+                } else {
+                    double br = vr, bi = vi;
+                    for (int e = kh; e; e >>= 1) {
+                        if (e & 1) {
+                            const double nr = pr * br - pi * bi;
+                            pi = pr * bi + pi * br;
+                            pr = nr;
+                        }
+                        const double sr = br * br - bi * bi;
+                        bi = 2.0 * br * bi;
+                        br = sr;
+                    }
+                    k0 = kh + 1;
+                    k1 = P;
+                }
+                for (int k = k0; k <= k1; ++k) {
+                    const double nr = pr * vr - pi * vi;
+                    const double ni = pr * vi + pi * vr;
+                    pr = nr;
+                    pi = ni;
+                    const double f = c_neg_inv_k[k];
+                    row[k] = make_double2(f * pr, f * pi);
+                }
+            }
+            __syncwarp();
+            for (int t = 0; t < cnt; ++t) {
+                if (lane <= P) {
+                    const double2 v0 = panel[t * n + lane];
+                    acc0.x += v0.x;
+                    acc0.y += v0.y;
+                }
+                if (lane + 32 <= P) {
+                    const double2 v1 = panel[t * n + lane + 32];
+                    acc1.x += v1.x;
+                    acc1.y += v1.y;
+                }
+            }
+            __syncwarp();
+        }
+    }
+    double2* dst = loc + int64_t(r) * n;
+    if (lane <= P) {
+        double2 v = dst[lane];
+        v.x += acc0.x;
+        v.y += acc0.y;
+        dst[lane] = v;
+    }
+    if (lane + 32 <= P) {
+        double2 v = dst[lane + 32];
+        v.x += acc1.x;
+        v.y += acc1.y;
+        dst[lane + 32] = v;
+    }
+}
+
 __global__ void gather_q(const double* q, const int32_t* ids, int64_t n, double* qs, unsigned* gbar) {
     const int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
     if (e < 2) gbar[e] = 0u;
@@ -962,13 +1111,14 @@ void build_laplace_ops(Plan& pl) {
         pl.exp_off[size_t(l)] = off;
         off += (int64_t(1) << (2 * l)) * n;
     }
-    pl.exp_total = off;
+    pl.exp_total = pl.adaptive ? pl.n_rows * n : off;
     pl.exp_off_dev.alloc(pl.exp_off.size());
     VPG_CUDA(cudaMemcpy(pl.exp_off_dev.p, pl.exp_off.data(), pl.exp_off_dev.bytes(),
                         cudaMemcpyHostToDevice));
 
     smem_optin((const void*)m2l_kernel, 225 * 1024);
     smem_optin((const void*)p2m_kernel, 100 * 1024);
+    smem_optin((const void*)p2l_kernel, 100 * 1024);
     smem_optin((const void*)shift_kernel<true>, 220 * 1024);
     smem_optin((const void*)shift_kernel<false>, 220 * 1024);
     {
@@ -1074,6 +1224,14 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
                    (const double2*)pl.logmd.p, (const double2*)mult, loc, P, pl.RP, pl.KP, pl.side);
         ++launches;
     }
+    if (pl.n_p2l_work > 0) {
+        launch_pdl(p2l_kernel, dim3(nblk(pl.n_p2l_work, kP2MWarps)), dim3(kP2MWarps * 32),
+                   size_t(kP2MWarps) * kP2MSrc * n * sizeof(double2), st, (const int4*)pl.p2l_work.p,
+                   pl.n_p2l_work, (const int2*)pl.p2l_ranges.p, (const double2*)pl.src_sorted.p,
+                   (const double*)qs, (const int32_t*)pl.row_level.p, (const int32_t*)pl.row_morton.p, P,
+                   pl.x0, pl.y0, pl.side, loc);
+        ++launches;
+    }
     mark(4);
     if (!pl.multilevel_down) {
         ShiftLevels lv{};
@@ -1100,6 +1258,14 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
                    (const double2*)loc, (const int32_t*)pl.row_level.p, (const int32_t*)pl.row_morton.p,
                    (const int32_t*)pl.row_parent.p, pl.multilevel_down ? 1 : 0, P, pl.x0, pl.y0, pl.side,
                    pot_far, ticket);
+        ++launches;
+    }
+    if (pl.n_m2p_work > 0) {
+        launch_pdl(m2p_kernel, dim3(nblk(pl.n_m2p_work, kM2PWarps)), dim3(kM2PWarps * 32),
+                   size_t(kM2PWarps) * n * sizeof(double2), st, (const int4*)pl.m2p_work.p, pl.n_m2p_work,
+                   (const int32_t*)pl.m2p_rows.p, (const double2*)pl.tgt_sorted.p, (const double2*)mult,
+                   (const int32_t*)pl.row_level.p, (const int32_t*)pl.row_morton.p, P, pl.x0, pl.y0,
+                   pl.side, pot_far);
         ++launches;
     }
     if (pl.n_p2p_chunks > 0) {

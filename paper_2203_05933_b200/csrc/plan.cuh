@@ -137,6 +137,15 @@ struct Plan {
     // M2M chain, L2P of every ancestor instead of the L2L chain -- one
     // launch each instead of one per level (tree.cu, choose_passes).
     bool multilevel_up = false, multilevel_down = false;
+    // Adaptive trees (VPG_MODE_NATIVE, adaptive.cu): W-list M2P and X-list
+    // P2L work on top of the V (M2L) and U (near-field) lists.
+    bool adaptive = false;
+    DBuf<int4> m2p_work;    // (target begin, count, first W row, W count)
+    DBuf<int32_t> m2p_rows;
+    int64_t n_m2p_work = 0, m2p_evals = 0;
+    DBuf<int4> p2l_work;    // (receiving row, first range, range count, 0)
+    DBuf<int2> p2l_ranges;  // X-leaf source ranges
+    int64_t n_p2l_work = 0, p2l_sources = 0;
     std::vector<int64_t> m2m_first, m2m_count;  // into updown_boxes, per level
     std::vector<int64_t> l2l_first, l2l_count;
     DBuf<int32_t> updown_boxes;
@@ -170,6 +179,8 @@ struct Plan {
 void build_tree(Plan& pl);
 void build_schedules(Plan& pl, int64_t leaf_begin, int64_t leaf_end);
 void choose_passes(Plan& pl);
+// adaptive.cu
+void build_adaptive(Plan& pl, cudaStream_t st);
 // fmm.cu
 void build_laplace_ops(Plan& pl);
 void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,

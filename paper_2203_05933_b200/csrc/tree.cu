@@ -258,15 +258,14 @@ void build_tree(Plan& pl) {
     if (pl.direct) return;
 
     const double big = double(std::max(pl.ns, pl.nt));
-    if (pl.mode == VPG_MODE_REFERENCE) {
-        pl.L = std::clamp(int(std::ceil(std::log(big / 32.0) / std::log(4.0))), 2, 7);
-    } else {
-        // NATIVE: same leaf-size target, depth cap lifted to 9 levels.
-        pl.L = std::clamp(int(std::ceil(std::log(big / 32.0) / std::log(4.0))), 2, 9);
-    }
     pl.x0 = bb.x;
     pl.y0 = bb.z;
     pl.side = side * (1.0 + 1e-12);
+    if (pl.mode == VPG_MODE_NATIVE && pl.family == VPG_LAPLACE) {
+        build_adaptive(pl, st);  // adaptive quadtree + U/V/W/X lists (adaptive.cu)
+        return;
+    }
+    pl.L = std::clamp(int(std::ceil(std::log(big / 32.0) / std::log(4.0))), 2, 7);
     const int L = pl.L;
     const int64_t nleaf = int64_t(1) << (2 * L);
     const int64_t nall = lvl_base(L + 1);

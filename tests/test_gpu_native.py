@@ -1,0 +1,137 @@
+"""NATIVE mode: the adaptive quadtree FMM (adaptive.cu + the M2P/P2L passes
+in fmm.cu) against long-double direct sums from the oracle.
+
+The reference has no adaptive tree (its depth is clamped to 7,
+summation.cpp:560-567), so the oracle here is the exact pairwise sum
+(summation.cpp:501-540 semantics: coincident pairs skipped), and the bar is
+the requested epsilon.  The point sets stress the parts a uniform tree never
+exercises: deep refinement (depth > 7), W/X lists (leaves of very different
+sizes side by side), targets far from every source, and coincident points.
+"""
+import numpy as np
+import pytest
+
+from conftest import rel_l2
+from paper_2203_05933_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+def lap(vp):
+    return vp.make_kernel(vp.KernelFamily.Laplace)
+
+
+def native(vp, src, tgt, q, eps=1e-12):
+    with vp.SummationPlan(lap(vp), src, tgt, eps, mode="native") as plan:
+        out = plan.apply(q)
+        again = plan.apply(q)
+        info = plan.info()
+    assert np.array_equal(out, again)  # run-to-run bit identical
+    return out, info
+
+
+def check(rest, src, q, tgt, out, eps, nsample=1500, seed=0):
+    idx = np.random.default_rng(seed).choice(len(tgt), min(nsample, len(tgt)), replace=False)
+    ld = rest.pairwise_ld(0, 0.0, src, q, tgt[idx])
+    err = rel_l2(out[idx], ld)
+    assert err <= eps, f"rel l2 {err:.3e} > {eps:.0e}"
+    return err
+
+
+def clusters(rng, n, centres, widths, background=0.1):
+    nb = int(n * background)
+    parts = [rng.uniform(-1, 1, (nb, 2))]
+    per = (n - nb) // len(centres)
+    for c, w in zip(centres, widths):
+        parts.append(np.asarray(c) + w * rng.standard_normal((per, 2)))
+    return np.concatenate(parts)
+
+
+def test_cfg3_native(vp, rest):
+    w = W.cfg3()
+    out, info = native(vp, w.src, w.tgt, w.q)
+    assert info["levels"] > 7  # deeper than the reference's clamp
+    check(rest, w.src, w.q, w.tgt, out, 1e-12, nsample=600)
+
+
+@pytest.mark.parametrize("eps", [1e-12, 1e-9, 1e-6])
+def test_clustered_sources_and_targets(vp, rest, eps):
+    rng = np.random.default_rng(31)
+    src = clusters(rng, 120_000, [(0.3, 0.2), (-0.5, -0.4), (0.6, -0.7)], [1e-3, 2e-2, 1e-4])
+    tgt = clusters(rng, 90_000, [(0.3, 0.2), (-0.1, 0.5)], [5e-3, 1e-1])
+    q = rng.standard_normal(len(src))
+    out, info = native(vp, src, tgt, q, eps)
+    check(rest, src, q, tgt, out, eps)
+
+
+def test_tiny_source_disk_uniform_targets(vp, rest):
+    """All sources in a disk of radius 1e-4: the targets' leaves are coarse
+    and see the source cluster through W (M2P) and V lists only."""
+    rng = np.random.default_rng(32)
+    src = np.array([0.2, -0.1]) + 1e-4 * rng.uniform(-1, 1, (50_000, 2))
+    tgt = rng.uniform(-1, 1, (40_000, 2))
+    q = rng.uniform(0.5, 1.5, len(src))
+    out, _ = native(vp, src, tgt, q)
+    check(rest, src, q, tgt, out, 1e-12)
+
+
+def test_tiny_target_disk_uniform_sources(vp, rest):
+    """The mirror case: coarse source leaves next to a deep target cluster
+    reach it through X (P2L) lists."""
+    rng = np.random.default_rng(33)
+    src = rng.uniform(-1, 1, (40_000, 2))
+    tgt = np.array([-0.3, 0.4]) + 1e-4 * rng.uniform(-1, 1, (50_000, 2))
+    q = rng.standard_normal(len(src))
+    out, _ = native(vp, src, tgt, q)
+    check(rest, src, q, tgt, out, 1e-12)
+
+
+def test_coincident_points_skipped(vp, rest):
+    """targets == sources: every self pair is skipped, as in the reference
+    near field (summation.cpp:340)."""
+    rng = np.random.default_rng(34)
+    src = clusters(rng, 80_000, [(0.1, 0.1), (-0.6, 0.3)], [3e-3, 5e-2])
+    q = rng.standard_normal(len(src))
+    out, _ = native(vp, src, src, q)
+    check(rest, src, q, src, out, 1e-12)
+
+
+def test_geometric_line_depth_cap(vp, rest):
+    """Points accumulating geometrically at a corner: the tree hits the depth
+    cap (16) and the deepest leaves hold more than the leaf capacity."""
+    rng = np.random.default_rng(35)
+    t = 0.5 ** rng.uniform(0, 30, 30_000)
+    src = np.stack([t, 0.5 * t + 1e-3 * rng.uniform(0, 1, t.size) * t], 1)
+    q = rng.standard_normal(len(src))
+    out, info = native(vp, src, src, q)
+    assert info["levels"] == 16
+    check(rest, src, q, src, out, 1e-12)
+
+
+def test_native_matches_reference_mode_uniform(vp):
+    """On a uniform node set both trees are accurate: the two modes agree to
+    well below epsilon."""
+    w = W.cfg1()
+    with vp.SummationPlan(lap(vp), w.src, w.tgt, 1e-12) as plan:
+        ref = plan.apply(w.q)
+    out, _ = native(vp, w.src, w.tgt, w.q)
+    assert rel_l2(out, ref) <= 1e-12
+
+
+def test_native_plan_rebuild_bit_identical(vp):
+    rng = np.random.default_rng(36)
+    src = clusters(rng, 30_000, [(0.0, 0.0)], [1e-2])
+    q = rng.standard_normal(len(src))
+    a, _ = native(vp, src, src, q)
+    b, _ = native(vp, src, src, q)
+    assert np.array_equal(a, b)
+
+
+def test_native_rejects_uniform_only_queries(vp):
+    rng = np.random.default_rng(37)
+    src = rng.uniform(-1, 1, (20_000, 2))
+    with vp.SummationPlan(lap(vp), src, src, 1e-12, mode="native") as plan:
+        with pytest.raises(vp.InvalidArgument):
+            plan.set_shard(0, 1)
+        with pytest.raises(vp.InvalidArgument):
+            plan.dump_m2l(2)

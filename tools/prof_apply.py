@@ -16,11 +16,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="cfg2")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--eps", type=float, default=1e-12)
+ap.add_argument("--mode", default="reference")
 a = ap.parse_args()
 w = W.CONFIGS[a.workload]()
 k = vp.make_kernel(vp.KernelFamily.ModifiedHelmholtz, w.lam) if w.kernel == "helmholtz" else \
     vp.make_kernel(vp.KernelFamily.Laplace)
-plan = vp.SummationPlan(k, w.src, w.tgt, a.eps)
+plan = vp.SummationPlan(k, w.src, w.tgt, a.eps, mode=a.mode)
 q = torch.from_numpy(w.q).cuda()
 out = torch.empty(w.nt, dtype=torch.float64, device="cuda")
 s = torch.cuda.current_stream().cuda_stream
