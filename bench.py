@@ -74,6 +74,10 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 5.0 and self.proc.poll() is None:
+                time.sleep(0.02)  # first sample in before the load starts
+            self.rows.clear()
         except OSError:
             self.proc = None
         return self
@@ -228,10 +232,20 @@ def run_gpu(args):
     def step():
         plan.apply_device(q_d.data_ptr(), out_d.data_ptr(), sh)
 
+    # clocks are sampled (every 100 ms) from the first warm-up step to the end
+    # of the timed region; untimed steps keep the GPU loaded for >= 0.5 s
+    # first, so the samples see clocks under load
+    clk = ClockSampler(local).__enter__()
     for _ in range(args.warmup):
         flush.zero_()
         step()
     torch.cuda.synchronize()
+    t_hold = time.time()
+    while time.time() - t_hold < 0.5:
+        for _ in range(8):
+            flush.zero_()
+            step()
+        torch.cuda.synchronize()
 
     # ---- timed region: K device-resident steps, L2 flushed between steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -239,13 +253,13 @@ def run_gpu(args):
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        for i in range(args.steps):
-            flush.zero_()
-            ev[i][0].record(stream)
-            step()
-            ev[i][1].record(stream)
-        torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    clk.__exit__(None, None, None)
     if dist:
         dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in ev]

@@ -36,6 +36,7 @@ namespace {
 
 constexpr int kDepth = 16;     // 32-bit Morton keys
 constexpr int kLeafCap = 64;   // points per leaf (sources or targets)
+constexpr int kL2PChainCap = 256;  // rows with more targets push their local down (L2L)
 
 inline unsigned nblk(int64_t n, int t) { return unsigned((n + t - 1) / t); }
 
@@ -299,7 +300,7 @@ void sort_by_key16(const double2* pts, int64_t n, const Plan& pl, DBuf<uint32_t>
 
 void build_adaptive(Plan& pl, cudaStream_t st) {
     pl.adaptive = true;
-    pl.multilevel_up = pl.multilevel_down = true;
+    pl.multilevel_up = pl.multilevel_down = false;  // hybrid passes (schedules below)
     DBuf<uint32_t> sk, tk;
     sort_by_key16(pl.src.p, pl.ns, pl, sk, pl.src_ids, pl.src_sorted, st);
     sort_by_key16(pl.tgt.p, pl.nt, pl, tk, pl.tgt_ids, pl.tgt_sorted, st);
@@ -484,19 +485,76 @@ void build_adaptive(Plan& pl, cudaStream_t st) {
 
     // ---- schedules
     {
-        // P2M at every level >= 2 (multilevel upward pass)
+        // Upward pass, hybrid: a row with at most kP2MItemCap sources gets its
+        // multipole by P2M straight from its points (one warp item); a larger
+        // non-leaf row by M2M from its children, level by level bottom-up
+        // (cooperative shift kernel).  Each point then feeds ~2 rows instead
+        // of every ancestor.  Oversized leaves (depth cap) are split into
+        // items and reduced.
         std::vector<P2MItem> items;
         std::vector<P2MSplit> splits;
         for (int64_t r = 0; r < nrows; ++r) {
             const int l = h_level[size_t(r)];
             const int4 g = h_rng[size_t(r)];
             if (l < 2 || g.y <= g.x) continue;
+            if (h_first[size_t(r)] >= 0 && g.y - g.x > kP2MItemCap) continue;  // M2M
             const int32_t pieces = (g.y - g.x + kP2MItemCap - 1) / kP2MItemCap;
             if (pieces > 1) splits.push_back(P2MSplit{int32_t(r), int32_t(items.size()), pieces});
             for (int32_t e = g.x; e < g.y; e += kP2MItemCap)
                 items.push_back(P2MItem{l, h_morton[size_t(r)], int32_t(r), e, std::min(g.y, e + kP2MItemCap),
                                         pieces == 1 ? 1 : 0});
         }
+        // M2M parents (bottom-up) then L2L parents (top-down), per level
+        std::vector<int32_t> boxes;
+        std::vector<int4> kids;
+        pl.m2m_first.assign(size_t(depth + 1), 0);
+        pl.m2m_count.assign(size_t(depth + 1), 0);
+        pl.l2l_first.assign(size_t(depth + 1), 0);
+        pl.l2l_count.assign(size_t(depth + 1), 0);
+        pl.m2m_children = pl.l2l_children = 0;
+        auto children = [&](int64_t r, bool tgt, int64_t& nkids) {
+            int k4[4] = {-1, -1, -1, -1};
+            for (int c = 0, k = 0; c < 4; ++c)
+                if (h_cmask[size_t(r)] & (1 << c)) {
+                    const int32_t cr = h_first[size_t(r)] + k++;
+                    const int4 gc = h_rng[size_t(cr)];
+                    if (tgt ? gc.w > gc.z : gc.y > gc.x) {
+                        k4[c] = cr;
+                        ++nkids;
+                    }
+                }
+            return make_int4(k4[0], k4[1], k4[2], k4[3]);
+        };
+        for (int l = 2; l < depth; ++l) {
+            pl.m2m_first[size_t(l)] = int64_t(boxes.size());
+            for (int64_t r = lvl_first[size_t(l)]; r < lvl_first[size_t(l + 1)]; ++r) {
+                const int4 g = h_rng[size_t(r)];
+                if (h_first[size_t(r)] < 0 || g.y - g.x <= kP2MItemCap) continue;
+                boxes.push_back(int32_t(r));
+                kids.push_back(children(r, false, pl.m2m_children));
+            }
+            pl.m2m_count[size_t(l)] = int64_t(boxes.size()) - pl.m2m_first[size_t(l)];
+        }
+        std::vector<char> pushed(size_t(nrows), 0);
+        for (int l = 2; l < depth; ++l) {
+            pl.l2l_first[size_t(l)] = int64_t(boxes.size());
+            for (int64_t r = lvl_first[size_t(l)]; r < lvl_first[size_t(l + 1)]; ++r) {
+                const int4 g = h_rng[size_t(r)];
+                if (h_first[size_t(r)] < 0 || g.w - g.z <= kL2PChainCap) continue;
+                pushed[size_t(r)] = 1;
+                boxes.push_back(int32_t(r));
+                kids.push_back(children(r, true, pl.l2l_children));
+            }
+            pl.l2l_count[size_t(l)] = int64_t(boxes.size()) - pl.l2l_first[size_t(l)];
+        }
+        std::vector<int32_t> chain(size_t(nrows), -1);
+        for (int64_t r = 0; r < nrows; ++r) {
+            const int32_t p = h_parent[size_t(r)];
+            chain[size_t(r)] = (p >= 0 && !pushed[size_t(p)]) ? p : -1;
+        }
+        h2d(pl.updown_boxes, boxes, st);
+        h2d(pl.updown_kids, kids, st);
+        h2d(pl.row_chain, chain, st);
         pl.n_p2m_items = int64_t(items.size());
         pl.n_p2m_splits = int64_t(splits.size());
         h2d(pl.p2m_items, items, st);

@@ -113,7 +113,7 @@ int64_t Plan::device_bytes() const {
                    m2l_src.bytes() + m2l_oidx.bytes() + m2l_batches.bytes() + m2m_ops.bytes() +
                    l2l_ops.bytes() + h_t.bytes() + dpow.bytes() + logmd.bytes() +
                    p2p_chunks.bytes() + near_ranges.bytes() + row_level.bytes() + row_morton.bytes() +
-                   row_parent.bytes() + tgt_row.bytes() + p2m_items.bytes() + p2m_splits.bytes() + updown_boxes.bytes() +
+                   row_parent.bytes() + tgt_row.bytes() + p2m_items.bytes() + p2m_splits.bytes() + updown_boxes.bytes() + updown_kids.bytes() + row_chain.bytes() +
                    helm_nodes.bytes() + helm_bw.bytes() + exp_off_dev.bytes());
 }
 

@@ -121,23 +121,39 @@ p2m_kernel(const P2MItem* items, int64_t nitems, const int32_t* sorted_unused,
 }
 
 // Boxes split over several P2M items: sum the item partials in item order.
-__global__ void p2m_reduce_kernel(const P2MSplit* splits, int64_t nsplit, const double2* partial,
-                                  int P, double2* mult) {
+// One CTA per split row: kRedGroups groups of 64 threads stride over the
+// pieces (coefficient k on thread k of a group), then the group partials are
+// added in group order -- a fixed order, so results are run-to-run
+// identical.  (Level-2 rows of a million-point tree have ~10^3 pieces; a
+// serial walk per coefficient was latency bound.)
+constexpr int kRedGroups = 8;
+
+__global__ void __launch_bounds__(kRedGroups * 64)
+p2m_reduce_kernel(const P2MSplit* splits, const double2* partial, int P, double2* mult) {
+    __shared__ double2 part[kRedGroups][64];
     pdl_trigger();
     pdl_wait();
     const int n = P + 1;
-    const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-    if (i >= nsplit * n) return;
-    const int64_t sp = i / n;
-    const int k = int(i - sp * n);
-    const P2MSplit b = splits[sp];
+    const P2MSplit b = splits[blockIdx.x];
+    const int k = threadIdx.x & 63, g = threadIdx.x >> 6;
     double2 acc = make_double2(0.0, 0.0);
-    for (int t = 0; t < b.count; ++t) {
-        const double2 v = partial[int64_t(b.first + t) * n + k];
-        acc.x += v.x;
-        acc.y += v.y;
+    if (k < n) {
+#pragma unroll 4
+        for (int t = g; t < b.count; t += kRedGroups) {
+            const double2 v = partial[int64_t(b.first + t) * n + k];
+            acc.x += v.x;
+            acc.y += v.y;
+        }
     }
-    mult[int64_t(b.row) * n + k] = acc;
+    part[g][k] = acc;
+    __syncthreads();
+    if (g == 0 && k < n) {
+        for (int i = 1; i < kRedGroups; ++i) {
+            acc.x += part[i][k].x;
+            acc.y += part[i][k].y;
+        }
+        mult[int64_t(b.row) * n + k] = acc;
+    }
 }
 
 // ------------------------------------------------------------ M2M / L2L --
@@ -165,6 +181,7 @@ struct ShiftLevels {
     const int32_t* parents[kMaxShiftLevels];
     int64_t nparents[kMaxShiftLevels];
     const int32_t* cnt_child[kMaxShiftLevels];
+    const int4* kids[kMaxShiftLevels];  // adaptive: child rows per quadrant (else nullptr)
     const double2* in_level[kMaxShiftLevels];
     double2* out_level[kMaxShiftLevels];
 };
@@ -184,6 +201,10 @@ __device__ __forceinline__ void grid_barrier(unsigned* count, unsigned& target) 
         } while (v < target);
     }
     __syncthreads();
+}
+
+__device__ __forceinline__ int quad(const int4& v, int c) {
+    return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
 }
 
 template <bool kUp>
@@ -210,6 +231,7 @@ shift_kernel(ShiftLevels lv, const double2* ops_t, int P, unsigned* gbar) {
         const int32_t* parents = lv.parents[li];
         const int64_t np = lv.nparents[li];
         const int32_t* cnt_child = lv.cnt_child[li];
+        const int4* kids = lv.kids[li];
         const double2* in_level = lv.in_level[li];
         double2* out_level = lv.out_level[li];
         for (int64_t g0 = int64_t(blockIdx.x) * kShiftGroup; g0 < np; g0 += int64_t(gridDim.x) * kShiftGroup) {
@@ -218,8 +240,16 @@ shift_kernel(ShiftLevels lv, const double2* ops_t, int P, unsigned* gbar) {
             if (kUp) {
                 for (int i = threadIdx.x; i < ng * 4 * n; i += blockDim.x) {
                     const int gg = i / (4 * n), rem = i % (4 * n), c = rem / n, kk = rem % n;
-                    const int64_t child = (int64_t(parents[g0 + gg]) << 2) | c;
-                    vec[i] = cnt_child[child] > 0 ? __ldcg(in_level + child * n + kk) : make_double2(0.0, 0.0);
+                    int64_t child;
+                    bool has;
+                    if (kids) {
+                        child = quad(kids[g0 + gg], c);
+                        has = child >= 0;
+                    } else {
+                        child = (int64_t(parents[g0 + gg]) << 2) | c;
+                        has = cnt_child[child] > 0;
+                    }
+                    vec[i] = has ? __ldcg(in_level + child * n + kk) : make_double2(0.0, 0.0);
                 }
             } else {
                 for (int i = threadIdx.x; i < ng * n; i += blockDim.x) {
@@ -266,8 +296,14 @@ shift_kernel(ShiftLevels lv, const double2* ops_t, int P, unsigned* gbar) {
                 } else {
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
-                        const int64_t child = (parent << 2) | c;
-                        if (cnt_child[child] == 0) continue;
+                        int64_t child;
+                        if (kids) {
+                            child = quad(kids[g0 + g], c);
+                            if (child < 0) continue;
+                        } else {
+                            child = (parent << 2) | c;
+                            if (cnt_child[child] == 0) continue;
+                        }
                         double2* dst = out_level + child * n + r;
                         double2 d = __ldcg(dst);
                         d.x += yr[c];
@@ -1178,8 +1214,8 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
         ++launches;
     }
     if (pl.n_p2m_splits > 0) {
-        launch_pdl(p2m_reduce_kernel, dim3(nblk(pl.n_p2m_splits * n, 256)), dim3(256), 0, st,
-                   (const P2MSplit*)pl.p2m_splits.p, pl.n_p2m_splits, (const double2*)partial, P, mult);
+        launch_pdl(p2m_reduce_kernel, dim3(unsigned(pl.n_p2m_splits)), dim3(kRedGroups * 64), 0, st,
+                   (const P2MSplit*)pl.p2m_splits.p, (const double2*)partial, P, mult);
         ++launches;
         VPG_CUDA(cudaFreeAsync(partial, st));
     }
@@ -1188,7 +1224,24 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
     const size_t down_smem = sizeof(double2) * size_t(4 * n * n + kShiftGroup * n);
     const double2* m2m_ops = reinterpret_cast<const double2*>(pl.m2m_ops.p);
     const double2* l2l_ops = reinterpret_cast<const double2*>(pl.l2l_ops.p);
-    if (!pl.multilevel_up) {
+    if (pl.adaptive) {
+        ShiftLevels lv{};
+        for (int l = L - 1; l >= 2; --l) {
+            const int64_t np = pl.m2m_count[size_t(l)];
+            if (!np) continue;
+            lv.parents[lv.nlev] = pl.updown_boxes.p + pl.m2m_first[size_t(l)];
+            lv.kids[lv.nlev] = pl.updown_kids.p + pl.m2m_first[size_t(l)];
+            lv.nparents[lv.nlev] = np;
+            lv.in_level[lv.nlev] = mult;
+            lv.out_level[lv.nlev] = mult;
+            ++lv.nlev;
+        }
+        if (lv.nlev) {
+            launch_coop(shift_kernel<true>, pl.shift_grid, dim3(kShiftGroup * kRowSlots * kKSplit), up_smem, st,
+                        lv, m2m_ops, P, gbar + 0);
+            ++launches;
+        }
+    } else if (!pl.multilevel_up) {
         ShiftLevels lv{};
         for (int l = L - 1; l >= 2; --l) {
             const int64_t np = pl.m2m_count[size_t(l)];
@@ -1233,7 +1286,24 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
         ++launches;
     }
     mark(4);
-    if (!pl.multilevel_down) {
+    if (pl.adaptive) {
+        ShiftLevels lv{};
+        for (int l = 2; l < L; ++l) {
+            const int64_t np = pl.l2l_count[size_t(l)];
+            if (!np) continue;
+            lv.parents[lv.nlev] = pl.updown_boxes.p + pl.l2l_first[size_t(l)];
+            lv.kids[lv.nlev] = pl.updown_kids.p + pl.l2l_first[size_t(l)];
+            lv.nparents[lv.nlev] = np;
+            lv.in_level[lv.nlev] = loc;
+            lv.out_level[lv.nlev] = loc;
+            ++lv.nlev;
+        }
+        if (lv.nlev) {
+            launch_coop(shift_kernel<false>, pl.shift_grid, dim3(kShiftGroup * kRowSlots * kKSplit), down_smem,
+                        st, lv, l2l_ops, P, gbar + 1);
+            ++launches;
+        }
+    } else if (!pl.multilevel_down) {
         ShiftLevels lv{};
         for (int l = 2; l < L; ++l) {
             const int64_t np = pl.l2l_count[size_t(l)];
@@ -1256,7 +1326,8 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
         launch_pdl(l2p_kernel, dim3(nblk(pl.shard_t1 - pl.shard_t0, 256)), dim3(256), 0, st,
                    (const int32_t*)pl.tgt_row.p, pl.shard_t0, pl.shard_t1, (const double2*)pl.tgt_sorted.p,
                    (const double2*)loc, (const int32_t*)pl.row_level.p, (const int32_t*)pl.row_morton.p,
-                   (const int32_t*)pl.row_parent.p, pl.multilevel_down ? 1 : 0, P, pl.x0, pl.y0, pl.side,
+                   pl.adaptive ? (const int32_t*)pl.row_chain.p : (const int32_t*)pl.row_parent.p,
+                   (pl.adaptive || pl.multilevel_down) ? 1 : 0, P, pl.x0, pl.y0, pl.side,
                    pot_far, ticket);
         ++launches;
     }

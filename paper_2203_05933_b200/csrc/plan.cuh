@@ -149,6 +149,12 @@ struct Plan {
     std::vector<int64_t> m2m_first, m2m_count;  // into updown_boxes, per level
     std::vector<int64_t> l2l_first, l2l_count;
     DBuf<int32_t> updown_boxes;
+    // adaptive trees: child rows per quadrant (-1 = no child / empty) of the
+    // updown_boxes parents, and the L2P ancestor chain (next row whose local
+    // expansion a target still evaluates; -1 once the parent pushed its local
+    // down by L2L)
+    DBuf<int4> updown_kids;
+    DBuf<int32_t> row_chain;
 
     // Modified Helmholtz (treecode) state.
     int helm_min_level = 2;
