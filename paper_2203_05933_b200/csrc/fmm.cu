@@ -327,11 +327,14 @@ shift_kernel(ShiftLevels lv, const double2* ops_t, int P, unsigned* gbar) {
 //   y = H a~,  b_0 = y_0 + log(-d) a_0,  b_l = d^-l (y_l - a_0 / l).
 // A batch (<= kM2LPairs list entries of consecutive target boxes of one
 // level) becomes ONE dense real GEMM Y[RP x 2*pairs] = H[RP x P] X[P x
-// 2*pairs] (re and im columns).  Persistent CTAs (one per SM) keep H^T and
-// the offset power table d^-j (j <= P) resident in smem; per batch:
-//   1. X build: warp per list entry, lane per coefficient (coalesced rows);
-//   2. GEMM: 8x4 register micro-tile per thread, H rows broadcast, X
-//      columns interleaved (conflict-free);
+// 2*pairs] (re and im columns).  Persistent CTAs keep H^T and the canonical
+// offset power table c^-j (j <= P, 7 offsets up to the square's symmetry)
+// resident in smem; two batch groups of six warps per CTA, each:
+//   0. the NEXT batch's source rows arrive by 1-D TMA bulk copies
+//      (cp.async.bulk, mbarrier completion) while this batch computes;
+//   1. X build: warp per list entry, lane per coefficient;
+//   2. GEMM on the FP64 tensor cores: mma.sync m8n8k4 f64 (DMMA), warp w
+//      owns column tiles w, w+6, w+12, all row tiles in registers;
 //   3. epilogue in two passes: b = D'(y ...) per (entry, l) in place, then
 //      each target box sums its entries in list order and adds the monopole
 //      shift qsum*log(s_l) (summation.cpp:297-301).
