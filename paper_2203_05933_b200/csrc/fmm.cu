@@ -341,16 +341,11 @@ shift_kernel(ShiftLevels lv, const double2* ops_t, int P, unsigned* gbar) {
 // Executed flops per pair: 4 P (P+1) for the GEMM + O(P), half the dense
 // 8 (P+1)^2 of the reference matvec.
 constexpr int kM2LCols = 2 * kM2LPairs;          // 108 used columns
-constexpr int kM2LNTiles = (kM2LCols + 7) / 8;   // 14 DMMA column tiles
+static_assert((kM2LCols + 7) / 8 <= 2 * 7, "two column tiles per MMA warp");
 constexpr int kM2LXS = 116;                      // X/Y row stride (== 4 mod 16: conflict-free fragments)
 constexpr int kM2LHS = 60;                       // H^T row stride (== 12 mod 16)
-constexpr int kM2LGroupThreads = 192;            // six warps per batch group
-constexpr int kM2LGroupWarps = kM2LGroupThreads / 32;
-constexpr int kM2LGroups = 2;                    // two batches in flight per CTA
-constexpr int kM2LThreads = kM2LGroups * kM2LGroupThreads;
 constexpr int kM2LCanon = 7;                     // offsets up to the square's symmetry
 constexpr int kM2LMaxMT = 7;                     // RP <= 56
-constexpr int kM2LNTPerWarp = (kM2LNTiles + kM2LGroupWarps - 1) / kM2LGroupWarps;  // 3
 
 // Offset powers through the symmetry of the square: every interaction offset
 // d is u * conj^s(c) for a canonical c in {(2,0),(2,1),(2,2),(3,0),(3,1),
@@ -375,9 +370,6 @@ struct M2LStage {
     int32_t oidx[kM2LPairs];
 };
 
-__device__ __forceinline__ void group_sync(int g) {
-    asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(kM2LGroupThreads) : "memory");
-}
 
 __device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
@@ -385,31 +377,53 @@ __device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, doubl
                  : "d"(a), "d"(b));
 }
 
+// One warp stages a batch: list metadata into the ring slot, then the
+// source rows by 1-D TMA bulk copies completing on the batch's mbarrier.
 __device__ __forceinline__ void m2l_issue(const M2LBatch& bt, const int32_t* esrc,
                                           const int32_t* eoidx, const int32_t* omap_s,
                                           const double2* mult, int n, M2LStage* stg, double2* raw,
-                                          uint64_t* bar, int gtid) {
-    const double2* mlev = mult;  // list entries are expansion rows
-    if (gtid == 0) mbar_arrive_expect_tx(bar, uint32_t(bt.ecount) * uint32_t(n) * 16u);
-    if (gtid < bt.ecount) {
-        const int64_t e = int64_t(bt.efirst) + gtid;
-        const int sid = esrc[e];
-        const int o = eoidx[e];
-        stg->src[gtid] = sid;
-        stg->oidx[gtid] = o;
-        stg->omap[gtid] = omap_s[o];
-        tma_load_1d(raw + gtid * n, mlev + int64_t(sid) * n, uint32_t(n) * 16u, bar);
+                                          uint64_t* bar, int lane) {
+    for (int e = lane; e < bt.ecount; e += 32) {
+        const int64_t g = int64_t(bt.efirst) + e;
+        const int o = eoidx[g];
+        stg->src[e] = esrc[g];
+        stg->oidx[e] = o;
+        stg->omap[e] = omap_s[o];
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive_expect_tx(bar, uint32_t(bt.ecount) * uint32_t(n) * 16u);
+    __syncwarp();
+    for (int e = lane; e < bt.ecount; e += 32)
+        tma_load_1d(raw + e * n, mult + int64_t(stg->src[e]) * n, uint32_t(n) * 16u, bar);
 }
 
 // Factorised M2L (see the block comment above): per batch one dense real
 // GEMM Y = H X on the FP64 tensor cores (mma.sync m8n8k4, DMMA: 256 FMA per
 // warp instruction, measured 36.9 TFLOP/s on this B200 vs 34.2 for DFMA).
-// A CTA runs two independent batch groups of 192 threads (named barriers)
-// that share H^T, the canonical offset-power table and log(-d); each group
-// double-buffers its source rows with 1-D TMA bulk copies (mbarrier
-// completion) so the next batch lands while the current one computes.
-__global__ void __launch_bounds__(kM2LThreads, 1)
+// Warp-specialised, one CTA per SM, pipelined over the CTA's batches:
+//   warp 0      TMA producer: the source rows of batch i+2 are copied into
+//               staging buffer i%2 as soon as batch i has consumed it;
+//   warps 1-7   MMA: warp w owns the column tiles 2(w-1), 2(w-1)+1 (entries
+//               8(w-1) .. +7).  X is never materialised: each lane builds
+//               its B fragment (-1)^k d^-k a_k straight from the staged row,
+//               and the diagonal epilogue b_l = d^-l (y_l - a0/l) runs on
+//               the accumulators in registers (a lane holds re and im of one
+//               (l, entry)); b goes to the Y buffer i%2;
+//   warps 8-11  reduction: per target box and l, the entries' b in list
+//               order plus the monopole shift; frees Y buffer i%2.
+// The MMA warps only wait for the Y buffer right before their register
+// epilogue, so batch i+1's GEMM overlaps batch i's reduction.
+constexpr int kWSMMAWarps = 7;               // 14 column tiles, two per warp
+constexpr int kWSRedThreads = 128;
+constexpr int kWSThreads = 32 * (1 + kWSMMAWarps) + kWSRedThreads;
+constexpr int kWSStages = 4;                 // batch metadata ring
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int MT>  // row tiles: RP / 8
+__global__ void __launch_bounds__(kWSThreads, 1)
 m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
            const int32_t* toff, const int32_t* esrc, const int32_t* eoidx,
            const double* h_t, const double2* canon_g, const int32_t* omap_g,
@@ -417,26 +431,29 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
            double side) {
     extern __shared__ __align__(16) double smd[];
     const int n = P + 1;
-    const int XR = max(KP, n);                                  // X/Y rows
-    double* hs = smd;                                           // [KP][kM2LHS]
+    double* hs = smd;                                               // [KP][kM2LHS]
     double2* canon = reinterpret_cast<double2*>(hs + KP * kM2LHS);  // [7][n]
-    double2* logmd = canon + kM2LCanon * n;                     // [49]
-    int32_t* omap_s = reinterpret_cast<int32_t*>(logmd + 49);   // [49] (+pad)
-    char* gbase = reinterpret_cast<char*>(omap_s + 52);
-    const size_t gbytes = sizeof(double2) * (size_t(kM2LPairs) * n + kM2LPairs) +
-                          sizeof(double) * size_t(XR) * kM2LXS + 2 * sizeof(M2LStage);
-    __shared__ __align__(8) uint64_t bars[1 + kM2LGroups];
+    double2* logmd = canon + kM2LCanon * n;                         // [49]
+    int32_t* omap_s = reinterpret_cast<int32_t*>(logmd + 49);       // [49] (+pad)
+    double2* raw0 = reinterpret_cast<double2*>(omap_s + 52);        // [2][kM2LPairs][n]
+    double* yb0 = reinterpret_cast<double*>(raw0 + 2 * kM2LPairs * n);  // [2][n][kM2LXS]
+    double2* a0s0 = reinterpret_cast<double2*>(yb0 + 2 * n * kM2LXS);   // [2][kM2LPairs]
+    M2LStage* stg = reinterpret_cast<M2LStage*>(a0s0 + 2 * kM2LPairs);  // [kWSStages]
+    __shared__ __align__(8) uint64_t bars[7];
+    uint64_t* full = bars + 1;     // [2] source rows landed (TMA tx count)
+    uint64_t* mmadone = bars + 3;  // [2] rows consumed, Y written (MMA warps)
+    uint64_t* yfree = bars + 5;    // [2] Y consumed (reduction warps)
 
     const int tid = threadIdx.x;
-    const int g = tid / kM2LGroupThreads, gtid = tid % kM2LGroupThreads;
-    const int lane = gtid & 31, warp = gtid >> 5;
-    char* gp = gbase + size_t(g) * gbytes;
-    double2* raw = reinterpret_cast<double2*>(gp);
-    double* xy = reinterpret_cast<double*>(raw + kM2LPairs * n);
-    double2* a0s = reinterpret_cast<double2*>(xy + XR * kM2LXS);
-    M2LStage* stg = reinterpret_cast<M2LStage*>(a0s + kM2LPairs);
-    if (tid == 0)
-        for (int i = 0; i <= kM2LGroups; ++i) mbar_init(&bars[i], 1);
+    const int warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        for (int j = 0; j < 2; ++j) {
+            mbar_init(&full[j], 1);
+            mbar_init(&mmadone[j], 32 * kWSMMAWarps);
+            mbar_init(&yfree[j], kWSRedThreads);
+        }
+    }
     for (int i = tid; i < kM2LCanon * n; i += blockDim.x) canon[i] = canon_g[i];
     for (int i = tid; i < 49; i += blockDim.x) {
         logmd[i] = logmd_g[i];
@@ -448,131 +465,143 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
     pdl_trigger();
     pdl_wait();
 
-    uint64_t* bar = &bars[1 + g];
-    const int MT = RP / 8;
-    uint32_t phase = 0;
-    int cur = 0;
-    const int64_t stride = int64_t(gridDim.x) * kM2LGroups;
-    int64_t bi = int64_t(blockIdx.x) * kM2LGroups + g;
-    if (bi < nbatch)
-        m2l_issue(batches[bi], esrc, eoidx, omap_s, mult, n, &stg[0], raw, bar, gtid);
-
-    for (; bi < nbatch; bi += stride) {
-        const M2LBatch bt = batches[bi];
-        double2* llev = loc;  // target entries are expansion rows
-        const M2LStage& sg = stg[cur];
-        mbar_wait(bar, phase);
-        phase ^= 1u;
-        // 1. X[k-1][2p | 2p+1] = (-1)^k d^-k a_k (warp per entry, lane per k);
-        //    (-1)^k d^-k = i^((m+2)k) conj^s(c^-k)
-        for (int p = warp; p < bt.ecount; p += kM2LGroupWarps) {
-            const double2* rr = raw + p * n;
-            const int om = sg.omap[p];
-            const int ci = om & 7, sc = (om >> 3) & 1, m2 = ((om >> 4) & 3) + 2;
-            const double2* crow = canon + ci * n;
-            for (int k = lane; k <= P; k += 32) {
-                const double2 a = rr[k];
-                if (k == 0) {
-                    a0s[p] = a;
-                } else {
-                    const double2 d = turn(crow[k], (m2 * k) & 3, sc);
-                    double* xr = xy + (k - 1) * kM2LXS + 2 * p;
-                    xr[0] = a.x * d.x - a.y * d.y;
-                    xr[1] = a.x * d.y + a.y * d.x;
-                }
-            }
+    const int64_t stride = gridDim.x;
+    if (warp == 0) {
+        // ------------------------------------------------- TMA producer
+        for (int j = 0; j < 2; ++j) {
+            const int64_t bi = blockIdx.x + j * stride;
+            if (bi < nbatch)
+                m2l_issue(batches[bi], esrc, eoidx, omap_s, mult, n, &stg[j], raw0 + j * kM2LPairs * n,
+                          &full[j], lane);
         }
-        for (int i = gtid; i < (KP - P) * kM2LXS; i += kM2LGroupThreads) xy[P * kM2LXS + i] = 0.0;
-        group_sync(g);
-        // raw[] is free: start the next batch's copies under this GEMM
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        const int64_t bn = bi + stride;
-        if (bn < nbatch)
-            m2l_issue(batches[bn], esrc, eoidx, omap_s, mult, n, &stg[cur ^ 1], raw, bar, gtid);
-
-        // 2. DMMA GEMM: warp w owns column tiles w, w+6, w+12 and all row tiles
-        double acc[kM2LMaxMT][kM2LNTPerWarp][2];
+        for (int it = 0;; ++it) {
+            const int64_t bn = blockIdx.x + (it + 2) * stride;
+            if (bn >= nbatch) break;
+            const int j = it & 1;
+            mbar_wait(&mmadone[j], uint32_t(it >> 1) & 1u);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            m2l_issue(batches[bn], esrc, eoidx, omap_s, mult, n, &stg[(it + 2) % kWSStages],
+                      raw0 + j * kM2LPairs * n, &full[j], lane);
+        }
+    } else if (warp <= kWSMMAWarps) {
+        // ---------------------------------------------------------- MMA
+        const int w = warp - 1;
+        const int kq = lane & 3, rq = lane >> 2;
+        for (int it = 0;; ++it) {
+            const int64_t bi = blockIdx.x + it * stride;
+            if (bi >= nbatch) break;
+            const int j = it & 1;
+            const uint32_t use = uint32_t(it >> 1);
+            const M2LBatch bt = batches[bi];
+            const M2LStage& sg = stg[it % kWSStages];
+            const double2* raw = raw0 + j * kM2LPairs * n;
+            mbar_wait(&full[j], use & 1u);
+            // B-fragment sources: tile 2w+t, column 8(2w+t) + rq -> entry
+            // 4(2w+t) + rq/2, part rq&1; row k4 + kq <-> k = k4 + kq + 1
+            const double2* brow[2];
+            const double2* bcan[2];
+            int bm2[2], bsc[2];
+            bool blive[2];
 #pragma unroll
-        for (int i = 0; i < kM2LMaxMT; ++i)
+            for (int t = 0; t < 2; ++t) {
+                const int p = 4 * (2 * w + t) + (rq >> 1);
+                blive[t] = p < bt.ecount;
+                const int pp = blive[t] ? p : 0;
+                const int om = sg.omap[pp];
+                brow[t] = raw + pp * n;
+                bcan[t] = canon + (om & 7) * n;
+                bsc[t] = (om >> 3) & 1;
+                bm2[t] = ((om >> 4) & 3) + 2;
+            }
+            const bool im = rq & 1;
+            double acc[MT][2][2];
 #pragma unroll
-            for (int j = 0; j < kM2LNTPerWarp; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-        {
-            const int kq = lane & 3, rq = lane >> 2;
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+                for (int t = 0; t < 2; ++t) acc[i][t][0] = acc[i][t][1] = 0.0;
             const double* hcol = hs + kq * kM2LHS + rq;
-            const double* xcol = xy + kq * kM2LXS + rq;
-            for (int k4 = 0; k4 < KP; k4 += 4) {
-                double bfr[kM2LNTPerWarp];
+            if (8 * w < bt.ecount) {  // warp-uniform: the warp's first tile is in use
+#pragma unroll 2
+                for (int k4 = 0; k4 < KP; k4 += 4) {
+                    double afr[MT];
 #pragma unroll
-                for (int j = 0; j < kM2LNTPerWarp; ++j) {
-                    const int nt = warp + kM2LGroupWarps * j;
-                    bfr[j] = nt < kM2LNTiles ? xcol[k4 * kM2LXS + 8 * nt] : 0.0;
-                }
+                    for (int i = 0; i < MT; ++i) afr[i] = hcol[k4 * kM2LHS + 8 * i];
+                    // branch-free B fragments (mma.sync needs a converged warp)
+                    const int k = k4 + kq + 1;
+                    const int kc = min(k, P);
+                    double bfr[2];
 #pragma unroll
-                for (int i = 0; i < kM2LMaxMT; ++i) {
-                    if (i < MT) {
-                        const double afr = hcol[k4 * kM2LHS + 8 * i];
+                    for (int t = 0; t < 2; ++t) {
+                        const double2 a = brow[t][kc];
+                        const double2 d = turn(bcan[t][kc], (bm2[t] * kc) & 3, bsc[t]);
+                        const double v = im ? fma(a.x, d.y, a.y * d.x) : fma(a.x, d.x, -(a.y * d.y));
+                        bfr[t] = (blive[t] && k <= P) ? v : 0.0;
+                    }
 #pragma unroll
-                        for (int j = 0; j < kM2LNTPerWarp; ++j)
-                            if (warp + kM2LGroupWarps * j < kM2LNTiles)
-                                dmma_884(acc[i][j][0], acc[i][j][1], afr, bfr[j]);
+                    for (int i = 0; i < MT; ++i) {
+                        dmma_884(acc[i][0][0], acc[i][0][1], afr[i], bfr[0]);
+                        dmma_884(acc[i][1][0], acc[i][1][1], afr[i], bfr[1]);
                     }
                 }
             }
-        }
-        group_sync(g);  // everyone done reading X
-        {
-            const int r0 = lane >> 2, c0 = 2 * (lane & 3);
+            // register epilogue: lane holds (re, im) of row l = 8i + rq,
+            // entry p = 4(2w+t) + kq
+            if (it >= 2) mbar_wait(&yfree[j], (use - 1u) & 1u);
+            double* yb = yb0 + j * n * kM2LXS;
+            double2* a0s = a0s0 + j * kM2LPairs;
 #pragma unroll
-            for (int i = 0; i < kM2LMaxMT; ++i) {
-                const int l = 8 * i + r0;
-                if (i < MT && l <= P)
+            for (int t = 0; t < 2; ++t) {
+                const int p = 4 * (2 * w + t) + kq;
+                if (p < bt.ecount) {
+                    const double2 a0 = raw[p * n];
+                    const int om = sg.omap[p];
+                    const int ci = om & 7, sc = (om >> 3) & 1, m = (om >> 4) & 3;
+                    if (rq == 0) a0s[p] = a0;
 #pragma unroll
-                    for (int j = 0; j < kM2LNTPerWarp; ++j) {
-                        const int nt = warp + kM2LGroupWarps * j;
-                        if (nt < kM2LNTiles) {
-                            double* y = xy + l * kM2LXS + 8 * nt + c0;
-                            y[0] = acc[i][j][0];
-                            y[1] = acc[i][j][1];
+                    for (int i = 0; i < MT; ++i) {
+                        const int l = 8 * i + rq;
+                        if (l <= P) {
+                            const double yr = acc[i][t][0], yi = acc[i][t][1];
+                            double br, bim;
+                            if (l == 0) {
+                                const double2 lg = logmd[sg.oidx[p]];
+                                br = yr + (lg.x * a0.x - lg.y * a0.y);
+                                bim = yi + (lg.x * a0.y + lg.y * a0.x);
+                            } else {
+                                const double inv_l = c_neg_inv_k[l];  // -1/l
+                                const double zr = fma(inv_l, a0.x, yr), zi = fma(inv_l, a0.y, yi);
+                                const double2 dl = turn(canon[ci * n + l], (m * l) & 3, sc);
+                                br = dl.x * zr - dl.y * zi;
+                                bim = dl.x * zi + dl.y * zr;
+                            }
+                            *reinterpret_cast<double2*>(yb + l * kM2LXS + 2 * p) = make_double2(br, bim);
                         }
                     }
-            }
-        }
-        group_sync(g);
-        // 3a. per (row l, entry p): b_0 = y_0 + log(-d) a_0,
-        //     b_l = d^-l (y_l - a_0 / l), in place
-        for (int l = warp; l <= P; l += kM2LGroupWarps) {
-            const double inv_l = l > 0 ? c_neg_inv_k[l] : 0.0;  // -1/l
-            double* yrow = xy + l * kM2LXS;
-            for (int p = lane; p < bt.ecount; p += 32) {
-                const double yr = yrow[2 * p], yi = yrow[2 * p + 1];
-                const double2 a0 = a0s[p];
-                const int om = sg.omap[p];
-                double br, bim;
-                if (l == 0) {
-                    const double2 lg = logmd[sg.oidx[p]];
-                    br = yr + (lg.x * a0.x - lg.y * a0.y);
-                    bim = yi + (lg.x * a0.y + lg.y * a0.x);
-                } else {
-                    const double zr = fma(inv_l, a0.x, yr), zi = fma(inv_l, a0.y, yi);
-                    const double2 dl = turn(canon[(om & 7) * n + l], (((om >> 4) & 3) * l) & 3, (om >> 3) & 1);
-                    br = dl.x * zr - dl.y * zi;
-                    bim = dl.x * zi + dl.y * zr;
                 }
-                yrow[2 * p] = br;
-                yrow[2 * p + 1] = bim;
             }
+            mbar_arrive(&mmadone[j]);
         }
-        group_sync(g);
-        // 3b. per (target t, row l): sum the entries in list order and add
-        //     the monopole shift (summation.cpp:297-301)
-        const double logs = log(side / double(1 << bt.level));
-        {
-            const int l = gtid & 63;
+    } else {
+        // ---------------------------------------------------- reduction
+        const int rtid = tid - 32 * (1 + kWSMMAWarps);
+        for (int it = 0;; ++it) {
+            const int64_t bi = blockIdx.x + it * stride;
+            if (bi >= nbatch) break;
+            const int j = it & 1;
+            const uint32_t use = uint32_t(it >> 1);
+            const M2LBatch bt = batches[bi];
+            const double* yb = yb0 + j * n * kM2LXS;
+            const double2* a0s = a0s0 + j * kM2LPairs;
+            mbar_wait(&mmadone[j], use & 1u);
+            // per (target t, row l): entries summed in list order, plus the
+            // monopole shift (summation.cpp:297-301)
+            const double logs = log(side / double(1 << bt.level));
+            const int l = rtid & 63;
             if (l <= P)
-                for (int t = gtid >> 6; t < bt.tcount; t += kM2LGroupThreads >> 6) {
+                for (int t = rtid >> 6; t < bt.tcount; t += kWSRedThreads >> 6) {
                     const int64_t tg = int64_t(bt.tfirst) + t;
                     const int p0 = toff[tg] - bt.efirst, p1 = toff[tg + 1] - bt.efirst;
-                    const double* yrow = xy + l * kM2LXS;
+                    const double* yrow = yb + l * kM2LXS;
                     double sr = 0.0, si = 0.0, qsum = 0.0;
 #pragma unroll 4
                     for (int p = p0; p < p1; ++p) {
@@ -581,11 +610,25 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
                         if (l == 0) qsum += a0s[p].x;
                     }
                     if (l == 0) sr += qsum * logs;
-                    llev[int64_t(tbox[tg]) * n + l] = make_double2(sr, si);
+                    loc[int64_t(tbox[tg]) * n + l] = make_double2(sr, si);
                 }
+            mbar_arrive(&yfree[j]);
         }
-        cur ^= 1;
-        group_sync(g);  // xy / a0s reused by the next batch
+    }
+}
+
+using M2LKernel = void (*)(const M2LBatch*, int64_t, const int32_t*, const int32_t*, const int32_t*,
+                          const int32_t*, const double*, const double2*, const int32_t*, const double2*,
+                          const double2*, double2*, int, int, int, double);
+
+M2LKernel m2l_kernel_for(int mt) {
+    switch (mt) {
+        case 2: return m2l_kernel<2>;
+        case 3: return m2l_kernel<3>;
+        case 4: return m2l_kernel<4>;
+        case 5: return m2l_kernel<5>;
+        case 6: return m2l_kernel<6>;
+        default: return m2l_kernel<7>;
     }
 }
 
@@ -1155,7 +1198,7 @@ void build_laplace_ops(Plan& pl) {
     VPG_CUDA(cudaMemcpy(pl.exp_off_dev.p, pl.exp_off.data(), pl.exp_off_dev.bytes(),
                         cudaMemcpyHostToDevice));
 
-    smem_optin((const void*)m2l_kernel, 225 * 1024);
+    for (int mt = 2; mt <= kM2LMaxMT; ++mt) smem_optin((const void*)m2l_kernel_for(mt), 225 * 1024);
     smem_optin((const void*)p2m_kernel, 100 * 1024);
     smem_optin((const void*)p2l_kernel, 100 * 1024);
     smem_optin((const void*)shift_kernel<true>, 220 * 1024);
@@ -1197,7 +1240,6 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
                 if (x) cudaFreeAsync(x, s);
         }
     } fr{{qs, mult, loc, pot_far, ticket}, st};
-    const int64_t* exp_off_d = pl.exp_off_dev.p;
     unsigned* gbar = reinterpret_cast<unsigned*>(ticket) + 8;  // grid barriers of the shift passes
 
     mark(0);
@@ -1264,15 +1306,16 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
     }
     mark(3);
     if (pl.n_m2l_batches > 0) {
-        const int XR = std::max(pl.KP, n);
-        const size_t gbytes = sizeof(double2) * (size_t(kM2LPairs) * n + kM2LPairs) +
-                              sizeof(double) * size_t(XR) * kM2LXS + 2 * sizeof(M2LStage);
         const size_t smem = sizeof(double) * size_t(pl.KP) * kM2LHS +
                             sizeof(double2) * (size_t(kM2LCanon) * n + 49) + sizeof(int32_t) * 52 +
-                            kM2LGroups * gbytes;
-        const unsigned grid = unsigned(std::min<int64_t>((pl.n_m2l_batches + kM2LGroups - 1) / kM2LGroups,
-                                                         int64_t(pl.sm_count)));
-        launch_pdl(m2l_kernel, dim3(grid), dim3(kM2LThreads), smem, st,
+                            2 * (sizeof(double2) * (size_t(kM2LPairs) * n + kM2LPairs) +
+                                 sizeof(double) * size_t(n) * kM2LXS) +
+                            kWSStages * sizeof(M2LStage);
+        const unsigned grid = unsigned(std::min<int64_t>(pl.n_m2l_batches, int64_t(pl.sm_count)));
+        void (*kern)(const M2LBatch*, int64_t, const int32_t*, const int32_t*, const int32_t*,
+                     const int32_t*, const double*, const double2*, const int32_t*, const double2*,
+                     const double2*, double2*, int, int, int, double) = m2l_kernel_for(pl.RP / 8);
+        launch_pdl(kern, dim3(grid), dim3(kWSThreads), smem, st,
                    (const M2LBatch*)pl.m2l_batches.p, pl.n_m2l_batches, (const int32_t*)pl.m2l_tbox.p,
                    (const int32_t*)pl.m2l_toff.p, (const int32_t*)pl.m2l_src.p,
                    (const int32_t*)pl.m2l_oidx.p, (const double*)pl.h_t.p,
