@@ -341,7 +341,7 @@ shift_kernel(ShiftLevels lv, const double2* ops_t, int P, unsigned* gbar) {
 // Executed flops per pair: 4 P (P+1) for the GEMM + O(P), half the dense
 // 8 (P+1)^2 of the reference matvec.
 constexpr int kM2LCols = 2 * kM2LPairs;          // 108 used columns
-static_assert((kM2LCols + 7) / 8 <= 2 * 7, "two column tiles per MMA warp");
+static_assert((kM2LCols + 7) / 8 <= 14, "14 column tiles");
 constexpr int kM2LXS = 116;                      // X/Y row stride (== 4 mod 16: conflict-free fragments)
 constexpr int kM2LHS = 60;                       // H^T row stride (== 12 mod 16)
 constexpr int kM2LCanon = 7;                     // offsets up to the square's symmetry
@@ -403,17 +403,23 @@ __device__ __forceinline__ void m2l_issue(const M2LBatch& bt, const int32_t* esr
 // Warp-specialised, one CTA per SM, pipelined over the CTA's batches:
 //   warp 0      TMA producer: the source rows of batch i+2 are copied into
 //               staging buffer i%2 as soon as batch i has consumed it;
-//   warps 1-7   MMA: warp w owns the column tiles 2(w-1), 2(w-1)+1 (entries
-//               8(w-1) .. +7).  X is never materialised: each lane builds
-//               its B fragment (-1)^k d^-k a_k straight from the staged row,
-//               and the diagonal epilogue b_l = d^-l (y_l - a0/l) runs on
-//               the accumulators in registers (a lane holds re and im of one
+//   warps 1-14  MMA: warp w owns column tile w-1 (entries 4(w-1) .. +3).
+//               X is never materialised: each lane builds its B fragment
+//               (-1)^k d^-k a_k straight from the staged row, and the
+//               diagonal epilogue b_l = d^-l (y_l - a0/l) runs on the
+//               accumulators in registers (a lane holds re and im of one
 //               (l, entry)); b goes to the Y buffer i%2;
-//   warps 8-11  reduction: per target box and l, the entries' b in list
+//   warps 15-18 reduction: per target box and l, the entries' b in list
 //               order plus the monopole shift; frees Y buffer i%2.
 // The MMA warps only wait for the Y buffer right before their register
-// epilogue, so batch i+1's GEMM overlaps batch i's reduction.
-constexpr int kWSMMAWarps = 7;               // 14 column tiles, two per warp
+// epilogue, so batch i+1's GEMM overlaps batch i's reduction.  One column
+// tile per MMA warp keeps ~3 MMA warps per SM sub-partition for typical
+// batches (measured: 2 tiles per warp was 14% slower on cfg2).
+#ifndef VPG_M2L_TPW
+#define VPG_M2L_TPW 1
+#endif
+constexpr int kWSTPW = VPG_M2L_TPW;          // column tiles per MMA warp
+constexpr int kWSMMAWarps = 14 / kWSTPW;     // 14 column tiles
 constexpr int kWSRedThreads = 128;
 constexpr int kWSThreads = 32 * (1 + kWSMMAWarps) + kWSRedThreads;
 constexpr int kWSStages = 4;                 // batch metadata ring
@@ -496,15 +502,15 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
             const M2LStage& sg = stg[it % kWSStages];
             const double2* raw = raw0 + j * kM2LPairs * n;
             mbar_wait(&full[j], use & 1u);
-            // B-fragment sources: tile 2w+t, column 8(2w+t) + rq -> entry
-            // 4(2w+t) + rq/2, part rq&1; row k4 + kq <-> k = k4 + kq + 1
-            const double2* brow[2];
-            const double2* bcan[2];
-            int bm2[2], bsc[2];
-            bool blive[2];
+            // B-fragment sources: tile TPW w + t, column 8(TPW w + t) + rq ->
+            // entry 4(TPW w + t) + rq/2, part rq&1; row k4 + kq <-> k = k4 + kq + 1
+            const double2* brow[kWSTPW];
+            const double2* bcan[kWSTPW];
+            int bm2[kWSTPW], bsc[kWSTPW];
+            bool blive[kWSTPW];
 #pragma unroll
-            for (int t = 0; t < 2; ++t) {
-                const int p = 4 * (2 * w + t) + (rq >> 1);
+            for (int t = 0; t < kWSTPW; ++t) {
+                const int p = 4 * (kWSTPW * w + t) + (rq >> 1);
                 blive[t] = p < bt.ecount;
                 const int pp = blive[t] ? p : 0;
                 const int om = sg.omap[pp];
@@ -514,13 +520,13 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
                 bm2[t] = ((om >> 4) & 3) + 2;
             }
             const bool im = rq & 1;
-            double acc[MT][2][2];
+            double acc[MT][kWSTPW][2];
 #pragma unroll
             for (int i = 0; i < MT; ++i)
 #pragma unroll
-                for (int t = 0; t < 2; ++t) acc[i][t][0] = acc[i][t][1] = 0.0;
+                for (int t = 0; t < kWSTPW; ++t) acc[i][t][0] = acc[i][t][1] = 0.0;
             const double* hcol = hs + kq * kM2LHS + rq;
-            if (8 * w < bt.ecount) {  // warp-uniform: the warp's first tile is in use
+            if (4 * kWSTPW * w < bt.ecount) {  // warp-uniform: the warp's first tile is in use
 #pragma unroll 2
                 for (int k4 = 0; k4 < KP; k4 += 4) {
                     double afr[MT];
@@ -529,19 +535,19 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
                     // branch-free B fragments (mma.sync needs a converged warp)
                     const int k = k4 + kq + 1;
                     const int kc = min(k, P);
-                    double bfr[2];
+                    double bfr[kWSTPW];
 #pragma unroll
-                    for (int t = 0; t < 2; ++t) {
+                    for (int t = 0; t < kWSTPW; ++t) {
                         const double2 a = brow[t][kc];
                         const double2 d = turn(bcan[t][kc], (bm2[t] * kc) & 3, bsc[t]);
                         const double v = im ? fma(a.x, d.y, a.y * d.x) : fma(a.x, d.x, -(a.y * d.y));
                         bfr[t] = (blive[t] && k <= P) ? v : 0.0;
                     }
 #pragma unroll
-                    for (int i = 0; i < MT; ++i) {
-                        dmma_884(acc[i][0][0], acc[i][0][1], afr[i], bfr[0]);
-                        dmma_884(acc[i][1][0], acc[i][1][1], afr[i], bfr[1]);
-                    }
+                    for (int i = 0; i < MT; ++i)
+#pragma unroll
+                        for (int t = 0; t < kWSTPW; ++t)
+                            dmma_884(acc[i][t][0], acc[i][t][1], afr[i], bfr[t]);
                 }
             }
             // register epilogue: lane holds (re, im) of row l = 8i + rq,
@@ -550,8 +556,8 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
             double* yb = yb0 + j * n * kM2LXS;
             double2* a0s = a0s0 + j * kM2LPairs;
 #pragma unroll
-            for (int t = 0; t < 2; ++t) {
-                const int p = 4 * (2 * w + t) + kq;
+            for (int t = 0; t < kWSTPW; ++t) {
+                const int p = 4 * (kWSTPW * w + t) + kq;
                 if (p < bt.ecount) {
                     const double2 a0 = raw[p * n];
                     const int om = sg.omap[p];
