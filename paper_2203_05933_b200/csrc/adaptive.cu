@@ -484,6 +484,7 @@ void build_adaptive(Plan& pl, cudaStream_t st) {
     }
 
     // ---- schedules
+    std::vector<int32_t> chain;  // L2P chain: next row a target evaluates (-1: done)
     {
         // Upward pass, hybrid: a row with at most kP2MItemCap sources gets its
         // multipole by P2M straight from its points (one warp item); a larger
@@ -547,7 +548,7 @@ void build_adaptive(Plan& pl, cudaStream_t st) {
             }
             pl.l2l_count[size_t(l)] = int64_t(boxes.size()) - pl.l2l_first[size_t(l)];
         }
-        std::vector<int32_t> chain(size_t(nrows), -1);
+        chain.assign(size_t(nrows), -1);
         for (int64_t r = 0; r < nrows; ++r) {
             const int32_t p = h_parent[size_t(r)];
             chain[size_t(r)] = (p >= 0 && !pushed[size_t(p)]) ? p : -1;
@@ -564,6 +565,7 @@ void build_adaptive(Plan& pl, cudaStream_t st) {
         // near field: U lists as source ranges
         std::vector<P2PChunk> chunks;
         std::vector<int2> ranges;
+        std::vector<int32_t> lrows;
         pl.p2p_pairs = 0;
         int max_ranges = 0;
         for (int64_t r = 0; r < nrows; ++r) {
@@ -602,9 +604,12 @@ void build_adaptive(Plan& pl, cudaStream_t st) {
                 rself = rcount;
             }
             pl.p2p_pairs += int64_t(g.w - g.z) * nsrc;
+            const int32_t lfirst = int32_t(lrows.size());
+            for (int32_t c = int32_t(r); c >= 0; c = chain[size_t(c)]) lrows.push_back(c);
+            const int32_t lcount = int32_t(lrows.size()) - lfirst;
             for (int32_t t = g.z; t < g.w; t += 64)
                 chunks.push_back(P2PChunk{t, std::min(64, g.w - t), int32_t(std::min<int64_t>(nsrc, INT32_MAX)),
-                                          rfirst, int32_t(ranges.size()) - rfirst, rself});
+                                          rfirst, int32_t(ranges.size()) - rfirst, rself, lfirst, lcount});
         }
         if (max_ranges + 1 > kMaxNearRanges)
             throw Error{VPG_ERR_INVALID_ARGUMENT,
@@ -619,6 +624,7 @@ void build_adaptive(Plan& pl, cudaStream_t st) {
         pl.p2p_tpt = 2;
         h2d(pl.p2p_chunks, chunks, st);
         h2d(pl.near_ranges, ranges, st);
+        h2d(pl.l2p_rows, lrows, st);
     }
     {
         // M2P (W lists): chunks of 32 targets of a leaf

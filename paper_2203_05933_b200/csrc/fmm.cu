@@ -639,46 +639,84 @@ M2LKernel m2l_kernel_for(int mt) {
 }
 
 // ------------------------------------------------------------------ L2P --
-// One thread per (Morton-sorted) target: Horner of the leaf's local
-// expansion in u = (t-c)/s, pot = -(1/2pi) Re (summation.cpp:323-329).
-// Threads of one leaf read the same coefficients (L1 broadcast).  The
-// near-field kernel adds its sum on top (fixed order: far, then near).
-__global__ void __launch_bounds__(256)
-l2p_kernel(const int32_t* trow, int64_t t0, int64_t t1, const double2* txy, const double2* loc,
-           const int32_t* row_level, const int32_t* row_morton, const int32_t* row_parent,
-           int multilevel, int P, double x0, double y0, double side, double* pot_far, int* ticket) {
+// Warp per near-field chunk (<= 64 targets of one leaf, two per lane):
+// Horner of every local expansion on the leaf's L2P chain (the leaf after
+// the L2L pass, summation.cpp:323-329; in the multilevel / hybrid downward
+// passes also the ancestors whose locals were not pushed down), summed in
+// chain order, pot = -(1/2pi) Re.  A row is staged through a per-warp smem
+// slot with coalesced loads while the next row's coefficients are already
+// in flight (register prefetch).  Zeroes the near-field tickets.
+constexpr int kL2PWarps = 8;
+
+__global__ void __launch_bounds__(kL2PWarps * 32)
+l2p_kernel(const P2PChunk* chunks, int64_t nchunks, const int32_t* lrows, const double2* txy,
+           const double2* loc, const int32_t* row_level, const int32_t* row_morton, int P,
+           double x0, double y0, double side, double* pot_far, int* ticket) {
+    __shared__ double2 rowbuf[kL2PWarps][64];
     pdl_trigger();
     pdl_wait();
-    const int64_t e = t0 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-    if (e == t0) {  // near-field work counters for l2p_p2p_kernel
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // near-field work counters for l2p_p2p_kernel
         ticket[0] = 0;
         ticket[1] = 0;
     }
-    if (e >= t1) return;
-    const double2 t = txy[e];
-    // The leaf's local expansion (after the L2L chain: summation.cpp:323-329)
-    // or, in the multilevel downward pass, the leaf's and every ancestor's
-    // (M2L / P2L contributions per level, no L2L), summed fine to coarse.
-    double sum = 0.0;
-    for (int r = trow[e]; r >= 0; r = multilevel ? row_parent[r] : -1) {
-        const int l = row_level[r];
-        const double s = side / double(1 << l);
-        double cx, cy;
-        box_center(x0, y0, s, uint32_t(row_morton[r]), cx, cy);
-        const double inv_s = 1.0 / s;
-        const double ur = (t.x - cx) * inv_s, ui = (t.y - cy) * inv_s;
-        const double2* ab = loc + int64_t(r) * (P + 1);
-        double vr = ab[P].x, vi = ab[P].y;
-        for (int k = P - 1; k >= 0; --k) {
-            const double2 a = ab[k];
-            const double nr = fma(vr, ur, fma(-vi, ui, a.x));
-            const double ni = fma(vr, ui, fma(vi, ur, a.y));
-            vr = nr;
-            vi = ni;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int n = P + 1;
+    double2* buf = rowbuf[warp];
+    for (int64_t ci = int64_t(blockIdx.x) * kL2PWarps + warp; ci < nchunks;
+         ci += int64_t(gridDim.x) * kL2PWarps) {
+        const P2PChunk c = chunks[ci];
+        const int myrow = lane < c.lcount ? lrows[c.lfirst + lane] : 0;
+        const double2 t0 = txy[c.tbegin + min(lane, c.tcount - 1)];
+        const double2 t1 = txy[c.tbegin + min(lane + 32, c.tcount - 1)];
+        double s0 = 0.0, s1 = 0.0;
+        int r = __shfl_sync(0xffffffffu, myrow, 0);
+        double2 v0 = lane < n ? loc[int64_t(r) * n + lane] : make_double2(0.0, 0.0);
+        double2 v1 = lane + 32 < n ? loc[int64_t(r) * n + lane + 32] : make_double2(0.0, 0.0);
+        for (int q = 0; q < c.lcount; ++q) {
+            buf[lane] = v0;
+            buf[lane + 32] = v1;
+            __syncwarp();
+            const int rc = r;
+            if (q + 1 < c.lcount) {  // prefetch the next row under this row's Horner
+                r = __shfl_sync(0xffffffffu, myrow, q + 1);
+                v0 = lane < n ? loc[int64_t(r) * n + lane] : make_double2(0.0, 0.0);
+                v1 = lane + 32 < n ? loc[int64_t(r) * n + lane + 32] : make_double2(0.0, 0.0);
+            }
+            const double s = side / double(1 << row_level[rc]);
+            double cx, cy;
+            box_center(x0, y0, s, uint32_t(row_morton[rc]), cx, cy);
+            const double inv_s = 1.0 / s;
+            const double u0r = (t0.x - cx) * inv_s, u0i = (t0.y - cy) * inv_s;
+            const double u1r = (t1.x - cx) * inv_s, u1i = (t1.y - cy) * inv_s;
+            double ar = buf[P].x, ai = buf[P].y, br = ar, bi = ai;
+            if (c.tcount > 32) {  // two targets per lane
+                for (int k = P - 1; k >= 0; --k) {
+                    const double2 a = buf[k];
+                    const double nar = fma(ar, u0r, fma(-ai, u0i, a.x));
+                    const double nai = fma(ar, u0i, fma(ai, u0r, a.y));
+                    const double nbr = fma(br, u1r, fma(-bi, u1i, a.x));
+                    const double nbi = fma(br, u1i, fma(bi, u1r, a.y));
+                    ar = nar;
+                    ai = nai;
+                    br = nbr;
+                    bi = nbi;
+                }
+            } else {  // warp-uniform: one target per lane, half the FP64 work
+                for (int k = P - 1; k >= 0; --k) {
+                    const double2 a = buf[k];
+                    const double nar = fma(ar, u0r, fma(-ai, u0i, a.x));
+                    const double nai = fma(ar, u0i, fma(ai, u0r, a.y));
+                    ar = nar;
+                    ai = nai;
+                }
+            }
+            s0 += ar;
+            s1 += br;
+            __syncwarp();
         }
-        sum += vr;
+        if (lane < c.tcount) pot_far[c.tbegin + lane] = -kInv2Pi * s0;
+        if (lane + 32 < c.tcount) pot_far[c.tbegin + lane + 32] = -kInv2Pi * s1;
     }
-    pot_far[e] = -kInv2Pi * sum;
 }
 
 // ------------------------------------------------------- near-field P2P --
@@ -1292,7 +1330,7 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
                         lv, m2m_ops, P, gbar + 0);
             ++launches;
         }
-    } else if (!pl.multilevel_up) {
+    } else {
         ShiftLevels lv{};
         for (int l = L - 1; l >= 2; --l) {
             const int64_t np = pl.m2m_count[size_t(l)];
@@ -1355,7 +1393,7 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
                         st, lv, l2l_ops, P, gbar + 1);
             ++launches;
         }
-    } else if (!pl.multilevel_down) {
+    } else {
         ShiftLevels lv{};
         for (int l = 2; l < L; ++l) {
             const int64_t np = pl.l2l_count[size_t(l)];
@@ -1374,13 +1412,13 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
         }
     }
     mark(5);
-    if (pl.shard_t1 > pl.shard_t0) {
-        launch_pdl(l2p_kernel, dim3(nblk(pl.shard_t1 - pl.shard_t0, 256)), dim3(256), 0, st,
-                   (const int32_t*)pl.tgt_row.p, pl.shard_t0, pl.shard_t1, (const double2*)pl.tgt_sorted.p,
-                   (const double2*)loc, (const int32_t*)pl.row_level.p, (const int32_t*)pl.row_morton.p,
-                   pl.adaptive ? (const int32_t*)pl.row_chain.p : (const int32_t*)pl.row_parent.p,
-                   (pl.adaptive || pl.multilevel_down) ? 1 : 0, P, pl.x0, pl.y0, pl.side,
-                   pot_far, ticket);
+    if (pl.n_p2p_chunks > 0) {
+        const int64_t want = (pl.n_p2p_chunks + kL2PWarps - 1) / kL2PWarps;
+        const unsigned grid = unsigned(std::min<int64_t>(want, int64_t(pl.sm_count) * 8));
+        launch_pdl(l2p_kernel, dim3(grid), dim3(kL2PWarps * 32), 0, st, (const P2PChunk*)pl.p2p_chunks.p,
+                   pl.n_p2p_chunks, (const int32_t*)pl.l2p_rows.p, (const double2*)pl.tgt_sorted.p,
+                   (const double2*)loc, (const int32_t*)pl.row_level.p, (const int32_t*)pl.row_morton.p, P,
+                   pl.x0, pl.y0, pl.side, pot_far, ticket);
         ++launches;
     }
     if (pl.n_m2p_work > 0) {

@@ -69,6 +69,8 @@ struct P2PChunk {
     int32_t rfirst;  // near source ranges [rfirst, rfirst + rcount) in near_ranges
     int32_t rcount;  // <= kMaxNearRanges
     int32_t rself;   // index (within the list) of the target's own leaf
+    int32_t lfirst;  // local-expansion rows the targets evaluate (L2P chain):
+    int32_t lcount;  //   l2p_rows[lfirst, lfirst + lcount), leaf first
 };
 constexpr int kMaxNearRanges = 64;
 
@@ -137,6 +139,12 @@ struct Plan {
     // M2M chain, L2P of every ancestor instead of the L2L chain -- one
     // launch each instead of one per level (tree.cu, choose_passes).
     bool multilevel_up = false, multilevel_down = false;
+    // Uniform trees: hybrid pass thresholds.  A box with <= up_cap sources
+    // gets its multipole by direct P2M, a larger non-leaf box by M2M; a
+    // non-leaf box with > dn_cap targets pushes its local down by L2L, the
+    // others are evaluated directly on the L2P chain.  0 = the classical
+    // chain (summation.cpp:257-267, 305-312), INT32_MAX = multilevel.
+    int32_t up_cap = 0, dn_cap = 0;
     // Adaptive trees (VPG_MODE_NATIVE, adaptive.cu): W-list M2P and X-list
     // P2L work on top of the V (M2L) and U (near-field) lists.
     bool adaptive = false;
@@ -155,6 +163,7 @@ struct Plan {
     // down by L2L)
     DBuf<int4> updown_kids;
     DBuf<int32_t> row_chain;
+    DBuf<int32_t> l2p_rows;  // per-leaf L2P chains (P2PChunk::lfirst/lcount)
 
     // Modified Helmholtz (treecode) state.
     int helm_min_level = 2;

@@ -365,13 +365,15 @@ void build_tree(Plan& pl) {
     }
     choose_passes(pl);
     {
-        // P2M items: leaves only for the M2M chain, every level otherwise
+        // P2M items: every box with <= up_cap sources, and oversized leaves
+        // (split into items + an ordered reduction)
         std::vector<P2MItem> items;
         std::vector<P2MSplit> splits;
-        for (int l = pl.multilevel_up ? 2 : L; l <= L; ++l) {
+        for (int l = 2; l <= L; ++l) {
             const int sh = 2 * (L - l);
             for (int64_t b = 0; b < (int64_t(1) << (2 * l)); ++b) {
-                if (pl.h_scnt[size_t(lvl_base(l) + b)] == 0) continue;
+                const int32_t cnt = pl.h_scnt[size_t(lvl_base(l) + b)];
+                if (cnt == 0 || (l < L && cnt > pl.up_cap)) continue;
                 const int32_t e0 = pl.h_soff[size_t(b << sh)], e1 = pl.h_soff[size_t((b + 1) << sh)];
                 const int32_t pieces = (e1 - e0 + kP2MItemCap - 1) / kP2MItemCap;
                 const int32_t row = int32_t(lvl_base(l) - lvl_base(2) + b);
@@ -388,22 +390,58 @@ void build_tree(Plan& pl) {
     build_schedules(pl, 0, nleaf);
 }
 
-// Small problems pay more for the level-by-level M2M / L2L chains (~20 us
-// of latency per level, measured) than for evaluating every level directly:
-// P2M costs ~6 (L-1) P flops per source and L2P ~8 (L-1) P per target.
-// VPG_MULTILEVEL=0/1 forces the choice (tests cover both).
+// Pass selection for uniform trees: per direction, the threshold (see
+// Plan::up_cap) minimising a cost model fitted to B200 measurements:
+// direct P2M ~11 G (point, row)/s, L2P ~24 G (target, row)/s, M2M / L2L
+// ~3.7 ns per child plus ~12 us per level of the cooperative shift kernel.
+// VPG_MULTILEVEL=0/1 forces the classical chain / the multilevel passes.
 void choose_passes(Plan& pl) {
+    const int L = pl.L;
+    const int32_t kInf = INT32_MAX;
     const char* env = std::getenv("VPG_MULTILEVEL");
+    const char* cap_env = std::getenv("VPG_PASS_CAP");  // tests: force one threshold
     if (env && (env[0] == '0' || env[0] == '1')) {
-        pl.multilevel_up = pl.multilevel_down = env[0] == '1';
-        return;
+        pl.up_cap = pl.dn_cap = env[0] == '1' ? kInf : 0;
+    } else if (cap_env && cap_env[0]) {
+        pl.up_cap = pl.dn_cap = int32_t(std::atoi(cap_env));
+    } else {
+        const int32_t caps[] = {0, 32, 64, 128, 256, 512, 1024, 4096, kInf};
+        auto cost = [&](const std::vector<int32_t>& cnt, int32_t cap, bool up) {
+            // direct: every (point, box) pair with box count <= cap (leaves always);
+            // shifts: boxes above cap at levels < L, their non-empty children
+            double direct = 0.0, children = 0.0;
+            int levels = 0;
+            for (int l = 2; l <= L; ++l) {
+                bool any = false;
+                for (int64_t b = 0; b < (int64_t(1) << (2 * l)); ++b) {
+                    const int32_t c = cnt[size_t(lvl_base(l) + b)];
+                    if (c == 0) continue;
+                    if (l == L || c <= cap) {
+                        direct += c;
+                    } else {
+                        any = true;
+                        for (int q = 0; q < 4; ++q) children += cnt[size_t(lvl_base(l + 1) + (b << 2) + q)] > 0;
+                    }
+                }
+                levels += any;
+            }
+            return direct / (up ? 11e9 : 24e9) + children * 3.7e-9 + levels * 12e-6;
+        };
+        double bu = 1e30, bd = 1e30;
+        for (const int32_t cap : caps) {
+            const double cu = cost(pl.h_scnt, cap, true), cd = cost(pl.h_tcnt, cap, false);
+            if (cu < bu) {
+                bu = cu;
+                pl.up_cap = cap;
+            }
+            if (cd < bd) {
+                bd = cd;
+                pl.dn_cap = cap;
+            }
+        }
     }
-    const double chain_s = 20e-6 * double(std::max(0, pl.L - 2));
-    const double rate = 15e12;  // sustained FP64 flop/s of these passes
-    const double up_s = double(pl.ns) * (pl.L - 1) * 6.0 * 50.0 / rate;
-    const double down_s = double(pl.nt) * (pl.L - 1) * 8.0 * 51.0 / rate;
-    pl.multilevel_up = up_s < chain_s;
-    pl.multilevel_down = down_s < chain_s;
+    pl.multilevel_up = pl.up_cap == kInf;
+    pl.multilevel_down = pl.dn_cap == kInf;
 }
 
 // Target-side schedules restricted to the Morton leaf range [lb, le): M2L
@@ -468,7 +506,7 @@ void build_schedules(Plan& pl, int64_t lb, int64_t le) {
             // M2M: parents at level l with src_cnt > 0 (summation.cpp:257-267)
             pl.m2m_first[size_t(l)] = int64_t(boxes.size());
             for (int64_t b = 0; b < (int64_t(1) << (2 * l)); ++b)
-                if (pl.h_scnt[size_t(lvl_base(l) + b)] > 0) {
+                if (pl.h_scnt[size_t(lvl_base(l) + b)] > pl.up_cap) {
                     boxes.push_back(int32_t(b));
                     for (int c = 0; c < 4; ++c)
                         pl.m2m_children += pl.h_scnt[size_t(lvl_base(l + 1) + (b << 2) + c)] > 0;
@@ -480,7 +518,7 @@ void build_schedules(Plan& pl, int64_t lb, int64_t le) {
             // (summation.cpp:305-312); parent tgt_cnt > 0 is equivalent.
             pl.l2l_first[size_t(l)] = int64_t(boxes.size());
             for (int64_t b = 0; b < (int64_t(1) << (2 * l)); ++b)
-                if (pl.h_tcnt[size_t(lvl_base(l) + b)] > 0 && overlaps(l, b)) {
+                if (pl.h_tcnt[size_t(lvl_base(l) + b)] > pl.dn_cap && overlaps(l, b)) {
                     boxes.push_back(int32_t(b));
                     for (int c = 0; c < 4; ++c)
                         pl.l2l_children += pl.h_tcnt[size_t(lvl_base(l + 1) + (b << 2) + c)] > 0;
@@ -500,10 +538,20 @@ void build_schedules(Plan& pl, int64_t lb, int64_t le) {
         const int chunk = 64;  // kP2PChunk: two targets per lane
         std::vector<P2PChunk> chunks;
         std::vector<int2> ranges;
+        std::vector<int32_t> lrows;
         pl.p2p_pairs = 0;
         for (int64_t b = lb; b < le; ++b) {
             const int32_t t0 = h_toff[size_t(b)], t1 = h_toff[size_t(b) + 1];
             if (t1 == t0) continue;
+            // L2P chain: the leaf's local expansion after the L2L pass, or
+            // in the multilevel downward pass the leaf's and every ancestor's
+            const int32_t lfirst = int32_t(lrows.size());
+            for (int l = L; l >= 2; --l) {
+                lrows.push_back(int32_t(lvl_base(l) - lvl_base(2) + (b >> (2 * (L - l)))));
+                // stop below a parent that pushed its local down by L2L
+                if (l > 2 && pl.h_tcnt[size_t(lvl_base(l - 1) + (b >> (2 * (L - l + 1))))] > pl.dn_cap) break;
+            }
+            const int32_t lcount = int32_t(lrows.size()) - lfirst;
             const int ix = int(squash2(uint32_t(b))), iy = int(squash2(uint32_t(b) >> 1));
             // 3x3 neighbour leaves in the reference order (summation.cpp:330-334)
             const int32_t rfirst = int32_t(ranges.size());
@@ -520,9 +568,10 @@ void build_schedules(Plan& pl, int64_t lb, int64_t le) {
             pl.p2p_pairs += int64_t(t1 - t0) * nsrc;
             for (int32_t t = t0; t < t1; t += chunk)
                 chunks.push_back(P2PChunk{t, std::min(chunk, t1 - t), int32_t(std::min<int64_t>(nsrc, INT32_MAX)),
-                                          rfirst, rcount, rself});
+                                          rfirst, rcount, rself, lfirst, lcount});
         }
         to_device(pl.near_ranges, ranges, st);
+        to_device(pl.l2p_rows, lrows, st);
         // Heavy chunks (large neighbourhoods, > 32 targets) first -- a whole
         // CTA processes each (l2p_p2p_kernel phase 1) -- then the light ones
         // for single warps; costliest first within each part, so the

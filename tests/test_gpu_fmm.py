@@ -159,12 +159,14 @@ def test_target_shards_assemble_bit_exact(vp, world):
         assert np.array_equal(plan.apply(w.q), full)
 
 
-@pytest.mark.parametrize("multilevel", ["0", "1"])
-def test_chain_and_multilevel_passes(vp, rest, monkeypatch, multilevel):
+@pytest.mark.parametrize("env", [("VPG_MULTILEVEL", "0"), ("VPG_MULTILEVEL", "1"),
+                                 ("VPG_PASS_CAP", "64"), ("VPG_PASS_CAP", "1024")])
+def test_chain_multilevel_and_hybrid_passes(vp, rest, monkeypatch, env):
     """Upward/downward passes as level chains (M2M/L2L, the reference
-    structure) or as direct per-level P2M/L2P (small problems) agree with the
-    oracle to the same tolerance."""
-    monkeypatch.setenv("VPG_MULTILEVEL", multilevel)
+    structure), as direct per-level P2M/L2P (multilevel), or hybrid (direct
+    below a box-size threshold, shifts above) agree with the oracle to the
+    same tolerance."""
+    monkeypatch.setenv(*env)
     w = W.cfg2()
     with vp.SummationPlan(lap(vp), w.src, w.tgt, 1e-12) as plan:
         gpu = plan.apply(w.q)
