@@ -609,19 +609,14 @@ void build_adaptive(Plan& pl, cudaStream_t st) {
             const int32_t lcount = int32_t(lrows.size()) - lfirst;
             for (int32_t t = g.z; t < g.w; t += 64)
                 chunks.push_back(P2PChunk{t, std::min(64, g.w - t), int32_t(std::min<int64_t>(nsrc, INT32_MAX)),
-                                          rfirst, int32_t(ranges.size()) - rfirst, rself, lfirst, lcount});
+                                          rfirst, int32_t(ranges.size()) - rfirst, rself, lfirst, lcount, 0, 1,
+                                          -1, -1});
         }
         if (max_ranges + 1 > kMaxNearRanges)
             throw Error{VPG_ERR_INVALID_ARGUMENT,
                         "adaptive tree: a leaf has " + std::to_string(max_ranges) + " near leaves (max " +
                             std::to_string(kMaxNearRanges - 1) + ")"};
-        // all light (per-warp) chunks, costliest first
-        std::stable_sort(chunks.begin(), chunks.end(), [](const P2PChunk& a, const P2PChunk& b) {
-            return int64_t(a.pad) * a.tcount > int64_t(b.pad) * b.tcount;
-        });
-        pl.n_p2p_heavy = 0;
-        pl.n_p2p_chunks = int64_t(chunks.size());
-        pl.p2p_tpt = 2;
+        schedule_near_chunks(pl, chunks);
         h2d(pl.p2p_chunks, chunks, st);
         h2d(pl.near_ranges, ranges, st);
         h2d(pl.l2p_rows, lrows, st);

@@ -651,20 +651,22 @@ constexpr int kL2PWarps = 8;
 __global__ void __launch_bounds__(kL2PWarps * 32)
 l2p_kernel(const P2PChunk* chunks, int64_t nchunks, const int32_t* lrows, const double2* txy,
            const double2* loc, const int32_t* row_level, const int32_t* row_morton, int P,
-           double x0, double y0, double side, double* pot_far, int* ticket) {
+           double x0, double y0, double side, double* pot_far, int* ticket, int* pcount,
+           int64_t nslots) {
     __shared__ double2 rowbuf[kL2PWarps][64];
     pdl_trigger();
     pdl_wait();
-    if (blockIdx.x == 0 && threadIdx.x == 0) {  // near-field work counters for l2p_p2p_kernel
-        ticket[0] = 0;
-        ticket[1] = 0;
-    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) ticket[0] = 0;  // near-field task counter
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nslots;
+         i += int64_t(gridDim.x) * blockDim.x)
+        pcount[i] = 0;  // split-chunk completion counters
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int n = P + 1;
     double2* buf = rowbuf[warp];
     for (int64_t ci = int64_t(blockIdx.x) * kL2PWarps + warp; ci < nchunks;
          ci += int64_t(gridDim.x) * kL2PWarps) {
         const P2PChunk c = chunks[ci];
+        if (c.part != 0) continue;  // split chunks: evaluated once
         const int myrow = lane < c.lcount ? lrows[c.lfirst + lane] : 0;
         const double2 t0 = txy[c.tbegin + min(lane, c.tcount - 1)];
         const double2 t1 = txy[c.tbegin + min(lane + 32, c.tcount - 1)];
@@ -730,17 +732,19 @@ l2p_kernel(const P2PChunk* chunks, int64_t nchunks, const int32_t* lrows, const 
 // hot loop has no zero test: pairs of the centre leaf (the only place equal
 // coordinates can meet) are undone and redone with the reference skip rule
 // right after their batch (lap_pair_fixup).
-//   Heavy chunks (>= kP2PCoopSources sources) are processed by the whole CTA:
-//   warp w takes batches w, w+8, ...; the eight partial sums per target are
-//   added in warp order through smem.
-//   Light chunks (small leaves, cfg1/cfg2 interior) are taken by single
-//   warps; to keep lanes busy with ~15-target leaves the warp splits into
-//   S = 32 / ceil(nT/2) groups taking every S-th source, partials added in
-//   group order.
-// Both phases draw from ticket counters zeroed by l2p_kernel; every sum has
-// a fixed order, so results are run-to-run identical.  Output: far field
-// (l2p_kernel) + near field, scattered to the original target order
-// (summation.cpp:345).
+// Every task is one warp, drawn from a ticket counter (zeroed by
+// l2p_kernel) in plan-time cost order:
+//   split chunks (large neighbourhoods, see schedule_near_chunks): part i of
+//   n takes the i-th contiguous share of the flat source list for all the
+//   chunk's targets, writes 64 partial sums, and the last of the n warps to
+//   finish (completion counter) adds the parts in part order -- no CTA
+//   barriers, so no warp idles behind a slower sibling;
+//   whole chunks (small leaves, cfg1/cfg2 interior): to keep lanes busy with
+//   ~15-target leaves the warp splits into S = 32 / ceil(nT/2) groups taking
+//   every S-th source, partials added in group order.
+// Every sum has a fixed order, so results are run-to-run identical.  Output:
+// far field (l2p_kernel) + near field, scattered to the original target
+// order (summation.cpp:345).
 constexpr int kP2PWarps = 8;
 constexpr int kP2PBatch = 64;
 constexpr int kP2PChunk = 64;
@@ -842,18 +846,16 @@ __device__ __forceinline__ void near_batch(const NearList& nl, int base, int cnt
 }
 
 __global__ void __launch_bounds__(kP2PWarps * 32, kP2PMinBlocks)
-l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, int64_t nheavy, const int2* ranges,
+l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, const int2* ranges,
                const double2* sxy, const double* q, const double2* txy,
                const int32_t* tids, const double* pot_far,
-               const double2* gtab, int* ticket, double* out) {
+               const double2* gtab, int* ticket, double* partial, int* pcount, double* out) {
     extern __shared__ double2 smp[];
     double2* tab = smp;                                                  // log table
     double2* sbuf = smp + kLogTableSize * kLogTableCopies;               // [warps][batch] xy
     double* qbuf = reinterpret_cast<double*>(sbuf + kP2PWarps * kP2PBatch);  // [warps][batch]
-    double* red = qbuf + kP2PWarps * kP2PBatch;                          // [warps][64]
-    int* rbuf = reinterpret_cast<int*>(red + kP2PWarps * 64);            // [warps][2][64]
+    int* rbuf = reinterpret_cast<int*>(qbuf + kP2PWarps * kP2PBatch);   // [warps][2][64]
     __shared__ __align__(8) uint64_t bar;
-    __shared__ int s_ch;
     if (threadIdx.x == 0) mbar_init(&bar, 1);
     __syncthreads();
     // one bulk copy of the 257-entry table into the (still unused) source
@@ -870,51 +872,51 @@ l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, int64_t nheavy, const in
     int* pre_s = rbuf + warp * 2 * kMaxNearRanges;
     int* st_s = pre_s + kMaxNearRanges;
 
-    // ---- phase 1: heavy chunks, the whole CTA per chunk
-    for (;;) {
-        if (threadIdx.x == 0) s_ch = atomicAdd(&ticket[0], 1);
-        __syncthreads();
-        const int64_t ch = s_ch;
-        __syncthreads();
-        if (ch >= nheavy) break;
-        const P2PChunk c = chunks[ch];
-        const int nT = c.tcount;
-        double tx[2], ty[2];
-        LapAcc acc[2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            const double2 t = txy[c.tbegin + min(lane + 32 * u, nT - 1)];
-            tx[u] = t.x;
-            ty[u] = t.y;
-        }
-        const NearList nl = near_list(ranges, c.rfirst, c.rcount, c.rself, lane, pre_s, st_s);
-        // warp w takes the w-th eighth of the flat source list
-        const int f0 = int(int64_t(nl.total) * warp / kP2PWarps);
-        const int f1 = int(int64_t(nl.total) * (warp + 1) / kP2PWarps);
-        for (int base = f0; base < f1; base += kP2PBatch)
-            near_batch(nl, base, min(kP2PBatch, f1 - base), 0, 1, true, lane, sxy, q, mxy, mq,
-                       tab_lane, tx, ty, acc);
-        red[warp * 64 + lane] = lap_total(acc[0]);
-        red[warp * 64 + lane + 32] = lap_total(acc[1]);
-        __syncthreads();
-        if (threadIdx.x < nT) {
-            double sum = 0.0;
-#pragma unroll
-            for (int w = 0; w < kP2PWarps; ++w) sum += red[w * 64 + threadIdx.x];
-            const int e = c.tbegin + threadIdx.x;
-            out[tids[e]] = pot_far[e] - kInv4Pi * sum;
-        }
-        __syncthreads();
-    }
-
-    // ---- phase 2: light chunks, one warp each
     for (;;) {
         int k = 0;
-        if (lane == 0) k = atomicAdd(&ticket[1], 1);
-        const int64_t ch = nheavy + __shfl_sync(0xffffffffu, k, 0);
+        if (lane == 0) k = atomicAdd(&ticket[0], 1);
+        const int64_t ch = __shfl_sync(0xffffffffu, k, 0);
         if (ch >= nchunks) break;
         const P2PChunk c = chunks[ch];
         const int nT = c.tcount;
+        const NearList nl = near_list(ranges, c.rfirst, c.rcount, c.rself, lane, pre_s, st_s);
+        if (c.nparts > 1) {
+            // ---- one part of a split chunk: targets lane, lane + 32
+            double tx[2], ty[2];
+            LapAcc acc[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const double2 t = txy[c.tbegin + min(lane + 32 * u, nT - 1)];
+                tx[u] = t.x;
+                ty[u] = t.y;
+            }
+            const int f0 = int(int64_t(nl.total) * c.part / c.nparts);
+            const int f1 = int(int64_t(nl.total) * (c.part + 1) / c.nparts);
+            for (int base = f0; base < f1; base += kP2PBatch)
+                near_batch(nl, base, min(kP2PBatch, f1 - base), 0, 1, true, lane, sxy, q, mxy, mq,
+                           tab_lane, tx, ty, acc);
+            double* prow = partial + int64_t(c.pbase + c.part) * 64;
+            prow[lane] = lap_total(acc[0]);
+            prow[lane + 32] = lap_total(acc[1]);
+            __threadfence();
+            __syncwarp();
+            int last = 0;
+            if (lane == 0) last = atomicAdd(&pcount[c.slot], 1) == c.nparts - 1;
+            if (__shfl_sync(0xffffffffu, last, 0)) {
+                // last finisher: add the parts in part order
+                __threadfence();
+                const double* pr = partial + int64_t(c.pbase) * 64;
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int li = lane + 32 * u;
+                    double sum = 0.0;
+                    for (int i = 0; i < c.nparts; ++i) sum += __ldcg(pr + i * 64 + li);
+                    if (li < nT) out[tids[c.tbegin + li]] = pot_far[c.tbegin + li] - kInv4Pi * sum;
+                }
+            }
+            continue;
+        }
+        // ---- a whole chunk: nTh target slots (two targets each), S source groups
         const int nTh = (nT + 1) >> 1;
         const int S = max(1, 32 / nTh);
         const int tl = lane % nTh;  // target slot: targets tl and tl + nTh
@@ -928,7 +930,6 @@ l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, int64_t nheavy, const in
             tx[u] = t.x;
             ty[u] = t.y;
         }
-        const NearList nl = near_list(ranges, c.rfirst, c.rcount, c.rself, lane, pre_s, st_s);
         for (int base = 0; base < nl.total; base += kP2PBatch)
             near_batch(nl, base, min(kP2PBatch, nl.total - base), grp, S, active, lane, sxy, q, mxy,
                        mq, tab_lane, tx, ty, acc);
@@ -1273,17 +1274,22 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
     int* ticket = nullptr;
     VPG_CUDA(cudaMallocAsync(&qs, sizeof(double) * size_t(std::max<int64_t>(pl.ns, 1)), st));
     VPG_CUDA(cudaMallocAsync(&ticket, sizeof(int) * 32, st));
+    // split near-field chunks: partial sums and completion counters
+    double* partial_p2p = nullptr;
+    int* pcount = nullptr;
+    VPG_CUDA(cudaMallocAsync(&partial_p2p, sizeof(double) * 64 * size_t(std::max<int64_t>(pl.n_p2p_parts, 1)), st));
+    VPG_CUDA(cudaMallocAsync(&pcount, sizeof(int) * size_t(std::max<int64_t>(pl.n_p2p_heavy, 1)), st));
     VPG_CUDA(cudaMallocAsync(&pot_far, sizeof(double) * size_t(std::max<int64_t>(pl.nt, 1)), st));
     VPG_CUDA(cudaMallocAsync(&mult, sizeof(double2) * size_t(pl.exp_total), st));
     VPG_CUDA(cudaMallocAsync(&loc, sizeof(double2) * size_t(pl.exp_total), st));
     struct Free {
-        void* p[5];
+        void* p[7];
         cudaStream_t s;
         ~Free() {
             for (void* x : p)
                 if (x) cudaFreeAsync(x, s);
         }
-    } fr{{qs, mult, loc, pot_far, ticket}, st};
+    } fr{{qs, mult, loc, pot_far, ticket, partial_p2p, pcount}, st};
     unsigned* gbar = reinterpret_cast<unsigned*>(ticket) + 8;  // grid barriers of the shift passes
 
     mark(0);
@@ -1418,7 +1424,7 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
         launch_pdl(l2p_kernel, dim3(grid), dim3(kL2PWarps * 32), 0, st, (const P2PChunk*)pl.p2p_chunks.p,
                    pl.n_p2p_chunks, (const int32_t*)pl.l2p_rows.p, (const double2*)pl.tgt_sorted.p,
                    (const double2*)loc, (const int32_t*)pl.row_level.p, (const int32_t*)pl.row_morton.p, P,
-                   pl.x0, pl.y0, pl.side, pot_far, ticket);
+                   pl.x0, pl.y0, pl.side, pot_far, ticket, pcount, pl.n_p2p_heavy);
         ++launches;
     }
     if (pl.n_m2p_work > 0) {
@@ -1432,16 +1438,16 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
     if (pl.n_p2p_chunks > 0) {
         const size_t smem = size_t(kLogTableBytes) +
                             (sizeof(double2) + sizeof(double)) * kP2PBatch * kP2PWarps +
-                            sizeof(double) * 64 * kP2PWarps + sizeof(int) * 2 * kMaxNearRanges * kP2PWarps;
+                            sizeof(int) * 2 * kMaxNearRanges * kP2PWarps;
         int per_sm = 1;
         VPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, l2p_p2p_kernel, kP2PWarps * 32, smem));
         const int64_t want = (pl.n_p2p_chunks + kP2PWarps - 1) / kP2PWarps;
         const unsigned grid = unsigned(std::min<int64_t>(want, int64_t(pl.sm_count) * std::max(per_sm, 1)));
         launch_pdl(l2p_p2p_kernel, dim3(grid), dim3(kP2PWarps * 32), smem, st,
-                   (const P2PChunk*)pl.p2p_chunks.p, pl.n_p2p_chunks, pl.n_p2p_heavy,
+                   (const P2PChunk*)pl.p2p_chunks.p, pl.n_p2p_chunks,
                    (const int2*)pl.near_ranges.p, (const double2*)pl.src_sorted.p, (const double*)qs,
                    (const double2*)pl.tgt_sorted.p, (const int32_t*)pl.tgt_ids.p, (const double*)pot_far,
-                   log_table_dev(), ticket, out_dev);
+                   log_table_dev(), ticket, partial_p2p, pcount, out_dev);
         ++launches;
     }
     mark(6);

@@ -71,6 +71,10 @@ struct P2PChunk {
     int32_t rself;   // index (within the list) of the target's own leaf
     int32_t lfirst;  // local-expansion rows the targets evaluate (L2P chain):
     int32_t lcount;  //   l2p_rows[lfirst, lfirst + lcount), leaf first
+    int32_t part;    // split chunks: this task's share of the flat source list,
+    int32_t nparts;  //   part of nparts (1 = whole chunk, written directly)
+    int32_t slot;    //   counter of the split chunk (last finisher reduces)
+    int32_t pbase;   //   first partial-sum row of the split chunk
 };
 constexpr int kMaxNearRanges = 64;
 
@@ -125,7 +129,10 @@ struct Plan {
     DBuf<P2PChunk> p2p_chunks;
     DBuf<int2> near_ranges;  // (first sorted source, count) per near leaf
     int64_t n_p2p_chunks = 0;
-    int64_t n_p2p_heavy = 0;  // leading chunks handled by a whole CTA
+    int64_t n_p2p_heavy = 0;  // split chunks (counters)
+    int64_t n_p2p_parts = 0;  // partial-sum rows of the split chunks
+    double near_fair = 0.0;   // split threshold, fixed by the whole-tree schedule
+                              // (shards must split chunks identically)
     int64_t p2p_pairs = 0;
     int64_t m2m_children = 0, l2l_children = 0;
 
@@ -193,6 +200,7 @@ struct Plan {
 // tree.cu
 void build_tree(Plan& pl);
 void build_schedules(Plan& pl, int64_t leaf_begin, int64_t leaf_end);
+void schedule_near_chunks(Plan& pl, std::vector<P2PChunk>& chunks);
 void choose_passes(Plan& pl);
 // adaptive.cu
 void build_adaptive(Plan& pl, cudaStream_t st);

@@ -444,6 +444,47 @@ void choose_passes(Plan& pl) {
     pl.multilevel_down = pl.dn_cap == kInf;
 }
 
+// Near-field task list (both trees).  A chunk (<= 64 targets of one leaf)
+// worth more than a quarter of a warp's fair share of the near field (~24
+// resident warps per SM) and with a large neighbourhood is split into parts
+// -- contiguous shares of its flat source list, one warp each -- whose
+// partial sums the last finishing warp adds in part order; all other chunks
+// are one warp task.  Costliest first (dynamic ticket), stable (equal costs
+// keep Morton order).
+void schedule_near_chunks(Plan& pl, std::vector<P2PChunk>& chunks) {
+    if (pl.near_fair <= 0.0)  // first (whole-tree) schedule of the plan
+        pl.near_fair = double(std::max<int64_t>(pl.p2p_pairs, 1)) / (double(pl.sm_count) * 24.0);
+    const double fair = pl.near_fair;
+    std::vector<P2PChunk> tasks;
+    tasks.reserve(chunks.size());
+    int32_t slots = 0, parts = 0;
+    for (P2PChunk c : chunks) {
+        const double pairs = double(c.pad) * c.tcount;
+        int np = 1;
+        if (c.pad >= kP2PCoopSources && c.tcount > 32 && pairs >= 0.25 * fair)
+            np = int(std::min(16.0, std::max(2.0, std::ceil(pairs / (0.25 * fair)))));
+        c.nparts = np;
+        c.slot = np > 1 ? slots++ : -1;
+        c.pbase = np > 1 ? parts : -1;
+        for (int i = 0; i < np; ++i) {
+            c.part = i;
+            tasks.push_back(c);
+        }
+        if (np > 1) parts += np;
+    }
+    auto cost = [](const P2PChunk& c) {
+        if (c.nparts > 1) return int64_t(c.pad) * 32 / c.nparts;  // 2 targets per lane, one group
+        const int nth = (c.tcount + 1) / 2;
+        return int64_t(c.pad) * nth / std::max(1, 32 / nth);
+    };
+    std::stable_sort(tasks.begin(), tasks.end(),
+                     [&](const P2PChunk& x, const P2PChunk& y) { return cost(x) > cost(y); });
+    chunks.swap(tasks);
+    pl.n_p2p_heavy = slots;
+    pl.n_p2p_parts = parts;
+    pl.n_p2p_chunks = int64_t(chunks.size());
+}
+
 // Target-side schedules restricted to the Morton leaf range [lb, le): M2L
 // batches and L2L parents of every box overlapping the range, P2P chunks of
 // the leaves inside it.  The upward pass (P2M, M2M) always covers the whole
@@ -568,33 +609,11 @@ void build_schedules(Plan& pl, int64_t lb, int64_t le) {
             pl.p2p_pairs += int64_t(t1 - t0) * nsrc;
             for (int32_t t = t0; t < t1; t += chunk)
                 chunks.push_back(P2PChunk{t, std::min(chunk, t1 - t), int32_t(std::min<int64_t>(nsrc, INT32_MAX)),
-                                          rfirst, rcount, rself, lfirst, lcount});
+                                          rfirst, rcount, rself, lfirst, lcount, 0, 1, -1, -1});
         }
         to_device(pl.near_ranges, ranges, st);
         to_device(pl.l2p_rows, lrows, st);
-        // Heavy chunks (large neighbourhoods, > 32 targets) first -- a whole
-        // CTA processes each (l2p_p2p_kernel phase 1) -- then the light ones
-        // for single warps; costliest first within each part, so the
-        // dynamic ticket schedule starts the long work early.  Stable:
-        // equal-cost chunks keep Morton order.
-        // "heavy" = a chunk worth more than half a warp's fair share of the
-        // near field (~24 resident warps per SM); uniform grids (cfg4) have
-        // none and run barrier-free, the dense strip of cfg2 has many.
-        const double fair = double(pl.p2p_pairs) / (double(pl.sm_count) * 24.0);
-        auto heavy = [&](const P2PChunk& c) {
-            return c.pad >= kP2PCoopSources && c.tcount > 32 && double(c.pad) * c.tcount >= 0.5 * fair;
-        };
-        auto cost = [](const P2PChunk& c) {
-            const int nth = (c.tcount + 1) / 2;
-            return int64_t(c.pad) * nth / std::max(1, 32 / nth);
-        };
-        auto mid = std::stable_partition(chunks.begin(), chunks.end(), heavy);
-        std::stable_sort(chunks.begin(), mid,
-                         [&](const P2PChunk& x, const P2PChunk& y) { return cost(x) > cost(y); });
-        std::stable_sort(mid, chunks.end(),
-                         [&](const P2PChunk& x, const P2PChunk& y) { return cost(x) > cost(y); });
-        pl.n_p2p_heavy = int64_t(mid - chunks.begin());
-        pl.n_p2p_chunks = int64_t(chunks.size());
+        schedule_near_chunks(pl, chunks);
         to_device(pl.p2p_chunks, chunks, st);
     }
     {
