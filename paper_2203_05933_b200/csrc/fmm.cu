@@ -157,33 +157,34 @@ p2m_reduce_kernel(const P2MSplit* splits, const double2* partial, int P, double2
 }
 
 // ------------------------------------------------------------ M2M / L2L --
-// One cooperative launch per pass (all levels): the four child operators
-// (transposed, 4 x (P+1)^2 complex = 166 KB at P=50) are bulk-copied into
-// smem once per CTA; then for each level (bottom-up for M2M, top-down for
-// L2L) the grid splits that level's parents, four threads per output row
-// (each sums a quarter of k for all four children, a fixed xor-shuffle
-// combines the quarters), and a grid-wide barrier separates the levels.
-// The per-level separate launches this replaces were latency-bound at
-// ~20 us each.
-//   Upward (M2M, summation.cpp:257-267): parent[r] = sum_c (m2m[c] child_c)[r]
-//     over children with src_cnt > 0, reduced in c order.
-//   Downward (L2L, summation.cpp:305-312): child_c[r] += (l2l[c] parent)[r]
-//     for children with tgt_cnt > 0.
-// Each output element has exactly one writer: no atomics on values, fixed
-// order.  Cross-level reads use ld.global.cg (L2), never a stale L1 line.
-constexpr int kRowSlots = 64;  // rows per box (>= P+1)
-constexpr int kKSplit = 4;     // threads per row
-constexpr int kShiftGroup = 4; // boxes per CTA round (4 x 64 x 4 = 1024 threads)
+// Factorised shifts.  With the child centre at t = (+-1/4, +-1/4) parent
+// sides, the reference operators (summation.cpp:170-197) are, up to
+// diagonal factors, real binomial triangles:
+//   M2M  b_l = t^l ( sum_{k=1..l} C(l-1,k-1) (2t)^-k a_k - a_0 / l ),  b_0 = a_0
+//   L2L  b'_m = (2t)^-m sum_{l>=m} C(l,m) t^l b_l
+// (|t| = 0.35, |2t| = 0.71: every factor stays within 1e+-23 at P = 55).
+// Per parent the four children's (re, im) columns form exactly one DMMA
+// n-tile: Y[n x 8] = B[n x P] X[P x 8] on the FP64 tensor cores, B (the
+// binomial triangle, transposed) resident in smem, only the k-steps that
+// meet the triangle issued.  A warp per parent: each lane builds its B
+// fragment (scaled child or parent coefficient) in registers; the
+// epilogue applies the output diagonal on the accumulators (a lane holds
+// re and im of one (row, child)):
+//   M2M: the four children are added in quadrant order (shuffles) and the
+//        parent row written (one writer per row);
+//   L2L: child_c[m] += b'_m (one writer per child element).
+// One cooperative launch covers all levels (bottom-up / top-down) with a
+// grid-wide barrier between them; cross-level reads use ld.global.cg.
+// Flops per child: 2 P^2 (one triangle, re and im) vs the dense 8 (P+1)^2.
+constexpr int kShiftWarps = 8;
 constexpr int kMaxShiftLevels = 16;
+constexpr int kM2LHS = 60;  // row stride of the transposed operator tiles (== 12 mod 16)
 
 struct ShiftLevels {
-    int nlev;                          // levels processed, in order
-    const int32_t* parents[kMaxShiftLevels];
+    int nlev;                                 // levels processed, in order
+    const int32_t* parents[kMaxShiftLevels];  // parent rows
+    const int4* kids[kMaxShiftLevels];        // child rows per quadrant (-1: none)
     int64_t nparents[kMaxShiftLevels];
-    const int32_t* cnt_child[kMaxShiftLevels];
-    const int4* kids[kMaxShiftLevels];  // adaptive: child rows per quadrant (else nullptr)
-    const double2* in_level[kMaxShiftLevels];
-    double2* out_level[kMaxShiftLevels];
 };
 
 // Grid-wide barrier for a cooperative launch (all CTAs co-resident):
@@ -207,113 +208,130 @@ __device__ __forceinline__ int quad(const int4& v, int c) {
     return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
 }
 
-template <bool kUp>
-__global__ void __launch_bounds__(kShiftGroup * kRowSlots * kKSplit)
-shift_kernel(ShiftLevels lv, const double2* ops_t, int P, unsigned* gbar) {
-    extern __shared__ __align__(16) double2 sm[];
-    __shared__ __align__(8) uint64_t bar;
+__device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ double2 cmul2(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -(a.y * b.y)), fma(a.x, b.y, a.y * b.x));
+}
+
+template <bool kUp, int MT>
+__global__ void __launch_bounds__(kShiftWarps * 32)
+shift_kernel(ShiftLevels lv, const double* bmat_t, const double2* tab_g, int P, int KP, double2* ex,
+             unsigned* gbar) {
+    extern __shared__ __align__(16) double smb[];
     const int n = P + 1;
-    const int nn = n * n;
-    double2* op = sm;              // [c][k][r]
-    double2* vec = sm + 4 * nn;    // up: [g][c][k]; down: [g][k]
+    double* bs = smb;                                            // [KP][kM2LHS]
+    double2* tpow = reinterpret_cast<double2*>(bs + KP * kM2LHS);  // [4][n]  t_c^j
+    double2* tinv = tpow + 4 * n;                                // [4][n]  (2 t_c)^-j
+    __shared__ __align__(8) uint64_t bar;
     if (threadIdx.x == 0) mbar_init(&bar, 1);
+    for (int i = threadIdx.x; i < 8 * n; i += blockDim.x) tpow[i] = tab_g[i];
     __syncthreads();
-    bulk_stage(op, ops_t, uint32_t(4 * nn) * 16u, &bar, 0);
+    bulk_stage(bs, bmat_t, uint32_t(KP * kM2LHS) * 8u, &bar, 0);
+    __syncthreads();
     pdl_trigger();
     pdl_wait();
-    const int ks = threadIdx.x & (kKSplit - 1);
-    const int r = (threadIdx.x / kKSplit) % kRowSlots;
-    const int g = threadIdx.x / (kKSplit * kRowSlots);
-    const int kspan = (n + kKSplit - 1) / kKSplit;
-    const int k0 = ks * kspan, k1 = min(n, k0 + kspan);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int kq = lane & 3, rq = lane >> 2;
+    const int cb = rq >> 1;    // child of this lane's B-fragment column
+    const bool im = rq & 1;
+    const int ce = lane & 3;   // child of this lane's accumulator columns
+    const double* acol = bs + kq * kM2LHS + rq;
     unsigned target = 0;
     for (int li = 0; li < lv.nlev; ++li) {
         const int32_t* parents = lv.parents[li];
-        const int64_t np = lv.nparents[li];
-        const int32_t* cnt_child = lv.cnt_child[li];
         const int4* kids = lv.kids[li];
-        const double2* in_level = lv.in_level[li];
-        double2* out_level = lv.out_level[li];
-        for (int64_t g0 = int64_t(blockIdx.x) * kShiftGroup; g0 < np; g0 += int64_t(gridDim.x) * kShiftGroup) {
-            const int ng = int(min(int64_t(kShiftGroup), np - g0));
-            __syncthreads();  // vec reuse
+        const int64_t np = lv.nparents[li];
+        for (int64_t pi = int64_t(blockIdx.x) * kShiftWarps + warp; pi < np;
+             pi += int64_t(gridDim.x) * kShiftWarps) {
+            const int64_t prow = parents[pi];
+            const int4 kd = kids[pi];
+            const int kb = quad(kd, cb), kc = quad(kd, ce);
+            double acc[MT][2];
+#pragma unroll
+            for (int i = 0; i < MT; ++i) acc[i][0] = acc[i][1] = 0.0;
+            // B rows: M2M k = k4 + kq + 1 (x_k = (2t)^-k a_k of the child),
+            //         L2L l = k4 + kq     (x_l = t^l b_l of the parent)
+            const double2* src = kUp ? ex + int64_t(max(kb, 0)) * n : ex + prow * n;
+            const double2* dtab = (kUp ? tinv : tpow) + cb * n;
+            const int off = kUp ? 1 : 0;
+            // all of this lane's coefficients in flight at once (KP <= 8 MT)
+            double2 av[2 * MT];
+#pragma unroll
+            for (int j = 0; j < 2 * MT; ++j)
+                av[j] = 4 * j < KP ? __ldcg(src + min(4 * j + kq + off, P)) : make_double2(0.0, 0.0);
+            const double2 a0 = (kUp && kc >= 0) ? __ldcg(ex + int64_t(kc) * n) : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int j = 0; j < 2 * MT; ++j) {
+                const int k4 = 4 * j;
+                if (k4 >= KP) break;
+                const int k = k4 + kq + off;
+                const double2 d = dtab[min(k, P)];
+                const double2 a = av[j];
+                const double v = im ? fma(a.x, d.y, a.y * d.x) : fma(a.x, d.x, -(a.y * d.y));
+                const double bfr = (kb >= 0 && k <= P) ? v : 0.0;
+#pragma unroll
+                for (int i = 0; i < MT; ++i) {
+                    // triangle: M2M rows 8i.. need k <= l; L2L rows 8i.. need l >= m
+                    if (kUp ? (k4 < 8 * i + 8) : (k4 >= 8 * i))
+                        dmma_884(acc[i][0], acc[i][1], acol[k4 * kM2LHS + 8 * i], bfr);
+                }
+            }
             if (kUp) {
-                for (int i = threadIdx.x; i < ng * 4 * n; i += blockDim.x) {
-                    const int gg = i / (4 * n), rem = i % (4 * n), c = rem / n, kk = rem % n;
-                    int64_t child;
-                    bool has;
-                    if (kids) {
-                        child = quad(kids[g0 + gg], c);
-                        has = child >= 0;
-                    } else {
-                        child = (int64_t(parents[g0 + gg]) << 2) | c;
-                        has = cnt_child[child] > 0;
+#pragma unroll
+                for (int i = 0; i < MT; ++i) {
+                    const int l = 8 * i + rq;
+                    double2 b = a0;
+                    if (l > 0 && l <= P) {
+                        const double inv_l = c_neg_inv_k[l];  // -1/l
+                        b = cmul2(tpow[ce * n + l], make_double2(fma(inv_l, a0.x, acc[i][0]),
+                                                                 fma(inv_l, a0.y, acc[i][1])));
                     }
-                    vec[i] = has ? __ldcg(in_level + child * n + kk) : make_double2(0.0, 0.0);
-                }
-            } else {
-                for (int i = threadIdx.x; i < ng * n; i += blockDim.x) {
-                    const int gg = i / n, kk = i % n;
-                    vec[i] = __ldcg(in_level + int64_t(parents[g0 + gg]) * n + kk);
-                }
-            }
-            __syncthreads();
-            const bool live = g < ng && r <= P;
-            double yr[4] = {0.0, 0.0, 0.0, 0.0}, yi[4] = {0.0, 0.0, 0.0, 0.0};
-            if (live) {
-                const double2* x0v = kUp ? vec + (g * 4) * n : vec + g * n;
-#pragma unroll 2
-                for (int kk = k0; kk < k1; ++kk) {
+                    // children in quadrant order (summation.cpp:257-267)
+                    double2 sum = make_double2(0.0, 0.0);
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
-                        const double2 m = op[c * nn + kk * n + r];
-                        const double2 v = kUp ? x0v[c * n + kk] : x0v[kk];
-                        yr[c] = fma(m.x, v.x, fma(-m.y, v.y, yr[c]));
-                        yi[c] = fma(m.x, v.y, fma(m.y, v.x, yi[c]));
+                        const double bx = __shfl_sync(0xffffffffu, b.x, (lane & ~3) | c);
+                        const double by = __shfl_sync(0xffffffffu, b.y, (lane & ~3) | c);
+                        sum.x += bx;
+                        sum.y += by;
                     }
+                    if (ce == 0 && l <= P) ex[prow * n + l] = sum;
                 }
-            }
-            // combine the k quarters: fixed butterfly, identical on all four lanes
+            } else if (kc >= 0) {
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-#pragma unroll
-                for (int o = 1; o < kKSplit; o <<= 1) {
-                    yr[c] += __shfl_xor_sync(0xffffffffu, yr[c], o);
-                    yi[c] += __shfl_xor_sync(0xffffffffu, yi[c], o);
-                }
-            }
-            if (live && ks == 0) {
-                const int64_t parent = parents[g0 + g];
-                if (kUp) {
-                    // children with src_cnt == 0 were staged as zeros; sum in c order
-                    double ar = 0.0, ai = 0.0;
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        ar += yr[c];
-                        ai += yi[c];
-                    }
-                    out_level[parent * n + r] = make_double2(ar, ai);
-                } else {
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        int64_t child;
-                        if (kids) {
-                            child = quad(kids[g0 + g], c);
-                            if (child < 0) continue;
-                        } else {
-                            child = (parent << 2) | c;
-                            if (cnt_child[child] == 0) continue;
-                        }
-                        double2* dst = out_level + child * n + r;
+                for (int i = 0; i < MT; ++i) {
+                    const int m = 8 * i + rq;
+                    if (m <= P) {
+                        const double2 b = cmul2(tinv[ce * n + m], make_double2(acc[i][0], acc[i][1]));
+                        double2* dst = ex + int64_t(kc) * n + m;
                         double2 d = __ldcg(dst);
-                        d.x += yr[c];
-                        d.y += yi[c];
+                        d.x += b.x;
+                        d.y += b.y;
                         *dst = d;
                     }
                 }
             }
         }
         if (li + 1 < lv.nlev) grid_barrier(gbar, target);
+    }
+}
+
+using ShiftKernel = void (*)(ShiftLevels, const double*, const double2*, int, int, double2*, unsigned*);
+
+template <bool kUp>
+ShiftKernel shift_kernel_for(int mt) {
+    switch (mt) {
+        case 2: return shift_kernel<kUp, 2>;
+        case 3: return shift_kernel<kUp, 3>;
+        case 4: return shift_kernel<kUp, 4>;
+        case 5: return shift_kernel<kUp, 5>;
+        case 6: return shift_kernel<kUp, 6>;
+        default: return shift_kernel<kUp, 7>;
     }
 }
 
@@ -343,7 +361,6 @@ shift_kernel(ShiftLevels lv, const double2* ops_t, int P, unsigned* gbar) {
 constexpr int kM2LCols = 2 * kM2LPairs;          // 108 used columns
 static_assert((kM2LCols + 7) / 8 <= 14, "14 column tiles");
 constexpr int kM2LXS = 116;                      // X/Y row stride (== 4 mod 16: conflict-free fragments)
-constexpr int kM2LHS = 60;                       // H^T row stride (== 12 mod 16)
 constexpr int kM2LCanon = 7;                     // offsets up to the square's symmetry
 constexpr int kM2LMaxMT = 7;                     // RP <= 56
 
@@ -371,11 +388,6 @@ struct M2LStage {
 };
 
 
-__device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-                 : "+d"(c0), "+d"(c1)
-                 : "d"(a), "d"(b));
-}
 
 // One warp stages a batch: list metadata into the ring slot, then the
 // source rows by 1-D TMA bulk copies completing on the batch's mbarrier.
@@ -1122,39 +1134,32 @@ void build_laplace_ops(Plan& pl) {
         for (int j = 1; j <= i; ++j) B(i, j) = B(i - 1, j - 1) + (j <= i - 1 ? B(i - 1, j) : 0.0);
     }
 
-    // M2M / L2L for child c at (+-1/4, +-1/4) of the parent side, bit 0 = x
-    // (summation.cpp:170-197); stored transposed ([k][r]) for the kernels.
-    std::vector<cplx> up_t(size_t(4) * n * n, cplx{0, 0}), dn_t(size_t(4) * n * n, cplx{0, 0});
+    // M2M / L2L, factorised (shift_kernel): binomial triangles, transposed
+    // [k][row] with row stride kM2LHS, and per child c at (+-1/4, +-1/4) of
+    // the parent side (bit 0 = x, summation.cpp:170-197) the diagonals
+    // t_c^j and (2 t_c)^-j.
+    pl.KP = ((P + 3) / 4) * 4;      // M2M (and M2L): k = 1..P
+    pl.KPd = ((P + 1 + 3) / 4) * 4;  // L2L: l = 0..P
+    std::vector<double> up_b(size_t(pl.KP) * kM2LHS, 0.0), dn_b(size_t(pl.KPd) * kM2LHS, 0.0);
+    for (int l = 1; l <= P; ++l)
+        for (int k = 1; k <= l; ++k) up_b[size_t(k - 1) * kM2LHS + l] = B(l - 1, k - 1);
+    for (int l = 0; l <= P; ++l)
+        for (int m = 0; m <= l; ++m) dn_b[size_t(l) * kM2LHS + m] = B(l, m);
+    std::vector<cplx> stab(size_t(8) * n);
     for (int c = 0; c < 4; ++c) {
         const cplx t{(c & 1) ? 0.25 : -0.25, (c & 2) ? 0.25 : -0.25};
-        std::vector<cplx> tp(size_t(2 * P + 1));
-        tp[0] = {1.0, 0.0};
-        for (int j = 1; j <= 2 * P; ++j) tp[size_t(j)] = cmul(tp[size_t(j - 1)], t);
-        cplx* U = up_t.data() + size_t(c) * n * n;
-        cplx* D = dn_t.data() + size_t(c) * n * n;
-        U[0] = {1.0, 0.0};
-        double sig = 1.0;
-        std::vector<double> sg(static_cast<size_t>(n));
-        for (int k = 0; k <= P; ++k, sig *= 0.5) sg[size_t(k)] = sig;
-        for (int l = 1; l <= P; ++l) {
-            const double f = -1.0 / l;
-            U[size_t(0) * n + l] = {f * tp[size_t(l)].re, f * tp[size_t(l)].im};  // [k=0][r=l]
-            for (int k = 1; k <= l; ++k) {
-                const double w = sg[size_t(k)] * B(l - 1, k - 1);
-                U[size_t(k) * n + l] = {w * tp[size_t(l - k)].re, w * tp[size_t(l - k)].im};
-            }
+        const double m2 = 4.0 * (t.re * t.re + t.im * t.im);
+        const cplx inv2t{2.0 * t.re / m2, -2.0 * t.im / m2};  // 1 / (2t)
+        cplx tp{1.0, 0.0}, ti{1.0, 0.0};
+        for (int j = 0; j <= P; ++j) {
+            stab[size_t(c) * n + j] = tp;
+            stab[size_t(4 + c) * n + j] = ti;
+            tp = cmul(tp, t);
+            ti = cmul(ti, inv2t);
         }
-        double half = 1.0;
-        for (int m = 0; m <= P; ++m, half *= 0.5)
-            for (int l = m; l <= P; ++l) {
-                const double w = half * B(l, m);
-                D[size_t(l) * n + m] = {w * tp[size_t(l - m)].re, w * tp[size_t(l - m)].im};
-            }
     }
-
     // M2L factors: H^T[k-1][l] = C(l+k-1, k-1); d^-j and log(-d) per offset
     // (summation.cpp:199-220).
-    pl.KP = ((P + 3) / 4) * 4;  // DMMA k-steps of 4
     std::vector<double> ht(size_t(pl.KP) * kM2LHS, 0.0);
     for (int k = 1; k <= P; ++k)
         for (int l = 0; l <= P; ++l) ht[size_t(k - 1) * kM2LHS + l] = B(l + k - 1, k - 1);
@@ -1216,13 +1221,15 @@ void build_laplace_ops(Plan& pl) {
     pl.m2l_omap.alloc(omap.size());
     VPG_CUDA(cudaMemcpyAsync(pl.m2l_canon.p, canon.data(), pl.m2l_canon.bytes(), cudaMemcpyHostToDevice, st));
     VPG_CUDA(cudaMemcpyAsync(pl.m2l_omap.p, omap.data(), pl.m2l_omap.bytes(), cudaMemcpyHostToDevice, st));
-    pl.m2m_ops.alloc(size_t(4) * n * n * 2);
-    pl.l2l_ops.alloc(size_t(4) * n * n * 2);
+    pl.m2m_ops.alloc(up_b.size());
+    pl.l2l_ops.alloc(dn_b.size());
+    pl.shift_tab.alloc(stab.size());
     pl.h_t.alloc(ht.size());
     pl.dpow.alloc(dpw.size());
     pl.logmd.alloc(lg.size());
-    VPG_CUDA(cudaMemcpyAsync(pl.m2m_ops.p, up_t.data(), pl.m2m_ops.bytes(), cudaMemcpyHostToDevice, st));
-    VPG_CUDA(cudaMemcpyAsync(pl.l2l_ops.p, dn_t.data(), pl.l2l_ops.bytes(), cudaMemcpyHostToDevice, st));
+    VPG_CUDA(cudaMemcpyAsync(pl.m2m_ops.p, up_b.data(), pl.m2m_ops.bytes(), cudaMemcpyHostToDevice, st));
+    VPG_CUDA(cudaMemcpyAsync(pl.l2l_ops.p, dn_b.data(), pl.l2l_ops.bytes(), cudaMemcpyHostToDevice, st));
+    VPG_CUDA(cudaMemcpyAsync(pl.shift_tab.p, stab.data(), pl.shift_tab.bytes(), cudaMemcpyHostToDevice, st));
     VPG_CUDA(cudaMemcpyAsync(pl.h_t.p, ht.data(), pl.h_t.bytes(), cudaMemcpyHostToDevice, st));
     VPG_CUDA(cudaMemcpyAsync(pl.dpow.p, dpw.data(), pl.dpow.bytes(), cudaMemcpyHostToDevice, st));
     VPG_CUDA(cudaMemcpyAsync(pl.logmd.p, lg.data(), pl.logmd.bytes(), cudaMemcpyHostToDevice, st));
@@ -1246,15 +1253,16 @@ void build_laplace_ops(Plan& pl) {
     for (int mt = 2; mt <= kM2LMaxMT; ++mt) smem_optin((const void*)m2l_kernel_for(mt), 225 * 1024);
     smem_optin((const void*)p2m_kernel, 100 * 1024);
     smem_optin((const void*)p2l_kernel, 100 * 1024);
-    smem_optin((const void*)shift_kernel<true>, 220 * 1024);
-    smem_optin((const void*)shift_kernel<false>, 220 * 1024);
     {
         // co-resident CTAs for the cooperative shift passes
-        const size_t up_smem = sizeof(double2) * size_t(4 * n * n + kShiftGroup * 4 * n);
-        int per_sm = 0;
-        VPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per_sm, shift_kernel<true>, kShiftGroup * kRowSlots * kKSplit, up_smem));
-        pl.shift_grid = std::max(1, per_sm) * pl.sm_count;
+        const size_t sm_up = sizeof(double) * size_t(pl.KP) * kM2LHS + sizeof(double2) * 8 * n;
+        const size_t sm_dn = sizeof(double) * size_t(pl.KPd) * kM2LHS + sizeof(double2) * 8 * n;
+        int pu = 0, pd = 0;
+        VPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pu, shift_kernel_for<true>(pl.RP / 8),
+                                                               kShiftWarps * 32, sm_up));
+        VPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pd, shift_kernel_for<false>(pl.RP / 8),
+                                                               kShiftWarps * 32, sm_dn));
+        pl.shift_grid = std::max(1, std::min(pu, pd)) * pl.sm_count;
     }
     smem_optin((const void*)l2p_p2p_kernel, 64 * 1024);
 }
@@ -1315,11 +1323,8 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
         VPG_CUDA(cudaFreeAsync(partial, st));
     }
     mark(2);
-    const size_t up_smem = sizeof(double2) * size_t(4 * n * n + kShiftGroup * 4 * n);
-    const size_t down_smem = sizeof(double2) * size_t(4 * n * n + kShiftGroup * n);
-    const double2* m2m_ops = reinterpret_cast<const double2*>(pl.m2m_ops.p);
-    const double2* l2l_ops = reinterpret_cast<const double2*>(pl.l2l_ops.p);
-    if (pl.adaptive) {
+    {
+        // M2M, bottom-up (summation.cpp:257-267)
         ShiftLevels lv{};
         for (int l = L - 1; l >= 2; --l) {
             const int64_t np = pl.m2m_count[size_t(l)];
@@ -1327,30 +1332,12 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
             lv.parents[lv.nlev] = pl.updown_boxes.p + pl.m2m_first[size_t(l)];
             lv.kids[lv.nlev] = pl.updown_kids.p + pl.m2m_first[size_t(l)];
             lv.nparents[lv.nlev] = np;
-            lv.in_level[lv.nlev] = mult;
-            lv.out_level[lv.nlev] = mult;
             ++lv.nlev;
         }
         if (lv.nlev) {
-            launch_coop(shift_kernel<true>, pl.shift_grid, dim3(kShiftGroup * kRowSlots * kKSplit), up_smem, st,
-                        lv, m2m_ops, P, gbar + 0);
-            ++launches;
-        }
-    } else {
-        ShiftLevels lv{};
-        for (int l = L - 1; l >= 2; --l) {
-            const int64_t np = pl.m2m_count[size_t(l)];
-            if (!np) continue;
-            lv.parents[lv.nlev] = pl.updown_boxes.p + pl.m2m_first[size_t(l)];
-            lv.nparents[lv.nlev] = np;
-            lv.cnt_child[lv.nlev] = pl.src_cnt.p + lvl_base(l + 1);
-            lv.in_level[lv.nlev] = mult + pl.exp_off[size_t(l + 1)];
-            lv.out_level[lv.nlev] = mult + pl.exp_off[size_t(l)];
-            ++lv.nlev;
-        }
-        if (lv.nlev) {
-            launch_coop(shift_kernel<true>, pl.shift_grid, dim3(kShiftGroup * kRowSlots * kKSplit), up_smem, st,
-                        lv, m2m_ops, P, gbar + 0);
+            const size_t smem = sizeof(double) * size_t(pl.KP) * kM2LHS + sizeof(double2) * 8 * n;
+            launch_coop(shift_kernel_for<true>(pl.RP / 8), pl.shift_grid, dim3(kShiftWarps * 32), smem, st, lv,
+                        (const double*)pl.m2m_ops.p, (const double2*)pl.shift_tab.p, P, pl.KP, mult, gbar + 0);
             ++launches;
         }
     }
@@ -1382,7 +1369,8 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
         ++launches;
     }
     mark(4);
-    if (pl.adaptive) {
+    {
+        // L2L, top-down (summation.cpp:305-312)
         ShiftLevels lv{};
         for (int l = 2; l < L; ++l) {
             const int64_t np = pl.l2l_count[size_t(l)];
@@ -1390,30 +1378,12 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
             lv.parents[lv.nlev] = pl.updown_boxes.p + pl.l2l_first[size_t(l)];
             lv.kids[lv.nlev] = pl.updown_kids.p + pl.l2l_first[size_t(l)];
             lv.nparents[lv.nlev] = np;
-            lv.in_level[lv.nlev] = loc;
-            lv.out_level[lv.nlev] = loc;
             ++lv.nlev;
         }
         if (lv.nlev) {
-            launch_coop(shift_kernel<false>, pl.shift_grid, dim3(kShiftGroup * kRowSlots * kKSplit), down_smem,
-                        st, lv, l2l_ops, P, gbar + 1);
-            ++launches;
-        }
-    } else {
-        ShiftLevels lv{};
-        for (int l = 2; l < L; ++l) {
-            const int64_t np = pl.l2l_count[size_t(l)];
-            if (!np) continue;
-            lv.parents[lv.nlev] = pl.updown_boxes.p + pl.l2l_first[size_t(l)];
-            lv.nparents[lv.nlev] = np;
-            lv.cnt_child[lv.nlev] = pl.tgt_cnt.p + lvl_base(l + 1);
-            lv.in_level[lv.nlev] = loc + pl.exp_off[size_t(l)];
-            lv.out_level[lv.nlev] = loc + pl.exp_off[size_t(l + 1)];
-            ++lv.nlev;
-        }
-        if (lv.nlev) {
-            launch_coop(shift_kernel<false>, pl.shift_grid, dim3(kShiftGroup * kRowSlots * kKSplit), down_smem,
-                        st, lv, l2l_ops, P, gbar + 1);
+            const size_t smem = sizeof(double) * size_t(pl.KPd) * kM2LHS + sizeof(double2) * 8 * n;
+            launch_coop(shift_kernel_for<false>(pl.RP / 8), pl.shift_grid, dim3(kShiftWarps * 32), smem, st, lv,
+                        (const double*)pl.l2l_ops.p, (const double2*)pl.shift_tab.p, P, pl.KPd, loc, gbar + 1);
             ++launches;
         }
     }

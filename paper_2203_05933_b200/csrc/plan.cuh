@@ -110,7 +110,7 @@ struct Plan {
     int64_t n_m2l_batches = 0;
 
     // Laplace operators (summation.cpp:150-222), uploaded once.
-    DBuf<double> m2m_ops, l2l_ops;  // 4 x (P+1)^2 complex, transposed
+    DBuf<double> m2m_ops, l2l_ops;  // binomial triangles of the factorised M2M / L2L
     DBuf<double> h_t;               // H^T: P x RP (k-major), real
     DBuf<double2> dpow;             // 49 x (2P+1): d^-j per offset
     DBuf<double2> logmd;            // 49: log(-d)
@@ -163,7 +163,9 @@ struct Plan {
     int64_t n_p2l_work = 0, p2l_sources = 0;
     std::vector<int64_t> m2m_first, m2m_count;  // into updown_boxes, per level
     std::vector<int64_t> l2l_first, l2l_count;
-    DBuf<int32_t> updown_boxes;
+    DBuf<int32_t> updown_boxes;  // parent rows of the M2M / L2L passes
+    DBuf<double2> shift_tab;      // [4][P+1] t_c^j, then [4][P+1] (2 t_c)^-j
+    int KPd = 0;                  // L2L k-extent (multiple of 4, >= P+1)
     // adaptive trees: child rows per quadrant (-1 = no child / empty) of the
     // updown_boxes parents, and the L2P ancestor chain (next row whose local
     // expansion a target still evaluates; -1 once the parent pushed its local

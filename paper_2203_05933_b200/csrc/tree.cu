@@ -537,35 +537,45 @@ void build_schedules(Plan& pl, int64_t lb, int64_t le) {
         to_device(pl.m2l_batches, batches, st);
     }
     {
-        std::vector<int32_t> boxes;
+        std::vector<int32_t> boxes;  // parent rows
+        std::vector<int4> kids;      // child rows per quadrant, -1 = none
         pl.m2m_first.assign(size_t(L + 1), 0);
         pl.m2m_count.assign(size_t(L + 1), 0);
         pl.l2l_first.assign(size_t(L + 1), 0);
         pl.l2l_count.assign(size_t(L + 1), 0);
         pl.m2m_children = pl.l2l_children = 0;
+        auto children = [&](int l, int64_t b, const std::vector<int32_t>& cnt, int64_t& nk) {
+            int k4[4];
+            for (int c = 0; c < 4; ++c) {
+                const int64_t cb = (b << 2) | c;
+                k4[c] = cnt[size_t(lvl_base(l + 1) + cb)] > 0 ? int32_t(lvl_base(l + 1) - lvl_base(2) + cb) : -1;
+                nk += k4[c] >= 0;
+            }
+            return make_int4(k4[0], k4[1], k4[2], k4[3]);
+        };
         for (int l = 2; l < L; ++l) {
-            // M2M: parents at level l with src_cnt > 0 (summation.cpp:257-267)
+            // M2M: parents at level l above up_cap sources (summation.cpp:257-267
+            // with up_cap = 0), children with src_cnt > 0
             pl.m2m_first[size_t(l)] = int64_t(boxes.size());
             for (int64_t b = 0; b < (int64_t(1) << (2 * l)); ++b)
                 if (pl.h_scnt[size_t(lvl_base(l) + b)] > pl.up_cap) {
-                    boxes.push_back(int32_t(b));
-                    for (int c = 0; c < 4; ++c)
-                        pl.m2m_children += pl.h_scnt[size_t(lvl_base(l + 1) + (b << 2) + c)] > 0;
+                    boxes.push_back(int32_t(lvl_base(l) - lvl_base(2) + b));
+                    kids.push_back(children(l, b, pl.h_scnt, pl.m2m_children));
                 }
             pl.m2m_count[size_t(l)] = int64_t(boxes.size()) - pl.m2m_first[size_t(l)];
         }
         for (int l = 2; l < L; ++l) {
-            // L2L: parents at level l having a child with tgt_cnt > 0
-            // (summation.cpp:305-312); parent tgt_cnt > 0 is equivalent.
+            // L2L: parents at level l above dn_cap targets (summation.cpp:305-312
+            // with dn_cap = 0), children with tgt_cnt > 0
             pl.l2l_first[size_t(l)] = int64_t(boxes.size());
             for (int64_t b = 0; b < (int64_t(1) << (2 * l)); ++b)
                 if (pl.h_tcnt[size_t(lvl_base(l) + b)] > pl.dn_cap && overlaps(l, b)) {
-                    boxes.push_back(int32_t(b));
-                    for (int c = 0; c < 4; ++c)
-                        pl.l2l_children += pl.h_tcnt[size_t(lvl_base(l + 1) + (b << 2) + c)] > 0;
+                    boxes.push_back(int32_t(lvl_base(l) - lvl_base(2) + b));
+                    kids.push_back(children(l, b, pl.h_tcnt, pl.l2l_children));
                 }
             pl.l2l_count[size_t(l)] = int64_t(boxes.size()) - pl.l2l_first[size_t(l)];
         }
+        to_device(pl.updown_kids, kids, st);
         to_device(pl.updown_boxes, boxes, st);
     }
     {
