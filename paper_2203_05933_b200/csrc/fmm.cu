@@ -663,15 +663,10 @@ constexpr int kL2PWarps = 8;
 __global__ void __launch_bounds__(kL2PWarps * 32)
 l2p_kernel(const P2PChunk* chunks, int64_t nchunks, const int32_t* lrows, const double2* txy,
            const double2* loc, const int32_t* row_level, const int32_t* row_morton, int P,
-           double x0, double y0, double side, double* pot_far, int* ticket, int* pcount,
-           int64_t nslots) {
+           double x0, double y0, double side, const int32_t* tids, double* out) {
     __shared__ double2 rowbuf[kL2PWarps][64];
     pdl_trigger();
     pdl_wait();
-    if (blockIdx.x == 0 && threadIdx.x == 0) ticket[0] = 0;  // near-field task counter
-    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nslots;
-         i += int64_t(gridDim.x) * blockDim.x)
-        pcount[i] = 0;  // split-chunk completion counters
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int n = P + 1;
     double2* buf = rowbuf[warp];
@@ -728,8 +723,9 @@ l2p_kernel(const P2PChunk* chunks, int64_t nchunks, const int32_t* lrows, const 
             s1 += br;
             __syncwarp();
         }
-        if (lane < c.tcount) pot_far[c.tbegin + lane] = -kInv2Pi * s0;
-        if (lane + 32 < c.tcount) pot_far[c.tbegin + lane + 32] = -kInv2Pi * s1;
+        // the near field is already in out (l2p_p2p_kernel): out += far
+        if (lane < c.tcount) out[tids[c.tbegin + lane]] += -kInv2Pi * s0;
+        if (lane + 32 < c.tcount) out[tids[c.tbegin + lane + 32]] += -kInv2Pi * s1;
     }
 }
 
@@ -860,8 +856,8 @@ __device__ __forceinline__ void near_batch(const NearList& nl, int base, int cnt
 __global__ void __launch_bounds__(kP2PWarps * 32, kP2PMinBlocks)
 l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, const int2* ranges,
                const double2* sxy, const double* q, const double2* txy,
-               const int32_t* tids, const double* pot_far,
-               const double2* gtab, int* ticket, double* partial, int* pcount, double* out) {
+               const int32_t* tids, const double2* gtab, int* ticket, double* partial, int* pcount,
+               double* out) {
     extern __shared__ double2 smp[];
     double2* tab = smp;                                                  // log table
     double2* sbuf = smp + kLogTableSize * kLogTableCopies;               // [warps][batch] xy
@@ -923,7 +919,7 @@ l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, const int2* ranges,
                     const int li = lane + 32 * u;
                     double sum = 0.0;
                     for (int i = 0; i < c.nparts; ++i) sum += __ldcg(pr + i * 64 + li);
-                    if (li < nT) out[tids[c.tbegin + li]] = pot_far[c.tbegin + li] - kInv4Pi * sum;
+                    if (li < nT) out[tids[c.tbegin + li]] = -kInv4Pi * sum;
                 }
             }
             continue;
@@ -954,7 +950,7 @@ l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, const int2* ranges,
                 if (grp == 0) v += w;
             }
             const int li = tl + nTh * u;
-            if (grp == 0 && li < nT) out[tids[c.tbegin + li]] = pot_far[c.tbegin + li] - kInv4Pi * v;
+            if (grp == 0 && li < nT) out[tids[c.tbegin + li]] = -kInv4Pi * v;
         }
     }
 }
@@ -971,7 +967,7 @@ constexpr int kM2PWarps = 4;
 __global__ void __launch_bounds__(kM2PWarps * 32)
 m2p_kernel(const int4* work, int64_t nwork, const int32_t* wrows, const double2* txy,
            const double2* mult, const int32_t* row_level, const int32_t* row_morton, int P,
-           double x0, double y0, double side, double* pot_far) {
+           double x0, double y0, double side, const int32_t* tids, double* out) {
     extern __shared__ double2 coef[];
     pdl_trigger();
     pdl_wait();
@@ -1007,7 +1003,7 @@ m2p_kernel(const int4* work, int64_t nwork, const int32_t* wrows, const double2*
         const double re = vr * ur - vi * ui;  // times u once more: sum_{k>=1} a_k u^k
         acc += re + cw[0].x * 0.5 * log(d2);
     }
-    if (lane < w.y) pot_far[e] += -kInv2Pi * acc;
+    if (lane < w.y) out[tids[e]] += -kInv2Pi * acc;
 }
 
 // P2L (X lists of adaptive trees): a coarser leaf's sources straight into a
@@ -1108,9 +1104,15 @@ p2l_kernel(const int4* work, int64_t nwork, const int2* ranges, const double2* s
     }
 }
 
-__global__ void gather_q(const double* q, const int32_t* ids, int64_t n, double* qs, unsigned* gbar) {
+// Charges into leaf order; also zeroes the apply's counters: the two grid-
+// barrier words of the shift passes, the near-field task ticket and the
+// split-chunk completion counters.
+__global__ void gather_q(const double* q, const int32_t* ids, int64_t n, double* qs, unsigned* gbar,
+                         int* ticket, int* pcount, int64_t nslots) {
     const int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
     if (e < 2) gbar[e] = 0u;
+    if (e == 0) ticket[0] = 0;
+    for (int64_t i = e; i < nslots; i += int64_t(gridDim.x) * blockDim.x) pcount[i] = 0;
     if (e < n) qs[e] = q[ids[e]];
 }
 
@@ -1268,47 +1270,110 @@ void build_laplace_ops(Plan& pl) {
 }
 
 // ----------------------------------------------------------------- apply --
+// Per-apply scratch of the Laplace FMM, carved from one block: sorted
+// charges, mult / loc rows, far-field potentials, task counters (+ grid
+// barrier words), split-chunk partials and counters, P2M split partials.
+namespace {
+size_t al256(size_t b) { return (b + 255) & ~size_t(255); }
+}  // namespace
+
+size_t laplace_work_bytes(const Plan& pl) {
+    const size_t n = size_t(pl.P + 1);
+    return al256(sizeof(double) * size_t(std::max<int64_t>(pl.ns, 1))) +
+           2 * al256(sizeof(double2) * size_t(std::max<int64_t>(pl.exp_total, 1))) +
+           al256(sizeof(double) * size_t(std::max<int64_t>(pl.nt, 1))) + al256(sizeof(int) * 32) +
+           al256(sizeof(double) * 64 * size_t(std::max<int64_t>(pl.n_p2p_parts, 1))) +
+           al256(sizeof(int) * size_t(std::max<int64_t>(pl.n_p2p_heavy, 1))) +
+           al256(sizeof(double2) * n * size_t(pl.n_p2m_splits > 0 ? pl.n_p2m_items : 1));
+}
+
+LaplaceWork laplace_work_at(const Plan& pl, void* base) {
+    const size_t n = size_t(pl.P + 1);
+    char* p = static_cast<char*>(base);
+    auto take = [&](size_t bytes) {
+        char* r = p;
+        p += al256(bytes);
+        return r;
+    };
+    LaplaceWork w;
+    w.qs = reinterpret_cast<double*>(take(sizeof(double) * size_t(std::max<int64_t>(pl.ns, 1))));
+    w.mult = reinterpret_cast<double2*>(take(sizeof(double2) * size_t(std::max<int64_t>(pl.exp_total, 1))));
+    w.loc = reinterpret_cast<double2*>(take(sizeof(double2) * size_t(std::max<int64_t>(pl.exp_total, 1))));
+    w.pot_far = reinterpret_cast<double*>(take(sizeof(double) * size_t(std::max<int64_t>(pl.nt, 1))));
+    w.ticket = reinterpret_cast<int*>(take(sizeof(int) * 32));
+    w.partial_p2p = reinterpret_cast<double*>(take(sizeof(double) * 64 * size_t(std::max<int64_t>(pl.n_p2p_parts, 1))));
+    w.pcount = reinterpret_cast<int*>(take(sizeof(int) * size_t(std::max<int64_t>(pl.n_p2p_heavy, 1))));
+    w.p2m_partial = reinterpret_cast<double2*>(take(sizeof(double2) * n * size_t(pl.n_p2m_splits > 0 ? pl.n_p2m_items : 1)));
+    return w;
+}
+
 void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
                    cudaStream_t st, cudaEvent_t* ev, int64_t& launches) {
+    void* base = nullptr;
+    VPG_CUDA(cudaMallocAsync(&base, laplace_work_bytes(pl), st));
+    struct Free {
+        void* p;
+        cudaStream_t s;
+        ~Free() {
+            if (p) cudaFreeAsync(p, s);
+        }
+    } fr{base, st};
+    laplace_issue(pl, q_dev, out_dev, laplace_work_at(pl, base), st, ev, launches, nullptr, nullptr, nullptr);
+}
+
+// The kernels of one Laplace apply, in stream order, on a given workspace
+// (no allocation: the sequence can be captured into a CUDA graph).
+//   With a side stream (graph capture) the near field runs concurrently
+// with the whole far-field chain: gather -> [near field (side)] -> P2M ->
+// M2M -> M2L -> P2L -> L2L -> join -> L2P (out += far) -> M2P (out += W).
+// Without one, the same kernels run in one stream with the near field right
+// before L2P.  out = near + far either way (one fixed order).
+void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const LaplaceWork& w,
+                   cudaStream_t st, cudaEvent_t* ev, int64_t& launches, cudaStream_t side,
+                   cudaEvent_t fork, cudaEvent_t join) {
     const int P = pl.P, n = P + 1, L = pl.L;
     auto mark = [&](int i) {
         if (ev) VPG_CUDA(cudaEventRecord(ev[i], st));
     };
-    // scratch: sorted charges, then mult and loc expansions (stream-ordered)
-    double* qs = nullptr;
-    double2* mult = nullptr;
-    double2* loc = nullptr;
-    double* pot_far = nullptr;
-    int* ticket = nullptr;
-    VPG_CUDA(cudaMallocAsync(&qs, sizeof(double) * size_t(std::max<int64_t>(pl.ns, 1)), st));
-    VPG_CUDA(cudaMallocAsync(&ticket, sizeof(int) * 32, st));
-    // split near-field chunks: partial sums and completion counters
-    double* partial_p2p = nullptr;
-    int* pcount = nullptr;
-    VPG_CUDA(cudaMallocAsync(&partial_p2p, sizeof(double) * 64 * size_t(std::max<int64_t>(pl.n_p2p_parts, 1)), st));
-    VPG_CUDA(cudaMallocAsync(&pcount, sizeof(int) * size_t(std::max<int64_t>(pl.n_p2p_heavy, 1)), st));
-    VPG_CUDA(cudaMallocAsync(&pot_far, sizeof(double) * size_t(std::max<int64_t>(pl.nt, 1)), st));
-    VPG_CUDA(cudaMallocAsync(&mult, sizeof(double2) * size_t(pl.exp_total), st));
-    VPG_CUDA(cudaMallocAsync(&loc, sizeof(double2) * size_t(pl.exp_total), st));
-    struct Free {
-        void* p[7];
-        cudaStream_t s;
-        ~Free() {
-            for (void* x : p)
-                if (x) cudaFreeAsync(x, s);
-        }
-    } fr{{qs, mult, loc, pot_far, ticket, partial_p2p, pcount}, st};
+    double* qs = w.qs;
+    double2* mult = w.mult;
+    double2* loc = w.loc;
+    int* ticket = w.ticket;
+    double* partial_p2p = w.partial_p2p;
+    int* pcount = w.pcount;
     unsigned* gbar = reinterpret_cast<unsigned*>(ticket) + 8;  // grid barriers of the shift passes
 
+    auto near_field = [&](cudaStream_t s) {
+        if (pl.n_p2p_chunks == 0) return;
+        const size_t smem = size_t(kLogTableBytes) +
+                            (sizeof(double2) + sizeof(double)) * kP2PBatch * kP2PWarps +
+                            sizeof(int) * 2 * kMaxNearRanges * kP2PWarps;
+        int per_sm = 1;
+        VPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, l2p_p2p_kernel, kP2PWarps * 32, smem));
+        const int64_t want = (pl.n_p2p_chunks + kP2PWarps - 1) / kP2PWarps;
+        const unsigned grid = unsigned(std::min<int64_t>(want, int64_t(pl.sm_count) * std::max(per_sm, 1)));
+        launch_pdl(l2p_p2p_kernel, dim3(grid), dim3(kP2PWarps * 32), smem, s,
+                   (const P2PChunk*)pl.p2p_chunks.p, pl.n_p2p_chunks,
+                   (const int2*)pl.near_ranges.p, (const double2*)pl.src_sorted.p, (const double*)qs,
+                   (const double2*)pl.tgt_sorted.p, (const int32_t*)pl.tgt_ids.p, log_table_dev(), ticket,
+                   partial_p2p, pcount, out_dev);
+        ++launches;
+    };
+
     mark(0);
-    gather_q<<<nblk(pl.ns, 256), 256, 0, st>>>(q_dev, pl.src_ids.p, pl.ns, qs, gbar);
+    gather_q<<<nblk(std::max<int64_t>(pl.ns, pl.n_p2p_heavy), 256), 256, 0, st>>>(
+        q_dev, pl.src_ids.p, pl.ns, qs, gbar, ticket, pcount, pl.n_p2p_heavy);
     VPG_LAUNCH_CHECK();
     ++launches;
+    if (side) {
+        VPG_CUDA(cudaEventRecord(fork, st));
+        VPG_CUDA(cudaStreamWaitEvent(side, fork, 0));
+        near_field(side);
+        VPG_CUDA(cudaEventRecord(join, side));
+    }
     mark(1);
 
-    double2* partial = nullptr;
-    if (pl.n_p2m_splits > 0)
-        VPG_CUDA(cudaMallocAsync(&partial, sizeof(double2) * size_t(pl.n_p2m_items) * n, st));
+    double2* partial = w.p2m_partial;
     if (pl.n_p2m_items > 0) {
         launch_pdl(p2m_kernel, dim3(nblk(pl.n_p2m_items, kP2MWarps)), dim3(kP2MWarps * 32),
                    size_t(kP2MWarps) * kP2MSrc * n * sizeof(double2), st, (const P2MItem*)pl.p2m_items.p,
@@ -1320,7 +1385,6 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
         launch_pdl(p2m_reduce_kernel, dim3(unsigned(pl.n_p2m_splits)), dim3(kRedGroups * 64), 0, st,
                    (const P2MSplit*)pl.p2m_splits.p, (const double2*)partial, P, mult);
         ++launches;
-        VPG_CUDA(cudaFreeAsync(partial, st));
     }
     mark(2);
     {
@@ -1388,13 +1452,15 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
         }
     }
     mark(5);
+    if (side) VPG_CUDA(cudaStreamWaitEvent(st, join, 0));
+    else near_field(st);
     if (pl.n_p2p_chunks > 0) {
         const int64_t want = (pl.n_p2p_chunks + kL2PWarps - 1) / kL2PWarps;
         const unsigned grid = unsigned(std::min<int64_t>(want, int64_t(pl.sm_count) * 8));
         launch_pdl(l2p_kernel, dim3(grid), dim3(kL2PWarps * 32), 0, st, (const P2PChunk*)pl.p2p_chunks.p,
                    pl.n_p2p_chunks, (const int32_t*)pl.l2p_rows.p, (const double2*)pl.tgt_sorted.p,
                    (const double2*)loc, (const int32_t*)pl.row_level.p, (const int32_t*)pl.row_morton.p, P,
-                   pl.x0, pl.y0, pl.side, pot_far, ticket, pcount, pl.n_p2p_heavy);
+                   pl.x0, pl.y0, pl.side, (const int32_t*)pl.tgt_ids.p, out_dev);
         ++launches;
     }
     if (pl.n_m2p_work > 0) {
@@ -1402,22 +1468,7 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
                    size_t(kM2PWarps) * n * sizeof(double2), st, (const int4*)pl.m2p_work.p, pl.n_m2p_work,
                    (const int32_t*)pl.m2p_rows.p, (const double2*)pl.tgt_sorted.p, (const double2*)mult,
                    (const int32_t*)pl.row_level.p, (const int32_t*)pl.row_morton.p, P, pl.x0, pl.y0,
-                   pl.side, pot_far);
-        ++launches;
-    }
-    if (pl.n_p2p_chunks > 0) {
-        const size_t smem = size_t(kLogTableBytes) +
-                            (sizeof(double2) + sizeof(double)) * kP2PBatch * kP2PWarps +
-                            sizeof(int) * 2 * kMaxNearRanges * kP2PWarps;
-        int per_sm = 1;
-        VPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, l2p_p2p_kernel, kP2PWarps * 32, smem));
-        const int64_t want = (pl.n_p2p_chunks + kP2PWarps - 1) / kP2PWarps;
-        const unsigned grid = unsigned(std::min<int64_t>(want, int64_t(pl.sm_count) * std::max(per_sm, 1)));
-        launch_pdl(l2p_p2p_kernel, dim3(grid), dim3(kP2PWarps * 32), smem, st,
-                   (const P2PChunk*)pl.p2p_chunks.p, pl.n_p2p_chunks,
-                   (const int2*)pl.near_ranges.p, (const double2*)pl.src_sorted.p, (const double*)qs,
-                   (const double2*)pl.tgt_sorted.p, (const int32_t*)pl.tgt_ids.p, (const double*)pot_far,
-                   log_table_dev(), ticket, partial_p2p, pcount, out_dev);
+                   pl.side, (const int32_t*)pl.tgt_ids.p, out_dev);
         ++launches;
     }
     mark(6);

@@ -3,6 +3,7 @@
 // summation.cpp:542-549).
 #pragma once
 
+#include <memory>
 #include <mutex>
 #include <vector>
 
@@ -77,6 +78,33 @@ struct P2PChunk {
     int32_t pbase;   //   first partial-sum row of the split chunk
 };
 constexpr int kMaxNearRanges = 64;
+
+// One captured apply (CUDA graph) with its own persistent workspace, keyed
+// by the device pointers it was captured for (host-pointer applies use the
+// entry's staging buffers).  `done` orders successive uses of the entry.
+struct GraphEntry {
+    const double* q = nullptr;
+    double* out = nullptr;
+    bool host = false;
+    void* work = nullptr;
+    double* qstage = nullptr;
+    double* ostage = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaEvent_t done = nullptr;
+    uint64_t last_use = 0;
+    int64_t launches = 0;
+    GraphEntry() = default;
+    GraphEntry(const GraphEntry&) = delete;
+    GraphEntry& operator=(const GraphEntry&) = delete;
+    ~GraphEntry() {
+        if (done) cudaEventSynchronize(done);
+        if (exec) cudaGraphExecDestroy(exec);
+        if (done) cudaEventDestroy(done);
+        if (work) cudaFree(work);
+        if (qstage) cudaFree(qstage);
+        if (ostage) cudaFree(ostage);
+    }
+};
 
 struct Plan {
     int device = 0;
@@ -195,6 +223,12 @@ struct Plan {
     mutable std::mutex prof_mu;
     mutable float phase_ms[VPG_PHASE_COUNT] = {};
     mutable int64_t last_launches = 0;
+    // CUDA-graph cache of the apply (api.cu); declared last so it is torn
+    // down before the buffers it references
+    mutable std::mutex graph_mu;
+    mutable std::vector<std::unique_ptr<GraphEntry>> graphs;
+    mutable uint64_t graph_clock = 0;
+    mutable bool graph_broken = false;  // capture unsupported: plain launches
 
     int64_t device_bytes() const;
 };
@@ -208,6 +242,21 @@ void choose_passes(Plan& pl);
 void build_adaptive(Plan& pl, cudaStream_t st);
 // fmm.cu
 void build_laplace_ops(Plan& pl);
+struct LaplaceWork {
+    double* qs;
+    double2* mult;
+    double2* loc;
+    double* pot_far;
+    int* ticket;
+    double* partial_p2p;
+    int* pcount;
+    double2* p2m_partial;
+};
+size_t laplace_work_bytes(const Plan& pl);
+LaplaceWork laplace_work_at(const Plan& pl, void* base);
+void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const LaplaceWork& w,
+                   cudaStream_t st, cudaEvent_t* ev, int64_t& launches, cudaStream_t side,
+                   cudaEvent_t fork, cudaEvent_t join);
 void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
                    cudaStream_t st, cudaEvent_t* ev, int64_t& launches);
 // direct.cu

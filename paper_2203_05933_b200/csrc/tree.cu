@@ -391,45 +391,68 @@ void build_tree(Plan& pl) {
 }
 
 // Pass selection for uniform trees: per direction, the threshold (see
-// Plan::up_cap) minimising a cost model fitted to B200 measurements:
-// direct P2M ~11 G (point, row)/s, L2P ~24 G (target, row)/s, M2M / L2L
-// ~3.7 ns per child plus ~12 us per level of the cooperative shift kernel.
-// VPG_MULTILEVEL=0/1 forces the classical chain / the multilevel passes.
+// Plan::up_cap) minimising a cost model fitted to B200 measurements
+// (tools/cap_sweep.sh on cfg1/cfg2/cfg4):
+//   direct P2M: max(critical path ~90 ns x points of the largest item,
+//               4 ns per item + 45 ps per (point, row));
+//   direct L2P: 1.1 ns per (64-target chunk, chain row);
+//   M2M / L2L (DMMA shift kernel): ~7.5 us per level with any shifted
+//               parent + 1 ns per child.
+// VPG_MULTILEVEL=0/1 forces the classical chain / the multilevel passes;
+// VPG_PASS_CAP=N forces N in both directions (tests).
 void choose_passes(Plan& pl) {
     const int L = pl.L;
     const int32_t kInf = INT32_MAX;
     const char* env = std::getenv("VPG_MULTILEVEL");
-    const char* cap_env = std::getenv("VPG_PASS_CAP");  // tests: force one threshold
+    const char* cap_env = std::getenv("VPG_PASS_CAP");
     if (env && (env[0] == '0' || env[0] == '1')) {
         pl.up_cap = pl.dn_cap = env[0] == '1' ? kInf : 0;
     } else if (cap_env && cap_env[0]) {
         pl.up_cap = pl.dn_cap = int32_t(std::atoi(cap_env));
     } else {
-        const int32_t caps[] = {0, 32, 64, 128, 256, 512, 1024, 4096, kInf};
-        auto cost = [&](const std::vector<int32_t>& cnt, int32_t cap, bool up) {
-            // direct: every (point, box) pair with box count <= cap (leaves always);
-            // shifts: boxes above cap at levels < L, their non-empty children
-            double direct = 0.0, children = 0.0;
+        const int32_t caps[] = {0, 16, 32, 64, 128, 256, 1024, 4096, kInf};
+        auto shifts = [&](const std::vector<int32_t>& cnt, int32_t cap) {
+            double children = 0.0;
             int levels = 0;
-            for (int l = 2; l <= L; ++l) {
+            for (int l = 2; l < L; ++l) {
                 bool any = false;
                 for (int64_t b = 0; b < (int64_t(1) << (2 * l)); ++b) {
-                    const int32_t c = cnt[size_t(lvl_base(l) + b)];
-                    if (c == 0) continue;
-                    if (l == L || c <= cap) {
-                        direct += c;
-                    } else {
-                        any = true;
-                        for (int q = 0; q < 4; ++q) children += cnt[size_t(lvl_base(l + 1) + (b << 2) + q)] > 0;
-                    }
+                    if (cnt[size_t(lvl_base(l) + b)] <= cap) continue;
+                    any = true;
+                    for (int q = 0; q < 4; ++q) children += cnt[size_t(lvl_base(l + 1) + (b << 2) + q)] > 0;
                 }
                 levels += any;
             }
-            return direct / (up ? 11e9 : 24e9) + children * 3.7e-9 + levels * 12e-6;
+            return levels * 7.5e-6 + children * 1e-9;
+        };
+        auto up_cost = [&](int32_t cap) {
+            double items = 0.0, rows = 0.0, longest = 0.0;
+            for (int l = 2; l <= L; ++l)
+                for (int64_t b = 0; b < (int64_t(1) << (2 * l)); ++b) {
+                    const int32_t c = pl.h_scnt[size_t(lvl_base(l) + b)];
+                    if (c == 0 || (l < L && c > cap)) continue;
+                    items += (c + kP2MItemCap - 1) / kP2MItemCap;
+                    rows += c;
+                    longest = std::max(longest, double(std::min(c, kP2MItemCap)));
+                }
+            return std::max(90e-9 * longest, items * 4e-9 + rows * 45e-12) + shifts(pl.h_scnt, cap);
+        };
+        auto down_cost = [&](int32_t cap) {
+            double chunk_rows = 0.0;
+            const int64_t nleaf = int64_t(1) << (2 * L);
+            for (int64_t b = 0; b < nleaf; ++b) {
+                const int32_t t = pl.h_tcnt[size_t(lvl_base(L) + b)];
+                if (t == 0) continue;
+                int chain = 1;
+                for (int l = L - 1; l >= 2 && pl.h_tcnt[size_t(lvl_base(l) + (b >> (2 * (L - l))))] <= cap; --l)
+                    ++chain;
+                chunk_rows += double((t + 63) / 64) * chain;
+            }
+            return chunk_rows * 1.1e-9 + shifts(pl.h_tcnt, cap);
         };
         double bu = 1e30, bd = 1e30;
         for (const int32_t cap : caps) {
-            const double cu = cost(pl.h_scnt, cap, true), cd = cost(pl.h_tcnt, cap, false);
+            const double cu = up_cost(cap), cd = down_cost(cap);
             if (cu < bu) {
                 bu = cu;
                 pl.up_cap = cap;
