@@ -8,11 +8,12 @@
 //     one thread per (a, b), sources staged 32 at a time with their
 //     barycentric weight rows in smem.  Sums run in source order like the
 //     reference loop.
-//   traversal (summation.cpp:449-496): one thread per (Morton-sorted)
-//     target, explicit DFS stack with the reference push order, acceptance
-//     d^2 >= 4.5 s^2 at levels >= min_level, far boxes beyond the decay
-//     cutoff skipped, direct K0 sums at leaves.  Results scatter back to the
-//     original target order.
+//   traversal (summation.cpp:449-496): per target, the reference DFS (push
+//     order, acceptance d^2 >= 4.5 s^2 at levels >= min_level, far boxes
+//     beyond the decay cutoff skipped, direct K0 sums at leaves), executed
+//     warp-cooperatively: 32 neighbouring targets share one stack with lane
+//     masks (traverse_kernel).  Results scatter back to the original target
+//     order.
 #include <algorithm>
 #include <cmath>
 #include <vector>
@@ -99,58 +100,104 @@ __global__ void anterp_kernel(HelmParams hp, int level, const int32_t* src_cnt_l
     if (threadIdx.x < mm) W[hp.w_off[level] + b * mm + threadIdx.x] = acc;
 }
 
-constexpr int kTravThreads = 128;
+// Warp-cooperative traversal.  A warp takes 32 consecutive (Morton-sorted,
+// hence spatially close) targets and walks ONE shared DFS stack in smem
+// whose entries carry the mask of lanes still descending.  For the popped
+// box every active lane makes the reference decision for its own target
+// (skip / proxies / direct leaf / descend); the lanes that take the proxies
+// (or the leaf) evaluate them together -- same box, same W row, broadcast
+// loads, no divergence in the loop structure -- and the descending lanes'
+// mask goes with the four children, pushed in the reference order.  Each
+// lane therefore visits exactly the boxes of its own DFS, in the same
+// order, with the same arithmetic as a per-target traversal: results are
+// those of summation.cpp:449-496 bit for bit.
+constexpr int kTravWarps = 4;
+constexpr int kTravStack = 96;
 
-__global__ void __launch_bounds__(kTravThreads)
+__global__ void __launch_bounds__(kTravWarps * 32)
 traverse_kernel(HelmParams hp, const int32_t* src_cnt, const int32_t* soff,
                 const double2* sxy, const double* q, const double2* txy,
                 const int32_t* tids, int64_t nt, const double* nodes_all,
                 const double* W, const double* k0tab, double* out) {
-    const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-    if (i >= nt) return;
-    const double2 t = txy[i];
+    __shared__ uint64_t st_ent[kTravWarps][kTravStack];
+    __shared__ uint32_t st_mask[kTravWarps][kTravStack];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t i0 = (int64_t(blockIdx.x) * kTravWarps + warp) * 32;
+    if (i0 >= nt) return;
+    const int64_t i = i0 + lane;
+    const bool valid = i < nt;
+    const double2 t = txy[valid ? i : nt - 1];
     const double lambda = hp.lambda;
     double pot = 0.0;
-    uint64_t stack[128];
+    uint64_t* sent = st_ent[warp];
+    uint32_t* smask = st_mask[warp];
     int top = 0;
-    stack[top++] = 0;
+    if (lane == 0) {
+        sent[0] = 0;
+        smask[0] = __ballot_sync(0xffffffffu, valid);
+    } else {
+        (void)__ballot_sync(0xffffffffu, valid);
+    }
+    top = 1;
+    __syncwarp();
     while (top > 0) {
-        const uint64_t ent = stack[--top];
+        --top;
+        const uint64_t ent = sent[top];
+        const uint32_t mask = smask[top];
+        __syncwarp();
         const int l = int(ent >> 32);
         const uint32_t id = uint32_t(ent);
         if (src_cnt[lvl_base(l) + id] == 0) continue;
+        const bool me = (mask >> lane) & 1u;
         const double s = hp.side / double(1 << l);
         const double cx = hp.x0 + (squash2(id) + 0.5) * s;
         const double cy = hp.y0 + (squash2(id >> 1) + 0.5) * s;
         const double dx = t.x - cx, dy = t.y - cy;
         const double d2 = dx * dx + dy * dy;
         const double rbox = s * 0.7071067811865476;
-        if (lambda * (sqrt(d2) - rbox) > hp.skip_x) continue;
-        if (l >= hp.min_level && d2 >= 4.5 * s * s) {
+        const bool skip = lambda * (sqrt(d2) - rbox) > hp.skip_x;
+        const bool proxy = !skip && l >= hp.min_level && d2 >= 4.5 * s * s;
+        const bool direct = !skip && !proxy && l == hp.L;
+        const uint32_t pm = __ballot_sync(0xffffffffu, me && proxy);
+        const uint32_t dm = __ballot_sync(0xffffffffu, me && direct);
+        const uint32_t cm = __ballot_sync(0xffffffffu, me && !skip && !proxy && !direct);
+        if (pm) {
+            const bool on = (pm >> lane) & 1u;
             const int m = hp.m[l];
             const double* wb = W + hp.w_off[l] + int64_t(id) * m * m;
             const double* nd = nodes_all + l * 32;
             const double h = 0.5 * s;
+            double acc = pot;
             for (int a = 0; a < m; ++a) {
                 const double ex = t.x - (cx + h * nd[a]);
                 const double ex2 = ex * ex;
                 for (int bb = 0; bb < m; ++bb) {
                     const double ey = t.y - (cy + h * nd[bb]);
                     const double r = sqrt(fma(ey, ey, ex2));
-                    pot = fma(wb[a * m + bb], kInv2Pi * k0_dev(lambda * r, k0tab), pot);
+                    acc = fma(wb[a * m + bb], kInv2Pi * k0_dev(lambda * r, k0tab), acc);
                 }
             }
-        } else if (l == hp.L) {
+            if (on) pot = acc;
+        }
+        if (dm) {
+            const bool on = (dm >> lane) & 1u;
+            double acc = pot;
             for (int f = soff[id]; f < soff[id + 1]; ++f) {
                 const double2 sp = sxy[f];
-                pot = fma(kInv2Pi, k0_pair(t.x, t.y, sp.x, sp.y, q[f], lambda, k0tab), pot);
+                acc = fma(kInv2Pi, k0_pair(t.x, t.y, sp.x, sp.y, q[f], lambda, k0tab), acc);
             }
-        } else {
-            for (int cc = 0; cc < 4; ++cc)
-                stack[top++] = (uint64_t(l + 1) << 32) | ((uint64_t(id) << 2) | uint64_t(cc));
+            if (on) pot = acc;
+        }
+        if (cm) {
+            if (lane < 4) {
+                sent[top + lane] = (uint64_t(l + 1) << 32) | ((uint64_t(id) << 2) | uint64_t(lane));
+                smask[top + lane] = cm;
+            }
+            top += 4;
+            __syncwarp();
         }
     }
-    out[tids[i]] = pot;
+    if (valid) out[tids[i]] = pot;
 }
 
 __global__ void gather_q_h(const double* q, const int32_t* ids, int64_t n, double* qs) {
@@ -249,7 +296,7 @@ void helm_apply(const Plan& pl, const double* q_dev, double* out_dev,
     mark(4);
     mark(5);
     if (pl.nt > 0) {
-        traverse_kernel<<<nblk(pl.nt, kTravThreads), kTravThreads, 0, st>>>(
+        traverse_kernel<<<nblk(pl.nt, kTravWarps * 32), kTravWarps * 32, 0, st>>>(
             hp, pl.src_cnt.p, pl.src_off.p, pl.src_sorted.p, qs, pl.tgt_sorted.p,
             pl.tgt_ids.p, pl.nt, pl.helm_nodes.p, W, k0_table_dev(), out_dev);
         VPG_LAUNCH_CHECK();
