@@ -21,20 +21,25 @@ namespace vpg {
 constexpr int kK0Intervals = 9;
 constexpr int kK0Coeffs = 25;
 
+// 1/(k!)^2 and H_k/(k!)^2, k = 0..16, in constant memory: the Horner
+// steps take them as c[bank][offset] operands instead of materialising 34
+// double immediates per call site.
+static __constant__ double c_k0_i0[17] = {
+    1.0, 1.0, 0.25, 0.027777777777777776, 0.001736111111111111,
+    6.944444444444444e-05, 1.9290123456790124e-06, 3.936759889140842e-08,
+    6.151187326782565e-10, 7.594058428126624e-12, 7.594058428126623e-14,
+    6.276081345559193e-16, 4.358389823304995e-18, 2.5789288895295828e-20,
+    1.3157800456783586e-22, 5.8479113141260385e-25, 2.2843403570804838e-27};
+static __constant__ double c_k0_h[17] = {
+    0.0, 1.0, 0.375, 0.05092592592592592, 0.003616898148148148,
+    0.0001585648148148148, 4.72608024691358e-06, 1.0207455998272325e-07,
+    1.6718048413148328e-09, 2.1483350211950277e-11, 2.224275605476294e-13,
+    1.895299587006153e-15, 1.3525001839484812e-17, 8.201338813682637e-20,
+    4.278340826570208e-22, 1.9404708872364884e-24, 7.722735675585063e-27};
+
 __device__ __forceinline__ double k0_small(double x) {
-    // 1/(k!)^2 and H_k/(k!)^2, k = 0..16
-    constexpr double c[17] = {
-        1.0, 1.0, 0.25, 0.027777777777777776, 0.001736111111111111,
-        6.944444444444444e-05, 1.9290123456790124e-06, 3.936759889140842e-08,
-        6.151187326782565e-10, 7.594058428126624e-12, 7.594058428126623e-14,
-        6.276081345559193e-16, 4.358389823304995e-18, 2.5789288895295828e-20,
-        1.3157800456783586e-22, 5.8479113141260385e-25, 2.2843403570804838e-27};
-    constexpr double d[17] = {
-        0.0, 1.0, 0.375, 0.05092592592592592, 0.003616898148148148,
-        0.0001585648148148148, 4.72608024691358e-06, 1.0207455998272325e-07,
-        1.6718048413148328e-09, 2.1483350211950277e-11, 2.224275605476294e-13,
-        1.895299587006153e-15, 1.3525001839484812e-17, 8.201338813682637e-20,
-        4.278340826570208e-22, 1.9404708872364884e-24, 7.722735675585063e-27};
+    const double* c = c_k0_i0;
+    const double* d = c_k0_h;
     const double q = 0.25 * x * x;
     double i0 = c[16], s = d[16];
 #pragma unroll

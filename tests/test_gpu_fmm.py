@@ -172,3 +172,51 @@ def test_chain_multilevel_and_hybrid_passes(vp, rest, monkeypatch, env):
         gpu = plan.apply(w.q)
     cpu = rest.plan_sum(0, 0.0, w.src, w.q, w.tgt, 1e-12)
     assert rel_l2(gpu, cpu) <= 1e-13
+
+
+def test_graph_cache_pointer_pairs_and_profiling_agree(vp):
+    """Device-pointer applies are replayed from a per-(q, out) CUDA graph;
+    more pointer pairs than cache slots, host-pointer applies and the
+    profiled (plain-launch) path all give bit-identical potentials."""
+    torch = pytest.importorskip("torch")
+    w = W.cfg2()
+    with vp.SummationPlan(lap(vp), w.src, w.tgt, 1e-12) as plan:
+        ref = plan.apply(w.q)
+        s = torch.cuda.current_stream()
+        qd = torch.tensor(w.q, device="cuda")
+        outs = [torch.empty(w.nt, dtype=torch.float64, device="cuda") for _ in range(11)]
+        for rep in range(2):
+            for o in outs:
+                o.fill_(float("nan"))
+                plan.apply_device(qd.data_ptr(), o.data_ptr(), s.cuda_stream)
+            torch.cuda.synchronize()
+            for o in outs:
+                assert np.array_equal(o.cpu().numpy(), ref)
+        plan.set_profiling(True)
+        prof = plan.apply(w.q)
+        plan.set_profiling(False)
+        assert np.array_equal(prof, ref)
+
+
+def test_concurrent_host_threads(vp):
+    """apply is const and may run from several host threads at once
+    (summation.hpp:32-33): every thread gets the single-thread result."""
+    import threading
+    w = W.cfg1()
+    rng = np.random.default_rng(3)
+    qs = [rng.standard_normal(w.ns) for _ in range(6)]
+    with vp.SummationPlan(lap(vp), w.src, w.tgt, 1e-12) as plan:
+        want = [plan.apply(q) for q in qs]
+        got = [None] * len(qs)
+
+        def run(i):
+            for _ in range(3):
+                got[i] = plan.apply(qs[i])
+
+        th = [threading.Thread(target=run, args=(i,)) for i in range(len(qs))]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+    for a, b in zip(got, want):
+        assert np.array_equal(a, b)
