@@ -21,6 +21,7 @@
  *   correction loop of VolumePotentialOperator::apply
  *                                 (potential.cpp:446-462)  vpg_corr_create/apply
  *   build_charges                 (potential.cpp:397-412)  vpg_charges_create/apply
+ *   VolumePotentialOperator::apply (potential.cpp:431-470) vpg_operator_create/apply
  *
  * Conventions
  *   - Point arrays are interleaved xy float64 (the reference Vec2 is a
@@ -79,6 +80,7 @@ typedef enum { VPG_MODE_REFERENCE = 0, VPG_MODE_NATIVE = 1 } vpg_mode;
 typedef struct vpg_plan vpg_plan;
 typedef struct vpg_corr vpg_corr;
 typedef struct vpg_charges vpg_charges;
+typedef struct vpg_operator vpg_operator;
 
 typedef struct {
     int64_t num_sources, num_targets;
@@ -189,6 +191,22 @@ int vpg_charges_create(int64_t ncell, const int32_t* cell_type,
 int vpg_charges_apply(const vpg_charges* ch, const double* f, int64_t nf,
                       double* charges, unsigned flags, void* stream);
 int vpg_charges_destroy(vpg_charges* ch);
+
+/* The operator-level apply of VolumePotentialOperator::apply
+ * (potential.cpp:431-470), device-resident end to end:
+ *   out = plan.apply(build_charges(f)) + C f
+ * with the charge map, the plan and the correction map borrowed (they must
+ * outlive the operator; ch may be NULL when the plan's sources are the
+ * samples themselves with unit weights, i.e. charges = f).  The operator
+ * owns persistent device buffers, so its FMM step replays the plan's cached
+ * CUDA graph.  timings_ms (may be NULL) receives {smooth, correction} in
+ * milliseconds, split like ApplyTimings (smooth includes build_charges,
+ * potential.cpp:440-444); asking for timings synchronises. */
+int vpg_operator_create(const vpg_plan* plan, const vpg_charges* ch, const vpg_corr* corr,
+                        vpg_operator** op);
+int vpg_operator_apply(const vpg_operator* op, const double* f, int64_t nf, double* out,
+                       unsigned flags, void* stream, float* timings_ms);
+int vpg_operator_destroy(vpg_operator* op);
 
 #ifdef __cplusplus
 }

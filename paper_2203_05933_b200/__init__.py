@@ -9,12 +9,12 @@ C++ API; include/volpot_b200/summation.hpp is the C++ mirror.
 """
 from ._lib import (CoincidentPoint, CudaError, DomainError, InvalidArgument,  # noqa: F401
                    OutOfMemory, VolpotError, device_count)
-from .correction import ChargeMap, CorrectionMap  # noqa: F401
+from .correction import ChargeMap, CorrectionMap, VolumePotentialOperator  # noqa: F401
 from .summation import (Kernel, KernelFamily, SourceSet, SummationPlan,  # noqa: F401
                         accelerated_sum, bessel_k0, direct_sum, make_kernel)
 
 __all__ = [
     "Kernel", "KernelFamily", "make_kernel", "SourceSet", "SummationPlan", "direct_sum",
-    "accelerated_sum", "bessel_k0", "CorrectionMap", "ChargeMap", "InvalidArgument",
+    "accelerated_sum", "bessel_k0", "CorrectionMap", "ChargeMap", "VolumePotentialOperator", "InvalidArgument",
     "CoincidentPoint", "DomainError", "CudaError", "OutOfMemory", "VolpotError", "device_count",
 ]

@@ -107,6 +107,9 @@ _SIGS = {
                                      C.c_int, _P, C.c_int, C.POINTER(_P)]),
     "vpg_charges_apply": (C.c_int, [_P, _P, C.c_int64, _P, C.c_uint, _P]),
     "vpg_charges_destroy": (C.c_int, [_P]),
+    "vpg_operator_create": (C.c_int, [_P, _P, _P, C.POINTER(_P)]),
+    "vpg_operator_apply": (C.c_int, [_P, _P, C.c_int64, _P, C.c_uint, _P, C.POINTER(C.c_float)]),
+    "vpg_operator_destroy": (C.c_int, [_P]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

@@ -110,3 +110,48 @@ class ChargeMap:
             self.close()
         except Exception:
             pass
+
+
+class VolumePotentialOperator:
+    """The operator-level apply of VolumePotentialOperator::apply
+    (potential.cpp:431-470), device-resident: out = plan.apply(
+    build_charges(f)) + C f.  Borrows the plan and maps (keeps Python
+    references so they outlive the operator).  ``charges=None`` means the
+    plan's sources are the samples themselves (charges = f)."""
+
+    def __init__(self, plan, corr: CorrectionMap, charges: "ChargeMap | None" = None):
+        self._keep = (plan, corr, charges)
+        h = C.c_void_p()
+        L.check(L.lib().vpg_operator_create(plan._h, charges._h if charges is not None else None,
+                                            corr._h, C.byref(h)), "VolumePotentialOperator")
+        self._h = h
+        self.ndofs = corr.ndofs
+        self.num_targets = corr.num_targets
+
+    def apply(self, f, timings: bool = False):
+        """Potentials at the targets; with ``timings`` also the ApplyTimings
+        split {smooth_ms, correction_ms} (potential.cpp:440-468)."""
+        fv = _f64(f)
+        out = np.empty(self.num_targets)
+        tm = (C.c_float * 2)()
+        L.check(L.lib().vpg_operator_apply(self._h, _p(fv), fv.size, _p(out), 0, None,
+                                           tm if timings else None), "VolumePotentialOperator.apply")
+        if timings:
+            return out, {"smooth_ms": float(tm[0]), "correction_ms": float(tm[1])}
+        return out
+
+    def apply_device(self, f_ptr, out_ptr, stream=0, sync=False):
+        flags = L.VPG_DEVICE_POINTERS | (0 if sync else L.VPG_NO_SYNC)
+        L.check(L.lib().vpg_operator_apply(self._h, f_ptr, self.ndofs, out_ptr, flags, stream or None, None),
+                "VolumePotentialOperator.apply")
+
+    def close(self):
+        if getattr(self, "_h", None):
+            L.lib().vpg_operator_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

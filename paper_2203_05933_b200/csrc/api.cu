@@ -15,6 +15,7 @@
 
 #include "k0.cuh"
 
+#include "maps.cuh"
 #include "plan.cuh"
 
 struct vpg_plan {
@@ -597,6 +598,114 @@ int vpg_bessel_k0(const double* x, int64_t n, double* out, int device) {
         k0_device(xd.p, n, od.p, cs.s);
         if (n) VPG_CUDA(cudaMemcpyAsync(out, od.p, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, cs.s));
         VPG_CUDA(cudaStreamSynchronize(cs.s));
+    });
+}
+
+
+struct vpg_operator {
+    const vpg_plan* plan = nullptr;
+    const vpg_charges* ch = nullptr;
+    const vpg_corr* corr = nullptr;
+    int device = 0;
+    int64_t ndofs = 0, ns = 0, nt = 0;
+    double* fd = nullptr;  // persistent device buffers: samples, charges, potentials
+    double* qd = nullptr;
+    double* od = nullptr;
+    cudaEvent_t done = nullptr;
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    mutable std::mutex mu;
+    ~vpg_operator() {
+        if (done) cudaEventSynchronize(done);
+        for (cudaEvent_t e : ev)
+            if (e) cudaEventDestroy(e);
+        if (done) cudaEventDestroy(done);
+        cudaFree(fd);
+        cudaFree(qd);
+        cudaFree(od);
+    }
+};
+
+int vpg_operator_create(const vpg_plan* plan, const vpg_charges* ch, const vpg_corr* corr,
+                        vpg_operator** op) {
+    return guarded([&] {
+        if (!plan || !corr || !op) throw Error{VPG_ERR_INVALID_ARGUMENT, "NULL argument"};
+        const Plan& pl = plan->impl;
+        const int64_t ndofs = corr->ndofs;
+        if (corr->nt != pl.nt)
+            throw Error{VPG_ERR_INVALID_ARGUMENT, "operator: correction map has " + std::to_string(corr->nt) +
+                                                      " targets, plan has " + std::to_string(pl.nt)};
+        if (ch ? (ch->nsrc != pl.ns || ch->ndofs != ndofs) : (pl.ns != ndofs))
+            throw Error{VPG_ERR_INVALID_ARGUMENT, "operator: charge map does not match the plan's sources"};
+        if ((ch && ch->device != pl.device) || corr->device != pl.device)
+            throw Error{VPG_ERR_INVALID_ARGUMENT, "operator: maps and plan on different devices"};
+        VPG_CUDA(cudaSetDevice(pl.device));
+        auto o = std::make_unique<vpg_operator>();
+        o->plan = plan;
+        o->ch = ch;
+        o->corr = corr;
+        o->device = pl.device;
+        o->ndofs = ndofs;
+        o->ns = pl.ns;
+        o->nt = pl.nt;
+        VPG_CUDA(cudaMalloc(&o->fd, sizeof(double) * size_t(std::max<int64_t>(ndofs, 1))));
+        VPG_CUDA(cudaMalloc(&o->qd, sizeof(double) * size_t(std::max<int64_t>(pl.ns, 1))));
+        VPG_CUDA(cudaMalloc(&o->od, sizeof(double) * size_t(std::max<int64_t>(pl.nt, 1))));
+        VPG_CUDA(cudaEventCreateWithFlags(&o->done, cudaEventDisableTiming));
+        for (cudaEvent_t& e : o->ev) VPG_CUDA(cudaEventCreate(&e));
+        *op = o.release();
+    });
+}
+
+int vpg_operator_apply(const vpg_operator* op, const double* f, int64_t nf, double* out,
+                       unsigned flags, void* stream, float* timings_ms) {
+    return guarded([&] {
+        if (!op) throw Error{VPG_ERR_INVALID_ARGUMENT, "operator is NULL"};
+        if (nf != op->ndofs)  // potential.cpp:434-438
+            throw Error{VPG_ERR_INVALID_ARGUMENT,
+                        "apply: expected " + std::to_string(op->ndofs) + " samples, got " + std::to_string(nf)};
+        if ((nf > 0 && !f) || (op->nt > 0 && !out)) throw Error{VPG_ERR_INVALID_ARGUMENT, "NULL sample or output array"};
+        VPG_CUDA(cudaSetDevice(op->device));
+        CallStream cs(stream);
+        cudaStream_t st = cs.s;
+        const bool dev = flags & VPG_DEVICE_POINTERS;
+        const unsigned dflags = VPG_DEVICE_POINTERS | VPG_NO_SYNC;
+        std::lock_guard<std::mutex> lk(op->mu);  // persistent buffers: one use at a time per stream order
+        VPG_CUDA(cudaStreamWaitEvent(st, op->done, 0));
+        const double* fdev = dev ? f : op->fd;
+        double* odev = dev ? out : op->od;
+        if (!dev && nf)
+            VPG_CUDA(cudaMemcpyAsync(op->fd, f, sizeof(double) * size_t(nf), cudaMemcpyHostToDevice, st));
+        if (timings_ms) VPG_CUDA(cudaEventRecord(op->ev[0], st));
+        // build_charges (potential.cpp:397-412) -> plan apply (potential.cpp:443)
+        const double* q = fdev;
+        if (op->ch) {
+            const int rc = vpg_charges_apply(op->ch, fdev, nf, op->qd, dflags, st);
+            if (rc) throw Error{rc, vpg_last_error()};
+            q = op->qd;
+        }
+        int rc = vpg_plan_apply(op->plan, q, op->ns, odev, dflags, st);
+        if (rc) throw Error{rc, vpg_last_error()};
+        if (timings_ms) VPG_CUDA(cudaEventRecord(op->ev[1], st));
+        // correction (potential.cpp:446-462): out += C f
+        rc = vpg_corr_apply(op->corr, fdev, nf, odev, dflags, st);
+        if (rc) throw Error{rc, vpg_last_error()};
+        if (timings_ms) VPG_CUDA(cudaEventRecord(op->ev[2], st));
+        if (!dev && op->nt)
+            VPG_CUDA(cudaMemcpyAsync(out, op->od, sizeof(double) * size_t(op->nt), cudaMemcpyDeviceToHost, st));
+        VPG_CUDA(cudaEventRecord(op->done, st));
+        if (timings_ms || !(flags & VPG_NO_SYNC) || cs.owned || !dev) VPG_CUDA(cudaStreamSynchronize(st));
+        if (timings_ms) {
+            VPG_CUDA(cudaEventElapsedTime(&timings_ms[0], op->ev[0], op->ev[1]));
+            VPG_CUDA(cudaEventElapsedTime(&timings_ms[1], op->ev[1], op->ev[2]));
+        }
+    });
+}
+
+int vpg_operator_destroy(vpg_operator* op) {
+    return guarded([&] {
+        if (!op) return;
+        cudaSetDevice(op->device);
+        delete op;
     });
 }
 

@@ -50,3 +50,45 @@ def test_build_charges_matches_restatement(vp, rest):
     gpu = ch.apply(f)
     cpu = rest.build_charges(ct, node_off, src_off, over0, over1, wj, f)
     assert rel_l2(gpu, cpu) <= 1e-14
+
+
+@pytest.mark.parametrize("family", ["laplace", "helmholtz"])
+def test_operator_apply_matches_composition(vp, ref, rest, family):
+    """VolumePotentialOperator::apply (potential.cpp:431-470) on the device:
+    build_charges -> FMM step -> + correction, against the reference plan
+    applied to the restated build_charges plus the restated correction."""
+    n = 20
+    ij = _mesh(n)
+    h = 2.0 / n
+    cx = -1.0 + (ij[:, 0] + 0.5) * h
+    cy = -1.0 + (ij[:, 1] + 0.5) * h
+    pts, wgt = W.box_nodes(cx, cy, h)           # sources = targets = the sample nodes
+    nbox = len(ij)
+    csr = W.correction_csr(nbox, ij, ntri_cells=0)
+    ndofs = int(csr["node_off"][-1])
+    assert ndofs == len(pts)
+    rng = np.random.default_rng(8)
+    over0 = np.eye(64) + 0.01 * rng.standard_normal((64, 64))
+    ct = np.zeros(nbox, np.int32)
+    off = (np.arange(nbox + 1) * 64).astype(np.int32)
+    f = np.exp(-20 * (pts[:, 0] ** 2 + pts[:, 1] ** 2))
+    fam, lam = (0, 0.0) if family == "laplace" else (1, 10.0)
+    k = vp.make_kernel(vp.KernelFamily.Laplace) if fam == 0 else \
+        vp.make_kernel(vp.KernelFamily.ModifiedHelmholtz, lam)
+    with vp.SummationPlan(k, pts, pts, 1e-12) as plan:
+        cm = vp.CorrectionMap(csr["blk_off"], csr["blk_cell"], csr["blk_pool"], csr["pool_off"],
+                              csr["pool_vals"], csr["node_off"])
+        ch = vp.ChargeMap(ct, off, off, over0, np.zeros((0, 0)), wgt)
+        op = vp.VolumePotentialOperator(plan, cm, ch)
+        out, tm = op.apply(f, timings=True)
+        again = op.apply(f)
+        with pytest.raises(vp.InvalidArgument, match="apply: expected"):
+            op.apply(f[:-1])
+        op.close()
+    assert np.array_equal(out, again)
+    assert tm["smooth_ms"] > 0 and tm["correction_ms"] > 0
+    q = rest.build_charges(ct, off, off, over0, np.zeros((0, 0)), wgt, f)
+    smooth = ref.plan(fam, lam, pts, pts, 1e-12).apply(q)
+    want = rest.correction_apply(csr["blk_off"], csr["blk_cell"], csr["blk_pool"], csr["pool_off"],
+                                 csr["pool_vals"], csr["node_off"], f, smooth)
+    assert rel_l2(out, want) <= 1e-13
