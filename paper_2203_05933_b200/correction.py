@@ -145,6 +145,12 @@ class VolumePotentialOperator:
         L.check(L.lib().vpg_operator_apply(self._h, f_ptr, self.ndofs, out_ptr, flags, stream or None, None),
                 "VolumePotentialOperator.apply")
 
+    def apply_host_ptr(self, f_ptr, out_ptr, stream=0, sync=True):
+        """Host-pointer apply (pinned buffers for async copies)."""
+        flags = 0 if sync else L.VPG_NO_SYNC
+        L.check(L.lib().vpg_operator_apply(self._h, f_ptr, self.ndofs, out_ptr, flags, stream or None, None),
+                "VolumePotentialOperator.apply")
+
     def close(self):
         if getattr(self, "_h", None):
             L.lib().vpg_operator_destroy(self._h)

@@ -216,8 +216,10 @@ def cfg5(seed=5, n_side=192, ntri=2000):
     cen = rng.uniform(-0.6, 0.6, size=(3, 2))
     alpha = rng.uniform(20, 80, size=3)
     f = sum(gaussian(p, cen[k], alpha[k]) for k in range(3))
+    ij = np.stack([np.rint((cx + 1.3) / h - 0.5), np.rint((cy + 1.3) / h - 0.5)], 1).astype(np.int64)
     wl = Workload("cfg5", p, w * f, p.copy(), kernel="helmholtz", lam=10.0,
-                  notes={"boxes": len(cx), "triangles": ntri, "h": h, "f": f})
+                  notes={"boxes": len(cx), "triangles": ntri, "h": h, "f": f, "w": w,
+                         "corr": lambda: correction_csr(len(cx), ij, ntri)})
     return wl
 
 
@@ -235,33 +237,42 @@ def correction_csr(nbox_cells, box_ij, ntri_cells, seed=55, np_box=64, np_tri=64
     node_off = np.zeros(ncell + 1, np.int64)
     node_off[1:nbox_cells + 1] = np.arange(1, nbox_cells + 1) * np_box
     node_off[nbox_cells + 1:] = nbox_cells * np_box + np.arange(1, ntri_cells + 1) * np_tri
-    index = {tuple(ij): k for k, ij in enumerate(map(tuple, box_ij))}
     offsets = [(0, 0)] + [(dx, dy) for dy in (-1, 0, 1) for dx in (-1, 0, 1) if (dx, dy) != (0, 0)]
     # shared lattice rows: 9 offsets x np_box local nodes
     lattice = rng.standard_normal((len(offsets), np_box, np_box)) * 1e-3
-    blk_cell, blk_pool, blk_off = [], [], [0]
     pool_rows = [lattice.reshape(-1, np_box)]
     npool = len(offsets) * np_box
-    for c, (i, j) in enumerate(map(tuple, box_ij)):
-        nbrs = [(o, index.get((i + o[0], j + o[1]))) for o in offsets]
-        nbrs = [(k, cell) for k, (o, cell) in enumerate(nbrs) if cell is not None]
-        for t in range(np_box):
-            for k, cell in nbrs:
-                blk_cell.append(cell)
-                blk_pool.append(k * np_box + t)
-            blk_off.append(len(blk_cell))
+    # neighbour table (box, offset) -> cell or -1, via a dense grid index
+    box_ij = np.asarray(box_ij, np.int64).reshape(-1, 2)
+    if nbox_cells:
+        lo = box_ij.min(0) - 1
+        dims = box_ij.max(0) - lo + 2
+        grid = np.full((dims[0], dims[1]), -1, np.int64)
+        grid[box_ij[:, 0] - lo[0], box_ij[:, 1] - lo[1]] = np.arange(nbox_cells)
+        nbr = np.stack([grid[box_ij[:, 0] + o[0] - lo[0], box_ij[:, 1] + o[1] - lo[1]] for o in offsets], 1)
+    else:
+        nbr = np.zeros((0, len(offsets)), np.int64)
+    # box targets: cell-major, node t, existing neighbours in offset order
+    exist = nbr >= 0                                             # (nbox, 9)
+    cells = np.broadcast_to(nbr[:, None, :], (nbox_cells, np_box, len(offsets)))
+    pools = (np.arange(len(offsets))[None, None, :] * np_box + np.arange(np_box)[None, :, None])
+    pools = np.broadcast_to(pools, cells.shape)
+    m = np.broadcast_to(exist[:, None, :], cells.shape)
+    box_cell = cells[m]
+    box_pool = pools[m]
+    box_cnt = np.repeat(exist.sum(1), np_box)
     tri_rows = rng.standard_normal((ntri_cells * np_tri, np_tri)) * 1e-3
-    for c in range(ntri_cells):
-        for t in range(np_tri):
-            blk_cell.append(nbox_cells + c)
-            blk_pool.append(npool + c * np_tri + t)
-            blk_off.append(len(blk_cell))
+    tri_cell = np.repeat(nbox_cells + np.arange(ntri_cells), np_tri)
+    tri_pool = npool + np.arange(ntri_cells * np_tri)
+    blk_cell = np.concatenate([box_cell, tri_cell])
+    blk_pool = np.concatenate([box_pool, tri_pool])
+    blk_off = np.concatenate([[0], np.cumsum(np.concatenate([box_cnt, np.ones(ntri_cells * np_tri, np.int64)]))])
     pool_rows.append(tri_rows)
     vals = np.concatenate([r.reshape(-1) for r in pool_rows])
     lens = np.concatenate([np.full(len(offsets) * np_box, np_box), np.full(ntri_cells * np_tri, np_tri)])
     pool_off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
-    return {"blk_off": np.array(blk_off, np.int32), "blk_cell": np.array(blk_cell, np.int32),
-            "blk_pool": np.array(blk_pool, np.int32), "pool_off": pool_off, "pool_vals": vals,
+    return {"blk_off": blk_off.astype(np.int32), "blk_cell": blk_cell.astype(np.int32),
+            "blk_pool": blk_pool.astype(np.int32), "pool_off": pool_off, "pool_vals": vals,
             "node_off": node_off.astype(np.int32)}
 
 
