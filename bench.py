@@ -42,10 +42,15 @@ THROTTLE_BITS = {
 }
 
 
-def fp64_peak_tflops():
+def fp64_peak_tflops(pipe="any"):
+    """Measured FP64 peak on this pool's B200 (profiles/fp64_peak_r01.json):
+    the DMMA (tensor) figure for tensor-core kernels, the DFMA figure for
+    FP64 CUDA-core kernels, the larger of the two for "any"."""
     with open(FP64_PEAK_FILE) as f:
         rows = [json.loads(x) for x in f if x.strip()]
-    return max(max(r.get("fp64_dfma_tflops_best", 0.0), r.get("fp64_dmma_tflops_best", 0.0)) for r in rows)
+    dfma = max(r.get("fp64_dfma_tflops_best", 0.0) for r in rows)
+    dmma = max(r.get("fp64_dmma_tflops_best", 0.0) for r in rows)
+    return {"tensor": dmma, "fp64": dfma}.get(pipe, max(dfma, dmma))
 
 
 def hbm_peak_gbs():
@@ -111,6 +116,17 @@ class ClockSampler:
         reasons = [n for b, n in THROTTLE_BITS.items() if mask & b and n != "gpu_idle"]
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(r[1] for r in self.rows),
                 "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_traffic(workload, kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture
+    (profiles/traffic_r01.json), or None when that workload was not captured."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic_r01.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(workload, {}).get(kernel)
+    except (OSError, ValueError):
+        return None
 
 
 def load_workload(name):
@@ -358,12 +374,17 @@ def run_gpu(args):
         dom = "m2l" if phases["m2l"] >= phases["p2p"] else "p2p"
         flops = m2l_flops if dom == "m2l" else p2p_flops
         achieved = flops / (phases[dom] * 1e-3) / 1e12
-        roofline = {"bound": "fp64", "kernel": "m2l_kernel" if dom == "m2l" else "l2p_p2p_kernel",
+        kname = "m2l_kernel" if dom == "m2l" else "l2p_p2p_kernel"
+        bound = "tensor" if dom == "m2l" else "fp64"
+        peak = fp64_peak_tflops(bound)
+        roofline = {"bound": bound, "kernel": kname,
                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                    "traffic": None,
-                    "peak_source": "measured FP64 peak, max of DFMA (tools/fp64_peak.cu) and DMMA "
-                                   "(tools/dmma_peak.cu) microbenchmarks, profiles/fp64_peak_r01.json; "
-                                   "MEASURED_PEAKS.json has no FP64 entry",
+                    "traffic": measured_traffic(args.workload, kname),
+                    "peak_source": ("measured FP64 tensor-core (DMMA, tools/dmma_peak.cu)" if bound == "tensor"
+                                    else "measured FP64 CUDA-core (DFMA, tools/fp64_peak.cu)")
+                                   + " peak, profiles/fp64_peak_r01.json; MEASURED_PEAKS.json has no FP64 entry",
+                    "bound_note": ("M2L runs on the FP64 tensor cores (mma.sync m8n8k4 f64)" if bound == "tensor"
+                                   else "the near-field log sum is FP64 CUDA-core work (no tensor-core form)"),
                     "flops_per_unit": ("4P(P+1)+8(P+1)+6P executed per M2L pair" if dom == "m2l"
                                        else "27 per near-field pair (SURVEY.md 8d convention)")}
     else:
