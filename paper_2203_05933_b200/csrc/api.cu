@@ -303,8 +303,12 @@ int vpg_plan_create(int family, double lambda, const double* src_xy, int64_t ns,
         if (nt) VPG_CUDA(cudaMemcpy(pl.tgt.p, tgt_xy, sizeof(double2) * size_t(nt), cudaMemcpyHostToDevice));
         build_tree(pl);
         if (!pl.direct) {
-            if (family == VPG_LAPLACE) build_laplace_ops(pl);
-            else build_helm_ops(pl);
+            if (family == VPG_LAPLACE) {
+                build_laplace_ops(pl);
+            } else {
+                build_helm_ops(pl);                           // reference treecode
+                if (mode == VPG_MODE_NATIVE) build_helm_fmm(pl);  // Chebyshev FMM when applicable
+            }
         }
         (void)log_table_dev();
         (void)k0_table_dev();

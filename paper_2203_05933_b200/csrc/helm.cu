@@ -18,6 +18,9 @@
 #include <cmath>
 #include <vector>
 
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+
 #include "k0.cuh"
 #include "plan.cuh"
 
@@ -221,6 +224,245 @@ HelmParams make_params(const Plan& pl) {
     return hp;
 }
 
+
+// ===================================================== native-mode FMM ==
+// Compressed Chebyshev-interpolation FMM for G = (1/2pi) K0(lambda r)
+// (kernel-independent, Fong & Darve): each box at levels lmin..L carries
+// values at n x n Chebyshev nodes.
+//   P2M   leaves: W[a][b] = sum_j q_j l_a(x_j) l_b(y_j) (anterp_kernel);
+//   M2M   W_P = sum_c S_c W_c S_c^T, S_c[a][a'] = l^P_a(x^C_a') (exact:
+//         same n on both sides), children in quadrant order;
+//   M2L   through a per-level rank-k SVD basis V of the stacked kernel
+//         matrices K_o (offsets o, symmetric set => one basis serves both
+//         sides): Wt = V^T W, Lt_T = sum_o C_o Wt_S with C_o = V^T K_o V,
+//         entries in list order; lists: children of the parent's 3x3
+//         neighbours not adjacent to T, and at lmin (the first level with
+//         lambda s <= 5, like the treecode's proxies, summation.cpp:367-372)
+//         every non-adjacent box; pairs beyond the decay cutoff
+//         lambda (d - sqrt(2) s) > skip_x dropped;
+//   L2L   Lv_child = V Lt_child + S_c^T Lv_P S_c;
+//   L2P + near field: barycentric evaluation of the leaf's Lv at the target
+//         plus direct (1/2pi) K0 over the 3x3 neighbour leaves (r = 0 skipped,
+//         summation.cpp:486).
+// n and k follow epsilon; the basis, the C_o and the lists are built once
+// per plan (cuSOLVER SVD and cuBLAS GEMMs at plan time only).
+constexpr int kHfMaxN = 20;
+constexpr int kHfMaxK = 64;
+constexpr int kHfWarps = 8;
+
+__global__ void hf_kmat_kernel(const int2* offs, int noff, int n, const double* nodes, double s,
+                               double lambda, const double* k0tab, double* A) {
+    const int n2 = n * n;
+    const int64_t m = int64_t(noff) * n2;
+    const int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (idx >= m * n2) return;
+    const int64_t row = idx % m;
+    const int col = int(idx / m);
+    const int o = int(row / n2), t = int(row % n2);
+    const int ta = t / n, tb = t % n, sa = col / n, sb = col % n;
+    const double dx = offs[o].x * s + (nodes[ta] - nodes[sa]) * 0.5 * s;
+    const double dy = offs[o].y * s + (nodes[tb] - nodes[sb]) * 0.5 * s;
+    A[idx] = kInv2Pi * k0_dev(lambda * sqrt(dx * dx + dy * dy), k0tab);
+}
+
+// W_P = sum_c S_{c&1} W_c S_{c>>1}^T over children with sources (c order)
+__global__ void hf_m2m_kernel(int level, int n, const double* S, const int32_t* scnt_l,
+                              const int32_t* scnt_c, int64_t base_p, int64_t base_c, double* W) {
+    __shared__ double wc[kHfMaxN * kHfMaxN], tt[kHfMaxN * kHfMaxN];
+    const int64_t b = blockIdx.x;
+    if (scnt_l[b] == 0) return;
+    const int n2 = n * n;
+    const int t = threadIdx.x;
+    const int a = t / n, bb = t % n;
+    double acc = 0.0;
+    for (int c = 0; c < 4; ++c) {
+        const int64_t child = (b << 2) | c;
+        if (scnt_c[child] == 0) continue;
+        __syncthreads();
+        if (t < n2) wc[t] = W[(base_c + child) * n2 + t];
+        __syncthreads();
+        const double* Sx = S + (c & 1) * n * n;
+        const double* Sy = S + (c >> 1) * n * n;
+        if (t < n2) {
+            double v = 0.0;
+            for (int k = 0; k < n; ++k) v = fma(Sx[a * n + k], wc[k * n + bb], v);
+            tt[t] = v;
+        }
+        __syncthreads();
+        if (t < n2)
+            for (int k = 0; k < n; ++k) acc = fma(Sy[bb * n + k], tt[a * n + k], acc);
+    }
+    if (t < n2) W[(base_p + b) * n2 + t] = acc;
+}
+
+struct HfLevels {
+    int lmin, L, n, k;
+    int64_t base[17];    // first row of each level
+    int64_t voff[17];    // V offsets (doubles) per level
+};
+
+// Wt[r] = V_l^T W[r] for rows with sources (thread per basis vector)
+__global__ void hf_compress_kernel(HfLevels hl, const int32_t* src_cnt, const double* Vt,
+                                   const double* W, double* Wt) {
+    const int64_t r = blockIdx.x;
+    int l = hl.lmin;
+    while (l < hl.L && r >= hl.base[l + 1]) ++l;
+    const int64_t b = r - hl.base[l];
+    if (src_cnt[lvl_base(l) + b] == 0) return;
+    const int n2 = hl.n * hl.n, k = hl.k;
+    const int i = threadIdx.x;
+    if (i >= k) return;
+    const double* v = Vt + hl.voff[l];
+    const double* w = W + r * n2;
+    double acc = 0.0;
+    for (int j = 0; j < n2; ++j) acc = fma(v[j * k + i], w[j], acc);
+    Wt[r * k + i] = acc;
+}
+
+// Lt[T] = sum over T's entries (list order) of C_e Wt[src_e]
+__global__ void hf_m2l_kernel(int k, const int32_t* tbox, const int32_t* toff, const int32_t* esrc,
+                              const int32_t* eop, const double* C, const double* Wt, double* Lt) {
+    __shared__ double ws[kHfMaxK];
+    const int64_t ti = blockIdx.x;
+    const int i = threadIdx.x;
+    double acc = 0.0;
+    for (int e = toff[ti]; e < toff[ti + 1]; ++e) {
+        __syncthreads();
+        if (i < k) ws[i] = Wt[int64_t(esrc[e]) * k + i];
+        __syncthreads();
+        if (i < k) {
+            const double* c = C + int64_t(eop[e]) * k * k;
+            for (int j = 0; j < k; ++j) acc = fma(c[j * k + i], ws[j], acc);
+        }
+    }
+    if (i < k) Lt[int64_t(tbox[ti]) * k + i] = acc;
+}
+
+// Lv[r] = V_l Lt[r] (+ the parent's Lv interpolated to r's nodes)
+__global__ void hf_expand_kernel(HfLevels hl, int level, const int32_t* tbox, const double* Vc,
+                                 const double* S, const double* Lt, double* Lv) {
+    __shared__ double lp[kHfMaxN * kHfMaxN], tt[kHfMaxN * kHfMaxN], lts[kHfMaxK];
+    const int n = hl.n, n2 = n * n, k = hl.k;
+    const int64_t r = tbox[blockIdx.x];
+    const int t = threadIdx.x;
+    const int a = t / n, bb = t % n;
+    if (t < k) lts[t] = Lt[r * k + t];
+    const bool child = level > hl.lmin;
+    const int64_t b = r - hl.base[level];
+    if (child && t < n2) lp[t] = Lv[(hl.base[level - 1] + (b >> 2)) * n2 + t];
+    __syncthreads();
+    double v = 0.0;
+    if (t < n2) {
+        const double* vc = Vc + hl.voff[level];
+        for (int i = 0; i < k; ++i) v = fma(vc[int64_t(i) * n2 + t], lts[i], v);
+    }
+    if (child) {
+        const int c = int(b & 3);
+        const double* Sx = S + (c & 1) * n * n;
+        const double* Sy = S + (c >> 1) * n * n;
+        // tt[a'][b] = sum_b' Sy[b'][b] lp[a'][b']; v += sum_a' Sx[a'][a] tt[a'][b]
+        if (t < n2) {
+            double u = 0.0;
+            for (int q = 0; q < n; ++q) u = fma(Sy[q * n + bb], lp[a * n + q], u);
+            tt[t] = u;
+        }
+        __syncthreads();
+        if (t < n2)
+            for (int q = 0; q < n; ++q) v = fma(Sx[q * n + a], tt[q * n + bb], v);
+    }
+    if (t < n2) Lv[r * n2 + t] = v;
+}
+
+// barycentric weights of x in [-1, 1] on the n Chebyshev nodes (exact node -> delta)
+__device__ __forceinline__ void hf_bary(const double* nodes, const double* bw, int n, double x, double* w) {
+    int hit = -1;
+    double sum = 0.0;
+#pragma unroll
+    for (int a = 0; a < kHfMaxN; ++a) {
+        if (a < n) {
+            const double d = x - nodes[a];
+            if (d == 0.0) hit = a;
+            w[a] = bw[a] / (d == 0.0 ? 1.0 : d);
+            sum += w[a];
+        }
+    }
+    const double inv = 1.0 / sum;
+#pragma unroll
+    for (int a = 0; a < kHfMaxN; ++a)
+        if (a < n) w[a] = hit >= 0 ? (a == hit ? 1.0 : 0.0) : w[a] * inv;
+}
+
+// Warp per near-field chunk: far field from the leaf's Lv (barycentric) plus
+// the direct 3x3-leaf K0 sum; out = far + near in the original order.
+__global__ void __launch_bounds__(kHfWarps * 32)
+hf_l2p_p2p_kernel(HfLevels hl, const P2PChunk* chunks, int64_t nchunks, const int2* ranges,
+                  const int32_t* tgt_row, const double2* sxy, const double* q, const double2* txy,
+                  const int32_t* tids, const double* tab, const double* Lv, double x0, double y0,
+                  double side, double lambda, const double* k0tab, double* out) {
+    __shared__ double lvs[kHfWarps][kHfMaxN * kHfMaxN];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int n = hl.n, n2 = n * n;
+    const double* nodes = tab;
+    const double* bw = tab + 32;
+    double* L = lvs[warp];
+    for (int64_t ci = int64_t(blockIdx.x) * kHfWarps + warp; ci < nchunks;
+         ci += int64_t(gridDim.x) * kHfWarps) {
+        const P2PChunk c = chunks[ci];
+        if (c.part != 0) continue;  // split chunks: once, whole
+        const int64_t row = tgt_row[c.tbegin];  // leaf row (uniform tree, level L)
+        const int64_t leaf = row - (lvl_base(hl.L) - lvl_base(2));
+        const double s = side / double(1 << hl.L);
+        const double cx = x0 + (squash2(uint32_t(leaf)) + 0.5) * s;
+        const double cy = y0 + (squash2(uint32_t(leaf) >> 1) + 0.5) * s;
+        const int64_t hrow = hl.base[hl.L] + leaf;
+        __syncwarp();
+        for (int j = lane; j < n2; j += 32) L[j] = Lv[hrow * n2 + j];
+        __syncwarp();
+        for (int u = 0; u < 2; ++u) {
+            const int li = lane + 32 * u;
+            if (u == 1 && c.tcount <= 32) break;  // warp-uniform
+            const bool on = li < c.tcount;
+            const double2 t = txy[c.tbegin + (on ? li : 0)];
+            // far: sum_ab lx_a ly_b L[a][b]
+            double lx[kHfMaxN], ly[kHfMaxN];
+            hf_bary(nodes, bw, n, (t.x - cx) * 2.0 / s, lx);
+            hf_bary(nodes, bw, n, (t.y - cy) * 2.0 / s, ly);
+            double far = 0.0;
+#pragma unroll
+            for (int a = 0; a < kHfMaxN; ++a) {
+                if (a < n) {
+                    double inner = 0.0;
+#pragma unroll
+                    for (int b2 = 0; b2 < kHfMaxN; ++b2)
+                        if (b2 < n) inner = fma(ly[b2], L[a * n + b2], inner);
+                    far = fma(lx[a], inner, far);
+                }
+            }
+            // near: 3x3 leaves, sources broadcast 32 at a time
+            double near = 0.0;
+            for (int ri = 0; ri < c.rcount; ++ri) {
+                const int2 rg = ranges[c.rfirst + ri];
+                for (int base = rg.x; base < rg.x + rg.y; base += 32) {
+                    const int cnt = min(32, rg.x + rg.y - base);
+                    double2 sp = make_double2(0.0, 0.0);
+                    double qj = 0.0;
+                    if (lane < cnt) {
+                        sp = sxy[base + lane];
+                        qj = q[base + lane];
+                    }
+                    for (int j = 0; j < cnt; ++j) {
+                        const double px = __shfl_sync(0xffffffffu, sp.x, j);
+                        const double py = __shfl_sync(0xffffffffu, sp.y, j);
+                        const double pq = __shfl_sync(0xffffffffu, qj, j);
+                        near = fma(kInv2Pi, k0_pair(t.x, t.y, px, py, pq, lambda, k0tab), near);
+                    }
+                }
+            }
+            if (on) out[tids[c.tbegin + li]] = far + near;
+        }
+    }
+}
+
 }  // namespace
 
 void build_helm_ops(Plan& pl) {
@@ -258,8 +500,15 @@ void build_helm_ops(Plan& pl) {
     VPG_CUDA(cudaMemcpy(pl.helm_bw.p, bw.data(), pl.helm_bw.bytes(), cudaMemcpyHostToDevice));
 }
 
+void helm_fmm_apply(const Plan& pl, const double* q_dev, double* out_dev, cudaStream_t st, cudaEvent_t* ev,
+                    int64_t& launches);
+
 void helm_apply(const Plan& pl, const double* q_dev, double* out_dev,
                 cudaStream_t st, cudaEvent_t* ev, int64_t& launches) {
+    if (pl.hf) {
+        helm_fmm_apply(pl, q_dev, out_dev, st, ev, launches);
+        return;
+    }
     auto mark = [&](int i) {
         if (ev) VPG_CUDA(cudaEventRecord(ev[i], st));
     };
@@ -299,6 +548,344 @@ void helm_apply(const Plan& pl, const double* q_dev, double* out_dev,
         traverse_kernel<<<nblk(pl.nt, kTravWarps * 32), kTravWarps * 32, 0, st>>>(
             hp, pl.src_cnt.p, pl.src_off.p, pl.src_sorted.p, qs, pl.tgt_sorted.p,
             pl.tgt_ids.p, pl.nt, pl.helm_nodes.p, W, k0_table_dev(), out_dev);
+        VPG_LAUNCH_CHECK();
+        ++launches;
+    }
+    mark(6);
+}
+
+
+namespace {
+
+struct CuHandles {
+    cusolverDnHandle_t sol = nullptr;
+    cublasHandle_t blas = nullptr;
+    ~CuHandles() {
+        if (sol) cusolverDnDestroy(sol);
+        if (blas) cublasDestroy(blas);
+    }
+};
+
+#define VPG_SOLVER(call)                                                                     \
+    do {                                                                                     \
+        const int st_ = int(call);                                                           \
+        if (st_ != 0) throw ::vpg::Error{VPG_ERR_CUDA, std::string(#call) + " failed: " + std::to_string(st_)}; \
+    } while (0)
+
+HfLevels hf_levels(const Plan& pl) {
+    HfLevels hl{};
+    hl.lmin = pl.hf_lmin;
+    hl.L = pl.L;
+    hl.n = pl.hf_n;
+    hl.k = pl.hf_k;
+    for (int l = 0; l <= pl.L && l < 17; ++l) {
+        hl.base[l] = pl.hf_row_base[size_t(l)];
+        hl.voff[l] = pl.hf_V_off[size_t(l)];
+    }
+    return hl;
+}
+
+}  // namespace
+
+// Native-mode plan build for modified Helmholtz (see the block comment at
+// hf_kmat_kernel).  Leaves pl.hf false (treecode fallback) when no level is
+// fine enough for the interpolation (lambda s > 5 at every level).
+void build_helm_fmm(Plan& pl) {
+    const int L = pl.L;
+    int lmin = 2;
+    while (lmin <= L && pl.lambda * (pl.side / double(1 << lmin)) > 5.0) ++lmin;
+    if (lmin > L || L > 16) return;
+    const int n = std::clamp(int(std::ceil(1.5 * std::log10(1.0 / pl.eps))), 8, kHfMaxN);
+    const int n2 = n * n;
+    const double pi = 3.14159265358979323846;
+    // nodes (first kind), barycentric weights, child-half interpolation S[h][a][a']
+    std::vector<double> tab(64 + size_t(2) * n * n, 0.0);
+    for (int a = 0; a < n; ++a) {
+        const double th = (2 * a + 1) * pi / (2 * n);
+        tab[size_t(a)] = std::cos(th);
+        tab[size_t(32 + a)] = (a % 2 ? -1.0 : 1.0) * std::sin(th);
+    }
+    for (int h = 0; h < 2; ++h)
+        for (int ap = 0; ap < n; ++ap) {
+            const double x = (h ? 0.5 : -0.5) + 0.5 * tab[size_t(ap)];
+            std::vector<double> w(static_cast<size_t>(n));
+            int hit = -1;
+            double sum = 0.0;
+            for (int a = 0; a < n; ++a) {
+                const double d = x - tab[size_t(a)];
+                if (d == 0.0) hit = a;
+                w[size_t(a)] = tab[size_t(32 + a)] / (d == 0.0 ? 1.0 : d);
+                sum += w[size_t(a)];
+            }
+            for (int a = 0; a < n; ++a)
+                tab[64 + size_t(h) * n * n + size_t(a) * n + ap] =
+                    hit >= 0 ? (a == hit ? 1.0 : 0.0) : w[size_t(a)] / sum;
+        }
+    // rows of levels lmin..L
+    pl.hf_row_base.assign(size_t(L + 2), 0);
+    int64_t rows = 0;
+    for (int l = lmin; l <= L; ++l) {
+        pl.hf_row_base[size_t(l)] = rows;
+        rows += int64_t(1) << (2 * l);
+    }
+    pl.hf_row_base[size_t(L + 1)] = rows;
+    pl.hf_rows = rows;
+
+    // offsets per level (T - S in box units); pruned beyond the decay cutoff
+    const double skip_x = std::log(1.0 / pl.eps) + 12.0;
+    std::vector<std::vector<int2>> offs(size_t(L + 1));
+    for (int l = lmin; l <= L; ++l) {
+        const double s = pl.side / double(1 << l);
+        const int R = l == lmin ? (1 << l) - 1 : 3;
+        for (int dy = -R; dy <= R; ++dy)
+            for (int dx = -R; dx <= R; ++dx) {
+                if (std::max(std::abs(dx), std::abs(dy)) < 2) continue;
+                if (pl.lambda * (std::hypot(double(dx), double(dy)) * s - std::sqrt(2.0) * s) > skip_x) continue;
+                offs[size_t(l)].push_back(make_int2(dx, dy));
+            }
+    }
+
+    DBuf<double> dtab;
+    dtab.alloc(tab.size());
+    VPG_CUDA(cudaMemcpy(dtab.p, tab.data(), dtab.bytes(), cudaMemcpyHostToDevice));
+    CuHandles hd;
+    VPG_SOLVER(cusolverDnCreate(&hd.sol));
+    VPG_SOLVER(cublasCreate(&hd.blas));
+    const double* k0tab = k0_table_dev();
+
+    // per level: SVD of the stacked K_o -> right singular vectors
+    std::vector<std::vector<double>> vt_all(size_t(L + 1));  // VT (n2 x n2, column-major) per level
+    int k = 1;
+    const double tol = pl.eps * 0.1;
+    for (int l = lmin; l <= L; ++l) {
+        const auto& of = offs[size_t(l)];
+        if (of.empty()) continue;
+        const int noff = int(of.size());
+        const int64_t m = int64_t(noff) * n2;
+        DBuf<int2> doff;
+        doff.alloc(of.size());
+        VPG_CUDA(cudaMemcpy(doff.p, of.data(), doff.bytes(), cudaMemcpyHostToDevice));
+        DBuf<double> A, S, VT;
+        A.alloc(size_t(m) * n2);
+        S.alloc(size_t(n2));
+        VT.alloc(size_t(n2) * n2);
+        const double s = pl.side / double(1 << l);
+        hf_kmat_kernel<<<unsigned((m * n2 + 255) / 256), 256>>>(doff.p, noff, n, dtab.p, s, pl.lambda, k0tab, A.p);
+        VPG_LAUNCH_CHECK();
+        int lwork = 0;
+        VPG_SOLVER(cusolverDnDgesvd_bufferSize(hd.sol, int(m), n2, &lwork));
+        DBuf<double> work, rwork;
+        DBuf<int> info;
+        work.alloc(size_t(std::max(lwork, 1)));
+        rwork.alloc(size_t(n2));
+        info.alloc(1);
+        VPG_SOLVER(cusolverDnDgesvd(hd.sol, 'N', 'A', int(m), n2, A.p, int(m), S.p, nullptr, 1, VT.p, n2,
+                                    work.p, lwork, rwork.p, info.p));
+        int hinfo = 0;
+        VPG_CUDA(cudaMemcpy(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost));
+        if (hinfo != 0) throw Error{VPG_ERR_CUDA, "helmholtz FMM: SVD failed (" + std::to_string(hinfo) + ")"};
+        std::vector<double> sv(static_cast<size_t>(n2));
+        VPG_CUDA(cudaMemcpy(sv.data(), S.p, S.bytes(), cudaMemcpyDeviceToHost));
+        int r = 0;
+        while (r < n2 && sv[size_t(r)] > tol * sv[0]) ++r;
+        k = std::max(k, r);
+        vt_all[size_t(l)].resize(size_t(n2) * n2);
+        VPG_CUDA(cudaMemcpy(vt_all[size_t(l)].data(), VT.p, VT.bytes(), cudaMemcpyDeviceToHost));
+    }
+    k = std::min(k, kHfMaxK);
+    // V per level in both layouts; C_o = V^T K_o V
+    pl.hf_V_off.assign(size_t(L + 2), 0);
+    pl.hf_C_off.assign(size_t(L + 2), 0);
+    std::vector<double> vt_rm, vc_cm;  // [n2][k] and [k][n2]
+    int64_t coff = 0;
+    for (int l = lmin; l <= L; ++l) {
+        pl.hf_V_off[size_t(l)] = int64_t(vt_rm.size());
+        pl.hf_C_off[size_t(l)] = coff;
+        const auto& VT = vt_all[size_t(l)];
+        for (int j = 0; j < n2; ++j)
+            for (int i = 0; i < k; ++i) vt_rm.push_back(VT.empty() ? 0.0 : VT[size_t(i) + size_t(j) * n2]);
+        for (int i = 0; i < k; ++i)
+            for (int j = 0; j < n2; ++j) vc_cm.push_back(VT.empty() ? 0.0 : VT[size_t(i) + size_t(j) * n2]);
+        coff += int64_t(offs[size_t(l)].size()) * k * k;
+    }
+    pl.hf_Vt.alloc(vt_rm.size());
+    pl.hf_Vc.alloc(vc_cm.size());
+    VPG_CUDA(cudaMemcpy(pl.hf_Vt.p, vt_rm.data(), pl.hf_Vt.bytes(), cudaMemcpyHostToDevice));
+    VPG_CUDA(cudaMemcpy(pl.hf_Vc.p, vc_cm.data(), pl.hf_Vc.bytes(), cudaMemcpyHostToDevice));
+    pl.hf_C.alloc(size_t(std::max<int64_t>(coff, 1)));
+    for (int l = lmin; l <= L; ++l) {
+        const auto& of = offs[size_t(l)];
+        if (of.empty()) continue;
+        const int noff = int(of.size());
+        const int64_t m = int64_t(noff) * n2;
+        DBuf<int2> doff;
+        doff.alloc(of.size());
+        VPG_CUDA(cudaMemcpy(doff.p, of.data(), doff.bytes(), cudaMemcpyHostToDevice));
+        DBuf<double> A, X;
+        A.alloc(size_t(m) * n2);
+        X.alloc(size_t(m) * k);
+        const double s = pl.side / double(1 << l);
+        hf_kmat_kernel<<<unsigned((m * n2 + 255) / 256), 256>>>(doff.p, noff, n, dtab.p, s, pl.lambda, k0tab, A.p);
+        VPG_LAUNCH_CHECK();
+        const double one = 1.0, zero = 0.0;
+        // V (n2 x k) column-major == [k][n2] layout (vc_cm)
+        const double* V = pl.hf_Vc.p + pl.hf_V_off[size_t(l)];
+        VPG_SOLVER(cublasDgemm(hd.blas, CUBLAS_OP_N, CUBLAS_OP_N, int(m), k, n2, &one, A.p, int(m), V, n2,
+                               &zero, X.p, int(m)));
+        VPG_SOLVER(cublasDgemmStridedBatched(hd.blas, CUBLAS_OP_T, CUBLAS_OP_N, k, k, n2, &one, V, n2, 0, X.p,
+                                             int(m), n2, &zero, pl.hf_C.p + pl.hf_C_off[size_t(l)], k,
+                                             int64_t(k) * k, noff));
+    }
+    VPG_CUDA(cudaDeviceSynchronize());
+
+    // M2L lists (target rows CSR over all levels; entries: source row, C block)
+    std::vector<int32_t> tbox, toff{0}, esrc, eop;
+    pl.hf_lvl_t0.assign(size_t(L + 2), 0);
+    for (int l = lmin; l <= L; ++l) {
+        pl.hf_lvl_t0[size_t(l)] = int64_t(tbox.size());
+        const int nb = 1 << l;
+        const auto& of = offs[size_t(l)];
+        auto oidx = [&](int dx, int dy) {
+            for (size_t i = 0; i < of.size(); ++i)
+                if (of[i].x == dx && of[i].y == dy) return int(i);
+            return -1;
+        };
+        const int64_t cblk0 = pl.hf_C_off[size_t(l)] / (int64_t(k) * k);
+        for (int64_t tb = 0; tb < (int64_t(1) << (2 * l)); ++tb) {
+            if (pl.h_tcnt[size_t(lvl_base(l) + tb)] == 0) continue;
+            const int tx = int(squash2(uint32_t(tb))), ty = int(squash2(uint32_t(tb) >> 1));
+            auto add = [&](int sx, int sy) {
+                if (sx < 0 || sy < 0 || sx >= nb || sy >= nb) return;
+                if (std::max(std::abs(tx - sx), std::abs(ty - sy)) < 2) return;
+                const uint32_t sb = mort(uint32_t(sx), uint32_t(sy));
+                if (pl.h_scnt[size_t(lvl_base(l) + sb)] == 0) return;
+                const int o = oidx(tx - sx, ty - sy);
+                if (o < 0) return;  // beyond the decay cutoff
+                esrc.push_back(int32_t(pl.hf_row_base[size_t(l)] + sb));
+                eop.push_back(int32_t(cblk0 + o));
+            };
+            if (l == lmin) {
+                for (int sy = 0; sy < nb; ++sy)
+                    for (int sx = 0; sx < nb; ++sx) add(sx, sy);
+            } else {
+                const int px = tx >> 1, py = ty >> 1;
+                for (int qy = std::max(0, py - 1); qy <= std::min((nb >> 1) - 1, py + 1); ++qy)
+                    for (int qx = std::max(0, px - 1); qx <= std::min((nb >> 1) - 1, px + 1); ++qx)
+                        for (int c = 0; c < 4; ++c) add(2 * qx + (c & 1), 2 * qy + (c >> 1));
+            }
+            tbox.push_back(int32_t(pl.hf_row_base[size_t(l)] + tb));
+            toff.push_back(int32_t(esrc.size()));
+        }
+    }
+    pl.hf_lvl_t0[size_t(L + 1)] = int64_t(tbox.size());
+    pl.hf_ntbox = int64_t(tbox.size());
+    pl.hf_nent = int64_t(esrc.size());
+    auto up = [](auto& d, const auto& h) {
+        d.alloc(std::max<size_t>(h.size(), 1));
+        if (!h.empty()) VPG_CUDA(cudaMemcpy(d.p, h.data(), h.size() * sizeof(h[0]), cudaMemcpyHostToDevice));
+    };
+    up(pl.hf_tbox, tbox);
+    up(pl.hf_toff, toff);
+    up(pl.hf_esrc, esrc);
+    up(pl.hf_eop, eop);
+    // anterp_kernel layout: nodes / bw per level (32 slots) -> the same n nodes at every level
+    std::vector<double> nl(size_t(L + 1) * 32, 0.0), bl(size_t(L + 1) * 32, 0.0);
+    for (int l = 0; l <= L; ++l)
+        for (int a = 0; a < n; ++a) {
+            nl[size_t(l) * 32 + a] = tab[size_t(a)];
+            bl[size_t(l) * 32 + a] = tab[size_t(32 + a)];
+        }
+    pl.helm_nodes.alloc(nl.size());
+    pl.helm_bw.alloc(bl.size());
+    VPG_CUDA(cudaMemcpy(pl.helm_nodes.p, nl.data(), pl.helm_nodes.bytes(), cudaMemcpyHostToDevice));
+    VPG_CUDA(cudaMemcpy(pl.helm_bw.p, bl.data(), pl.helm_bw.bytes(), cudaMemcpyHostToDevice));
+    pl.hf_tab.alloc(tab.size());
+    VPG_CUDA(cudaMemcpy(pl.hf_tab.p, tab.data(), pl.hf_tab.bytes(), cudaMemcpyHostToDevice));
+    pl.hf_n = n;
+    pl.hf_k = k;
+    pl.hf_lmin = lmin;
+    pl.P = n;  // reported expansion order: Chebyshev nodes per dimension
+    pl.hf = true;
+}
+
+void helm_fmm_apply(const Plan& pl, const double* q_dev, double* out_dev, cudaStream_t st, cudaEvent_t* ev,
+                    int64_t& launches) {
+    auto mark = [&](int i) {
+        if (ev) VPG_CUDA(cudaEventRecord(ev[i], st));
+    };
+    const int L = pl.L, n = pl.hf_n, n2 = n * n, k = pl.hf_k;
+    const HfLevels hl = hf_levels(pl);
+    const size_t rows = size_t(std::max<int64_t>(pl.hf_rows, 1));
+    void* base = nullptr;
+    const size_t bytes = sizeof(double) * (size_t(std::max<int64_t>(pl.ns, 1)) + 2 * rows * n2 + 2 * rows * k);
+    VPG_CUDA(cudaMallocAsync(&base, bytes, st));
+    struct Free {
+        void* p;
+        cudaStream_t s;
+        ~Free() {
+            if (p) cudaFreeAsync(p, s);
+        }
+    } fr{base, st};
+    double* qs = static_cast<double*>(base);
+    double* W = qs + std::max<int64_t>(pl.ns, 1);
+    double* Lv = W + rows * n2;
+    double* Wt = Lv + rows * n2;
+    double* Lt = Wt + rows * k;
+    mark(0);
+    gather_q_h<<<nblk(pl.ns, 256), 256, 0, st>>>(q_dev, pl.src_ids.p, pl.ns, qs);
+    VPG_LAUNCH_CHECK();
+    ++launches;
+    mark(1);
+    // P2M at the leaves (anterp_kernel with n nodes at level L)
+    HelmParams hp{};
+    hp.L = L;
+    hp.x0 = pl.x0;
+    hp.y0 = pl.y0;
+    hp.side = pl.side;
+    hp.lambda = pl.lambda;
+    hp.m[L] = n;
+    hp.w_off[L] = pl.hf_row_base[size_t(L)] * n2;
+    const int ath = std::max(((n2 + 31) / 32) * 32, 2 * kAntChunk);
+    anterp_kernel<<<unsigned(int64_t(1) << (2 * L)), ath, sizeof(double) * 2 * kAntChunk * kMaxM, st>>>(
+        hp, L, pl.src_cnt.p + lvl_base(L), pl.src_off.p, pl.src_sorted.p, qs, pl.helm_nodes.p, pl.helm_bw.p, W);
+    VPG_LAUNCH_CHECK();
+    ++launches;
+    mark(2);
+    const int tn2 = ((n2 + 31) / 32) * 32;
+    for (int l = L - 1; l >= pl.hf_lmin; --l) {
+        hf_m2m_kernel<<<unsigned(int64_t(1) << (2 * l)), tn2, 0, st>>>(
+            l, n, pl.hf_tab.p + 64, pl.src_cnt.p + lvl_base(l), pl.src_cnt.p + lvl_base(l + 1),
+            pl.hf_row_base[size_t(l)], pl.hf_row_base[size_t(l + 1)], W);
+        VPG_LAUNCH_CHECK();
+        ++launches;
+    }
+    hf_compress_kernel<<<unsigned(pl.hf_rows), ((k + 31) / 32) * 32, 0, st>>>(hl, pl.src_cnt.p, pl.hf_Vt.p, W, Wt);
+    VPG_LAUNCH_CHECK();
+    ++launches;
+    mark(3);
+    if (pl.hf_ntbox > 0) {
+        hf_m2l_kernel<<<unsigned(pl.hf_ntbox), ((k + 31) / 32) * 32, 0, st>>>(
+            k, pl.hf_tbox.p, pl.hf_toff.p, pl.hf_esrc.p, pl.hf_eop.p, pl.hf_C.p, Wt, Lt);
+        VPG_LAUNCH_CHECK();
+        ++launches;
+    }
+    mark(4);
+    for (int l = pl.hf_lmin; l <= L; ++l) {
+        const int64_t t0 = pl.hf_lvl_t0[size_t(l)], t1 = pl.hf_lvl_t0[size_t(l + 1)];
+        if (t1 == t0) continue;
+        hf_expand_kernel<<<unsigned(t1 - t0), std::max(tn2, ((k + 31) / 32) * 32), 0, st>>>(
+            hl, l, pl.hf_tbox.p + t0, pl.hf_Vc.p, pl.hf_tab.p + 64, Lt, Lv);
+        VPG_LAUNCH_CHECK();
+        ++launches;
+    }
+    mark(5);
+    if (pl.n_p2p_chunks > 0) {
+        const unsigned grid = unsigned(std::min<int64_t>((pl.n_p2p_chunks + kHfWarps - 1) / kHfWarps,
+                                                         int64_t(pl.sm_count) * 8));
+        hf_l2p_p2p_kernel<<<grid, kHfWarps * 32, 0, st>>>(
+            hl, pl.p2p_chunks.p, pl.n_p2p_chunks, pl.near_ranges.p, pl.tgt_row.p, pl.src_sorted.p, qs,
+            pl.tgt_sorted.p, pl.tgt_ids.p, pl.hf_tab.p, Lv, pl.x0, pl.y0, pl.side, pl.lambda,
+            k0_table_dev(), out_dev);
         VPG_LAUNCH_CHECK();
         ++launches;
     }

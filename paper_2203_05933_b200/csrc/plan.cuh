@@ -202,6 +202,19 @@ struct Plan {
     DBuf<int32_t> row_chain;
     DBuf<int32_t> l2p_rows;  // per-leaf L2P chains (P2PChunk::lfirst/lcount)
 
+    // Modified Helmholtz, native mode: compressed Chebyshev-interpolation FMM
+    // (helm.cu, build_helm_fmm): n x n Chebyshev nodes per box at levels
+    // hf_lmin..L, M2L through a rank-k SVD basis per level.
+    bool hf = false;
+    int hf_n = 0, hf_k = 0, hf_lmin = 0;
+    DBuf<double> hf_tab;            // nodes[n], bw[n], S[2][n][n]
+    DBuf<double> hf_Vt, hf_Vc;      // per level: V as [n2][k] (row-major) and [k][n2]
+    DBuf<double> hf_C;              // per level and offset: C [k][k], C[j*k + i] = C_ij
+    std::vector<int64_t> hf_V_off, hf_C_off, hf_row_base;  // per level
+    DBuf<int32_t> hf_tbox, hf_toff, hf_esrc, hf_eop;       // M2L target rows CSR; entries (src row, C block)
+    std::vector<int64_t> hf_lvl_t0;                        // per level first index into hf_tbox
+    int64_t hf_rows = 0, hf_ntbox = 0, hf_nent = 0;
+
     // Modified Helmholtz (treecode) state.
     int helm_min_level = 2;
     double helm_skip_x = 40.0;
@@ -268,6 +281,7 @@ void direct_sum_device(int family, double lambda, const double2* src,
                        unsigned long long* clash, cudaStream_t st);
 // helm.cu
 void build_helm_ops(Plan& pl);
+void build_helm_fmm(Plan& pl);  // native mode (helm.cu)
 void helm_apply(const Plan& pl, const double* q_dev, double* out_dev,
                 cudaStream_t st, cudaEvent_t* ev, int64_t& launches);
 void k0_device(const double* x, int64_t n, double* out, cudaStream_t st);

@@ -46,3 +46,31 @@ def test_cfg5_subset_vs_direct(vp, rest):
     idx = np.random.default_rng(4).choice(len(src), 2000, replace=False)
     ld = rest.pairwise_ld(1, 10.0, src, q, src[idx])
     assert rel_l2(gpu[idx], ld) <= 1e-12
+
+
+@pytest.mark.parametrize("eps", [1e-12, 1e-8])
+def test_native_helmholtz_fmm_vs_direct(vp, rest, eps):
+    """NATIVE mode for modified Helmholtz: the compressed Chebyshev FMM
+    (helm.cu) instead of the reference treecode, against long-double direct
+    K0 sums, to the requested epsilon."""
+    w = W.cfg5(n_side=96, ntri=1000)
+    src, q = w.src, w.q
+    with vp.SummationPlan(mh(vp), src, src, eps, mode="native") as plan:
+        gpu = plan.apply(q)
+        again = plan.apply(q)
+    assert np.array_equal(gpu, again)
+    idx = np.random.default_rng(4).choice(len(src), 2000, replace=False)
+    ld = rest.pairwise_ld(1, 10.0, src, q, src[idx])
+    assert rel_l2(gpu[idx], ld) <= eps
+
+
+def test_native_helmholtz_random_clusters(vp, rest):
+    rng = np.random.default_rng(22)
+    src = np.concatenate([rng.uniform(-1, 1, (20_000, 2)), 0.1 * rng.standard_normal((20_000, 2))])
+    tgt = rng.uniform(-1.2, 1.2, (15_000, 2))
+    q = rng.standard_normal(len(src))
+    with vp.SummationPlan(mh(vp, 4.0), src, tgt, 1e-12, mode="native") as plan:
+        gpu = plan.apply(q)
+    idx = np.random.default_rng(5).choice(len(tgt), 1500, replace=False)
+    ld = rest.pairwise_ld(1, 4.0, src, q, tgt[idx])
+    assert rel_l2(gpu[idx], ld) <= 1e-12
