@@ -394,7 +394,7 @@ __device__ __forceinline__ void hf_bary(const double* nodes, const double* bw, i
 
 // Warp per near-field chunk: far field from the leaf's Lv (barycentric) plus
 // the direct 3x3-leaf K0 sum; out = far + near in the original order.
-__global__ void __launch_bounds__(kHfWarps * 32)
+__global__ void __launch_bounds__(kHfWarps * 32, 2)
 hf_l2p_p2p_kernel(HfLevels hl, const P2PChunk* chunks, int64_t nchunks, const int2* ranges,
                   const int32_t* tgt_row, const double2* sxy, const double* q, const double2* txy,
                   const int32_t* tids, const double* tab, const double* Lv, double x0, double y0,
@@ -418,47 +418,76 @@ hf_l2p_p2p_kernel(HfLevels hl, const P2PChunk* chunks, int64_t nchunks, const in
         __syncwarp();
         for (int j = lane; j < n2; j += 32) L[j] = Lv[hrow * n2 + j];
         __syncwarp();
+        const bool two = c.tcount > 32;  // warp-uniform: second target per lane
+        double2 t[2];
+        double far[2] = {0.0, 0.0};
+#pragma unroll
         for (int u = 0; u < 2; ++u) {
             const int li = lane + 32 * u;
-            if (u == 1 && c.tcount <= 32) break;  // warp-uniform
-            const bool on = li < c.tcount;
-            const double2 t = txy[c.tbegin + (on ? li : 0)];
-            // far: sum_ab lx_a ly_b L[a][b]
-            double lx[kHfMaxN], ly[kHfMaxN];
-            hf_bary(nodes, bw, n, (t.x - cx) * 2.0 / s, lx);
-            hf_bary(nodes, bw, n, (t.y - cy) * 2.0 / s, ly);
-            double far = 0.0;
+            t[u] = txy[c.tbegin + min(li, c.tcount - 1)];
+            if (u == 1 && !two) continue;
+            // far: sum_ab lx_a ly_b L[a][b] at this target (ly held, lx recomputed)
+            double ly[kHfMaxN];
+            hf_bary(nodes, bw, n, (t[u].y - cy) * 2.0 / s, ly);
+            const double x = (t[u].x - cx) * 2.0 / s;
+            int hit = -1;
+            double sx = 0.0;
+            for (int a = 0; a < n; ++a) {
+                const double d = x - nodes[a];
+                if (d == 0.0) hit = a;
+                sx += bw[a] / (d == 0.0 ? 1.0 : d);
+            }
+            const double inv = 1.0 / sx;
+            for (int a = 0; a < n; ++a) {
+                const double d = x - nodes[a];
+                const double lxa = hit >= 0 ? (a == hit ? 1.0 : 0.0) : bw[a] / d * inv;
+                double inner = 0.0;
 #pragma unroll
-            for (int a = 0; a < kHfMaxN; ++a) {
-                if (a < n) {
-                    double inner = 0.0;
+                for (int b2 = 0; b2 < kHfMaxN; ++b2)
+                    if (b2 < n) inner = fma(ly[b2], L[a * n + b2], inner);
+                far[u] = fma(lxa, inner, far[u]);
+            }
+        }
+        // near: the 3x3 leaves, sources broadcast 32 at a time, both targets
+        // per source; K0 through q = (lambda r / 2)^2 (no square root) while
+        // every pair of the batch has lambda r <= 2, else the general K0
+        double near[2] = {0.0, 0.0};
+        const double l2q = 0.25 * lambda * lambda;
+        for (int ri = 0; ri < c.rcount; ++ri) {
+            const int2 rg = ranges[c.rfirst + ri];
+            for (int base = rg.x; base < rg.x + rg.y; base += 32) {
+                const int cnt = min(32, rg.x + rg.y - base);
+                double2 sp = make_double2(0.0, 0.0);
+                double qj = 0.0;
+                if (lane < cnt) {
+                    sp = sxy[base + lane];
+                    qj = q[base + lane];
+                }
+                for (int j = 0; j < cnt; ++j) {
+                    const double px = __shfl_sync(0xffffffffu, sp.x, j);
+                    const double py = __shfl_sync(0xffffffffu, sp.y, j);
+                    const double pq = __shfl_sync(0xffffffffu, qj, j);
 #pragma unroll
-                    for (int b2 = 0; b2 < kHfMaxN; ++b2)
-                        if (b2 < n) inner = fma(ly[b2], L[a * n + b2], inner);
-                    far = fma(lx[a], inner, far);
+                    for (int u = 0; u < 2; ++u) {
+                        if (u == 1 && !two) continue;
+                        const double dx = t[u].x - px, dy = t[u].y - py;
+                        const double r2 = fma(dy, dy, dx * dx);
+                        const double qq = l2q * r2;
+                        double v;
+                        if (__all_sync(0xffffffffu, qq <= 1.0)) {
+                            v = r2 == 0.0 ? 0.0 : pq * k0_small_q(qq);
+                        } else {
+                            v = r2 == 0.0 ? 0.0 : pq * k0_dev(lambda * sqrt(r2), k0tab);
+                        }
+                        near[u] = fma(kInv2Pi, v, near[u]);
+                    }
                 }
             }
-            // near: 3x3 leaves, sources broadcast 32 at a time
-            double near = 0.0;
-            for (int ri = 0; ri < c.rcount; ++ri) {
-                const int2 rg = ranges[c.rfirst + ri];
-                for (int base = rg.x; base < rg.x + rg.y; base += 32) {
-                    const int cnt = min(32, rg.x + rg.y - base);
-                    double2 sp = make_double2(0.0, 0.0);
-                    double qj = 0.0;
-                    if (lane < cnt) {
-                        sp = sxy[base + lane];
-                        qj = q[base + lane];
-                    }
-                    for (int j = 0; j < cnt; ++j) {
-                        const double px = __shfl_sync(0xffffffffu, sp.x, j);
-                        const double py = __shfl_sync(0xffffffffu, sp.y, j);
-                        const double pq = __shfl_sync(0xffffffffu, qj, j);
-                        near = fma(kInv2Pi, k0_pair(t.x, t.y, px, py, pq, lambda, k0tab), near);
-                    }
-                }
-            }
-            if (on) out[tids[c.tbegin + li]] = far + near;
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int li = lane + 32 * u;
+            if (li < c.tcount) out[tids[c.tbegin + li]] = far[u] + near[u];
         }
     }
 }

@@ -51,6 +51,21 @@ __device__ __forceinline__ double k0_small(double x) {
     return -(log(0.5 * x) + kGamma) * i0 + s;
 }
 
+// The x <= 2 branch from q = x^2 / 4 directly (no square root):
+// ln(x/2) = ln(q) / 2.
+__device__ __forceinline__ double k0_small_q(double q) {
+    const double* c = c_k0_i0;
+    const double* d = c_k0_h;
+    double i0 = c[16], s = d[16];
+#pragma unroll
+    for (int k = 15; k >= 0; --k) {
+        i0 = fma(i0, q, c[k]);
+        s = fma(s, q, d[k]);
+    }
+    constexpr double kGamma = 0.57721566490153286061;
+    return -(0.5 * log(q) + kGamma) * i0 + s;
+}
+
 __device__ __forceinline__ double k0_large(double x, const double* tab) {
     const double ex = exp(-x);
     if (ex == 0.0) return 0.0;
