@@ -16,6 +16,7 @@
 //     order.
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 #include <vector>
 
 #include <cublas_v2.h>
@@ -398,9 +399,15 @@ __global__ void __launch_bounds__(kHfWarps * 32, 2)
 hf_l2p_p2p_kernel(HfLevels hl, const P2PChunk* chunks, int64_t nchunks, const int2* ranges,
                   const int32_t* tgt_row, const double2* sxy, const double* q, const double2* txy,
                   const int32_t* tids, const double* tab, const double* Lv, double x0, double y0,
-                  double side, double lambda, const double* k0tab, double* out) {
-    __shared__ double lvs[kHfWarps][kHfMaxN * kHfMaxN];
+                  double side, double lambda, const double* k0tab, const double2* gtab, double* out) {
+    extern __shared__ double2 hsm[];
+    double2* ltab = hsm;  // log table, 8 copies (common.cuh)
+    double (*lvs)[kHfMaxN * kHfMaxN] =
+        reinterpret_cast<double (*)[kHfMaxN * kHfMaxN]>(hsm + kLogTableSize * kLogTableCopies);
+    log_table_to_smem(ltab, gtab);
+    __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t tab_lane = log_table_lane_addr(ltab, lane & 7);
     const int n = hl.n, n2 = n * n;
     const double* nodes = tab;
     const double* bw = tab + 32;
@@ -453,37 +460,54 @@ hf_l2p_p2p_kernel(HfLevels hl, const P2PChunk* chunks, int64_t nchunks, const in
         // every pair of the batch has lambda r <= 2, else the general K0
         double near[2] = {0.0, 0.0};
         const double l2q = 0.25 * lambda * lambda;
-        for (int ri = 0; ri < c.rcount; ++ri) {
-            const int2 rg = ranges[c.rfirst + ri];
-            for (int base = rg.x; base < rg.x + rg.y; base += 32) {
-                const int cnt = min(32, rg.x + rg.y - base);
-                double2 sp = make_double2(0.0, 0.0);
-                double qj = 0.0;
-                if (lane < cnt) {
-                    sp = sxy[base + lane];
-                    qj = q[base + lane];
-                }
-                for (int j = 0; j < cnt; ++j) {
-                    const double px = __shfl_sync(0xffffffffu, sp.x, j);
-                    const double py = __shfl_sync(0xffffffffu, sp.y, j);
-                    const double pq = __shfl_sync(0xffffffffu, qj, j);
+        // K0 = -(ln(x/2) + gamma) I0(q) + S(q), q = (x/2)^2, ln(x/2) =
+        // (ln r^2 + ln(lambda^2/4)) / 2 with the table log of the Laplace
+        // near field; for q <= 1/4 (the near field: lambda r <= 1) the two
+        // series end at q^9 (tail < 3e-17 relative)
+        const double c0 = 0.5 * log(l2q) + 0.57721566490153286061;
+        // every pair of the chunk lies within the 3x3 leaves: |r| <= 3 sqrt(2) s
+        const bool fast = l2q * 18.0 * s * s <= 0.25;
+        auto sweep = [&](auto fast_tag) {
+            constexpr bool kFast = decltype(fast_tag)::value;
+            for (int ri = 0; ri < c.rcount; ++ri) {
+                const int2 rg = ranges[c.rfirst + ri];
+                for (int base = rg.x; base < rg.x + rg.y; base += 32) {
+                    const int cnt = min(32, rg.x + rg.y - base);
+                    double2 sp = make_double2(0.0, 0.0);
+                    double qj = 0.0;
+                    if (lane < cnt) {
+                        sp = sxy[base + lane];
+                        qj = q[base + lane];
+                    }
+                    for (int j = 0; j < cnt; ++j) {
+                        const double px = __shfl_sync(0xffffffffu, sp.x, j);
+                        const double py = __shfl_sync(0xffffffffu, sp.y, j);
+                        const double pq = __shfl_sync(0xffffffffu, qj, j);
 #pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        if (u == 1 && !two) continue;
-                        const double dx = t[u].x - px, dy = t[u].y - py;
-                        const double r2 = fma(dy, dy, dx * dx);
-                        const double qq = l2q * r2;
-                        double v;
-                        if (__all_sync(0xffffffffu, qq <= 1.0)) {
-                            v = r2 == 0.0 ? 0.0 : pq * k0_small_q(qq);
-                        } else {
-                            v = r2 == 0.0 ? 0.0 : pq * k0_dev(lambda * sqrt(r2), k0tab);
+                        for (int u = 0; u < 2; ++u) {
+                            if (u == 1 && !two) continue;
+                            const double dx = t[u].x - px, dy = t[u].y - py;
+                            const double r2 = fma(dy, dy, dx * dx);
+                            const double qq = l2q * r2;
+                            double v;
+                            if (kFast) {
+                                double ed;
+                                const double tl = fast_log_split(r2, tab_lane, ed);
+                                const double lnr2 = fma(ed, kLn2Hi, fma(ed, kLn2Lo, tl));
+                                v = fma(-fma(0.5, lnr2, c0), k0_i0_9(qq), k0_h_9(qq));
+                                if (__double2hiint(r2) < 0x00100000) v = r2 == 0.0 ? 0.0 : k0_small_q(qq);
+                            } else {
+                                v = r2 == 0.0 ? 0.0
+                                              : (qq <= 1.0 ? k0_small_q(qq) : k0_dev(lambda * sqrt(r2), k0tab));
+                            }
+                            near[u] = fma(kInv2Pi * pq, v, near[u]);
                         }
-                        near[u] = fma(kInv2Pi, v, near[u]);
                     }
                 }
             }
-        }
+        };
+        if (fast) sweep(std::true_type{});
+        else sweep(std::false_type{});
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
             const int li = lane + 32 * u;
@@ -834,6 +858,8 @@ void build_helm_fmm(Plan& pl) {
     pl.hf_k = k;
     pl.hf_lmin = lmin;
     pl.P = n;  // reported expansion order: Chebyshev nodes per dimension
+    smem_optin((const void*)hf_l2p_p2p_kernel,
+               int(size_t(kLogTableBytes) + sizeof(double) * kHfWarps * kHfMaxN * kHfMaxN));
     pl.hf = true;
 }
 
@@ -911,10 +937,11 @@ void helm_fmm_apply(const Plan& pl, const double* q_dev, double* out_dev, cudaSt
     if (pl.n_p2p_chunks > 0) {
         const unsigned grid = unsigned(std::min<int64_t>((pl.n_p2p_chunks + kHfWarps - 1) / kHfWarps,
                                                          int64_t(pl.sm_count) * 8));
-        hf_l2p_p2p_kernel<<<grid, kHfWarps * 32, 0, st>>>(
+        const size_t smem = size_t(kLogTableBytes) + sizeof(double) * kHfWarps * kHfMaxN * kHfMaxN;
+        hf_l2p_p2p_kernel<<<grid, kHfWarps * 32, smem, st>>>(
             hl, pl.p2p_chunks.p, pl.n_p2p_chunks, pl.near_ranges.p, pl.tgt_row.p, pl.src_sorted.p, qs,
             pl.tgt_sorted.p, pl.tgt_ids.p, pl.hf_tab.p, Lv, pl.x0, pl.y0, pl.side, pl.lambda,
-            k0_table_dev(), out_dev);
+            k0_table_dev(), log_table_dev(), out_dev);
         VPG_LAUNCH_CHECK();
         ++launches;
     }

@@ -66,6 +66,21 @@ __device__ __forceinline__ double k0_small_q(double q) {
     return -(0.5 * log(q) + kGamma) * i0 + s;
 }
 
+// Degree-9 truncations of the two series for q <= 1/4 (the dropped tail is
+// below q^10 / (10!)^2 ~ 7e-20 relative).
+__device__ __forceinline__ double k0_i0_9(double q) {
+    double v = c_k0_i0[9];
+#pragma unroll
+    for (int k = 8; k >= 0; --k) v = fma(v, q, c_k0_i0[k]);
+    return v;
+}
+__device__ __forceinline__ double k0_h_9(double q) {
+    double v = c_k0_h[9];
+#pragma unroll
+    for (int k = 8; k >= 0; --k) v = fma(v, q, c_k0_h[k]);
+    return v;
+}
+
 __device__ __forceinline__ double k0_large(double x, const double* tab) {
     const double ex = exp(-x);
     if (ex == 0.0) return 0.0;
