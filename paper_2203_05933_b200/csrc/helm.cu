@@ -479,6 +479,7 @@ hf_l2p_p2p_kernel(HfLevels hl, const P2PChunk* chunks, int64_t nchunks, const in
                         sp = sxy[base + lane];
                         qj = q[base + lane];
                     }
+#pragma unroll 2
                     for (int j = 0; j < cnt; ++j) {
                         const double px = __shfl_sync(0xffffffffu, sp.x, j);
                         const double py = __shfl_sync(0xffffffffu, sp.y, j);
