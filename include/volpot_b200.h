@@ -64,13 +64,16 @@ typedef enum { VPG_LAPLACE = 0, VPG_MODIFIED_HELMHOLTZ = 1 } vpg_family;
 /* Tree policy.  REFERENCE reproduces the reference plan bit-exactly (same
  * bounding box, depth clamp(ceil(log4(max(ns,nt)/32)),2,7), same P, same
  * pairwise threshold ns*nt <= 4e6), so trees and interaction lists can be
- * compared entry by entry.  NATIVE (Laplace only; modified Helmholtz plans
- * use the REFERENCE tree) builds an adaptive quadtree -- a box splits while
- * it holds more than 64 sources or targets, down to depth 16 -- with
- * U/V/W/X interaction lists (P2P, M2L, M2P, P2L), so clustered points stay
- * O(n); the pairwise threshold (ns*nt <= 4e6) and P are the reference's.
- * Parity against the reference is then to the requested tolerance, and the
- * uniform-tree dumps and leaf shards are not available. */
+ * compared entry by entry.  NATIVE departs from the reference algorithm
+ * where a B200-first one is faster, with parity to the requested tolerance:
+ *   Laplace: an adaptive quadtree -- a box splits while it holds more than
+ *     64 sources or targets, down to depth 16 -- with U/V/W/X interaction
+ *     lists (P2P, M2L, M2P, P2L), so clustered points stay O(n); the
+ *     uniform-tree dumps and leaf shards are not available.
+ *   Modified Helmholtz: the reference tree with a compressed Chebyshev-
+ *     interpolation FMM (SVD-based M2L) instead of the proxy treecode;
+ *     expansion_order then reports the Chebyshev nodes per dimension.
+ * The pairwise threshold (ns*nt <= 4e6) is the reference's in both modes. */
 typedef enum { VPG_MODE_REFERENCE = 0, VPG_MODE_NATIVE = 1 } vpg_mode;
 
 /* vpg_plan_apply flags */
