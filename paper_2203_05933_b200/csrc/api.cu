@@ -217,7 +217,12 @@ GraphEntry* graph_entry(const Plan& pl, const double* q, double* out, bool host)
     try {
         if (!pl.adaptive && (pl.shard_lb != 0 || pl.shard_le != (int64_t(1) << (2 * pl.L))) && pl.nt)
             VPG_CUDA(cudaMemsetAsync(od, 0, sizeof(double) * size_t(pl.nt), cap));
-        laplace_issue(pl, qd, od, laplace_work_at(pl, e->work), cap, nullptr, e->launches, side, fork, join);
+        static const bool no_fork = [] {
+            const char* v = std::getenv("VPG_NO_FORK");
+            return v && v[0] == '1';
+        }();
+        laplace_issue(pl, qd, od, laplace_work_at(pl, e->work), cap, nullptr, e->launches,
+                      no_fork ? nullptr : side, fork, join);
     } catch (...) {  // not capturable here: the caller falls back to plain launches
         cudaStreamEndCapture(cap, &g);
         if (g) cudaGraphDestroy(g);
