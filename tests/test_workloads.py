@@ -57,3 +57,46 @@ def test_correction_csr_bounds():
     nb = np.diff(csr["blk_off"])
     assert nb.max() <= 9 and nb.min() >= 1
     assert csr["pool_off"][-1] == len(csr["pool_vals"])
+
+
+def _correction_csr_loops(nbox_cells, box_ij, ntri_cells, np_box=64, np_tri=64):
+    """Plain-loop statement of the synthetic correction map's block layout
+    (per target: self + existing 8-neighbour boxes in offset order; triangle
+    nodes: one private row) -- the check for the vectorised builder."""
+    index = {tuple(ij): k for k, ij in enumerate(map(tuple, box_ij))}
+    offsets = [(0, 0)] + [(dx, dy) for dy in (-1, 0, 1) for dx in (-1, 0, 1) if (dx, dy) != (0, 0)]
+    npool = len(offsets) * np_box
+    blk_cell, blk_pool, blk_off = [], [], [0]
+    for c, (i, j) in enumerate(map(tuple, box_ij)):
+        nbrs = [(k, index.get((i + o[0], j + o[1]))) for k, o in enumerate(offsets)]
+        nbrs = [(k, cell) for k, cell in nbrs if cell is not None]
+        for t in range(np_box):
+            for k, cell in nbrs:
+                blk_cell.append(cell)
+                blk_pool.append(k * np_box + t)
+            blk_off.append(len(blk_cell))
+    for c in range(ntri_cells):
+        for t in range(np_tri):
+            blk_cell.append(nbox_cells + c)
+            blk_pool.append(npool + c * np_tri + t)
+            blk_off.append(len(blk_cell))
+    return np.array(blk_off), np.array(blk_cell), np.array(blk_pool)
+
+
+def test_correction_csr_vectorised_matches_loops():
+    n = 18
+    ij = np.array([(i, j) for j in range(n) for i in range(n) if (i - n / 2) ** 2 + (j - n / 2) ** 2 < (n / 2) ** 2])
+    v = W.correction_csr(len(ij), ij, 25)
+    bo, bc, bp = _correction_csr_loops(len(ij), ij, 25)
+    assert np.array_equal(v["blk_off"], bo) and np.array_equal(v["blk_cell"], bc)
+    assert np.array_equal(v["blk_pool"], bp)
+    assert int(v["node_off"][-1]) == (len(ij) + 25) * 64
+    assert v["pool_off"][-1] == v["pool_vals"].size
+
+
+def test_cfg5_correction_map_shape():
+    w = W.cfg5(n_side=64, ntri=200)
+    c = w.notes["corr"]()
+    assert c["blk_off"].size - 1 == w.nt == int(c["node_off"][-1])
+    assert np.diff(c["blk_off"]).max() <= 9 and np.diff(c["blk_off"]).min() >= 1
+    assert np.allclose(w.notes["w"] * w.notes["f"], w.q, rtol=0, atol=0)
