@@ -136,6 +136,93 @@ class SummationPlan {
     vpg_plan_info_t info_{};
 };
 
+// Correction map (potential.cpp:92-110, 446-462) on the device: out += C f.
+class CorrectionMap {
+  public:
+    CorrectionMap(const std::vector<int32_t>& blk_off, const std::vector<int32_t>& blk_cell,
+                  const std::vector<int32_t>& blk_pool, const std::vector<int64_t>& pool_off,
+                  const std::vector<double>& pool_vals, const std::vector<int32_t>& node_off, int device = 0)
+        : nt_(int64_t(blk_off.size()) - 1), ndofs_(node_off.empty() ? 0 : node_off.back()) {
+        detail::check(vpg_corr_create(nt_, blk_off.data(), int64_t(blk_cell.size()), blk_cell.data(),
+                                      blk_pool.data(), int64_t(pool_off.size()) - 1, pool_off.data(),
+                                      pool_vals.data(), int64_t(node_off.size()) - 1, node_off.data(), device,
+                                      &h_));
+    }
+    ~CorrectionMap() {
+        if (h_) vpg_corr_destroy(h_);
+    }
+    CorrectionMap(const CorrectionMap&) = delete;
+    CorrectionMap& operator=(const CorrectionMap&) = delete;
+    void apply(const std::vector<double>& f, std::vector<double>& out) const {
+        detail::check(vpg_corr_apply(h_, f.data(), int64_t(f.size()), out.data(), 0u, nullptr));
+    }
+    vpg_corr* handle() const { return h_; }
+    int64_t num_targets() const { return nt_; }
+
+  private:
+    vpg_corr* h_ = nullptr;
+    int64_t nt_ = 0, ndofs_ = 0;
+};
+
+// build_charges (potential.cpp:397-412): charges = src_wj * (O_type f) per cell.
+class ChargeMap {
+  public:
+    ChargeMap(const std::vector<int32_t>& cell_type, const std::vector<int32_t>& node_off,
+              const std::vector<int32_t>& src_off, const std::vector<double>& over0, int np0, int nq0,
+              const std::vector<double>& over1, int np1, int nq1, const std::vector<double>& src_wj,
+              int device = 0) {
+        detail::check(vpg_charges_create(int64_t(cell_type.size()), cell_type.data(), node_off.data(),
+                                         src_off.data(), over0.data(), np0, nq0, over1.data(), np1, nq1,
+                                         src_wj.data(), device, &h_));
+    }
+    ~ChargeMap() {
+        if (h_) vpg_charges_destroy(h_);
+    }
+    ChargeMap(const ChargeMap&) = delete;
+    ChargeMap& operator=(const ChargeMap&) = delete;
+    vpg_charges* handle() const { return h_; }
+
+  private:
+    vpg_charges* h_ = nullptr;
+};
+
+// VolumePotentialOperator::apply (potential.cpp:431-470), device-resident:
+// out = plan.apply(build_charges(f)) + C f.  Borrows the plan and the maps.
+struct ApplyTimings {
+    double smooth_seconds = 0.0;
+    double correction_seconds = 0.0;
+};
+
+class VolumePotentialOperator {
+  public:
+    VolumePotentialOperator(const SummationPlan& plan, const CorrectionMap& corr,
+                            const ChargeMap* charges = nullptr)
+        : nt_(int64_t(plan.num_targets())) {
+        detail::check(vpg_operator_create(plan.handle(), charges ? charges->handle() : nullptr, corr.handle(),
+                                          &h_));
+    }
+    ~VolumePotentialOperator() {
+        if (h_) vpg_operator_destroy(h_);
+    }
+    VolumePotentialOperator(const VolumePotentialOperator&) = delete;
+    VolumePotentialOperator& operator=(const VolumePotentialOperator&) = delete;
+    std::vector<double> apply(const std::vector<double>& f_samples, ApplyTimings* timings = nullptr) const {
+        std::vector<double> out(static_cast<std::size_t>(nt_));
+        float t[2] = {0.f, 0.f};
+        detail::check(vpg_operator_apply(h_, f_samples.data(), int64_t(f_samples.size()), out.data(), 0u, nullptr,
+                                         timings ? t : nullptr));
+        if (timings) {
+            timings->smooth_seconds = t[0] * 1e-3;
+            timings->correction_seconds = t[1] * 1e-3;
+        }
+        return out;
+    }
+
+  private:
+    vpg_operator* h_ = nullptr;
+    int64_t nt_ = 0;
+};
+
 inline std::vector<double> accelerated_sum(const Kernel& kernel, const SourceSet& sources,
                                            const std::vector<Vec2>& targets,
                                            double epsilon = 1e-12) {

@@ -50,6 +50,16 @@ int main(int argc, char** argv) {
     }
     SummationPlan moved = std::move(plan);
     std::vector<double> c = moved.apply(q);
+    // operator-level apply with an empty correction map and charges = samples:
+    // identical to the plan's apply
+    if (ns == nt) {
+        std::vector<int32_t> blk_off(static_cast<size_t>(nt) + 1, 0), node_off{0, int32_t(ns)};
+        CorrectionMap corr(blk_off, {}, {}, {0, 1}, {0.0}, node_off);
+        VolumePotentialOperator op(moved, corr);
+        ApplyTimings tm;
+        const std::vector<double> d = op.apply(q, &tm);
+        errors += (d == c) && tm.smooth_seconds > 0.0 ? 0 : 100;
+    }
     std::ofstream out(argv[2], std::ios::binary);
     out.write(reinterpret_cast<const char*>(a.data()), 8 * nt);
     out.write(reinterpret_cast<const char*>(b.data()), 8 * nt);
