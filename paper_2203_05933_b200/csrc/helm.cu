@@ -339,6 +339,82 @@ __global__ void hf_m2l_kernel(int k, const int32_t* tbox, const int32_t* toff, c
     if (i < k) Lt[int64_t(tbox[ti]) * k + i] = acc;
 }
 
+// M2L on the FP64 tensor cores: a CTA takes a tile of up to 16 target boxes
+// of one level and walks the level's offsets in a fixed order; per offset
+// it stages C_o (64 x 64) once for the whole tile and the sources' Wt as
+// the B operand (zeros where a target has no source at that offset), and
+// warp w accumulates output rows 8w..8w+7 for the 16 targets with
+// mma.sync m8n8k4 f64.  C_o is read once per tile instead of once per list
+// entry (the per-entry form was L2-bandwidth bound).
+constexpr int kHfTile = 16;
+
+__global__ void __launch_bounds__(256)
+hf_m2l_tc_kernel(const int4* tiles, const int32_t* tbox, const int32_t* srcof, const double* C,
+                 const double* Wt, double* Lt, double* Lpart) {
+    constexpr int k = kHfMaxK;
+    __shared__ __align__(16) double cs[k * k];          // [j][i]
+    __shared__ __align__(16) double ws[k * kHfTile];     // [j][t]
+    __shared__ int32_t src_s[kHfTile];
+    const int4 tl = tiles[2 * blockIdx.x], tr = tiles[2 * blockIdx.x + 1];
+    const int t0 = tl.x, nt = tl.y, sbase = tl.z, noff = tl.w;
+    const int o0 = tr.x, o1 = tr.y, slot = tr.z;
+    const int64_t cb = tr.w;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int kq = lane & 3, rq = lane >> 2;
+    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    for (int o = o0; o < o1; ++o) {
+        __syncthreads();
+        if (threadIdx.x < kHfTile)
+            src_s[threadIdx.x] = threadIdx.x < nt ? srcof[sbase + int64_t(t0 + threadIdx.x) * noff + o] : -1;
+        __syncthreads();
+        bool any = false;
+#pragma unroll
+        for (int t = 0; t < kHfTile; ++t) any |= src_s[t] >= 0;
+        if (!any) continue;  // block-uniform
+        const double2* cg = reinterpret_cast<const double2*>(C + (cb + o) * int64_t(k) * k);
+        for (int i = threadIdx.x; i < k * k / 2; i += blockDim.x) reinterpret_cast<double2*>(cs)[i] = cg[i];
+        for (int i = threadIdx.x; i < k * kHfTile; i += blockDim.x) {
+            const int t = i % kHfTile, j = i / kHfTile;
+            const int sr = src_s[t];
+            ws[j * kHfTile + t] = sr >= 0 ? Wt[int64_t(sr) * k + j] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int k4 = 0; k4 < k; k4 += 4) {
+            const double a = cs[(k4 + kq) * k + 8 * warp + rq];
+#pragma unroll
+            for (int n8 = 0; n8 < 2; ++n8) {
+                const double b = ws[(k4 + kq) * kHfTile + 8 * n8 + rq];
+                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                             : "+d"(acc[n8][0]), "+d"(acc[n8][1])
+                             : "d"(a), "d"(b));
+            }
+        }
+    }
+    // lane holds rows 8w + rq, targets 8 n8 + 2 kq + {0, 1}
+    const int i = 8 * warp + rq;
+#pragma unroll
+    for (int n8 = 0; n8 < 2; ++n8)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int t = 8 * n8 + 2 * kq + h;
+            if (t >= nt) continue;
+            if (slot < 0) Lt[int64_t(tbox[t0 + t]) * k + i] = acc[n8][h];
+            else Lpart[(int64_t(slot) + t) * k + i] = acc[n8][h];  // one target per split tile
+        }
+}
+
+// Split targets (the first M2L level has up to ~200 offsets per box): the
+// offset ranges' partial sums added in range order.
+__global__ void hf_m2l_reduce_kernel(const int2* splits, int nparts, const double* Lpart, double* Lt) {
+    const int2 sp = splits[blockIdx.x];
+    const int i = threadIdx.x;
+    if (i >= kHfMaxK) return;
+    double acc = 0.0;
+    for (int p = 0; p < nparts; ++p) acc += Lpart[(int64_t(sp.y) + p) * kHfMaxK + i];
+    Lt[int64_t(sp.x) * kHfMaxK + i] = acc;
+}
+
 // Lv[r] = V_l Lt[r] (+ the parent's Lv interpolated to r's nodes)
 __global__ void hf_expand_kernel(HfLevels hl, int level, const int32_t* tbox, const double* Vc,
                                  const double* S, const double* Lt, double* Lv) {
@@ -746,7 +822,7 @@ void build_helm_fmm(Plan& pl) {
         vt_all[size_t(l)].resize(size_t(n2) * n2);
         VPG_CUDA(cudaMemcpy(vt_all[size_t(l)].data(), VT.p, VT.bytes(), cudaMemcpyDeviceToHost));
     }
-    k = std::min(k, kHfMaxK);
+    k = kHfMaxK;  // rank r <= 64 needed (~50 at 1e-12); the DMMA M2L tile is 64 rows
     // V per level in both layouts; C_o = V^T K_o V
     pl.hf_V_off.assign(size_t(L + 2), 0);
     pl.hf_C_off.assign(size_t(L + 2), 0);
@@ -833,6 +909,62 @@ void build_helm_fmm(Plan& pl) {
     }
     pl.hf_lvl_t0[size_t(L + 1)] = int64_t(tbox.size());
     pl.hf_ntbox = int64_t(tbox.size());
+    // dense (target, offset) -> source row table and 16-target tiles per level
+    {
+        std::vector<int32_t> srcof;
+        std::vector<int4> tiles;
+        std::vector<int2> splits;
+        constexpr int kSplitOffsets = 48;  // offsets per tile above which targets are split
+        int parts_per_split = 0;           // one part count for every split level
+        for (int l = lmin; l <= L; ++l) {
+            const int noff = int(offs[size_t(l)].size());
+            if (noff > kSplitOffsets)
+                parts_per_split = std::max(parts_per_split, (noff + kSplitOffsets - 1) / kSplitOffsets);
+        }
+        int64_t slot = 0;
+        for (int l = lmin; l <= L; ++l) {
+            const int64_t a0 = pl.hf_lvl_t0[size_t(l)], a1 = pl.hf_lvl_t0[size_t(l + 1)];
+            const int noff = int(offs[size_t(l)].size());
+            const int64_t cblk0 = pl.hf_C_off[size_t(l)] / (int64_t(k) * k);
+            const int64_t sbase = int64_t(srcof.size()) - a0 * noff;
+            for (int64_t ti = a0; ti < a1; ++ti) {
+                const size_t row0 = srcof.size();
+                srcof.resize(row0 + size_t(noff), -1);
+                for (int e = toff[size_t(ti)]; e < toff[size_t(ti + 1)]; ++e)
+                    srcof[row0 + size_t(eop[size_t(e)] - cblk0)] = esrc[size_t(e)];
+            }
+            if (noff > kSplitOffsets) {
+                // one target per tile, offsets in ranges -> partials, reduced in order
+                const int np = parts_per_split;
+                for (int64_t ti = a0; ti < a1; ++ti) {
+                    splits.push_back(make_int2(tbox[size_t(ti)], int(slot)));
+                    for (int p = 0; p < np; ++p) {
+                        const int o0 = int(int64_t(noff) * p / np), o1 = int(int64_t(noff) * (p + 1) / np);
+                        tiles.push_back(make_int4(int(ti), 1, int(sbase), noff));
+                        tiles.push_back(make_int4(o0, o1, int(slot + p), int(cblk0)));
+                    }
+                    slot += np;
+                }
+            } else {
+                for (int64_t ti = a0; ti < a1; ti += kHfTile) {
+                    tiles.push_back(make_int4(int(ti), int(std::min<int64_t>(kHfTile, a1 - ti)), int(sbase), noff));
+                    tiles.push_back(make_int4(0, noff, -1, int(cblk0)));
+                }
+            }
+        }
+        // every split level uses the same part count (ranges of equal count)
+        pl.hf_split_parts = parts_per_split;
+        pl.hf_nsplit = int64_t(splits.size());
+        pl.hf_nparts = slot;
+        pl.hf_ntiles = int64_t(tiles.size()) / 2;
+        auto up2 = [](auto& d, const auto& h) {
+            d.alloc(std::max<size_t>(h.size(), 1));
+            if (!h.empty()) VPG_CUDA(cudaMemcpy(d.p, h.data(), h.size() * sizeof(h[0]), cudaMemcpyHostToDevice));
+        };
+        up2(pl.hf_srcof, srcof);
+        up2(pl.hf_tiles, tiles);
+        up2(pl.hf_splits, splits);
+    }
     pl.hf_nent = int64_t(esrc.size());
     auto up = [](auto& d, const auto& h) {
         d.alloc(std::max<size_t>(h.size(), 1));
@@ -920,8 +1052,18 @@ void helm_fmm_apply(const Plan& pl, const double* q_dev, double* out_dev, cudaSt
     ++launches;
     mark(3);
     if (pl.hf_ntbox > 0) {
-        hf_m2l_kernel<<<unsigned(pl.hf_ntbox), ((k + 31) / 32) * 32, 0, st>>>(
-            k, pl.hf_tbox.p, pl.hf_toff.p, pl.hf_esrc.p, pl.hf_eop.p, pl.hf_C.p, Wt, Lt);
+        double* Lpart = nullptr;
+        if (pl.hf_nparts > 0)
+            VPG_CUDA(cudaMallocAsync(&Lpart, sizeof(double) * size_t(pl.hf_nparts) * kHfMaxK, st));
+        hf_m2l_tc_kernel<<<unsigned(pl.hf_ntiles), 256, 0, st>>>(pl.hf_tiles.p, pl.hf_tbox.p, pl.hf_srcof.p,
+                                                                  pl.hf_C.p, Wt, Lt, Lpart);
+        VPG_LAUNCH_CHECK();
+        ++launches;
+        if (pl.hf_nsplit > 0) {
+            hf_m2l_reduce_kernel<<<unsigned(pl.hf_nsplit), kHfMaxK, 0, st>>>(pl.hf_splits.p, pl.hf_split_parts,
+                                                                            Lpart, Lt);
+        }
+        if (Lpart) VPG_CUDA(cudaFreeAsync(Lpart, st));
         VPG_LAUNCH_CHECK();
         ++launches;
     }

@@ -213,6 +213,12 @@ struct Plan {
     std::vector<int64_t> hf_V_off, hf_C_off, hf_row_base;  // per level
     DBuf<int32_t> hf_tbox, hf_toff, hf_esrc, hf_eop;       // M2L target rows CSR; entries (src row, C block)
     std::vector<int64_t> hf_lvl_t0;                        // per level first index into hf_tbox
+    DBuf<int32_t> hf_srcof;  // per level [targets][offsets]: source row or -1
+    DBuf<int4> hf_tiles;     // M2L tiles, 2 x int4: (first target, count, srcof base, noff),
+                             // (first offset, end offset, partial slot or -1, C block base)
+    DBuf<int2> hf_splits;    // split targets: (target row, first partial slot); nparts per split
+    int64_t hf_ntiles = 0, hf_nsplit = 0, hf_nparts = 0;
+    int hf_split_parts = 0;
     int64_t hf_rows = 0, hf_ntbox = 0, hf_nent = 0;
 
     // Modified Helmholtz (treecode) state.
