@@ -266,6 +266,10 @@ void build_tree(Plan& pl) {
         return;
     }
     pl.L = std::clamp(int(std::ceil(std::log(big / 32.0) / std::log(4.0))), 2, 7);
+    if (pl.mode == VPG_MODE_NATIVE && pl.family == VPG_MODIFIED_HELMHOLTZ)
+        // Chebyshev FMM (helm.cu): ~16 points per leaf -- the K0 near field
+        // dominates, the compressed M2L is cheap
+        pl.L = std::clamp(int(std::ceil(std::log(big / 16.0) / std::log(4.0))), 2, 8);
     const int L = pl.L;
     const int64_t nleaf = int64_t(1) << (2 * L);
     const int64_t nall = lvl_base(L + 1);
