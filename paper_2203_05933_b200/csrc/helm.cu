@@ -320,25 +320,6 @@ __global__ void hf_compress_kernel(HfLevels hl, const int32_t* src_cnt, const do
     Wt[r * k + i] = acc;
 }
 
-// Lt[T] = sum over T's entries (list order) of C_e Wt[src_e]
-__global__ void hf_m2l_kernel(int k, const int32_t* tbox, const int32_t* toff, const int32_t* esrc,
-                              const int32_t* eop, const double* C, const double* Wt, double* Lt) {
-    __shared__ double ws[kHfMaxK];
-    const int64_t ti = blockIdx.x;
-    const int i = threadIdx.x;
-    double acc = 0.0;
-    for (int e = toff[ti]; e < toff[ti + 1]; ++e) {
-        __syncthreads();
-        if (i < k) ws[i] = Wt[int64_t(esrc[e]) * k + i];
-        __syncthreads();
-        if (i < k) {
-            const double* c = C + int64_t(eop[e]) * k * k;
-            for (int j = 0; j < k; ++j) acc = fma(c[j * k + i], ws[j], acc);
-        }
-    }
-    if (i < k) Lt[int64_t(tbox[ti]) * k + i] = acc;
-}
-
 // M2L on the FP64 tensor cores: a CTA takes a tile of up to 16 target boxes
 // of one level and walks the level's offsets in a fixed order; per offset
 // it stages C_o (64 x 64) once for the whole tile and the sources' Wt as
