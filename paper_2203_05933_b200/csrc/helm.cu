@@ -266,34 +266,45 @@ __global__ void hf_kmat_kernel(const int2* offs, int noff, int n, const double* 
     A[idx] = kInv2Pi * k0_dev(lambda * sqrt(dx * dx + dy * dy), k0tab);
 }
 
-// W_P = sum_c S_{c&1} W_c S_{c>>1}^T over children with sources (c order)
+// W_P = sum_c S_{c&1} W_c S_{c>>1}^T over children with sources (c order):
+// the four children staged together, T_c = S_{c&1} W_c for all c in one
+// pass, then the second products summed in quadrant order.
 __global__ void hf_m2m_kernel(int level, int n, const double* S, const int32_t* scnt_l,
                               const int32_t* scnt_c, int64_t base_p, int64_t base_c, double* W) {
-    __shared__ double wc[kHfMaxN * kHfMaxN], tt[kHfMaxN * kHfMaxN];
+    __shared__ double wc[4][kHfMaxN * kHfMaxN], tt[4][kHfMaxN * kHfMaxN];
     const int64_t b = blockIdx.x;
     if (scnt_l[b] == 0) return;
     const int n2 = n * n;
     const int t = threadIdx.x;
     const int a = t / n, bb = t % n;
-    double acc = 0.0;
-    for (int c = 0; c < 4; ++c) {
-        const int64_t child = (b << 2) | c;
-        if (scnt_c[child] == 0) continue;
-        __syncthreads();
-        if (t < n2) wc[t] = W[(base_c + child) * n2 + t];
-        __syncthreads();
-        const double* Sx = S + (c & 1) * n * n;
-        const double* Sy = S + (c >> 1) * n * n;
-        if (t < n2) {
-            double v = 0.0;
-            for (int k = 0; k < n; ++k) v = fma(Sx[a * n + k], wc[k * n + bb], v);
-            tt[t] = v;
-        }
-        __syncthreads();
-        if (t < n2)
-            for (int k = 0; k < n; ++k) acc = fma(Sy[bb * n + k], tt[a * n + k], acc);
+    bool has[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) has[c] = scnt_c[(b << 2) | c] > 0;
+    for (int i = t; i < 4 * n2; i += blockDim.x) {
+        const int c = i / n2, e = i % n2;
+        wc[c][e] = has[c] ? W[(base_c + ((b << 2) | c)) * n2 + e] : 0.0;
     }
-    if (t < n2) W[(base_p + b) * n2 + t] = acc;
+    __syncthreads();
+    if (t < n2)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            if (!has[c]) continue;
+            const double* Sx = S + (c & 1) * n * n;
+            double v = 0.0;
+            for (int q = 0; q < n; ++q) v = fma(Sx[a * n + q], wc[c][q * n + bb], v);
+            tt[c][t] = v;
+        }
+    __syncthreads();
+    if (t < n2) {
+        double acc = 0.0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            if (!has[c]) continue;
+            const double* Sy = S + (c >> 1) * n * n;
+            for (int q = 0; q < n; ++q) acc = fma(Sy[bb * n + q], tt[c][a * n + q], acc);
+        }
+        W[(base_p + b) * n2 + t] = acc;
+    }
 }
 
 struct HfLevels {
@@ -302,39 +313,22 @@ struct HfLevels {
     int64_t voff[17];    // V offsets (doubles) per level
 };
 
-// Wt[r] = V_l^T W[r] for rows with sources (thread per basis vector)
-__global__ void hf_compress_kernel(HfLevels hl, const int32_t* src_cnt, const double* Vt,
-                                   const double* W, double* Wt) {
-    const int64_t r = blockIdx.x;
-    int l = hl.lmin;
-    while (l < hl.L && r >= hl.base[l + 1]) ++l;
-    const int64_t b = r - hl.base[l];
-    if (src_cnt[lvl_base(l) + b] == 0) return;
-    const int n2 = hl.n * hl.n, k = hl.k;
-    const int i = threadIdx.x;
-    if (i >= k) return;
-    const double* v = Vt + hl.voff[l];
-    const double* w = W + r * n2;
-    double acc = 0.0;
-    for (int j = 0; j < n2; ++j) acc = fma(v[j * k + i], w[j], acc);
-    Wt[r * k + i] = acc;
-}
-
-// M2L on the FP64 tensor cores: a CTA takes a tile of up to 16 target boxes
+// M2L on the FP64 tensor cores: a CTA takes a tile of up to 64 target boxes
 // of one level and walks the level's offsets in a fixed order; per offset
 // it stages C_o (64 x 64) once for the whole tile and the sources' Wt as
 // the B operand (zeros where a target has no source at that offset), and
 // warp w accumulates output rows 8w..8w+7 for the 16 targets with
 // mma.sync m8n8k4 f64.  C_o is read once per tile instead of once per list
 // entry (the per-entry form was L2-bandwidth bound).
-constexpr int kHfTile = 16;
+constexpr int kHfTile = 64;
 
 __global__ void __launch_bounds__(256)
 hf_m2l_tc_kernel(const int4* tiles, const int32_t* tbox, const int32_t* srcof, const double* C,
                  const double* Wt, double* Lt, double* Lpart) {
     constexpr int k = kHfMaxK;
-    __shared__ __align__(16) double cs[k * k];          // [j][i]
-    __shared__ __align__(16) double ws[k * kHfTile];     // [j][t]
+    extern __shared__ __align__(16) double hm2l[];
+    double* cs = hm2l;                 // [j][i]  (k x k)
+    double* ws = hm2l + k * k;         // [j][t]  (k x tile)
     __shared__ int32_t src_s[kHfTile];
     const int4 tl = tiles[2 * blockIdx.x], tr = tiles[2 * blockIdx.x + 1];
     const int t0 = tl.x, nt = tl.y, sbase = tl.z, noff = tl.w;
@@ -342,7 +336,10 @@ hf_m2l_tc_kernel(const int4* tiles, const int32_t* tbox, const int32_t* srcof, c
     const int64_t cb = tr.w;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int kq = lane & 3, rq = lane >> 2;
-    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    constexpr int kNT = kHfTile / 8;  // n-tiles per warp (all of them)
+    double acc[kNT][2];
+#pragma unroll
+    for (int q = 0; q < kNT; ++q) acc[q][0] = acc[q][1] = 0.0;
     for (int o = o0; o < o1; ++o) {
         __syncthreads();
         if (threadIdx.x < kHfTile)
@@ -364,7 +361,7 @@ hf_m2l_tc_kernel(const int4* tiles, const int32_t* tbox, const int32_t* srcof, c
         for (int k4 = 0; k4 < k; k4 += 4) {
             const double a = cs[(k4 + kq) * k + 8 * warp + rq];
 #pragma unroll
-            for (int n8 = 0; n8 < 2; ++n8) {
+            for (int n8 = 0; n8 < kNT; ++n8) {
                 const double b = ws[(k4 + kq) * kHfTile + 8 * n8 + rq];
                 asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                              : "+d"(acc[n8][0]), "+d"(acc[n8][1])
@@ -375,7 +372,7 @@ hf_m2l_tc_kernel(const int4* tiles, const int32_t* tbox, const int32_t* srcof, c
     // lane holds rows 8w + rq, targets 8 n8 + 2 kq + {0, 1}
     const int i = 8 * warp + rq;
 #pragma unroll
-    for (int n8 = 0; n8 < 2; ++n8)
+    for (int n8 = 0; n8 < kNT; ++n8)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int t = 8 * n8 + 2 * kq + h;
@@ -396,39 +393,32 @@ __global__ void hf_m2l_reduce_kernel(const int2* splits, int nparts, const doubl
     Lt[int64_t(sp.x) * kHfMaxK + i] = acc;
 }
 
-// Lv[r] = V_l Lt[r] (+ the parent's Lv interpolated to r's nodes)
-__global__ void hf_expand_kernel(HfLevels hl, int level, const int32_t* tbox, const double* Vc,
-                                 const double* S, const double* Lt, double* Lv) {
-    __shared__ double lp[kHfMaxN * kHfMaxN], tt[kHfMaxN * kHfMaxN], lts[kHfMaxK];
-    const int n = hl.n, n2 = n * n, k = hl.k;
+// L2L: Lv[r] += the parent's Lv interpolated to r's nodes (Lv[r] = V_l Lt[r]
+// already, one cuBLAS GEMM per level); top-down, one launch per level.
+__global__ void hf_l2l_kernel(HfLevels hl, int level, const int32_t* tbox, const double* S, double* Lv) {
+    __shared__ double lp[kHfMaxN * kHfMaxN], tt[kHfMaxN * kHfMaxN];
+    const int n = hl.n, n2 = n * n;
     const int64_t r = tbox[blockIdx.x];
     const int t = threadIdx.x;
     const int a = t / n, bb = t % n;
-    if (t < k) lts[t] = Lt[r * k + t];
-    const bool child = level > hl.lmin;
     const int64_t b = r - hl.base[level];
-    if (child && t < n2) lp[t] = Lv[(hl.base[level - 1] + (b >> 2)) * n2 + t];
+    if (t < n2) lp[t] = Lv[(hl.base[level - 1] + (b >> 2)) * n2 + t];
     __syncthreads();
-    double v = 0.0;
+    const int c = int(b & 3);
+    const double* Sx = S + (c & 1) * n * n;
+    const double* Sy = S + (c >> 1) * n * n;
+    // tt[a'][b] = sum_b' Sy[b'][b] lp[a'][b']; Lv += sum_a' Sx[a'][a] tt[a'][b]
     if (t < n2) {
-        const double* vc = Vc + hl.voff[level];
-        for (int i = 0; i < k; ++i) v = fma(vc[int64_t(i) * n2 + t], lts[i], v);
+        double u = 0.0;
+        for (int q = 0; q < n; ++q) u = fma(Sy[q * n + bb], lp[a * n + q], u);
+        tt[t] = u;
     }
-    if (child) {
-        const int c = int(b & 3);
-        const double* Sx = S + (c & 1) * n * n;
-        const double* Sy = S + (c >> 1) * n * n;
-        // tt[a'][b] = sum_b' Sy[b'][b] lp[a'][b']; v += sum_a' Sx[a'][a] tt[a'][b]
-        if (t < n2) {
-            double u = 0.0;
-            for (int q = 0; q < n; ++q) u = fma(Sy[q * n + bb], lp[a * n + q], u);
-            tt[t] = u;
-        }
-        __syncthreads();
-        if (t < n2)
-            for (int q = 0; q < n; ++q) v = fma(Sx[q * n + a], tt[q * n + bb], v);
+    __syncthreads();
+    if (t < n2) {
+        double v = Lv[r * n2 + t];
+        for (int q = 0; q < n; ++q) v = fma(Sx[q * n + a], tt[q * n + bb], v);
+        Lv[r * n2 + t] = v;
     }
-    if (t < n2) Lv[r * n2 + t] = v;
 }
 
 // barycentric weights of x in [-1, 1] on the n Chebyshev nodes (exact node -> delta)
@@ -972,6 +962,12 @@ void build_helm_fmm(Plan& pl) {
     pl.hf_k = k;
     pl.hf_lmin = lmin;
     pl.P = n;  // reported expansion order: Chebyshev nodes per dimension
+    {
+        cublasHandle_t h = nullptr;
+        VPG_SOLVER(cublasCreate(&h));
+        pl.hf_blas = std::shared_ptr<void>(h, [](void* p) { cublasDestroy(static_cast<cublasHandle_t>(p)); });
+    }
+    smem_optin((const void*)hf_m2l_tc_kernel, int(sizeof(double) * kHfMaxK * (kHfMaxK + kHfTile)));
     smem_optin((const void*)hf_l2p_p2p_kernel,
                int(size_t(kLogTableBytes) + sizeof(double) * kHfWarps * kHfMaxN * kHfMaxN));
     pl.hf = true;
@@ -1028,16 +1024,27 @@ void helm_fmm_apply(const Plan& pl, const double* q_dev, double* out_dev, cudaSt
         VPG_LAUNCH_CHECK();
         ++launches;
     }
-    hf_compress_kernel<<<unsigned(pl.hf_rows), ((k + 31) / 32) * 32, 0, st>>>(hl, pl.src_cnt.p, pl.hf_Vt.p, W, Wt);
-    VPG_LAUNCH_CHECK();
-    ++launches;
+    {
+        // compress: Wt_l (k x rows, column-major) = Vt_l (k x n2) . W_l (n2 x rows), one GEMM per level
+        std::lock_guard<std::mutex> lk(pl.hf_mu);
+        cublasHandle_t h = static_cast<cublasHandle_t>(pl.hf_blas.get());
+        VPG_SOLVER(cublasSetStream(h, st));
+        const double one = 1.0, zero = 0.0;
+        for (int l = pl.hf_lmin; l <= L; ++l) {
+            const int rows_l = 1 << (2 * l);
+            const int64_t b0 = pl.hf_row_base[size_t(l)];
+            VPG_SOLVER(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, k, rows_l, n2, &one, pl.hf_Vt.p + pl.hf_V_off[size_t(l)],
+                                   k, W + b0 * n2, n2, &zero, Wt + b0 * k, k));
+            ++launches;
+        }
+    }
     mark(3);
     if (pl.hf_ntbox > 0) {
         double* Lpart = nullptr;
         if (pl.hf_nparts > 0)
             VPG_CUDA(cudaMallocAsync(&Lpart, sizeof(double) * size_t(pl.hf_nparts) * kHfMaxK, st));
-        hf_m2l_tc_kernel<<<unsigned(pl.hf_ntiles), 256, 0, st>>>(pl.hf_tiles.p, pl.hf_tbox.p, pl.hf_srcof.p,
-                                                                  pl.hf_C.p, Wt, Lt, Lpart);
+        hf_m2l_tc_kernel<<<unsigned(pl.hf_ntiles), 256, sizeof(double) * kHfMaxK * (kHfMaxK + kHfTile), st>>>(
+            pl.hf_tiles.p, pl.hf_tbox.p, pl.hf_srcof.p, pl.hf_C.p, Wt, Lt, Lpart);
         VPG_LAUNCH_CHECK();
         ++launches;
         if (pl.hf_nsplit > 0) {
@@ -1049,11 +1056,25 @@ void helm_fmm_apply(const Plan& pl, const double* q_dev, double* out_dev, cudaSt
         ++launches;
     }
     mark(4);
-    for (int l = pl.hf_lmin; l <= L; ++l) {
+    {
+        // expand: Lv_l (n2 x rows) = Vc_l (n2 x k) . Lt_l (k x rows), one GEMM per level
+        std::lock_guard<std::mutex> lk(pl.hf_mu);
+        cublasHandle_t h = static_cast<cublasHandle_t>(pl.hf_blas.get());
+        VPG_SOLVER(cublasSetStream(h, st));
+        const double one = 1.0, zero = 0.0;
+        for (int l = pl.hf_lmin; l <= L; ++l) {
+            const int rows_l = 1 << (2 * l);
+            const int64_t b0 = pl.hf_row_base[size_t(l)];
+            VPG_SOLVER(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, n2, rows_l, k, &one, pl.hf_Vc.p + pl.hf_V_off[size_t(l)],
+                                   n2, Lt + b0 * k, k, &zero, Lv + b0 * n2, n2));
+            ++launches;
+        }
+    }
+    // L2L, top-down
+    for (int l = pl.hf_lmin + 1; l <= L; ++l) {
         const int64_t t0 = pl.hf_lvl_t0[size_t(l)], t1 = pl.hf_lvl_t0[size_t(l + 1)];
         if (t1 == t0) continue;
-        hf_expand_kernel<<<unsigned(t1 - t0), std::max(tn2, ((k + 31) / 32) * 32), 0, st>>>(
-            hl, l, pl.hf_tbox.p + t0, pl.hf_Vc.p, pl.hf_tab.p + 64, Lt, Lv);
+        hf_l2l_kernel<<<unsigned(t1 - t0), tn2, 0, st>>>(hl, l, pl.hf_tbox.p + t0, pl.hf_tab.p + 64, Lv);
         VPG_LAUNCH_CHECK();
         ++launches;
     }
