@@ -326,10 +326,12 @@ __global__ void __launch_bounds__(256)
 hf_m2l_tc_kernel(const int4* tiles, const int32_t* tbox, const int32_t* srcof, const double* C,
                  const double* Wt, double* Lt, double* Lpart) {
     constexpr int k = kHfMaxK;
+    // row strides == 4 (mod 16) doubles: the DMMA fragment loads are
+    // bank-conflict free (lanes (kq, rq) -> 4 kq + rq distinct)
+    constexpr int kCS = k + 4, kWS = kHfTile + 4;
     extern __shared__ __align__(16) double hm2l[];
-    double* cs = hm2l;                 // [j][i]  (k x k)
-    double* ws = hm2l + k * k;         // [j][t]  (k x tile)
-    __shared__ int32_t src_s[kHfTile];
+    double* cs = hm2l;                 // [j][i]  (k x kCS)
+    double* ws = hm2l + k * kCS;       // [j][t]  (k x kWS)
     const int4 tl = tiles[2 * blockIdx.x], tr = tiles[2 * blockIdx.x + 1];
     const int t0 = tl.x, nt = tl.y, sbase = tl.z, noff = tl.w;
     const int o0 = tr.x, o1 = tr.y, slot = tr.z;
@@ -340,29 +342,42 @@ hf_m2l_tc_kernel(const int4* tiles, const int32_t* tbox, const int32_t* srcof, c
     double acc[kNT][2];
 #pragma unroll
     for (int q = 0; q < kNT; ++q) acc[q][0] = acc[q][1] = 0.0;
-    for (int o = o0; o < o1; ++o) {
-        __syncthreads();
-        if (threadIdx.x < kHfTile)
-            src_s[threadIdx.x] = threadIdx.x < nt ? srcof[sbase + int64_t(t0 + threadIdx.x) * noff + o] : -1;
-        __syncthreads();
-        bool any = false;
-#pragma unroll
-        for (int t = 0; t < kHfTile; ++t) any |= src_s[t] >= 0;
-        if (!any) continue;  // block-uniform
+    // per thread: C elements i2 = tid + 256 r (double2), W column j = tid % 64
+    // for targets tid / 64 + 4 r -- all loads of offset o+1 are in flight
+    // while the DMMAs of offset o run (register double buffer)
+    constexpr int kCR = k * k / 2 / 256, kWR = k * kHfTile / 256;
+    const int wj = threadIdx.x & 63, wt0 = threadIdx.x >> 6;
+    double2 creg[kCR];
+    double wreg[kWR];
+    auto fetch = [&](int o) {
         const double2* cg = reinterpret_cast<const double2*>(C + (cb + o) * int64_t(k) * k);
-        for (int i = threadIdx.x; i < k * k / 2; i += blockDim.x) reinterpret_cast<double2*>(cs)[i] = cg[i];
-        for (int i = threadIdx.x; i < k * kHfTile; i += blockDim.x) {
-            const int t = i % kHfTile, j = i / kHfTile;
-            const int sr = src_s[t];
-            ws[j * kHfTile + t] = sr >= 0 ? Wt[int64_t(sr) * k + j] : 0.0;
+#pragma unroll
+        for (int r = 0; r < kCR; ++r) creg[r] = cg[threadIdx.x + 256 * r];
+#pragma unroll
+        for (int r = 0; r < kWR; ++r) {
+            const int t = wt0 + 4 * r;
+            const int sr = t < nt ? srcof[sbase + int64_t(t0 + t) * noff + o] : -1;
+            wreg[r] = sr >= 0 ? Wt[int64_t(sr) * k + wj] : 0.0;
         }
+    };
+    if (o0 < o1) fetch(o0);
+    for (int o = o0; o < o1; ++o) {
+        __syncthreads();  // the previous offset's DMMAs are done with cs / ws
+#pragma unroll
+        for (int r = 0; r < kCR; ++r) {
+            const int e = 2 * (threadIdx.x + 256 * r), jj = e / k, ii = e % k;
+            *reinterpret_cast<double2*>(cs + jj * kCS + ii) = creg[r];
+        }
+#pragma unroll
+        for (int r = 0; r < kWR; ++r) ws[wj * kWS + wt0 + 4 * r] = wreg[r];
         __syncthreads();
+        if (o + 1 < o1) fetch(o + 1);
 #pragma unroll 4
         for (int k4 = 0; k4 < k; k4 += 4) {
-            const double a = cs[(k4 + kq) * k + 8 * warp + rq];
+            const double a = cs[(k4 + kq) * kCS + 8 * warp + rq];
 #pragma unroll
             for (int n8 = 0; n8 < kNT; ++n8) {
-                const double b = ws[(k4 + kq) * kHfTile + 8 * n8 + rq];
+                const double b = ws[(k4 + kq) * kWS + 8 * n8 + rq];
                 asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                              : "+d"(acc[n8][0]), "+d"(acc[n8][1])
                              : "d"(a), "d"(b));
@@ -967,7 +982,7 @@ void build_helm_fmm(Plan& pl) {
         VPG_SOLVER(cublasCreate(&h));
         pl.hf_blas = std::shared_ptr<void>(h, [](void* p) { cublasDestroy(static_cast<cublasHandle_t>(p)); });
     }
-    smem_optin((const void*)hf_m2l_tc_kernel, int(sizeof(double) * kHfMaxK * (kHfMaxK + kHfTile)));
+    smem_optin((const void*)hf_m2l_tc_kernel, int(sizeof(double) * kHfMaxK * (kHfMaxK + kHfTile + 8)));
     smem_optin((const void*)hf_l2p_p2p_kernel,
                int(size_t(kLogTableBytes) + sizeof(double) * kHfWarps * kHfMaxN * kHfMaxN));
     pl.hf = true;
@@ -1043,7 +1058,7 @@ void helm_fmm_apply(const Plan& pl, const double* q_dev, double* out_dev, cudaSt
         double* Lpart = nullptr;
         if (pl.hf_nparts > 0)
             VPG_CUDA(cudaMallocAsync(&Lpart, sizeof(double) * size_t(pl.hf_nparts) * kHfMaxK, st));
-        hf_m2l_tc_kernel<<<unsigned(pl.hf_ntiles), 256, sizeof(double) * kHfMaxK * (kHfMaxK + kHfTile), st>>>(
+        hf_m2l_tc_kernel<<<unsigned(pl.hf_ntiles), 256, sizeof(double) * kHfMaxK * (kHfMaxK + kHfTile + 8), st>>>(
             pl.hf_tiles.p, pl.hf_tbox.p, pl.hf_srcof.p, pl.hf_C.p, Wt, Lt, Lpart);
         VPG_LAUNCH_CHECK();
         ++launches;
