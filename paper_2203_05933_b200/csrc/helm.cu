@@ -393,18 +393,18 @@ hf_m2l_tc_kernel(const int4* tiles, const int32_t* tbox, const int32_t* srcof, c
             const int t = 8 * n8 + 2 * kq + h;
             if (t >= nt) continue;
             if (slot < 0) Lt[int64_t(tbox[t0 + t]) * k + i] = acc[n8][h];
-            else Lpart[(int64_t(slot) + t) * k + i] = acc[n8][h];  // one target per split tile
+            else Lpart[(int64_t(slot) + t) * k + i] = acc[n8][h];
         }
 }
 
 // Split targets (the first M2L level has up to ~200 offsets per box): the
-// offset ranges' partial sums added in range order.
+// offset ranges' partial sums (kHfTile apart) added in range order.
 __global__ void hf_m2l_reduce_kernel(const int2* splits, int nparts, const double* Lpart, double* Lt) {
     const int2 sp = splits[blockIdx.x];
     const int i = threadIdx.x;
     if (i >= kHfMaxK) return;
     double acc = 0.0;
-    for (int p = 0; p < nparts; ++p) acc += Lpart[(int64_t(sp.y) + p) * kHfMaxK + i];
+    for (int p = 0; p < nparts; ++p) acc += Lpart[(int64_t(sp.y) + int64_t(p) * kHfTile) * kHfMaxK + i];
     Lt[int64_t(sp.x) * kHfMaxK + i] = acc;
 }
 
@@ -920,16 +920,18 @@ void build_helm_fmm(Plan& pl) {
                     srcof[row0 + size_t(eop[size_t(e)] - cblk0)] = esrc[size_t(e)];
             }
             if (noff > kSplitOffsets) {
-                // one target per tile, offsets in ranges -> partials, reduced in order
+                // target tiles x offset ranges -> partial sums (slot + p * kHfTile + t),
+                // reduced per target in range order
                 const int np = parts_per_split;
-                for (int64_t ti = a0; ti < a1; ++ti) {
-                    splits.push_back(make_int2(tbox[size_t(ti)], int(slot)));
+                for (int64_t ti = a0; ti < a1; ti += kHfTile) {
+                    const int cnt = int(std::min<int64_t>(kHfTile, a1 - ti));
+                    for (int t = 0; t < cnt; ++t) splits.push_back(make_int2(tbox[size_t(ti + t)], int(slot + t)));
                     for (int p = 0; p < np; ++p) {
                         const int o0 = int(int64_t(noff) * p / np), o1 = int(int64_t(noff) * (p + 1) / np);
-                        tiles.push_back(make_int4(int(ti), 1, int(sbase), noff));
-                        tiles.push_back(make_int4(o0, o1, int(slot + p), int(cblk0)));
+                        tiles.push_back(make_int4(int(ti), cnt, int(sbase), noff));
+                        tiles.push_back(make_int4(o0, o1, int(slot + p * kHfTile), int(cblk0)));
                     }
-                    slot += np;
+                    slot += int64_t(np) * kHfTile;
                 }
             } else {
                 for (int64_t ti = a0; ti < a1; ti += kHfTile) {
