@@ -307,6 +307,85 @@ __global__ void hf_m2m_kernel(int level, int n, const double* S, const int32_t* 
     }
 }
 
+// barycentric weights of x in [-1, 1] on the n Chebyshev nodes (exact node -> delta)
+__device__ __forceinline__ void hf_bary(const double* nodes, const double* bw, int n, double x, double* w) {
+    int hit = -1;
+    double sum = 0.0;
+#pragma unroll
+    for (int a = 0; a < kHfMaxN; ++a) {
+        if (a < n) {
+            const double d = x - nodes[a];
+            if (d == 0.0) hit = a;
+            w[a] = bw[a] / (d == 0.0 ? 1.0 : d);
+            sum += w[a];
+        }
+    }
+    const double inv = 1.0 / sum;
+#pragma unroll
+    for (int a = 0; a < kHfMaxN; ++a)
+        if (a < n) w[a] = hit >= 0 ? (a == hit ? 1.0 : 0.0) : w[a] * inv;
+}
+
+// P2M at the leaves of the Chebyshev FMM: a warp per leaf (leaves hold
+// ~16 points), sources 32 at a time: lane j builds the barycentric rows
+// l_a(x_j), l_b(y_j) in smem, then each lane accumulates its ~n^2/32 of
+// W[a][b] = sum_j q_j l_a(x_j) l_b(y_j) in source order.
+constexpr int kAntWarps = 4;  // 41 KB of static smem
+
+__global__ void __launch_bounds__(kAntWarps * 32)
+hf_anterp_leaf_kernel(int L, int n, double x0, double y0, double side, const int32_t* scnt_leaf,
+                      const int32_t* soff, const double2* sxy, const double* q, const double* tab,
+                      int64_t base_leaf, double* W) {
+    __shared__ double rows[kAntWarps][2][32][kHfMaxN];
+    __shared__ double qsh[kAntWarps][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t b = int64_t(blockIdx.x) * kAntWarps + warp;
+    if (b >= (int64_t(1) << (2 * L)) || scnt_leaf[b] == 0) return;
+    const int n2 = n * n;
+    const double* nodes = tab;
+    const double* bw = tab + 32;
+    const double s = side / double(1 << L);
+    const double cx = x0 + (squash2(uint32_t(b)) + 0.5) * s;
+    const double cy = y0 + (squash2(uint32_t(b) >> 1) + 0.5) * s;
+    const int e0 = soff[b], e1 = soff[b + 1];
+    double acc[(kHfMaxN * kHfMaxN + 31) / 32];
+#pragma unroll
+    for (int r = 0; r < (kHfMaxN * kHfMaxN + 31) / 32; ++r) acc[r] = 0.0;
+    for (int base = e0; base < e1; base += 32) {
+        const int cnt = min(32, e1 - base);
+        __syncwarp();
+        if (lane < cnt) {
+            const double2 p = sxy[base + lane];
+            double w[kHfMaxN];
+            hf_bary(nodes, bw, n, (p.x - cx) * 2.0 / s, w);
+#pragma unroll
+            for (int a = 0; a < kHfMaxN; ++a)
+                if (a < n) rows[warp][0][lane][a] = w[a];
+            hf_bary(nodes, bw, n, (p.y - cy) * 2.0 / s, w);
+#pragma unroll
+            for (int a = 0; a < kHfMaxN; ++a)
+                if (a < n) rows[warp][1][lane][a] = w[a];
+            qsh[warp][lane] = q[base + lane];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < (kHfMaxN * kHfMaxN + 31) / 32; ++r) {
+            const int e = lane + 32 * r;
+            if (e < n2) {
+                const int a = e / n, bb = e % n;
+                double v = acc[r];
+                for (int j = 0; j < cnt; ++j) v = fma(qsh[warp][j] * rows[warp][0][j][a], rows[warp][1][j][bb], v);
+                acc[r] = v;
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < (kHfMaxN * kHfMaxN + 31) / 32; ++r) {
+        const int e = lane + 32 * r;
+        if (e < n2) W[(base_leaf + b) * n2 + e] = acc[r];
+    }
+}
+
 struct HfLevels {
     int lmin, L, n, k;
     int64_t base[17];    // first row of each level
@@ -434,25 +513,6 @@ __global__ void hf_l2l_kernel(HfLevels hl, int level, const int32_t* tbox, const
         for (int q = 0; q < n; ++q) v = fma(Sx[q * n + a], tt[q * n + bb], v);
         Lv[r * n2 + t] = v;
     }
-}
-
-// barycentric weights of x in [-1, 1] on the n Chebyshev nodes (exact node -> delta)
-__device__ __forceinline__ void hf_bary(const double* nodes, const double* bw, int n, double x, double* w) {
-    int hit = -1;
-    double sum = 0.0;
-#pragma unroll
-    for (int a = 0; a < kHfMaxN; ++a) {
-        if (a < n) {
-            const double d = x - nodes[a];
-            if (d == 0.0) hit = a;
-            w[a] = bw[a] / (d == 0.0 ? 1.0 : d);
-            sum += w[a];
-        }
-    }
-    const double inv = 1.0 / sum;
-#pragma unroll
-    for (int a = 0; a < kHfMaxN; ++a)
-        if (a < n) w[a] = hit >= 0 ? (a == hit ? 1.0 : 0.0) : w[a] * inv;
 }
 
 // Warp per near-field chunk: far field from the leaf's Lv (barycentric) plus
@@ -1018,18 +1078,10 @@ void helm_fmm_apply(const Plan& pl, const double* q_dev, double* out_dev, cudaSt
     VPG_LAUNCH_CHECK();
     ++launches;
     mark(1);
-    // P2M at the leaves (anterp_kernel with n nodes at level L)
-    HelmParams hp{};
-    hp.L = L;
-    hp.x0 = pl.x0;
-    hp.y0 = pl.y0;
-    hp.side = pl.side;
-    hp.lambda = pl.lambda;
-    hp.m[L] = n;
-    hp.w_off[L] = pl.hf_row_base[size_t(L)] * n2;
-    const int ath = std::max(((n2 + 31) / 32) * 32, 2 * kAntChunk);
-    anterp_kernel<<<unsigned(int64_t(1) << (2 * L)), ath, sizeof(double) * 2 * kAntChunk * kMaxM, st>>>(
-        hp, L, pl.src_cnt.p + lvl_base(L), pl.src_off.p, pl.src_sorted.p, qs, pl.helm_nodes.p, pl.helm_bw.p, W);
+    // P2M at the leaves (warp per leaf)
+    hf_anterp_leaf_kernel<<<unsigned(((int64_t(1) << (2 * L)) + kAntWarps - 1) / kAntWarps), kAntWarps * 32, 0, st>>>(
+        L, n, pl.x0, pl.y0, pl.side, pl.src_cnt.p + lvl_base(L), pl.src_off.p, pl.src_sorted.p, qs, pl.hf_tab.p,
+        pl.hf_row_base[size_t(L)], W);
     VPG_LAUNCH_CHECK();
     ++launches;
     mark(2);
