@@ -12,6 +12,7 @@
 //     per oversampled source node.
 #include <algorithm>
 #include <memory>
+#include <map>
 #include <vector>
 
 #include "plan.cuh"
@@ -26,13 +27,14 @@ inline unsigned nblk(int64_t n, int t) { return unsigned((n + t - 1) / t); }
 constexpr int kCorrWarps = 8;
 
 __global__ void __launch_bounds__(kCorrWarps * 32)
-corr_apply_kernel(int64_t nt, const int32_t* blk_off, const int32_t* blk_cell,
+corr_apply_kernel(int64_t nt, const int32_t* tlist, const int32_t* blk_off, const int32_t* blk_cell,
                   const int32_t* blk_pool, const int64_t* pool_off,
                   const double* pool_vals, const int32_t* node_off,
                   const double* f, double* out) {
     const int lane = threadIdx.x & 31;
-    const int64_t t = int64_t(blockIdx.x) * kCorrWarps + (threadIdx.x >> 5);
-    if (t >= nt) return;
+    const int64_t ti = int64_t(blockIdx.x) * kCorrWarps + (threadIdx.x >> 5);
+    if (ti >= nt) return;
+    const int64_t t = tlist ? tlist[ti] : ti;
     double acc = 0.0;
     const int k0 = blk_off[t], k1 = blk_off[t + 1];
     for (int k = k0; k < k1; ++k) {
@@ -45,6 +47,61 @@ corr_apply_kernel(int64_t nt, const int32_t* blk_off, const int32_t* blk_cell,
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) out[t] += acc;
+}
+
+// Lattice groups on the FP64 tensor cores: a CTA takes 64 groups (64
+// targets each) and walks the shared 64 x 64 row blocks M_q: out[64g + u] +=
+// sum_q sum_i M_q[u][i] f[cell(g, q) + i] as Y = M_q F_q (mma.sync m8n8k4),
+// M_q and the tile's f segments staged in smem (strides == 4 mod 16).
+constexpr int kLatTile = 64;
+
+__global__ void __launch_bounds__(256)
+corr_lattice_kernel(int64_t ngroups, int nmat, const int32_t* group, const int32_t* cellof,
+                    const int64_t* moff, const double* pool_vals, const double* f, double* out) {
+    constexpr int K = 64, kS = K + 4;
+    extern __shared__ __align__(16) double lsm[];
+    double* ms = lsm;            // [u][i]
+    double* fs = lsm + K * kS;   // [i][g]
+    const int64_t g0 = int64_t(blockIdx.x) * kLatTile;
+    const int ng = int(min(int64_t(kLatTile), ngroups - g0));
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int kq = lane & 3, rq = lane >> 2;
+    double acc[8][2];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q][0] = acc[q][1] = 0.0;
+    for (int q = 0; q < nmat; ++q) {
+        __syncthreads();
+        const double* mg = pool_vals + moff[q];
+        for (int e = threadIdx.x; e < K * K; e += blockDim.x) ms[(e / K) * kS + (e % K)] = mg[e];
+        bool any = false;
+        for (int e = threadIdx.x; e < K * kLatTile; e += blockDim.x) {
+            const int g = e / K, i = e % K;  // coalesced over i
+            const int c = g < ng ? cellof[(g0 + g) * nmat + q] : -1;
+            any |= c >= 0;
+            fs[i * kS + g] = c >= 0 ? f[int64_t(c) + i] : 0.0;
+        }
+        if (!__syncthreads_or(any)) continue;
+#pragma unroll 4
+        for (int k4 = 0; k4 < K; k4 += 4) {
+            const double a = ms[(8 * warp + rq) * kS + k4 + kq];
+#pragma unroll
+            for (int n8 = 0; n8 < 8; ++n8) {
+                const double b = fs[(k4 + kq) * kS + 8 * n8 + rq];
+                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                             : "+d"(acc[n8][0]), "+d"(acc[n8][1])
+                             : "d"(a), "d"(b));
+            }
+        }
+    }
+    // lane holds rows u = 8 warp + rq, groups 8 n8 + 2 kq + {0, 1}
+    const int u = 8 * warp + rq;
+#pragma unroll
+    for (int n8 = 0; n8 < 8; ++n8)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int g = 8 * n8 + 2 * kq + h;
+            if (g < ng) out[int64_t(group[g0 + g]) * K + u] += acc[n8][h];
+        }
 }
 
 __global__ void charges_kernel(const int32_t* cell_type, const int32_t* node_off,
@@ -148,6 +205,99 @@ int vpg_corr_create(int64_t nt, const int32_t* blk_off, int64_t nblocks,
         upload(c->pool_off, pool_off, size_t(npool + 1));
         upload(c->pool_vals, pool_vals, size_t(nvals));
         upload(c->node_off, node_off, size_t(ncell + 1));
+        // lattice groups: 64 consecutive targets with identical block-cell
+        // sequences whose rows are base_r + u of contiguous 64 x 64 blocks
+        {
+            std::map<int64_t, int> mat_of;  // pool_off of the block -> matrix index
+            std::vector<int64_t> moff;
+            std::vector<int32_t> groups, cells_tmp, other;
+            std::vector<std::vector<std::pair<int, int32_t>>> gcells;  // per group: (matrix, cell f offset)
+            for (int64_t g = 0; g * 64 < nt; ++g) {
+                const int64_t t0 = g * 64;
+                bool ok = t0 + 64 <= nt;
+                const int m = ok ? blk_off[t0 + 1] - blk_off[t0] : 0;
+                std::vector<std::pair<int, int32_t>> mine;
+                for (int64_t u = 0; ok && u < 64; ++u) ok = blk_off[t0 + u + 1] - blk_off[t0 + u] == m;
+                for (int r = 0; ok && r < m; ++r) {
+                    const int64_t k0 = blk_off[t0] + r;
+                    const int32_t cell = blk_cell[k0], base = blk_pool[k0];
+                    if (base + 63 >= npool) { ok = false; break; }
+                    const int64_t p0 = pool_off[base];
+                    for (int64_t u = 0; ok && u < 64; ++u) {
+                        const int64_t ku = blk_off[t0 + u] + r;
+                        ok = blk_cell[ku] == cell && blk_pool[ku] == base + u && pool_off[base + u] == p0 + 64 * u &&
+                             pool_off[base + u + 1] == p0 + 64 * (u + 1) && node_off[cell] + 64 <= node_off[ncell];
+                    }
+                    if (!ok) break;
+                    auto it = mat_of.find(p0);
+                    int q;
+                    if (it == mat_of.end()) {
+                        q = int(moff.size());
+                        mat_of[p0] = q;
+                        moff.push_back(p0);
+                    } else {
+                        q = it->second;
+                    }
+                    for (const auto& e : mine) ok = ok && e.first != q;  // one cell per matrix
+                    mine.emplace_back(q, node_off[cell]);
+                }
+                if (ok && m > 0) {
+                    groups.push_back(int32_t(t0 / 64));
+                    gcells.push_back(std::move(mine));
+                } else {
+                    for (int64_t u = t0; u < std::min<int64_t>(t0 + 64, nt); ++u) other.push_back(int32_t(u));
+                }
+            }
+            // only blocks shared by many groups (the lattice table) pay off as
+            // GEMMs: groups touching a rarely used block go to the CSR kernel
+            std::vector<int> uses(moff.size(), 0);
+            for (const auto& gc : gcells)
+                for (const auto& e : gc) ++uses[size_t(e.first)];
+            std::vector<int> remap(moff.size(), -1);
+            std::vector<int64_t> shared_off;
+            for (size_t q = 0; q < moff.size(); ++q)
+                if (uses[q] >= 32 && shared_off.size() < 64) {
+                    remap[q] = int(shared_off.size());
+                    shared_off.push_back(moff[q]);
+                }
+            {
+                std::vector<int32_t> g2;
+                std::vector<std::vector<std::pair<int, int32_t>>> c2;
+                for (size_t g = 0; g < groups.size(); ++g) {
+                    bool all = true;
+                    for (auto& e : gcells[g]) all = all && remap[size_t(e.first)] >= 0;
+                    if (all) {
+                        for (auto& e : gcells[g]) e.first = remap[size_t(e.first)];
+                        g2.push_back(groups[g]);
+                        c2.push_back(std::move(gcells[g]));
+                    } else {
+                        for (int64_t u = int64_t(groups[g]) * 64; u < int64_t(groups[g]) * 64 + 64; ++u)
+                            other.push_back(int32_t(u));
+                    }
+                }
+                groups.swap(g2);
+                gcells.swap(c2);
+                moff.swap(shared_off);
+                std::sort(other.begin(), other.end());
+            }
+            const int nmat = int(moff.size());
+            if (groups.size() < 16) {  // not worth it: everything through the CSR kernel
+                groups.clear();
+                other.resize(size_t(nt));
+                for (int64_t u = 0; u < nt; ++u) other[size_t(u)] = int32_t(u);
+            }
+            std::vector<int32_t> cellof(groups.size() * size_t(std::max(nmat, 1)), -1);
+            for (size_t g = 0; g < groups.size(); ++g)
+                for (const auto& e : gcells[g]) cellof[g * size_t(nmat) + size_t(e.first)] = e.second;
+            c->nlat = int64_t(groups.size());
+            c->nmat = groups.empty() ? 0 : nmat;
+            c->nother = int64_t(other.size());
+            upload(c->lat_group, groups.data(), groups.size());
+            upload(c->lat_cell, cellof.data(), groups.empty() ? 0 : cellof.size());
+            upload(c->lat_moff, moff.data(), groups.empty() ? 0 : moff.size());
+            upload(c->other_t, other.data(), other.size());
+            if (c->nlat) smem_optin((const void*)corr_lattice_kernel, int(sizeof(double) * 64 * 68 * 2));
+        }
         *corr = c.release();
     });
 }
@@ -171,10 +321,16 @@ int vpg_corr_apply(const vpg_corr* c, const double* f, int64_t nf, double* out,
             if (c->nt)
                 VPG_CUDA(cudaMemcpyAsync(od, out, sizeof(double) * size_t(c->nt), cudaMemcpyHostToDevice, os.s));
         }
-        if (c->nt) {
-            corr_apply_kernel<<<nblk(c->nt, kCorrWarps), kCorrWarps * 32, 0, os.s>>>(
-                c->nt, c->blk_off.p, c->blk_cell.p, c->blk_pool.p, c->pool_off.p, c->pool_vals.p,
-                c->node_off.p, dev ? f : fd, dev ? out : od);
+        if (c->nlat > 0) {
+            corr_lattice_kernel<<<nblk(c->nlat, kLatTile), 256, sizeof(double) * 64 * 68 * 2, os.s>>>(
+                c->nlat, int(c->nmat), c->lat_group.p, c->lat_cell.p, c->lat_moff.p, c->pool_vals.p, dev ? f : fd,
+                dev ? out : od);
+            VPG_LAUNCH_CHECK();
+        }
+        if (c->nother) {
+            corr_apply_kernel<<<nblk(c->nother, kCorrWarps), kCorrWarps * 32, 0, os.s>>>(
+                c->nother, c->other_t.p, c->blk_off.p, c->blk_cell.p, c->blk_pool.p, c->pool_off.p,
+                c->pool_vals.p, c->node_off.p, dev ? f : fd, dev ? out : od);
             VPG_LAUNCH_CHECK();
         }
         if (!dev) {

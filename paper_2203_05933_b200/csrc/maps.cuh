@@ -10,6 +10,14 @@ struct vpg_corr {
     vpg::DBuf<int32_t> blk_off, blk_cell, blk_pool, node_off;
     vpg::DBuf<int64_t> pool_off;
     vpg::DBuf<double> pool_vals;
+    // lattice fast path (corr.cu): 64-target groups whose blocks read shared
+    // 64 x 64 row blocks (the box lattice table, potential.cpp:256-267) run
+    // as tensor-core GEMMs; every other target through the CSR kernel
+    int64_t nlat = 0, nmat = 0, nother = 0;
+    vpg::DBuf<int32_t> lat_group;   // group g -> first target 64 g
+    vpg::DBuf<int32_t> lat_cell;    // [group][matrix] -> f offset of the cell (node_off), -1 none
+    vpg::DBuf<int64_t> lat_moff;    // [matrix] -> offset of its 64 x 64 block in pool_vals
+    vpg::DBuf<int32_t> other_t;     // targets of the CSR kernel
 };
 
 struct vpg_charges {
