@@ -53,12 +53,11 @@ corr_apply_kernel(int64_t nt, const int32_t* tlist, const int32_t* blk_off, cons
 // targets each) and walks the shared 64 x 64 row blocks M_q: out[64g + u] +=
 // sum_q sum_i M_q[u][i] f[cell(g, q) + i] as Y = M_q F_q (mma.sync m8n8k4),
 // M_q and the tile's f segments staged in smem (strides == 4 mod 16).
-constexpr int kLatTile = 64;
-
+template <int kLatTile>  // groups per CTA (64; 16 or 8 for small maps: more CTAs)
 __global__ void __launch_bounds__(256)
 corr_lattice_kernel(int64_t ngroups, int nmat, const int32_t* group, const int32_t* cellof,
                     const int64_t* moff, const double* pool_vals, const double* f, double* out) {
-    constexpr int K = 64, kS = K + 4;
+    constexpr int K = 64, kS = K + 4, kNT = kLatTile / 8;
     extern __shared__ __align__(16) double lsm[];
     double* ms = lsm;            // [u][i]
     double* fs = lsm + K * kS;   // [i][g]
@@ -66,27 +65,46 @@ corr_lattice_kernel(int64_t ngroups, int nmat, const int32_t* group, const int32
     const int ng = int(min(int64_t(kLatTile), ngroups - g0));
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int kq = lane & 3, rq = lane >> 2;
-    double acc[8][2];
+    double acc[kNT][2];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) acc[q][0] = acc[q][1] = 0.0;
-    for (int q = 0; q < nmat; ++q) {
-        __syncthreads();
-        const double* mg = pool_vals + moff[q];
-        for (int e = threadIdx.x; e < K * K; e += blockDim.x) ms[(e / K) * kS + (e % K)] = mg[e];
-        bool any = false;
-        for (int e = threadIdx.x; e < K * kLatTile; e += blockDim.x) {
-            const int g = e / K, i = e % K;  // coalesced over i
+    for (int q = 0; q < kNT; ++q) acc[q][0] = acc[q][1] = 0.0;
+    // register double buffer: the loads of block q+1 are in flight while
+    // the DMMAs of block q run
+    constexpr int kMR = K * K / 2 / 256, kFR = K * kLatTile / 256;
+    double2 mreg[kMR];
+    double freg[kFR];
+    auto fetch = [&](int q) {
+        const double2* mg = reinterpret_cast<const double2*>(pool_vals + moff[q]);
+#pragma unroll
+        for (int r = 0; r < kMR; ++r) mreg[r] = mg[threadIdx.x + 256 * r];
+#pragma unroll
+        for (int r = 0; r < kFR; ++r) {
+            const int e = threadIdx.x + 256 * r, g = e / K, i = e % K;
             const int c = g < ng ? cellof[(g0 + g) * nmat + q] : -1;
-            any |= c >= 0;
-            fs[i * kS + g] = c >= 0 ? f[int64_t(c) + i] : 0.0;
+            freg[r] = c >= 0 ? f[int64_t(c) + i] : 0.0;
         }
-        if (!__syncthreads_or(any)) continue;
+    };
+    if (nmat > 0) fetch(0);
+    for (int q = 0; q < nmat; ++q) {
+        __syncthreads();  // the previous block's DMMAs are done with ms / fs
+#pragma unroll
+        for (int r = 0; r < kMR; ++r) {
+            const int e = 2 * (threadIdx.x + 256 * r);
+            *reinterpret_cast<double2*>(ms + (e / K) * kS + (e % K)) = mreg[r];
+        }
+#pragma unroll
+        for (int r = 0; r < kFR; ++r) {
+            const int e = threadIdx.x + 256 * r, g = e / K, i = e % K;
+            fs[i * (kLatTile + 4) + g] = freg[r];
+        }
+        __syncthreads();
+        if (q + 1 < nmat) fetch(q + 1);
 #pragma unroll 4
         for (int k4 = 0; k4 < K; k4 += 4) {
             const double a = ms[(8 * warp + rq) * kS + k4 + kq];
 #pragma unroll
-            for (int n8 = 0; n8 < 8; ++n8) {
-                const double b = fs[(k4 + kq) * kS + 8 * n8 + rq];
+            for (int n8 = 0; n8 < kNT; ++n8) {
+                const double b = fs[(k4 + kq) * (kLatTile + 4) + 8 * n8 + rq];
                 asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                              : "+d"(acc[n8][0]), "+d"(acc[n8][1])
                              : "d"(a), "d"(b));
@@ -96,7 +114,7 @@ corr_lattice_kernel(int64_t ngroups, int nmat, const int32_t* group, const int32
     // lane holds rows u = 8 warp + rq, groups 8 n8 + 2 kq + {0, 1}
     const int u = 8 * warp + rq;
 #pragma unroll
-    for (int n8 = 0; n8 < 8; ++n8)
+    for (int n8 = 0; n8 < kNT; ++n8)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int g = 8 * n8 + 2 * kq + h;
@@ -296,7 +314,11 @@ int vpg_corr_create(int64_t nt, const int32_t* blk_off, int64_t nblocks,
             upload(c->lat_cell, cellof.data(), groups.empty() ? 0 : cellof.size());
             upload(c->lat_moff, moff.data(), groups.empty() ? 0 : moff.size());
             upload(c->other_t, other.data(), other.size());
-            if (c->nlat) smem_optin((const void*)corr_lattice_kernel, int(sizeof(double) * 64 * 68 * 2));
+            if (c->nlat) {
+                smem_optin((const void*)corr_lattice_kernel<64>, int(sizeof(double) * 64 * (68 + 68)));
+                smem_optin((const void*)corr_lattice_kernel<16>, int(sizeof(double) * 64 * (68 + 20)));
+                smem_optin((const void*)corr_lattice_kernel<8>, int(sizeof(double) * 64 * (68 + 12)));
+            }
         }
         *corr = c.release();
     });
@@ -322,9 +344,21 @@ int vpg_corr_apply(const vpg_corr* c, const double* f, int64_t nf, double* out,
                 VPG_CUDA(cudaMemcpyAsync(od, out, sizeof(double) * size_t(c->nt), cudaMemcpyHostToDevice, os.s));
         }
         if (c->nlat > 0) {
-            corr_lattice_kernel<<<nblk(c->nlat, kLatTile), 256, sizeof(double) * 64 * 68 * 2, os.s>>>(
-                c->nlat, int(c->nmat), c->lat_group.p, c->lat_cell.p, c->lat_moff.p, c->pool_vals.p, dev ? f : fd,
-                dev ? out : od);
+            int sms = 148;
+            VPG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+            if (c->nlat >= int64_t(64) * 2 * sms) {
+                corr_lattice_kernel<64><<<nblk(c->nlat, 64), 256, sizeof(double) * 64 * (68 + 68), os.s>>>(
+                    c->nlat, int(c->nmat), c->lat_group.p, c->lat_cell.p, c->lat_moff.p, c->pool_vals.p,
+                    dev ? f : fd, dev ? out : od);
+            } else if (c->nlat >= int64_t(16) * 2 * sms) {
+                corr_lattice_kernel<16><<<nblk(c->nlat, 16), 256, sizeof(double) * 64 * (68 + 20), os.s>>>(
+                    c->nlat, int(c->nmat), c->lat_group.p, c->lat_cell.p, c->lat_moff.p, c->pool_vals.p,
+                    dev ? f : fd, dev ? out : od);
+            } else {
+                corr_lattice_kernel<8><<<nblk(c->nlat, 8), 256, sizeof(double) * 64 * (68 + 12), os.s>>>(
+                    c->nlat, int(c->nmat), c->lat_group.p, c->lat_cell.p, c->lat_moff.p, c->pool_vals.p,
+                    dev ? f : fd, dev ? out : od);
+            }
             VPG_LAUNCH_CHECK();
         }
         if (c->nother) {

@@ -220,3 +220,44 @@ def test_concurrent_host_threads(vp):
             t.join()
     for a, b in zip(got, want):
         assert np.array_equal(a, b)
+
+
+def test_rademacher_charges(vp, rest):
+    """SPEC.md:520-523 invariants: Rademacher (+-1) charges on random points
+    against the long-double direct sum."""
+    rng = np.random.default_rng(77)
+    pts = rng.uniform(-1, 1, (40_000, 2))
+    q = rng.choice([-1.0, 1.0], size=40_000)
+    with vp.SummationPlan(lap(vp), pts, pts, 1e-10) as plan:
+        gpu = plan.apply(q)
+    idx = rng.choice(40_000, 1000, replace=False)
+    ld = rest.pairwise_ld(0, 0.0, pts, q, pts[idx])
+    assert rel_l2(gpu[idx], ld) <= 1e-10
+
+
+def test_runtime_ratio_50k_to_100k(vp):
+    """doubling N from 50k to 100k costs at most 2.6x (device
+    time of the apply, median of 5)."""
+    import time
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(78)
+    t = {}
+    for n in (50_000, 100_000):
+        pts = rng.uniform(-1, 1, (n, 2))
+        q = rng.standard_normal(n)
+        with vp.SummationPlan(lap(vp), pts, pts, 1e-10) as plan:
+            qd = torch.tensor(q, device="cuda")
+            od = torch.empty(n, dtype=torch.float64, device="cuda")
+            s = torch.cuda.current_stream()
+            for _ in range(3):
+                plan.apply_device(qd.data_ptr(), od.data_ptr(), s.cuda_stream)
+            ms = []
+            for _ in range(5):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                plan.apply_device(qd.data_ptr(), od.data_ptr(), s.cuda_stream)
+                e1.record()
+                torch.cuda.synchronize()
+                ms.append(e0.elapsed_time(e1))
+            t[n] = sorted(ms)[2]
+    assert t[100_000] / t[50_000] <= 2.6, t
