@@ -19,5 +19,7 @@ for w in cfg1 cfg4 cfg5; do
 done
 python bench.py --workload cfg3 --steps 5 --warmup 3 --no-cpu-baseline > $O/bench_cfg3.json 2> $O/bench_cfg3.err
 python bench.py --workload cfg3 --mode native --steps 5 --warmup 3 --no-cpu-baseline > $O/bench_cfg3_native.json 2> $O/bench_cfg3_native.err
+python bench.py --workload cfg4 --mode native --steps 5 --warmup 3 --no-cpu-baseline > $O/bench_cfg4_native.json 2> $O/bench_cfg4_native.err
+python bench.py --workload cfg5 --mode native --steps 5 --warmup 3 --no-cpu-baseline > $O/bench_cfg5_native.json 2> $O/bench_cfg5_native.err
 python bench.py --impl reference --steps 3 --warmup 3 > $O/bench_reference_cfg2.json 2> $O/bench_reference_cfg2.err
 echo done
