@@ -67,7 +67,7 @@ typedef enum { VPG_LAPLACE = 0, VPG_MODIFIED_HELMHOLTZ = 1 } vpg_family;
  * compared entry by entry.  NATIVE departs from the reference algorithm
  * where a B200-first one is faster, with parity to the requested tolerance:
  *   Laplace: an adaptive quadtree -- a box splits while it holds more than
- *     64 sources or targets, down to depth 16 -- with U/V/W/X interaction
+ *     96 sources or targets, down to depth 16 -- with U/V/W/X interaction
  *     lists (P2P, M2L, M2P, P2L), so clustered points stay O(n); the
  *     uniform-tree dumps and leaf shards are not available.
  *   Modified Helmholtz: the reference tree with a compressed Chebyshev-

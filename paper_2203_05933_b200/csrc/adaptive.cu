@@ -26,6 +26,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -35,7 +36,8 @@ namespace vpg {
 namespace {
 
 constexpr int kDepth = 16;     // 32-bit Morton keys
-constexpr int kLeafCap = 64;   // points per leaf (sources or targets)
+constexpr int kLeafCap = 96;   // points per leaf (sources or targets); VPG_LEAF_CAP overrides
+                               // (sweep: 96 best on cfg2, ties 64 on cfg3 / cfg4)
 constexpr int kL2PChainCap = 256;  // rows with more targets push their local down (L2L)
 
 inline unsigned nblk(int64_t n, int t) { return unsigned((n + t - 1) / t); }
@@ -66,7 +68,7 @@ __device__ inline int lbound(const uint32_t* k, int n, uint64_t v) {
 // One level of refinement: point ranges, split decision, non-empty children.
 __global__ void level_pass(const uint32_t* sk, int ns, const uint32_t* tk, int nt,
                            const int32_t* morton, int nbox, int level, int4* rng,
-                           int32_t* cmask, int32_t* nchild) {
+                           int32_t* cmask, int32_t* nchild, int cap) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nbox) return;
     const uint64_t m = uint32_t(morton[i]);
@@ -75,7 +77,7 @@ __global__ void level_pass(const uint32_t* sk, int ns, const uint32_t* tk, int n
     const int sb = lbound(sk, ns, lo), se = lbound(sk, ns, hi);
     const int tb = lbound(tk, nt, lo), te = lbound(tk, nt, hi);
     rng[i] = make_int4(sb, se, tb, te);
-    const bool split = level < kDepth && (level < 2 || se - sb > kLeafCap || te - tb > kLeafCap);
+    const bool split = level < kDepth && (level < 2 || se - sb > cap || te - tb > cap);
     int mask = 0, cnt = 0;
     if (split) {
         for (int c = 0; c < 4; ++c) {
@@ -298,6 +300,15 @@ void sort_by_key16(const double2* pts, int64_t n, const Plan& pl, DBuf<uint32_t>
 
 }  // namespace
 
+int leaf_cap() {
+    static const int cap = [] {
+        const char* v = std::getenv("VPG_LEAF_CAP");
+        const int c = v ? std::atoi(v) : 0;
+        return c > 0 ? c : kLeafCap;
+    }();
+    return cap;
+}
+
 void build_adaptive(Plan& pl, cudaStream_t st) {
     pl.adaptive = true;
     pl.multilevel_up = pl.multilevel_down = false;  // hybrid passes (schedules below)
@@ -322,7 +333,7 @@ void build_adaptive(Plan& pl, cudaStream_t st) {
         nchild.alloc(size_t(ncur));
         cpos.alloc(size_t(ncur));
         level_pass<<<nblk(ncur, 128), 128, 0, st>>>(sk.p, int(pl.ns), tk.p, int(pl.nt), cur.p, int(ncur),
-                                                     level, rng.p, cmask.p, nchild.p);
+                                                     level, rng.p, cmask.p, nchild.p, leaf_cap());
         VPG_LAUNCH_CHECK();
         exclusive_scan(nchild.p, cpos.p, ncur, st);
         const std::vector<int32_t> m = d2h(cur.p, size_t(ncur), st);
