@@ -122,9 +122,12 @@ __global__ void __launch_bounds__(kTravWarps * 32)
 traverse_kernel(HelmParams hp, const int32_t* src_cnt, const int32_t* soff,
                 const double2* sxy, const double* q, const double2* txy,
                 const int32_t* tids, int64_t nt, const double* nodes_all,
-                const double* W, const double* k0tab, double* out) {
+                const double* W, const double* k0f, double* out) {
     __shared__ uint64_t st_ent[kTravWarps][kTravStack];
     __shared__ uint32_t st_mask[kTravWarps][kTravStack];
+    __shared__ double k0tab[kK0FastIntervals * kK0FastStride];
+    for (int i = threadIdx.x; i < kK0FastIntervals * kK0FastStride; i += blockDim.x) k0tab[i] = k0f[i];
+    __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t i0 = (int64_t(blockIdx.x) * kTravWarps + warp) * 32;
     if (i0 >= nt) return;
@@ -178,7 +181,7 @@ traverse_kernel(HelmParams hp, const int32_t* src_cnt, const int32_t* soff,
                 for (int bb = 0; bb < m; ++bb) {
                     const double ey = t.y - (cy + h * nd[bb]);
                     const double r = sqrt(fma(ey, ey, ex2));
-                    acc = fma(wb[a * m + bb], kInv2Pi * k0_dev(lambda * r, k0tab), acc);
+                    acc = fma(wb[a * m + bb], kInv2Pi * k0_fast(lambda * r, k0tab), acc);
                 }
             }
             if (on) pot = acc;
@@ -188,7 +191,9 @@ traverse_kernel(HelmParams hp, const int32_t* src_cnt, const int32_t* soff,
             double acc = pot;
             for (int f = soff[id]; f < soff[id + 1]; ++f) {
                 const double2 sp = sxy[f];
-                acc = fma(kInv2Pi, k0_pair(t.x, t.y, sp.x, sp.y, q[f], lambda, k0tab), acc);
+                const double dx = t.x - sp.x, dy = t.y - sp.y;
+                const double r2 = fma(dy, dy, dx * dx);  // r^2 == 0 skipped (summation.cpp:486)
+                acc = fma(kInv2Pi, r2 == 0.0 ? 0.0 : q[f] * k0_fast(lambda * sqrt(r2), k0tab), acc);
             }
             if (on) pot = acc;
         }
@@ -723,7 +728,7 @@ void helm_apply(const Plan& pl, const double* q_dev, double* out_dev,
     if (pl.nt > 0) {
         traverse_kernel<<<nblk(pl.nt, kTravWarps * 32), kTravWarps * 32, 0, st>>>(
             hp, pl.src_cnt.p, pl.src_off.p, pl.src_sorted.p, qs, pl.tgt_sorted.p,
-            pl.tgt_ids.p, pl.nt, pl.helm_nodes.p, W, k0_table_dev(), out_dev);
+            pl.tgt_ids.p, pl.nt, pl.helm_nodes.p, W, k0_fast_table_dev(), out_dev);
         VPG_LAUNCH_CHECK();
         ++launches;
     }

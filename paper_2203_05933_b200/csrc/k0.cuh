@@ -122,4 +122,49 @@ __device__ __forceinline__ double k0_pair(double tx, double ty, double sx,
 // Host: builds the Chebyshev table (kK0Intervals x kK0Coeffs doubles).
 void k0_fit_host(double* out);
 
+// ---- fast K0 for the treecode's proxy loop (same accuracy, fewer ops) ----
+// x > 2: quarter-octave intervals with 14-term Chebyshev fits (the nearest
+// singularity of g at 0 is >= 11 half-widths away: rho^-14 < 1e-18); the
+// interval comes from the exponent and two mantissa compares, the map onto
+// [-1, 1] is one FMA.  x <= 2: the series truncated at q^12 (tail < 1e-19).
+constexpr int kK0FastIntervals = 36;  // [2, 1024]
+constexpr int kK0FastCoeffs = 14;
+constexpr int kK0FastStride = 16;     // 14 coefficients + (a, b)
+void k0_fit_fast_host(double* out);
+
+__device__ __forceinline__ double k0_small12(double x) {
+    const double q = 0.25 * x * x;
+    double i0 = c_k0_i0[12], s = c_k0_h[12];
+#pragma unroll
+    for (int k = 11; k >= 0; --k) {
+        i0 = fma(i0, q, c_k0_i0[k]);
+        s = fma(s, q, c_k0_h[k]);
+    }
+    constexpr double kGamma = 0.57721566490153286061;
+    return -(log(0.5 * x) + kGamma) * i0 + s;
+}
+
+// tab: kK0FastIntervals x kK0FastStride doubles (shared memory)
+__device__ __forceinline__ double k0_fast(double x, const double* tab) {
+    if (x <= 2.0) return k0_small12(x);
+    if (x > 745.0) return 0.0;  // exp(-x) underflows (kernel.cpp:158-161)
+    const int hi = __double2hiint(x);
+    const int e = (hi >> 20) - 1023;                       // x = 2^e m, e >= 1
+    const double m = __hiloint2double((hi & 0x000FFFFF) | 0x3FF00000, __double2loint(x));
+    int iv = 4 * (e - 1) + (m >= 1.189207115002721) + (m >= 1.4142135623730951) + (m >= 1.6817928305074290);
+    iv = min(iv, kK0FastIntervals - 1);
+    const double* c = tab + iv * kK0FastStride;
+    const double u = fma(x, c[kK0FastCoeffs], c[kK0FastCoeffs + 1]);
+    const double u2 = 2.0 * u;
+    double b1 = 0.0, b2 = 0.0;
+#pragma unroll
+    for (int k = kK0FastCoeffs - 1; k >= 1; --k) {
+        const double b0 = fma(u2, b1, c[k] - b2);
+        b2 = b1;
+        b1 = b0;
+    }
+    const double g = fma(u, b1, 0.5 * c[0] - b2);
+    return g * exp(-x) * rsqrt(x);
+}
+
 }  // namespace vpg

@@ -79,4 +79,31 @@ void k0_fit_host(double* out) {
     }
 }
 
+// Quarter-octave fit for the treecode's hot loop (k0_fast, k0.cuh):
+// intervals [2 * 2^(i/4), 2 * 2^((i+1)/4)], i = 0..kK0FastIntervals-1, each
+// with kK0FastCoeffs Chebyshev coefficients of g(x) = K0(x) e^x sqrt(x)
+// plus the map u = x * a + b onto [-1, 1]; record stride kK0FastStride.
+void k0_fit_fast_host(double* out) {
+    const GL g(20);
+    const long double pi = 3.141592653589793238462643383279502884L;
+    const int N = kK0FastCoeffs;
+    for (int iv = 0; iv < kK0FastIntervals; ++iv) {
+        const long double lo = 2.0L * std::pow(2.0L, iv / 4.0L), hi = 2.0L * std::pow(2.0L, (iv + 1) / 4.0L);
+        long double f[kK0FastCoeffs];
+        for (int j = 0; j < N; ++j) {
+            const long double th = pi * (j + 0.5L) / N;
+            const long double xj = 0.5L * (lo + hi) + 0.5L * (hi - lo) * std::cos(th);
+            f[j] = scaled_k0(xj, g) * std::sqrt(xj);
+        }
+        double* rec = out + iv * kK0FastStride;
+        for (int k = 0; k < N; ++k) {
+            long double s = 0;
+            for (int j = 0; j < N; ++j) s += f[j] * std::cos(k * pi * (j + 0.5L) / N);
+            rec[k] = double(2 * s / N);
+        }
+        rec[N] = double(2.0L / (hi - lo));
+        rec[N + 1] = double(-(hi + lo) / (hi - lo));
+    }
+}
+
 }  // namespace vpg
