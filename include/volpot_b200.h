@@ -145,13 +145,17 @@ int vpg_plan_dump_m2l(const vpg_plan* plan, int level, int32_t* ntbox,
                       int64_t* nent, int32_t* tbox, int32_t* toff,
                       int32_t* src, int32_t* oidx);
 /* Multi-GPU target sharding (one process per GPU): restricts
- * the target side of later applies (M2L, L2L, L2P+P2P) to the target leaves
- * of Morton range [leaf_begin, leaf_end); the upward pass stays complete.
- * Outputs of targets outside the range are written as 0.0, so summing the
- * shards' outputs (one all-reduce) reproduces the unsharded plan bit for
- * bit.  Not to be called concurrently with apply.  [0, 4^levels) restores
- * the full plan. */
-int vpg_plan_set_shard(vpg_plan* plan, int64_t leaf_begin, int64_t leaf_end);
+ * the target side of later applies (M2L, L2L, L2P+P2P, and M2P / P2L on
+ * adaptive trees) to the shard units [unit_begin, unit_end); the upward pass
+ * stays complete.  Units are the 4^levels Morton leaves of a reference-mode
+ * tree, or the leaves holding targets (in target order) of an adaptive tree;
+ * vpg_plan_shard_units gives their count and a work estimate per unit for
+ * balancing.  Outputs of targets outside the shard are written as 0.0, so
+ * summing the shards' outputs (one all-reduce) reproduces the unsharded plan
+ * bit for bit.  Not to be called concurrently with apply.  [0, nunits)
+ * restores the full plan.  Modified-Helmholtz plans cannot be sharded. */
+int vpg_plan_set_shard(vpg_plan* plan, int64_t unit_begin, int64_t unit_end);
+int vpg_plan_shard_units(const vpg_plan* plan, int64_t* nunits, double* costs /* [nunits] or NULL */);
 int vpg_plan_destroy(vpg_plan* plan);
 
 /* direct_sum (summation.cpp:501-540).  skip_coincident = 0: reference

@@ -95,6 +95,7 @@ _SIGS = {
     "vpg_plan_dump_tree": (C.c_int, [_P, _P, _P, _P, _P, _P, _P]),
     "vpg_plan_dump_m2l": (C.c_int, [_P, C.c_int, _I32, _I64, _P, _P, _P, _P]),
     "vpg_plan_set_shard": (C.c_int, [_P, C.c_int64, C.c_int64]),
+    "vpg_plan_shard_units": (C.c_int, [_P, _I64, _P]),
     "vpg_plan_destroy": (C.c_int, [_P]),
     "vpg_direct_sum": (C.c_int, [C.c_int, C.c_double, _P, _P, C.c_int64, _P, C.c_int64, _P,
                                  C.c_int, _I64, _I64, C.c_int, C.c_uint, _P]),

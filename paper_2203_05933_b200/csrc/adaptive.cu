@@ -449,6 +449,9 @@ void build_adaptive(Plan& pl, cudaStream_t st) {
         std::swap(pl.m2l_oidx.p, voidx.p);
         pl.n_m2l_batches = int64_t(batches.size());
         h2d(pl.m2l_batches, batches, st);
+        pl.ad_vc = vc;
+        pl.ad_vp = vp;
+        pl.ad_nv = nv;
     }
 
     // ---- U / W / X pairs, sorted by (kind, owner, partner)
@@ -567,6 +570,12 @@ void build_adaptive(Plan& pl, cudaStream_t st) {
         h2d(pl.updown_boxes, boxes, st);
         h2d(pl.updown_kids, kids, st);
         h2d(pl.row_chain, chain, st);
+        pl.ad_ud_boxes = boxes;
+        pl.ad_ud_kids = kids;
+        pl.ad_m2m_first = pl.m2m_first;
+        pl.ad_m2m_count = pl.m2m_count;
+        pl.ad_l2l_first = pl.l2l_first;
+        pl.ad_l2l_count = pl.l2l_count;
         pl.n_p2m_items = int64_t(items.size());
         pl.n_p2m_splits = int64_t(splits.size());
         h2d(pl.p2m_items, items, st);
@@ -627,6 +636,7 @@ void build_adaptive(Plan& pl, cudaStream_t st) {
             throw Error{VPG_ERR_INVALID_ARGUMENT,
                         "adaptive tree: a leaf has " + std::to_string(max_ranges) + " near leaves (max " +
                             std::to_string(kMaxNearRanges - 1) + ")"};
+        pl.ad_chunks = chunks;
         schedule_near_chunks(pl, chunks);
         h2d(pl.p2p_chunks, chunks, st);
         h2d(pl.near_ranges, ranges, st);
@@ -650,6 +660,7 @@ void build_adaptive(Plan& pl, cudaStream_t st) {
         pl.m2p_evals = nw;
         pl.n_m2p_work = int64_t(work.size());
         h2d(pl.m2p_work, work, st);
+        pl.ad_m2p = work;
         h2d(pl.m2p_rows, wrows, st);
     }
     {
@@ -671,12 +682,142 @@ void build_adaptive(Plan& pl, cudaStream_t st) {
         pl.p2l_sources = np2l;
         pl.n_p2l_work = int64_t(work.size());
         h2d(pl.p2l_work, work, st);
+        pl.ad_p2l = work;
         h2d(pl.p2l_ranges, ranges, st);
     }
+    pl.ad_rng = h_rng;
+    pl.ad_level = h_level;
+    // shard units: leaves with targets, in target (Morton) order
+    pl.ad_leaves.clear();
+    for (int64_t r = 0; r < nrows; ++r)
+        if (h_first[size_t(r)] < 0 && h_rng[size_t(r)].w > h_rng[size_t(r)].z) pl.ad_leaves.push_back(int32_t(r));
+    std::sort(pl.ad_leaves.begin(), pl.ad_leaves.end(),
+              [&](int32_t a, int32_t b) { return h_rng[size_t(a)].z < h_rng[size_t(b)].z; });
     pl.shard_lb = 0;
-    pl.shard_le = 0;
+    pl.shard_le = int64_t(pl.ad_leaves.size());
     pl.shard_t0 = 0;
     pl.shard_t1 = pl.nt;
+}
+
+// Restricts the target side of an adaptive plan to the targets of the
+// leaves [leaf_begin, leaf_end) of ad_leaves (a contiguous sorted-target
+// range): near-field chunks and L2P chains, M2P work of those targets, M2L /
+// P2L / L2L of every box whose target range meets it.  The upward pass stays
+// whole.  The per-target arithmetic is unchanged, so the shards' outputs
+// (0.0 elsewhere) sum to the single-plan result bit for bit.
+void adaptive_set_targets(Plan& pl, int64_t leaf_begin, int64_t leaf_end) {
+    cudaStream_t st = 0;
+    const int64_t nl = int64_t(pl.ad_leaves.size());
+    int32_t T0 = 0, T1 = 0;
+    if (leaf_begin < leaf_end) {
+        T0 = pl.ad_rng[size_t(pl.ad_leaves[size_t(leaf_begin)])].z;
+        T1 = pl.ad_rng[size_t(pl.ad_leaves[size_t(leaf_end - 1)])].w;
+    }
+    if (leaf_begin == 0 && leaf_end == nl) {
+        T0 = 0;
+        T1 = int32_t(pl.nt);
+    }
+    auto meets = [&](int64_t r) {
+        const int4 g = pl.ad_rng[size_t(r)];
+        return g.w > g.z && g.z < T1 && g.w > T0;
+    };
+    // near field + L2P
+    {
+        std::vector<P2PChunk> chunks;
+        pl.p2p_pairs = 0;
+        for (const P2PChunk& c : pl.ad_chunks)
+            if (c.tbegin >= T0 && c.tbegin < T1) {
+                chunks.push_back(c);
+                pl.p2p_pairs += int64_t(c.pad) * c.tcount;
+            }
+        schedule_near_chunks(pl, chunks);
+        h2d(pl.p2p_chunks, chunks, st);
+    }
+    // M2L target boxes and batches (same packing rule as build_adaptive)
+    {
+        std::vector<int32_t> tbox, toff;
+        std::vector<M2LBatch> batches;
+        M2LBatch curb{};
+        bool open = false;
+        int64_t nent = 0;
+        const int64_t nrows = int64_t(pl.ad_rng.size());
+        for (int64_t r = 0; r < nrows; ++r) {
+            const int l = pl.ad_level[size_t(r)];
+            if (l < 2 || !meets(r)) continue;
+            const int32_t ne = pl.ad_vc[size_t(r)];
+            if (open && (l != curb.level || curb.ecount + ne > kM2LPairs)) {
+                batches.push_back(curb);
+                open = false;
+            }
+            if (!open) {
+                curb = M2LBatch{l, int32_t(tbox.size()), 0, int32_t(pl.ad_vp[size_t(r)]), 0};
+                open = true;
+            }
+            // a batch's entries must be contiguous: close it when this box's
+            // entries do not follow the previous box's
+            if (curb.tcount > 0 && int64_t(curb.efirst) + curb.ecount != pl.ad_vp[size_t(r)]) {
+                batches.push_back(curb);
+                curb = M2LBatch{l, int32_t(tbox.size()), 0, int32_t(pl.ad_vp[size_t(r)]), 0};
+            }
+            tbox.push_back(int32_t(r));
+            toff.push_back(int32_t(pl.ad_vp[size_t(r)]));
+            curb.tcount += 1;
+            curb.ecount += ne;
+            nent += ne;
+        }
+        if (open) batches.push_back(curb);
+        // toff: CSR over the kept boxes (entry positions are the global ones)
+        toff.push_back(tbox.empty() ? 0 : int32_t(pl.ad_vp[size_t(tbox.back())] + pl.ad_vc[size_t(tbox.back())]));
+        pl.n_tbox = int64_t(tbox.size());
+        pl.shard_m2l = nent;
+        h2d(pl.m2l_tbox, tbox, st);
+        h2d(pl.m2l_toff, toff, st);
+        pl.n_m2l_batches = int64_t(batches.size());
+        h2d(pl.m2l_batches, batches, st);
+    }
+    // L2L parents meeting the range (the M2M part is unchanged)
+    {
+        std::vector<int32_t> boxes;
+        std::vector<int4> kids;
+        const int L = pl.L;
+        for (int l = 2; l < L; ++l) {
+            pl.m2m_first[size_t(l)] = int64_t(boxes.size());
+            const int64_t f = pl.ad_m2m_first[size_t(l)];
+            for (int64_t i = f; i < f + pl.ad_m2m_count[size_t(l)]; ++i) {
+                boxes.push_back(pl.ad_ud_boxes[size_t(i)]);
+                kids.push_back(pl.ad_ud_kids[size_t(i)]);
+            }
+            pl.m2m_count[size_t(l)] = int64_t(boxes.size()) - pl.m2m_first[size_t(l)];
+        }
+        for (int l = 2; l < L; ++l) {
+            pl.l2l_first[size_t(l)] = int64_t(boxes.size());
+            const int64_t f = pl.ad_l2l_first[size_t(l)];
+            for (int64_t i = f; i < f + pl.ad_l2l_count[size_t(l)]; ++i)
+                if (meets(pl.ad_ud_boxes[size_t(i)])) {
+                    boxes.push_back(pl.ad_ud_boxes[size_t(i)]);
+                    kids.push_back(pl.ad_ud_kids[size_t(i)]);
+                }
+            pl.l2l_count[size_t(l)] = int64_t(boxes.size()) - pl.l2l_first[size_t(l)];
+        }
+        h2d(pl.updown_boxes, boxes, st);
+        h2d(pl.updown_kids, kids, st);
+    }
+    // M2P and P2L
+    {
+        std::vector<int4> m2p, p2l;
+        for (const int4& w : pl.ad_m2p)
+            if (w.x >= T0 && w.x < T1) m2p.push_back(w);
+        for (const int4& w : pl.ad_p2l)
+            if (meets(w.x)) p2l.push_back(w);
+        pl.n_m2p_work = int64_t(m2p.size());
+        pl.n_p2l_work = int64_t(p2l.size());
+        h2d(pl.m2p_work, m2p, st);
+        h2d(pl.p2l_work, p2l, st);
+    }
+    pl.shard_lb = leaf_begin;
+    pl.shard_le = leaf_end;
+    pl.shard_t0 = T0;
+    pl.shard_t1 = T1;
 }
 
 }  // namespace vpg

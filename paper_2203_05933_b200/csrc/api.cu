@@ -189,6 +189,11 @@ struct Scratch {  // stream-ordered device scratch
 // per plan, least recently used evicted.  Caller holds pl.graph_mu.
 constexpr size_t kMaxGraphs = 8;
 
+bool plan_is_sharded(const Plan& pl) {
+    if (pl.adaptive) return pl.shard_t0 != 0 || pl.shard_t1 != pl.nt;
+    return pl.shard_lb != 0 || pl.shard_le != (int64_t(1) << (2 * pl.L));
+}
+
 GraphEntry* graph_entry(const Plan& pl, const double* q, double* out, bool host) {
     for (auto& e : pl.graphs)
         if (e->host == host && e->q == q && e->out == out) return e.get();
@@ -228,7 +233,7 @@ GraphEntry* graph_entry(const Plan& pl, const double* q, double* out, bool host)
     VPG_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
     cudaGraph_t g = nullptr;
     try {
-        if (!pl.adaptive && (pl.shard_lb != 0 || pl.shard_le != (int64_t(1) << (2 * pl.L))) && pl.nt)
+        if (plan_is_sharded(pl) && pl.nt)
             VPG_CUDA(cudaMemsetAsync(od, 0, sizeof(double) * size_t(pl.nt), cap));
         static const bool no_fork = [] {
             const char* v = std::getenv("VPG_NO_FORK");
@@ -391,7 +396,7 @@ int vpg_plan_apply(const vpg_plan* plan, const double* q, int64_t nq, double* ou
             VPG_CUDA(cudaMemcpyAsync(qd.p, q, sizeof(double) * size_t(pl.ns), cudaMemcpyHostToDevice, st));
         int64_t launches = 0;
         cudaEvent_t* inner = prof ? ev + 1 : nullptr;  // GATHER .. DOWNLOAD
-        if (!pl.direct && !pl.adaptive && (pl.shard_lb != 0 || pl.shard_le != (int64_t(1) << (2 * pl.L))) && pl.nt)
+        if (!pl.direct && plan_is_sharded(pl) && pl.nt)
             VPG_CUDA(cudaMemsetAsync(out_dev, 0, sizeof(double) * size_t(pl.nt), st));
         if (pl.direct) {
             if (prof)
@@ -529,9 +534,9 @@ int vpg_plan_set_shard(vpg_plan* plan, int64_t leaf_begin, int64_t leaf_end) {
         if (!plan) throw Error{VPG_ERR_INVALID_ARGUMENT, "plan is NULL"};
         Plan& pl = plan->impl;
         if (pl.direct) throw Error{VPG_ERR_INVALID_ARGUMENT, "pairwise plan cannot be sharded"};
-        if (pl.adaptive)
-            throw Error{VPG_ERR_INVALID_ARGUMENT, "adaptive (native) plan cannot be leaf-sharded"};
-        const int64_t nleaf = int64_t(1) << (2 * pl.L);
+        if (pl.family != VPG_LAPLACE)
+            throw Error{VPG_ERR_INVALID_ARGUMENT, "modified-Helmholtz plans cannot be sharded"};
+        const int64_t nleaf = pl.adaptive ? int64_t(pl.ad_leaves.size()) : int64_t(1) << (2 * pl.L);
         if (leaf_begin < 0 || leaf_end > nleaf || leaf_begin > leaf_end)
             throw Error{VPG_ERR_INVALID_ARGUMENT, "shard leaf range out of bounds"};
         VPG_CUDA(cudaSetDevice(pl.device));
@@ -539,7 +544,53 @@ int vpg_plan_set_shard(vpg_plan* plan, int64_t leaf_begin, int64_t leaf_end) {
             std::lock_guard<std::mutex> lk(pl.graph_mu);
             pl.graphs.clear();  // captured schedules are stale
         }
-        build_schedules(pl, leaf_begin, leaf_end);
+        if (pl.adaptive) adaptive_set_targets(pl, leaf_begin, leaf_end);
+        else build_schedules(pl, leaf_begin, leaf_end);
+    });
+}
+
+int vpg_plan_shard_units(const vpg_plan* plan, int64_t* nunits, double* costs) {
+    return guarded([&] {
+        if (!plan || !nunits) throw Error{VPG_ERR_INVALID_ARGUMENT, "NULL argument"};
+        const Plan& pl = plan->impl;
+        if (pl.direct) throw Error{VPG_ERR_INVALID_ARGUMENT, "pairwise plan cannot be sharded"};
+        if (pl.family != VPG_LAPLACE)
+            throw Error{VPG_ERR_INVALID_ARGUMENT, "modified-Helmholtz plans cannot be sharded"};
+        const double P = pl.P;
+        if (pl.adaptive) {
+            *nunits = int64_t(pl.ad_leaves.size());
+            if (!costs) return;
+            std::map<int32_t, size_t> at;  // target begin -> leaf position
+            for (size_t i = 0; i < pl.ad_leaves.size(); ++i) {
+                at[pl.ad_rng[size_t(pl.ad_leaves[i])].z] = i;
+                costs[i] = 0.0;
+            }
+            for (const P2PChunk& c : pl.ad_chunks) {
+                auto it = at.upper_bound(c.tbegin);
+                const size_t i = std::prev(it)->second;
+                // near field + local evaluation of the chain + ~27 M2L entries
+                costs[i] += double(c.tcount) * (double(c.pad) * 14.0 + 4.0 * (P + 1) * c.lcount) +
+                            (c.tbegin == pl.ad_rng[size_t(pl.ad_leaves[i])].z ? 27.0 * 4.0 * P * (P + 1) : 0.0);
+            }
+            return;
+        }
+        const int L = pl.L;
+        const int64_t nleaf = int64_t(1) << (2 * L);
+        *nunits = nleaf;
+        if (!costs) return;
+        const int nb = 1 << L;
+        for (int64_t b = 0; b < nleaf; ++b) {
+            const int64_t ntgt = pl.h_toff[size_t(b) + 1] - pl.h_toff[size_t(b)];
+            const int ix = int(squash2(uint32_t(b))), iy = int(squash2(uint32_t(b) >> 1));
+            int64_t nsrc = 0;
+            for (int jy = std::max(0, iy - 1); jy <= std::min(nb - 1, iy + 1); ++jy)
+                for (int jx = std::max(0, ix - 1); jx <= std::min(nb - 1, ix + 1); ++jx) {
+                    const uint32_t sid = mort(uint32_t(jx), uint32_t(jy));
+                    nsrc += pl.h_soff[sid + 1] - pl.h_soff[sid];
+                }
+            costs[b] = double(ntgt) * double(nsrc) * 14.0 + double(ntgt) * 4.0 * (P + 1) +
+                       (ntgt > 0 ? 27.0 * 4.0 * P * (P + 1) : 0.0);
+        }
     });
 }
 

@@ -618,7 +618,10 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
             if (l <= P)
                 for (int t = rtid >> 6; t < bt.tcount; t += kWSRedThreads >> 6) {
                     const int64_t tg = int64_t(bt.tfirst) + t;
-                    const int p0 = toff[tg] - bt.efirst, p1 = toff[tg + 1] - bt.efirst;
+                    // the batch's entries are contiguous; its last box ends at the
+                    // batch end (toff[tg + 1] may start a non-adjacent box: shards)
+                    const int p0 = toff[tg] - bt.efirst;
+                    const int p1 = t + 1 < bt.tcount ? toff[tg + 1] - bt.efirst : bt.ecount;
                     const double* yrow = yb + l * kM2LXS;
                     double sr = 0.0, si = 0.0, qsum = 0.0;
 #pragma unroll 4

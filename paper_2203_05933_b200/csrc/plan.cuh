@@ -187,6 +187,18 @@ struct Plan {
     DBuf<int32_t> m2p_rows;
     int64_t n_m2p_work = 0, m2p_evals = 0;
     DBuf<int4> p2l_work;    // (receiving row, first range, range count, 0)
+    // adaptive shards (vpg_plan_set_shard): host copies of the full
+    // target-side schedules, filtered per target range
+    std::vector<int4> ad_rng;             // per row (src begin, end, tgt begin, end)
+    std::vector<int32_t> ad_level, ad_vc;
+    std::vector<int64_t> ad_vp;
+    int64_t ad_nv = 0;
+    std::vector<P2PChunk> ad_chunks;      // unsplit near-field chunks
+    std::vector<int4> ad_m2p, ad_p2l;     // full M2P / P2L work
+    std::vector<int32_t> ad_ud_boxes;     // M2M parents, then L2L parents (rows)
+    std::vector<int4> ad_ud_kids;
+    std::vector<int64_t> ad_m2m_first, ad_m2m_count, ad_l2l_first, ad_l2l_count;
+    std::vector<int32_t> ad_leaves;       // leaves with targets, in target order (shard units)
     DBuf<int2> p2l_ranges;  // X-leaf source ranges
     int64_t n_p2l_work = 0, p2l_sources = 0;
     std::vector<int64_t> m2m_first, m2m_count;  // into updown_boxes, per level
@@ -261,6 +273,7 @@ void schedule_near_chunks(Plan& pl, std::vector<P2PChunk>& chunks);
 void choose_passes(Plan& pl);
 // adaptive.cu
 void build_adaptive(Plan& pl, cudaStream_t st);
+void adaptive_set_targets(Plan& pl, int64_t leaf_begin, int64_t leaf_end);  // shard
 // fmm.cu
 void build_laplace_ops(Plan& pl);
 struct LaplaceWork {

@@ -77,7 +77,16 @@ def balanced_ranges(costs, world):
 
 
 def shard_plan(plan, rank, world):
-    """Restricts ``plan`` to this rank's balanced leaf range; returns the range."""
+    """Restricts ``plan`` to this rank's balanced unit range; returns the range.
+
+    Reference-mode (uniform) trees are balanced with ``leaf_costs`` from the
+    dumped tree; adaptive (native-mode) trees with the library's per-unit
+    estimates (vpg_plan_shard_units: their units are the target leaves)."""
+    if plan.info()["mode"] == 1 and plan.info()["family"] == 0:
+        costs = plan.shard_units()
+        lo, hi = balanced_ranges(costs, world)[rank]
+        plan.set_shard(lo, hi)
+        return lo, hi
     t = plan.dump_tree()
     costs = leaf_costs(t["src_off"], t["tgt_off"], plan.levels(), plan.expansion_order())
     lo, hi = balanced_ranges(costs, world)[rank]

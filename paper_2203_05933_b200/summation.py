@@ -202,8 +202,18 @@ class SummationPlan:
         L.check(L.lib().vpg_plan_apply(self._h, q_ptr, self._info.num_sources, out_ptr, flags,
                                        stream or None), "SummationPlan::apply")
 
+    def shard_units(self) -> np.ndarray:
+        """Work estimate per shard unit (Morton leaves, or the target leaves
+        of an adaptive tree) for balancing set_shard ranges."""
+        n = C.c_int64(0)
+        L.check(L.lib().vpg_plan_shard_units(self._h, C.byref(n), None), "shard_units")
+        costs = np.empty(n.value)
+        L.check(L.lib().vpg_plan_shard_units(self._h, C.byref(n), costs.ctypes.data_as(C.c_void_p)),
+                "shard_units")
+        return costs
+
     def set_shard(self, leaf_begin: int, leaf_end: int) -> None:
-        """Restrict the target side to Morton leaves [leaf_begin, leaf_end)."""
+        """Restrict the target side to shard units [leaf_begin, leaf_end)."""
         L.check(L.lib().vpg_plan_set_shard(self._h, int(leaf_begin), int(leaf_end)), "set_shard")
         self._info = self._read_info()
 

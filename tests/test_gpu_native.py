@@ -132,6 +132,41 @@ def test_native_rejects_uniform_only_queries(vp):
     src = rng.uniform(-1, 1, (20_000, 2))
     with vp.SummationPlan(lap(vp), src, src, 1e-12, mode="native") as plan:
         with pytest.raises(vp.InvalidArgument):
-            plan.set_shard(0, 1)
-        with pytest.raises(vp.InvalidArgument):
             plan.dump_m2l(2)
+        with pytest.raises(vp.InvalidArgument):
+            plan.set_shard(0, plan.shard_units().size + 1)
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_native_target_shards_assemble_bit_exact(vp, world):
+    """Adaptive plans shard by target leaves (in target order): every target
+    is owned by exactly one shard and the sum of the shards' outputs is the
+    single-plan result bit for bit (W/X lists included)."""
+    from paper_2203_05933_b200 import multigpu
+    rng = np.random.default_rng(38)
+    src = clusters(rng, 90_000, [(0.3, 0.2), (-0.5, -0.4)], [2e-3, 3e-2])
+    tgt = clusters(rng, 70_000, [(0.3, 0.2), (-0.1, 0.5)], [5e-3, 1e-1])
+    q = rng.standard_normal(len(src))
+    with vp.SummationPlan(lap(vp), src, tgt, 1e-12, mode="native") as plan:
+        full = plan.apply(q)
+        nunits = plan.shard_units().size
+        total = np.zeros_like(full)
+        owners = np.zeros(len(tgt), np.int64)
+        for r in range(world):
+            multigpu.shard_plan(plan, r, world)
+            part = plan.apply(q)
+            owners += part != 0.0
+            total += part
+        plan.set_shard(0, nunits)
+        again = plan.apply(q)
+    assert np.all(owners == 1)
+    assert np.array_equal(total, full)
+    assert np.array_equal(again, full)
+
+
+def test_helmholtz_plans_refuse_shards(vp):
+    rng = np.random.default_rng(39)
+    src = rng.uniform(-1, 1, (20_000, 2))
+    with vp.SummationPlan(vp.make_kernel(vp.KernelFamily.ModifiedHelmholtz, 10.0), src, src, 1e-12) as plan:
+        with pytest.raises(vp.InvalidArgument, match="cannot be sharded"):
+            plan.set_shard(0, 1)
