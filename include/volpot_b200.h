@@ -153,7 +153,8 @@ int vpg_plan_dump_m2l(const vpg_plan* plan, int level, int32_t* ntbox,
  * balancing.  Outputs of targets outside the shard are written as 0.0, so
  * summing the shards' outputs (one all-reduce) reproduces the unsharded plan
  * bit for bit.  Not to be called concurrently with apply.  [0, nunits)
- * restores the full plan.  Modified-Helmholtz plans cannot be sharded. */
+ * restores the full plan.  Modified-Helmholtz plans shard their target side
+ * too (treecode: the traversal; Chebyshev FMM: L2P and near field). */
 int vpg_plan_set_shard(vpg_plan* plan, int64_t unit_begin, int64_t unit_end);
 int vpg_plan_shard_units(const vpg_plan* plan, int64_t* nunits, double* costs /* [nunits] or NULL */);
 int vpg_plan_destroy(vpg_plan* plan);

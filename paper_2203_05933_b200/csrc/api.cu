@@ -534,8 +534,6 @@ int vpg_plan_set_shard(vpg_plan* plan, int64_t leaf_begin, int64_t leaf_end) {
         if (!plan) throw Error{VPG_ERR_INVALID_ARGUMENT, "plan is NULL"};
         Plan& pl = plan->impl;
         if (pl.direct) throw Error{VPG_ERR_INVALID_ARGUMENT, "pairwise plan cannot be sharded"};
-        if (pl.family != VPG_LAPLACE)
-            throw Error{VPG_ERR_INVALID_ARGUMENT, "modified-Helmholtz plans cannot be sharded"};
         const int64_t nleaf = pl.adaptive ? int64_t(pl.ad_leaves.size()) : int64_t(1) << (2 * pl.L);
         if (leaf_begin < 0 || leaf_end > nleaf || leaf_begin > leaf_end)
             throw Error{VPG_ERR_INVALID_ARGUMENT, "shard leaf range out of bounds"};
@@ -554,8 +552,6 @@ int vpg_plan_shard_units(const vpg_plan* plan, int64_t* nunits, double* costs) {
         if (!plan || !nunits) throw Error{VPG_ERR_INVALID_ARGUMENT, "NULL argument"};
         const Plan& pl = plan->impl;
         if (pl.direct) throw Error{VPG_ERR_INVALID_ARGUMENT, "pairwise plan cannot be sharded"};
-        if (pl.family != VPG_LAPLACE)
-            throw Error{VPG_ERR_INVALID_ARGUMENT, "modified-Helmholtz plans cannot be sharded"};
         const double P = pl.P;
         if (pl.adaptive) {
             *nunits = int64_t(pl.ad_leaves.size());

@@ -726,9 +726,12 @@ void helm_apply(const Plan& pl, const double* q_dev, double* out_dev,
     mark(4);
     mark(5);
     if (pl.nt > 0) {
-        traverse_kernel<<<nblk(pl.nt, kTravWarps * 32), kTravWarps * 32, 0, st>>>(
-            hp, pl.src_cnt.p, pl.src_off.p, pl.src_sorted.p, qs, pl.tgt_sorted.p,
-            pl.tgt_ids.p, pl.nt, pl.helm_nodes.p, W, k0_fast_table_dev(), out_dev);
+        // targets are independent: a shard traverses its sorted-target range only
+        const int64_t t0 = pl.shard_t0, nts = pl.shard_t1 - pl.shard_t0;
+        if (nts > 0)
+            traverse_kernel<<<nblk(nts, kTravWarps * 32), kTravWarps * 32, 0, st>>>(
+                hp, pl.src_cnt.p, pl.src_off.p, pl.src_sorted.p, qs, pl.tgt_sorted.p + t0,
+                pl.tgt_ids.p + t0, nts, pl.helm_nodes.p, W, k0_fast_table_dev(), out_dev);
         VPG_LAUNCH_CHECK();
         ++launches;
     }

@@ -164,9 +164,26 @@ def test_native_target_shards_assemble_bit_exact(vp, world):
     assert np.array_equal(again, full)
 
 
-def test_helmholtz_plans_refuse_shards(vp):
+@pytest.mark.parametrize("mode", ["reference", "native"])
+def test_helmholtz_target_shards_assemble_bit_exact(vp, mode):
+    """Modified Helmholtz shards: the treecode traverses only the shard's
+    targets; the Chebyshev FMM evaluates L2P + near field only for them (its
+    far field stays whole on every rank).  Bit-exact assembly."""
+    from paper_2203_05933_b200 import multigpu
     rng = np.random.default_rng(39)
-    src = rng.uniform(-1, 1, (20_000, 2))
-    with vp.SummationPlan(vp.make_kernel(vp.KernelFamily.ModifiedHelmholtz, 10.0), src, src, 1e-12) as plan:
-        with pytest.raises(vp.InvalidArgument, match="cannot be sharded"):
-            plan.set_shard(0, 1)
+    src = rng.uniform(-1, 1, (30_000, 2))
+    q = rng.standard_normal(len(src))
+    with vp.SummationPlan(vp.make_kernel(vp.KernelFamily.ModifiedHelmholtz, 10.0), src, src, 1e-12,
+                          mode=mode) as plan:
+        full = plan.apply(q)
+        total = np.zeros_like(full)
+        owners = np.zeros(len(src), np.int64)
+        for r in range(3):
+            multigpu.shard_plan(plan, r, 3)
+            part = plan.apply(q)
+            owners += part != 0.0
+            total += part
+        plan.set_shard(0, plan.shard_units().size)
+        assert np.array_equal(plan.apply(q), full)
+    assert np.all(owners == 1)
+    assert np.array_equal(total, full)
