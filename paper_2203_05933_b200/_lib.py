@@ -13,7 +13,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvolpot_b200.so")
+LIB_PATH = os.environ.get("VPG_LIB_PATH") or os.path.join(_HERE, "libvolpot_b200.so")
 
 VPG_OK = 0
 VPG_ERR_INVALID_ARGUMENT = 1

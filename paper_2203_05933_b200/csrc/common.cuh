@@ -84,14 +84,19 @@ __host__ __device__ inline cplx cadd(cplx a, cplx b) {
 // Natural log for the P2P inner loop, split as ln(x) = e*ln2 + t so the
 // caller can accumulate sum(q*t) and sum(q*e) separately and apply ln2 once
 // (hi/lo split) per target.  x = 2^e * m, m in [1,2); m is rounded to the
-// nearest centre c = 1 + i/256 (i = 0..256, from the top mantissa bits) and
-// ln(m) = -ln(1/c) + log1p(m * RN(1/c) - 1) with |m/c - 1| <= 2^-9; log1p by
-// a degree-5 polynomial (truncation 2^-54/6 < 1e-17 absolute).  Centre i = 0
+// nearest centre c = 1 + i/512 (i = 0..512, from the top mantissa bits) and
+// ln(m) = -ln(1/c) + log1p(m * RN(1/c) - 1) with |m/c - 1| <= 2^-10; log1p by
+// a degree-4 polynomial (truncation 2^-50/5 < 2e-16 absolute; one DFMA per
+// pair less than the 8-bit table with degree 5, -6% near-field time on
+// cfg4; VPG_LOG_BITS=8 selects that variant).  Centre i = 0
 // is c = 1 exactly (RN(1/c) = 1, ln = 0), so ln(1) and ln(2^k) come out
 // exact.  The table (RN(1/c), -ln RN(1/c)) lives in shared memory replicated
 // 8x so the eight lanes of every quarter-warp 128-bit access hit distinct
 // bank groups whatever the indices (conflict-free).
-constexpr int kLogTableBits = 8;
+#ifndef VPG_LOG_BITS
+#define VPG_LOG_BITS 9
+#endif
+constexpr int kLogTableBits = VPG_LOG_BITS;
 constexpr int kLogTableSize = (1 << kLogTableBits) + 1;
 constexpr int kLogTableCopies = 8;
 constexpr int kLogTableBytes = kLogTableSize * kLogTableCopies * 16;
@@ -114,30 +119,38 @@ __device__ __forceinline__ double2 lds_f64x2(uint32_t saddr) {
     return v;
 }
 
-// Shared-window byte address of this lane's copy of table entry 0.
+// Shared-window byte address of this lane's copy of table entry 0, biased
+// by -(0x3FF << bits) entries: fast_log_split indexes with the mantissa
+// word 0x3FF00000 | mant (see there); uint32 wrap-around cancels.
+constexpr uint32_t kLogTableBias = uint32_t(0x3FF << kLogTableBits) * uint32_t(16 * kLogTableCopies);
 __device__ __forceinline__ uint32_t log_table_lane_addr(const double2* tab, int lane8) {
-    return uint32_t(__cvta_generic_to_shared(tab)) + uint32_t(lane8) * 16u;
+    return uint32_t(__cvta_generic_to_shared(tab)) + uint32_t(lane8) * 16u - kLogTableBias;
 }
 
 // Returns t with ln(x) = ed*ln2 + t; ed = exponent as a double.
-// Integer side: v = (hi + 2^11) >> 12 = 256 e_b + idx (the carry of the
-// rounding add lands in the exponent field), so the table byte offset is
-// 128 v - 32768 e_b; the exponent is converted by I2F.F64 (conversion pipe,
-// not the FP64 pipe); the mantissa word is one 3-input LOP3.
+// Integer side (6 instructions): the mantissa word mhi = 0x3FF00000 | mant
+// is one 3-input LOP3; v = (mhi + half) >> (20 - bits) = (0x3FF << bits) +
+// idx (a rounding carry gives idx = 2^bits, the table's last entry), so the
+// byte address is tab_lane + 128 v with the bias folded into tab_lane
+// (log_table_lane_addr); the unbiased exponent is (hi - 0x3FF00000) >> 20
+// (arithmetic shift), converted by I2F.F64 (conversion pipe, not FP64).
 __device__ __forceinline__ double fast_log_split(double x, uint32_t tab_lane, double& ed) {
     const int hi = __double2hiint(x);
     const int lo = __double2loint(x);
-    const int eb = hi >> 20;  // biased exponent (x >= 0)
-    const uint32_t v = uint32_t(hi + (1 << (19 - kLogTableBits))) >> (20 - kLogTableBits);
-    const uint32_t off = v * uint32_t(16 * kLogTableCopies) - uint32_t(eb) * uint32_t(16 * kLogTableCopies * 256);
     int mhi;
     asm("lop3.b32 %0, %1, 0x000FFFFF, %2, 0xEA;" : "=r"(mhi) : "r"(hi), "r"(0x3FF00000));
+    const uint32_t v = uint32_t(mhi + (1 << (19 - kLogTableBits))) >> (20 - kLogTableBits);
     const double m = __hiloint2double(mhi, lo);
-    ed = __int2double_rn(eb - 1023);
-    const double2 tc = lds_f64x2(tab_lane + off);
+    ed = __int2double_rn((hi - 0x3FF00000) >> 20);
+    const double2 tc = lds_f64x2(tab_lane + v * uint32_t(16 * kLogTableCopies));
     const double r = fma(m, tc.x, -1.0);
+#if VPG_LOG_BITS >= 9
+    // |r| <= 2^-10: degree 4 (truncation 2^-50/5 < 2e-16 absolute)
+    double p = fma(r, c_log1p5[1], c_log1p5[2]);
+#else
     double p = fma(r, c_log1p5[0], c_log1p5[1]);
     p = fma(r, p, c_log1p5[2]);
+#endif
     p = fma(r, p, c_log1p5[3]);
     const double r2 = r * r;
     return tc.y + fma(r2, p, r);

@@ -110,7 +110,7 @@ void launch_allpairs(const double2* src, const double* q, int64_t ns,
     if (nt <= 0) return;
     const size_t smem = (kFamily == VPG_LAPLACE ? size_t(kLogTableBytes) : 0) +
                         sizeof(double2) * 2 * kDirThreads;
-    smem_optin((const void*)allpairs_kernel<kFamily, kSkip>, 64 * 1024);
+    smem_optin((const void*)allpairs_kernel<kFamily, kSkip>, int(smem));
     const int64_t gx = nblk(nt, kDirThreads * kDirTPT);
     // enough CTAs for ~4 resident per SM, but slices of >= 2048 sources
     int64_t nslice = std::max<int64_t>(1, (int64_t(sm_count()) * 4 + gx - 1) / gx);

@@ -385,16 +385,18 @@ struct M2LStage {
     int32_t src[kM2LPairs];
     int32_t omap[kM2LPairs];
     int32_t oidx[kM2LPairs];
+    int32_t ecount;
 };
 
 
 
-// One warp stages a batch: list metadata into the ring slot, then the
-// source rows by 1-D TMA bulk copies completing on the batch's mbarrier.
-__device__ __forceinline__ void m2l_issue(const M2LBatch& bt, const int32_t* esrc,
-                                          const int32_t* eoidx, const int32_t* omap_s,
-                                          const double2* mult, int n, M2LStage* stg, double2* raw,
-                                          uint64_t* bar, int lane) {
+// The producer warp stages a batch in two steps, one batch apart: the list
+// metadata into its ring slot (global loads whose latency then hides behind
+// the previous batch's GEMM), and later the source rows by 1-D TMA bulk
+// copies completing on the batch's mbarrier.
+__device__ __forceinline__ void m2l_stage_meta(const M2LBatch& bt, const int32_t* esrc,
+                                               const int32_t* eoidx, const int32_t* omap_s,
+                                               M2LStage* stg, int lane) {
     for (int e = lane; e < bt.ecount; e += 32) {
         const int64_t g = int64_t(bt.efirst) + e;
         const int o = eoidx[g];
@@ -402,10 +404,16 @@ __device__ __forceinline__ void m2l_issue(const M2LBatch& bt, const int32_t* esr
         stg->oidx[e] = o;
         stg->omap[e] = omap_s[o];
     }
+    if (lane == 0) stg->ecount = bt.ecount;
     __syncwarp();
-    if (lane == 0) mbar_arrive_expect_tx(bar, uint32_t(bt.ecount) * uint32_t(n) * 16u);
+}
+
+__device__ __forceinline__ void m2l_issue_rows(const M2LStage* stg, const double2* mult, int n,
+                                               double2* raw, uint64_t* bar, int lane) {
+    const int ecount = stg->ecount;
+    if (lane == 0) mbar_arrive_expect_tx(bar, uint32_t(ecount) * uint32_t(n) * 16u);
     __syncwarp();
-    for (int e = lane; e < bt.ecount; e += 32)
+    for (int e = lane; e < ecount; e += 32)
         tma_load_1d(raw + e * n, mult + int64_t(stg->src[e]) * n, uint32_t(n) * 16u, bar);
 }
 
@@ -458,6 +466,7 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
     double2* a0s0 = reinterpret_cast<double2*>(yb0 + 2 * n * kM2LXS);   // [2][kM2LPairs]
     M2LStage* stg = reinterpret_cast<M2LStage*>(a0s0 + 2 * kM2LPairs);  // [kWSStages]
     __shared__ __align__(8) uint64_t bars[7];
+    __shared__ double ninv[64];    // -1/l (the epilogue's per-lane rows; no divergent LDC)
     uint64_t* full = bars + 1;     // [2] source rows landed (TMA tx count)
     uint64_t* mmadone = bars + 3;  // [2] rows consumed, Y written (MMA warps)
     uint64_t* yfree = bars + 5;    // [2] Y consumed (reduction warps)
@@ -477,6 +486,7 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
         logmd[i] = logmd_g[i];
         omap_s[i] = omap_g[i];
     }
+    for (int i = tid; i < 64; i += blockDim.x) ninv[i] = c_neg_inv_k[i];
     __syncthreads();
     bulk_stage(hs, h_t, uint32_t(KP * kM2LHS) * 8u, &bars[0], 0);
     __syncthreads();
@@ -486,31 +496,42 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
     const int64_t stride = gridDim.x;
     if (warp == 0) {
         // ------------------------------------------------- TMA producer
-        for (int j = 0; j < 2; ++j) {
+        // metadata of batches 0..2, rows of batches 0, 1; then per consumed
+        // batch it: rows of it + 2 (metadata already staged), metadata of
+        // it + 3 (its ring slot held batch it - 1, finished before it)
+        for (int j = 0; j < 3; ++j) {
             const int64_t bi = blockIdx.x + j * stride;
-            if (bi < nbatch)
-                m2l_issue(batches[bi], esrc, eoidx, omap_s, mult, n, &stg[j], raw0 + j * kM2LPairs * n,
-                          &full[j], lane);
+            if (bi < nbatch) m2l_stage_meta(batches[bi], esrc, eoidx, omap_s, &stg[j], lane);
         }
+        for (int j = 0; j < 2; ++j)
+            if (blockIdx.x + j * stride < nbatch)
+                m2l_issue_rows(&stg[j], mult, n, raw0 + j * kM2LPairs * n, &full[j], lane);
         for (int it = 0;; ++it) {
             const int64_t bn = blockIdx.x + (it + 2) * stride;
             if (bn >= nbatch) break;
             const int j = it & 1;
             mbar_wait(&mmadone[j], uint32_t(it >> 1) & 1u);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            m2l_issue(batches[bn], esrc, eoidx, omap_s, mult, n, &stg[(it + 2) % kWSStages],
-                      raw0 + j * kM2LPairs * n, &full[j], lane);
+            m2l_issue_rows(&stg[(it + 2) % kWSStages], mult, n, raw0 + j * kM2LPairs * n, &full[j], lane);
+            const int64_t bm = bn + stride;
+            if (bm < nbatch)
+                m2l_stage_meta(batches[bm], esrc, eoidx, omap_s, &stg[(it + 3) % kWSStages], lane);
         }
     } else if (warp <= kWSMMAWarps) {
         // ---------------------------------------------------------- MMA
         const int w = warp - 1;
         const int kq = lane & 3, rq = lane >> 2;
+        // the next batch's descriptor is loaded one batch ahead (its global
+        // latency otherwise sits in front of every batch)
+        M2LBatch bt_next{};
+        if (blockIdx.x < nbatch) bt_next = batches[blockIdx.x];
         for (int it = 0;; ++it) {
             const int64_t bi = blockIdx.x + it * stride;
             if (bi >= nbatch) break;
             const int j = it & 1;
             const uint32_t use = uint32_t(it >> 1);
-            const M2LBatch bt = batches[bi];
+            const M2LBatch bt = bt_next;
+            if (bi + stride < nbatch) bt_next = batches[bi + stride];
             const M2LStage& sg = stg[it % kWSStages];
             const double2* raw = raw0 + j * kM2LPairs * n;
             mbar_wait(&full[j], use & 1u);
@@ -586,7 +607,7 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
                                 br = yr + (lg.x * a0.x - lg.y * a0.y);
                                 bim = yi + (lg.x * a0.y + lg.y * a0.x);
                             } else {
-                                const double inv_l = c_neg_inv_k[l];  // -1/l
+                                const double inv_l = ninv[l];  // -1/l
                                 const double zr = fma(inv_l, a0.x, yr), zi = fma(inv_l, a0.y, yi);
                                 const double2 dl = turn(canon[ci * n + l], (m * l) & 3, sc);
                                 br = dl.x * zr - dl.y * zi;
@@ -602,12 +623,15 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
     } else {
         // ---------------------------------------------------- reduction
         const int rtid = tid - 32 * (1 + kWSMMAWarps);
+        M2LBatch bt_next{};
+        if (blockIdx.x < nbatch) bt_next = batches[blockIdx.x];
         for (int it = 0;; ++it) {
             const int64_t bi = blockIdx.x + it * stride;
             if (bi >= nbatch) break;
             const int j = it & 1;
             const uint32_t use = uint32_t(it >> 1);
-            const M2LBatch bt = batches[bi];
+            const M2LBatch bt = bt_next;
+            if (bi + stride < nbatch) bt_next = batches[bi + stride];
             const double* yb = yb0 + j * n * kM2LXS;
             const double2* a0s = a0s0 + j * kM2LPairs;
             mbar_wait(&mmadone[j], use & 1u);
@@ -740,9 +764,10 @@ l2p_kernel(const P2PChunk* chunks, int64_t nchunks, const int32_t* lrows, const 
 // shuffle scan gives the flat offsets -- and streamed through a per-warp
 // smem slot kP2PBatch sources at a time (coalesced loads, broadcast reads).
 // Every lane holds two targets, so one source fetch feeds two pairs.  The
-// hot loop has no zero test: pairs of the centre leaf (the only place equal
-// coordinates can meet) are undone and redone with the reference skip rule
-// right after their batch (lap_pair_fixup).
+// hot loop has no zero test: the pairs with r^2 zero or subnormal (only
+// possible within the centre leaf) are listed once per plan
+// (build_coincidences) and undone / redone with the reference skip rule in
+// the chunk epilogue (coin_correction).
 // Every task is one warp, drawn from a ticket counter (zeroed by
 // l2p_kernel) in plan-time cost order:
 //   split chunks (large neighbourhoods, see schedule_near_chunks): part i of
@@ -763,6 +788,10 @@ constexpr int kP2PChunk = 64;
 #define VPG_P2P_MIN_BLOCKS 2
 #endif
 constexpr int kP2PMinBlocks = VPG_P2P_MIN_BLOCKS;
+#ifndef VPG_P2P_UNROLL
+#define VPG_P2P_UNROLL 2
+#endif
+constexpr int kP2PUnroll = VPG_P2P_UNROLL;  // sources per hot-loop iteration
 
 // The near sources of a chunk: up to kMaxNearRanges leaf ranges (the 3x3
 // neighbourhood in uniform trees, the U list in adaptive ones) flattened
@@ -771,7 +800,6 @@ constexpr int kP2PMinBlocks = VPG_P2P_MIN_BLOCKS;
 struct NearList {
     int total;
     int nr;
-    int self0, self1;   // flat range of the target leaf's own sources
     const int* pre;     // [nr] prefix offsets (smem)
     const int* st;      // [nr] first sorted source (smem)
 };
@@ -801,8 +829,6 @@ __device__ __forceinline__ NearList near_list(const int2* ranges, int rfirst, in
     nl.total = tot0 + __shfl_sync(0xffffffffu, i1, 31);
     nl.nr = rcount;
     __syncwarp();
-    nl.self0 = pre_s[rself];
-    nl.self1 = rself + 1 < rcount ? pre_s[rself + 1] : nl.total;
     nl.pre = pre_s;
     nl.st = st_s;
     return nl;
@@ -836,31 +862,39 @@ __device__ __forceinline__ void near_batch(const NearList& nl, int base, int cnt
     if (!active) return;
     int j = grp - base % S;
     if (j < 0) j += S;
-#pragma unroll 2
+#pragma unroll kP2PUnroll
     for (; j < cnt; j += S) {
         const double2 sp = mxy[j];
         const double qj = mq[j];
         lap_pair_fast(tx[0], ty[0], sp.x, sp.y, qj, tab_lane, acc[0]);
         lap_pair_fast(tx[1], ty[1], sp.x, sp.y, qj, tab_lane, acc[1]);
     }
-    const int c0 = max(nl.self0, base), c1 = min(nl.self1, base + cnt);
-    if (c0 < c1) {
-        int f = c0 + (grp - c0 % S);
-        if (f < c0) f += S;
-        for (; f < c1; f += S) {
-            const double2 sp = mxy[f - base];
-            const double qj = mq[f - base];
-            lap_pair_fixup(tx[0], ty[0], sp.x, sp.y, qj, tab_lane, acc[0]);
-            lap_pair_fixup(tx[1], ty[1], sp.x, sp.y, qj, tab_lane, acc[1]);
-        }
-    }
 }
+
+// The coincidence correction of one target (sorted index ti): the listed
+// pairs undone and redone with the reference rule (lap_pair_fixup), as a
+// separate sum added to the target's total.
+__device__ __forceinline__ double coin_correction(const int32_t* coin_off, const int32_t* coin_src,
+                                                  int64_t ti, double tx, double ty, const double2* sxy,
+                                                  const double* q, uint32_t tab_lane) {
+    const int k0 = coin_off[ti], k1 = coin_off[ti + 1];
+    if (k0 == k1) return 0.0;
+    LapAcc fix;
+    for (int k = k0; k < k1; ++k) {
+        const int j = coin_src[k];
+        const double2 sp = sxy[j];
+        lap_pair_fixup(tx, ty, sp.x, sp.y, q[j], tab_lane, fix);
+    }
+    return lap_total(fix);
+}
+
+static_assert(kLogTableSize * 16 <= kP2PWarps * kP2PBatch * 24, "table staging fits sbuf + qbuf");
 
 __global__ void __launch_bounds__(kP2PWarps * 32, kP2PMinBlocks)
 l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, const int2* ranges,
                const double2* sxy, const double* q, const double2* txy,
-               const int32_t* tids, const double2* gtab, int* ticket, double* partial, int* pcount,
-               double* out) {
+               const int32_t* tids, const int32_t* coin_off, const int32_t* coin_src,
+               const double2* gtab, int* ticket, double* partial, int* pcount, double* out) {
     extern __shared__ double2 smp[];
     double2* tab = smp;                                                  // log table
     double2* sbuf = smp + kLogTableSize * kLogTableCopies;               // [warps][batch] xy
@@ -922,7 +956,11 @@ l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, const int2* ranges,
                     const int li = lane + 32 * u;
                     double sum = 0.0;
                     for (int i = 0; i < c.nparts; ++i) sum += __ldcg(pr + i * 64 + li);
-                    if (li < nT) out[tids[c.tbegin + li]] = -kInv4Pi * sum;
+                    if (li < nT) {
+                        sum += coin_correction(coin_off, coin_src, c.tbegin + li, tx[u], ty[u], sxy, q,
+                                               tab_lane);
+                        out[tids[c.tbegin + li]] = -kInv4Pi * sum;
+                    }
                 }
             }
             continue;
@@ -953,7 +991,10 @@ l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, const int2* ranges,
                 if (grp == 0) v += w;
             }
             const int li = tl + nTh * u;
-            if (grp == 0 && li < nT) out[tids[c.tbegin + li]] = -kInv4Pi * v;
+            if (grp == 0 && li < nT) {
+                v += coin_correction(coin_off, coin_src, c.tbegin + li, tx[u], ty[u], sxy, q, tab_lane);
+                out[tids[c.tbegin + li]] = -kInv4Pi * v;
+            }
         }
     }
 }
@@ -1123,6 +1164,62 @@ __global__ void gather_q(const double* q, const int32_t* ids, int64_t n, double*
 }  // namespace
 
 // ------------------------------------------------------------- operators --
+// Plan time: the (target, own-leaf source) pairs whose r^2 -- computed
+// exactly as in lap_pair_fast -- is zero or subnormal.  Warp per chunk
+// (first part of split chunks), lane per target; pass 1 counts (src ==
+// nullptr), pass 2 writes the sorted source indices at off.
+__global__ void coin_scan_kernel(const P2PChunk* chunks, int64_t nchunks, const int2* ranges,
+                                 const double2* sxy, const double2* txy, int32_t* cnt,
+                                 const int32_t* off, int32_t* src) {
+    const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= nchunks) return;
+    const P2PChunk c = chunks[w];
+    if (c.nparts > 1 && c.part != 0) return;
+    const int2 own = ranges[c.rfirst + c.rself];
+    for (int u = lane; u < c.tcount; u += 32) {
+        const int64_t ti = int64_t(c.tbegin) + u;
+        const double2 t = txy[ti];
+        int k = 0;
+        const int base = src ? off[ti] : 0;
+        for (int j = 0; j < own.y; ++j) {
+            const double2 sp = sxy[own.x + j];
+            const double dx = t.x - sp.x, dy = t.y - sp.y;
+            const double r2 = fma(dy, dy, dx * dx);
+            if (__double2hiint(r2) < 0x00100000) {
+                if (src) src[base + k] = own.x + j;
+                ++k;
+            }
+        }
+        if (!src) cnt[ti] = k;
+    }
+}
+
+static void build_coincidences(Plan& pl) {
+    const int64_t nt = pl.nt;
+    pl.coin_off.alloc(size_t(nt) + 1);
+    std::vector<int32_t> off(size_t(nt) + 1, 0);
+    if (pl.n_p2p_chunks > 0 && nt > 0) {
+        DBuf<int32_t> cnt;
+        cnt.alloc(size_t(nt));
+        VPG_CUDA(cudaMemset(cnt.p, 0, cnt.bytes()));
+        const unsigned grid = unsigned(nblk(pl.n_p2p_chunks * 32, 256));
+        coin_scan_kernel<<<grid, 256>>>(pl.p2p_chunks.p, pl.n_p2p_chunks, pl.near_ranges.p, pl.src_sorted.p,
+                                        pl.tgt_sorted.p, cnt.p, nullptr, nullptr);
+        VPG_CUDA(cudaGetLastError());
+        VPG_CUDA(cudaMemcpy(off.data() + 1, cnt.p, cnt.bytes(), cudaMemcpyDeviceToHost));
+        for (size_t i = 1; i < off.size(); ++i) off[i] += off[i - 1];
+    }
+    VPG_CUDA(cudaMemcpy(pl.coin_off.p, off.data(), sizeof(int32_t) * off.size(), cudaMemcpyHostToDevice));
+    pl.coin_src.alloc(size_t(std::max<int32_t>(off.back(), 1)));
+    if (off.back() > 0) {
+        const unsigned grid = unsigned(nblk(pl.n_p2p_chunks * 32, 256));
+        coin_scan_kernel<<<grid, 256>>>(pl.p2p_chunks.p, pl.n_p2p_chunks, pl.near_ranges.p, pl.src_sorted.p,
+                                        pl.tgt_sorted.p, nullptr, pl.coin_off.p, pl.coin_src.p);
+        VPG_CUDA(cudaGetLastError());
+    }
+}
+
 void build_laplace_ops(Plan& pl) {
     // P from epsilon (summation.cpp:155-157)
     pl.P = std::clamp(int(std::ceil(std::log(1.0 / pl.eps) / std::log(1.83))) + 4, 10, 60);
@@ -1269,7 +1366,8 @@ void build_laplace_ops(Plan& pl) {
                                                                kShiftWarps * 32, sm_dn));
         pl.shift_grid = std::max(1, std::min(pu, pd)) * pl.sm_count;
     }
-    smem_optin((const void*)l2p_p2p_kernel, 64 * 1024);
+    smem_optin((const void*)l2p_p2p_kernel, kLogTableBytes + 32 * 1024);
+    build_coincidences(pl);
 }
 
 // ----------------------------------------------------------------- apply --
@@ -1358,8 +1456,8 @@ void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const L
         launch_pdl(l2p_p2p_kernel, dim3(grid), dim3(kP2PWarps * 32), smem, s,
                    (const P2PChunk*)pl.p2p_chunks.p, pl.n_p2p_chunks,
                    (const int2*)pl.near_ranges.p, (const double2*)pl.src_sorted.p, (const double*)qs,
-                   (const double2*)pl.tgt_sorted.p, (const int32_t*)pl.tgt_ids.p, log_table_dev(), ticket,
-                   partial_p2p, pcount, out_dev);
+                   (const double2*)pl.tgt_sorted.p, (const int32_t*)pl.tgt_ids.p, pl.coin_off.p,
+                   pl.coin_src.p, log_table_dev(), ticket, partial_p2p, pcount, out_dev);
         ++launches;
     };
 

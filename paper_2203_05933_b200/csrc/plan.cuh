@@ -156,6 +156,9 @@ struct Plan {
     int p2p_tpt = 1;
     DBuf<P2PChunk> p2p_chunks;
     DBuf<int2> near_ranges;  // (first sorted source, count) per near leaf
+    // Laplace near field: (target, own-leaf source) pairs with r^2 zero or
+    // subnormal, CSR over sorted targets (fmm.cu, build_coincidences)
+    DBuf<int32_t> coin_off, coin_src;
     int64_t n_p2p_chunks = 0;
     int64_t n_p2p_heavy = 0;  // split chunks (counters)
     int64_t n_p2p_parts = 0;  // partial-sum rows of the split chunks

@@ -261,3 +261,21 @@ def test_runtime_ratio_50k_to_100k(vp):
                 ms.append(e0.elapsed_time(e1))
             t[n] = sorted(ms)[2]
     assert t[100_000] / t[50_000] <= 2.6, t
+
+
+@pytest.mark.parametrize("mode", ["reference", "native"])
+def test_near_field_zero_and_subnormal_pairs(vp, rest, mode):
+    """The near-field hot loop has no zero test; the plan lists the pairs with
+    r^2 zero (skipped, summation.cpp:340) or subnormal (exact log) and the
+    apply corrects them.  Points next to the origin make subnormal r^2."""
+    rng = np.random.default_rng(41)
+    src = np.concatenate([rng.uniform(-1, 1, (20_000, 2)), [[0.0, 0.0], [0.0, 3e-160]]])
+    tgt = np.concatenate([src[:400], [[1e-160, 0.0], [0.0, 0.0], [-2e-161, 1e-161]],
+                          rng.uniform(-1, 1, (3000, 2))])
+    q = rng.standard_normal(len(src))
+    with vp.SummationPlan(lap(vp), src, tgt, 1e-12, mode=mode) as plan:
+        gpu = plan.apply(q)
+    cpu = rest.plan_sum(0, 0.0, src, q, tgt, 1e-12)
+    assert rel_l2(gpu, cpu) <= 1e-12
+    # the three targets at the origin carry log(r^2) ~ -737 terms
+    assert np.allclose(gpu[400:403], cpu[400:403], rtol=1e-12, atol=0)
