@@ -7,6 +7,7 @@
 // c holds multipoles in s/(z-c) and locals in (z-c)/s (summation.cpp:131-134),
 // so every operator depends only on integer offsets and is shared by all
 // levels.
+#include <cstdlib>
 #include <algorithm>
 #include <cmath>
 #include <vector>
@@ -1452,7 +1453,13 @@ void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const L
         int per_sm = 1;
         VPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, l2p_p2p_kernel, kP2PWarps * 32, smem));
         const int64_t want = (pl.n_p2p_chunks + kP2PWarps - 1) / kP2PWarps;
-        const unsigned grid = unsigned(std::min<int64_t>(want, int64_t(pl.sm_count) * std::max(per_sm, 1)));
+        int64_t cap = int64_t(pl.sm_count) * std::max(per_sm, 1);
+        static const int pct = [] {
+            const char* v = std::getenv("VPG_P2P_SIDE_PCT");
+            return v ? std::atoi(v) : 100;
+        }();
+        if (s != st && pct > 0 && pct < 100) cap = std::max<int64_t>(1, cap * pct / 100);
+        const unsigned grid = unsigned(std::min<int64_t>(want, cap));
         launch_pdl(l2p_p2p_kernel, dim3(grid), dim3(kP2PWarps * 32), smem, s,
                    (const P2PChunk*)pl.p2p_chunks.p, pl.n_p2p_chunks,
                    (const int2*)pl.near_ranges.p, (const double2*)pl.src_sorted.p, (const double*)qs,
