@@ -419,16 +419,153 @@ def run_gpu(args):
     return 0
 
 
+# ----------------------------------------------------------------- layer potential
+LAYER_METRIC = "target-boundary node interactions/s (FP64) for the layer-potential evaluation"
+LAYER_FLOPS = {0: 15.0, 1: 80.0}  # per evaluated pair: Laplace dn/r^2 (+min), MH with K1 by convention
+
+
+def _layer_pairs(sys, tgt):
+    """Evaluated pairs of one eval: every target against every coarse node,
+    plus 8n fine nodes for the targets the refined check sends to the fine
+    rule (bie.cpp:414-440), counted on the host from the coarse distance."""
+    coarse = fine = 0
+    for c in sys.curves:
+        h = c.length / c.n
+        d2 = np.full(len(tgt), np.inf)
+        for j0 in range(0, c.n, 64):
+            blk = c.x[j0:j0 + 64]
+            d2 = np.minimum(d2, ((tgt[:, None, :] - blk[None, :, :]) ** 2).sum(axis=2).min(axis=1))
+        cand = np.sqrt(d2) - 0.75 * h <= 5.0 * h
+        coarse += len(tgt) * c.n
+        fine += int(cand.sum()) * c.n * 8
+    return coarse, fine
+
+
+def run_layer(args):
+    import torch
+
+    import paper_2203_05933_b200 as vp
+    from paper_2203_05933_b200 import workloads as W
+
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        import oracle
+        sys_, cf, tg = W.layer_cfg2()
+        rest = oracle.restatement()
+        cores = os.cpu_count() or 1
+        sub = tg[:: max(1, len(tg) // 60000)]
+        for _ in range(args.warmup):
+            rest.layer_eval(0, 0.0, sys_.curves, sys_.n_density, sys_.n_aux, cf, sub, True, cores)
+        times = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            rest.layer_eval(0, 0.0, sys_.curves, sys_.n_density, sys_.n_aux, cf, sub, True, cores)
+            times.append(time.perf_counter() - t0)
+        co, fi = _layer_pairs(sys_, sub)
+        t = float(np.mean(times))
+        v = (co + fi) / t
+        print(json.dumps({
+            "impl": "reference", "metric": LAYER_METRIC, "value": v, "unit": "interactions/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, configs[1] shapes)",
+            "config": {"workload": "layer", "nt": len(sub), "n_boundary": sys_.n_density},
+            "cpu_baseline": {"value": v, "unit": "interactions/s", "cores": cores, "kind": "port",
+                             "sample": f"every {max(1, len(tg) // 60000)}-th configs[1] target ({len(sub)}), "
+                                       "oracle vo_layer_eval (bie.cpp:383-461 restated; bie.cpp needs Eigen)"},
+            "e2e": {"value": v, "unit": "interactions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+            flush=True)
+        return 0
+    torch.cuda.set_device(local)
+    sys_, cf, tg = W.layer_cfg2()
+    ev_obj = sys_.evaluator(local)
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+    cf_d = torch.from_numpy(cf).to("cuda")
+    tg_d = torch.from_numpy(np.ascontiguousarray(tg)).to("cuda")
+    out_d = torch.empty(len(tg), dtype=torch.float64, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def step():
+        ev_obj.eval_device(cf_d.data_ptr(), cf_d.numel(), tg_d.data_ptr(), len(tg), out_d.data_ptr(),
+                           allow_close=True, stream=sh)
+
+    clk = ClockSampler(local).__enter__()
+    for _ in range(args.warmup):
+        step()
+    t_hold = time.time()
+    while time.time() - t_hold < 0.5:
+        step()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    clk.__exit__(None, None, None)
+    ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    # end to end: host arrays through vpg_layer_eval (H2D of density + targets, D2H of u_H)
+    host = ev_obj.eval(cf, tg, allow_close=True)
+    e2e = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        host = ev_obj.eval(cf, tg, allow_close=True)
+        e2e.append(time.perf_counter() - t0)
+    e2e_ms = float(np.mean(e2e)) * 1e3
+    if not np.array_equal(host, out_d.cpu().numpy()):
+        raise RuntimeError("host and device layer evaluations differ")
+    co, fi = _layer_pairs(sys_, tg)
+    pairs = co + fi
+    achieved = pairs * LAYER_FLOPS[0] / (ms * 1e-3) / 1e12
+    peak = fp64_peak_tflops("fp64")
+    line = {
+        "metric": LAYER_METRIC, "value": pairs / (ms * 1e-3), "unit": "interactions/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, configs[1] shapes)",
+        "config": {"workload": "layer", "nt": len(tg), "n_boundary": sys_.n_density, "coarse_pairs": co,
+                   "fine_pairs": fi, "allow_close": True, "l2": "flushed (256 MB write) before every timed step",
+                   "step": "eval_layer_potential (bie.cpp:383-468), Laplace, star boundary"},
+        "e2e": {"value": pairs / (e2e_ms * 1e-3), "unit": "interactions/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": 8 * cf.size + 16 * len(tg), "d2h_bytes_per_step": 8 * len(tg),
+                "path": "vpg_layer_eval with host arrays (wall clock, includes the reject readback)"},
+        "gpu_launches": (4 + len(sys_.curves)) * args.steps,
+        "roofline": {"bound": "fp64", "kernel": "coarse_kernel+fine_kernel", "achieved": achieved, "peak": peak,
+                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                     "flops_per_unit": "15 per evaluated (target, node) pair (2 sub, 3 r^2, 3 dn, 1 min, "
+                                       "4 reciprocal, 2 accumulate)"},
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline:
+        import oracle
+        rest = oracle.restatement()
+        cores = os.cpu_count() or 1
+        sub = tg[:: max(1, len(tg) // 60000)]
+        t0 = time.perf_counter()
+        rest.layer_eval(0, 0.0, sys_.curves, sys_.n_density, sys_.n_aux, cf, sub, True, cores)
+        t = time.perf_counter() - t0
+        cs, fs = _layer_pairs(sys_, sub)
+        line["cpu_baseline"] = {"value": (cs + fs) / t, "unit": "interactions/s", "cores": cores, "kind": "port",
+                                "sample": f"{len(sub)} of the configs[1] targets (every "
+                                          f"{max(1, len(tg) // 60000)}-th), oracle vo_layer_eval"}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "layer"])
     ap.add_argument("--mode", default="reference", choices=["reference", "native"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.workload == "layer":
+        return run_layer(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_gpu(args)

@@ -22,6 +22,8 @@
  *                                 (potential.cpp:446-462)  vpg_corr_create/apply
  *   build_charges                 (potential.cpp:397-412)  vpg_charges_create/apply
  *   VolumePotentialOperator::apply (potential.cpp:431-470) vpg_operator_create/apply
+ *   eval_layer_potential          (bie.hpp:87-90,
+ *                                  bie.cpp:383-468)       vpg_layer_create/eval
  *
  * Conventions
  *   - Point arrays are interleaved xy float64 (the reference Vec2 is a
@@ -215,6 +217,42 @@ int vpg_operator_create(const vpg_plan* plan, const vpg_charges* ch, const vpg_c
 int vpg_operator_apply(const vpg_operator* op, const double* f, int64_t nf, double* out,
                        unsigned flags, void* stream, float* timings_ms);
 int vpg_operator_destroy(vpg_operator* op);
+
+/* Double-layer potential at volume targets, eval_layer_potential
+ * (bie.hpp:87-90, bie.cpp:383-468): the trapezoidal Nystrom sum of every
+ * curve, the 8x trig-upsampled rule within 5 node spacings (bie.cpp:414-
+ * 440), plus the log-completion terms of the holes (bie.cpp:443-446).
+ * A curve block carries the BoundarySystem::CurveBlock fields the
+ * evaluation reads (bie.hpp:30-47): n nodes (even, >= 16) with interleaved
+ * xy positions and outward normals and speeds, the 8n-point refined
+ * geometry, total arclength, node-set diameter and log_center (holes). */
+typedef struct vpg_layer vpg_layer;
+typedef struct {
+    int n;
+    int offset; /* first density coefficient of the curve */
+    double length;
+    double diam;
+    const double* x;           /* [n][2] */
+    const double* normal;      /* [n][2] */
+    const double* speed;       /* [n] */
+    const double* fine_x;      /* [8n][2] */
+    const double* fine_normal; /* [8n][2] */
+    const double* fine_speed;  /* [8n] */
+    double log_center[2];
+} vpg_curve_block;
+/* Uploads the boundary geometry once (the BoundarySystem is immutable). */
+int vpg_layer_create(int family, double lambda, const vpg_curve_block* curves,
+                     int ncurves, int n_density, int n_aux, int device,
+                     vpg_layer** layer);
+/* coeffs: n_density + n_aux values (density then log coefficients);
+ * targets nt interleaved xy.  Errors with the reference messages:
+ * "eval_layer_potential: coefficient length mismatch", "... target lies on a
+ * boundary node", "... target inside the close-evaluation collar ..."
+ * (VPG_ERR_INVALID_ARGUMENT; the on-node error wins when both occur). */
+int vpg_layer_eval(const vpg_layer* layer, const double* coeffs,
+                   int64_t ncoeffs, const double* tgt_xy, int64_t nt,
+                   int allow_close, double* out, unsigned flags, void* stream);
+int vpg_layer_destroy(vpg_layer* layer);
 
 #ifdef __cplusplus
 }

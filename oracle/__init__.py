@@ -59,6 +59,12 @@ class VoParams(C.Structure):
                 ("side", C.c_double)]
 
 
+class VoCurve(C.Structure):
+    _fields_ = [("n", C.c_int), ("offset", C.c_int), ("length", C.c_double), ("diam", C.c_double),
+                ("x", _P), ("normal", _P), ("speed", _P), ("fine_x", _P), ("fine_normal", _P),
+                ("fine_speed", _P), ("log_center", C.c_double * 2)]
+
+
 class Restatement:
     """Our CPU restatement (volpot_oracle.h)."""
 
@@ -83,6 +89,12 @@ class Restatement:
         h.vo_pairwise_sum_ld.restype = None
         h.vo_bessel_k0.argtypes = [C.c_double]
         h.vo_bessel_k0.restype = C.c_double
+        h.vo_bessel_k1.argtypes = [C.c_double]
+        h.vo_bessel_k1.restype = C.c_double
+        h.vo_trig_upsample.argtypes = [_P, C.c_int, C.c_int, _P]
+        h.vo_trig_upsample.restype = None
+        h.vo_layer_eval.argtypes = [C.c_int, C.c_double, _P, C.c_int, C.c_int, C.c_int, _P, i64, _P, i64,
+                                    C.c_int, _P, C.c_int]
         h.vo_correction_apply.argtypes = [i64, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int]
         h.vo_correction_apply.restype = None
         h.vo_build_charges.argtypes = [i64, _P, _P, _P, _P, C.c_int, C.c_int, _P, C.c_int,
@@ -149,6 +161,40 @@ class Restatement:
     def bessel_k0(self, xs):
         return np.array([self.h.vo_bessel_k0(float(x)) for x in np.ravel(xs)])
 
+    def bessel_k1(self, xs):
+        return np.array([self.h.vo_bessel_k1(float(x)) for x in np.ravel(xs)])
+
+    def trig_upsample(self, f, factor=8):
+        f = _vec(f)
+        out = np.empty(f.size * factor)
+        self.h.vo_trig_upsample(_p(f), f.size, factor, _p(out))
+        return out
+
+    def layer_eval(self, family, lam, curves, n_density, n_aux, coeffs, targets, allow_close=False,
+                   threads=0):
+        """bie.cpp:383-461 restated.  ``curves``: objects with the CurveBlock
+        fields (n, offset, length, diam, x, normal, speed, fine_*,
+        log_center).  Returns (out, rc): rc 0 ok, 1 length mismatch, 2 on a
+        node, 3 inside the collar."""
+        keep = []
+        arr = (VoCurve * len(curves))()
+        for i, c in enumerate(curves):
+            fields = {}
+            for name in ("x", "normal", "speed", "fine_x", "fine_normal", "fine_speed"):
+                a = np.ascontiguousarray(getattr(c, name), dtype=np.float64)
+                keep.append(a)
+                fields[name] = a.ctypes.data
+            arr[i].n, arr[i].offset, arr[i].length, arr[i].diam = int(c.n), int(c.offset), float(c.length), \
+                float(c.diam)
+            for k, v in fields.items():
+                setattr(arr[i], k, v)
+            arr[i].log_center[0], arr[i].log_center[1] = float(c.log_center[0]), float(c.log_center[1])
+        cf, tg = _vec(coeffs), _pts(targets)
+        out = np.zeros(len(tg))
+        rc = self.h.vo_layer_eval(int(family), float(lam), arr, len(curves), int(n_density), int(n_aux),
+                                  _p(cf), cf.size, _p(tg), len(tg), int(bool(allow_close)), _p(out), threads)
+        return out, rc
+
     def correction_apply(self, blk_off, blk_cell, blk_pool, pool_off, pool_vals, node_off, f, out,
                          threads=0):
         a = [np.ascontiguousarray(blk_off, np.int32), np.ascontiguousarray(blk_cell, np.int32),
@@ -192,6 +238,7 @@ class Reference:
         h.ref_plan_destroy.restype = None
         h.ref_direct_sum.argtypes = [C.c_int, C.c_double, _P, _P, i64, _P, i64, _P]
         h.ref_bessel_k0.argtypes = [_P, i64, _P]
+        h.ref_bessel_k1.argtypes = [_P, i64, _P]
         self.h = h
 
     def set_threads(self, n):
@@ -219,6 +266,12 @@ class Reference:
         x = _vec(xs)
         out = np.empty_like(x)
         self._err(self.h.ref_bessel_k0(_p(x), x.size, _p(out)), "bessel_k0")
+        return out
+
+    def bessel_k1(self, xs):
+        x = _vec(xs)
+        out = np.empty_like(x)
+        self._err(self.h.ref_bessel_k1(_p(x), x.size, _p(out)), "bessel_k1")
         return out
 
 

@@ -8,6 +8,7 @@
 //   volpot::SummationPlan ctor/apply/levels/expansion_order  (summation.hpp:34-55)
 //   volpot::direct_sum                                       (summation.hpp:22-23)
 //   volpot::bessel_k0                                        (kernel.hpp:11)
+//   volpot::bessel_k1                                        (kernel.hpp:12)
 //   volpot::set_thread_count                                 (common.hpp:44)
 #include <cstdint>
 #include <cstring>
@@ -102,6 +103,12 @@ int ref_direct_sum(int family, double lambda, const double* src_xy,
 int ref_bessel_k0(const double* x, int64_t n, double* out) {
     return guarded([&] {
         for (int64_t i = 0; i < n; ++i) out[i] = volpot::bessel_k0(x[i]);
+    });
+}
+
+int ref_bessel_k1(const double* x, int64_t n, double* out) {
+    return guarded([&] {
+        for (int64_t i = 0; i < n; ++i) out[i] = volpot::bessel_k1(x[i]);
     });
 }
 

@@ -120,9 +120,27 @@ double series_k0(double x) {
     return -(std::log(0.5 * x) + kGamma) * i0 + acc;
 }
 
-// kernel.cpp:57-91: e^x K0(x) by composite 10-point Gauss-Legendre on the
+// kernel.cpp:33-49 restated: K1 = (ln(x/2) + gamma) I1 + 1/x - (x/4) sum,
+// I1 = (x/2) sum_k c_k, c_k = q^k / (k! (k+1)!), the sum weighted by
+// H_k + H_{k+1}.
+double series_k1(double x) {
+    const double t = 0.25 * x * x;
+    double c = 1.0, i1s = 1.0, acc = 1.0, h0 = 0.0, h1 = 1.0;
+    for (int k = 1; k < 40; ++k) {
+        c *= t / (static_cast<double>(k) * (k + 1));
+        h0 += 1.0 / k;
+        h1 += 1.0 / (k + 1);
+        i1s += c;
+        acc += (h0 + h1) * c;
+        if (c < 1e-19 * i1s) break;
+    }
+    const double i1 = 0.5 * x * i1s;
+    return (std::log(0.5 * x) + kGamma) * i1 + 1.0 / x - 0.25 * x * acc;
+}
+
+// kernel.cpp:57-91: e^x K0(x) (e^x K1(x) with order1) by composite 10-point Gauss-Legendre on the
 // truncated integral representation, doubling panels until converged.
-long double scaled_k0_integral(long double x) {
+long double scaled_k0_integral(long double x, bool order1 = false) {
     static const long double nodes[10] = {
         -0.9739065285171717L, -0.8650633666889845L, -0.6794095682990244L,
         -0.4333953941292472L, -0.1488743389816312L, 0.1488743389816312L,
@@ -143,7 +161,10 @@ long double scaled_k0_integral(long double x) {
             const long double a = p * hp;
             for (int i = 0; i < 10; ++i) {
                 const long double t = a + 0.5L * hp * (nodes[i] + 1.0L);
-                s += wts[i] * std::exp(-x * (std::cosh(t) - 1.0L));
+                const long double ch = std::cosh(t);
+                long double v = std::exp(-x * (ch - 1.0L));
+                if (order1) v *= ch;
+                s += wts[i] * v;
             }
         }
         s *= 0.5L * hp;
@@ -154,17 +175,18 @@ long double scaled_k0_integral(long double x) {
 }
 
 // kernel.cpp:93-149: 9 dyadic intervals [2,4]..[512,1024], 25 coefficients
+// (order1: the K1 fit, kernel.cpp:123-124)
 struct K0Fit {
     static constexpr int NI = 9, NC = 25;
     double c[NI][NC];
-    K0Fit() {
+    explicit K0Fit(bool order1 = false) {
         for (int iv = 0; iv < NI; ++iv) {
             const long double a = std::pow(2.0L, iv + 1), b = 2.0L * a;
             long double fv[NC];
             for (int j = 0; j < NC; ++j) {
                 const long double th = std::numbers::pi_v<long double> * (j + 0.5L) / NC;
                 const long double xj = 0.5L * (a + b) + 0.5L * (b - a) * std::cos(th);
-                fv[j] = scaled_k0_integral(xj) * std::sqrt(xj);
+                fv[j] = scaled_k0_integral(xj, order1) * std::sqrt(xj);
             }
             for (int k = 0; k < NC; ++k) {
                 long double s = 0.0L;
@@ -205,6 +227,16 @@ double k0(double x) {
     const double ex = std::exp(-x);
     if (ex == 0.0) return 0.0;
     return k0fit().eval(x) * ex / std::sqrt(x);
+}
+
+// kernel.cpp:174-179
+double k1(double x) {
+    if (!(x > 0.0)) return std::nan("");
+    if (x <= 2.0) return series_k1(x);
+    const double ex = std::exp(-x);
+    if (ex == 0.0) return 0.0;
+    static const K0Fit fit1(true);
+    return fit1.eval(x) * ex / std::sqrt(x);
 }
 
 // kernel.cpp:181-186
@@ -835,6 +867,113 @@ void vo_build_charges(int64_t ncell, const int32_t* cell_type,
             charges[base + s] = src_wj[base + s] * v;
         }
     }
+}
+
+
+double vo_bessel_k1(double x) { return k1(x); }
+
+// bie.cpp:112-135
+void vo_trig_upsample(const double* f, int n, int factor, double* out) {
+    constexpr double kTwoPi = 2.0 * std::numbers::pi;
+    const int half = n / 2;
+    std::vector<double> a(size_t(half) + 1, 0.0), b(size_t(half), 0.0);
+    for (int m = 0; m <= half; ++m) {
+        double ca = 0.0, cb = 0.0;
+        for (int j = 0; j < n; ++j) {
+            const double ang = kTwoPi * m * j / n;
+            ca += f[j] * std::cos(ang);
+            cb += f[j] * std::sin(ang);
+        }
+        a[size_t(m)] = 2.0 * ca / n;
+        if (m >= 1 && m < half) b[size_t(m)] = 2.0 * cb / n;
+    }
+    a[0] *= 0.5;
+    a[size_t(half)] *= 0.5;
+    for (int j = 0; j < n * factor; ++j) {
+        const double t = kTwoPi * j / (n * factor);
+        double s = a[0] + a[size_t(half)] * std::cos(half * t);
+        for (int m = 1; m < half; ++m) s += a[size_t(m)] * std::cos(m * t) + b[size_t(m)] * std::sin(m * t);
+        out[j] = s;
+    }
+}
+
+// bie.cpp:383-461 with dlp_entry (bie.cpp:43-50); kFineFactor 8, kFineReach
+// 5, kCollarFraction 0.02 (bie.cpp:18-20)
+int vo_layer_eval(int family, double lambda, const vo_curve* curves, int ncurves, int n_density,
+                  int n_aux, const double* coeffs, int64_t ncoeffs, const double* tgt, int64_t nt,
+                  int allow_close, double* out, int nthreads) {
+    constexpr double kTwoPi = 2.0 * std::numbers::pi;
+    constexpr int kFine = 8;
+    constexpr double kReach = 5.0, kCollar = 0.02;
+    if (ncoeffs != int64_t(n_density) + n_aux) return 1;
+    g_threads = nthreads;
+    std::vector<std::vector<double>> fine_phi(static_cast<size_t>(ncurves));
+    for (int c = 0; c < ncurves; ++c) {
+        const vo_curve& B = curves[c];
+        fine_phi[size_t(c)].resize(size_t(B.n) * kFine);
+        vo_trig_upsample(coeffs + B.offset, B.n, kFine, fine_phi[size_t(c)].data());
+    }
+    auto dlp = [&](double x0, double x1, const double* y, const double* ny, double speed) {
+        const double d0 = y[0] - x0, d1 = y[1] - x1;
+        const double r2 = d0 * d0 + d1 * d1;
+        const double dn = d0 * ny[0] + d1 * ny[1];
+        if (family == 0) return -dn / (kTwoPi * r2) * speed;
+        const double r = std::sqrt(r2);
+        return -(lambda / kTwoPi) * k1(lambda * r) * (dn / r) * speed;
+    };
+    std::atomic<int> reject{0};
+    pfor(nt, [&](int64_t ti) {
+        const double x0 = tgt[2 * ti], x1 = tgt[2 * ti + 1];
+        double acc = 0.0;
+        for (int c = 0; c < ncurves; ++c) {
+            const vo_curve& B = curves[c];
+            const double h = B.length / B.n;
+            const double collar = allow_close ? 0.0 : kCollar * B.diam;
+            double d2 = 1e300;
+            for (int j = 0; j < B.n; ++j) {
+                const double e0 = x0 - B.x[2 * j], e1 = x1 - B.x[2 * j + 1];
+                d2 = std::min(d2, e0 * e0 + e1 * e1);
+            }
+            double d = std::sqrt(d2);
+            bool fine = false;
+            if (d - 0.75 * h <= std::max(collar, kReach * h)) {
+                d2 = 1e300;
+                for (int j = 0; j < B.n * kFine; ++j) {
+                    const double e0 = x0 - B.fine_x[2 * j], e1 = x1 - B.fine_x[2 * j + 1];
+                    d2 = std::min(d2, e0 * e0 + e1 * e1);
+                }
+                d = std::sqrt(d2);
+                if (d == 0.0) {
+                    reject.store(2);
+                    return;
+                }
+                if (d < collar) {
+                    int want = 0;
+                    reject.compare_exchange_strong(want, 1);
+                    return;
+                }
+                fine = d <= kReach * h;
+            }
+            if (fine) {
+                const int nf = B.n * kFine;
+                const double w = kTwoPi / nf;
+                const double* phi = fine_phi[size_t(c)].data();
+                for (int j = 0; j < nf; ++j)
+                    acc += w * phi[j] * dlp(x0, x1, B.fine_x + 2 * j, B.fine_normal + 2 * j, B.fine_speed[j]);
+            } else {
+                const double w = kTwoPi / B.n;
+                for (int j = 0; j < B.n; ++j)
+                    acc += w * coeffs[B.offset + j] * dlp(x0, x1, B.x + 2 * j, B.normal + 2 * j, B.speed[j]);
+            }
+        }
+        for (int k = 0; k < n_aux; ++k) {
+            const double d0 = x0 - curves[k + 1].log_center[0], d1 = x1 - curves[k + 1].log_center[1];
+            acc += coeffs[n_density + k] * (-std::log(std::sqrt(d0 * d0 + d1 * d1)) / kTwoPi);
+        }
+        out[ti] = acc;
+    });
+    const int r = reject.load();
+    return r == 2 ? 2 : r == 1 ? 3 : 0;
 }
 
 }  // extern "C"

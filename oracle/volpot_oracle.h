@@ -96,6 +96,39 @@ void vo_build_charges(int64_t ncell, const int32_t* cell_type,
                       const double* over1, int np1, int nq1,
                       const double* src_wj, const double* f, double* charges);
 
+/* kernel.cpp:174-179 -- K1 (series below 2, Chebyshev fits above). */
+double vo_bessel_k1(double x);
+
+/* bie.cpp:112-135 -- trig_upsample: zero-padded Fourier interpolation of n
+ * (even) periodic samples onto factor*n points. */
+void vo_trig_upsample(const double* f, int n, int factor, double* out);
+
+/* One curve block of BoundarySystem (bie.hpp:30-47): the fields that
+ * eval_layer_potential reads.  x/normal are n interleaved xy, speed n;
+ * fine_* the 8n-point refined geometry (bie.cpp:206-215). */
+typedef struct {
+    int n;
+    int offset;
+    double length;
+    double diam;
+    const double* x;
+    const double* normal;
+    const double* speed;
+    const double* fine_x;
+    const double* fine_normal;
+    const double* fine_speed;
+    double log_center[2];
+} vo_curve;
+
+/* bie.cpp:383-461 -- eval_layer_potential(sys, coeffs, targets,
+ * allow_close).  Returns 0, 1 (coefficient length mismatch), 2 (a target
+ * lies on a boundary node) or 3 (a target inside the collar); 2 wins over 3
+ * when both occur (the reference keeps whichever store came last). */
+int vo_layer_eval(int family, double lambda, const vo_curve* curves,
+                  int ncurves, int n_density, int n_aux,
+                  const double* coeffs, int64_t ncoeffs, const double* tgt,
+                  int64_t nt, int allow_close, double* out, int nthreads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -9,6 +9,8 @@ C++ API; include/volpot_b200/summation.hpp is the C++ mirror.
 """
 from ._lib import (CoincidentPoint, CudaError, DomainError, InvalidArgument,  # noqa: F401
                    OutOfMemory, VolpotError, device_count)
+from .bie import (BoundarySystem, CurveBlock, LayerEvaluator, assemble_geometry,  # noqa: F401
+                  eval_layer_potential)
 from .correction import ChargeMap, CorrectionMap, VolumePotentialOperator  # noqa: F401
 from .summation import (Kernel, KernelFamily, SourceSet, SummationPlan,  # noqa: F401
                         accelerated_sum, bessel_k0, direct_sum, make_kernel)
@@ -17,4 +19,5 @@ __all__ = [
     "Kernel", "KernelFamily", "make_kernel", "SourceSet", "SummationPlan", "direct_sum",
     "accelerated_sum", "bessel_k0", "CorrectionMap", "ChargeMap", "VolumePotentialOperator", "InvalidArgument",
     "CoincidentPoint", "DomainError", "CudaError", "OutOfMemory", "VolpotError", "device_count",
+    "BoundarySystem", "CurveBlock", "LayerEvaluator", "assemble_geometry", "eval_layer_potential",
 ]

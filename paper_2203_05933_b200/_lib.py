@@ -61,6 +61,16 @@ class OutOfMemory(CudaError, MemoryError):
     pass
 
 
+class CurveBlockC(C.Structure):
+    """vpg_curve_block (include/volpot_b200.h)."""
+    _fields_ = [
+        ("n", C.c_int), ("offset", C.c_int), ("length", C.c_double), ("diam", C.c_double),
+        ("x", C.c_void_p), ("normal", C.c_void_p), ("speed", C.c_void_p),
+        ("fine_x", C.c_void_p), ("fine_normal", C.c_void_p), ("fine_speed", C.c_void_p),
+        ("log_center", C.c_double * 2),
+    ]
+
+
 class PlanInfo(C.Structure):
     _fields_ = [
         ("num_sources", C.c_int64), ("num_targets", C.c_int64),
@@ -111,6 +121,10 @@ _SIGS = {
     "vpg_operator_create": (C.c_int, [_P, _P, _P, C.POINTER(_P)]),
     "vpg_operator_apply": (C.c_int, [_P, _P, C.c_int64, _P, C.c_uint, _P, C.POINTER(C.c_float)]),
     "vpg_operator_destroy": (C.c_int, [_P]),
+    "vpg_layer_create": (C.c_int, [C.c_int, C.c_double, _P, C.c_int, C.c_int, C.c_int, C.c_int,
+                                   C.POINTER(_P)]),
+    "vpg_layer_eval": (C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, C.c_int, _P, C.c_uint, _P]),
+    "vpg_layer_destroy": (C.c_int, [_P]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

@@ -31,6 +31,7 @@ struct DeviceTables {
     double2* log_tab = nullptr;
     double* k0_tab = nullptr;
     double* k0f_tab = nullptr;
+    double* k1_tab = nullptr;
 };
 std::map<int, DeviceTables> g_tables;
 std::set<std::pair<const void*, int>> g_optin;
@@ -86,6 +87,12 @@ static DeviceTables& tables_locked(int dev) {
         VPG_CUDA(cudaMalloc(&t.k0_tab, sizeof(double) * h.size()));
         VPG_CUDA(cudaMemcpy(t.k0_tab, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
     }
+    if (!t.k1_tab) {
+        std::vector<double> h(size_t(kK0Intervals) * kK0Coeffs);
+        k1_fit_host(h.data());
+        VPG_CUDA(cudaMalloc(&t.k1_tab, sizeof(double) * h.size()));
+        VPG_CUDA(cudaMemcpy(t.k1_tab, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
+    }
     if (!t.k0f_tab) {
         std::vector<double> h(size_t(kK0FastIntervals) * kK0FastStride, 0.0);
         k0_fit_fast_host(h.data());
@@ -106,6 +113,12 @@ const double* k0_fast_table_dev() {
     VPG_CUDA(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lk(g_mu);
     return tables_locked(dev).k0f_tab;
+}
+const double* k1_table_dev() {
+    int dev = 0;
+    VPG_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_mu);
+    return tables_locked(dev).k1_tab;
 }
 const double* k0_table_dev() {
     int dev = 0;

@@ -254,6 +254,7 @@ void launch_coop(void (*kern)(KArgs...), int grid, dim3 block, size_t smem, cuda
 // Per-device constant tables, built on first use (api.cu).
 const double2* log_table_dev();  // kLogTableSize entries (inv_c, -ln inv_c)
 const double* k0_table_dev();    // K0 Chebyshev fits, see k0.cuh
+const double* k1_table_dev();    // K1 Chebyshev fits (same layout)
 const double* k0_fast_table_dev();  // quarter-octave K0 fits (k0_fast)
 
 // Opt a kernel into > 48 KB dynamic shared memory once per device.

@@ -121,6 +121,40 @@ __device__ __forceinline__ double k0_pair(double tx, double ty, double sx,
 
 // Host: builds the Chebyshev table (kK0Intervals x kK0Coeffs doubles).
 void k0_fit_host(double* out);
+void k1_fit_host(double* out);  // the K1 table, same layout
+
+// ---- K1 (kernel.cpp:33-49, 174-179), for the double-layer kernel ----
+// x <= 2: K1 = (ln(x/2) + gamma) I1 + 1/x - (x/4) S with I1 = (x/2) sum c_k q^k,
+// c_k = 1/(k! (k+1)!), S = sum (H_k + H_{k+1}) c_k q^k, q = x^2/4: fixed
+// degree-16 polynomials (tail < 1e-27 for q <= 1, where the reference loop
+// stops at a 1e-19 relative term).  x > 2: the K1 Chebyshev fit of
+// K1(x) e^x sqrt(x) on the reference's dyadic intervals.
+static __constant__ double c_k1_c[17] = {
+    1.0, 0.5, 0.08333333333333333, 0.006944444444444444, 0.00034722222222222224,
+    1.1574074074074073e-05, 2.755731922398589e-07, 4.920949861426052e-09, 6.834652585313961e-11,
+    7.594058428126623e-13, 6.903689480115112e-15, 5.230067787965994e-17, 3.352607556388458e-19,
+    1.842092063949702e-21, 8.771866971189057e-24, 3.654944571328774e-26, 1.3437296218120491e-28};
+static __constant__ double c_k1_s[17] = {
+    1.0, 1.25, 0.2777777777777778, 0.027199074074074073, 0.0015162037037037036,
+    5.4783950617283953e-05, 1.3896762408667172e-06, 2.613375872835907e-08, 3.791062453869784e-10,
+    4.3726106266713215e-12, 4.106898277957945e-14, 3.202416543243305e-16, 2.1065588026621898e-18,
+    1.1847776309828747e-20, 5.762933548568204e-23, 2.448432012616415e-25, 9.16461430197137e-28};
+
+__device__ __forceinline__ double k1_small(double x) {
+    const double q = 0.25 * x * x;
+    double i1s = c_k1_c[16], s = c_k1_s[16];
+#pragma unroll
+    for (int k = 15; k >= 0; --k) {
+        i1s = fma(i1s, q, c_k1_c[k]);
+        s = fma(s, q, c_k1_s[k]);
+    }
+    constexpr double kGamma = 0.57721566490153286061;
+    return (log(0.5 * x) + kGamma) * (0.5 * x * i1s) + 1.0 / x - 0.25 * x * s;
+}
+
+__device__ __forceinline__ double k1_dev(double x, const double* tab1) {
+    return x <= 2.0 ? k1_small(x) : k0_large(x, tab1);  // same fit layout
+}
 
 // ---- fast K0 for the treecode's proxy loop (same accuracy, fewer ops) ----
 // x > 2: quarter-octave intervals with 14-term Chebyshev fits (the nearest

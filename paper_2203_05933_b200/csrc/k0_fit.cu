@@ -38,8 +38,9 @@ struct GL {
     }
 };
 
-// e^x K0(x) for x >= 2.
-long double scaled_k0(long double x, const GL& g) {
+// e^x K0(x) for x >= 2 (e^x K1(x) with order1: integrand times cosh t,
+// kernel.cpp:57-91).
+long double scaled_k0(long double x, const GL& g, bool order1 = false) {
     const long double T = std::acosh(1.0L + 64.0L / x);  // integrand ~ e^-64
     long double prev = 0;
     for (int panels = 4; panels <= 4096; panels *= 2) {
@@ -48,7 +49,8 @@ long double scaled_k0(long double x, const GL& g) {
         for (int p = 0; p < panels; ++p)
             for (size_t i = 0; i < g.x.size(); ++i) {
                 const long double t = h * (p + 0.5L * (g.x[i] + 1));
-                sum += g.w[i] * std::exp(-x * (std::cosh(t) - 1));
+                const long double ch = std::cosh(t);
+                sum += g.w[i] * std::exp(-x * (ch - 1)) * (order1 ? ch : 1.0L);
             }
         sum *= 0.5L * h;
         if (panels > 4 && std::fabs(sum - prev) <= 1e-20L * sum) return sum;
@@ -70,6 +72,27 @@ void k0_fit_host(double* out) {
             const long double th = pi * (j + 0.5L) / N;
             const long double xj = 0.5L * (lo + hi) + 0.5L * (hi - lo) * std::cos(th);
             f[j] = scaled_k0(xj, g) * std::sqrt(xj);
+        }
+        for (int k = 0; k < N; ++k) {
+            long double s = 0;
+            for (int j = 0; j < N; ++j) s += f[j] * std::cos(k * pi * (j + 0.5L) / N);
+            out[iv * N + k] = double(2 * s / N);
+        }
+    }
+}
+
+// The K1 fit of the reference (kernel.cpp:93-149 with order1).
+void k1_fit_host(double* out) {
+    const GL g(20);
+    const long double pi = 3.141592653589793238462643383279502884L;
+    const int N = kK0Coeffs;
+    for (int iv = 0; iv < kK0Intervals; ++iv) {
+        const long double lo = std::ldexp(1.0L, iv + 1), hi = 2 * lo;
+        long double f[kK0Coeffs];
+        for (int j = 0; j < N; ++j) {
+            const long double th = pi * (j + 0.5L) / N;
+            const long double xj = 0.5L * (lo + hi) + 0.5L * (hi - lo) * std::cos(th);
+            f[j] = scaled_k0(xj, g, true) * std::sqrt(xj);
         }
         for (int k = 0; k < N; ++k) {
             long double s = 0;

@@ -282,3 +282,53 @@ CONFIGS = {"cfg1": cfg1, "cfg2": cfg2, "cfg3": cfg3, "cfg4": cfg4, "cfg5": cfg5}
 def random_points(n, seed, lo=0.0, hi=1.0):
     rng = np.random.default_rng(seed)
     return rng.uniform(lo, hi, size=(n, 2))
+
+
+def layer_system(kernel=None, n=None, holes=False):
+    """Star boundary r = 1 + 0.3 cos 5t (configs[1]) as a BoundarySystem
+    geometry; n defaults to solve_bvp's rule ceil(max(64, 40 L)), made even,
+    and at least 0.5 lambda L for modified Helmholtz (bie.cpp:478-491).
+    ``holes`` adds a circular hole (a Laplace log-completion coefficient)."""
+    from . import bie
+    from .summation import KernelFamily, make_kernel
+    kernel = kernel or make_kernel(KernelFamily.Laplace)
+    curves = [bie.star_curve()]
+    if holes:
+        curves.append(bie.circle_curve(0.15, -0.1, 0.3, hole=True))
+    counts = []
+    for c in curves:
+        if n:
+            counts.append(n + n % 2)
+            continue
+        ln = c.total_arclength()
+        want = max(64.0, 40.0 * ln)
+        if kernel.family == KernelFamily.ModifiedHelmholtz:
+            want = max(want, 0.5 * kernel.lam * ln)
+        k = int(np.ceil(want))
+        counts.append(k + k % 2)
+    return bie.assemble_geometry(curves, counts, kernel)
+
+
+def layer_density(sys, seed=7, modes=12):
+    """A seeded smooth periodic density per curve (a few Fourier modes with
+    decaying amplitudes) plus seeded log coefficients."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for c in sys.curves:
+        t = 2.0 * np.pi * np.arange(c.n) / c.n
+        v = np.full(c.n, rng.uniform(-1, 1))
+        for m in range(1, modes + 1):
+            a, b = rng.uniform(-1, 1, 2) / m
+            v += a * np.cos(m * t) + b * np.sin(m * t)
+        out.append(v)
+    return np.concatenate(out + [rng.uniform(-1, 1, sys.n_aux)])
+
+
+def layer_cfg2(kernel=None, seed=2):
+    """Layer-potential workload on configs[1]: the star boundary system, a
+    seeded density, targets = the cfg2 nodes + 10,000 interior points
+    (solve_bvp evaluates at mesh nodes + targets with allow_close,
+    bie.cpp:520-523)."""
+    w = cfg2(seed)
+    sys = layer_system(kernel)
+    return sys, layer_density(sys), w.tgt
