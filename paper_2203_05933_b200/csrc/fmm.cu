@@ -835,14 +835,17 @@ __device__ __forceinline__ NearList near_list(const int2* ranges, int rfirst, in
     return nl;
 }
 
-// One batch [base, base+cnt) of the flat list: stage, evaluate (sources
-// f == grp mod S), then fix up the pairs with the target leaf's own sources.
-__device__ __forceinline__ void near_batch(const NearList& nl, int base, int cnt, int grp, int S,
-                                           bool active, int lane, const double2* sxy,
-                                           const double* q, double2* mxy, double* mq,
-                                           uint32_t tab_lane, const double (&tx)[2],
-                                           const double (&ty)[2], LapAcc (&acc)[2]) {
-    __syncwarp();
+// One batch [base, base+cnt) of the flat list, software-pipelined: the
+// sources of batch b+1 are fetched (global -> registers) while batch b is
+// evaluated from smem, so the L2 latency of the staging loads hides behind
+// the pair loop (small leaves have only ~2-3 batches per chunk).
+struct NearRegs {
+    double2 xy[kP2PBatch / 32];
+    double q[kP2PBatch / 32];
+};
+
+__device__ __forceinline__ void near_fetch(const NearList& nl, int base, int cnt, int lane,
+                                           const double2* sxy, const double* q, NearRegs& r) {
 #pragma unroll
     for (int h = 0; h < kP2PBatch / 32; ++h) {
         const int f = h * 32 + lane;
@@ -855,8 +858,24 @@ __device__ __forceinline__ void near_batch(const NearList& nl, int base, int cnt
                 if (nl.pre[mid] <= ff) lo = mid; else hi = mid - 1;
             }
             const int src = nl.st[lo] + (ff - nl.pre[lo]);
-            mxy[f] = sxy[src];
-            mq[f] = q[src];
+            r.xy[h] = sxy[src];
+            r.q[h] = q[src];
+        }
+    }
+}
+
+// evaluate (sources f == grp mod S) from the staged batch
+__device__ __forceinline__ void near_batch(const NearRegs& r, int base, int cnt, int grp, int S,
+                                           bool active, int lane, double2* mxy, double* mq,
+                                           uint32_t tab_lane, const double (&tx)[2],
+                                           const double (&ty)[2], LapAcc (&acc)[2]) {
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < kP2PBatch / 32; ++h) {
+        const int f = h * 32 + lane;
+        if (f < cnt) {
+            mxy[f] = r.xy[h];
+            mq[f] = r.q[h];
         }
     }
     __syncwarp();
@@ -869,6 +888,24 @@ __device__ __forceinline__ void near_batch(const NearList& nl, int base, int cnt
         const double qj = mq[j];
         lap_pair_fast(tx[0], ty[0], sp.x, sp.y, qj, tab_lane, acc[0]);
         lap_pair_fast(tx[1], ty[1], sp.x, sp.y, qj, tab_lane, acc[1]);
+    }
+}
+
+// all batches of [f0, f1): fetch b+1 while b is evaluated
+__device__ __forceinline__ void near_range(const NearList& nl, int f0, int f1, int grp, int S,
+                                           bool active, int lane, const double2* sxy, const double* q,
+                                           double2* mxy, double* mq, uint32_t tab_lane,
+                                           const double (&tx)[2], const double (&ty)[2],
+                                           LapAcc (&acc)[2]) {
+    if (f0 >= f1) return;
+    NearRegs r;
+    near_fetch(nl, f0, min(kP2PBatch, f1 - f0), lane, sxy, q, r);
+    for (int base = f0; base < f1; base += kP2PBatch) {
+        const int cnt = min(kP2PBatch, f1 - base);
+        NearRegs cur = r;
+        if (base + kP2PBatch < f1)
+            near_fetch(nl, base + kP2PBatch, min(kP2PBatch, f1 - base - kP2PBatch), lane, sxy, q, r);
+        near_batch(cur, base, cnt, grp, S, active, lane, mxy, mq, tab_lane, tx, ty, acc);
     }
 }
 
@@ -938,9 +975,7 @@ l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, const int2* ranges,
             }
             const int f0 = int(int64_t(nl.total) * c.part / c.nparts);
             const int f1 = int(int64_t(nl.total) * (c.part + 1) / c.nparts);
-            for (int base = f0; base < f1; base += kP2PBatch)
-                near_batch(nl, base, min(kP2PBatch, f1 - base), 0, 1, true, lane, sxy, q, mxy, mq,
-                           tab_lane, tx, ty, acc);
+            near_range(nl, f0, f1, 0, 1, true, lane, sxy, q, mxy, mq, tab_lane, tx, ty, acc);
             double* prow = partial + int64_t(c.pbase + c.part) * 64;
             prow[lane] = lap_total(acc[0]);
             prow[lane + 32] = lap_total(acc[1]);
@@ -980,9 +1015,7 @@ l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, const int2* ranges,
             tx[u] = t.x;
             ty[u] = t.y;
         }
-        for (int base = 0; base < nl.total; base += kP2PBatch)
-            near_batch(nl, base, min(kP2PBatch, nl.total - base), grp, S, active, lane, sxy, q, mxy,
-                       mq, tab_lane, tx, ty, acc);
+        near_range(nl, 0, nl.total, grp, S, active, lane, sxy, q, mxy, mq, tab_lane, tx, ty, acc);
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
             double v = active ? lap_total(acc[u]) : 0.0;
