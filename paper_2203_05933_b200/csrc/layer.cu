@@ -15,12 +15,12 @@
 //                        B = -w phi speed / 2pi (Laplace) or
 //                        -w phi speed lambda / 2pi (modified Helmholtz), so a
 //                        pair costs dn / r^2 (dn K1(lambda r) / r).
-//   3. coarse_kernel     a thread per target, 256-record tiles in smem: the
+//   3. coarse_kernel     two targets per thread, 256-record smem tiles: the
 //                        coarse min distance and the coarse sum of every curve
 //                        in one pass; targets whose coarse distance asks for
 //                        the refined check (bie.cpp:414) are appended to the
 //                        curve's fine list.
-//   4. fine_kernel       a thread per listed target over the curve's 8n fine
+//   4. fine_kernel       two listed targets per thread over the curve's 8n fine
 //                        records: refined distance, the reject rules
 //                        (bie.cpp:417-425) and the fine sum.
 //   5. finalize_kernel   out = per-curve values in curve order + aux logs.
@@ -43,7 +43,21 @@ constexpr double kTwoPiL = 6.283185307179586476925286766559;  // bie.cpp:17
 constexpr int kFineFactor = 8;      // bie.cpp:18
 constexpr double kFineReach = 5.0;  // bie.cpp:19
 constexpr double kCollarFraction = 0.02;  // bie.cpp:20
-constexpr int kLayerThreads = 256;
+constexpr int kLayerTile = 256;  // records per smem tile
+#ifndef VPG_LAYER_CT
+#define VPG_LAYER_CT 256
+#endif
+#ifndef VPG_LAYER_CTPT
+#define VPG_LAYER_CTPT 1
+#endif
+#ifndef VPG_LAYER_FT
+#define VPG_LAYER_FT 256
+#endif
+#ifndef VPG_LAYER_FTPT
+#define VPG_LAYER_FTPT 1
+#endif
+constexpr int kCoarseThreads = VPG_LAYER_CT, kCoarseTPT = VPG_LAYER_CTPT;  // CTA size, targets per thread
+constexpr int kFineThreads = VPG_LAYER_FT, kFineTPT = VPG_LAYER_FTPT;
 
 struct CurveDev {
     int n, offset;
@@ -143,88 +157,121 @@ __global__ void records_kernel(const CurveDev* cv, int nc, int64_t ncoarse, int6
     frec[gf] = make_double4(y.x, y.y, B * nv.x, B * nv.y);
 }
 
-// Sum over records [r0, r1) for the target (tx, ty): min r^2 and the sum of
-// B dn / r^2 (Laplace) or B dn K1(lambda r) / r (modified Helmholtz).
-// Records are staged in 256-entry smem tiles by the whole CTA.
+// Sum over records [r0, r1) for two targets per thread: min r^2 and the sum
+// of B dn / r^2 (Laplace) or B dn K1(lambda r) / r (modified Helmholtz).
+// Records are staged in kLayerTile-entry smem tiles by the whole CTA; each
+// staged record serves both targets of a thread (two independent chains).
 template <int kFamily>
-__device__ __forceinline__ void tile_sum(const double4* rec, int r0, int r1, double tx, double ty,
-                                         bool active, double lambda, const double* k1tab,
-                                         double4* sm, double& d2min, double& acc) {
-    for (int b = r0; b < r1; b += kLayerThreads) {
-        const int cnt = min(kLayerThreads, r1 - b);
+__device__ __forceinline__ void pair_acc(const double4& r, double tx, double ty, double lambda,
+                                         const double* k1tab, double& d2min, double& acc) {
+    const double dx = r.x - tx, dy = r.y - ty;
+    const double r2 = fma(dy, dy, dx * dx);
+    d2min = fmin(d2min, r2);
+    const double dn = fma(dy, r.w, dx * r.z);
+    if (kFamily == VPG_LAPLACE) {
+        acc = fma(dn, rcp_nr(r2), acc);
+    } else {
+        const double rr = sqrt(r2);
+        acc = fma(dn * k1_dev(lambda * rr, k1tab), rcp_nr(rr), acc);
+    }
+}
+
+template <int kFamily, int TPT>
+__device__ __forceinline__ void tile_sum(const double4* rec, int r0, int r1, const double (&tx)[TPT],
+                                         const double (&ty)[TPT], bool active, double lambda,
+                                         const double* k1tab, double4* sm, double (&d2min)[TPT],
+                                         double (&acc)[TPT]) {
+    for (int b = r0; b < r1; b += kLayerTile) {
+        const int cnt = min(kLayerTile, r1 - b);
         __syncthreads();
-        if (int(threadIdx.x) < cnt) sm[threadIdx.x] = rec[b + threadIdx.x];
+        for (int i = threadIdx.x; i < cnt; i += blockDim.x) sm[i] = rec[b + i];
         __syncthreads();
         if (!active) continue;
 #pragma unroll 4
         for (int k = 0; k < cnt; ++k) {
             const double4 r = sm[k];
-            const double dx = r.x - tx, dy = r.y - ty;
-            const double r2 = fma(dy, dy, dx * dx);
-            d2min = fmin(d2min, r2);
-            const double dn = fma(dy, r.w, dx * r.z);
-            if (kFamily == VPG_LAPLACE) {
-                acc = fma(dn, rcp_nr(r2), acc);
-            } else {
-                const double rr = sqrt(r2);
-                acc = fma(dn * k1_dev(lambda * rr, k1tab), rcp_nr(rr), acc);
+#pragma unroll
+            for (int u = 0; u < TPT; ++u) pair_acc<kFamily>(r, tx[u], ty[u], lambda, k1tab, d2min[u], acc[u]);
+        }
+    }
+}
+
+// Targets t + u * blockDim.x (u < TPT) of a TPT * blockDim.x tile per thread.
+template <int kFamily, int TPT>
+__global__ void __launch_bounds__(512)
+coarse_kernel(const CurveDev* cv, int nc, const double4* crec, const double2* tgt, int64_t nt,
+              int allow_close, double lambda, const double* k1tab, double* cval, int* fcount,
+              int32_t* flist, uint8_t* fflag) {
+    __shared__ double4 sm[kLayerTile];
+    const int64_t t0 = int64_t(blockIdx.x) * TPT * blockDim.x + threadIdx.x;
+    const bool active = t0 < nt;
+    double tx[TPT], ty[TPT];
+#pragma unroll
+    for (int u = 0; u < TPT; ++u) {
+        const double2 p = tgt[min(t0 + u * int64_t(blockDim.x), nt - 1)];
+        tx[u] = p.x;
+        ty[u] = p.y;
+    }
+    for (int c = 0; c < nc; ++c) {
+        const CurveDev C = cv[c];
+        double d2[TPT], acc[TPT];
+#pragma unroll
+        for (int u = 0; u < TPT; ++u) d2[u] = 1e300, acc[u] = 0.0;
+        tile_sum<kFamily, TPT>(crec, C.cbase, C.cbase + C.n, tx, ty, active, lambda, k1tab, sm, d2, acc);
+        const double collar = allow_close ? 0.0 : kCollarFraction * C.diam;
+#pragma unroll
+        for (int u = 0; u < TPT; ++u) {
+            const int64_t t = t0 + u * int64_t(blockDim.x);
+            if (t >= nt) continue;
+            cval[int64_t(c) * nt + t] = acc[u];
+            fflag[int64_t(c) * nt + t] = 0;
+            const double d = sqrt(d2[u]);
+            if (d - 0.75 * C.h <= fmax(collar, kFineReach * C.h)) {  // bie.cpp:414
+                const int slot = atomicAdd(&fcount[c], 1);
+                flist[int64_t(c) * nt + slot] = int32_t(t);
             }
         }
     }
 }
 
-template <int kFamily>
-__global__ void __launch_bounds__(kLayerThreads)
-coarse_kernel(const CurveDev* cv, int nc, const double4* crec, const double2* tgt, int64_t nt,
-              int allow_close, double lambda, const double* k1tab, double* cval, int* fcount,
-              int32_t* flist, uint8_t* fflag) {
-    __shared__ double4 sm[kLayerThreads];
-    const int64_t t = int64_t(blockIdx.x) * kLayerThreads + threadIdx.x;
-    const bool active = t < nt;
-    const double2 p = active ? tgt[t] : make_double2(0.0, 0.0);
-    for (int c = 0; c < nc; ++c) {
-        const CurveDev C = cv[c];
-        double d2 = 1e300, acc = 0.0;
-        tile_sum<kFamily>(crec, C.cbase, C.cbase + C.n, p.x, p.y, active, lambda, k1tab, sm, d2, acc);
-        if (!active) continue;
-        cval[int64_t(c) * nt + t] = acc;
-        fflag[int64_t(c) * nt + t] = 0;
-        const double collar = allow_close ? 0.0 : kCollarFraction * C.diam;
-        const double d = sqrt(d2);
-        if (d - 0.75 * C.h <= fmax(collar, kFineReach * C.h)) {  // bie.cpp:414
-            const int slot = atomicAdd(&fcount[c], 1);
-            flist[int64_t(c) * nt + slot] = int32_t(t);
-        }
-    }
-}
-
-template <int kFamily>
-__global__ void __launch_bounds__(kLayerThreads)
+template <int kFamily, int TPT>
+__global__ void __launch_bounds__(512)
 fine_kernel(const CurveDev* cv, int c, const double4* frec, const double2* tgt, int64_t nt,
             int allow_close, double lambda, const double* k1tab, const int* fcount,
             const int32_t* flist, double* fval, uint8_t* fflag, int* reject) {
-    __shared__ double4 sm[kLayerThreads];
+    __shared__ double4 sm[kLayerTile];
     const CurveDev C = cv[c];
     const int cnt = fcount[c];
     const int nf = C.n * kFineFactor;
     const double collar = allow_close ? 0.0 : kCollarFraction * C.diam;
-    for (int64_t base = int64_t(blockIdx.x) * kLayerThreads; base < cnt;
-         base += int64_t(gridDim.x) * kLayerThreads) {
-        const int64_t i = base + threadIdx.x;
-        const bool active = i < cnt;
-        const int64_t t = active ? flist[int64_t(c) * nt + i] : 0;
-        const double2 p = active ? tgt[t] : make_double2(0.0, 0.0);
-        double d2 = 1e300, acc = 0.0;
-        tile_sum<kFamily>(frec, C.fbase, C.fbase + nf, p.x, p.y, active, lambda, k1tab, sm, d2, acc);
-        if (!active) continue;
-        const double d = sqrt(d2);
-        if (d == 0.0) {  // bie.cpp:417-420
-            atomicMax(reject, 2);
-        } else if (d < collar) {  // bie.cpp:421-424
-            atomicMax(reject, 1);
-        } else if (d <= kFineReach * C.h) {  // bie.cpp:425
-            fval[int64_t(c) * nt + t] = acc;
-            fflag[int64_t(c) * nt + t] = 1;
+    const int64_t tile = int64_t(TPT) * blockDim.x;
+    for (int64_t base = int64_t(blockIdx.x) * tile; base < cnt; base += int64_t(gridDim.x) * tile) {
+        int64_t t[TPT];
+        double tx[TPT], ty[TPT];
+#pragma unroll
+        for (int u = 0; u < TPT; ++u) {
+            const int64_t i = base + threadIdx.x + u * int64_t(blockDim.x);
+            t[u] = i < cnt ? flist[int64_t(c) * nt + i] : -1;
+            const double2 p = tgt[t[u] >= 0 ? t[u] : 0];
+            tx[u] = p.x;
+            ty[u] = p.y;
+        }
+        double d2[TPT], acc[TPT];
+#pragma unroll
+        for (int u = 0; u < TPT; ++u) d2[u] = 1e300, acc[u] = 0.0;
+        tile_sum<kFamily, TPT>(frec, C.fbase, C.fbase + nf, tx, ty, t[0] >= 0, lambda, k1tab, sm, d2, acc);
+#pragma unroll
+        for (int u = 0; u < TPT; ++u) {
+            if (t[u] < 0) continue;
+            const double d = sqrt(d2[u]);
+            if (d == 0.0) {  // bie.cpp:417-420
+                atomicMax(reject, 2);
+            } else if (d < collar) {  // bie.cpp:421-424
+                atomicMax(reject, 1);
+            } else if (d <= kFineReach * C.h) {  // bie.cpp:425
+                fval[int64_t(c) * nt + t[u]] = acc[u];
+                fflag[int64_t(c) * nt + t[u]] = 1;
+            }
         }
     }
 }
@@ -450,17 +497,18 @@ int vpg_layer_eval(const vpg_layer* L, const double* coeffs, int64_t ncoeffs, co
                                              frec);
         VPG_LAUNCH_CHECK();
         if (nt) {
-            (lap ? coarse_kernel<VPG_LAPLACE> : coarse_kernel<VPG_MODIFIED_HELMHOLTZ>)
-                <<<nblk(nt, kLayerThreads), kLayerThreads, 0, s>>>(cv, nc, crec, tg, nt, allow_close,
+            (lap ? coarse_kernel<VPG_LAPLACE, kCoarseTPT> : coarse_kernel<VPG_MODIFIED_HELMHOLTZ, kCoarseTPT>)
+                <<<nblk(nt, kCoarseTPT * kCoarseThreads), kCoarseThreads, 0, s>>>(cv, nc, crec, tg, nt, allow_close,
                                                                    L->lambda, L->k1tab, cval, cnt, flist,
                                                                    fflag);
             VPG_LAUNCH_CHECK();
             int sms = 148;
             VPG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, L->device));
-            const unsigned fgrid = unsigned(std::min<int64_t>(nblk(nt, kLayerThreads), int64_t(sms) * 8));
+            const unsigned fgrid =
+                unsigned(std::min<int64_t>(nblk(nt, kFineTPT * kFineThreads), int64_t(sms) * (2048 / kFineThreads)));
             for (int c = 0; c < nc; ++c) {
-                (lap ? fine_kernel<VPG_LAPLACE> : fine_kernel<VPG_MODIFIED_HELMHOLTZ>)
-                    <<<fgrid, kLayerThreads, 0, s>>>(cv, c, frec, tg, nt, allow_close, L->lambda, L->k1tab,
+                (lap ? fine_kernel<VPG_LAPLACE, kFineTPT> : fine_kernel<VPG_MODIFIED_HELMHOLTZ, kFineTPT>)
+                    <<<fgrid, kFineThreads, 0, s>>>(cv, c, frec, tg, nt, allow_close, L->lambda, L->k1tab,
                                                      cnt, flist, fval, fflag, cnt + nc);
                 VPG_LAUNCH_CHECK();
             }
