@@ -337,6 +337,9 @@ int vpg_plan_create(int family, double lambda, const double* src_xy, int64_t ns,
         pl.tgt.alloc(size_t(nt));
         if (ns) VPG_CUDA(cudaMemcpy(pl.src.p, src_xy, sizeof(double2) * size_t(ns), cudaMemcpyHostToDevice));
         if (nt) VPG_CUDA(cudaMemcpy(pl.tgt.p, tgt_xy, sizeof(double2) * size_t(nt), cudaMemcpyHostToDevice));
+        // "targets = nodes": the first ns targets are the sources, bitwise
+        // (enables the symmetric near field, plan.cuh SymTask)
+        pl.matched = ns > 0 && ns <= nt && std::memcmp(src_xy, tgt_xy, sizeof(double2) * size_t(ns)) == 0;
         build_tree(pl);
         if (!pl.direct) {
             if (family == VPG_LAPLACE) {

@@ -1033,6 +1033,194 @@ l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, const int2* ranges,
     }
 }
 
+// ------------------------------------------------- symmetric near field --
+// Plans with "targets = nodes" (SymTask, plan.cuh): log r^2 of an unordered
+// pair is evaluated once and feeds both targets.  A warp takes one task
+// (leaf A against its flat column list: A itself, then the neighbours whose
+// pairs A owns) from a ticket.  Rows are A's points, R = 1 or 2 per lane;
+// columns come in 32-wide tiles staged (twice, so lane + s needs no wrap)
+// in per-warp smem.  Step s pairs lane l's rows with column (l + s) mod 32:
+// the row sums stay in registers, the column sum travels with its column --
+// one shuffle per step hands lane l + 1's accumulator to lane l, so after 32
+// steps lane c holds column c again and adds it to the column's partial
+// (global, .cg, this warp is its only writer; one read-modify-write per row
+// tile).  v = ln r^2 as one double (t + e ln2 with the split constant: the
+// reference's own log is a single rounded double); r^2 of (i, j) and (j, i)
+// are bitwise equal, so each ordered pair sees the value the one-sided
+// kernel computes.  Flat column j vs row i: i <= j feeds the row, i < j the
+// column (the self part: i < j both ways, i == j row only -- the
+// coincidence list undoes it as in the one-sided kernel; neighbour columns
+// have j >= na > i).  Row sums are added to slot 4 of A's targets at the end
+// of each row tile, after the self-column sums of the earlier tiles.
+constexpr int kSymWarps = 8;
+constexpr size_t kSymSmem = size_t(kLogTableBytes) + size_t(kSymWarps) * (64 * 16 + 64 * 8 + kSymMaxRanges * 16);
+
+template <int R, bool kDiag>
+__device__ __forceinline__ void sym_block(const double2* cxy, const double* cq, int lane, int i0, int j0,
+                                          const double (&rx)[2], const double (&ry)[2], const double (&rq)[2],
+                                          uint32_t tab_lane, double (&racc)[2], double& cacc) {
+#pragma unroll 4
+    for (int st = 0; st < 32; ++st) {
+        const int c = lane + st;
+        const double2 sp = cxy[c];
+        const double qc = cq[c];
+#pragma unroll
+        for (int u = 0; u < R; ++u) {
+            const double dx = rx[u] - sp.x, dy = ry[u] - sp.y;
+            const double r2 = fma(dy, dy, dx * dx);
+            double ed;
+            const double t = fast_log_split(r2, tab_lane, ed);
+            const double v = fma(ed, kLn2Lo, fma(ed, kLn2Hi, t));
+            double qr = qc, qcol = rq[u];
+            if (kDiag) {
+                const int i = i0 + lane + 32 * u, j = j0 + (c & 31);
+                qr = i <= j ? qc : 0.0;
+                qcol = i < j ? rq[u] : 0.0;
+            }
+            racc[u] = fma(qr, v, racc[u]);
+            cacc = fma(qcol, v, cacc);
+        }
+        cacc = __shfl_sync(0xffffffffu, cacc, (lane + 1) & 31);
+    }
+}
+
+// flat column j -> (range index) by a linear scan of the task's ranges
+__device__ __forceinline__ int sym_range_of(const int4* rng, int rcount, int j) {
+    int r = 0;
+    for (int k = 1; k < rcount; ++k)
+        if (rng[k].z <= j) r = k;
+    return r;
+}
+
+template <int R>
+__device__ __forceinline__ void sym_task(const SymTask& T, const int4* rng, const double2* sxy, const double* q,
+                                         double2* cxy, double* cq, uint32_t tab_lane, int lane, double* part,
+                                         int64_t nt) {
+    constexpr double kFar = 1e100;
+    const int nct = (T.ncol + 31) >> 5;
+    for (int r0 = 0; r0 < T.na; r0 += 32 * R) {
+        double rx[2] = {kFar, kFar}, ry[2] = {kFar, kFar}, rq[2] = {0.0, 0.0}, racc[2] = {0.0, 0.0};
+#pragma unroll
+        for (int u = 0; u < R; ++u) {
+            const int i = r0 + lane + 32 * u;
+            if (i < T.na) {
+                const double2 p = sxy[T.a_src + i];
+                rx[u] = p.x;
+                ry[u] = p.y;
+                rq[u] = q[T.a_src + i];
+            }
+        }
+        // column tiles wholly below the row tile (self part) are skipped
+        for (int ct = r0 >> 5; ct < nct; ++ct) {
+            const int j = ct * 32 + lane;
+            int4 rg = make_int4(0, 0, 0, 0);
+            double2 p = make_double2(-kFar, -kFar);
+            double qj = 0.0;
+            if (j < T.ncol) {
+                rg = rng[sym_range_of(rng, T.rcount, j)];
+                p = sxy[rg.x + (j - rg.z)];
+                qj = q[rg.x + (j - rg.z)];
+            }
+            __syncwarp();
+            cxy[lane] = p;
+            cxy[lane + 32] = p;
+            cq[lane] = qj;
+            cq[lane + 32] = qj;
+            __syncwarp();
+            double cacc = 0.0;
+            if (ct * 32 < T.na)
+                sym_block<R, true>(cxy, cq, lane, r0, ct * 32, rx, ry, rq, tab_lane, racc, cacc);
+            else
+                sym_block<R, false>(cxy, cq, lane, r0, ct * 32, rx, ry, rq, tab_lane, racc, cacc);
+            if (j < T.ncol) {
+                double* dst = part + int64_t(rg.w) * nt + rg.y + (j - rg.z);
+                // row tile 0 is the first to touch every column (neighbour
+                // columns are in every tile's range, self column j from 0 on)
+                __stcg(dst, (r0 == 0 ? 0.0 : __ldcg(dst)) + cacc);
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < R; ++u) {
+            const int i = r0 + lane + 32 * u;
+            if (i < T.na) {
+                double* dst = part + int64_t(4) * nt + T.a_tgt + i;
+                __stcg(dst, __ldcg(dst) + racc[u]);
+            }
+        }
+        __syncwarp();
+    }
+}
+
+__global__ void __launch_bounds__(kSymWarps * 32, 2)
+p2p_sym_kernel(const SymTask* tasks, int64_t ntask, const int4* ranges, const double2* sxy, const double* q,
+               const double2* gtab, int* ticket, double* part, int64_t nt) {
+    extern __shared__ double2 smp[];
+    double2* tab = smp;                                                   // log table
+    double2* cbuf = smp + kLogTableSize * kLogTableCopies;                // [warps][64] xy
+    double* qbuf = reinterpret_cast<double*>(cbuf + kSymWarps * 64);     // [warps][64]
+    int4* rbuf = reinterpret_cast<int4*>(qbuf + kSymWarps * 64);         // [warps][kSymMaxRanges]
+    __shared__ __align__(8) uint64_t bar;
+    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    bulk_stage(cbuf, gtab, uint32_t(kLogTableSize) * 16u, &bar, 0);
+    log_table_to_smem(tab, cbuf);
+    pdl_trigger();
+    pdl_wait();
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t tab_lane = log_table_lane_addr(tab, lane & 7);
+    double2* cxy = cbuf + warp * 64;
+    double* cq = qbuf + warp * 64;
+    int4* rng = rbuf + warp * kSymMaxRanges;
+    for (;;) {
+        int k = 0;
+        if (lane == 0) k = atomicAdd(&ticket[1], 1);
+        const int64_t ti = __shfl_sync(0xffffffffu, k, 0);
+        if (ti >= ntask) break;
+        const SymTask T = tasks[ti];
+        __syncwarp();
+        if (lane < T.rcount) rng[lane] = ranges[T.rfirst + lane];
+        __syncwarp();
+        if (T.rows2) sym_task<2>(T, rng, sxy, q, cxy, cq, tab_lane, lane, part, nt);
+        else sym_task<1>(T, rng, sxy, q, cxy, cq, tab_lane, lane, part, nt);
+    }
+}
+
+// Per matched target: the slot partials in slot order, the coincidence
+// correction, the output scatter (out = near; L2P adds the far field).
+__global__ void __launch_bounds__(256)
+sym_finalize_kernel(const SymLeaf* leaves, int64_t nleaves, const double* part, int64_t nt,
+                    const double2* sxy, const double* q, const double2* txy, const int32_t* tids,
+                    const int32_t* coin_off, const int32_t* coin_src, const double2* gtab, double* out) {
+    extern __shared__ double2 smp[];
+    double2* tab = smp;
+    double2* tmp = smp + kLogTableSize * kLogTableCopies;
+    __shared__ __align__(8) uint64_t bar;
+    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    bulk_stage(tmp, gtab, uint32_t(kLogTableSize) * 16u, &bar, 0);
+    log_table_to_smem(tab, tmp);
+    pdl_trigger();
+    pdl_wait();
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const uint32_t tab_lane = log_table_lane_addr(tab, lane & 7);
+    const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (w >= nleaves) return;
+    const SymLeaf lf = leaves[w];
+    for (int k = lane; k < lf.n; k += 32) {
+        const int64_t t = int64_t(lf.tgt) + k;
+        double sum = 0.0;
+#pragma unroll
+        for (int s = 0; s < 9; ++s)
+            if (lf.mask >> s & 1) sum += part[int64_t(s) * nt + t];
+        const double2 tp = txy[t];
+        sum += coin_correction(coin_off, coin_src, t, tp.x, tp.y, sxy, q, tab_lane);
+        out[tids[t]] = -kInv4Pi * sum;
+    }
+}
+
 // ------------------------------------------------------ adaptive: M2P / P2L --
 // M2P (W lists of adaptive trees): a box's multipole evaluated directly at a
 // leaf's targets.  With a_0 = sum q and a_k = -(1/k) sum q w^k,
@@ -1189,7 +1377,7 @@ __global__ void gather_q(const double* q, const int32_t* ids, int64_t n, double*
                          int* ticket, int* pcount, int64_t nslots) {
     const int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
     if (e < 2) gbar[e] = 0u;
-    if (e == 0) ticket[0] = 0;
+    if (e < 2) ticket[e] = 0;
     for (int64_t i = e; i < nslots; i += int64_t(gridDim.x) * blockDim.x) pcount[i] = 0;
     if (e < n) qs[e] = q[ids[e]];
 }
@@ -1401,7 +1589,11 @@ void build_laplace_ops(Plan& pl) {
         pl.shift_grid = std::max(1, std::min(pu, pd)) * pl.sm_count;
     }
     smem_optin((const void*)l2p_p2p_kernel, kLogTableBytes + 32 * 1024);
+    smem_optin((const void*)p2p_sym_kernel, int(kSymSmem));
+    smem_optin((const void*)sym_finalize_kernel, kLogTableBytes + 16 * 1024);
     build_coincidences(pl);
+    pl.coin_ready = true;
+    if (!pl.adaptive) build_sym_near(pl, pl.shard_lb, pl.shard_le);
 }
 
 // ----------------------------------------------------------------- apply --
@@ -1419,7 +1611,8 @@ size_t laplace_work_bytes(const Plan& pl) {
            al256(sizeof(double) * size_t(std::max<int64_t>(pl.nt, 1))) + al256(sizeof(int) * 32) +
            al256(sizeof(double) * 64 * size_t(std::max<int64_t>(pl.n_p2p_parts, 1))) +
            al256(sizeof(int) * size_t(std::max<int64_t>(pl.n_p2p_heavy, 1))) +
-           al256(sizeof(double2) * n * size_t(pl.n_p2m_splits > 0 ? pl.n_p2m_items : 1));
+           al256(sizeof(double2) * n * size_t(pl.n_p2m_splits > 0 ? pl.n_p2m_items : 1)) +
+           (pl.sym ? al256(sizeof(double) * 9 * size_t(std::max<int64_t>(pl.nt, 1))) : 0);
 }
 
 LaplaceWork laplace_work_at(const Plan& pl, void* base) {
@@ -1439,6 +1632,8 @@ LaplaceWork laplace_work_at(const Plan& pl, void* base) {
     w.partial_p2p = reinterpret_cast<double*>(take(sizeof(double) * 64 * size_t(std::max<int64_t>(pl.n_p2p_parts, 1))));
     w.pcount = reinterpret_cast<int*>(take(sizeof(int) * size_t(std::max<int64_t>(pl.n_p2p_heavy, 1))));
     w.p2m_partial = reinterpret_cast<double2*>(take(sizeof(double2) * n * size_t(pl.n_p2m_splits > 0 ? pl.n_p2m_items : 1)));
+    w.sym_part = pl.sym ? reinterpret_cast<double*>(take(sizeof(double) * 9 * size_t(std::max<int64_t>(pl.nt, 1))))
+                        : nullptr;
     return w;
 }
 
@@ -1479,13 +1674,38 @@ void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const L
     unsigned* gbar = reinterpret_cast<unsigned*>(ticket) + 8;  // grid barriers of the shift passes
 
     auto near_field = [&](cudaStream_t s) {
-        if (pl.n_p2p_chunks == 0) return;
+        if (pl.sym) {
+            if (pl.n_sym_tasks > 0) {
+                int per_sm = 1;
+                VPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p2p_sym_kernel, kSymWarps * 32,
+                                                                       kSymSmem));
+                const int64_t want = (pl.n_sym_tasks + kSymWarps - 1) / kSymWarps;
+                const unsigned grid = unsigned(std::min<int64_t>(want, int64_t(pl.sm_count) * std::max(per_sm, 1)));
+                launch_pdl(p2p_sym_kernel, dim3(grid), dim3(kSymWarps * 32), kSymSmem, s,
+                           (const SymTask*)pl.sym_tasks.p, pl.n_sym_tasks, (const int4*)pl.sym_ranges.p,
+                           (const double2*)pl.src_sorted.p,
+                           (const double*)qs, log_table_dev(), ticket, w.sym_part, pl.nt);
+                ++launches;
+            }
+            if (pl.n_sym_leaves > 0) {
+                launch_pdl(sym_finalize_kernel, dim3(nblk(pl.n_sym_leaves * 32, 256)), dim3(256),
+                           size_t(kLogTableBytes) + 16 * 1024, s, (const SymLeaf*)pl.sym_leaves.p,
+                           pl.n_sym_leaves, (const double*)w.sym_part, pl.nt, (const double2*)pl.src_sorted.p,
+                           (const double*)qs, (const double2*)pl.tgt_sorted.p, (const int32_t*)pl.tgt_ids.p,
+                           (const int32_t*)pl.coin_off.p, (const int32_t*)pl.coin_src.p, log_table_dev(),
+                           out_dev);
+                ++launches;
+            }
+        }
+        const P2PChunk* nchunks = pl.sym ? pl.near_chunks.p : pl.p2p_chunks.p;
+        const int64_t nnear = pl.sym ? pl.n_near_chunks : pl.n_p2p_chunks;
+        if (nnear == 0) return;
         const size_t smem = size_t(kLogTableBytes) +
                             (sizeof(double2) + sizeof(double)) * kP2PBatch * kP2PWarps +
                             sizeof(int) * 2 * kMaxNearRanges * kP2PWarps;
         int per_sm = 1;
         VPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, l2p_p2p_kernel, kP2PWarps * 32, smem));
-        const int64_t want = (pl.n_p2p_chunks + kP2PWarps - 1) / kP2PWarps;
+        const int64_t want = (nnear + kP2PWarps - 1) / kP2PWarps;
         int64_t cap = int64_t(pl.sm_count) * std::max(per_sm, 1);
         static const int pct = [] {
             const char* v = std::getenv("VPG_P2P_SIDE_PCT");
@@ -1493,8 +1713,7 @@ void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const L
         }();
         if (s != st && pct > 0 && pct < 100) cap = std::max<int64_t>(1, cap * pct / 100);
         const unsigned grid = unsigned(std::min<int64_t>(want, cap));
-        launch_pdl(l2p_p2p_kernel, dim3(grid), dim3(kP2PWarps * 32), smem, s,
-                   (const P2PChunk*)pl.p2p_chunks.p, pl.n_p2p_chunks,
+        launch_pdl(l2p_p2p_kernel, dim3(grid), dim3(kP2PWarps * 32), smem, s, nchunks, nnear,
                    (const int2*)pl.near_ranges.p, (const double2*)pl.src_sorted.p, (const double*)qs,
                    (const double2*)pl.tgt_sorted.p, (const int32_t*)pl.tgt_ids.p, pl.coin_off.p,
                    pl.coin_src.p, log_table_dev(), ticket, partial_p2p, pcount, out_dev);

@@ -79,6 +79,36 @@ struct P2PChunk {
 };
 constexpr int kMaxNearRanges = 64;
 
+// Symmetric near field (uniform Laplace trees whose first ns targets are the
+// sources, the volume-potential case "targets = nodes"): every unordered pair
+// of near points is evaluated ONCE -- log r^2 feeds target i (with q_j) and
+// target j (with q_i).  A task is one leaf A (rows) against a flat column
+// list: A itself, then the neighbours B whose pair {A, B} A owns (the larger
+// leaf, ties to the smaller Morton id).  Row sums of A's targets go to slot
+// 4, column sums of B's targets to slot (dy+1)*3 + (dx+1) of B - A, so every
+// (target, slot) has one writer and the final per-target sum runs in a fixed
+// slot order (fmm.cu, p2p_sym_kernel / sym_finalize_kernel).
+struct SymTask {
+    int32_t a_src, a_tgt, na;  // rows: the sources of leaf A = its first na targets
+    int32_t ncol;              // flat columns: [0, na) = A itself, then the owned neighbours
+    int32_t rfirst, rcount;    // column ranges sym_ranges[rfirst, +rcount), the first is A
+    int32_t rows2;             // 1: two rows per lane (64-row tiles), 0: one (32-row tiles)
+    int32_t pad;
+};
+struct SymRange {
+    int32_t b_src, b_tgt, coff, slot;  // sorted source / target of the range, flat offset, slot
+};
+struct SymLeaf {
+    int32_t tgt, n;  // first matched target (sorted) and count
+    int32_t mask;    // slots written for this leaf's targets
+    int32_t pad;
+};
+constexpr int kSymMaxN = 512;     // largest leaf (sources) the symmetric path takes
+constexpr int kSymMaxRanges = 9;
+struct LeafNear {  // per-leaf near-field data of the last schedule (host)
+    int32_t leaf, t0, t1, rfirst, rcount, rself, lfirst, lcount;
+};
+
 // One captured apply (CUDA graph) with its own persistent workspace, keyed
 // by the device pointers it was captured for (host-pointer applies use the
 // entry's staging buffers).  `done` orders successive uses of the entry.
@@ -159,6 +189,17 @@ struct Plan {
     // Laplace near field: (target, own-leaf source) pairs with r^2 zero or
     // subnormal, CSR over sorted targets (fmm.cu, build_coincidences)
     DBuf<int32_t> coin_off, coin_src;
+    bool coin_ready = false;
+    // symmetric near field (see SymTask); near_chunks then holds the chunks
+    // of the unmatched targets only (p2p_chunks keeps every target for L2P)
+    bool matched = false;  // tgt[0, ns) == src bitwise (set at plan creation)
+    bool sym = false;
+    DBuf<SymTask> sym_tasks;
+    DBuf<SymRange> sym_ranges;
+    DBuf<SymLeaf> sym_leaves;
+    DBuf<P2PChunk> near_chunks;
+    int64_t n_sym_tasks = 0, n_sym_leaves = 0, n_near_chunks = 0;
+    std::vector<LeafNear> h_leafnear;
     int64_t n_p2p_chunks = 0;
     int64_t n_p2p_heavy = 0;  // split chunks (counters)
     int64_t n_p2p_parts = 0;  // partial-sum rows of the split chunks
@@ -273,6 +314,7 @@ struct Plan {
 void build_tree(Plan& pl);
 void build_schedules(Plan& pl, int64_t leaf_begin, int64_t leaf_end);
 void schedule_near_chunks(Plan& pl, std::vector<P2PChunk>& chunks);
+void build_sym_near(Plan& pl, int64_t leaf_begin, int64_t leaf_end);
 void choose_passes(Plan& pl);
 // adaptive.cu
 void build_adaptive(Plan& pl, cudaStream_t st);
@@ -288,6 +330,7 @@ struct LaplaceWork {
     double* partial_p2p;
     int* pcount;
     double2* p2m_partial;
+    double* sym_part;  // [9][nt] slot partials of the symmetric near field
 };
 size_t laplace_work_bytes(const Plan& pl);
 LaplaceWork laplace_work_at(const Plan& pl, void* base);

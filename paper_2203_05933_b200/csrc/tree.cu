@@ -618,6 +618,7 @@ void build_schedules(Plan& pl, int64_t lb, int64_t le) {
         std::vector<int2> ranges;
         std::vector<int32_t> lrows;
         pl.p2p_pairs = 0;
+        pl.h_leafnear.clear();
         for (int64_t b = lb; b < le; ++b) {
             const int32_t t0 = h_toff[size_t(b)], t1 = h_toff[size_t(b) + 1];
             if (t1 == t0) continue;
@@ -644,6 +645,7 @@ void build_schedules(Plan& pl, int64_t lb, int64_t le) {
                 }
             const int32_t rcount = int32_t(ranges.size()) - rfirst;
             pl.p2p_pairs += int64_t(t1 - t0) * nsrc;
+            pl.h_leafnear.push_back(LeafNear{int32_t(b), t0, t1, rfirst, rcount, rself, lfirst, lcount});
             for (int32_t t = t0; t < t1; t += chunk)
                 chunks.push_back(P2PChunk{t, std::min(chunk, t1 - t), int32_t(std::min<int64_t>(nsrc, INT32_MAX)),
                                           rfirst, rcount, rself, lfirst, lcount, 0, 1, -1, -1});
@@ -663,6 +665,114 @@ void build_schedules(Plan& pl, int64_t lb, int64_t le) {
         }
         pl.shard_m2l = m2l;
     }
+    if (pl.coin_ready) build_sym_near(pl, lb, le);
+}
+
+// The symmetric near-field schedule (SymTask, plan.cuh) for the targets of
+// the leaf range [lb, le): every pair {A, B} of near leaves (B >= A, 3x3
+// neighbourhood, both with sources) touching the range, the per-leaf slot
+// masks for the final sums, and one-sided chunks for the unmatched targets
+// (those beyond a leaf's first n_src targets).  Taken when the first ns
+// targets are the sources (so leaf A's first n_src sorted targets are its
+// sorted sources, both sorts being stable), the tree is uniform, the
+// kernel Laplace and no leaf holds more than kSymMaxN sources.
+void build_sym_near(Plan& pl, int64_t lb, int64_t le) {
+    pl.sym = false;
+    static const int force = [] {  // VPG_SYM=0: never, 1: always (when applicable), else by cost
+        const char* v = std::getenv("VPG_SYM");
+        return v ? std::atoi(v) : -1;
+    }();
+    if (force == 0 || !pl.matched || pl.adaptive || pl.direct || pl.family != VPG_LAPLACE) return;
+    const int L = pl.L;
+    const int nb = 1 << L;
+    const int64_t nleaf = int64_t(1) << (2 * L);
+    const std::vector<int32_t>& so = pl.h_soff;
+    const std::vector<int32_t>& to = pl.h_toff;
+    for (int64_t b = 0; b < nleaf; ++b)
+        if (so[size_t(b) + 1] - so[size_t(b)] > kSymMaxN) return;
+    auto in = [&](int64_t b) { return b >= lb && b < le; };
+    auto nsrc = [&](int64_t b) { return so[size_t(b) + 1] - so[size_t(b)]; };
+    // the owner of {A, B}: the larger leaf, ties to the smaller Morton id
+    auto owns = [&](int64_t a, int64_t b) {
+        const int32_t x = nsrc(a), y = nsrc(b);
+        return x > y || (x == y && a < b);
+    };
+    std::vector<SymTask> tasks;
+    std::vector<SymRange> ranges;
+    std::vector<SymLeaf> leaves;
+    double cost_sym = 0.0, cost_one = 0.0;  // modelled warp instructions (sym block vs one-sided pairs)
+    for (int64_t a = 0; a < nleaf; ++a) {
+        const int32_t na = nsrc(a);
+        if (!na) continue;
+        const int ax = int(squash2(uint32_t(a))), ay = int(squash2(uint32_t(a) >> 1));
+        int mask = 1 << 4;
+        std::vector<SymRange> mine{SymRange{so[size_t(a)], to[size_t(a)], 0, 4}};
+        int32_t ncol = na;
+        bool touches = in(a);
+        for (int dy = -1; dy <= 1; ++dy)
+            for (int dx = -1; dx <= 1; ++dx) {
+                const int bx = ax + dx, by = ay + dy;
+                if ((dx == 0 && dy == 0) || bx < 0 || by < 0 || bx >= nb || by >= nb) continue;
+                const int64_t bb = mort(uint32_t(bx), uint32_t(by));
+                if (!nsrc(bb)) continue;
+                if (!owns(a, bb)) {
+                    mask |= 1 << ((-dy + 1) * 3 + (-dx + 1));  // written by bb's task
+                    continue;
+                }
+                mine.push_back(SymRange{so[size_t(bb)], to[size_t(bb)], ncol, (dy + 1) * 3 + (dx + 1)});
+                ncol += nsrc(bb);
+                touches = touches || in(bb);
+                cost_one += 2.0 * double(na) * nsrc(bb) * 31.0 / 32.0;
+            }
+        cost_one += double(na) * na * 31.0 / 32.0;
+        if (in(a)) leaves.push_back(SymLeaf{to[size_t(a)], na, mask, 0});
+        if (!touches) continue;
+        const int rows2 = na > 32 ? 1 : 0;
+        const int rt = (na + (rows2 ? 63 : 31)) / (rows2 ? 64 : 32);
+        const int ct = (ncol + 31) / 32;
+        cost_sym += double(rt) * ct * 32.0 * (rows2 ? 56.0 : 31.0) + 200.0;
+        tasks.push_back(SymTask{so[size_t(a)], to[size_t(a)], na, ncol, int32_t(ranges.size()), int32_t(mine.size()),
+                                rows2, 0});
+        ranges.insert(ranges.end(), mine.begin(), mine.end());
+    }
+    // a task runs on one warp: it must not outlast the fair share of the
+    // whole-GPU work by much (a few huge leaves next to many small ones)
+    int64_t max_task = 0;
+    double total = 0.0;
+    for (const SymTask& t : tasks) {
+        max_task = std::max<int64_t>(max_task, int64_t(t.na) * t.ncol);
+        total += double(t.na) * t.ncol;
+    }
+    const double fair = total / (double(pl.sm_count) * 16.0);
+    if (force != 1 && !(cost_sym < 0.85 * cost_one && double(max_task) <= 2.0 * fair)) return;
+    auto cost = [](const SymTask& t) { return int64_t(t.na) * t.ncol; };
+    std::stable_sort(tasks.begin(), tasks.end(),
+                     [&](const SymTask& x, const SymTask& y) { return cost(x) > cost(y); });
+    // unmatched targets: one-sided chunks (<= 64 targets, never split)
+    std::vector<P2PChunk> extra;
+    for (const LeafNear& ln : pl.h_leafnear) {
+        const int32_t nsrc = so[size_t(ln.leaf) + 1] - so[size_t(ln.leaf)];
+        int64_t near_src = 0;
+        for (int dy = -1; dy <= 1; ++dy)
+            for (int dx = -1; dx <= 1; ++dx) {
+                const int bx = int(squash2(uint32_t(ln.leaf))) + dx, by = int(squash2(uint32_t(ln.leaf) >> 1)) + dy;
+                if (bx < 0 || by < 0 || bx >= nb || by >= nb) continue;
+                const int64_t bb = mort(uint32_t(bx), uint32_t(by));
+                near_src += so[size_t(bb) + 1] - so[size_t(bb)];
+            }
+        for (int32_t t = ln.t0 + nsrc; t < ln.t1; t += 64)
+            extra.push_back(P2PChunk{t, std::min(64, ln.t1 - t), int32_t(std::min<int64_t>(near_src, INT32_MAX)),
+                                     ln.rfirst, ln.rcount, ln.rself, ln.lfirst, ln.lcount, 0, 1, -1, -1});
+    }
+    cudaStream_t st = 0;
+    to_device(pl.sym_tasks, tasks, st);
+    to_device(pl.sym_ranges, ranges, st);
+    to_device(pl.sym_leaves, leaves, st);
+    to_device(pl.near_chunks, extra, st);
+    pl.n_sym_tasks = int64_t(tasks.size());
+    pl.n_sym_leaves = int64_t(leaves.size());
+    pl.n_near_chunks = int64_t(extra.size());
+    pl.sym = true;
 }
 
 }  // namespace vpg
