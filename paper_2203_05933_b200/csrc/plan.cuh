@@ -194,6 +194,7 @@ struct Plan {
     // of the unmatched targets only (p2p_chunks keeps every target for L2P)
     bool matched = false;  // tgt[0, ns) == src bitwise (set at plan creation)
     bool sym = false;
+    bool sym_auto = false;  // the cost model's choice for the whole tree
     DBuf<SymTask> sym_tasks;
     DBuf<SymRange> sym_ranges;
     DBuf<SymLeaf> sym_leaves;

@@ -678,10 +678,8 @@ void build_schedules(Plan& pl, int64_t lb, int64_t le) {
 // kernel Laplace and no leaf holds more than kSymMaxN sources.
 void build_sym_near(Plan& pl, int64_t lb, int64_t le) {
     pl.sym = false;
-    static const int force = [] {  // VPG_SYM=0: never, 1: always (when applicable), else by cost
-        const char* v = std::getenv("VPG_SYM");
-        return v ? std::atoi(v) : -1;
-    }();
+    const char* fv = std::getenv("VPG_SYM");  // 0: never, 1: always (when applicable), unset: by cost
+    const int force = fv ? std::atoi(fv) : -1;
     if (force == 0 || !pl.matched || pl.adaptive || pl.direct || pl.family != VPG_LAPLACE) return;
     const int L = pl.L;
     const int nb = 1 << L;
@@ -744,7 +742,10 @@ void build_sym_near(Plan& pl, int64_t lb, int64_t le) {
         total += double(t.na) * t.ncol;
     }
     const double fair = total / (double(pl.sm_count) * 16.0);
-    if (force != 1 && !(cost_sym < 0.85 * cost_one && double(max_task) <= 2.0 * fair)) return;
+    // decided once on the whole tree; shards follow it (their results must
+    // assemble bit-exactly to the single-GPU ones)
+    if (lb == 0 && le == nleaf) pl.sym_auto = cost_sym < 0.85 * cost_one && double(max_task) <= 2.0 * fair;
+    if (force != 1 && !pl.sym_auto) return;
     auto cost = [](const SymTask& t) { return int64_t(t.na) * t.ncol; };
     std::stable_sort(tasks.begin(), tasks.end(),
                      [&](const SymTask& x, const SymTask& y) { return cost(x) > cost(y); });

@@ -279,3 +279,43 @@ def test_near_field_zero_and_subnormal_pairs(vp, rest, mode):
     assert rel_l2(gpu, cpu) <= 1e-12
     # the three targets at the origin carry log(r^2) ~ -737 terms
     assert np.allclose(gpu[400:403], cpu[400:403], rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("sym", ["0", "1"])
+def test_symmetric_near_field(vp, rest, monkeypatch, sym):
+    """'Targets = nodes' plans may evaluate each unordered near pair once
+    (plan.cuh SymTask).  Forced on and off, cfg2 (nodes + 10,000 unmatched
+    targets) matches the oracle, and shards still assemble bit-exactly."""
+    from paper_2203_05933_b200 import multigpu
+    monkeypatch.setenv("VPG_SYM", sym)
+    w = W.cfg2()
+    with vp.SummationPlan(lap(vp), w.src, w.tgt, 1e-12) as plan:
+        gpu = plan.apply(w.q)
+        total = np.zeros_like(gpu)
+        for r in range(3):
+            multigpu.shard_plan(plan, r, 3)
+            total += plan.apply(w.q)
+        plan.set_shard(0, 4 ** plan.levels())
+        assert np.array_equal(total, gpu)
+        assert np.array_equal(plan.apply(w.q), gpu)
+    cpu = rest.plan_sum(0, 0.0, w.src, w.q, w.tgt, 1e-12)
+    assert rel_l2(gpu, cpu) <= 1e-13
+
+
+@pytest.mark.parametrize("sym", ["0", "1"])
+def test_symmetric_near_field_duplicates_and_subnormal(vp, rest, monkeypatch, sym):
+    """Coincident distinct sources and subnormal r^2 with targets = sources
+    (+ extras): the symmetric path feeds each pair to both targets and the
+    coincidence list undoes exactly what the hot loop added."""
+    monkeypatch.setenv("VPG_SYM", sym)
+    rng = np.random.default_rng(43)
+    base = rng.uniform(-1, 1, (30_000, 2))
+    src = np.concatenate([base, base[:500], [[0.0, 0.0], [0.0, 3e-160], [1e-160, 0.0]]])
+    tgt = np.concatenate([src, rng.uniform(-1, 1, (2000, 2)), [[-2e-161, 1e-161]]])
+    q = rng.standard_normal(len(src))
+    with vp.SummationPlan(lap(vp), src, tgt, 1e-12) as plan:
+        gpu = plan.apply(q)
+    cpu = rest.plan_sum(0, 0.0, src, q, tgt, 1e-12)
+    assert rel_l2(gpu, cpu) <= 1e-12
+    n = len(src)
+    assert np.allclose(gpu[n - 3:n], cpu[n - 3:n], rtol=1e-12, atol=0)
