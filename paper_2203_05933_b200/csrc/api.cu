@@ -229,8 +229,19 @@ GraphEntry* graph_entry(const Plan& pl, const double* q, double* out, bool host)
     double* od = host ? e->ostage : out;
     cudaStream_t cap = nullptr, side = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
-    VPG_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
-    VPG_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    static const bool prio = [] {  // VPG_PRIO=0: equal priorities (A/B)
+        const char* v = std::getenv("VPG_PRIO");
+        return !(v && v[0] == '0');
+    }();
+    if (prio) {  // far-field chain ahead of the side-stream near field (cfg2: -3%)
+        int lo = 0, hi = 0;
+        VPG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        VPG_CUDA(cudaStreamCreateWithPriority(&cap, cudaStreamNonBlocking, hi));
+        VPG_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, lo));
+    } else {
+        VPG_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+        VPG_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    }
     VPG_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
     VPG_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
     struct StreamGuard {
@@ -261,7 +272,7 @@ GraphEntry* graph_entry(const Plan& pl, const double* q, double* out, bool host)
         return nullptr;
     }
     VPG_CUDA(cudaStreamEndCapture(cap, &g));
-    const cudaError_t ie = cudaGraphInstantiate(&e->exec, g, 0);
+    const cudaError_t ie = cudaGraphInstantiate(&e->exec, g, prio ? cudaGraphInstantiateFlagUseNodePriority : 0);
     cudaGraphDestroy(g);
     if (ie != cudaSuccess) {
         (void)cudaGetLastError();

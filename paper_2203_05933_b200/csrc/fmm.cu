@@ -932,7 +932,7 @@ __global__ void __launch_bounds__(kP2PWarps * 32, kP2PMinBlocks)
 l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, const int2* ranges,
                const double2* sxy, const double* q, const double2* txy,
                const int32_t* tids, const int32_t* coin_off, const int32_t* coin_src,
-               const double2* gtab, int* ticket, double* partial, int* pcount, double* out) {
+               const double2* gtab, int* ticket, double* partial, int* pcount, double* out, int quota) {
     extern __shared__ double2 smp[];
     double2* tab = smp;                                                  // log table
     double2* sbuf = smp + kLogTableSize * kLogTableCopies;               // [warps][batch] xy
@@ -955,7 +955,7 @@ l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, const int2* ranges,
     int* pre_s = rbuf + warp * 2 * kMaxNearRanges;
     int* st_s = pre_s + kMaxNearRanges;
 
-    for (;;) {
+    for (int done = 0; done < quota; ++done) {  // quota: tasks per warp before the CTA retires
         int k = 0;
         if (lane == 0) k = atomicAdd(&ticket[0], 1);
         const int64_t ch = __shfl_sync(0xffffffffu, k, 0);
@@ -1712,11 +1712,17 @@ void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const L
             return v ? std::atoi(v) : 100;
         }();
         if (s != st && pct > 0 && pct < 100) cap = std::max<int64_t>(1, cap * pct / 100);
-        const unsigned grid = unsigned(std::min<int64_t>(want, cap));
+        static const int quota = [] {
+            const char* v = std::getenv("VPG_P2P_QUOTA");
+            return v ? std::max(1, std::atoi(v)) : 0;
+        }();
+        unsigned grid = unsigned(std::min<int64_t>(want, cap));
+        if (quota > 0 && s != st) grid = unsigned(std::max<int64_t>(1, (want + quota - 1) / quota));
         launch_pdl(l2p_p2p_kernel, dim3(grid), dim3(kP2PWarps * 32), smem, s, nchunks, nnear,
                    (const int2*)pl.near_ranges.p, (const double2*)pl.src_sorted.p, (const double*)qs,
                    (const double2*)pl.tgt_sorted.p, (const int32_t*)pl.tgt_ids.p, pl.coin_off.p,
-                   pl.coin_src.p, log_table_dev(), ticket, partial_p2p, pcount, out_dev);
+                   pl.coin_src.p, log_table_dev(), ticket, partial_p2p, pcount, out_dev,
+                   (quota > 0 && s != st) ? quota : INT32_MAX);
         ++launches;
     };
 
