@@ -374,7 +374,8 @@ def run_gpu(args):
         dom = "m2l" if phases["m2l"] >= phases["p2p"] else "p2p"
         flops = m2l_flops if dom == "m2l" else p2p_flops
         achieved = flops / (phases[dom] * 1e-3) / 1e12
-        kname = "m2l_kernel" if dom == "m2l" else "l2p_p2p_kernel"
+        near_k = "p2p_sym_kernel" if info.get("near_symmetric") else "l2p_p2p_kernel"
+        kname = "m2l_kernel" if dom == "m2l" else near_k
         bound = "tensor" if dom == "m2l" else "fp64"
         peak = fp64_peak_tflops(bound)
         roofline = {"bound": bound, "kernel": kname,
@@ -386,7 +387,10 @@ def run_gpu(args):
                     "bound_note": ("M2L runs on the FP64 tensor cores (mma.sync m8n8k4 f64)" if bound == "tensor"
                                    else "the near-field log sum is FP64 CUDA-core work (no tensor-core form)"),
                     "flops_per_unit": ("4P(P+1)+8(P+1)+6P executed per M2L pair" if dom == "m2l"
-                                       else "27 per near-field pair (SURVEY.md 8d convention)")}
+                                       else "27 per near-field pair (SURVEY.md 8d convention)"
+                                       + ("; the symmetric kernel evaluates each unordered pair once, so the "
+                                          "algorithmic rate counts both ordered pairs" if near_k == "p2p_sym_kernel"
+                                          else ""))}
     else:
         dom = "p2p"
         roofline = {"bound": "fp64", "kernel": "traverse_kernel" if wl.kernel == "helmholtz" else "allpairs_kernel",

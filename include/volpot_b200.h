@@ -98,6 +98,8 @@ typedef struct {
     int64_t p2p_pairs;       /* enumerated near-field pairs, self included */
     int64_t m2m_children, l2l_children;
     int64_t device_bytes;    /* resident plan footprint */
+    int32_t near_symmetric;  /* 1: near field by unordered pairs (fmm.cu p2p_sym_kernel) */
+    int32_t reserved;
 } vpg_plan_info_t;
 
 /* Phase timings of the most recent apply on a plan with profiling on, in
