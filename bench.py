@@ -372,6 +372,11 @@ def run_gpu(args):
                              "pairs_per_s": info["p2p_pairs"] / (phases["p2p"] * 1e-3) if phases["p2p"] else None,
                              "tflops_27": p2p_flops / (phases["p2p"] * 1e-3) / 1e12 if phases["p2p"] else None}
         dom = "m2l" if phases["m2l"] >= phases["p2p"] else "p2p"
+        if info.get("near_symmetric"):
+            # the symmetric kernel evaluates each unordered pair once: 27 flops
+            # for the pair plus 2 for the second accumulation, per 2 ordered pairs
+            p2p_flops = info["p2p_pairs"] / 2.0 * 29.0
+            kern_stats["p2p"]["tflops_executed_sym"] = p2p_flops / (phases["p2p"] * 1e-3) / 1e12 if phases["p2p"] else None
         flops = m2l_flops if dom == "m2l" else p2p_flops
         achieved = flops / (phases[dom] * 1e-3) / 1e12
         near_k = "p2p_sym_kernel" if info.get("near_symmetric") else "l2p_p2p_kernel"
@@ -388,9 +393,9 @@ def run_gpu(args):
                                    else "the near-field log sum is FP64 CUDA-core work (no tensor-core form)"),
                     "flops_per_unit": ("4P(P+1)+8(P+1)+6P executed per M2L pair" if dom == "m2l"
                                        else "27 per near-field pair (SURVEY.md 8d convention)"
-                                       + ("; the symmetric kernel evaluates each unordered pair once, so the "
-                                          "algorithmic rate counts both ordered pairs" if near_k == "p2p_sym_kernel"
-                                          else ""))}
+                                       if near_k != "p2p_sym_kernel" else
+                                       "29 per unordered near-field pair (27 per pair, SURVEY.md 8d, + 2 for the "
+                                       "second target's accumulation; ordered pairs / 2)")}
     else:
         dom = "p2p"
         roofline = {"bound": "fp64", "kernel": "traverse_kernel" if wl.kernel == "helmholtz" else "allpairs_kernel",
