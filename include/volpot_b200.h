@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define VPG_ABI_VERSION 1
+#define VPG_ABI_VERSION 2  /* 2: vpg_plan_info_t.near_symmetric, vpg_layer_* */
 
 typedef enum {
     VPG_OK = 0,

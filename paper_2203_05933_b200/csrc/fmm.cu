@@ -1053,7 +1053,7 @@ l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, const int2* ranges,
 // have j >= na > i).  Row sums are added to slot 4 of A's targets at the end
 // of each row tile, after the self-column sums of the earlier tiles.
 constexpr int kSymWarps = 8;
-constexpr size_t kSymSmem = size_t(kLogTableBytes) + size_t(kSymWarps) * (64 * 16 + 64 * 8 + kSymMaxRanges * 16);
+constexpr size_t kSymSmem = size_t(kLogTableBytes) + size_t(kSymWarps) * (64 * 16 + 64 * 8 + kSymMaxRanges * sizeof(SymRange));
 
 template <int R, bool kDiag>
 __device__ __forceinline__ void sym_block(const double2* cxy, const double* cq, int lane, int i0, int j0,
@@ -1085,41 +1085,53 @@ __device__ __forceinline__ void sym_block(const double2* cxy, const double* cq, 
 }
 
 // flat column j -> (range index) by a linear scan of the task's ranges
-__device__ __forceinline__ int sym_range_of(const int4* rng, int rcount, int j) {
+__device__ __forceinline__ int sym_range_of(const SymRange* rng, int rcount, int j) {
     int r = 0;
     for (int k = 1; k < rcount; ++k)
-        if (rng[k].z <= j) r = k;
+        if (rng[k].coff <= j) r = k;
     return r;
 }
 
+// One subtask: rows [r0, r1) of A (tiles of 32 R) x flat columns [c0, c1).
+// A column's partial is stored by the group's first row tile and updated by
+// the later ones (same lane: j mod 32); self columns below the group are
+// never visited, their slot gets a zero.  Row partials are stored per tile.
 template <int R>
-__device__ __forceinline__ void sym_task(const SymTask& T, const int4* rng, const double2* sxy, const double* q,
-                                         double2* cxy, double* cq, uint32_t tab_lane, int lane, double* part,
-                                         int64_t nt) {
+__device__ __forceinline__ void sym_task(const SymTask& T, const SymRange* rng, const double2* sxy,
+                                         const double* q, double2* cxy, double* cq, uint32_t tab_lane, int lane,
+                                         double* part) {
     constexpr double kFar = 1e100;
-    const int nct = (T.ncol + 31) >> 5;
-    for (int r0 = 0; r0 < T.na; r0 += 32 * R) {
+    const int ct_end = (T.c1 + 31) >> 5;
+    for (int ct = T.c0 >> 5; ct < min(ct_end, T.r0 >> 5); ++ct) {
+        const int j = ct * 32 + lane;
+        if (j < T.c1) {
+            const SymRange& g = rng[sym_range_of(rng, T.rcount, j)];
+            part[g.b_part + int64_t(T.rg) * g.nb + (j - g.coff)] = 0.0;
+        }
+    }
+    for (int r0 = T.r0; r0 < T.r1; r0 += 32 * R) {
         double rx[2] = {kFar, kFar}, ry[2] = {kFar, kFar}, rq[2] = {0.0, 0.0}, racc[2] = {0.0, 0.0};
 #pragma unroll
         for (int u = 0; u < R; ++u) {
             const int i = r0 + lane + 32 * u;
-            if (i < T.na) {
+            if (i < T.r1) {
                 const double2 p = sxy[T.a_src + i];
                 rx[u] = p.x;
                 ry[u] = p.y;
                 rq[u] = q[T.a_src + i];
             }
         }
-        // column tiles wholly below the row tile (self part) are skipped
-        for (int ct = r0 >> 5; ct < nct; ++ct) {
+        const bool first = r0 == T.r0;
+        for (int ct = max(T.c0 >> 5, r0 >> 5); ct < ct_end; ++ct) {
             const int j = ct * 32 + lane;
-            int4 rg = make_int4(0, 0, 0, 0);
             double2 p = make_double2(-kFar, -kFar);
             double qj = 0.0;
-            if (j < T.ncol) {
-                rg = rng[sym_range_of(rng, T.rcount, j)];
-                p = sxy[rg.x + (j - rg.z)];
-                qj = q[rg.x + (j - rg.z)];
+            int64_t dst = -1;
+            if (j < T.c1) {
+                const SymRange& g = rng[sym_range_of(rng, T.rcount, j)];
+                p = sxy[g.b_src + (j - g.coff)];
+                qj = q[g.b_src + (j - g.coff)];
+                dst = g.b_part + int64_t(T.rg) * g.nb + (j - g.coff);
             }
             __syncwarp();
             cxy[lane] = p;
@@ -1132,34 +1144,24 @@ __device__ __forceinline__ void sym_task(const SymTask& T, const int4* rng, cons
                 sym_block<R, true>(cxy, cq, lane, r0, ct * 32, rx, ry, rq, tab_lane, racc, cacc);
             else
                 sym_block<R, false>(cxy, cq, lane, r0, ct * 32, rx, ry, rq, tab_lane, racc, cacc);
-            if (j < T.ncol) {
-                double* dst = part + int64_t(rg.w) * nt + rg.y + (j - rg.z);
-                // row tile 0 is the first to touch every column (neighbour
-                // columns are in every tile's range, self column j from 0 on)
-                __stcg(dst, (r0 == 0 ? 0.0 : __ldcg(dst)) + cacc);
-            }
+            if (dst >= 0) part[dst] = first ? cacc : part[dst] + cacc;
         }
-        __syncwarp();
 #pragma unroll
         for (int u = 0; u < R; ++u) {
             const int i = r0 + lane + 32 * u;
-            if (i < T.na) {
-                double* dst = part + int64_t(4) * nt + T.a_tgt + i;
-                __stcg(dst, __ldcg(dst) + racc[u]);
-            }
+            if (i < T.r1) part[T.a_part + i] = racc[u];
         }
-        __syncwarp();
     }
 }
 
 __global__ void __launch_bounds__(kSymWarps * 32, 2)
-p2p_sym_kernel(const SymTask* tasks, int64_t ntask, const int4* ranges, const double2* sxy, const double* q,
-               const double2* gtab, int* ticket, double* part, int64_t nt) {
+p2p_sym_kernel(const SymTask* tasks, int64_t ntask, const SymRange* ranges, const double2* sxy, const double* q,
+               const double2* gtab, int* ticket, double* part) {
     extern __shared__ double2 smp[];
     double2* tab = smp;                                                   // log table
     double2* cbuf = smp + kLogTableSize * kLogTableCopies;                // [warps][64] xy
     double* qbuf = reinterpret_cast<double*>(cbuf + kSymWarps * 64);     // [warps][64]
-    int4* rbuf = reinterpret_cast<int4*>(qbuf + kSymWarps * 64);         // [warps][kSymMaxRanges]
+    SymRange* rbuf = reinterpret_cast<SymRange*>(qbuf + kSymWarps * 64);  // [warps][kSymMaxRanges]
     __shared__ __align__(8) uint64_t bar;
     if (threadIdx.x == 0) mbar_init(&bar, 1);
     __syncthreads();
@@ -1172,7 +1174,7 @@ p2p_sym_kernel(const SymTask* tasks, int64_t ntask, const int4* ranges, const do
     const uint32_t tab_lane = log_table_lane_addr(tab, lane & 7);
     double2* cxy = cbuf + warp * 64;
     double* cq = qbuf + warp * 64;
-    int4* rng = rbuf + warp * kSymMaxRanges;
+    SymRange* rng = rbuf + warp * kSymMaxRanges;
     for (;;) {
         int k = 0;
         if (lane == 0) k = atomicAdd(&ticket[1], 1);
@@ -1182,42 +1184,74 @@ p2p_sym_kernel(const SymTask* tasks, int64_t ntask, const int4* ranges, const do
         __syncwarp();
         if (lane < T.rcount) rng[lane] = ranges[T.rfirst + lane];
         __syncwarp();
-        if (T.rows2) sym_task<2>(T, rng, sxy, q, cxy, cq, tab_lane, lane, part, nt);
-        else sym_task<1>(T, rng, sxy, q, cxy, cq, tab_lane, lane, part, nt);
+        if (T.rows2) sym_task<2>(T, rng, sxy, q, cxy, cq, tab_lane, lane, part);
+        else sym_task<1>(T, rng, sxy, q, cxy, cq, tab_lane, lane, part);
     }
 }
 
-// Per matched target: the slot partials in slot order, the coincidence
-// correction, the output scatter (out = near; L2P adds the far field).
-__global__ void __launch_bounds__(256)
-sym_finalize_kernel(const SymLeaf* leaves, int64_t nleaves, const double* part, int64_t nt,
+// Per leaf (warp per leaf, persistent grid): matched targets add the leaf's
+// slot partials in slot order plus the coincidence correction; unmatched
+// targets sum their 3x3 near sources one-sided (lanes stride the flattened
+// list, butterfly reduction); then the output scatter (out = near; L2P adds
+// the far field).
+constexpr int kFinWarps = 8;
+constexpr size_t kFinScratch = size_t(kFinWarps) * 2 * kMaxNearRanges * sizeof(int) > size_t(kLogTableSize) * 16
+                                   ? size_t(kFinWarps) * 2 * kMaxNearRanges * sizeof(int)
+                                   : size_t(kLogTableSize) * 16;  // range slots, or the table's staging copy
+constexpr size_t kFinSmem = size_t(kLogTableBytes) + kFinScratch;
+__global__ void __launch_bounds__(kFinWarps * 32)
+sym_finalize_kernel(const SymLeaf* leaves, int64_t nleaves, const double* part, const int2* ranges,
                     const double2* sxy, const double* q, const double2* txy, const int32_t* tids,
                     const int32_t* coin_off, const int32_t* coin_src, const double2* gtab, double* out) {
     extern __shared__ double2 smp[];
     double2* tab = smp;
-    double2* tmp = smp + kLogTableSize * kLogTableCopies;
+    int* rbuf = reinterpret_cast<int*>(smp + kLogTableSize * kLogTableCopies);  // [warps][2][64]
     __shared__ __align__(8) uint64_t bar;
     if (threadIdx.x == 0) mbar_init(&bar, 1);
     __syncthreads();
-    bulk_stage(tmp, gtab, uint32_t(kLogTableSize) * 16u, &bar, 0);
-    log_table_to_smem(tab, tmp);
+    bulk_stage(rbuf, gtab, uint32_t(kLogTableSize) * 16u, &bar, 0);
+    log_table_to_smem(tab, reinterpret_cast<const double2*>(rbuf));
     pdl_trigger();
     pdl_wait();
     __syncthreads();
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t tab_lane = log_table_lane_addr(tab, lane & 7);
-    const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    if (w >= nleaves) return;
-    const SymLeaf lf = leaves[w];
-    for (int k = lane; k < lf.n; k += 32) {
-        const int64_t t = int64_t(lf.tgt) + k;
-        double sum = 0.0;
+    int* pre_s = rbuf + warp * 2 * kMaxNearRanges;
+    int* st_s = pre_s + kMaxNearRanges;
+    for (int64_t w = int64_t(blockIdx.x) * kFinWarps + warp; w < nleaves; w += int64_t(gridDim.x) * kFinWarps) {
+        const SymLeaf lf = leaves[w];
+        for (int k = lane; k < lf.n; k += 32) {
+            const int64_t t = int64_t(lf.tgt) + k;
+            const double* pk = part + lf.pbase + k;
+            double sum = 0.0;
+            for (int sl = 0; sl < lf.nslot; ++sl) sum += pk[int64_t(sl) * lf.n];
+            const double2 tp = txy[t];
+            sum += coin_correction(coin_off, coin_src, t, tp.x, tp.y, sxy, q, tab_lane);
+            out[tids[t]] = -kInv4Pi * sum;
+        }
+        if (lf.tgt + lf.n >= lf.t1) continue;
+        const NearList nl = near_list(ranges, lf.rfirst, lf.rcount, 0, lane, pre_s, st_s);
+        for (int t = lf.tgt + lf.n; t < lf.t1; ++t) {
+            const double2 tp = txy[t];
+            LapAcc acc;
+            for (int ff = lane; ff < nl.total; ff += 32) {
+                int lo = 0, hi = nl.nr - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (nl.pre[mid] <= ff) lo = mid; else hi = mid - 1;
+                }
+                const int src = nl.st[lo] + (ff - nl.pre[lo]);
+                const double2 sp = sxy[src];
+                lap_pair_fast(tp.x, tp.y, sp.x, sp.y, q[src], tab_lane, acc);
+            }
+            double v = lap_total(acc);
 #pragma unroll
-        for (int s = 0; s < 9; ++s)
-            if (lf.mask >> s & 1) sum += part[int64_t(s) * nt + t];
-        const double2 tp = txy[t];
-        sum += coin_correction(coin_off, coin_src, t, tp.x, tp.y, sxy, q, tab_lane);
-        out[tids[t]] = -kInv4Pi * sum;
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) {
+                v += coin_correction(coin_off, coin_src, t, tp.x, tp.y, sxy, q, tab_lane);
+                out[tids[t]] = -kInv4Pi * v;
+            }
+        }
     }
 }
 
@@ -1590,7 +1624,7 @@ void build_laplace_ops(Plan& pl) {
     }
     smem_optin((const void*)l2p_p2p_kernel, kLogTableBytes + 32 * 1024);
     smem_optin((const void*)p2p_sym_kernel, int(kSymSmem));
-    smem_optin((const void*)sym_finalize_kernel, kLogTableBytes + 16 * 1024);
+    smem_optin((const void*)sym_finalize_kernel, int(kFinSmem));
     build_coincidences(pl);
     pl.coin_ready = true;
     if (!pl.adaptive) build_sym_near(pl, pl.shard_lb, pl.shard_le);
@@ -1612,7 +1646,7 @@ size_t laplace_work_bytes(const Plan& pl) {
            al256(sizeof(double) * 64 * size_t(std::max<int64_t>(pl.n_p2p_parts, 1))) +
            al256(sizeof(int) * size_t(std::max<int64_t>(pl.n_p2p_heavy, 1))) +
            al256(sizeof(double2) * n * size_t(pl.n_p2m_splits > 0 ? pl.n_p2m_items : 1)) +
-           (pl.sym ? al256(sizeof(double) * 9 * size_t(std::max<int64_t>(pl.nt, 1))) : 0);
+           (pl.sym ? al256(sizeof(double) * size_t(std::max<int64_t>(pl.sym_nparts, 1))) : 0);
 }
 
 LaplaceWork laplace_work_at(const Plan& pl, void* base) {
@@ -1632,7 +1666,7 @@ LaplaceWork laplace_work_at(const Plan& pl, void* base) {
     w.partial_p2p = reinterpret_cast<double*>(take(sizeof(double) * 64 * size_t(std::max<int64_t>(pl.n_p2p_parts, 1))));
     w.pcount = reinterpret_cast<int*>(take(sizeof(int) * size_t(std::max<int64_t>(pl.n_p2p_heavy, 1))));
     w.p2m_partial = reinterpret_cast<double2*>(take(sizeof(double2) * n * size_t(pl.n_p2m_splits > 0 ? pl.n_p2m_items : 1)));
-    w.sym_part = pl.sym ? reinterpret_cast<double*>(take(sizeof(double) * 9 * size_t(std::max<int64_t>(pl.nt, 1))))
+    w.sym_part = pl.sym ? reinterpret_cast<double*>(take(sizeof(double) * size_t(std::max<int64_t>(pl.sym_nparts, 1))))
                         : nullptr;
     return w;
 }
@@ -1682,23 +1716,26 @@ void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const L
                 const int64_t want = (pl.n_sym_tasks + kSymWarps - 1) / kSymWarps;
                 const unsigned grid = unsigned(std::min<int64_t>(want, int64_t(pl.sm_count) * std::max(per_sm, 1)));
                 launch_pdl(p2p_sym_kernel, dim3(grid), dim3(kSymWarps * 32), kSymSmem, s,
-                           (const SymTask*)pl.sym_tasks.p, pl.n_sym_tasks, (const int4*)pl.sym_ranges.p,
-                           (const double2*)pl.src_sorted.p,
-                           (const double*)qs, log_table_dev(), ticket, w.sym_part, pl.nt);
+                           (const SymTask*)pl.sym_tasks.p, pl.n_sym_tasks, (const SymRange*)pl.sym_ranges.p,
+                           (const double2*)pl.src_sorted.p, (const double*)qs, log_table_dev(), ticket,
+                           w.sym_part);
                 ++launches;
             }
             if (pl.n_sym_leaves > 0) {
-                launch_pdl(sym_finalize_kernel, dim3(nblk(pl.n_sym_leaves * 32, 256)), dim3(256),
-                           size_t(kLogTableBytes) + 16 * 1024, s, (const SymLeaf*)pl.sym_leaves.p,
-                           pl.n_sym_leaves, (const double*)w.sym_part, pl.nt, (const double2*)pl.src_sorted.p,
+                const unsigned fgrid = unsigned(std::min<int64_t>(nblk(pl.n_sym_leaves, kFinWarps),
+                                                                  int64_t(pl.sm_count) * 2));
+                launch_pdl(sym_finalize_kernel, dim3(fgrid), dim3(kFinWarps * 32), kFinSmem, s,
+                           (const SymLeaf*)pl.sym_leaves.p, pl.n_sym_leaves, (const double*)w.sym_part,
+                           (const int2*)pl.near_ranges.p, (const double2*)pl.src_sorted.p,
                            (const double*)qs, (const double2*)pl.tgt_sorted.p, (const int32_t*)pl.tgt_ids.p,
                            (const int32_t*)pl.coin_off.p, (const int32_t*)pl.coin_src.p, log_table_dev(),
                            out_dev);
                 ++launches;
             }
         }
-        const P2PChunk* nchunks = pl.sym ? pl.near_chunks.p : pl.p2p_chunks.p;
-        const int64_t nnear = pl.sym ? pl.n_near_chunks : pl.n_p2p_chunks;
+        if (pl.sym) return;  // unmatched targets: sym_finalize_kernel
+        const P2PChunk* nchunks = pl.p2p_chunks.p;
+        const int64_t nnear = pl.n_p2p_chunks;
         if (nnear == 0) return;
         const size_t smem = size_t(kLogTableBytes) +
                             (sizeof(double2) + sizeof(double)) * kP2PBatch * kP2PWarps +

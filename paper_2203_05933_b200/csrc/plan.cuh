@@ -82,26 +82,36 @@ constexpr int kMaxNearRanges = 64;
 // Symmetric near field (uniform Laplace trees whose first ns targets are the
 // sources, the volume-potential case "targets = nodes"): every unordered pair
 // of near points is evaluated ONCE -- log r^2 feeds target i (with q_j) and
-// target j (with q_i).  A task is one leaf A (rows) against a flat column
-// list: A itself, then the neighbours B whose pair {A, B} A owns (the larger
-// leaf, ties to the smaller Morton id).  Row sums of A's targets go to slot
-// 4, column sums of B's targets to slot (dy+1)*3 + (dx+1) of B - A, so every
-// (target, slot) has one writer and the final per-target sum runs in a fixed
-// slot order (fmm.cu, p2p_sym_kernel / sym_finalize_kernel).
+// target j (with q_i).  Leaf A owns the pairs {A, B} with its neighbours B
+// when it is the larger leaf (ties: smaller Morton id); its flat column list
+// is A itself, then the owned neighbours.  The (rows of A) x (columns) block
+// is cut into subtasks of one row group (whole tiles of 32 R rows) x one
+// column chunk, sized to the GPU's fair share.  A subtask writes its
+// partials: row sums of A's targets into A's row slot of the chunk, column
+// sums (accumulated over the group's row tiles) into the column target's
+// slot for (owner A, row group).  Each (target, slot) has exactly one
+// writer and the final per-target sum runs over the leaf's slots in a fixed
+// order (fmm.cu, p2p_sym_kernel / sym_finalize_kernel).  Partial layout per
+// leaf A: pbase(A) + slot * n_A + k; slots: A's column chunks (row sums),
+// A's row groups (self columns), then per owning neighbour its row groups.
 struct SymTask {
-    int32_t a_src, a_tgt, na;  // rows: the sources of leaf A = its first na targets
-    int32_t ncol;              // flat columns: [0, na) = A itself, then the owned neighbours
-    int32_t rfirst, rcount;    // column ranges sym_ranges[rfirst, +rcount), the first is A
-    int32_t rows2;             // 1: two rows per lane (64-row tiles), 0: one (32-row tiles)
-    int32_t pad;
+    int32_t a_src, na;     // rows: leaf A's sources = its first na targets
+    int32_t r0, r1;        // row group [r0, r1): whole row tiles of 32 R rows
+    int32_t c0, c1;        // flat column chunk [c0, c1) (multiples of 32, c1 may be ncol)
+    int32_t rfirst, rcount;  // column ranges sym_ranges[rfirst, +rcount), the first is A
+    int64_t a_part;        // row partial of row i: part[a_part + i]
+    int32_t rg, rows2;     // row group index (column slots: b_part + rg * nb); R = 1 + rows2
 };
 struct SymRange {
-    int32_t b_src, b_tgt, coff, slot;  // sorted source / target of the range, flat offset, slot
+    int32_t b_src, coff, nb, pad;  // sorted source of the range, flat offset, leaf size
+    int64_t b_part;                // column j -> part[b_part + rt * nb + (j - coff)]
 };
 struct SymLeaf {
+    int64_t pbase;   // first partial of the leaf
     int32_t tgt, n;  // first matched target (sorted) and count
-    int32_t mask;    // slots written for this leaf's targets
-    int32_t pad;
+    int32_t nslot;
+    int32_t t1;      // end of the leaf's targets: [tgt + n, t1) are unmatched
+    int32_t rfirst, rcount;  // the leaf's 3x3 source ranges in near_ranges (unmatched targets)
 };
 constexpr int kSymMaxN = 512;     // largest leaf (sources) the symmetric path takes
 constexpr int kSymMaxRanges = 9;
@@ -200,6 +210,9 @@ struct Plan {
     DBuf<SymLeaf> sym_leaves;
     DBuf<P2PChunk> near_chunks;
     int64_t n_sym_tasks = 0, n_sym_leaves = 0, n_near_chunks = 0;
+    int64_t sym_nparts = 0;   // partial doubles per apply
+    int32_t sym_chunk = 0;    // column chunk (whole-tree decision, shards reuse it)
+    double sym_fair = 0.0;    // pairs per subtask (whole-tree decision)
     std::vector<LeafNear> h_leafnear;
     int64_t n_p2p_chunks = 0;
     int64_t n_p2p_heavy = 0;  // split chunks (counters)
@@ -331,7 +344,7 @@ struct LaplaceWork {
     double* partial_p2p;
     int* pcount;
     double2* p2m_partial;
-    double* sym_part;  // [9][nt] slot partials of the symmetric near field
+    double* sym_part;  // slot partials of the symmetric near field (SymLeaf::pbase)
 };
 size_t laplace_work_bytes(const Plan& pl);
 LaplaceWork laplace_work_at(const Plan& pl, void* base);

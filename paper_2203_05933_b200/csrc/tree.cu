@@ -684,71 +684,130 @@ void build_sym_near(Plan& pl, int64_t lb, int64_t le) {
     const int L = pl.L;
     const int nb = 1 << L;
     const int64_t nleaf = int64_t(1) << (2 * L);
+    const bool whole = lb == 0 && le == nleaf;
     const std::vector<int32_t>& so = pl.h_soff;
     const std::vector<int32_t>& to = pl.h_toff;
-    for (int64_t b = 0; b < nleaf; ++b)
-        if (so[size_t(b) + 1] - so[size_t(b)] > kSymMaxN) return;
-    auto in = [&](int64_t b) { return b >= lb && b < le; };
     auto nsrc = [&](int64_t b) { return so[size_t(b) + 1] - so[size_t(b)]; };
+    for (int64_t b = 0; b < nleaf; ++b)
+        if (nsrc(b) > kSymMaxN) return;
+    auto in = [&](int64_t b) { return b >= lb && b < le; };
     // the owner of {A, B}: the larger leaf, ties to the smaller Morton id
     auto owns = [&](int64_t a, int64_t b) {
         const int32_t x = nsrc(a), y = nsrc(b);
         return x > y || (x == y && a < b);
     };
-    std::vector<SymTask> tasks;
-    std::vector<SymRange> ranges;
-    std::vector<SymLeaf> leaves;
-    double cost_sym = 0.0, cost_one = 0.0;  // modelled warp instructions (sym block vs one-sided pairs)
+    auto neighbour = [&](int64_t a, int slot) -> int64_t {  // slot = (dy+1)*3 + (dx+1), -1 outside
+        const int bx = int(squash2(uint32_t(a))) + slot % 3 - 1, by = int(squash2(uint32_t(a) >> 1)) + slot / 3 - 1;
+        if (bx < 0 || by < 0 || bx >= nb || by >= nb) return -1;
+        return int64_t(mort(uint32_t(bx), uint32_t(by)));
+    };
+    auto rows2_of = [&](int32_t n) { return n > 32 ? 1 : 0; };
+    auto nrt_of = [&](int32_t n) { return (n + (rows2_of(n) ? 63 : 31)) / (rows2_of(n) ? 64 : 32); };
+    // pass 1: flat column counts, and on the whole tree the cost model and chunk size
+    std::vector<int32_t> ncol(size_t(nleaf), 0);
+    double cost_sym = 0.0, cost_one = 0.0, total = 0.0;
     for (int64_t a = 0; a < nleaf; ++a) {
         const int32_t na = nsrc(a);
         if (!na) continue;
-        const int ax = int(squash2(uint32_t(a))), ay = int(squash2(uint32_t(a) >> 1));
-        int mask = 1 << 4;
-        std::vector<SymRange> mine{SymRange{so[size_t(a)], to[size_t(a)], 0, 4}};
-        int32_t ncol = na;
-        bool touches = in(a);
-        for (int dy = -1; dy <= 1; ++dy)
-            for (int dx = -1; dx <= 1; ++dx) {
-                const int bx = ax + dx, by = ay + dy;
-                if ((dx == 0 && dy == 0) || bx < 0 || by < 0 || bx >= nb || by >= nb) continue;
-                const int64_t bb = mort(uint32_t(bx), uint32_t(by));
-                if (!nsrc(bb)) continue;
-                if (!owns(a, bb)) {
-                    mask |= 1 << ((-dy + 1) * 3 + (-dx + 1));  // written by bb's task
-                    continue;
-                }
-                mine.push_back(SymRange{so[size_t(bb)], to[size_t(bb)], ncol, (dy + 1) * 3 + (dx + 1)});
-                ncol += nsrc(bb);
-                touches = touches || in(bb);
-                cost_one += 2.0 * double(na) * nsrc(bb) * 31.0 / 32.0;
-            }
+        int32_t nc = na;
+        for (int sl = 0; sl < 9; ++sl) {
+            const int64_t b = sl == 4 ? -1 : neighbour(a, sl);
+            if (b < 0 || !nsrc(b) || !owns(a, b)) continue;
+            nc += nsrc(b);
+            cost_one += 2.0 * double(na) * nsrc(b) * 31.0 / 32.0;
+        }
         cost_one += double(na) * na * 31.0 / 32.0;
-        if (in(a)) leaves.push_back(SymLeaf{to[size_t(a)], na, mask, 0});
-        if (!touches) continue;
-        const int rows2 = na > 32 ? 1 : 0;
-        const int rt = (na + (rows2 ? 63 : 31)) / (rows2 ? 64 : 32);
-        const int ct = (ncol + 31) / 32;
-        cost_sym += double(rt) * ct * 32.0 * (rows2 ? 56.0 : 31.0) + 200.0;
-        tasks.push_back(SymTask{so[size_t(a)], to[size_t(a)], na, ncol, int32_t(ranges.size()), int32_t(mine.size()),
-                                rows2, 0});
-        ranges.insert(ranges.end(), mine.begin(), mine.end());
+        ncol[size_t(a)] = nc;
+        total += double(na) * nc;
+        cost_sym += double(nrt_of(na)) * ((nc + 31) / 32) * 32.0 * (rows2_of(na) ? 56.0 : 31.0) + 150.0;
     }
-    // a task runs on one warp: it must not outlast the fair share of the
-    // whole-GPU work by much (a few huge leaves next to many small ones)
-    int64_t max_task = 0;
-    double total = 0.0;
-    for (const SymTask& t : tasks) {
-        max_task = std::max<int64_t>(max_task, int64_t(t.na) * t.ncol);
-        total += double(t.na) * t.ncol;
+    if (whole) {
+        // measured: cfg4 (256 per leaf) model 0.50 -> near field 0.64x; cfg2
+        // (16..337 per leaf) model 0.76 -> 1.37x (staging latency, subtask
+        // and unmatched-target overheads the model leaves out)
+        pl.sym_auto = cost_sym < 0.6 * cost_one;
+        // subtasks of about half one warp's fair share (16 warps per SM)
+        pl.sym_fair = std::max(4096.0, total / (double(pl.sm_count) * 16.0 * 2.0));
+        pl.sym_chunk = int32_t(std::clamp(std::floor(pl.sym_fair / 64.0 / 32.0) * 32.0, 32.0, 8192.0));
     }
-    const double fair = total / (double(pl.sm_count) * 16.0);
-    // decided once on the whole tree; shards follow it (their results must
-    // assemble bit-exactly to the single-GPU ones)
-    if (lb == 0 && le == nleaf) pl.sym_auto = cost_sym < 0.85 * cost_one && double(max_task) <= 2.0 * fair;
     if (force != 1 && !pl.sym_auto) return;
-    auto cost = [](const SymTask& t) { return int64_t(t.na) * t.ncol; };
+    const int32_t C = std::max(32, pl.sym_chunk);
+    auto ncc_of = [&](int64_t a) { return (ncol[size_t(a)] + C - 1) / C; };
+    // row tiles per group: as many as keep group rows x chunk columns near the share
+    auto gsz_of = [&](int64_t a) {
+        const int32_t na = nsrc(a);
+        const double tile = (rows2_of(na) ? 64.0 : 32.0) * std::min(C, ncol[size_t(a)]);
+        return std::clamp(int32_t(pl.sym_fair / tile), 1, nrt_of(na));
+    };
+    auto nrg_of = [&](int64_t a) { return (nrt_of(nsrc(a)) + gsz_of(a) - 1) / gsz_of(a); };
+    // pass 2: slot layout per leaf (own chunks, own row tiles, then per owning
+    // neighbour in slot order its row tiles) and partial bases
+    std::vector<int32_t> nslot(size_t(nleaf), 0);
+    std::vector<int64_t> pbase(size_t(nleaf) + 1, 0);
+    for (int64_t a = 0; a < nleaf; ++a) {
+        const int32_t na = nsrc(a);
+        if (na) {
+            int32_t k = ncc_of(a) + nrg_of(a);
+            for (int sl = 0; sl < 9; ++sl) {
+                const int64_t b = sl == 4 ? -1 : neighbour(a, sl);
+                if (b >= 0 && nsrc(b) && owns(b, a)) k += nrg_of(b);
+            }
+            nslot[size_t(a)] = k;
+        }
+        pbase[size_t(a) + 1] = pbase[size_t(a)] + int64_t(na) * nslot[size_t(a)];
+    }
+    // first column slot of owner a in leaf b (b's own slots, then its owners in slot order)
+    auto col_slot = [&](int64_t b, int64_t a) {
+        int32_t k = ncc_of(b) + nrg_of(b);
+        for (int sl = 0; sl < 9; ++sl) {
+            const int64_t o = sl == 4 ? -1 : neighbour(b, sl);
+            if (o < 0 || !nsrc(o) || !owns(o, b)) continue;
+            if (o == a) return k;
+            k += nrg_of(o);
+        }
+        return -1;
+    };
+    std::vector<SymTask> tasks;
+    std::vector<SymRange> ranges;
+    std::vector<SymLeaf> leaves;
+    for (int64_t a = 0; a < nleaf; ++a) {
+        const int32_t na = nsrc(a);
+        if (!na) continue;
+
+        std::vector<SymRange> mine{SymRange{so[size_t(a)], 0, na, 0,
+                                            pbase[size_t(a)] + int64_t(ncc_of(a)) * na}};
+        bool touches = in(a);
+        int32_t off = na;
+        for (int sl = 0; sl < 9; ++sl) {
+            const int64_t b = sl == 4 ? -1 : neighbour(a, sl);
+            if (b < 0 || !nsrc(b) || !owns(a, b)) continue;
+            mine.push_back(SymRange{so[size_t(b)], off, nsrc(b), 0,
+                                    pbase[size_t(b)] + int64_t(col_slot(b, a)) * nsrc(b)});
+            off += nsrc(b);
+            touches = touches || in(b);
+        }
+        if (!touches) continue;
+        const int r2 = rows2_of(na);
+        const int32_t rows = (r2 ? 64 : 32) * gsz_of(a);
+        const int32_t rfirst = int32_t(ranges.size());
+        ranges.insert(ranges.end(), mine.begin(), mine.end());
+        for (int32_t rg = 0; rg < nrg_of(a); ++rg)
+            for (int32_t cc = 0; cc < ncc_of(a); ++cc)
+                tasks.push_back(SymTask{so[size_t(a)], na, rg * rows, std::min(na, (rg + 1) * rows), cc * C,
+                                        std::min(ncol[size_t(a)], (cc + 1) * C), rfirst, int32_t(mine.size()),
+                                        pbase[size_t(a)] + int64_t(cc) * na, rg, r2});
+    }
+    // every leaf of the range with targets: matched ones from the slots,
+    // unmatched ones one-sided over the 3x3 source ranges (sym_finalize_kernel)
+    for (const LeafNear& ln : pl.h_leafnear) {
+        const int32_t na = nsrc(ln.leaf);
+        leaves.push_back(SymLeaf{pbase[size_t(ln.leaf)], ln.t0, na, nslot[size_t(ln.leaf)], ln.t1, ln.rfirst,
+                                 ln.rcount});
+    }
+    auto cost = [](const SymTask& t) { return int64_t(t.c1 - t.c0) * (t.r1 - t.r0); };
     std::stable_sort(tasks.begin(), tasks.end(),
                      [&](const SymTask& x, const SymTask& y) { return cost(x) > cost(y); });
+    pl.sym_nparts = pbase.back();
     // unmatched targets: one-sided chunks (<= 64 targets, never split)
     std::vector<P2PChunk> extra;
     for (const LeafNear& ln : pl.h_leafnear) {
