@@ -113,7 +113,7 @@ struct SymLeaf {
     int32_t t1;      // end of the leaf's targets: [tgt + n, t1) are unmatched
     int32_t rfirst, rcount;  // the leaf's 3x3 source ranges in near_ranges (unmatched targets)
 };
-constexpr int kSymMaxN = 512;     // largest leaf (sources) the symmetric path takes
+constexpr int kSymMaxN = 4096;    // largest leaf (sources) the symmetric path takes
 constexpr int kSymMaxRanges = 9;
 struct LeafNear {  // per-leaf near-field data of the last schedule (host)
     int32_t leaf, t0, t1, rfirst, rcount, rself, lfirst, lcount;
