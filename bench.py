@@ -239,7 +239,11 @@ def run_gpu(args):
     if world > 1:
         shard = multigpu.shard_plan(plan, rank, world)
     info = plan.info()
-    stream = torch.cuda.current_stream()
+    # one explicit stream for the L2 flush, the events and every apply: the
+    # default stream's handle is 0, which the library would replace by a
+    # stream of its own (unordered with the flush, synchronised per call)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     sh = stream.cuda_stream
     q_d = torch.from_numpy(wl.q).to("cuda")
     out_d = torch.empty(wl.nt, dtype=torch.float64, device="cuda")
@@ -489,7 +493,8 @@ def run_layer(args):
     torch.cuda.set_device(local)
     sys_, cf, tg = W.layer_cfg2()
     ev_obj = sys_.evaluator(local)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     sh = stream.cuda_stream
     cf_d = torch.from_numpy(cf).to("cuda")
     tg_d = torch.from_numpy(np.ascontiguousarray(tg)).to("cuda")

@@ -8,7 +8,8 @@ import paper_2203_05933_b200 as vp
 from paper_2203_05933_b200 import workloads as W
 w = W.cfg2()
 plan = vp.SummationPlan(vp.make_kernel(vp.KernelFamily.Laplace), w.src, w.tgt, 1e-12)
-st = torch.cuda.current_stream(); sh = st.cuda_stream
+st = torch.cuda.Stream(); torch.cuda.set_stream(st); sh = st.cuda_stream
+print('stream handle', sh)
 qd = torch.from_numpy(w.q).cuda(); od = torch.empty(w.nt, dtype=torch.float64, device='cuda')
 qh = torch.from_numpy(w.q.copy()).pin_memory(); oh = torch.empty(w.nt, dtype=torch.float64).pin_memory()
 def timeit(fn, n=20):
