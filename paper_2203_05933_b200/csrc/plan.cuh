@@ -200,16 +200,15 @@ struct Plan {
     // subnormal, CSR over sorted targets (fmm.cu, build_coincidences)
     DBuf<int32_t> coin_off, coin_src;
     bool coin_ready = false;
-    // symmetric near field (see SymTask); near_chunks then holds the chunks
-    // of the unmatched targets only (p2p_chunks keeps every target for L2P)
+    // symmetric near field (see SymTask); unmatched targets are summed
+    // one-sided by sym_finalize_kernel (p2p_chunks keeps every target for L2P)
     bool matched = false;  // tgt[0, ns) == src bitwise (set at plan creation)
     bool sym = false;
     bool sym_auto = false;  // the cost model's choice for the whole tree
     DBuf<SymTask> sym_tasks;
     DBuf<SymRange> sym_ranges;
     DBuf<SymLeaf> sym_leaves;
-    DBuf<P2PChunk> near_chunks;
-    int64_t n_sym_tasks = 0, n_sym_leaves = 0, n_near_chunks = 0;
+    int64_t n_sym_tasks = 0, n_sym_leaves = 0;
     int64_t sym_nparts = 0;   // partial doubles per apply
     int32_t sym_chunk = 0;    // column chunk (whole-tree decision, shards reuse it)
     double sym_fair = 0.0;    // pairs per subtask (whole-tree decision)

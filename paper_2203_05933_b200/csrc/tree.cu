@@ -669,10 +669,10 @@ void build_schedules(Plan& pl, int64_t lb, int64_t le) {
 }
 
 // The symmetric near-field schedule (SymTask, plan.cuh) for the targets of
-// the leaf range [lb, le): every pair {A, B} of near leaves (B >= A, 3x3
-// neighbourhood, both with sources) touching the range, the per-leaf slot
-// masks for the final sums, and one-sided chunks for the unmatched targets
-// (those beyond a leaf's first n_src targets).  Taken when the first ns
+// the leaf range [lb, le): the subtasks of every leaf owning a pair {A, B}
+// of near leaves touching the range, the per-leaf slot layout (SymLeaf) for
+// the final sums, which also cover the unmatched targets (those beyond a
+// leaf's first n_src targets) one-sided.  Taken when the first ns
 // targets are the sources (so leaf A's first n_src sorted targets are its
 // sorted sources, both sorts being stable), the tree is uniform, the
 // kernel Laplace and no leaf holds more than kSymMaxN sources.
@@ -808,30 +808,12 @@ void build_sym_near(Plan& pl, int64_t lb, int64_t le) {
     std::stable_sort(tasks.begin(), tasks.end(),
                      [&](const SymTask& x, const SymTask& y) { return cost(x) > cost(y); });
     pl.sym_nparts = pbase.back();
-    // unmatched targets: one-sided chunks (<= 64 targets, never split)
-    std::vector<P2PChunk> extra;
-    for (const LeafNear& ln : pl.h_leafnear) {
-        const int32_t nsrc = so[size_t(ln.leaf) + 1] - so[size_t(ln.leaf)];
-        int64_t near_src = 0;
-        for (int dy = -1; dy <= 1; ++dy)
-            for (int dx = -1; dx <= 1; ++dx) {
-                const int bx = int(squash2(uint32_t(ln.leaf))) + dx, by = int(squash2(uint32_t(ln.leaf) >> 1)) + dy;
-                if (bx < 0 || by < 0 || bx >= nb || by >= nb) continue;
-                const int64_t bb = mort(uint32_t(bx), uint32_t(by));
-                near_src += so[size_t(bb) + 1] - so[size_t(bb)];
-            }
-        for (int32_t t = ln.t0 + nsrc; t < ln.t1; t += 64)
-            extra.push_back(P2PChunk{t, std::min(64, ln.t1 - t), int32_t(std::min<int64_t>(near_src, INT32_MAX)),
-                                     ln.rfirst, ln.rcount, ln.rself, ln.lfirst, ln.lcount, 0, 1, -1, -1});
-    }
     cudaStream_t st = 0;
     to_device(pl.sym_tasks, tasks, st);
     to_device(pl.sym_ranges, ranges, st);
     to_device(pl.sym_leaves, leaves, st);
-    to_device(pl.near_chunks, extra, st);
     pl.n_sym_tasks = int64_t(tasks.size());
     pl.n_sym_leaves = int64_t(leaves.size());
-    pl.n_near_chunks = int64_t(extra.size());
     pl.sym = true;
 }
 
