@@ -98,7 +98,10 @@ __host__ __device__ inline cplx cadd(cplx a, cplx b) {
 #endif
 constexpr int kLogTableBits = VPG_LOG_BITS;
 constexpr int kLogTableSize = (1 << kLogTableBits) + 1;
-constexpr int kLogTableCopies = 8;
+#ifndef VPG_LOG_COPIES
+#define VPG_LOG_COPIES 8
+#endif
+constexpr int kLogTableCopies = VPG_LOG_COPIES;
 constexpr int kLogTableBytes = kLogTableSize * kLogTableCopies * 16;
 
 // Host-built table (inv_c, -ln(inv_c)) in global memory (one per device,

@@ -31,7 +31,7 @@ allpairs_kernel(const double2* src, const double* q, int64_t ns,
     double2* tab = smd;
     double2* tile = smd + (kFamily == VPG_LAPLACE ? kLogTableSize * kLogTableCopies : 0);
     if (kFamily == VPG_LAPLACE) log_table_to_smem(tab, gtab);
-    const uint32_t tab_lane = log_table_lane_addr(tab, threadIdx.x & 7);
+    const uint32_t tab_lane = log_table_lane_addr(tab, threadIdx.x & (kLogTableCopies - 1));
     const int64_t j0 = int64_t(blockIdx.y) * slice;
     const int64_t j1 = min(ns, j0 + slice);
 

@@ -949,7 +949,7 @@ l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, const int2* ranges,
     pdl_wait();
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t tab_lane = log_table_lane_addr(tab, lane & 7);
+    const uint32_t tab_lane = log_table_lane_addr(tab, lane & (kLogTableCopies - 1));
     double2* mxy = sbuf + warp * kP2PBatch;
     double* mq = qbuf + warp * kP2PBatch;
     int* pre_s = rbuf + warp * 2 * kMaxNearRanges;
@@ -1171,7 +1171,7 @@ p2p_sym_kernel(const SymTask* tasks, int64_t ntask, const SymRange* ranges, cons
     pdl_wait();
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t tab_lane = log_table_lane_addr(tab, lane & 7);
+    const uint32_t tab_lane = log_table_lane_addr(tab, lane & (kLogTableCopies - 1));
     double2* cxy = cbuf + warp * 64;
     double* cq = qbuf + warp * 64;
     SymRange* rng = rbuf + warp * kSymMaxRanges;
@@ -1215,7 +1215,7 @@ sym_finalize_kernel(const SymLeaf* leaves, int64_t nleaves, const double* part, 
     pdl_wait();
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t tab_lane = log_table_lane_addr(tab, lane & 7);
+    const uint32_t tab_lane = log_table_lane_addr(tab, lane & (kLogTableCopies - 1));
     int* pre_s = rbuf + warp * 2 * kMaxNearRanges;
     int* st_s = pre_s + kMaxNearRanges;
     for (int64_t w = int64_t(blockIdx.x) * kFinWarps + warp; w < nleaves; w += int64_t(gridDim.x) * kFinWarps) {

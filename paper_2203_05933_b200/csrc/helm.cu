@@ -534,7 +534,7 @@ hf_l2p_p2p_kernel(HfLevels hl, const P2PChunk* chunks, int64_t nchunks, const in
     log_table_to_smem(ltab, gtab);
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t tab_lane = log_table_lane_addr(ltab, lane & 7);
+    const uint32_t tab_lane = log_table_lane_addr(ltab, lane & (kLogTableCopies - 1));
     const int n = hl.n, n2 = n * n;
     const double* nodes = tab;
     const double* bw = tab + 32;
