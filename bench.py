@@ -491,7 +491,14 @@ def run_layer(args):
             flush=True)
         return 0
     torch.cuda.set_device(local)
-    sys_, cf, tg = W.layer_cfg2()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    sys_, cf, tg_all = W.layer_cfg2()
+    # targets are independent: rank r evaluates a contiguous slice, no collective
+    lo, hi = len(tg_all) * rank // world, len(tg_all) * (rank + 1) // world
+    tg = np.ascontiguousarray(tg_all[lo:hi])
     ev_obj = sys_.evaluator(local)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
@@ -512,6 +519,8 @@ def run_layer(args):
     while time.time() - t_hold < 0.5:
         step()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if dist:
+        dist.barrier()
     torch.cuda.synchronize()
     for i in range(args.steps):
         flush.zero_()
@@ -520,7 +529,13 @@ def run_layer(args):
         ev[i][1].record(stream)
     torch.cuda.synchronize()
     clk.__exit__(None, None, None)
+    if dist:
+        dist.barrier()
     ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    if dist:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
     # end to end: host arrays through vpg_layer_eval (H2D of density + targets, D2H of u_H)
     host = ev_obj.eval(cf, tg, allow_close=True)
     e2e = []
@@ -531,6 +546,14 @@ def run_layer(args):
     e2e_ms = float(np.mean(e2e)) * 1e3
     if not np.array_equal(host, out_d.cpu().numpy()):
         raise RuntimeError("host and device layer evaluations differ")
+    if dist:
+        t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+        if rank != 0:
+            dist.destroy_process_group()
+            return 0
+    tg = tg_all  # the whole job's pairs (all ranks)
     co, fi = _layer_pairs(sys_, tg)
     pairs = co + fi
     achieved = pairs * LAYER_FLOPS[0] / (ms * 1e-3) / 1e12
@@ -538,7 +561,7 @@ def run_layer(args):
     line = {
         "metric": LAYER_METRIC, "value": pairs / (ms * 1e-3), "unit": "interactions/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, configs[1] shapes)",
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, configs[1] shapes)",
         "config": {"workload": "layer", "nt": len(tg), "n_boundary": sys_.n_density, "coarse_pairs": co,
                    "fine_pairs": fi, "allow_close": True, "l2": "flushed (256 MB write) before every timed step",
                    "step": "eval_layer_potential (bie.cpp:383-468), Laplace, star boundary"},
@@ -552,7 +575,7 @@ def run_layer(args):
                                        "4 reciprocal, 2 accumulate)"},
         "clocks": clk.summary(),
     }
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:
         import oracle
         rest = oracle.restatement()
         cores = os.cpu_count() or 1
@@ -565,6 +588,8 @@ def run_layer(args):
                                 "sample": f"{len(sub)} of the configs[1] targets (every "
                                           f"{max(1, len(tg) // 60000)}-th), oracle vo_layer_eval"}
     print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
     return 0
 
 
