@@ -1202,7 +1202,7 @@ constexpr size_t kFinSmem = size_t(kLogTableBytes) + kFinScratch;
 __global__ void __launch_bounds__(kFinWarps * 32)
 sym_finalize_kernel(const SymLeaf* leaves, int64_t nleaves, const double* part, const int2* ranges,
                     const double2* sxy, const double* q, const double2* txy, const int32_t* tids,
-                    const int32_t* coin_off, const int32_t* coin_src, const double2* gtab, double* out) {
+                    const int32_t* coin_off, const int32_t* coin_src, const double2* gtab, double* out, int add) {
     extern __shared__ double2 smp[];
     double2* tab = smp;
     int* rbuf = reinterpret_cast<int*>(smp + kLogTableSize * kLogTableCopies);  // [warps][2][64]
@@ -1225,11 +1225,15 @@ sym_finalize_kernel(const SymLeaf* leaves, int64_t nleaves, const double* part, 
             const double* pk = part + lf.pbase + k;
             double sum = 0.0;
             for (int sl = 0; sl < lf.nslot; ++sl) sum += pk[int64_t(sl) * lf.n];
+            if (add) {  // hybrid: the one-sided kernel wrote this target (coincidences included)
+                out[tids[t]] += -kInv4Pi * sum;
+                continue;
+            }
             const double2 tp = txy[t];
             sum += coin_correction(coin_off, coin_src, t, tp.x, tp.y, sxy, q, tab_lane);
             out[tids[t]] = -kInv4Pi * sum;
         }
-        if (lf.tgt + lf.n >= lf.t1) continue;
+        if (add || lf.tgt + lf.n >= lf.t1) continue;
         const NearList nl = near_list(ranges, lf.rfirst, lf.rcount, 0, lane, pre_s, st_s);
         for (int t = lf.tgt + lf.n; t < lf.t1; ++t) {
             const double2 tp = txy[t];
@@ -1707,35 +1711,7 @@ void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const L
     int* pcount = w.pcount;
     unsigned* gbar = reinterpret_cast<unsigned*>(ticket) + 8;  // grid barriers of the shift passes
 
-    auto near_field = [&](cudaStream_t s) {
-        if (pl.sym) {
-            if (pl.n_sym_tasks > 0) {
-                int per_sm = 1;
-                VPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p2p_sym_kernel, kSymWarps * 32,
-                                                                       kSymSmem));
-                const int64_t want = (pl.n_sym_tasks + kSymWarps - 1) / kSymWarps;
-                const unsigned grid = unsigned(std::min<int64_t>(want, int64_t(pl.sm_count) * std::max(per_sm, 1)));
-                launch_pdl(p2p_sym_kernel, dim3(grid), dim3(kSymWarps * 32), kSymSmem, s,
-                           (const SymTask*)pl.sym_tasks.p, pl.n_sym_tasks, (const SymRange*)pl.sym_ranges.p,
-                           (const double2*)pl.src_sorted.p, (const double*)qs, log_table_dev(), ticket,
-                           w.sym_part);
-                ++launches;
-            }
-            if (pl.n_sym_leaves > 0) {
-                const unsigned fgrid = unsigned(std::min<int64_t>(nblk(pl.n_sym_leaves, kFinWarps),
-                                                                  int64_t(pl.sm_count) * 2));
-                launch_pdl(sym_finalize_kernel, dim3(fgrid), dim3(kFinWarps * 32), kFinSmem, s,
-                           (const SymLeaf*)pl.sym_leaves.p, pl.n_sym_leaves, (const double*)w.sym_part,
-                           (const int2*)pl.near_ranges.p, (const double2*)pl.src_sorted.p,
-                           (const double*)qs, (const double2*)pl.tgt_sorted.p, (const int32_t*)pl.tgt_ids.p,
-                           (const int32_t*)pl.coin_off.p, (const int32_t*)pl.coin_src.p, log_table_dev(),
-                           out_dev);
-                ++launches;
-            }
-        }
-        if (pl.sym) return;  // unmatched targets: sym_finalize_kernel
-        const P2PChunk* nchunks = pl.p2p_chunks.p;
-        const int64_t nnear = pl.n_p2p_chunks;
+    auto one_sided = [&](cudaStream_t s, const P2PChunk* nchunks, int64_t nnear, const int2* nranges) {
         if (nnear == 0) return;
         const size_t smem = size_t(kLogTableBytes) +
                             (sizeof(double2) + sizeof(double)) * kP2PBatch * kP2PWarps +
@@ -1756,13 +1732,43 @@ void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const L
         unsigned grid = unsigned(std::min<int64_t>(want, cap));
         if (quota > 0 && s != st) grid = unsigned(std::max<int64_t>(1, (want + quota - 1) / quota));
         launch_pdl(l2p_p2p_kernel, dim3(grid), dim3(kP2PWarps * 32), smem, s, nchunks, nnear,
-                   (const int2*)pl.near_ranges.p, (const double2*)pl.src_sorted.p, (const double*)qs,
+                   nranges, (const double2*)pl.src_sorted.p, (const double*)qs,
                    (const double2*)pl.tgt_sorted.p, (const int32_t*)pl.tgt_ids.p, pl.coin_off.p,
                    pl.coin_src.p, log_table_dev(), ticket, partial_p2p, pcount, out_dev,
                    (quota > 0 && s != st) ? quota : INT32_MAX);
         ++launches;
     };
 
+    auto near_field = [&](cudaStream_t s) {
+        if (pl.sym) {
+            if (pl.n_sym_tasks > 0) {
+                int per_sm = 1;
+                VPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p2p_sym_kernel, kSymWarps * 32,
+                                                                       kSymSmem));
+                const int64_t want = (pl.n_sym_tasks + kSymWarps - 1) / kSymWarps;
+                const unsigned grid = unsigned(std::min<int64_t>(want, int64_t(pl.sm_count) * std::max(per_sm, 1)));
+                launch_pdl(p2p_sym_kernel, dim3(grid), dim3(kSymWarps * 32), kSymSmem, s,
+                           (const SymTask*)pl.sym_tasks.p, pl.n_sym_tasks, (const SymRange*)pl.sym_ranges.p,
+                           (const double2*)pl.src_sorted.p, (const double*)qs, log_table_dev(), ticket,
+                           w.sym_part);
+                ++launches;
+            }
+            if (pl.sym_hybrid) one_sided(s, pl.hyb_chunks.p, pl.n_hyb_chunks, pl.hyb_ranges.p);
+            if (pl.n_sym_leaves > 0) {
+                const unsigned fgrid = unsigned(std::min<int64_t>(nblk(pl.n_sym_leaves, kFinWarps),
+                                                                  int64_t(pl.sm_count) * 2));
+                launch_pdl(sym_finalize_kernel, dim3(fgrid), dim3(kFinWarps * 32), kFinSmem, s,
+                           (const SymLeaf*)pl.sym_leaves.p, pl.n_sym_leaves, (const double*)w.sym_part,
+                           (const int2*)pl.near_ranges.p, (const double2*)pl.src_sorted.p,
+                           (const double*)qs, (const double2*)pl.tgt_sorted.p, (const int32_t*)pl.tgt_ids.p,
+                           (const int32_t*)pl.coin_off.p, (const int32_t*)pl.coin_src.p, log_table_dev(),
+                           out_dev, pl.sym_hybrid ? 1 : 0);
+                ++launches;
+            }
+            return;  // unmatched targets: sym_finalize_kernel (full) or the one-sided pass (hybrid)
+        }
+        one_sided(s, pl.p2p_chunks.p, pl.n_p2p_chunks, pl.near_ranges.p);
+    };
     mark(0);
     gather_q<<<nblk(std::max<int64_t>(pl.ns, pl.n_p2p_heavy), 256), 256, 0, st>>>(
         q_dev, pl.src_ids.p, pl.ns, qs, gbar, ticket, pcount, pl.n_p2p_heavy);

@@ -204,7 +204,11 @@ struct Plan {
     // one-sided by sym_finalize_kernel (p2p_chunks keeps every target for L2P)
     bool matched = false;  // tgt[0, ns) == src bitwise (set at plan creation)
     bool sym = false;
-    bool sym_auto = false;  // the cost model's choice for the whole tree
+    int32_t sym_min = -1;   // whole-tree choice: -1 off, 0 every pair symmetric, T: pairs of leaves >= T (hybrid)
+    bool sym_hybrid = false;
+    DBuf<P2PChunk> hyb_chunks;  // hybrid: one-sided chunks over the non-symmetric ranges
+    DBuf<int2> hyb_ranges;
+    int64_t n_hyb_chunks = 0;
     DBuf<SymTask> sym_tasks;
     DBuf<SymRange> sym_ranges;
     DBuf<SymLeaf> sym_leaves;

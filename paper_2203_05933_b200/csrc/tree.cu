@@ -691,11 +691,6 @@ void build_sym_near(Plan& pl, int64_t lb, int64_t le) {
     for (int64_t b = 0; b < nleaf; ++b)
         if (nsrc(b) > kSymMaxN) return;
     auto in = [&](int64_t b) { return b >= lb && b < le; };
-    // the owner of {A, B}: the larger leaf, ties to the smaller Morton id
-    auto owns = [&](int64_t a, int64_t b) {
-        const int32_t x = nsrc(a), y = nsrc(b);
-        return x > y || (x == y && a < b);
-    };
     auto neighbour = [&](int64_t a, int slot) -> int64_t {  // slot = (dy+1)*3 + (dx+1), -1 outside
         const int bx = int(squash2(uint32_t(a))) + slot % 3 - 1, by = int(squash2(uint32_t(a) >> 1)) + slot / 3 - 1;
         if (bx < 0 || by < 0 || bx >= nb || by >= nb) return -1;
@@ -703,34 +698,67 @@ void build_sym_near(Plan& pl, int64_t lb, int64_t le) {
     };
     auto rows2_of = [&](int32_t n) { return n > 32 ? 1 : 0; };
     auto nrt_of = [&](int32_t n) { return (n + (rows2_of(n) ? 63 : 31)) / (rows2_of(n) ? 64 : 32); };
-    // pass 1: flat column counts, and on the whole tree the cost model and chunk size
-    std::vector<int32_t> ncol(size_t(nleaf), 0);
-    double cost_sym = 0.0, cost_one = 0.0, total = 0.0;
-    for (int64_t a = 0; a < nleaf; ++a) {
-        const int32_t na = nsrc(a);
-        if (!na) continue;
-        int32_t nc = na;
-        for (int sl = 0; sl < 9; ++sl) {
-            const int64_t b = sl == 4 ? -1 : neighbour(a, sl);
-            if (b < 0 || !nsrc(b) || !owns(a, b)) continue;
-            nc += nsrc(b);
-            cost_one += 2.0 * double(na) * nsrc(b) * 31.0 / 32.0;
-        }
-        cost_one += double(na) * na * 31.0 / 32.0;
-        ncol[size_t(a)] = nc;
-        total += double(na) * nc;
-        cost_sym += double(nrt_of(na)) * ((nc + 31) / 32) * 32.0 * (rows2_of(na) ? 56.0 : 31.0) + 150.0;
-    }
+    // Which pairs go symmetric: all of them (T = 0), or in the hybrid form only
+    // pairs of "big" leaves (>= T sources each); the other pairs of a target
+    // stay one-sided.  Decided once on the whole tree.
     if (whole) {
+        const char* mv = std::getenv("VPG_SYM_MIN");
+        const int tmin = mv ? std::atoi(mv) : -1;
+        double cost_sym = 0.0, cost_one = 0.0, total = 0.0, big_pairs = 0.0, all_pairs = 0.0;
+        constexpr int kBig = 64;
+        for (int64_t a = 0; a < nleaf; ++a) {
+            const int32_t na = nsrc(a);
+            if (!na) continue;
+            int32_t nc = na;
+            for (int sl = 0; sl < 9; ++sl) {
+                const int64_t b = neighbour(a, sl);
+                if (b < 0 || !nsrc(b)) continue;
+                all_pairs += double(na) * nsrc(b);
+                if (std::min(na, nsrc(b)) >= kBig) big_pairs += double(na) * nsrc(b);
+                if (sl == 4) continue;
+                const int32_t y = nsrc(b);
+                if (!(na > y || (na == y && a < b))) continue;
+                nc += y;
+                cost_one += 2.0 * double(na) * y * 31.0 / 32.0;
+            }
+            cost_one += double(na) * na * 31.0 / 32.0;
+            total += double(na) * nc;
+            cost_sym += double(nrt_of(na)) * ((nc + 31) / 32) * 32.0 * (rows2_of(na) ? 56.0 : 31.0) + 150.0;
+        }
         // measured: cfg4 (256 per leaf) model 0.50 -> near field 0.64x; cfg2
-        // (16..337 per leaf) model 0.76 -> 1.37x (staging latency, subtask
-        // and unmatched-target overheads the model leaves out)
-        pl.sym_auto = cost_sym < 0.6 * cost_one;
+        // (16..337 per leaf) model 0.76 -> 1.37x when every pair goes
+        // symmetric (staging latency, tile quantisation of the small leaves)
+        // The hybrid form (VPG_SYM_MIN=T) measured slower on cfg2 too (near field
+        // 0.204 ms one-sided vs 0.225 / 0.243 / 0.252 ms at T = 32 / 64 / 96,
+        // with 82% / 79% / 54% of the pairs symmetric), so it is opt-in only.
+        (void)big_pairs;
+        (void)all_pairs;
+        if (tmin >= 0) pl.sym_min = tmin;
+        else if (cost_sym < 0.6 * cost_one) pl.sym_min = 0;
+        else pl.sym_min = -1;
         // subtasks of about half one warp's fair share (16 warps per SM)
         pl.sym_fair = std::max(4096.0, total / (double(pl.sm_count) * 16.0 * 2.0));
         pl.sym_chunk = int32_t(std::clamp(std::floor(pl.sym_fair / 64.0 / 32.0) * 32.0, 32.0, 8192.0));
     }
-    if (force != 1 && !pl.sym_auto) return;
+    if (pl.sym_min < 0 && force != 1) return;
+    const int32_t T = std::max(0, pl.sym_min);
+    const bool hybrid = T > 0;
+    auto big = [&](int64_t a) { return nsrc(a) > 0 && nsrc(a) >= T; };
+    // the owner of a symmetric pair {A, B}: the larger leaf, ties to the smaller Morton id
+    auto owns = [&](int64_t a, int64_t b) {
+        const int32_t x = nsrc(a), y = nsrc(b);
+        return big(a) && big(b) && (x > y || (x == y && a < b));
+    };
+    std::vector<int32_t> ncol(size_t(nleaf), 0);
+    for (int64_t a = 0; a < nleaf; ++a) {
+        if (!big(a)) continue;
+        int32_t nc = nsrc(a);
+        for (int sl = 0; sl < 9; ++sl) {
+            const int64_t b = sl == 4 ? -1 : neighbour(a, sl);
+            if (b >= 0 && owns(a, b)) nc += nsrc(b);
+        }
+        ncol[size_t(a)] = nc;
+    }
     const int32_t C = std::max(32, pl.sym_chunk);
     auto ncc_of = [&](int64_t a) { return (ncol[size_t(a)] + C - 1) / C; };
     // row tiles per group: as many as keep group rows x chunk columns near the share
@@ -740,17 +768,17 @@ void build_sym_near(Plan& pl, int64_t lb, int64_t le) {
         return std::clamp(int32_t(pl.sym_fair / tile), 1, nrt_of(na));
     };
     auto nrg_of = [&](int64_t a) { return (nrt_of(nsrc(a)) + gsz_of(a) - 1) / gsz_of(a); };
-    // pass 2: slot layout per leaf (own chunks, own row tiles, then per owning
-    // neighbour in slot order its row tiles) and partial bases
+    // slot layout per big leaf (own chunks, own row groups, then per owning
+    // neighbour in slot order its row groups) and partial bases
     std::vector<int32_t> nslot(size_t(nleaf), 0);
     std::vector<int64_t> pbase(size_t(nleaf) + 1, 0);
     for (int64_t a = 0; a < nleaf; ++a) {
         const int32_t na = nsrc(a);
-        if (na) {
+        if (big(a)) {
             int32_t k = ncc_of(a) + nrg_of(a);
             for (int sl = 0; sl < 9; ++sl) {
                 const int64_t b = sl == 4 ? -1 : neighbour(a, sl);
-                if (b >= 0 && nsrc(b) && owns(b, a)) k += nrg_of(b);
+                if (b >= 0 && owns(b, a)) k += nrg_of(b);
             }
             nslot[size_t(a)] = k;
         }
@@ -761,7 +789,7 @@ void build_sym_near(Plan& pl, int64_t lb, int64_t le) {
         int32_t k = ncc_of(b) + nrg_of(b);
         for (int sl = 0; sl < 9; ++sl) {
             const int64_t o = sl == 4 ? -1 : neighbour(b, sl);
-            if (o < 0 || !nsrc(o) || !owns(o, b)) continue;
+            if (o < 0 || !owns(o, b)) continue;
             if (o == a) return k;
             k += nrg_of(o);
         }
@@ -772,15 +800,14 @@ void build_sym_near(Plan& pl, int64_t lb, int64_t le) {
     std::vector<SymLeaf> leaves;
     for (int64_t a = 0; a < nleaf; ++a) {
         const int32_t na = nsrc(a);
-        if (!na) continue;
-
+        if (!big(a)) continue;
         std::vector<SymRange> mine{SymRange{so[size_t(a)], 0, na, 0,
                                             pbase[size_t(a)] + int64_t(ncc_of(a)) * na}};
         bool touches = in(a);
         int32_t off = na;
         for (int sl = 0; sl < 9; ++sl) {
             const int64_t b = sl == 4 ? -1 : neighbour(a, sl);
-            if (b < 0 || !nsrc(b) || !owns(a, b)) continue;
+            if (b < 0 || !owns(a, b)) continue;
             mine.push_back(SymRange{so[size_t(b)], off, nsrc(b), 0,
                                     pbase[size_t(b)] + int64_t(col_slot(b, a)) * nsrc(b)});
             off += nsrc(b);
@@ -797,13 +824,51 @@ void build_sym_near(Plan& pl, int64_t lb, int64_t le) {
                                         std::min(ncol[size_t(a)], (cc + 1) * C), rfirst, int32_t(mine.size()),
                                         pbase[size_t(a)] + int64_t(cc) * na, rg, r2});
     }
-    // every leaf of the range with targets: matched ones from the slots,
-    // unmatched ones one-sided over the 3x3 source ranges (sym_finalize_kernel)
+    // full form: every leaf of the range with targets -- matched ones from
+    // the slots, unmatched ones one-sided (sym_finalize_kernel).  Hybrid: the
+    // big leaves' matched targets add their slots to what the one-sided
+    // kernel wrote (out +=); that kernel takes every target, over the 3x3
+    // ranges minus the symmetric pairs (big leaves' matched targets) or all
+    // of them (small leaves, unmatched targets).
+    std::vector<P2PChunk> hyb;
+    std::vector<int2> hranges;
     for (const LeafNear& ln : pl.h_leafnear) {
-        const int32_t na = nsrc(ln.leaf);
-        leaves.push_back(SymLeaf{pbase[size_t(ln.leaf)], ln.t0, na, nslot[size_t(ln.leaf)], ln.t1, ln.rfirst,
-                                 ln.rcount});
+        const int64_t x = ln.leaf;
+        const int32_t na = nsrc(x);
+        if (!hybrid || big(x))
+            leaves.push_back(SymLeaf{pbase[size_t(x)], ln.t0, hybrid ? na : na, nslot[size_t(x)], ln.t1, ln.rfirst,
+                                     ln.rcount});
+        if (!hybrid) continue;
+        for (int part = 0; part < 2; ++part) {  // 0: matched targets, 1: unmatched
+            const int32_t t0 = part == 0 ? ln.t0 : ln.t0 + na, t1 = part == 0 ? ln.t0 + na : ln.t1;
+            if (t1 <= t0) continue;
+            const int32_t rfirst = int32_t(hranges.size());
+            int32_t rself = 0;
+            int64_t near_src = 0;
+            const int ix = int(squash2(uint32_t(x))), iy = int(squash2(uint32_t(x) >> 1));
+            for (int jy = std::max(0, iy - 1); jy <= std::min(nb - 1, iy + 1); ++jy)  // summation.cpp:330-334
+                for (int jx = std::max(0, ix - 1); jx <= std::min(nb - 1, ix + 1); ++jx) {
+                    const int64_t y = mort(uint32_t(jx), uint32_t(jy));
+                    if (part == 0 && big(x) && big(y)) continue;  // symmetric pair
+                    if (jx == ix && jy == iy) rself = int32_t(hranges.size()) - rfirst;
+                    hranges.push_back(make_int2(so[size_t(y)], nsrc(y)));
+                    near_src += nsrc(y);
+                }
+            const int32_t rcount = int32_t(hranges.size()) - rfirst;
+            for (int32_t t = t0; t < t1; t += 64)
+                hyb.push_back(P2PChunk{t, std::min(64, t1 - t), int32_t(std::min<int64_t>(near_src, INT32_MAX)), rfirst,
+                                       rcount, rself, ln.lfirst, ln.lcount, 0, 1, -1, -1});
+        }
     }
+    if (hybrid) {
+        auto ccost = [](const P2PChunk& c) { return int64_t(c.pad) * c.tcount; };
+        std::stable_sort(hyb.begin(), hyb.end(),
+                         [&](const P2PChunk& a, const P2PChunk& b) { return ccost(a) > ccost(b); });
+        to_device(pl.hyb_chunks, hyb, 0);
+        to_device(pl.hyb_ranges, hranges, 0);
+    }
+    pl.n_hyb_chunks = hybrid ? int64_t(hyb.size()) : 0;
+    pl.sym_hybrid = hybrid;
     auto cost = [](const SymTask& t) { return int64_t(t.c1 - t.c0) * (t.r1 - t.r0); };
     std::stable_sort(tasks.begin(), tasks.end(),
                      [&](const SymTask& x, const SymTask& y) { return cost(x) > cost(y); });
