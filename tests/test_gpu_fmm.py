@@ -281,15 +281,20 @@ def test_near_field_zero_and_subnormal_pairs(vp, rest, mode):
     assert np.allclose(gpu[400:403], cpu[400:403], rtol=1e-12, atol=0)
 
 
-@pytest.mark.parametrize("sym", ["0", "1"])
-def test_symmetric_near_field(vp, rest, monkeypatch, sym):
+@pytest.mark.parametrize("sym,smin", [("0", None), ("1", "0"), ("1", "64")])
+def test_symmetric_near_field(vp, rest, monkeypatch, sym, smin):
     """'Targets = nodes' plans may evaluate each unordered near pair once
-    (plan.cuh SymTask).  Forced on and off, cfg2 (nodes + 10,000 unmatched
-    targets) matches the oracle, and shards still assemble bit-exactly."""
+    (plan.cuh SymTask), for every pair (VPG_SYM_MIN=0) or only for pairs of
+    leaves with >= 64 sources (hybrid).  Off, full and hybrid, cfg2 (nodes +
+    10,000 unmatched targets) matches the oracle, and shards still assemble
+    bit-exactly."""
     from paper_2203_05933_b200 import multigpu
     monkeypatch.setenv("VPG_SYM", sym)
+    if smin is not None:
+        monkeypatch.setenv("VPG_SYM_MIN", smin)
     w = W.cfg2()
     with vp.SummationPlan(lap(vp), w.src, w.tgt, 1e-12) as plan:
+        assert plan.info()["near_symmetric"] == (1 if sym == "1" else 0)
         gpu = plan.apply(w.q)
         total = np.zeros_like(gpu)
         for r in range(3):
