@@ -43,6 +43,12 @@ __device__ inline void box_center(double x0, double y0, double s, uint32_t id,
 constexpr int kP2MWarps = 4;
 constexpr int kP2MSrc = 16;
 
+#ifndef VPG_P2M_SRC
+#define VPG_P2M_SRC 16
+#endif
+constexpr int kP2MSrcRound = VPG_P2M_SRC;        // sources per round: 16 (2 lanes each) or 8 (4 lanes each)
+constexpr int kP2MLanes = 32 / kP2MSrcRound;     // lanes per source, each a contiguous share of k
+
 __global__ void __launch_bounds__(kP2MWarps * 32)
 p2m_kernel(const P2MItem* items, int64_t nitems, const int32_t* sorted_unused,
            const double2* sxy, const double* q, int P, double x0, double y0, double side,
@@ -55,31 +61,31 @@ p2m_kernel(const P2MItem* items, int64_t nitems, const int32_t* sorted_unused,
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t li = int64_t(blockIdx.x) * kP2MWarps + warp;
     if (li >= nitems) return;
-    double2* panel = panels + warp * kP2MSrc * n;
+    double2* panel = panels + warp * kP2MSrcRound * n;
     const P2MItem it = items[li];
     const double s = side / double(1 << it.level);
     double cx, cy;
     box_center(x0, y0, s, uint32_t(it.box), cx, cy);
     const double inv_s = 1.0 / s;
     const int e0 = it.e0, e1 = it.e1;
-    const int j = lane & (kP2MSrc - 1), h = lane >> 4;
-    const int kh = (P + 1) >> 1;
+    const int j = lane & (kP2MSrcRound - 1), h = lane / kP2MSrcRound;
+    const int kq = (P + kP2MLanes - 1) / kP2MLanes;  // powers per lane share
     double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
-    for (int base = e0; base < e1; base += kP2MSrc) {
-        const int cnt = min(kP2MSrc, e1 - base);
+    for (int base = e0; base < e1; base += kP2MSrcRound) {
+        const int cnt = min(kP2MSrcRound, e1 - base);
         if (j < cnt) {
             const double2 p = sxy[base + j];
             const double wr = (p.x - cx) * inv_s, wi = (p.y - cy) * inv_s;
             const double qj = q[base + j];
             double2* row = panel + j * n;
             double pr = qj, pi = 0.0;
-            int k0 = 1, k1 = kh;
+            const int k0 = h * kq + 1, k1 = min((h + 1) * kq, P);
             if (h == 0) {
                 row[0] = make_double2(qj, 0.0);
             } else {
-                // q w^kh by binary powering
+                // q w^(k0 - 1) by binary powering
                 double br = wr, bi = wi;
-                for (int e = kh; e; e >>= 1) {
+                for (int e = k0 - 1; e; e >>= 1) {
                     if (e & 1) {
                         const double nr = pr * br - pi * bi;
                         pi = pr * bi + pi * br;
@@ -89,8 +95,6 @@ p2m_kernel(const P2MItem* items, int64_t nitems, const int32_t* sorted_unused,
                     bi = 2.0 * br * bi;
                     br = sr;
                 }
-                k0 = kh + 1;
-                k1 = P;
             }
             for (int k = k0; k <= k1; ++k) {
                 const double nr = pr * wr - pi * wi;
@@ -1785,7 +1789,7 @@ void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const L
     double2* partial = w.p2m_partial;
     if (pl.n_p2m_items > 0) {
         launch_pdl(p2m_kernel, dim3(nblk(pl.n_p2m_items, kP2MWarps)), dim3(kP2MWarps * 32),
-                   size_t(kP2MWarps) * kP2MSrc * n * sizeof(double2), st, (const P2MItem*)pl.p2m_items.p,
+                   size_t(kP2MWarps) * kP2MSrcRound * n * sizeof(double2), st, (const P2MItem*)pl.p2m_items.p,
                    pl.n_p2m_items, (const int32_t*)nullptr, (const double2*)pl.src_sorted.p, (const double*)qs,
                    P, pl.x0, pl.y0, pl.side, mult, partial);
         ++launches;
