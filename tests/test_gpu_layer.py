@@ -136,3 +136,19 @@ def test_device_pointer_path(vp):
                                 allow_close=True, stream=st.cuda_stream)
     st.synchronize()
     assert np.array_equal(out.cpu().numpy(), host)
+
+
+def test_minimal_curve_and_large_lambda(vp, rest):
+    """n = 16 nodes (the smallest system assemble_nystrom accepts) and
+    lambda = 40 (K1 underflow far from the curve) against the restatement."""
+    sys = W.layer_system(n=16)
+    cf = W.layer_density(sys, seed=12, modes=4)
+    tg = _targets(sys, 300, 100, seed=13)
+    assert rel_l2(vp.eval_layer_potential(sys, cf, tg, allow_close=True), _ref(rest, sys, cf, tg, True)) <= 1e-13
+    k = vp.make_kernel(vp.KernelFamily.ModifiedHelmholtz, 40.0)
+    sysh = W.layer_system(k)
+    cfh = W.layer_density(sysh, seed=14)
+    tgh = _targets(sysh, 300, 100, seed=15)
+    gpu = vp.eval_layer_potential(sysh, cfh, tgh, allow_close=True)
+    cpu = _ref(rest, sysh, cfh, tgh, True)
+    assert rel_l2(gpu, cpu) <= 1e-12

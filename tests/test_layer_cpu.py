@@ -73,3 +73,42 @@ def test_layer_workload_shapes():
     sys, cf, tg = W.layer_cfg2()
     assert sys.curves[0].n == 362  # ceil(40 * 9.0172) = 361 -> even
     assert cf.shape == (362,) and tg.shape == (245136, 2)
+
+
+def test_restatement_coarse_rule_matches_numpy(rest):
+    """Far from the curve the evaluation is the plain trapezoidal sum
+    (bie.cpp:437-441): an independent numpy statement of dlp_entry
+    (bie.cpp:43-50) agrees with the C++ restatement."""
+    sys = W.layer_system()
+    cf = W.layer_density(sys, seed=3)
+    c = sys.curves[0]
+    rng = np.random.default_rng(8)
+    th = rng.uniform(0, 2 * np.pi, 300)
+    tg = np.stack([np.cos(th), np.sin(th)], 1) * rng.uniform(0.0, 0.45, 300)[:, None]
+    out, rc = rest.layer_eval(0, 0.0, sys.curves, sys.n_density, sys.n_aux, cf, tg, False)
+    assert rc == 0
+    d = c.x[None, :, :] - tg[:, None, :]
+    r2 = (d ** 2).sum(axis=2)
+    dn = (d * c.normal[None, :, :]).sum(axis=2)
+    dlp = -dn / (2 * np.pi * r2) * c.speed[None, :]
+    ref = (2 * np.pi / c.n) * (dlp * cf[None, :c.n]).sum(axis=1)
+    assert np.max(np.abs(out - ref)) <= 1e-13 * np.max(np.abs(ref))
+
+
+def test_restatement_helmholtz_coarse_rule_matches_scipy(rest):
+    """The modified-Helmholtz double layer -(lambda/2pi) K1(lambda r) dn/r
+    speed (bie.cpp:47-49) against scipy's K1, away from the curve."""
+    sp = pytest.importorskip("scipy.special")
+    k = bie.Kernel(bie.KernelFamily.ModifiedHelmholtz, 10.0)
+    sys = W.layer_system(k)
+    cf = W.layer_density(sys, seed=4)
+    c = sys.curves[0]
+    tg = np.array([[0.0, 0.0], [0.2, -0.1], [-0.3, 0.25]])
+    out, rc = rest.layer_eval(1, 10.0, sys.curves, sys.n_density, sys.n_aux, cf, tg, False)
+    assert rc == 0
+    d = c.x[None, :, :] - tg[:, None, :]
+    r = np.sqrt((d ** 2).sum(axis=2))
+    dn = (d * c.normal[None, :, :]).sum(axis=2)
+    dlp = -(10.0 / (2 * np.pi)) * sp.k1(10.0 * r) * (dn / r) * c.speed[None, :]
+    ref = (2 * np.pi / c.n) * (dlp * cf[None, :c.n]).sum(axis=1)
+    assert np.max(np.abs(out - ref)) <= 1e-12 * np.max(np.abs(ref))
