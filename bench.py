@@ -233,7 +233,7 @@ def run_gpu(args):
 
     wl = load_workload(args.workload)
     kern = kernel_for(wl)
-    eps = min(wl.eps)
+    eps = args.eps if args.eps else min(wl.eps)
     plan = vp.SummationPlan(kern, wl.src, wl.tgt, eps, mode=args.mode, device=local)
     shard = None
     if world > 1:
@@ -602,6 +602,8 @@ def main():
     ap.add_argument("--mode", default="reference", choices=["reference", "native"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--eps", type=float, default=None,
+                    help="FMM tolerance (default: the workload's tightest; cfg4 names 1e-6, 1e-9, 1e-12)")
     args = ap.parse_args()
     if args.workload == "layer":
         return run_layer(args)

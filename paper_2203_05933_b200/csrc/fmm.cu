@@ -61,7 +61,8 @@ p2m_kernel(const P2MItem* items, int64_t nitems, const int32_t* sorted_unused,
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t li = int64_t(blockIdx.x) * kP2MWarps + warp;
     if (li >= nitems) return;
-    double2* panel = panels + warp * kP2MSrcRound * n;
+    const int ps = n | 1;  // panel row stride: odd in double2 (an even n puts every row in one bank group)
+    double2* panel = panels + warp * kP2MSrcRound * ps;
     const P2MItem it = items[li];
     const double s = side / double(1 << it.level);
     double cx, cy;
@@ -77,7 +78,7 @@ p2m_kernel(const P2MItem* items, int64_t nitems, const int32_t* sorted_unused,
             const double2 p = sxy[base + j];
             const double wr = (p.x - cx) * inv_s, wi = (p.y - cy) * inv_s;
             const double qj = q[base + j];
-            double2* row = panel + j * n;
+            double2* row = panel + j * ps;
             double pr = qj, pi = 0.0;
             const int k0 = h * kq + 1, k1 = min((h + 1) * kq, P);
             if (h == 0) {
@@ -108,12 +109,12 @@ p2m_kernel(const P2MItem* items, int64_t nitems, const int32_t* sorted_unused,
         __syncwarp();
         for (int t = 0; t < cnt; ++t) {
             if (lane <= P) {
-                const double2 v0 = panel[t * n + lane];
+                const double2 v0 = panel[t * ps + lane];
                 acc0.x += v0.x;
                 acc0.y += v0.y;
             }
             if (lane + 32 <= P) {
-                const double2 v1 = panel[t * n + lane + 32];
+                const double2 v1 = panel[t * ps + lane + 32];
                 acc1.x += v1.x;
                 acc1.y += v1.y;
             }
@@ -1332,7 +1333,8 @@ p2l_kernel(const int4* work, int64_t nwork, const int2* ranges, const double2* s
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t wi = int64_t(blockIdx.x) * kP2MWarps + warp;
     if (wi >= nwork) return;
-    double2* panel = panels + warp * kP2MSrc * n;
+    const int ps = n | 1;  // odd row stride (see p2m_kernel)
+    double2* panel = panels + warp * kP2MSrc * ps;
     const int4 w = work[wi];
     const int r = w.x;
     const double s = side / double(1 << row_level[r]);
@@ -1352,7 +1354,7 @@ p2l_kernel(const int4* work, int64_t nwork, const int2* ranges, const double2* s
                 const double inv = s / d2;
                 const double vr = dx * inv, vi = -dy * inv;  // s / (z_j - c)
                 const double qj = q[base + j];
-                double2* row = panel + j * n;
+                double2* row = panel + j * ps;
                 double pr = qj, pi = 0.0;
                 int k0 = 1, k1 = kh;
                 if (h == 0) {
@@ -1384,12 +1386,12 @@ p2l_kernel(const int4* work, int64_t nwork, const int2* ranges, const double2* s
             __syncwarp();
             for (int t = 0; t < cnt; ++t) {
                 if (lane <= P) {
-                    const double2 v0 = panel[t * n + lane];
+                    const double2 v0 = panel[t * ps + lane];
                     acc0.x += v0.x;
                     acc0.y += v0.y;
                 }
                 if (lane + 32 <= P) {
-                    const double2 v1 = panel[t * n + lane + 32];
+                    const double2 v1 = panel[t * ps + lane + 32];
                     acc1.x += v1.x;
                     acc1.y += v1.y;
                 }
@@ -1789,7 +1791,7 @@ void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const L
     double2* partial = w.p2m_partial;
     if (pl.n_p2m_items > 0) {
         launch_pdl(p2m_kernel, dim3(nblk(pl.n_p2m_items, kP2MWarps)), dim3(kP2MWarps * 32),
-                   size_t(kP2MWarps) * kP2MSrcRound * n * sizeof(double2), st, (const P2MItem*)pl.p2m_items.p,
+                   size_t(kP2MWarps) * kP2MSrcRound * (n | 1) * sizeof(double2), st, (const P2MItem*)pl.p2m_items.p,
                    pl.n_p2m_items, (const int32_t*)nullptr, (const double2*)pl.src_sorted.p, (const double*)qs,
                    P, pl.x0, pl.y0, pl.side, mult, partial);
         ++launches;
@@ -1839,7 +1841,7 @@ void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const L
     }
     if (pl.n_p2l_work > 0) {
         launch_pdl(p2l_kernel, dim3(nblk(pl.n_p2l_work, kP2MWarps)), dim3(kP2MWarps * 32),
-                   size_t(kP2MWarps) * kP2MSrc * n * sizeof(double2), st, (const int4*)pl.p2l_work.p,
+                   size_t(kP2MWarps) * kP2MSrc * (n | 1) * sizeof(double2), st, (const int4*)pl.p2l_work.p,
                    pl.n_p2l_work, (const int2*)pl.p2l_ranges.p, (const double2*)pl.src_sorted.p,
                    (const double*)qs, (const int32_t*)pl.row_level.p, (const int32_t*)pl.row_morton.p, P,
                    pl.x0, pl.y0, pl.side, loc);
