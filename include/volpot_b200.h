@@ -250,7 +250,9 @@ int vpg_layer_create(int family, double lambda, const vpg_curve_block* curves,
  * targets nt interleaved xy.  Errors with the reference messages:
  * "eval_layer_potential: coefficient length mismatch", "... target lies on a
  * boundary node", "... target inside the close-evaluation collar ..."
- * (VPG_ERR_INVALID_ARGUMENT; the on-node error wins when both occur). */
+ * (VPG_ERR_INVALID_ARGUMENT; the on-node error wins when both occur).
+ * The call always synchronises its stream before returning: the reject
+ * rules are decided on the device and reported through the status. */
 int vpg_layer_eval(const vpg_layer* layer, const double* coeffs,
                    int64_t ncoeffs, const double* tgt_xy, int64_t nt,
                    int allow_close, double* out, unsigned flags, void* stream);
