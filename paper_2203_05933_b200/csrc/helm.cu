@@ -406,6 +406,11 @@ struct HfLevels {
 // entry (the per-entry form was L2-bandwidth bound).
 constexpr int kHfTile = 64;
 
+#ifndef VPG_HF_KUNROLL
+#define VPG_HF_KUNROLL 16
+#endif
+constexpr int kHfKUnroll = VPG_HF_KUNROLL;  // k-loop unroll of the tensor-core M2L
+
 __global__ void __launch_bounds__(256)
 hf_m2l_tc_kernel(const int4* tiles, const int32_t* tbox, const int32_t* srcof, const double* C,
                  const double* Wt, double* Lt, double* Lpart) {
@@ -456,7 +461,7 @@ hf_m2l_tc_kernel(const int4* tiles, const int32_t* tbox, const int32_t* srcof, c
         for (int r = 0; r < kWR; ++r) ws[wj * kWS + wt0 + 4 * r] = wreg[r];
         __syncthreads();
         if (o + 1 < o1) fetch(o + 1);
-#pragma unroll 4
+#pragma unroll kHfKUnroll
         for (int k4 = 0; k4 < k; k4 += 4) {
             const double a = cs[(k4 + kq) * kCS + 8 * warp + rq];
 #pragma unroll
