@@ -410,6 +410,10 @@ constexpr int kHfTile = 64;
 #define VPG_HF_KUNROLL 16
 #endif
 constexpr int kHfKUnroll = VPG_HF_KUNROLL;  // k-loop unroll of the tensor-core M2L
+#ifndef VPG_HF_NEAR_UNROLL
+#define VPG_HF_NEAR_UNROLL 2
+#endif
+constexpr int kHfNearUnroll = VPG_HF_NEAR_UNROLL;  // source-loop unroll of the K0 near field
 
 __global__ void __launch_bounds__(256)
 hf_m2l_tc_kernel(const int4* tiles, const int32_t* tbox, const int32_t* srcof, const double* C,
@@ -611,7 +615,7 @@ hf_l2p_p2p_kernel(HfLevels hl, const P2PChunk* chunks, int64_t nchunks, const in
                         sp = sxy[base + lane];
                         qj = q[base + lane];
                     }
-#pragma unroll 2
+#pragma unroll kHfNearUnroll
                     for (int j = 0; j < cnt; ++j) {
                         const double px = __shfl_sync(0xffffffffu, sp.x, j);
                         const double py = __shfl_sync(0xffffffffu, sp.y, j);

@@ -44,6 +44,10 @@ constexpr int kFineFactor = 8;      // bie.cpp:18
 constexpr double kFineReach = 5.0;  // bie.cpp:19
 constexpr double kCollarFraction = 0.02;  // bie.cpp:20
 constexpr int kLayerTile = 256;  // records per smem tile
+#ifndef VPG_LAYER_UNROLL
+#define VPG_LAYER_UNROLL 4
+#endif
+constexpr int kLayerUnroll = VPG_LAYER_UNROLL;
 #ifndef VPG_LAYER_CT
 #define VPG_LAYER_CT 256
 #endif
@@ -187,7 +191,7 @@ __device__ __forceinline__ void tile_sum(const double4* rec, int r0, int r1, con
         for (int i = threadIdx.x; i < cnt; i += blockDim.x) sm[i] = rec[b + i];
         __syncthreads();
         if (!active) continue;
-#pragma unroll 4
+#pragma unroll kLayerUnroll
         for (int k = 0; k < cnt; ++k) {
             const double4 r = sm[k];
 #pragma unroll
