@@ -454,6 +454,13 @@ def _layer_pairs(sys, tgt):
     return coarse, fine
 
 
+def _layer_kernel(workload):
+    import paper_2203_05933_b200 as vp
+    if workload == "layer_mh":  # configs[4]'s lambda on the configs[1] boundary
+        return vp.make_kernel(vp.KernelFamily.ModifiedHelmholtz, 10.0)
+    return vp.make_kernel(vp.KernelFamily.Laplace)
+
+
 def run_layer(args):
     import torch
 
@@ -465,16 +472,17 @@ def run_layer(args):
         if rank != 0:
             return 0
         import oracle
-        sys_, cf, tg = W.layer_cfg2()
+        sys_, cf, tg = W.layer_cfg2(_layer_kernel(args.workload))
+        fam, lam = int(sys_.kernel.family), sys_.kernel.lam
         rest = oracle.restatement()
         cores = os.cpu_count() or 1
         sub = tg[:: max(1, len(tg) // 60000)]
         for _ in range(args.warmup):
-            rest.layer_eval(0, 0.0, sys_.curves, sys_.n_density, sys_.n_aux, cf, sub, True, cores)
+            rest.layer_eval(fam, lam, sys_.curves, sys_.n_density, sys_.n_aux, cf, sub, True, cores)
         times = []
         for _ in range(args.steps):
             t0 = time.perf_counter()
-            rest.layer_eval(0, 0.0, sys_.curves, sys_.n_density, sys_.n_aux, cf, sub, True, cores)
+            rest.layer_eval(fam, lam, sys_.curves, sys_.n_density, sys_.n_aux, cf, sub, True, cores)
             times.append(time.perf_counter() - t0)
         co, fi = _layer_pairs(sys_, sub)
         t = float(np.mean(times))
@@ -483,7 +491,7 @@ def run_layer(args):
             "impl": "reference", "metric": LAYER_METRIC, "value": v, "unit": "interactions/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, configs[1] shapes)",
-            "config": {"workload": "layer", "nt": len(sub), "n_boundary": sys_.n_density},
+            "config": {"workload": args.workload, "nt": len(sub), "n_boundary": sys_.n_density},
             "cpu_baseline": {"value": v, "unit": "interactions/s", "cores": cores, "kind": "port",
                              "sample": f"every {max(1, len(tg) // 60000)}-th configs[1] target ({len(sub)}), "
                                        "oracle vo_layer_eval (bie.cpp:383-461 restated; bie.cpp needs Eigen)"},
@@ -495,7 +503,8 @@ def run_layer(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    sys_, cf, tg_all = W.layer_cfg2()
+    sys_, cf, tg_all = W.layer_cfg2(_layer_kernel(args.workload))
+    fam, lam = int(sys_.kernel.family), sys_.kernel.lam
     # targets are independent: rank r evaluates a contiguous slice, no collective
     lo, hi = len(tg_all) * rank // world, len(tg_all) * (rank + 1) // world
     tg = np.ascontiguousarray(tg_all[lo:hi])
@@ -556,23 +565,25 @@ def run_layer(args):
     tg = tg_all  # the whole job's pairs (all ranks)
     co, fi = _layer_pairs(sys_, tg)
     pairs = co + fi
-    achieved = pairs * LAYER_FLOPS[0] / (ms * 1e-3) / 1e12
+    achieved = pairs * LAYER_FLOPS[fam] / (ms * 1e-3) / 1e12
     peak = fp64_peak_tflops("fp64")
     line = {
         "metric": LAYER_METRIC, "value": pairs / (ms * 1e-3), "unit": "interactions/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, configs[1] shapes)",
-        "config": {"workload": "layer", "nt": len(tg), "n_boundary": sys_.n_density, "coarse_pairs": co,
+        "config": {"workload": args.workload, "nt": len(tg), "n_boundary": sys_.n_density, "coarse_pairs": co,
                    "fine_pairs": fi, "allow_close": True, "l2": "flushed (256 MB write) before every timed step",
-                   "step": "eval_layer_potential (bie.cpp:383-468), Laplace, star boundary"},
+                   "step": "eval_layer_potential (bie.cpp:383-468), "
+                           + ("Laplace" if fam == 0 else f"modified Helmholtz lambda={lam}") + ", star boundary"},
         "e2e": {"value": pairs / (e2e_ms * 1e-3), "unit": "interactions/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": 8 * cf.size + 16 * len(tg), "d2h_bytes_per_step": 8 * len(tg),
                 "path": "vpg_layer_eval with host arrays (wall clock, includes the reject readback)"},
         "gpu_launches": (4 + len(sys_.curves)) * args.steps,
         "roofline": {"bound": "fp64", "kernel": "coarse_kernel+fine_kernel", "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
-                     "flops_per_unit": "15 per evaluated (target, node) pair (2 sub, 3 r^2, 3 dn, 1 min, "
-                                       "4 reciprocal, 2 accumulate)"},
+                     "flops_per_unit": ("15 per evaluated (target, node) pair (2 sub, 3 r^2, 3 dn, 1 min, "
+                                        "4 reciprocal, 2 accumulate)") if fam == 0 else
+                                       "80 per evaluated (target, node) pair (K1 counted as 60 by convention)"},
         "clocks": clk.summary(),
     }
     if not args.no_cpu_baseline and world == 1:
@@ -581,7 +592,7 @@ def run_layer(args):
         cores = os.cpu_count() or 1
         sub = tg[:: max(1, len(tg) // 60000)]
         t0 = time.perf_counter()
-        rest.layer_eval(0, 0.0, sys_.curves, sys_.n_density, sys_.n_aux, cf, sub, True, cores)
+        rest.layer_eval(fam, lam, sys_.curves, sys_.n_density, sys_.n_aux, cf, sub, True, cores)
         t = time.perf_counter() - t0
         cs, fs = _layer_pairs(sys_, sub)
         line["cpu_baseline"] = {"value": (cs + fs) / t, "unit": "interactions/s", "cores": cores, "kind": "port",
@@ -598,14 +609,14 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "layer"])
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "layer", "layer_mh"])
     ap.add_argument("--mode", default="reference", choices=["reference", "native"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--eps", type=float, default=None,
                     help="FMM tolerance (default: the workload's tightest; cfg4 names 1e-6, 1e-9, 1e-12)")
     args = ap.parse_args()
-    if args.workload == "layer":
+    if args.workload in ("layer", "layer_mh"):
         return run_layer(args)
     if args.impl == "reference":
         return run_reference(args)
