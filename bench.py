@@ -2,12 +2,20 @@
 """FMM-step benchmark (BASELINE.json metric: source-target interactions/s, FP64).
 
 A step is one SummationPlan::apply (summation.cpp:610-643) of the workload:
-charges in -> potentials out at every target.  Throughput is counted as
-all-pairs-equivalent interactions, ns * nt per step (what a direct sum would
-evaluate); the per-kernel numbers (P2P pairs/s, M2L flop/s, fraction of the
-measured FP64 peak) explain it.
+charges in -> potentials out at every target.  The default workload is cfg4
+(BASELINE.json configs[3], 4,194,304 nodes: the largest configuration, one
+GPU) at eps = 1e-12.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2]
+Interactions per step: for Laplace tree plans, the near-field
+source-target pairs the reference enumerates (summation.cpp:330-344, the
+3x3-leaf lists of its uniform L = 7 tree including the skipped self pairs:
+9,563,275,264 at cfg4), the same count for both arms and both tree modes;
+value = those pairs / the whole FMM-step time (far field included), so the
+ratio to the reference arm is the step-time ratio.  Pairwise plans and the
+modified-Helmholtz treecode have no near-field list: there a step counts
+ns * nt.  kernels.p2p.pairs_per_s is the P2P-kernel-only rate.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg4]
     python bench.py --impl reference ...   # the reference CPU code (oracle/_ref)
 
 N > 1 runs under torchrun: every rank owns a Morton-contiguous shard of the
@@ -32,7 +40,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "source-target interactions/s (FP64) for the FMM step"
 FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peak_r01.json")
-DEFAULT_WORKLOAD = "cfg2"  # BASELINE.json configs[1]
+DEFAULT_WORKLOAD = "cfg4"  # BASELINE.json configs[3]: the largest config, fits one GPU
 
 THROTTLE_BITS = {
     0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
@@ -148,6 +156,14 @@ def dist_env():
     return world, rank, local
 
 
+def interaction_count(wl, levels, p2p_pairs):
+    """Interactions per step (module docstring): the reference near-field pair
+    count for Laplace tree plans, ns * nt otherwise."""
+    if wl.kernel == "laplace" and levels > 0:
+        return float(p2p_pairs), "near-field pairs of the reference tree (summation.cpp:330-344)"
+    return float(wl.ns) * float(wl.nt), "ns * nt (no near-field list: pairwise or treecode plan)"
+
+
 # ----------------------------------------------------------------- reference arm
 def run_reference(args):
     world, rank, _ = dist_env()
@@ -161,6 +177,13 @@ def run_reference(args):
     fam = 1 if wl.kernel == "helmholtz" else 0
     eps = min(wl.eps)
     plan = ref.plan(fam, wl.lam, wl.src, wl.tgt, eps)
+    levels = plan.levels()
+    pairs = 0
+    if fam == 0 and levels > 0:  # the reference tree's near-field count (restated binning, summation.cpp:81-129)
+        rest = oracle.restatement()
+        tr = rest.tree(wl.src, wl.tgt, eps)
+        pairs = rest.p2p_pairs(levels, tr["src_off"], tr["tgt_off"])
+    inter, counted = interaction_count(wl, levels, pairs)
     for _ in range(args.warmup):
         plan.apply(wl.q)
     times = []
@@ -169,7 +192,6 @@ def run_reference(args):
         plan.apply(wl.q)
         times.append(time.perf_counter() - t0)
     t = float(np.mean(times))
-    inter = float(wl.ns) * float(wl.nt)
     v = inter / t
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "interactions/s",
@@ -177,8 +199,9 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, BASELINE.json shapes)",
         "config": {"workload": args.workload, "ns": wl.ns, "nt": wl.nt, "epsilon": eps,
-                   "levels": plan.levels(), "order": plan.expansion_order(),
-                   "tree": "reference uniform quadtree"},
+                   "levels": levels, "order": plan.expansion_order(),
+                   "tree": "reference uniform quadtree",
+                   "interactions_per_step": inter, "interactions_counted": counted},
         "cpu_baseline": {"value": v, "unit": "interactions/s", "cores": cores, "kind": "reference",
                          "sample": f"{args.steps} full SummationPlan::apply of {args.workload} "
                                    f"(oracle/_ref = unmodified proj/src/summation.cpp, g++ -O3 "
@@ -190,7 +213,7 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------- GPU arm
-def cpu_baseline_sample(wl, budget_s=20.0):
+def cpu_baseline_sample(wl, inter, budget_s=20.0):
     """oracle/_ref on the host cores: full applies, bounded to ~budget_s."""
     import oracle
     try:
@@ -212,7 +235,7 @@ def cpu_baseline_sample(wl, budget_s=20.0):
         plan.apply(wl.q)
         times.append(time.perf_counter() - t0)
     t = float(np.median(times))
-    return {"value": float(wl.ns) * wl.nt / t, "unit": "interactions/s", "cores": cores,
+    return {"value": inter / t, "unit": "interactions/s", "cores": cores,
             "kind": "reference", "ms_per_step": t * 1e3,
             "sample": f"median of {n} full SummationPlan::apply of the workload after 1 warm-up "
                       f"(oracle/_ref, set_thread_count({cores}))"}
@@ -360,7 +383,12 @@ def run_gpu(args):
             dist.destroy_process_group()
         return 0
 
-    inter = float(wl.ns) * float(wl.nt)
+    ref_pairs = info["p2p_pairs"]
+    if args.mode == "native" and wl.kernel == "laplace":
+        # the workload's count is the reference tree's, whatever tree runs
+        with vp.SummationPlan(kern, wl.src, wl.tgt, eps, mode="reference", device=local) as rp:
+            ref_pairs = rp.info()["p2p_pairs"]
+    inter, counted = interaction_count(wl, info["levels"] if args.mode == "reference" else 1, ref_pairs)
     value = inter / (ms * 1e-3)
     P = info["expansion_order"]
     peak = fp64_peak_tflops()
@@ -412,6 +440,7 @@ def run_gpu(args):
         "config": {"workload": args.workload, "ns": wl.ns, "nt": wl.nt, "epsilon": eps,
                    "levels": info["levels"], "order": P, "mode": args.mode,
                    "parallelism": f"target-shard{world}" if world > 1 else "single",
+                   "interactions_per_step": inter, "interactions_counted": counted,
                    "l2": "flushed (256 MB write) before every timed step",
                    "step": ("operator apply: build_charges + FMM step + correction (potential.cpp:431-470)"
                             if op is not None else "FMM step: SummationPlan::apply (summation.cpp:610-643)")},
@@ -425,7 +454,7 @@ def run_gpu(args):
         "clocks": clk.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline_sample(wl)
+        line["cpu_baseline"] = cpu_baseline_sample(wl, inter)
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

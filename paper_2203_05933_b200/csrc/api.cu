@@ -173,7 +173,9 @@ struct CallStream {
         if (user) {
             s = static_cast<cudaStream_t>(user);
         } else {
-            VPG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+            // blocking: orders after work already queued on the legacy
+            // default stream (e.g. a q written there by the caller)
+            VPG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamDefault));
             owned = true;
         }
     }
@@ -195,38 +197,28 @@ struct Scratch {  // stream-ordered device scratch
 };
 
 // Graph-cached Laplace apply: the kernel sequence of laplace_issue is
-// captured once per (q, out) device-pointer pair (or once for host-pointer
-// applies, with staging buffers) into a CUDA graph and replayed with one
-// cudaGraphLaunch -- at ~0.7 ms per step the dozen launches and stream-
-// ordered allocations of a plain apply cost ~10%.  Up to kMaxGraphs entries
-// per plan, least recently used evicted.  Caller holds pl.graph_mu.
-constexpr size_t kMaxGraphs = 8;
+// captured into a CUDA graph and replayed with one cudaGraphLaunch -- at
+// ~0.5 ms per step the dozen launches and stream-ordered allocations of a
+// plain apply cost ~10%.  Entries are keyed by the (q, out) device pointers
+// they were captured for (host-pointer applies use the entry's own staging
+// buffers).  At most kMaxGraphs entries per plan, each with its persistent
+// workspace allocated once: a new pointer pair beyond that re-captures into
+// the least recently used entry of the same kind and patches its executable
+// in place (cudaGraphExecUpdate, in-flight launches unaffected), so steady
+// state applies with fresh output tensors never allocate, free or
+// instantiate.  Caller holds pl.graph_mu.
+constexpr size_t kMaxGraphs = 4;
 
 bool plan_is_sharded(const Plan& pl) {
     if (pl.adaptive) return pl.shard_t0 != 0 || pl.shard_t1 != pl.nt;
     return pl.shard_lb != 0 || pl.shard_le != (int64_t(1) << (2 * pl.L));
 }
 
-GraphEntry* graph_entry(const Plan& pl, const double* q, double* out, bool host) {
-    for (auto& e : pl.graphs)
-        if (e->host == host && e->q == q && e->out == out) return e.get();
-    if (pl.graphs.size() >= kMaxGraphs) {
-        auto it = std::min_element(pl.graphs.begin(), pl.graphs.end(),
-                                   [](const auto& a, const auto& b) { return a->last_use < b->last_use; });
-        pl.graphs.erase(it);
-    }
-    auto e = std::make_unique<GraphEntry>();
-    e->q = q;
-    e->out = out;
-    e->host = host;
-    VPG_CUDA(cudaMalloc(&e->work, laplace_work_bytes(pl)));
-    if (host) {
-        VPG_CUDA(cudaMalloc(&e->qstage, sizeof(double) * size_t(std::max<int64_t>(pl.ns, 1))));
-        VPG_CUDA(cudaMalloc(&e->ostage, sizeof(double) * size_t(std::max<int64_t>(pl.nt, 1))));
-    }
-    VPG_CUDA(cudaEventCreateWithFlags(&e->done, cudaEventDisableTiming));
-    const double* qd = host ? e->qstage : q;
-    double* od = host ? e->ostage : out;
+// Captures laplace_issue for e's pointers; nullptr when capture is not
+// supported here (the caller falls back to plain launches).
+static cudaGraph_t capture_apply(const Plan& pl, GraphEntry& e) {
+    const double* qd = e.host ? e.qstage : e.q;
+    double* od = e.host ? e.ostage : e.out;
     cudaStream_t cap = nullptr, side = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
     static const bool prio = [] {  // VPG_PRIO=0: equal priorities (A/B)
@@ -263,21 +255,73 @@ GraphEntry* graph_entry(const Plan& pl, const double* q, double* out, bool host)
             const char* v = std::getenv("VPG_NO_FORK");
             return v && v[0] == '1';
         }();
-        laplace_issue(pl, qd, od, laplace_work_at(pl, e->work), cap, nullptr, e->launches,
+        int64_t launches = 0;
+        laplace_issue(pl, qd, od, laplace_work_at(pl, e.work), cap, nullptr, launches,
                       no_fork ? nullptr : side, fork, join);
-    } catch (...) {  // not capturable here: the caller falls back to plain launches
+        e.launches = launches;
+    } catch (...) {
         cudaStreamEndCapture(cap, &g);
         if (g) cudaGraphDestroy(g);
         (void)cudaGetLastError();
         return nullptr;
     }
     VPG_CUDA(cudaStreamEndCapture(cap, &g));
-    const cudaError_t ie = cudaGraphInstantiate(&e->exec, g, prio ? cudaGraphInstantiateFlagUseNodePriority : 0);
-    cudaGraphDestroy(g);
+    return g;
+}
+
+static bool instantiate(GraphEntry& e, cudaGraph_t g) {
+    const cudaError_t ie = cudaGraphInstantiate(&e.exec, g, cudaGraphInstantiateFlagUseNodePriority);
     if (ie != cudaSuccess) {
         (void)cudaGetLastError();
-        return nullptr;  // caller falls back to plain launches
+        e.exec = nullptr;
+        return false;
     }
+    return true;
+}
+
+GraphEntry* graph_entry(const Plan& pl, const double* q, double* out, bool host) {
+    for (auto& e : pl.graphs)
+        if (e->host == host && e->q == q && e->out == out) return e.get();
+    GraphEntry* lru = nullptr;
+    size_t same_kind = 0;
+    for (auto& e : pl.graphs) {
+        if (e->host != host) continue;
+        ++same_kind;
+        if (!lru || e->last_use < lru->last_use) lru = e.get();
+    }
+    if (lru && (same_kind >= kMaxGraphs - 1 || pl.graphs.size() >= kMaxGraphs)) {
+        // re-target the least recently used entry: same workspace, patched exec
+        lru->q = q;
+        lru->out = out;
+        cudaGraph_t g = capture_apply(pl, *lru);
+        if (!g) return nullptr;
+        cudaGraphExecUpdateResultInfo info;
+        bool ok = cudaGraphExecUpdate(lru->exec, g, &info) == cudaSuccess;
+        if (!ok) {
+            (void)cudaGetLastError();
+            VPG_CUDA(cudaEventSynchronize(lru->done));  // not in flight before it goes
+            cudaGraphExecDestroy(lru->exec);
+            ok = instantiate(*lru, g);
+        }
+        cudaGraphDestroy(g);
+        if (!ok) return nullptr;
+        return lru;
+    }
+    auto e = std::make_unique<GraphEntry>();
+    e->q = q;
+    e->out = out;
+    e->host = host;
+    VPG_CUDA(cudaMalloc(&e->work, laplace_work_bytes(pl)));
+    if (host) {
+        VPG_CUDA(cudaMalloc(&e->qstage, sizeof(double) * size_t(std::max<int64_t>(pl.ns, 1))));
+        VPG_CUDA(cudaMalloc(&e->ostage, sizeof(double) * size_t(std::max<int64_t>(pl.nt, 1))));
+    }
+    VPG_CUDA(cudaEventCreateWithFlags(&e->done, cudaEventDisableTiming));
+    cudaGraph_t g = capture_apply(pl, *e);
+    if (!g) return nullptr;
+    const bool ok = instantiate(*e, g);
+    cudaGraphDestroy(g);
+    if (!ok) return nullptr;
     pl.graphs.push_back(std::move(e));
     return pl.graphs.back().get();
 }
@@ -394,7 +438,7 @@ int vpg_plan_apply(const vpg_plan* plan, const double* q, int64_t nq, double* ou
                 if (!dev && pl.nt)
                     VPG_CUDA(cudaMemcpyAsync(out, e->ostage, sizeof(double) * size_t(pl.nt), cudaMemcpyDeviceToHost, st));
                 VPG_CUDA(cudaEventRecord(e->done, st));
-                pl.last_launches = e->launches;
+                pl.last_launches.store(e->launches, std::memory_order_relaxed);
                 lk.unlock();
                 if (!(flags & VPG_NO_SYNC) || cs.owned) VPG_CUDA(cudaStreamSynchronize(st));
                 return;
@@ -445,7 +489,7 @@ int vpg_plan_apply(const vpg_plan* plan, const double* q, int64_t nq, double* ou
             for (int i = 0; i < VPG_PHASE_COUNT; ++i)
                 VPG_CUDA(cudaEventElapsedTime(&pl.phase_ms[i], ev[i], ev[i + 1]));
         }
-        pl.last_launches = launches;
+        pl.last_launches.store(launches, std::memory_order_relaxed);
     });
 }
 
@@ -493,7 +537,7 @@ int vpg_plan_phase_times(const vpg_plan* plan, float* ms) {
 int vpg_plan_last_launches(const vpg_plan* plan, int64_t* launches) {
     return guarded([&] {
         if (!plan || !launches) throw Error{VPG_ERR_INVALID_ARGUMENT, "NULL argument"};
-        *launches = plan->impl.last_launches;
+        *launches = plan->impl.last_launches.load(std::memory_order_relaxed);
     });
 }
 

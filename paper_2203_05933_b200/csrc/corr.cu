@@ -170,7 +170,9 @@ struct OwnStream {
         if (u) {
             s = static_cast<cudaStream_t>(u);
         } else {
-            VPG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+            // blocking: orders after work already queued on the legacy
+            // default stream (e.g. a q written there by the caller)
+            VPG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamDefault));
             owned = true;
         }
     }
@@ -241,6 +243,9 @@ int vpg_corr_create(int64_t nt, const int32_t* blk_off, int64_t nblocks,
                     const int32_t cell = blk_cell[k0], base = blk_pool[k0];
                     if (base + 63 >= npool) { ok = false; break; }
                     const int64_t p0 = pool_off[base];
+                    // the kernel stages M_q with 16-byte loads: an odd p0 would
+                    // be a misaligned access -- such groups take the CSR path
+                    if (p0 & 1) { ok = false; break; }
                     for (int64_t u = 0; ok && u < 64; ++u) {
                         const int64_t ku = blk_off[t0 + u] + r;
                         ok = blk_cell[ku] == cell && blk_pool[ku] == base + u && pool_off[base + u] == p0 + 64 * u &&

@@ -1446,10 +1446,12 @@ __global__ void gather_q(const double* q, const int32_t* ids, int64_t n, double*
 }  // namespace
 
 // ------------------------------------------------------------- operators --
-// Plan time: the (target, own-leaf source) pairs whose r^2 -- computed
-// exactly as in lap_pair_fast -- is zero or subnormal.  Warp per chunk
-// (first part of split chunks), lane per target; pass 1 counts (src ==
-// nullptr), pass 2 writes the sorted source indices at off.
+// Plan time: the (target, near source) pairs whose r^2 -- computed exactly
+// as in lap_pair_fast -- is zero or subnormal.  All of the chunk's near
+// ranges are scanned (exact duplicates share a leaf, but a pair closer than
+// 2^-511 can straddle a leaf edge).  Warp per chunk (first part of split
+// chunks), lane per target; pass 1 counts (src == nullptr), pass 2 writes
+// the sorted source indices at off.
 __global__ void coin_scan_kernel(const P2PChunk* chunks, int64_t nchunks, const int2* ranges,
                                  const double2* sxy, const double2* txy, int32_t* cnt,
                                  const int32_t* off, int32_t* src) {
@@ -1458,19 +1460,21 @@ __global__ void coin_scan_kernel(const P2PChunk* chunks, int64_t nchunks, const 
     if (w >= nchunks) return;
     const P2PChunk c = chunks[w];
     if (c.nparts > 1 && c.part != 0) return;
-    const int2 own = ranges[c.rfirst + c.rself];
     for (int u = lane; u < c.tcount; u += 32) {
         const int64_t ti = int64_t(c.tbegin) + u;
         const double2 t = txy[ti];
         int k = 0;
         const int base = src ? off[ti] : 0;
-        for (int j = 0; j < own.y; ++j) {
-            const double2 sp = sxy[own.x + j];
-            const double dx = t.x - sp.x, dy = t.y - sp.y;
-            const double r2 = fma(dy, dy, dx * dx);
-            if (__double2hiint(r2) < 0x00100000) {
-                if (src) src[base + k] = own.x + j;
-                ++k;
+        for (int r = 0; r < c.rcount; ++r) {
+            const int2 rg = ranges[c.rfirst + r];
+            for (int j = 0; j < rg.y; ++j) {
+                const double2 sp = sxy[rg.x + j];
+                const double dx = t.x - sp.x, dy = t.y - sp.y;
+                const double r2 = fma(dy, dy, dx * dx);
+                if (__double2hiint(r2) < 0x00100000) {
+                    if (src) src[base + k] = rg.x + j;
+                    ++k;
+                }
             }
         }
         if (!src) cnt[ti] = k;

@@ -430,7 +430,7 @@ int vpg_layer_eval(const vpg_layer* L, const double* coeffs, int64_t ncoeffs, co
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         bool owned = false;
         if (!s) {
-            VPG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+            VPG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamDefault));  // orders after the legacy stream
             owned = true;
         }
         struct SG {

@@ -4,6 +4,7 @@
 #pragma once
 
 #include <memory>
+#include <atomic>
 #include <mutex>
 #include <vector>
 
@@ -316,7 +317,7 @@ struct Plan {
     bool profiling = false;
     mutable std::mutex prof_mu;
     mutable float phase_ms[VPG_PHASE_COUNT] = {};
-    mutable int64_t last_launches = 0;
+    mutable std::atomic<int64_t> last_launches{0};  // written by concurrent applies
     // CUDA-graph cache of the apply (api.cu); declared last so it is torn
     // down before the buffers it references
     mutable std::mutex graph_mu;

@@ -324,3 +324,21 @@ def test_symmetric_near_field_duplicates_and_subnormal(vp, rest, monkeypatch, sy
     assert rel_l2(gpu, cpu) <= 1e-12
     n = len(src)
     assert np.allclose(gpu[n - 3:n], cpu[n - 3:n], rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("sym", ["0", "1"])
+def test_subnormal_pairs_across_leaf_edges(vp, rest, monkeypatch, sym):
+    """Points in a 1e-152 square: nearest neighbours are ~1e-155 apart, so
+    many near pairs have subnormal r^2, and with leaves ~3e-154 wide many of
+    them straddle a leaf edge.  The plan's coincidence scan covers every near
+    range (not just the own leaf), so each such pair gets the reference's
+    exact log (summation.cpp:340-341) in both near-field paths."""
+    monkeypatch.setenv("VPG_SYM", sym)
+    rng = np.random.default_rng(44)
+    pts = rng.uniform(0.0, 1e-152, (20_000, 2))
+    q = rng.standard_normal(len(pts))
+    with vp.SummationPlan(lap(vp), pts, pts, 1e-12) as plan:
+        assert plan.levels() > 0
+        gpu = plan.apply(q)
+    cpu = rest.plan_sum(0, 0.0, pts, q, pts, 1e-12)
+    assert rel_l2(gpu, cpu) <= 1e-13
