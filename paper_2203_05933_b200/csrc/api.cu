@@ -29,6 +29,7 @@ thread_local std::string t_err;
 std::mutex g_mu;
 struct DeviceTables {
     double2* log_tab = nullptr;
+    double2* log_tab2 = nullptr;  // fast_log's truncation table
     double* k0_tab = nullptr;
     double* k0f_tab = nullptr;
     double* k1_tab = nullptr;
@@ -81,6 +82,18 @@ static DeviceTables& tables_locked(int dev) {
         VPG_CUDA(cudaMalloc(&t.log_tab, sizeof(double2) * h.size()));
         VPG_CUDA(cudaMemcpy(t.log_tab, h.data(), sizeof(double2) * h.size(), cudaMemcpyHostToDevice));
     }
+    if (!t.log_tab2) {
+        // centres c = 1 + i/512 (fast_log): (RN(1/c), -ln RN(1/c) - i ln2/512)
+        std::vector<double2> h(kLogTableSize);
+        const long double ln2_512 = (long double)kLn2Over512;
+        for (int i = 0; i < kLogTableSize; ++i) {
+            const long double c = 1.0L + (long double)i / (kLogTableSize - 1);
+            const double inv = double(1.0L / c);
+            h[size_t(i)] = make_double2(inv, double(-std::log((long double)inv) - (long double)i * ln2_512));
+        }
+        VPG_CUDA(cudaMalloc(&t.log_tab2, sizeof(double2) * h.size()));
+        VPG_CUDA(cudaMemcpy(t.log_tab2, h.data(), sizeof(double2) * h.size(), cudaMemcpyHostToDevice));
+    }
     if (!t.k0_tab) {
         std::vector<double> h(size_t(kK0Intervals) * kK0Coeffs);
         k0_fit_host(h.data());
@@ -107,6 +120,16 @@ const double2* log_table_dev() {
     VPG_CUDA(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lk(g_mu);
     return tables_locked(dev).log_tab;
+}
+const double2* lap_log_table_dev() {
+#if VPG_LOG_FOLD
+    int dev = 0;
+    VPG_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_mu);
+    return tables_locked(dev).log_tab2;
+#else
+    return log_table_dev();
+#endif
 }
 const double* k0_fast_table_dev() {
     int dev = 0;
@@ -405,6 +428,7 @@ int vpg_plan_create(int family, double lambda, const double* src_xy, int64_t ns,
             }
         }
         (void)log_table_dev();
+        (void)lap_log_table_dev();
         (void)k0_table_dev();
         VPG_CUDA(cudaDeviceSynchronize());
         *plan = holder.release();

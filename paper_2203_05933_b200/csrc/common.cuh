@@ -159,6 +159,59 @@ __device__ __forceinline__ double fast_log_split(double x, uint32_t tab_lane, do
     return tc.y + fma(r2, p, r);
 }
 
+// ln(x) as one double, for the near-field loops: the same reduction as
+// fast_log_split, with the exponent term folded into the polynomial's
+// addend, w = e ln2 + (-ln RN(1/c)) (one DFMA, the product exact inside it),
+// and log1p by Horner in r (c_flog), so the last DFMA adds r p(r) to w:
+// ln x = fma(r, p, w), six FP64 instructions (fast_log_split plus combining
+// its split result: eight).  Error: truncation < 1.2e-17, p's rounding
+// scaled by |r| <= 2^-10, ln2's representation error times |e|, and two
+// roundings (w, the result): <= 1.3e-16 absolute for |ln x| < 1, <= 1.3
+// ulp above, exact 0 at x = 1 (mpmath check of this exact arithmetic over
+// 1e-30..1e3 and the interval edges).
+#ifndef VPG_LOG_FOLD
+#define VPG_LOG_FOLD 1
+#endif
+constexpr double kLn2 = 0.69314718055994530942;
+// The table of fast_log (lap_log_table_dev): the centres of fast_log_split,
+// c = 1 + i/512 (i = 0..512, the mantissa ROUNDED to its top 9 bits, |m/c -
+// 1| <= 2^-10, centre 0 exactly 1 so ln(2^k) = fl(k ln2) and ln 1 = 0 as
+// the SPEC examples need), entries (RN(1/c), -ln RN(1/c) - i ln2/512).  The
+// exponent goes in together with the index: with t = hi + half-an-index,
+// g = (t >> 11) - (0x3FF << 9) = e 512 + i exactly (a rounding carry into
+// the exponent field gives (e + 1) 512 + 0 = e 512 + 512, the same number),
+// and w = fma(g, ln2/512, entry) = e ln2 - ln RN(1/c), the product exact
+// inside the DFMA.  Integer side (8): IADD + LEA.HI for g, I2F.F64; the
+// mantissa word (LOP3) and, rounded, its index scaled to the 128-byte
+// entry stride (IADD, SHF, IMAD; bias folded into tab_lane as in
+// fast_log_split); the register-pair move for m.
+constexpr double kLn2Over512 = 0.69314718055994530942 / 512.0;
+// log1p(r) = r p(r), p = c1 + r(-1/2 + r(c3 - r/4)): the Taylor terms with
+// r^5/5 economised over |r| <= h = 2^-10 (Chebyshev: r^5 ~ (5/4)h^2 r^3 -
+// (5/16)h^4 r), c1 = 1 - h^4/16, c3 = 1/3 + h^2/4; truncation < 1.2e-17.
+// DFMA takes these as c[][] operands (no register materialisation).
+static __constant__ double c_flog[4] = {0.3333335717519124, kLn2Over512, -0.25, 0.99999999999994315658};
+__device__ __forceinline__ double fast_log(double x, uint32_t tab_lane) {
+    constexpr int kHalf = 1 << (19 - kLogTableBits);
+    const int hi = __double2hiint(x);
+    const int lo = __double2loint(x);
+    const double g = __int2double_rn(((hi + kHalf) >> 11) - (0x3FF << 9));
+    int mhi;
+    asm("lop3.b32 %0, %1, 0x000FFFFF, %2, 0xEA;" : "=r"(mhi) : "r"(hi), "r"(0x3FF00000));
+    uint32_t idx, addr;  // explicit shift + multiply-add: one IMAD, no mask
+    asm("shr.b32 %0, %1, 11;" : "=r"(idx) : "r"(mhi + kHalf));
+    asm("mad.lo.u32 %0, %1, 128, %2;" : "=r"(addr) : "r"(idx), "r"(tab_lane));
+    const double m = __hiloint2double(mhi, lo);
+    const double2 tc = lds_f64x2(addr);
+    const double r = fma(m, tc.x, -1.0);
+    const double w = fma(g, c_flog[1], tc.y);
+    double p = fma(r, c_flog[2], c_flog[0]);
+    p = fma(r, p, -0.5);
+    p = fma(r, p, c_flog[3]);
+    return fma(r, p, w);
+}
+static_assert(kLogTableBits == 9 && kLogTableCopies == 8, "fast_log assumes the 9-bit, 8-copy layout");
+
 // ----------------------------------------------- programmatic launches --
 // Kernels of one apply are chained with programmatic dependent launch: the
 // next grid may start (and stage its constant operators / tables) while the
@@ -255,7 +308,8 @@ void launch_coop(void (*kern)(KArgs...), int grid, dim3 block, size_t smem, cuda
 }
 
 // Per-device constant tables, built on first use (api.cu).
-const double2* log_table_dev();  // kLogTableSize entries (inv_c, -ln inv_c)
+const double2* log_table_dev();  // kLogTableSize entries (inv_c, -ln inv_c): fast_log_split
+const double2* lap_log_table_dev();  // the near-field table: fast_log's (VPG_LOG_FOLD=0: log_table_dev)
 const double* k0_table_dev();    // K0 Chebyshev fits, see k0.cuh
 const double* k1_table_dev();    // K1 Chebyshev fits (same layout)
 const double* k0_fast_table_dev();  // quarter-octave K0 fits (k0_fast)

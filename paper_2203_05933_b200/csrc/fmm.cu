@@ -1073,7 +1073,13 @@ l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, const int2* ranges,
 // coincidence list undoes it as in the one-sided kernel; neighbour columns
 // have j >= na > i).  Row sums are added to slot 4 of A's targets at the end
 // of each row tile, after the self-column sums of the earlier tiles.
-constexpr int kSymWarps = 8;
+#ifndef VPG_SYM_WARPS
+#define VPG_SYM_WARPS 8
+#endif
+#ifndef VPG_SYM_MINB
+#define VPG_SYM_MINB 2
+#endif
+constexpr int kSymWarps = VPG_SYM_WARPS;
 constexpr size_t kSymSmem = size_t(kLogTableBytes) + size_t(kSymWarps) * (64 * 16 + 64 * 8 + kSymMaxRanges * sizeof(SymRange));
 
 template <int R, bool kDiag>
@@ -1089,9 +1095,7 @@ __device__ __forceinline__ void sym_block(const double2* cxy, const double* cq, 
         for (int u = 0; u < R; ++u) {
             const double dx = rx[u] - sp.x, dy = ry[u] - sp.y;
             const double r2 = fma(dy, dy, dx * dx);
-            double ed;
-            const double t = fast_log_split(r2, tab_lane, ed);
-            const double v = fma(ed, kLn2Lo, fma(ed, kLn2Hi, t));
+            const double v = lap_log(r2, tab_lane);
             double qr = qc, qcol = rq[u];
             if (kDiag) {
                 const int i = i0 + lane + 32 * u, j = j0 + (c & 31);
@@ -1175,7 +1179,7 @@ __device__ __forceinline__ void sym_task(const SymTask& T, const SymRange* rng, 
     }
 }
 
-__global__ void __launch_bounds__(kSymWarps * 32, 2)
+__global__ void __launch_bounds__(kSymWarps * 32, VPG_SYM_MINB)
 p2p_sym_kernel(const SymTask* tasks, int64_t ntask, const SymRange* ranges, const double2* sxy, const double* q,
                const double2* gtab, int* ticket, double* part) {
     extern __shared__ double2 smp[];
@@ -1761,7 +1765,7 @@ void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const L
         launch_pdl(l2p_p2p_kernel, dim3(grid), dim3(kP2PWarps * 32), smem, s, nchunks, nnear,
                    nranges, (const double2*)pl.src_sorted.p, (const double*)qs,
                    (const double2*)pl.tgt_sorted.p, (const int32_t*)pl.tgt_ids.p, pl.coin_off.p,
-                   pl.coin_src.p, log_table_dev(), ticket, partial_p2p, pcount, out_dev,
+                   pl.coin_src.p, lap_log_table_dev(), ticket, partial_p2p, pcount, out_dev,
                    (quota > 0 && s != st) ? quota : INT32_MAX);
         ++launches;
     };
@@ -1776,7 +1780,7 @@ void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const L
                 const unsigned grid = unsigned(std::min<int64_t>(want, int64_t(pl.sm_count) * std::max(per_sm, 1)));
                 launch_pdl(p2p_sym_kernel, dim3(grid), dim3(kSymWarps * 32), kSymSmem, s,
                            (const SymTask*)pl.sym_tasks.p, pl.n_sym_tasks, (const SymRange*)pl.sym_ranges.p,
-                           (const double2*)pl.src_sorted.p, (const double*)qs, log_table_dev(), ticket,
+                           (const double2*)pl.src_sorted.p, (const double*)qs, lap_log_table_dev(), ticket,
                            w.sym_part);
                 ++launches;
             }
@@ -1788,7 +1792,7 @@ void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const L
                            (const SymLeaf*)pl.sym_leaves.p, pl.n_sym_leaves, (const double*)w.sym_part,
                            (const int2*)pl.near_ranges.p, (const double2*)pl.src_sorted.p,
                            (const double*)qs, (const double2*)pl.tgt_sorted.p, (const int32_t*)pl.tgt_ids.p,
-                           (const int32_t*)pl.coin_off.p, (const int32_t*)pl.coin_src.p, log_table_dev(),
+                           (const int32_t*)pl.coin_off.p, (const int32_t*)pl.coin_src.p, lap_log_table_dev(),
                            out_dev, pl.sym_hybrid ? 1 : 0);
                 ++launches;
             }

@@ -1,10 +1,10 @@
 // p2p.cuh -- the Laplace pair interaction shared by the near-field and
 // all-pairs kernels.
 //
-// One pair costs 14 FP64 instructions: dx, dy, r^2 (2), the exponent
-// conversion, the table reduction, the degree-5 log1p, and two
-// accumulations (sum q*t and sum q*e, so ln2 is applied once per target),
-// plus ~7 integer/LDS instructions (table address, mantissa, exponent).
+// One pair costs 11 FP64 instructions: dx, dy, r^2 (2), the table
+// reduction, the exponent term, the degree-4 log1p (4 with the addend) and
+// the accumulation, plus ~9 integer/LDS/conversion instructions (table
+// address, mantissa, exponent).
 #pragma once
 
 #include "common.cuh"
@@ -12,25 +12,33 @@
 namespace vpg {
 
 struct LapAcc {
-    double a = 0.0;  // sum q * t
-    double b = 0.0;  // sum q * e
+    double a = 0.0;  // sum q * ln(r2)  (VPG_LOG_FOLD=0: sum q * t)
+    double b = 0.0;  // VPG_LOG_FOLD=0 only: sum q * e
     double c = 0.0;  // rare-path sum q * log(r2) for subnormal r2
 };
 
-// Hot-loop pair: no zero test at all.  r^2 == 0 yields t = 0 and
-// e = -1023 (the pattern's exponent field is 0), i.e. a spurious -1023 q ln2
-// that the caller removes in a fix-up pass (lap_pair_fixup) over the pairs
-// that can be coincident -- for the near field, only sources of the
-// target's own leaf (equal coordinates fall in the same leaf).
+// One pair's contribution to the accumulators (the hot-loop form).
+__device__ __forceinline__ void lap_acc(double r2, double q, uint32_t tab_lane, LapAcc& acc) {
+#if VPG_LOG_FOLD
+    acc.a = fma(q, fast_log(r2, tab_lane), acc.a);
+#else
+    double ed;
+    const double t = fast_log_split(r2, tab_lane, ed);
+    acc.a = fma(q, t, acc.a);
+    acc.b = fma(q, ed, acc.b);
+#endif
+}
+
+// Hot-loop pair: no zero test at all.  r^2 == 0 yields ln = -1023 ln2 +
+// (table entry 0) -- a spurious term that the caller removes in a fix-up
+// pass (lap_pair_fixup) over the pairs that can be coincident or subnormal
+// (the plan's coincidence list).
 __device__ __forceinline__ void lap_pair_fast(double tx, double ty, double sx,
                                               double sy, double q, uint32_t tab_lane,
                                               LapAcc& acc) {
     const double dx = tx - sx, dy = ty - sy;
     const double r2 = fma(dy, dy, dx * dx);
-    double ed;
-    const double t = fast_log_split(r2, tab_lane, ed);
-    acc.a = fma(q, t, acc.a);
-    acc.b = fma(q, ed, acc.b);
+    lap_acc(r2, q, tab_lane, acc);
 }
 
 // Undoes lap_pair_fast for r^2 below the normal range and applies the
@@ -42,10 +50,7 @@ __device__ __forceinline__ void lap_pair_fixup(double tx, double ty, double sx,
     const double dx = tx - sx, dy = ty - sy;
     const double r2 = fma(dy, dy, dx * dx);
     if (__double2hiint(r2) >= 0x00100000) return;
-    double ed;
-    const double t = fast_log_split(r2, tab_lane, ed);
-    acc.a = fma(-q, t, acc.a);
-    acc.b = fma(-q, ed, acc.b);
+    lap_acc(r2, -q, tab_lane, acc);
     if (r2 != 0.0) acc.c = fma(q, log(r2), acc.c);
 }
 
@@ -62,15 +67,27 @@ __device__ __forceinline__ void lap_pair(double tx, double ty, double sx,
         if ((hi | __double2loint(r2)) != 0) acc.c = fma(q, log(r2), acc.c);
         qe = 0.0;
     }
-    double ed;
-    const double t = fast_log_split(r2, tab_lane, ed);
-    acc.a = fma(qe, t, acc.a);
-    acc.b = fma(qe, ed, acc.b);
+    lap_acc(r2, qe, tab_lane, acc);
 }
 
-// sum_j q_j log(r2_j) from the split accumulators.
+// sum_j q_j log(r2_j) from the accumulators.
 __device__ __forceinline__ double lap_total(const LapAcc& acc) {
+#if VPG_LOG_FOLD
+    return acc.a + acc.c;
+#else
     return fma(acc.b, kLn2Hi, fma(acc.b, kLn2Lo, acc.a)) + acc.c;
+#endif
+}
+
+// ln(r2) of the symmetric kernel: one double feeding both targets.
+__device__ __forceinline__ double lap_log(double r2, uint32_t tab_lane) {
+#if VPG_LOG_FOLD
+    return fast_log(r2, tab_lane);
+#else
+    double ed;
+    const double t = fast_log_split(r2, tab_lane, ed);
+    return fma(ed, kLn2Lo, fma(ed, kLn2Hi, t));
+#endif
 }
 
 }  // namespace vpg

@@ -276,7 +276,154 @@ def correction_csr(nbox_cells, box_ij, ntri_cells, seed=55, np_box=64, np_tri=64
             "node_off": node_off.astype(np.int32)}
 
 
-CONFIGS = {"cfg1": cfg1, "cfg2": cfg2, "cfg3": cfg3, "cfg4": cfg4, "cfg5": cfg5}
+def reference_correction_csr(box_ij, node_local, ntri_cells=0, np_tri=64, D=0.4, seed=56):
+    """Correction map with the reference's near rule and pool layout.
+
+    Targets are the mesh nodes in order (boxes, then triangles).  A box node
+    at local coordinates (a, b) in [-1, 1]^2 gets its self block and the
+    neighbour boxes closer than D h (classify_target, mesh.cpp:410-448,
+    D = 0.4 from mesh.hpp:52): the edge neighbour when (1 -+ a)/2 < D, the
+    corner neighbour when both edge distances put it within D h of the
+    corner; cells beyond the first ring are >= h away.  Box blocks ride the
+    lattice: pool rows shared per key offset_idx * 256 + node, slots in
+    order of first appearance (potential.cpp:193-252), offset index
+    (oy + 2) * 5 + (ox + 2) of the TARGET's box minus the source box
+    (lattice_offset, potential.cpp:196-205).  Triangle nodes get one private
+    self row (their near cells are out of this model).  Row values are
+    seeded: their provenance does not matter for apply parity.
+    """
+    rng = np.random.default_rng(seed)
+    box_ij = np.asarray(box_ij, np.int64).reshape(-1, 2)
+    nbox = len(box_ij)
+    node_local = np.asarray(node_local, float).reshape(-1, 2)
+    npb = len(node_local)
+    a, b = node_local[:, 0], node_local[:, 1]
+    dl, dr, db, dt = (a + 1) / 2, (1 - a) / 2, (b + 1) / 2, (1 - b) / 2
+    # per node: the neighbour offsets (source box - target box) it is near, cell order below
+    near = {}
+    for ox in (-1, 0, 1):
+        for oy in (-1, 0, 1):
+            if ox == 0 and oy == 0:
+                continue
+            dx = dl if ox < 0 else dr if ox > 0 else np.zeros(npb)
+            dy = db if oy < 0 else dt if oy > 0 else np.zeros(npb)
+            near[(ox, oy)] = np.hypot(dx, dy) < D
+    lo = box_ij.min(0) - 2 if nbox else np.zeros(2, np.int64)
+    dims = (box_ij.max(0) - lo + 3) if nbox else np.ones(2, np.int64)
+    grid = np.full((int(dims[0]), int(dims[1])), -1, np.int64)
+    if nbox:
+        grid[box_ij[:, 0] - lo[0], box_ij[:, 1] - lo[1]] = np.arange(nbox)
+    blk_cell, blk_key, cnt = [], [], []
+    order = sorted(near)  # neighbour scan order (fixed)
+    for c in range(nbox):
+        i, j = box_ij[c]
+        nb = [(o, grid[i + o[0] - lo[0], j + o[1] - lo[1]]) for o in order]
+        nb = [(o, k) for o, k in nb if k >= 0]
+        for u in range(npb):
+            blk_cell.append(c)
+            blk_key.append(12 * 256 + u)  # self: offset (0, 0)
+            m = 1
+            for o, k in nb:
+                if near[o][u]:
+                    blk_cell.append(k)
+                    blk_key.append(((-o[1] + 2) * 5 + (-o[0] + 2)) * 256 + u)
+                    m += 1
+            cnt.append(m)
+    slot = {}
+    blk_pool = []
+    for key in blk_key:
+        if key not in slot:
+            slot[key] = len(slot)
+        blk_pool.append(slot[key])
+    nlat = len(slot)
+    lat_rows = rng.standard_normal((nlat, npb)) * 1e-3
+    tri_rows = rng.standard_normal((ntri_cells * np_tri, np_tri)) * 1e-3
+    tri_cell = np.repeat(nbox + np.arange(ntri_cells), np_tri)
+    blk_cell = np.concatenate([np.asarray(blk_cell, np.int64), tri_cell])
+    blk_pool = np.concatenate([np.asarray(blk_pool, np.int64), nlat + np.arange(ntri_cells * np_tri)])
+    cnt = np.concatenate([np.asarray(cnt, np.int64), np.ones(ntri_cells * np_tri, np.int64)])
+    node_off = np.concatenate([[0], np.cumsum(np.concatenate([np.full(nbox, npb), np.full(ntri_cells, np_tri)]))])
+    lens = np.concatenate([np.full(nlat, npb), np.full(ntri_cells * np_tri, np_tri)])
+    vals = np.concatenate([lat_rows.reshape(-1), tri_rows.reshape(-1)])
+    return {"blk_off": np.concatenate([[0], np.cumsum(cnt)]).astype(np.int32),
+            "blk_cell": blk_cell.astype(np.int32), "blk_pool": blk_pool.astype(np.int32),
+            "pool_off": np.concatenate([[0], np.cumsum(lens)]).astype(np.int64), "pool_vals": vals,
+            "node_off": node_off.astype(np.int32)}
+
+
+def fejer1(p):
+    """Chebyshev roots ascending with Fejer-1 weights (basis.cpp:140-156)."""
+    th = (2 * np.arange(p) + 1) * np.pi / (2 * p)
+    k = np.arange(1, p // 2 + 1)
+    s = (np.cos(2 * k[None, :] * th[:, None]) / (4.0 * k * k - 1.0)).sum(1)
+    return -np.cos(th), (2.0 / p) * (1 - 2 * s)
+
+
+def _cheb1d(p, z):
+    t = np.zeros((len(z), p))
+    t[:, 0] = 1.0
+    if p > 1:
+        t[:, 1] = z
+    for k in range(2, p):
+        t[:, k] = 2 * z * t[:, k - 1] - t[:, k - 2]
+    return t
+
+
+def chebyshev2d(p, zx, zy):
+    """chebyshev2d_eval (basis.cpp:259-265): out[a p + b] = T_a(x) T_b(y)."""
+    tx, ty = _cheb1d(p, np.asarray(zx, float)), _cheb1d(p, np.asarray(zy, float))
+    return (tx[:, :, None] * ty[:, None, :]).reshape(len(tx), p * p)
+
+
+def box_tables(p, q):
+    """The reference's box tables: p-node Fejer tensor nodes (index ix * p +
+    iy, basis.cpp:158-177), the q-node source rule (basis.cpp:281-303) and
+    box_oversample(p, q) = B C with B the degree-p Chebyshev basis at the
+    source nodes and C = V^-1 (basis.cpp:305-322)."""
+    z, w = fejer1(p)
+    ix, iy = np.meshgrid(np.arange(p), np.arange(p), indexing="ij")
+    nodes = np.stack([z[ix.ravel()], z[iy.ravel()]], 1)
+    zq, wq = fejer1(q)
+    jx, jy = np.meshgrid(np.arange(q), np.arange(q), indexing="ij")
+    src = np.stack([zq[jx.ravel()], zq[jy.ravel()]], 1)
+    wsrc = wq[jx.ravel()] * wq[jy.ravel()]
+    V = chebyshev2d(p, nodes[:, 0], nodes[:, 1])
+    C = np.linalg.inv(V)
+    O = chebyshev2d(p, src[:, 0], src[:, 1]) @ C
+    return nodes, src, wsrc, O, C
+
+
+def op_box(n_side=32, p=8, q=16, seed=7):
+    """The reference operator's data on a box mesh (SPEC acceptance 7 size:
+    32 x 32 boxes on [-1,1]^2, p = 8 -> 65,536 ndofs): targets = the p x p
+    Fejer nodes of every box, sources = the q x q oversampled nodes
+    (q = 2p, 262,144) with weights w_s * jacobian, build_charges through
+    O = box_oversample(p, q) (256 x 64), the correction CSR from the
+    reference near rule (reference_correction_csr).  f = a seeded smooth
+    field at the nodes."""
+    rng = np.random.default_rng(seed)
+    cx, cy, h = uniform_grid(n_side)
+    nodes, src, wsrc, O, _ = box_tables(p, q)
+    tgt = np.stack([(cx[:, None] + 0.5 * h * nodes[None, :, 0]).ravel(),
+                    (cy[:, None] + 0.5 * h * nodes[None, :, 1]).ravel()], 1)
+    spts = np.stack([(cx[:, None] + 0.5 * h * src[None, :, 0]).ravel(),
+                     (cy[:, None] + 0.5 * h * src[None, :, 1]).ravel()], 1)
+    wj = np.tile(wsrc * (h * h / 4.0), len(cx))
+    cen = rng.uniform(-0.6, 0.6, size=(3, 2))
+    f = sum(gaussian(tgt, cen[k], 40.0) for k in range(3))
+    ij = np.stack([np.rint((cx + 1.0) / h - 0.5), np.rint((cy + 1.0) / h - 0.5)], 1).astype(np.int64)
+    nbox = len(cx)
+    charge_map = {"cell_type": np.zeros(nbox, np.int32),
+                  "node_off": (np.arange(nbox + 1) * p * p).astype(np.int32),
+                  "src_off": (np.arange(nbox + 1) * q * q).astype(np.int32),
+                  "over0": O, "over1": np.zeros((0, 0)), "src_wj": wj}
+    q_ch = wj * (np.einsum("sij,cj->csi", O[None], f.reshape(nbox, p * p)).reshape(-1))
+    return Workload("op_box", spts, q_ch, tgt, notes={
+        "h": h, "f": f, "charges": charge_map, "boxes": nbox,
+        "corr": lambda: reference_correction_csr(ij, nodes)})
+
+
+CONFIGS = {"cfg1": cfg1, "cfg2": cfg2, "cfg3": cfg3, "cfg4": cfg4, "cfg5": cfg5, "op_box": op_box}
 
 
 def random_points(n, seed, lo=0.0, hi=1.0):
