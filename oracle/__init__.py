@@ -12,6 +12,10 @@ imports it).
   reference summation sources compiled in place from /root/reference
   (oracle/Makefile) behind a tiny extern "C" shim.  Travels to the GPU box
   as a prebuilt .so.
+* :func:`reference_operator` -- oracle/_ref/libvolpot_ref_op.so, the
+  UNMODIFIED reference operator sources (mesh, basis, quadrature, singular
+  rules, potential, bie) compiled in place against our restatement of the
+  Eigen subset they use (oracle/eigen_restated/; Eigen is absent here).
 """
 from __future__ import annotations
 
@@ -24,6 +28,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "libvolpot_oracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libvolpot_ref.so")
+REFOP_SO = os.path.join(HERE, "_ref", "libvolpot_ref_op.so")
 REF_SRC = "/root/reference/proj"
 
 _P = C.c_void_p
@@ -33,9 +38,9 @@ def build(force: bool = False) -> None:
     """make -C oracle (the reference .so only where /root/reference exists)."""
     targets = ["oracle"]
     if os.path.isdir(REF_SRC):
-        targets.append("ref")
+        targets += ["ref", "refop"]
     if force or not os.path.exists(ORACLE_SO) or (
-            "ref" in targets and not os.path.exists(REF_SO)):
+            "ref" in targets and not (os.path.exists(REF_SO) and os.path.exists(REFOP_SO))):
         subprocess.run(["make", "-C", HERE] + targets, check=True,
                        stdout=subprocess.DEVNULL)
 
@@ -308,8 +313,253 @@ class RefPlan:
             pass
 
 
+class ReferenceOperator:
+    """The unmodified reference operator code (oracle/_ref/libvolpot_ref_op.so,
+    oracle/ref_op_shim.cpp): star-domain hybrid meshes (mesh.cpp:262-408),
+    VolumePotentialOperator build/apply (potential.cpp:360-470) with its
+    private correction map, build_charges, and the single-cell rows of
+    singular.cpp (smooth_potential_row, SingularTargetRule::row, ray
+    quadrature, box_correction_table)."""
+
+    def __init__(self):
+        if not os.path.exists(REFOP_SO):
+            build()
+        if not os.path.exists(REFOP_SO):
+            raise FileNotFoundError(f"{REFOP_SO} not built (needs /root/reference at build time)")
+        h = C.CDLL(REFOP_SO)
+        d, i, i64 = C.c_double, C.c_int, C.c_int64
+        h.refop_last_error.restype = C.c_char_p
+        h.refop_set_threads.argtypes = [i]
+        h.refop_set_threads.restype = None
+        h.refop_mesh_star.argtypes = [d, d, d, d, i, d, d, d, C.POINTER(_P)]
+        h.refop_mesh_free.argtypes = [_P]
+        h.refop_mesh_free.restype = None
+        h.refop_mesh_info.argtypes = [_P, _P, _P, _P, _P]
+        h.refop_mesh_cells.argtypes = [_P, _P, _P, _P, _P, _P]
+        h.refop_mesh_nodes.argtypes = [_P, i, _P]
+        h.refop_classify.argtypes = [_P, d, d, d, _P, _P, _P]
+        h.refop_op_create.argtypes = [_P, i, d, i, i, _P, i64, d, C.POINTER(_P)]
+        h.refop_op_free.argtypes = [_P]
+        h.refop_op_free.restype = None
+        h.refop_op_sizes.argtypes = [_P, _P]
+        h.refop_op_export.argtypes = [_P] + [_P] * 10
+        h.refop_op_apply.argtypes = [_P, _P, i64, _P, _P]
+        h.refop_op_build_charges.argtypes = [_P, _P, i64, _P]
+        h.refop_op_correction_row_generic.argtypes = [_P, i, d, d, i, _P]
+        h.refop_smooth_row.argtypes = [_P, i, i, i, d, d, i, d, _P]
+        h.refop_self_row.argtypes = [_P, i, i, d, d, d, d, i, d, _P]
+        h.refop_ray_row.argtypes = [_P, i, i, d, d, d, d, d, d, i, d, _P]
+        h.refop_nearest_reference_point.argtypes = [_P, i, d, d, _P, _P]
+        h.refop_cell_invert.argtypes = [_P, i, d, d, _P]
+        h.refop_cell_map_deriv.argtypes = [_P, i, d, d, _P]
+        h.refop_box_table.argtypes = [i, i, d, d, _P]
+        h.refop_box_log.argtypes = [i, _P]
+        h.refop_basis.argtypes = [i, i, i, _P, C.POINTER(i64)]
+        h.refop_rule1d.argtypes = [i, i, d, _P, _P, C.POINTER(i)]
+        h.refop_boundary.argtypes = [i, d, d, _P, _P, _P, C.POINTER(i)]
+        self.h = h
+
+    def _err(self, rc, what):
+        if rc:
+            msg = self.h.refop_last_error().decode()
+            raise (ValueError if rc in (1, 3) else RuntimeError)(f"{what}: {msg}")
+
+    def set_threads(self, n):
+        self.h.refop_set_threads(int(n))
+
+    def star_mesh(self, h, r0=1.0, amp=0.3, arms=5, phase=0.0, center=(0.0, 0.0), delta=0.8):
+        return RefMesh(self, h, r0, amp, arms, phase, center, delta)
+
+    def basis(self, which, p, q=0):
+        """0 tri nodes, 1 tri C, 2 box nodes, 3 box C, 4/5 tri source nodes/w,
+        6/7 box source nodes/w, 8 triangle_oversample, 9 box_oversample."""
+        n = C.c_int64()
+        self._err(self.h.refop_basis(which, p, q, None, C.byref(n)), "basis")
+        out = np.empty(n.value)
+        self._err(self.h.refop_basis(which, p, q, _p(out), C.byref(n)), "basis")
+        shapes = {0: (-1, 2), 2: (-1, 2), 4: (-1, 2), 6: (-1, 2)}
+        if which in (1, 3):
+            k = int(round(np.sqrt(out.size)))
+            return out.reshape(k, k)
+        if which == 8:
+            return out.reshape(-1, p * (p + 1) // 2)
+        if which == 9:
+            return out.reshape(-1, p * p)
+        return out.reshape(shapes[which]) if which in shapes else out
+
+    def rule1d(self, which, n=0, d=0.0):
+        sz = C.c_int()
+        self._err(self.h.refop_rule1d(which, n, d, None, None, C.byref(sz)), "rule1d")
+        x, w = np.empty(sz.value), np.empty(sz.value)
+        self._err(self.h.refop_rule1d(which, n, d, _p(x), _p(w), C.byref(sz)), "rule1d")
+        return x, w
+
+    def boundary(self, kind, star):
+        n = C.c_int()
+        self._err(self.h.refop_boundary(kind, star[0], star[1], None, None, None, C.byref(n)), "boundary")
+        z, t, f = np.empty((n.value, 2)), np.empty(n.value), np.empty(n.value)
+        self._err(self.h.refop_boundary(kind, star[0], star[1], _p(z), _p(t), _p(f), C.byref(n)), "boundary")
+        return z, t, f
+
+    def box_table(self, p, family, lam, h):
+        nb = p * p
+        out = np.empty(25 * nb * nb)
+        self._err(self.h.refop_box_table(p, family, lam, h, _p(out)), "box_correction_table")
+        return out.reshape(25, nb, nb)
+
+    def box_log(self, p):
+        nb = p * p
+        out = np.empty(25 * nb * nb)
+        self._err(self.h.refop_box_log(p, _p(out)), "box_log")
+        return out.reshape(25, nb, nb)
+
+
+class RefMesh:
+    def __init__(self, ref, h, r0, amp, arms, phase, center, delta):
+        self.ref = ref
+        m = C.c_void_p()
+        ref._err(ref.h.refop_mesh_star(center[0], center[1], r0, amp, arms, phase, h, delta, C.byref(m)),
+                 "build_mesh")
+        self.handle = m
+        nc, nt, nb, hh = C.c_int(), C.c_int(), C.c_int(), C.c_double()
+        ref.h.refop_mesh_info(m, C.byref(nc), C.byref(nt), C.byref(nb), C.byref(hh))
+        self.ncell, self.n_tri, self.n_box, self.h = nc.value, nt.value, nb.value, hh.value
+        self.star = dict(center=tuple(center), r0=r0, amp=amp, arms=arms, phase=phase)
+        n = self.ncell
+        self.type = np.empty(n, np.int32)
+        self.v = np.empty((n, 3, 2))
+        self.tt = np.empty((n, 2))
+        self.ch = np.empty((n, 3))
+        self.curve = np.empty(n, np.int32)
+        ref.h.refop_mesh_cells(m, _p(self.type), _p(self.v), _p(self.tt), _p(self.ch), _p(self.curve))
+
+    def ndofs(self, p):
+        return self.n_tri * p * (p + 1) // 2 + self.n_box * p * p
+
+    def nodes(self, p):
+        out = np.empty((self.ndofs(p), 2))
+        self.ref._err(self.ref.h.refop_mesh_nodes(self.handle, p, _p(out)), "mesh_nodes")
+        return out
+
+    def classify(self, pt, D=0.4):
+        s, nn = C.c_int(), C.c_int()
+        near = np.empty(64, np.int32)
+        self.ref._err(self.ref.h.refop_classify(self.handle, pt[0], pt[1], D, C.byref(s), _p(near),
+                                                C.byref(nn)), "classify_target")
+        return s.value, near[:nn.value].copy()
+
+    def _row(self, fn, n, *args):
+        out = np.empty(n)
+        self.ref._err(fn(self.handle, *args, _p(out)), fn.__name__)
+        return out
+
+    def nb(self, cell, p):
+        return p * p if self.type[cell] == 2 else p * (p + 1) // 2
+
+    def smooth_row(self, cell, p, q, r0, family=0, lam=0.0):
+        return self._row(self.ref.h.refop_smooth_row, self.nb(cell, p), cell, p, q, r0[0], r0[1], family, lam)
+
+    def self_row(self, cell, p, zeta0, r0, family=0, lam=0.0):
+        return self._row(self.ref.h.refop_self_row, self.nb(cell, p), cell, p, zeta0[0], zeta0[1], r0[0],
+                         r0[1], family, lam)
+
+    def ray_row(self, cell, p, zeta0, zstar, r0, family=0, lam=0.0):
+        return self._row(self.ref.h.refop_ray_row, self.nb(cell, p), cell, p, zeta0[0], zeta0[1], zstar[0],
+                         zstar[1], r0[0], r0[1], family, lam)
+
+    def nearest_reference_point(self, cell, x):
+        z, d = np.empty(2), C.c_double()
+        self.ref._err(self.ref.h.refop_nearest_reference_point(self.handle, cell, x[0], x[1], _p(z),
+                                                               C.byref(d)), "nearest_reference_point")
+        return z, d.value
+
+    def invert(self, cell, x):
+        z = np.empty(2)
+        self.ref._err(self.ref.h.refop_cell_invert(self.handle, cell, x[0], x[1], _p(z)), "invert")
+        return z
+
+    def map_deriv(self, cell, z):
+        o = np.empty(7)
+        self.ref._err(self.ref.h.refop_cell_map_deriv(self.handle, cell, z[0], z[1], _p(o)), "map_deriv")
+        return o
+
+    def operator(self, p, q, targets, family=0, lam=0.0, eps=1e-12):
+        return RefOperator(self, p, q, _pts(targets), family, lam, eps)
+
+    def close(self):
+        if self.handle:
+            self.ref.h.refop_mesh_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class RefOperator:
+    """VolumePotentialOperator on a RefMesh (the mesh must outlive it)."""
+
+    def __init__(self, mesh, p, q, tgt, family, lam, eps):
+        self.mesh, self.ref = mesh, mesh.ref
+        self.p, self.q, self.family, self.lam = p, q, family, lam
+        h = C.c_void_p()
+        self.ref._err(self.ref.h.refop_op_create(mesh.handle, family, lam, p, q, _p(tgt), len(tgt), eps,
+                                                 C.byref(h)), "VolumePotentialOperator")
+        self.handle = h
+        s = np.empty(8)
+        self.ref.h.refop_op_sizes(h, _p(s))
+        (self.ndofs, self.nsrcs, self.nt, self.ncell, self.nblocks, self.npool, self.pool_len) = \
+            (int(x) for x in s[:7])
+        self.build_ms = float(s[7])
+
+    def export(self):
+        """The operator's layouts: nodes, node_off, src_off, src_xy, src_wj and
+        the correction map (blk_off, blk_cell, blk_pool, pool_off, pool_vals)."""
+        d = dict(nodes=np.empty((self.ndofs, 2)), node_off=np.empty(self.ncell + 1, np.int32),
+                 src_off=np.empty(self.ncell + 1, np.int32), src_xy=np.empty((self.nsrcs, 2)),
+                 src_wj=np.empty(self.nsrcs), blk_off=np.empty(self.nt + 1, np.int32),
+                 blk_cell=np.empty(self.nblocks, np.int32), blk_pool=np.empty(self.nblocks, np.int32),
+                 pool_off=np.empty(self.npool + 1, np.int64), pool_vals=np.empty(self.pool_len))
+        self.ref.h.refop_op_export(self.handle, *(_p(d[k]) for k in (
+            "nodes", "node_off", "src_off", "src_xy", "src_wj", "blk_off", "blk_cell", "blk_pool",
+            "pool_off", "pool_vals")))
+        return d
+
+    def apply(self, f, timings=False):
+        f = _vec(f)
+        out, tm = np.empty(self.nt), np.empty(2)
+        self.ref._err(self.ref.h.refop_op_apply(self.handle, _p(f), f.size, _p(out), _p(tm)), "apply")
+        return (out, {"smooth_s": tm[0], "correction_s": tm[1]}) if timings else out
+
+    def build_charges(self, f):
+        f = _vec(f)
+        q = np.empty(self.nsrcs)
+        self.ref._err(self.ref.h.refop_op_build_charges(self.handle, _p(f), f.size, _p(q)), "build_charges")
+        return q
+
+    def correction_row_generic(self, cell, pt, is_self):
+        out = np.empty(self.mesh.nb(cell, self.p))
+        self.ref._err(self.ref.h.refop_op_correction_row_generic(self.handle, cell, pt[0], pt[1], int(is_self),
+                                                                 _p(out)), "correction_row_generic")
+        return out
+
+    def close(self):
+        if self.handle:
+            self.ref.h.refop_op_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 _rest = None
 _ref = None
+_refop = None
 
 
 def restatement() -> Restatement:
@@ -324,6 +574,13 @@ def reference() -> Reference:
     if _ref is None:
         _ref = Reference()
     return _ref
+
+
+def reference_operator() -> ReferenceOperator:
+    global _refop
+    if _refop is None:
+        _refop = ReferenceOperator()
+    return _refop
 
 
 def ref_available() -> bool:
