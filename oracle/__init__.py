@@ -357,6 +357,13 @@ class ReferenceOperator:
         h.refop_basis.argtypes = [i, i, i, _P, C.POINTER(i64)]
         h.refop_rule1d.argtypes = [i, i, d, _P, _P, C.POINTER(i)]
         h.refop_boundary.argtypes = [i, d, d, _P, _P, _P, C.POINTER(i)]
+        h.refop_layer_create.argtypes = [i, d, _P, i, _P, _P, i, C.POINTER(_P)]
+        h.refop_layer_free.argtypes = [_P]
+        h.refop_layer_free.restype = None
+        h.refop_layer_info.argtypes = [_P, _P, _P, _P]
+        h.refop_layer_curve.argtypes = [_P, i] + [_P] * 7
+        h.refop_layer_solve.argtypes = [_P, _P, _P]
+        h.refop_layer_eval.argtypes = [_P, _P, i64, _P, i64, i, _P]
         self.h = h
 
     def _err(self, rc, what):
@@ -407,11 +414,72 @@ class ReferenceOperator:
         self._err(self.h.refop_box_table(p, family, lam, h, _p(out)), "box_correction_table")
         return out.reshape(25, nb, nb)
 
+    def layer(self, family, lam, n_per_curve, **kw):
+        return RefLayer(self, family, lam, n_per_curve, **kw)
+
     def box_log(self, p):
         nb = p * p
         out = np.empty(25 * nb * nb)
         self._err(self.h.refop_box_log(p, _p(out)), "box_log")
         return out.reshape(25, nb, nb)
+
+
+class RefLayer:
+    """BoundarySystem of a star domain with optional circular holes
+    (assemble_nystrom, bie.cpp:156-293), solve_density (bie.cpp:295-380) and
+    eval_layer_potential (bie.cpp:383-468) of the reference."""
+
+    def __init__(self, ref, family, lam, n_per_curve, r0=1.0, amp=0.3, arms=5, phase=0.0, center=(0.0, 0.0),
+                 holes=()):
+        self.ref = ref
+        star = np.array([center[0], center[1], r0, amp, arms, phase], float)
+        hl = np.array(holes, float).reshape(-1)
+        npc = np.ascontiguousarray(n_per_curve, np.int32).reshape(-1)
+        h = C.c_void_p()
+        ref._err(ref.h.refop_layer_create(family, lam, _p(star), len(hl) // 3, _p(hl) if hl.size else None,
+                                          _p(npc), npc.size, C.byref(h)), "assemble_nystrom")
+        self.handle = h
+        nc, nd, na = C.c_int(), C.c_int(), C.c_int()
+        ref.h.refop_layer_info(h, C.byref(nc), C.byref(nd), C.byref(na))
+        self.ncurves, self.n_density, self.n_aux = nc.value, nd.value, na.value
+        self.curves = []
+        for c in range(self.ncurves):
+            sc = np.empty(6)
+            ref.h.refop_layer_curve(h, c, _p(sc), None, None, None, None, None, None)
+            n = int(sc[0])
+            b = dict(n=n, offset=int(sc[1]), length=sc[2], diam=sc[3], log_center=sc[4:6].copy(),
+                     x=np.empty((n, 2)), normal=np.empty((n, 2)), speed=np.empty(n),
+                     fine_x=np.empty((8 * n, 2)), fine_normal=np.empty((8 * n, 2)), fine_speed=np.empty(8 * n))
+            ref.h.refop_layer_curve(h, c, _p(sc), *(_p(b[k]) for k in (
+                "x", "normal", "speed", "fine_x", "fine_normal", "fine_speed")))
+            self.curves.append(b)
+
+    def size(self):
+        return self.n_density + self.n_aux
+
+    def solve(self, rhs):
+        rhs = _vec(rhs)
+        out = np.empty(self.size())
+        self.ref._err(self.ref.h.refop_layer_solve(self.handle, _p(rhs), _p(out)), "solve_density")
+        return out
+
+    def eval(self, coeffs, targets, allow_close=False):
+        cf, tg = _vec(coeffs), _pts(targets)
+        out = np.empty(len(tg))
+        self.ref._err(self.ref.h.refop_layer_eval(self.handle, _p(cf), cf.size, _p(tg), len(tg),
+                                                  int(allow_close), _p(out)), "eval_layer_potential")
+        return out
+
+    def close(self):
+        if self.handle:
+            self.ref.h.refop_layer_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class RefMesh:

@@ -52,6 +52,7 @@
 #include "volpot/potential.hpp"
 #undef private
 #include "../src/potential.cpp"  // NOLINT: compiled in place for Impl access
+#include "volpot/bie.hpp"
 
 namespace {
 thread_local std::string g_err;
@@ -399,6 +400,89 @@ int refop_boundary(int kind, double sx, double sy, double* zeta, double* t, doub
                 t[i] = bd.nodes[i].t;
                 factor[i] = bd.nodes[i].factor;
             }
+    });
+}
+
+}  // extern "C"
+
+// ---- boundary integral layer (bie.hpp:29-90) ----
+namespace {
+struct LayerBox {
+    volpot::Domain dom;
+    volpot::BoundarySystem sys;
+};
+}  // namespace
+
+extern "C" {
+
+int refop_layer_create(int family, double lambda, const double* star /*cx,cy,r0,amp,arms,phase*/, int nholes,
+                       const double* holes /*cx,cy,r per hole*/, const int* n_per_curve, int ncount, void** out) {
+    return guarded([&] {
+        auto lb = std::make_unique<LayerBox>();
+        lb->dom.outer = std::make_shared<volpot::StarCurve>(volpot::Vec2{star[0], star[1]}, star[2], star[3],
+                                                            static_cast<int>(star[4]), star[5]);
+        for (int k = 0; k < nholes; ++k)
+            lb->dom.holes.push_back(std::make_shared<volpot::Circle>(
+                volpot::Vec2{holes[3 * k], holes[3 * k + 1]}, holes[3 * k + 2]));
+        lb->sys = volpot::assemble_nystrom(lb->dom, kern(family, lambda),
+                                           std::vector<int>(n_per_curve, n_per_curve + ncount));
+        *out = lb.release();
+    });
+}
+
+void refop_layer_free(void* s) { delete static_cast<LayerBox*>(s); }
+
+int refop_layer_info(void* s, int* ncurves, int* n_density, int* n_aux) {
+    const auto& sys = static_cast<LayerBox*>(s)->sys;
+    *ncurves = static_cast<int>(sys.curves.size());
+    *n_density = sys.n_density;
+    *n_aux = sys.n_aux;
+    return 0;
+}
+
+// geometry of curve block c; scal = (n, offset, length, diam, log_center.x, log_center.y)
+int refop_layer_curve(void* s, int c, double* scal, double* x, double* normal, double* speed, double* fx,
+                      double* fnormal, double* fspeed) {
+    const auto& b = static_cast<LayerBox*>(s)->sys.curves[size_t(c)];
+    scal[0] = b.n;
+    scal[1] = b.offset;
+    scal[2] = b.length;
+    scal[3] = b.diam;
+    scal[4] = b.log_center.x;
+    scal[5] = b.log_center.y;
+    auto v2 = [](const std::vector<volpot::Vec2>& v, double* o) {
+        if (!o) return;
+        for (size_t i = 0; i < v.size(); ++i) {
+            o[2 * i] = v[i].x;
+            o[2 * i + 1] = v[i].y;
+        }
+    };
+    v2(b.x, x);
+    v2(b.normal, normal);
+    v2(b.fine_x, fx);
+    v2(b.fine_normal, fnormal);
+    if (speed) std::copy(b.speed.begin(), b.speed.end(), speed);
+    if (fspeed) std::copy(b.fine_speed.begin(), b.fine_speed.end(), fspeed);
+    return 0;
+}
+
+int refop_layer_solve(void* s, const double* rhs, double* out) {
+    return guarded([&] {
+        const auto& sys = static_cast<LayerBox*>(s)->sys;
+        const auto r = volpot::solve_density(sys, std::vector<double>(rhs, rhs + sys.size()));
+        std::copy(r.begin(), r.end(), out);
+    });
+}
+
+int refop_layer_eval(void* s, const double* coeffs, int64_t nc, const double* tgt, int64_t nt, int allow_close,
+                     double* out) {
+    return guarded([&] {
+        const auto& sys = static_cast<LayerBox*>(s)->sys;
+        std::vector<volpot::Vec2> t(static_cast<size_t>(nt));
+        for (int64_t i = 0; i < nt; ++i) t[size_t(i)] = {tgt[2 * i], tgt[2 * i + 1]};
+        const auto r = volpot::eval_layer_potential(sys, std::vector<double>(coeffs, coeffs + nc), t,
+                                                    allow_close != 0);
+        std::copy(r.begin(), r.end(), out);
     });
 }
 

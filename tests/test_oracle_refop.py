@@ -90,3 +90,24 @@ def test_restated_correction_apply_vs_reference(R, rest, ref, small):
     # the map's shape follows the reference near rule: 1 self block + <= 30 near
     nblk = np.diff(d["blk_off"])
     assert nblk.min() >= 1 and nblk.max() <= 31
+
+
+@pytest.mark.parametrize("family,lam,holes", [(0, 0.0, ()), (0, 0.0, ((0.3, 0.1, 0.2),)), (1, 10.0, ())])
+def test_restated_layer_eval_vs_reference(R, rest, family, lam, holes):
+    """Our restatement of eval_layer_impl (vo_layer_eval) against the compiled
+    reference bie.cpp on the reference's own BoundarySystem and density."""
+    from types import SimpleNamespace
+    lay = R.layer(family, lam, [128] * (1 + len(holes)), holes=holes)
+    nodes = np.concatenate([c["x"] for c in lay.curves])
+    dens = lay.solve(np.concatenate([np.sin(nodes[:, 0] + 2 * nodes[:, 1]), np.zeros(lay.n_aux)]))
+    rng = np.random.default_rng(9)
+    th = rng.uniform(0, 2 * np.pi, 800)
+    rad = (1 + 0.3 * np.cos(5 * th)) * rng.uniform(0.05, 0.985, th.size) ** 0.5
+    tg = np.stack([rad * np.cos(th), rad * np.sin(th)], 1)
+    for hc in holes:
+        tg = tg[np.hypot(tg[:, 0] - hc[0], tg[:, 1] - hc[1]) > hc[2] * 1.05]
+    ref_out = lay.eval(dens, tg, allow_close=True)
+    curves = [SimpleNamespace(**c) for c in lay.curves]
+    out, rc = rest.layer_eval(family, lam, curves, lay.n_density, lay.n_aux, dens, tg, True)
+    assert rc == 0
+    assert rel_l2(out, ref_out) <= (1e-13 if family == 0 else 1e-12)
