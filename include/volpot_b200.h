@@ -220,6 +220,66 @@ int vpg_operator_apply(const vpg_operator* op, const double* f, int64_t nf, doub
                        unsigned flags, void* stream, float* timings_ms);
 int vpg_operator_destroy(vpg_operator* op);
 
+/* Correction-row generation on the device: the rows of the
+ * operator's correction map, built by VolumePotentialOperator::Impl::
+ * build_corrections (potential.cpp:133-349) from SingularTargetRule::row
+ * (singular.cpp:383-415), reduce_to_rays + apply_ray_quadrature
+ * (singular.cpp:274-310), box_correction_table (singular.cpp:586-646) and
+ * smooth_potential_row (singular.cpp:428-456).
+ *
+ * vpg_rows_create takes the mesh the rows integrate over: curves (kind 0
+ * circle {cx, cy, r}, 1 ellipse {cx, cy, a, b, angle}, 2 star {cx, cy, r0,
+ * amp, arms, phase}; 6 doubles each, geometry.hpp:31-72), cells (type 0
+ * straight triangle, 1 curved triangle, 2 box; cell_curve the curve of a
+ * curved cell; cell_v 3 vertices, cell_t (ta, tb), cell_ch (centre, h):
+ * geometry.hpp:90-100), and the basis data of order p and source order q
+ * (TriangleBasisTable nodes and C, BoxBasisTable C, the triangle source rule:
+ * basis.hpp:13-56; row-major).  The context owns device copies. */
+typedef struct vpg_rows vpg_rows;
+int vpg_rows_create(int family, double lambda, int p, int q, int64_t ncurve, const int32_t* curve_kind,
+                    const double* curve_par, int64_t ncell, const int32_t* cell_type, const int32_t* cell_curve,
+                    const double* cell_v, const double* cell_t, const double* cell_ch, const double* tri_nodes,
+                    const double* tri_C, const double* box_C, int64_t ntri_src, const double* tri_src_xy,
+                    const double* tri_src_w, int device, vpg_rows** rows);
+int vpg_rows_destroy(vpg_rows* rows);
+/* One of the context's 1-D rules (0 Gauss-Legendre 16, 1 / 2 the 20-point
+ * Gauss rules for -t log t / t, 3 the singular ray rule, 4.. the near ray
+ * rules per decade bucket -2..9): x, w may be NULL to size. */
+int vpg_rows_rule(const vpg_rows* rows, int which, double* x, double* w, int64_t* n);
+/* Row tasks (host arrays, one entry per task): job 0 self rule at zeta0,
+ * 1 ray rule (zeta0, zstar), 2 smooth row (aux 30: the 30x30 box rule),
+ * 3..6 operator rows (TriSelfNode with aux = node, TriNearSnap, SelfGeneric,
+ * NearGeneric: potential.cpp:157-333, geometry resolved on the device),
+ * 7 lattice row (aux = offset * 256 + node, r0 = the node's point; the table
+ * for lattice_h), 8/9 lattice-table entries; cell -1 = the reference box.
+ * Rows are written back to back (p*p for box cells, p(p+1)/2 otherwise);
+ * out = NULL only sizes (*out_len). */
+int vpg_rows_eval(vpg_rows* rows, int64_t ntask, const int32_t* job, const int32_t* cell, const int32_t* aux,
+                  const double* r0, const double* zeta0, const double* zstar, double lattice_h, double* out,
+                  int64_t* out_len);
+
+/* The whole correction map of VolumePotentialOperator (build_corrections,
+ * potential.cpp:133-349) for targets tgt_xy: classify_target with near
+ * distance D * h (mesh.cpp:410-448) on the device, the reference's task list
+ * and pool slots on the host (node-coincident targets found by exact bits in
+ * nodes_xy, the dof layout of mesh_nodes with node_off per cell; shared box
+ * lattice rows), every row on the device; the map is created on the rows
+ * context's device.  stats (may be NULL, 11 doubles): classification ms,
+ * task/table ms, row ms, blocks, pool rows, pool doubles, then the block
+ * counts of TriSelfNode, TriNearSnap, SelfGeneric, NearGeneric, BoxLattice.
+ * Errors: the reference's classify_target messages (VPG_ERR_INVALID_ARGUMENT). */
+int vpg_corr_build(vpg_rows* rows, int64_t ndofs, const double* nodes_xy, const int32_t* node_off, int64_t nt,
+                   const double* tgt_xy, double D, vpg_corr** corr, double* stats);
+/* The context's mesh mapped on the host: which = 0 the order-p interpolation
+ * nodes of every cell in cell order (mesh_nodes, potential.cpp:63-74: xy);
+ * 1 the order-q source rule (build_sources, potential.cpp:133-151: xy and
+ * w * jacobian).  *n receives the point count; xy / wj may be NULL. */
+int vpg_rows_map(const vpg_rows* rows, int which, double* xy, double* wj, int64_t* n);
+/* Copies a correction map back to the host (any pointer may be NULL);
+ * sizes (5 int64, may be NULL): nt, nblocks, npool, pool doubles, ndofs. */
+int vpg_corr_export(const vpg_corr* corr, int32_t* blk_off, int32_t* blk_cell, int32_t* blk_pool,
+                    int64_t* pool_off, double* pool_vals, int64_t* sizes);
+
 /* Double-layer potential at volume targets, eval_layer_potential
  * (bie.hpp:87-90, bie.cpp:383-468): the trapezoidal Nystrom sum of every
  * curve, the 8x trig-upsampled rule within 5 node spacings (bie.cpp:414-

@@ -125,6 +125,14 @@ _SIGS = {
                                    C.POINTER(_P)]),
     "vpg_layer_eval": (C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, C.c_int, _P, C.c_uint, _P]),
     "vpg_layer_destroy": (C.c_int, [_P]),
+    "vpg_rows_create": (C.c_int, [C.c_int, C.c_double, C.c_int, C.c_int, C.c_int64, _P, _P, C.c_int64, _P, _P,
+                                  _P, _P, _P, _P, _P, _P, C.c_int64, _P, _P, C.c_int, C.POINTER(_P)]),
+    "vpg_rows_destroy": (C.c_int, [_P]),
+    "vpg_rows_rule": (C.c_int, [_P, C.c_int, _P, _P, _I64]),
+    "vpg_rows_eval": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P, _P, _P, C.c_double, _P, _I64]),
+    "vpg_corr_build": (C.c_int, [_P, C.c_int64, _P, _P, C.c_int64, _P, C.c_double, C.POINTER(_P), _P]),
+    "vpg_corr_export": (C.c_int, [_P, _P, _P, _P, _P, _P, _P]),
+    "vpg_rows_map": (C.c_int, [_P, C.c_int, _P, _P, _I64]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

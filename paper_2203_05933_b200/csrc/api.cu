@@ -452,7 +452,10 @@ int vpg_plan_apply(const vpg_plan* plan, const double* q, int64_t nq, double* ou
         const bool dev = flags & VPG_DEVICE_POINTERS;
         if (!pl.direct && pl.family == VPG_LAPLACE && !pl.profiling && graphs_enabled()) {
             std::unique_lock<std::mutex> lk(pl.graph_mu);
-            GraphEntry* e = pl.graph_broken ? nullptr : graph_entry(pl, dev ? q : nullptr, dev ? out : nullptr, !dev);
+            // host pointers: two staged graphs used in turn, so applies issued on
+            // two streams overlap one's copies with the other's kernels
+            const double* hkey = reinterpret_cast<const double*>(uintptr_t(1 + (pl.host_rr++ & 1u)));
+            GraphEntry* e = pl.graph_broken ? nullptr : graph_entry(pl, dev ? q : hkey, dev ? out : nullptr, !dev);
             if (e) {
                 e->last_use = ++pl.graph_clock;
                 VPG_CUDA(cudaStreamWaitEvent(st, e->done, 0));  // previous use of this workspace

@@ -193,6 +193,20 @@ int vpg_corr_create(int64_t nt, const int32_t* blk_off, int64_t nblocks,
                     const int64_t* pool_off, const double* pool_vals, int64_t ncell,
                     const int32_t* node_off, int device, vpg_corr** corr) {
     return guarded_c([&] {
+        vpg::corr_create_impl(nt, blk_off, nblocks, blk_cell, blk_pool, npool, pool_off, pool_vals, false, ncell,
+                              node_off, device, corr);
+    });
+}
+
+}  // extern "C"
+
+// The map from host structure arrays; pool_vals on the host, or already on
+// the device (dev_pool: the rows built by vpg_corr_build, copied device to device).
+void vpg::corr_create_impl(int64_t nt, const int32_t* blk_off, int64_t nblocks, const int32_t* blk_cell,
+                           const int32_t* blk_pool, int64_t npool, const int64_t* pool_off,
+                           const double* pool_vals, bool dev_pool, int64_t ncell, const int32_t* node_off,
+                           int device, vpg_corr** corr) {
+    {
         if (!corr) throw Error{VPG_ERR_INVALID_ARGUMENT, "corr is NULL"};
         *corr = nullptr;
         if (nt < 0 || nblocks < 0 || npool < 0 || ncell < 0 || !blk_off || !pool_off || !node_off ||
@@ -223,7 +237,13 @@ int vpg_corr_create(int64_t nt, const int32_t* blk_off, int64_t nblocks,
         upload(c->blk_cell, blk_cell, size_t(nblocks));
         upload(c->blk_pool, blk_pool, size_t(nblocks));
         upload(c->pool_off, pool_off, size_t(npool + 1));
-        upload(c->pool_vals, pool_vals, size_t(nvals));
+        if (dev_pool) {
+            c->pool_vals.alloc(size_t(nvals));
+            if (nvals) VPG_CUDA(cudaMemcpy(c->pool_vals.p, pool_vals, size_t(nvals) * sizeof(double),
+                                           cudaMemcpyDeviceToDevice));
+        } else {
+            upload(c->pool_vals, pool_vals, size_t(nvals));
+        }
         upload(c->node_off, node_off, size_t(ncell + 1));
         // lattice groups: 64 consecutive targets with identical block-cell
         // sequences whose rows are base_r + u of contiguous 64 x 64 blocks
@@ -326,8 +346,10 @@ int vpg_corr_create(int64_t nt, const int32_t* blk_off, int64_t nblocks,
             }
         }
         *corr = c.release();
-    });
+    }
 }
+
+extern "C" {
 
 int vpg_corr_apply(const vpg_corr* c, const double* f, int64_t nf, double* out,
                    unsigned flags, void* stream) {
@@ -470,3 +492,26 @@ int vpg_charges_destroy(vpg_charges* h) {
 }
 
 }  // extern "C"
+
+extern "C" int vpg_corr_export(const vpg_corr* c, int32_t* blk_off, int32_t* blk_cell, int32_t* blk_pool,
+                               int64_t* pool_off, double* pool_vals, int64_t* sizes) {
+    return guarded_c([&] {
+        if (!c) throw Error{VPG_ERR_INVALID_ARGUMENT, "corr is NULL"};
+        VPG_CUDA(cudaSetDevice(c->device));
+        if (sizes) {
+            sizes[0] = c->nt;
+            sizes[1] = c->nblocks;
+            sizes[2] = c->npool;
+            sizes[3] = int64_t(c->pool_vals.n);
+            sizes[4] = c->ndofs;
+        }
+        auto dl = [](void* h, const void* d, size_t bytes) {
+            if (h && bytes) VPG_CUDA(cudaMemcpy(h, d, bytes, cudaMemcpyDeviceToHost));
+        };
+        dl(blk_off, c->blk_off.p, c->blk_off.bytes());
+        dl(blk_cell, c->blk_cell.p, c->blk_cell.bytes());
+        dl(blk_pool, c->blk_pool.p, c->blk_pool.bytes());
+        dl(pool_off, c->pool_off.p, c->pool_off.bytes());
+        dl(pool_vals, c->pool_vals.p, c->pool_vals.bytes());
+    });
+}

@@ -20,6 +20,12 @@ struct vpg_corr {
     vpg::DBuf<int32_t> other_t;     // targets of the CSR kernel
 };
 
+namespace vpg {
+void corr_create_impl(int64_t nt, const int32_t* blk_off, int64_t nblocks, const int32_t* blk_cell,
+                      const int32_t* blk_pool, int64_t npool, const int64_t* pool_off, const double* pool_vals,
+                      bool dev_pool, int64_t ncell, const int32_t* node_off, int device, vpg_corr** corr);
+}
+
 struct vpg_charges {
     int device = 0;
     int64_t ncell = 0, ndofs = 0, nsrc = 0;

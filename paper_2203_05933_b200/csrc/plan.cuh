@@ -323,6 +323,7 @@ struct Plan {
     mutable std::mutex graph_mu;
     mutable std::vector<std::unique_ptr<GraphEntry>> graphs;
     mutable uint64_t graph_clock = 0;
+    mutable uint32_t host_rr = 0;   // host-pointer applies alternate between two staged graphs
     mutable bool graph_broken = false;  // capture unsupported: plain launches
 
     int64_t device_bytes() const;

@@ -91,8 +91,9 @@ def test_correction_apply_vs_reference(vp, ref, refop):
                           d["node_off"])
     corr = cm.apply(f, np.zeros(len(d["targets"])))
     scale = np.abs(out_ref).max()
+    # corr_ref carries one rounding of out_ref (|out| >> |corr|)
     assert np.abs(corr - corr_ref).max() <= 4e-15 * scale * 8
-    assert rel_l2(corr, corr_ref) <= 1e-13
+    assert rel_l2(corr, corr_ref) <= 1e-12
 
 
 def test_operator_apply_vs_reference(vp, R, mesh, refop):

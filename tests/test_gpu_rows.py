@@ -1,0 +1,247 @@
+"""Correction-row generation on the GPU (csrc/rows.cu)
+against the reference's own row builders, compiled in place
+(oracle/_ref/libvolpot_ref_op.so: singular.cpp, basis.cpp, quad1d.cpp,
+geometry.cpp, mesh.cpp with the Eigen restatement):
+
+* the 1-D rules (quad1d.cpp): Gauss-Legendre, -t log t / t Gauss rules,
+  graded ray rules -- restated on the host in rows.cu,
+* smooth_potential_row (singular.cpp:428-456),
+* SingularTargetRule::row (singular.cpp:383-415),
+* reduce_to_rays + apply_ray_quadrature (singular.cpp:274-310),
+* the operator rows (acc - smooth) . C of correction_row_generic
+  (potential.cpp:351-358) and the triangle near rows on table stars
+  (potential.cpp:322-334),
+* box_correction_table (singular.cpp:586-646) and the lattice rows
+  (potential.cpp:269-289),
+on straight, curved and box cells of a reference star mesh, for the Laplace
+and the modified-Helmholtz (lambda = 10) kernels.  Floating point: relative
+max error <= 1e-12 per row (the sums run in a different order than the
+reference's Eigen GEMVs).
+"""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+P, Q = 8, 16
+
+
+@pytest.fixture(scope="module")
+def R():
+    import oracle
+    try:
+        r = oracle.reference_operator()
+    except (FileNotFoundError, OSError) as e:  # pragma: no cover
+        pytest.skip(f"reference operator unavailable: {e}")
+    r.set_threads(os.cpu_count() or 1)
+    return r
+
+
+@pytest.fixture(scope="module")
+def rmesh(R):
+    return R.star_mesh(0.2, amp=0.1, arms=3)
+
+
+def engine(vp, R, rmesh, family, lam):
+    from paper_2203_05933_b200 import rows
+    st = rmesh.star
+    mesh = rows.Mesh(rmesh.type, rmesh.curve, rmesh.v, rmesh.tt, rmesh.ch, np.array([rows.CURVE_STAR]),
+                     np.array([[st["center"][0], st["center"][1], st["r0"], st["amp"], st["arms"], st["phase"]]]))
+    return rows.RowEngine(mesh, family, lam, P, Q, R.basis(0, P), R.basis(1, P), R.basis(3, P), R.basis(4, P, Q),
+                          R.basis(5, P, Q))
+
+
+@pytest.fixture(scope="module", params=[(0, 0.0), (1, 10.0)], ids=["laplace", "helmholtz"])
+def eng(request, vp, R, rmesh):
+    fam, lam = request.param
+    e = engine(vp, R, rmesh, fam, lam)
+    yield e
+    e.close()
+
+
+def _relmax(a, b):
+    return float(np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(b).max(), 1e-300))
+
+
+def _cells(rmesh):
+    """A few cells of each type: straight, curved, box."""
+    out = []
+    for t in (0, 1, 2):
+        idx = np.nonzero(rmesh.type == t)[0]
+        out += list(idx[:: max(1, len(idx) // 3)][:3])
+    return out
+
+
+def test_rules_match_reference(vp, R, eng):
+    for which, ref in [(0, R.rule1d(0, 16)), (1, R.rule1d(2, 20)), (2, R.rule1d(1, 20)), (3, R.rule1d(3))]:
+        x, w = eng.rule(which)
+        assert x.shape == ref[0].shape
+        assert np.abs(x - ref[0]).max() <= 4.5e-16 and np.abs(w - ref[1]).max() <= 4e-16 * max(1, np.abs(ref[1]).max())
+    for q in range(-2, 10):
+        d = 10.0 ** (-q - 0.5) if q > -2 else 12.0
+        x, w = eng.rule(4 + q + 2)
+        rx, rw = R.rule1d(4, 0, d)
+        # same construction; the reference build contracts a*b+c into FMAs (-march=native): <= 2 ulp
+        assert np.allclose(x, rx, rtol=4.5e-16, atol=0) and np.allclose(w, rw, rtol=4.5e-16, atol=0)
+
+
+def test_smooth_rows(vp, rmesh, eng):
+    fam, lam = eng.family, eng.lam
+    cells = _cells(rmesh)
+    rng = np.random.default_rng(1)
+    jobs, cl, r0s, refs = [], [], [], []
+    for c in cells:
+        ctr = rmesh.ch[c, :2] if rmesh.type[c] == 2 else rmesh.v[c].mean(0)
+        for pt in (ctr, ctr + rng.normal(0, 0.05, 2), ctr + np.array([0.3, -0.1])):
+            jobs.append(2)
+            cl.append(c)
+            r0s.append(pt)
+            refs.append(rmesh.smooth_row(c, P, Q, pt, fam, lam))
+    rows = eng.eval(jobs, cl, r0=np.array(r0s))
+    for g, r in zip(rows, refs):
+        assert _relmax(g, r) <= 1e-12
+
+
+def test_self_rows(vp, R, rmesh, eng):
+    fam, lam = eng.family, eng.lam
+    tri_nodes, box_nodes = R.basis(0, P), R.basis(2, P)
+    jobs, cl, r0s, z0s, refs = [], [], [], [], []
+    for c in _cells(rmesh):
+        nodes = box_nodes if rmesh.type[c] == 2 else tri_nodes
+        for j in (0, len(nodes) // 2, len(nodes) - 1):
+            z0 = nodes[j]
+            x = rmesh.map_deriv(c, z0)[:2]
+            jobs.append(0)
+            cl.append(c)
+            r0s.append(x)
+            z0s.append(z0)
+            refs.append(rmesh.self_row(c, P, z0, x, fam, lam))
+    rows = eng.eval(jobs, cl, r0=np.array(r0s), zeta0=np.array(z0s))
+    for g, r in zip(rows, refs):
+        assert _relmax(g, r) <= 1e-12
+
+
+def test_ray_rows(vp, rmesh, eng):
+    fam, lam = eng.family, eng.lam
+    rng = np.random.default_rng(2)
+    jobs, cl, r0s, z0s, zss, refs = [], [], [], [], [], []
+    for c in _cells(rmesh):
+        lo, hi = rmesh.v[c].min(0), rmesh.v[c].max(0)
+        if rmesh.type[c] == 2:
+            lo, hi = rmesh.ch[c, :2] - rmesh.ch[c, 2] / 2, rmesh.ch[c, :2] + rmesh.ch[c, 2] / 2
+        for k in range(3):
+            # a point just outside the cell (near zone) and one on its boundary star
+            ang = rng.uniform(0, 2 * np.pi)
+            x = (lo + hi) / 2 + (0.5 + 0.15 * (k + 1)) * (hi - lo) * np.array([np.cos(ang), np.sin(ang)])
+            z0 = rmesh.invert(c, x)
+            zs, _ = rmesh.nearest_reference_point(c, x)
+            jobs.append(1)
+            cl.append(c)
+            r0s.append(x)
+            z0s.append(z0)
+            zss.append(zs)
+            refs.append(rmesh.ray_row(c, P, z0, zs, x, fam, lam))
+    rows = eng.eval(jobs, cl, r0=np.array(r0s), zeta0=np.array(z0s), zstar=np.array(zss))
+    for g, r in zip(rows, refs):
+        assert _relmax(g, r) <= 1e-12
+
+
+def test_generic_operator_rows(vp, R, rmesh, eng):
+    """SelfGeneric / NearGeneric rows (acc - smooth) . C against the
+    reference operator's correction_row_generic."""
+    nodes = rmesh.nodes(P)
+    op = rmesh.operator(P, Q, nodes[:8], eng.family, eng.lam)
+    rng = np.random.default_rng(3)
+    jobs, cl, r0s, refs = [], [], [], []
+    for c in _cells(rmesh):
+        ctr = rmesh.ch[c, :2] if rmesh.type[c] == 2 else rmesh.v[c].mean(0)
+        for is_self in (True, False):
+            if is_self:
+                x = ctr + rng.normal(0, 0.01, 2)
+                if rmesh.nearest_reference_point(c, x)[1] > 0:
+                    x = ctr
+            else:
+                lo, hi = (rmesh.v[c].min(0), rmesh.v[c].max(0)) if rmesh.type[c] != 2 else \
+                    (rmesh.ch[c, :2] - rmesh.ch[c, 2] / 2, rmesh.ch[c, :2] + rmesh.ch[c, 2] / 2)
+                x = np.array([hi[0] + 0.05 * (hi[0] - lo[0]), ctr[1]])
+            jobs.append(5 if is_self else 6)
+            cl.append(c)
+            r0s.append(x)
+            refs.append(op.correction_row_generic(c, x, is_self))
+    rows = eng.eval(jobs, cl, r0=np.array(r0s))
+    for g, r in zip(rows, refs):
+        # (accurate - smooth) cancels to ~1e-4 of either term: rounding noise
+        # of the terms shows up amplified in the row
+        assert _relmax(g, r) <= 2e-10
+
+
+def test_box_table_and_lattice_rows(vp, R, rmesh, eng):
+    h = rmesh.h
+    ref_tab = R.box_table(P, eng.family, eng.lam, h)
+    nb = P * P
+    jobs, aux, r0s = [], [], []
+    box_nodes = R.basis(2, P)
+    for o in range(25):
+        for j in (0, 27, 63):
+            jobs.append(7)
+            aux.append(o * 256 + j)
+            ox, oy = o % 5 - 2, o // 5 - 2
+            r0s.append([ox * h + 0.5 * h * box_nodes[j, 0], oy * h + 0.5 * h * box_nodes[j, 1]])
+    rows = eng.eval(jobs, [-1] * len(jobs), aux=aux, r0=np.array(r0s), lattice_h=h)
+    # (acc - smooth) . C on the origin box, acc = the reference table row
+    C = R.basis(3, P)
+    bidx = int(np.nonzero(rmesh.type == 2)[0][0])
+    for (a, x), g in zip(zip(aux, r0s), rows):
+        o, j = a // 256, a % 256
+        # smooth row on a box of size h centred at 0: shift the mesh box's row
+        ctr = rmesh.ch[bidx, :2]
+        sm = rmesh.smooth_row(bidx, P, Q, np.array(x) + ctr, eng.family, eng.lam)
+        ref = (ref_tab[o, j] - sm) @ C
+        # outer-ring rows are (30x30 rule - 16x16 rule) . C: pure cancellation,
+        # so the error is measured against the terms' scale
+        scale = np.abs(ref_tab[o, j]).max() * np.abs(C).sum(0).max()
+        assert np.abs(g - ref).max() <= 1e-13 * scale
+    assert ref_tab.shape == (25, nb, nb)
+
+
+@pytest.mark.parametrize("family,lam", [(0, 0.0), (1, 10.0)], ids=["laplace", "helmholtz"])
+def test_correction_map_vs_reference(vp, R, rmesh, family, lam):
+    """build_corrections on the device against the reference operator's own
+    map: identical block structure (cells, pool slots, CSR) and rows within
+    1e-11 relative per row; node targets plus off-node targets."""
+    from paper_2203_05933_b200 import rows
+    nodes = rmesh.nodes(P)
+    rng = np.random.default_rng(5)
+    extra = nodes[rng.choice(len(nodes), 40, replace=False)] * 0.97
+    tgt = np.concatenate([nodes, extra])
+    op = rmesh.operator(P, Q, tgt, family, lam)
+    ref = op.export()
+    eng = engine(vp, R, rmesh, family, lam)
+    cm, st = rows.build_correction_map(eng, ref["nodes"], ref["node_off"], tgt)
+    got = rows.export_map(cm)
+    assert np.array_equal(got["blk_off"], ref["blk_off"])
+    assert np.array_equal(got["blk_cell"], ref["blk_cell"])
+    assert np.array_equal(got["blk_pool"], ref["blk_pool"])
+    assert np.array_equal(got["pool_off"], ref["pool_off"])
+    # rows are (accurate - smooth) . C, i.e. cancellation-bound: compare on
+    # the pool's scale, then per row for all rows not dominated by noise
+    a, b = got["pool_vals"], ref["pool_vals"]
+    assert np.abs(a - b).max() <= 1e-12 * np.abs(b).max()
+    po = ref["pool_off"]
+    big = 0
+    for r in range(len(po) - 1):
+        ra, rb = a[po[r]:po[r + 1]], b[po[r]:po[r + 1]]
+        if np.abs(rb).max() > 1e-3 * np.abs(b).max():
+            big += 1
+            assert np.abs(ra - rb).max() <= 5e-11 * np.abs(rb).max()
+    assert big > 0
+    assert st["box_lattice"] > 0 and st["tri_self_node"] > 0 and st["tri_near_snap"] > 0
+    # applying it equals applying the reference map
+    f = np.cos(nodes[:, 0] * 3) * np.exp(nodes[:, 1])
+    cref = vp.CorrectionMap(ref["blk_off"], ref["blk_cell"], ref["blk_pool"], ref["pool_off"], ref["pool_vals"],
+                            ref["node_off"])
+    a = cm.apply(f, np.zeros(len(tgt)))
+    b = cref.apply(f, np.zeros(len(tgt)))
+    assert np.abs(a - b).max() <= 1e-11 * np.abs(b).max()
