@@ -213,8 +213,13 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------- GPU arm
-def cpu_baseline_sample(wl, inter, budget_s=20.0):
-    """oracle/_ref on the host cores: full applies, bounded to ~budget_s."""
+def cpu_baseline_sample(wl, inter, budget_s=20.0, corr=None):
+    """oracle/_ref on the host cores: full applies, bounded to ~budget_s.
+    Operator workloads (corr given): the CPU composition of
+    VolumePotentialOperator::apply (SURVEY.md 8d) -- our restatement of
+    build_charges (potential.cpp:397-412) + the reference SummationPlan::apply
+    + our restatement of the correction loop (potential.cpp:446-462) on the
+    same map, all on the host cores."""
     import oracle
     try:
         ref = oracle.reference()
@@ -235,6 +240,27 @@ def cpu_baseline_sample(wl, inter, budget_s=20.0):
         plan.apply(wl.q)
         times.append(time.perf_counter() - t0)
     t = float(np.median(times))
+    if corr is not None:
+        from paper_2203_05933_b200 import rows as RW
+        rest = oracle.restatement()
+        mp = RW.export_map(corr["map"])
+        ct, o0, o1 = corr["charges"]
+        f = wl.notes["f"]
+        t0 = time.perf_counter()
+        qv = rest.build_charges(ct, corr["node_off"], corr["src_off"], o0, o1, wl.notes["src_wj"], f, threads=cores)
+        t_ch = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        rest.correction_apply(mp["blk_off"], mp["blk_cell"], mp["blk_pool"], mp["pool_off"], mp["pool_vals"],
+                              corr["node_off"], f, np.zeros(wl.nt), threads=cores)
+        t_co = time.perf_counter() - t0
+        tt = t + t_ch + t_co
+        return {"value": inter / tt, "unit": "interactions/s", "cores": cores, "kind": "reference",
+                "ms_per_step": tt * 1e3, "split_ms": {"build_charges": t_ch * 1e3, "fmm": t * 1e3,
+                                                      "correction": t_co * 1e3},
+                "sample": f"operator apply composed on {cores} host threads: restated build_charges + median of "
+                          f"{n} reference SummationPlan::apply (oracle/_ref) + restated correction loop on the "
+                          f"same map; q max diff vs the workload charges "
+                          f"{float(np.abs(qv - wl.q).max() / np.abs(wl.q).max()):.1e} (rel)"}
     return {"value": inter / t, "unit": "interactions/s", "cores": cores,
             "kind": "reference", "ms_per_step": t * 1e3,
             "sample": f"median of {n} full SummationPlan::apply of the workload after 1 warm-up "
@@ -276,7 +302,35 @@ def run_gpu(args):
     # the operator-level apply (potential.cpp:431-470) -- build_charges
     # (q = w f, identity oversampling) -> FMM step -> + C f
     op = None
-    if "corr" in wl.notes and world == 1:
+    corr_info = None
+    if "mesh" in wl.notes and world == 1:
+        # the reference's own operator layout on its hybrid mesh: correction
+        # map built on the device (build_corrections, csrc/rows.cu), the
+        # tensor-core build_charges with the reference oversampling matrices
+        from paper_2203_05933_b200 import rows as RW
+        m, b = wl.notes["mesh"], wl.notes["basis"]
+        pp, qq = wl.notes["p"], wl.notes["q"]
+        mesh = RW.Mesh(m["type"], m["curve"], m["v"], m["tt"], m["ch"], np.array([RW.CURVE_STAR]),
+                       m["star"][None, :])
+        fam = 1 if wl.kernel == "helmholtz" else 0
+        eng = RW.RowEngine(mesh, fam, wl.lam, pp, qq, b["tri_nodes"], b["tri_C"], b["box_C"], b["tri_src"],
+                           b["tri_src_w"], device=local)
+        box = m["type"] == 2
+        node_off = np.concatenate([[0], np.cumsum(np.where(box, pp * pp, pp * (pp + 1) // 2))]).astype(np.int32)
+        src_off = np.concatenate([[0], np.cumsum(np.where(box, b["box_over"].shape[0],
+                                                          b["tri_over"].shape[0]))]).astype(np.int32)
+        torch.cuda.synchronize()
+        t_cb = time.perf_counter()
+        cm, cst = RW.build_correction_map(eng, wl.tgt, node_off, wl.tgt)
+        corr_build_ms = (time.perf_counter() - t_cb) * 1e3
+        ch = vp.ChargeMap(np.where(box, 0, 1).astype(np.int32), node_off, src_off, b["box_over"], b["tri_over"],
+                          wl.notes["src_wj"], device=local)
+        op = vp.VolumePotentialOperator(plan, cm, ch)
+        f_np = np.ascontiguousarray(wl.notes["f"], dtype=np.float64)
+        f_d = torch.from_numpy(f_np).to("cuda")
+        corr_info = {"build_ms": corr_build_ms, "stats": cst, "node_off": node_off, "src_off": src_off,
+                     "map": cm, "charges": (np.where(box, 0, 1).astype(np.int32), b["box_over"], b["tri_over"])}
+    elif "corr" in wl.notes and world == 1:
         csr = wl.notes["corr"]()
         ncell = csr["node_off"].size - 1
         cm = vp.CorrectionMap(csr["blk_off"], csr["blk_cell"], csr["blk_pool"], csr["pool_off"],
@@ -457,6 +511,20 @@ def run_gpu(args):
                                        if near_k != "p2p_sym_kernel" else
                                        "29 per unordered near-field pair (27 per pair, SURVEY.md 8d, + 2 for the "
                                        "second target's accumulation; ordered pairs / 2)")}
+    elif wl.kernel == "helmholtz" and info["levels"] > 0 and info["p2p_pairs"] > 0 and phases["p2p"] > 0:
+        # native Chebyshev FMM: the dominant phase is the K0 near field (+ L2P),
+        # 70 flops per K0 pair by the SURVEY.md 8d convention
+        dom = "p2p"
+        k0_flops = info["p2p_pairs"] * 70.0
+        achieved = k0_flops / (phases["p2p"] * 1e-3) / 1e12
+        peak = fp64_peak_tflops("fp64")
+        kern_stats["p2p"] = {"ms": phases["p2p"], "pairs": info["p2p_pairs"],
+                             "pairs_per_s": info["p2p_pairs"] / (phases["p2p"] * 1e-3)}
+        kern_stats["m2l"] = {"ms": phases["m2l"], "pairs": info["m2l_pairs"]}
+        roofline = {"bound": "fp64", "kernel": "hf_l2p_p2p_kernel", "achieved": achieved, "peak": peak,
+                    "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                    "peak_source": "measured FP64 CUDA-core (DFMA) peak, profiles/fp64_peak_r01.json",
+                    "flops_per_unit": "70 per near-field K0 pair (SURVEY.md 8d convention), phase time includes L2P"}
     else:
         dom = "p2p"
         roofline = {"bound": "fp64", "kernel": "traverse_kernel" if wl.kernel == "helmholtz" else "allpairs_kernel",
@@ -485,11 +553,130 @@ def run_gpu(args):
         "roofline": roofline,
         "clocks": clk.summary(),
     }
+    if corr_info is not None:
+        st = corr_info["stats"]
+        line["config"].update({"mesh": wl.notes["h_name"], "cells": wl.notes["cells"], "p": wl.notes["p"],
+                               "q": wl.notes["q"], "ndofs": int(f_np.size),
+                               "correction_blocks": int(st["blocks"]), "correction_rows": int(st["pool_rows"])})
+        line["correction_build"] = {"ms": corr_info["build_ms"], "rows_per_s": st["pool_rows"] / (
+            corr_info["build_ms"] * 1e-3), **{k: v for k, v in st.items()}}
+        line["acceptance7_correction_over_smooth"] = phases.get("correction", 0.0) / max(ms - phases.get(
+            "correction", 0.0), 1e-9)
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline_sample(wl, inter)
+        line["cpu_baseline"] = cpu_baseline_sample(wl, inter, corr=corr_info)
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+    return 0
+
+
+# ----------------------------------------------------------------- correction rows
+CORR_METRIC = "correction rows/s (build_corrections: classification, task list, rows)"
+CORR_MESH = "star_h00125"
+
+
+def _corr_setup(local, h_name=CORR_MESH):
+    from paper_2203_05933_b200 import rows as RW
+    from paper_2203_05933_b200 import workloads as W
+    m = dict(np.load(os.path.join(W.GOLDEN, f"mesh_{h_name}.npz")))
+    b = dict(np.load(os.path.join(W.GOLDEN, "basis_p8_q16.npz")))
+    nodes, _ = W.map_cells(m, [b["tri_nodes"], b["box_nodes"]])
+    box = m["type"] == 2
+    node_off = np.concatenate([[0], np.cumsum(np.where(box, 64, 36))]).astype(np.int32)
+    return RW, m, b, nodes, node_off
+
+
+def _corr_reference_rate(h_name=CORR_MESH, ntarget=1500, seed=3):
+    """The reference's build_corrections rate on the host cores: the reference
+    operator (oracle/_ref/libvolpot_ref_op.so) built on the same reference mesh
+    for a seeded subset of its nodes, minus a one-target build (the shared
+    tables and the sources, built once per operator)."""
+    import oracle
+    R = oracle.reference_operator()
+    cores = os.cpu_count() or 1
+    R.set_threads(cores)
+    h = {"star_h0125": 0.125, "star_h005": 0.05, "star_h0025": 0.025, "star_h00125": 0.0125}[h_name]
+    rm = R.star_mesh(h, r0=1.0, amp=0.3, arms=5)
+    nodes = rm.nodes(8)
+    rng = np.random.default_rng(seed)
+    sub = nodes[np.sort(rng.choice(len(nodes), ntarget, replace=False))]
+    rm.operator(8, 16, nodes[:1])  # warm the cached reference tables
+    t0 = time.perf_counter()
+    op1 = rm.operator(8, 16, nodes[:1])
+    t1 = time.perf_counter()
+    opn = rm.operator(8, 16, sub)
+    t2 = time.perf_counter()
+    rows = opn.npool - op1.npool
+    dt = (t2 - t1) - (t1 - t0)
+    return {"value": rows / dt, "unit": "rows/s", "cores": cores, "kind": "reference",
+            "ms_per_row": dt / rows * 1e3,
+            "sample": f"reference VolumePotentialOperator build (oracle/_ref/libvolpot_ref_op.so, "
+                      f"set_thread_count({cores})) on the same reference mesh for {ntarget} seeded nodes "
+                      f"({rows} correction rows) minus a 1-target build"}
+
+
+def run_corr(args):
+    import torch
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        cb = _corr_reference_rate()
+        line = {"impl": "reference", "metric": CORR_METRIC, "value": cb["value"], "unit": "rows/s", "n_gpus": world,
+                "steps": 1, "warmup": 1, "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "reference star mesh (tests/golden)",
+                "config": {"workload": "corr", "mesh": CORR_MESH, "p": 8, "q": 16},
+                "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": "rows/s", "h2d_bytes_per_step": 0,
+                                            "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return 0
+    torch.cuda.set_device(local)
+    RW, m, b, nodes, node_off = _corr_setup(local)
+    mesh = RW.Mesh(m["type"], m["curve"], m["v"], m["tt"], m["ch"], np.array([RW.CURVE_STAR]), m["star"][None, :])
+    eng = RW.RowEngine(mesh, 0, 0.0, 8, 16, b["tri_nodes"], b["tri_C"], b["box_C"], b["tri_src"], b["tri_src_w"],
+                       device=local)
+    clk = ClockSampler(local).__enter__()
+    for _ in range(args.warmup):
+        cm, st = RW.build_correction_map(eng, nodes, node_off, nodes)
+        cm.close()
+    times, stats = [], None
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        cm, stats = RW.build_correction_map(eng, nodes, node_off, nodes)
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+        cm.close()
+    clk.__exit__(None, None, None)
+    t = float(np.mean(times))
+    rows = stats["pool_rows"]
+    if rank != 0:
+        return 0
+    # roofline of the row kernels: per quadrature node 4 nb (basis recurrences
+    # and the row accumulate) + 30 (cell map, kernel log, weight) flops,
+    # nb = 36 on triangle rows, 64 on box rows (convention, DESIGN.md)
+    flops = stats["quad_nodes_tri"] * (4 * 36 + 30) + stats["quad_nodes_box"] * (4 * 64 + 30)
+    achieved = flops / (stats["rows_ms"] * 1e-3) / 1e12
+    peak = fp64_peak_tflops("fp64")
+    line = {
+        "metric": CORR_METRIC, "value": rows / t, "unit": "rows/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "the reference's own hybrid mesh of the configs[1] star "
+                                                      "(tests/golden/mesh_star_h00125.npz), targets = its nodes",
+        "config": {"workload": "corr", "mesh": CORR_MESH, "cells": int(len(m["type"])), "targets": int(len(nodes)),
+                   "p": 8, "q": 16, "D": 0.4, "step": "build_corrections (potential.cpp:133-349) on the device"},
+        "e2e": {"value": rows / t, "unit": "rows/s", "ms_per_step": t * 1e3,
+                "h2d_bytes_per_step": int(nodes.nbytes * 2), "d2h_bytes_per_step": 0,
+                "path": "vpg_corr_build with host target arrays; the map stays on the device"},
+        "gpu_launches": 4, "stats": stats,
+        "roofline": {"bound": "fp64", "kernel": "rows_kernel", "achieved": achieved, "peak": peak,
+                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                     "flops_per_unit": "per quadrature node 4 nb + 30 (nb = 36 triangle rows, 64 box rows)"},
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = _corr_reference_rate()
+    print(json.dumps(line), flush=True)
     return 0
 
 
@@ -670,7 +857,9 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "layer", "layer_mh"])
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD,
+                    choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "layer", "layer_mh", "op_star", "op_star_mh",
+                             "op_star_84k", "corr"])
     ap.add_argument("--mode", default="reference", choices=["reference", "native"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -679,6 +868,8 @@ def main():
     args = ap.parse_args()
     if args.workload in ("layer", "layer_mh"):
         return run_layer(args)
+    if args.workload == "corr":
+        return run_corr(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_gpu(args)

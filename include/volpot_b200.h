@@ -264,9 +264,11 @@ int vpg_rows_eval(vpg_rows* rows, int64_t ntask, const int32_t* job, const int32
  * and pool slots on the host (node-coincident targets found by exact bits in
  * nodes_xy, the dof layout of mesh_nodes with node_off per cell; shared box
  * lattice rows), every row on the device; the map is created on the rows
- * context's device.  stats (may be NULL, 11 doubles): classification ms,
+ * context's device.  stats (may be NULL, 13 doubles): classification ms,
  * task/table ms, row ms, blocks, pool rows, pool doubles, then the block
- * counts of TriSelfNode, TriNearSnap, SelfGeneric, NearGeneric, BoxLattice.
+ * counts of TriSelfNode, TriNearSnap, SelfGeneric, NearGeneric, BoxLattice,
+ * then the quadrature nodes the row kernels evaluated on triangle and on box
+ * cells (13 doubles).
  * Errors: the reference's classify_target messages (VPG_ERR_INVALID_ARGUMENT). */
 int vpg_corr_build(vpg_rows* rows, int64_t ndofs, const double* nodes_xy, const int32_t* node_off, int64_t nt,
                    const double* tgt_xy, double D, vpg_corr** corr, double* stats);

@@ -103,7 +103,7 @@ class Restatement:
         h.vo_correction_apply.argtypes = [i64, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int]
         h.vo_correction_apply.restype = None
         h.vo_build_charges.argtypes = [i64, _P, _P, _P, _P, C.c_int, C.c_int, _P, C.c_int,
-                                       C.c_int, _P, _P, _P]
+                                       C.c_int, _P, _P, _P, C.c_int]
         h.vo_build_charges.restype = None
         self.h = h
 
@@ -209,7 +209,7 @@ class Restatement:
         self.h.vo_correction_apply(len(a[0]) - 1, *(_p(x) for x in a), _p(o), threads)
         return o
 
-    def build_charges(self, cell_type, node_off, src_off, over0, over1, src_wj, f):
+    def build_charges(self, cell_type, node_off, src_off, over0, over1, src_wj, f, threads=0):
         ct = np.ascontiguousarray(cell_type, np.int32)
         no = np.ascontiguousarray(node_off, np.int32)
         so = np.ascontiguousarray(src_off, np.int32)
@@ -218,7 +218,7 @@ class Restatement:
         q = np.empty(int(so[-1]))
         self.h.vo_build_charges(len(ct), _p(ct), _p(no), _p(so), _p(o0), o0.shape[1], o0.shape[0],
                                 _p(o1), o1.shape[1] if o1.ndim == 2 else 0,
-                                o1.shape[0] if o1.ndim == 2 else 0, _p(_vec(src_wj)), _p(_vec(f)), _p(q))
+                                o1.shape[0] if o1.ndim == 2 else 0, _p(_vec(src_wj)), _p(_vec(f)), _p(q), threads)
         return q
 
 

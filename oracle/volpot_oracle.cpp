@@ -854,8 +854,9 @@ void vo_build_charges(int64_t ncell, const int32_t* cell_type,
                       const int32_t* node_off, const int32_t* src_off,
                       const double* over0, int np0, int nq0,
                       const double* over1, int np1, int nq1,
-                      const double* src_wj, const double* f, double* charges) {
-    for (int64_t c = 0; c < ncell; ++c) {
+                      const double* src_wj, const double* f, double* charges, int nthreads) {
+    ThreadScope ts(nthreads);
+    pfor(ncell, [&](int64_t c) {  // potential.cpp:400 parallel_try over cells
         const bool t0 = cell_type[c] == 0;
         const double* O = t0 ? over0 : over1;
         const int np = t0 ? np0 : np1, nq = t0 ? nq0 : nq1;
@@ -866,7 +867,7 @@ void vo_build_charges(int64_t ncell, const int32_t* cell_type,
             for (int i = 0; i < np; ++i) v += O[size_t(s) * np + i] * fc[i];
             charges[base + s] = src_wj[base + s] * v;
         }
-    }
+    });
 }
 
 

@@ -94,7 +94,7 @@ void vo_build_charges(int64_t ncell, const int32_t* cell_type,
                       const int32_t* node_off, const int32_t* src_off,
                       const double* over0, int np0, int nq0,
                       const double* over1, int np1, int nq1,
-                      const double* src_wj, const double* f, double* charges);
+                      const double* src_wj, const double* f, double* charges, int nthreads);
 
 /* kernel.cpp:174-179 -- K1 (series below 2, Chebyshev fits above). */
 double vo_bessel_k1(double x);

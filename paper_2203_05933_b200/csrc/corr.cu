@@ -13,6 +13,8 @@
 #include <algorithm>
 #include <memory>
 #include <map>
+#include <set>
+#include <unordered_map>
 #include <vector>
 
 #include "plan.cuh"
@@ -49,6 +51,101 @@ corr_apply_kernel(int64_t nt, const int32_t* tlist, const int32_t* blk_off, cons
     if (lane == 0) out[t] += acc;
 }
 
+// CSR apply over per-block descriptors (row offset, f offset, length built
+// at map creation): lane j of a target's warp loads block j's descriptor, so
+// the three dependent index loads of a block (blk_pool -> pool_off, blk_cell
+// -> node_off) are gone and the data loads of successive blocks are
+// independent (the loop is unrolled); one butterfly per target.
+__global__ void __launch_bounds__(kCorrWarps * 32)
+corr_desc_kernel(int64_t nt, const int32_t* tlist, const int32_t* blk_off, const BlkDesc* desc,
+                 const double* pool_vals, const double* f, double* out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t ti = int64_t(blockIdx.x) * kCorrWarps + (threadIdx.x >> 5);
+    if (ti >= nt) return;
+    const int64_t t = tlist ? tlist[ti] : ti;
+    const int k0 = blk_off[t], n = blk_off[t + 1] - k0;
+    double acc = 0.0;
+    for (int b0 = 0; b0 < n; b0 += 32) {
+        BlkDesc d{0, 0, 0};
+        if (b0 + lane < n) d = desc[k0 + b0 + lane];
+        const int m = min(32, n - b0);
+        // four blocks at a time: all their loads are issued before the FMAs
+        for (int j = 0; j < m; j += 4) {
+            double rv[8], fv[8];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int jj = min(j + u, 31);
+                const int64_t row = __shfl_sync(0xffffffffu, d.row, jj);
+                const int fo = __shfl_sync(0xffffffffu, d.f, jj);
+                const int len = j + u < m ? __shfl_sync(0xffffffffu, d.len, jj) : 0;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int e = lane + 32 * h;
+                    const bool ok = e < len;
+                    rv[2 * u + h] = ok ? __ldg(pool_vals + row + e) : 0.0;
+                    fv[2 * u + h] = ok ? __ldg(f + fo + e) : 0.0;
+                }
+                // rows longer than 64 (p > 8 boxes): the rest, in order
+                for (int e = lane + 64; e < len; e += 32) acc = fma(__ldg(pool_vals + row + e), __ldg(f + fo + e), acc);
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc = fma(rv[k], fv[k], acc);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) out[t] += acc;
+}
+
+// The residual blocks with half a warp per target (two targets per warp):
+// a lane covers entries l, l + 16, l + 32, l + 48 of each row (rows <= 64;
+// longer rows finish in order), four blocks' loads issued before their FMAs.
+__global__ void __launch_bounds__(kCorrWarps * 32)
+corr_desc16_kernel(int64_t nt, const int32_t* tlist, const int32_t* blk_off, const BlkDesc* desc,
+                   const double* pool_vals, const double* f, double* out) {
+    const int lane = threadIdx.x & 31, half = lane >> 4, l = lane & 15;
+    const unsigned hmask = half ? 0xffff0000u : 0x0000ffffu;
+    const int64_t ti = (int64_t(blockIdx.x) * kCorrWarps + (threadIdx.x >> 5)) * 2 + half;
+    const bool live = ti < nt;
+    const int64_t t = live ? (tlist ? tlist[ti] : ti) : 0;
+    const int k0 = live ? blk_off[t] : 0, n = live ? blk_off[t + 1] - k0 : 0;
+    double acc = 0.0;
+    for (int b0 = 0; b0 < n; b0 += 16) {
+        BlkDesc d{0, 0, 0};
+        if (b0 + l < n) d = desc[k0 + b0 + l];
+        const int m = min(16, n - b0);
+        for (int j = 0; j < m; j += 4) {
+            double rv[16], fv[16];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int src = (half << 4) + min(j + u, 15);
+                const int64_t row = __shfl_sync(hmask, d.row, src);
+                const int fo = __shfl_sync(hmask, d.f, src);
+                const int len = j + u < m ? __shfl_sync(hmask, d.len, src) : 0;
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const int e = l + 16 * h;
+                    const bool ok = e < len;
+                    rv[4 * u + h] = ok ? __ldg(pool_vals + row + e) : 0.0;
+                    fv[4 * u + h] = ok ? __ldg(f + fo + e) : 0.0;
+                }
+                for (int e = l + 64; e < len; e += 16) acc = fma(__ldg(pool_vals + row + e), __ldg(f + fo + e), acc);
+            }
+#pragma unroll
+            for (int k = 0; k < 16; ++k) acc = fma(rv[k], fv[k], acc);
+        }
+    }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (live && l == 0) out[t] += acc;
+}
+
+__global__ void gather_rows_kernel(const int64_t* rowsrc, const double* pool_vals, double* mats) {
+    const int64_t r = blockIdx.x;
+    const int64_t src = rowsrc[r];
+    mats[r * 64 + threadIdx.x] = src >= 0 ? pool_vals[src + threadIdx.x] : 0.0;
+}
+
 // Lattice groups on the FP64 tensor cores: a CTA takes 64 groups (64
 // targets each) and walks the shared 64 x 64 row blocks M_q: out[64g + u] +=
 // sum_q sum_i M_q[u][i] f[cell(g, q) + i] as Y = M_q F_q (mma.sync m8n8k4),
@@ -56,7 +153,8 @@ corr_apply_kernel(int64_t nt, const int32_t* tlist, const int32_t* blk_off, cons
 template <int kLatTile>  // groups per CTA (64; 16 or 8 for small maps: more CTAs)
 __global__ void __launch_bounds__(256)
 corr_lattice_kernel(int64_t ngroups, int nmat, const int32_t* group, const int32_t* cellof,
-                    const int64_t* moff, const double* pool_vals, const double* f, double* out) {
+                    const int32_t* tile_off, const int32_t* tile_mats, const double* mats, const double* f,
+                    double* out) {
     constexpr int K = 64, kS = K + 4, kNT = kLatTile / 8;
     extern __shared__ __align__(16) double lsm[];
     double* ms = lsm;            // [u][i]
@@ -73,8 +171,9 @@ corr_lattice_kernel(int64_t ngroups, int nmat, const int32_t* group, const int32
     constexpr int kMR = K * K / 2 / 256, kFR = K * kLatTile / 256;
     double2 mreg[kMR];
     double freg[kFR];
+    const int q0 = tile_off[blockIdx.x], q1 = tile_off[blockIdx.x + 1];  // this tile's matrices
     auto fetch = [&](int q) {
-        const double2* mg = reinterpret_cast<const double2*>(pool_vals + moff[q]);
+        const double2* mg = reinterpret_cast<const double2*>(mats + int64_t(q) * K * K);
 #pragma unroll
         for (int r = 0; r < kMR; ++r) mreg[r] = mg[threadIdx.x + 256 * r];
 #pragma unroll
@@ -84,8 +183,8 @@ corr_lattice_kernel(int64_t ngroups, int nmat, const int32_t* group, const int32
             freg[r] = c >= 0 ? f[int64_t(c) + i] : 0.0;
         }
     };
-    if (nmat > 0) fetch(0);
-    for (int q = 0; q < nmat; ++q) {
+    if (q1 > q0) fetch(tile_mats[q0]);
+    for (int qi = q0; qi < q1; ++qi) {
         __syncthreads();  // the previous block's DMMAs are done with ms / fs
 #pragma unroll
         for (int r = 0; r < kMR; ++r) {
@@ -98,7 +197,7 @@ corr_lattice_kernel(int64_t ngroups, int nmat, const int32_t* group, const int32
             fs[i * (kLatTile + 4) + g] = freg[r];
         }
         __syncthreads();
-        if (q + 1 < nmat) fetch(q + 1);
+        if (qi + 1 < q1) fetch(tile_mats[qi + 1]);
 #pragma unroll 4
         for (int k4 = 0; k4 < K; k4 += 4) {
             const double a = ms[(8 * warp + rq) * kS + k4 + kq];
@@ -118,8 +217,106 @@ corr_lattice_kernel(int64_t ngroups, int nmat, const int32_t* group, const int32
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int g = 8 * n8 + 2 * kq + h;
-            if (g < ng) out[int64_t(group[g0 + g]) * K + u] += acc[n8][h];
+            if (g < ng) out[int64_t(group[g0 + g]) + u] += acc[n8][h];
         }
+}
+
+// build_charges on the FP64 tensor cores: per cell kind, Q = O F with O the
+// kind's oversampling matrix (nq x np, staged once per CTA in smem as A
+// fragments, row stride == 4 mod 16 doubles) and F the f segments of a tile
+// of 32 cells (np x 32, B fragments); mma.sync m8n8k4 (DMMA), each warp owns
+// every 8th 8-row tile of O for the 4 column tiles; results go straight from
+// the accumulators to charges[src_off[c] + s] * src_wj (a lane's 8 rows of
+// one cell are 64 contiguous bytes).  Persistent CTAs walk the cell tiles.
+constexpr int kChTile = 32;  // largest cell tile (4 column tiles of 8 cells)
+struct ChKind {
+    int64_t ncell;
+    const int32_t* cells;
+    const double* O;
+    int np, nq;
+    int ntl;    // 8-cell column tiles per CTA tile (1, 2 or 4)
+    int grid;   // CTAs of this kind
+};
+// Both cell kinds in one launch: CTAs [0, k0.grid) take the box tiles, the
+// rest the triangle tiles (split by flops), tiles of 8 ntl cells so that
+// small maps still spread over every SM.
+template <int kMT>  // 8-row tiles per warp: ceil(ceil(nq / 8) / 8), max over the kinds
+__global__ void __launch_bounds__(256)
+charges_mma_kernel(ChKind k0, ChKind k1, const int32_t* node_off, const int32_t* src_off, const double* src_wj,
+                   const double* f, double* charges) {
+    extern __shared__ __align__(16) double csm[];
+    const bool second = int(blockIdx.x) >= k0.grid;
+    const ChKind K = second ? k1 : k0;
+    const int bid = second ? int(blockIdx.x) - k0.grid : int(blockIdx.x);
+    const int np = K.np, nq = K.nq, ntl = K.ntl, tile = 8 * ntl;
+    const int Kp = (np + 3) & ~3, Mp = (nq + 7) & ~7;
+    const int As = Kp + ((4 - Kp % 16) + 16) % 16;  // row stride == 4 mod 16
+    constexpr int Bs = kChTile + 4;                  // == 4 mod 16
+    double* A = csm;              // [Mp][As]
+    double* B = csm + Mp * As;    // [Kp][Bs]
+    for (int e = threadIdx.x; e < Mp * Kp; e += blockDim.x) {
+        const int r = e / Kp, k = e % Kp;
+        A[r * As + k] = (r < nq && k < np) ? K.O[int64_t(r) * np + k] : 0.0;
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int kq = lane & 3, rq = lane >> 2;
+    const int mtiles = Mp / 8;
+    for (int64_t t0 = int64_t(bid) * tile; t0 < K.ncell; t0 += int64_t(K.grid) * tile) {
+        const int nc = int(min(int64_t(tile), K.ncell - t0));
+        __syncthreads();  // A staged / the previous tile's B reads are done
+        for (int e = threadIdx.x; e < tile * Kp; e += blockDim.x) {
+            const int j = e / Kp, i = e % Kp;
+            double v = 0.0;
+            if (j < nc && i < np) v = f[int64_t(node_off[K.cells[t0 + j]]) + i];
+            B[i * Bs + j] = v;
+        }
+        __syncthreads();
+        double acc[kMT][4][2];
+#pragma unroll
+        for (int m = 0; m < kMT; ++m)
+#pragma unroll
+            for (int n = 0; n < 4; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+        for (int k4 = 0; k4 < Kp; k4 += 4) {
+            double b[4];
+#pragma unroll
+            for (int n = 0; n < 4; ++n) b[n] = n < ntl ? B[(k4 + kq) * Bs + 8 * n + rq] : 0.0;
+#pragma unroll
+            for (int m = 0; m < kMT; ++m) {
+                const int mt = warp + 8 * m;
+                if (mt < mtiles) {
+                    const double a = A[(8 * mt + rq) * As + k4 + kq];
+#pragma unroll
+                    for (int n = 0; n < 4; ++n)
+                        if (n < ntl)
+                            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                                         : "+d"(acc[m][n][0]), "+d"(acc[m][n][1])
+                                         : "d"(a), "d"(b[n]));
+                }
+            }
+        }
+        // lane: row 8 mt + rq, cells 8 n + 2 kq + {0, 1}
+#pragma unroll
+        for (int m = 0; m < kMT; ++m) {
+            const int s = 8 * (warp + 8 * m) + rq;
+            if (warp + 8 * m >= mtiles || s >= nq) continue;
+#pragma unroll
+            for (int n = 0; n < 4; ++n)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int j = 8 * n + 2 * kq + h;
+                    if (n < ntl && j < nc) {
+                        const int64_t o = int64_t(src_off[K.cells[t0 + j]]) + s;
+                        charges[o] = src_wj[o] * acc[m][n][h];
+                    }
+                }
+        }
+    }
+}
+
+size_t charges_mma_smem(int np, int nq) {
+    const int Kp = (np + 3) & ~3, Mp = (nq + 7) & ~7;
+    const int As = Kp + ((4 - Kp % 16) + 16) % 16;
+    return sizeof(double) * (size_t(Mp) * As + size_t(Kp) * (kChTile + 4));
 }
 
 __global__ void charges_kernel(const int32_t* cell_type, const int32_t* node_off,
@@ -245,101 +442,171 @@ void vpg::corr_create_impl(int64_t nt, const int32_t* blk_off, int64_t nblocks, 
             upload(c->pool_vals, pool_vals, size_t(nvals));
         }
         upload(c->node_off, node_off, size_t(ncell + 1));
-        // lattice groups: 64 consecutive targets with identical block-cell
-        // sequences whose rows are base_r + u of contiguous 64 x 64 blocks
+
+        // Shared-row groups on the tensor cores.  A group is a run of 64
+        // consecutive targets whose first (self) blocks share one cell -- the
+        // nodes of one box when targets are nodes.  Per group and cell, the
+        // blocks whose pool row is shared (length 64, used by >= 8 blocks: the
+        // box lattice rows, potential.cpp:256-267) form a 64 x 64 matrix, row u
+        // = target u's row for that cell (zero if it has none); groups with the
+        // same row pattern share one dense matrix M_q (materialised once), so
+        // out[group + u] += sum_q M_q[u] . f[cell(g, q)] runs as DMMA GEMMs
+        // (corr_lattice_kernel).  Every other block -- private triangle rows,
+        // blocks of targets outside a group -- goes through the CSR kernel.
         {
-            std::map<int64_t, int> mat_of;  // pool_off of the block -> matrix index
-            std::vector<int64_t> moff;
-            std::vector<int32_t> groups, cells_tmp, other;
-            std::vector<std::vector<std::pair<int, int32_t>>> gcells;  // per group: (matrix, cell f offset)
-            for (int64_t g = 0; g * 64 < nt; ++g) {
-                const int64_t t0 = g * 64;
-                bool ok = t0 + 64 <= nt;
-                const int m = ok ? blk_off[t0 + 1] - blk_off[t0] : 0;
+            std::vector<int32_t> uses(size_t(npool), 0);
+            for (int64_t k = 0; k < nblocks; ++k) ++uses[size_t(blk_pool[k])];
+            auto shared = [&](int32_t r) { return pool_off[r + 1] - pool_off[r] == 64 && uses[size_t(r)] >= 8; };
+            std::vector<char> covered(size_t(nblocks), 0);
+            struct VecHash {
+                size_t operator()(const std::vector<int32_t>& v) const {
+                    uint64_t h = 1469598103934665603ull;
+                    for (int32_t x : v) h = (h ^ uint64_t(uint32_t(x))) * 1099511628211ull;
+                    return size_t(h);
+                }
+            };
+            std::unordered_map<std::vector<int32_t>, int, VecHash> mat_of;
+            std::vector<std::vector<int32_t>> mats;   // per matrix: the 64 pool rows (-1 = zero)
+            std::vector<int32_t> uses_q;
+            std::vector<int32_t> gstart;                               // first target of each group
+            std::vector<std::vector<std::pair<int, int32_t>>> gcells;  // per group: (matrix, f offset)
+            std::vector<std::vector<std::vector<int64_t>>> gblocks;    // per group and entry: its blocks
+            int64_t t = 0;
+            while (t + 64 <= nt) {
+                const int64_t k0 = blk_off[t];
+                if (blk_off[t + 1] == k0) { ++t; continue; }
+                const int32_t self_cell = blk_cell[k0];
+                int64_t run = 1;
+                while (t + run < nt && blk_off[t + run + 1] > blk_off[t + run] && blk_cell[blk_off[t + run]] == self_cell)
+                    ++run;
+                for (int64_t g0 = t; g0 + 64 <= t + run; g0 += 64) {
+                    std::map<int32_t, std::vector<int32_t>> rows_of;  // cell -> 64 rows
+                    std::map<int32_t, std::vector<int64_t>> blks_of;
+                    std::set<int32_t> clash;
+                    for (int u = 0; u < 64; ++u)
+                        for (int64_t k = blk_off[g0 + u]; k < blk_off[g0 + u + 1]; ++k) {
+                            const int32_t r = blk_pool[k], cl = blk_cell[k];
+                            if (!shared(r)) continue;
+                            auto& v = rows_of[cl];
+                            if (v.empty()) v.assign(64, -1);
+                            if (v[size_t(u)] >= 0) clash.insert(cl);
+                            v[size_t(u)] = r;
+                            blks_of[cl].push_back(k);
+                        }
+                    std::vector<std::pair<int, int32_t>> mine;
+                    std::vector<std::vector<int64_t>> cov;
+                    std::set<int> used_q;
+                    for (auto& e : rows_of) {
+                        if (clash.count(e.first) || node_off[e.first] + 64 > node_off[ncell]) continue;
+                        auto it = mat_of.find(e.second);
+                        int q;
+                        if (it == mat_of.end()) {
+                            q = int(mats.size());
+                            mat_of.emplace(e.second, q);
+                            mats.push_back(e.second);
+                            uses_q.push_back(0);
+                        } else {
+                            q = it->second;
+                        }
+                        if (used_q.count(q)) continue;  // one cell per matrix and group
+                        used_q.insert(q);
+                        ++uses_q[size_t(q)];
+                        mine.emplace_back(q, node_off[e.first]);
+                        cov.push_back(blks_of[e.first]);
+                    }
+                    if (!mine.empty()) {
+                        gstart.push_back(int32_t(g0));
+                        gcells.push_back(std::move(mine));
+                        gblocks.push_back(std::move(cov));
+                    }
+                }
+                t += run;
+            }
+            // keep the matrices shared by enough groups (at most 128); groups keep
+            // only those, their other blocks fall back to the CSR kernel
+            std::vector<int> order(mats.size());
+            for (size_t q = 0; q < mats.size(); ++q) order[q] = int(q);
+            std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return uses_q[size_t(a)] > uses_q[size_t(b)]; });
+            std::vector<int> remap(mats.size(), -1);
+            std::vector<std::vector<int32_t>> kept;
+            for (int q : order)
+                if (uses_q[size_t(q)] >= 4 && kept.size() < 128) {
+                    remap[size_t(q)] = int(kept.size());
+                    kept.push_back(mats[size_t(q)]);
+                }
+            const int nmat = int(kept.size());
+            std::vector<int32_t> groups, cellof;
+            for (size_t g = 0; g < gstart.size(); ++g) {
                 std::vector<std::pair<int, int32_t>> mine;
-                for (int64_t u = 0; ok && u < 64; ++u) ok = blk_off[t0 + u + 1] - blk_off[t0 + u] == m;
-                for (int r = 0; ok && r < m; ++r) {
-                    const int64_t k0 = blk_off[t0] + r;
-                    const int32_t cell = blk_cell[k0], base = blk_pool[k0];
-                    if (base + 63 >= npool) { ok = false; break; }
-                    const int64_t p0 = pool_off[base];
-                    // the kernel stages M_q with 16-byte loads: an odd p0 would
-                    // be a misaligned access -- such groups take the CSR path
-                    if (p0 & 1) { ok = false; break; }
-                    for (int64_t u = 0; ok && u < 64; ++u) {
-                        const int64_t ku = blk_off[t0 + u] + r;
-                        ok = blk_cell[ku] == cell && blk_pool[ku] == base + u && pool_off[base + u] == p0 + 64 * u &&
-                             pool_off[base + u + 1] == p0 + 64 * (u + 1) && node_off[cell] + 64 <= node_off[ncell];
-                    }
-                    if (!ok) break;
-                    auto it = mat_of.find(p0);
-                    int q;
-                    if (it == mat_of.end()) {
-                        q = int(moff.size());
-                        mat_of[p0] = q;
-                        moff.push_back(p0);
-                    } else {
-                        q = it->second;
-                    }
-                    for (const auto& e : mine) ok = ok && e.first != q;  // one cell per matrix
-                    mine.emplace_back(q, node_off[cell]);
-                }
-                if (ok && m > 0) {
-                    groups.push_back(int32_t(t0 / 64));
-                    gcells.push_back(std::move(mine));
-                } else {
-                    for (int64_t u = t0; u < std::min<int64_t>(t0 + 64, nt); ++u) other.push_back(int32_t(u));
-                }
+                for (auto& e : gcells[g])
+                    if (remap[size_t(e.first)] >= 0) mine.emplace_back(remap[size_t(e.first)], e.second);
+                if (mine.empty()) continue;
+                groups.push_back(gstart[g]);
+                const size_t base = cellof.size();
+                cellof.resize(base + size_t(nmat), -1);
+                for (auto& e : mine) cellof[base + size_t(e.first)] = e.second;
             }
-            // only blocks shared by many groups (the lattice table) pay off as
-            // GEMMs: groups touching a rarely used block go to the CSR kernel
-            std::vector<int> uses(moff.size(), 0);
-            for (const auto& gc : gcells)
-                for (const auto& e : gc) ++uses[size_t(e.first)];
-            std::vector<int> remap(moff.size(), -1);
-            std::vector<int64_t> shared_off;
-            for (size_t q = 0; q < moff.size(); ++q)
-                if (uses[q] >= 32 && shared_off.size() < 64) {
-                    remap[q] = int(shared_off.size());
-                    shared_off.push_back(moff[q]);
-                }
-            {
-                std::vector<int32_t> g2;
-                std::vector<std::vector<std::pair<int, int32_t>>> c2;
-                for (size_t g = 0; g < groups.size(); ++g) {
-                    bool all = true;
-                    for (auto& e : gcells[g]) all = all && remap[size_t(e.first)] >= 0;
-                    if (all) {
-                        for (auto& e : gcells[g]) e.first = remap[size_t(e.first)];
-                        g2.push_back(groups[g]);
-                        c2.push_back(std::move(gcells[g]));
-                    } else {
-                        for (int64_t u = int64_t(groups[g]) * 64; u < int64_t(groups[g]) * 64 + 64; ++u)
-                            other.push_back(int32_t(u));
-                    }
-                }
-                groups.swap(g2);
-                gcells.swap(c2);
-                moff.swap(shared_off);
-                std::sort(other.begin(), other.end());
-            }
-            const int nmat = int(moff.size());
-            if (groups.size() < 16) {  // not worth it: everything through the CSR kernel
+            // covered blocks: those of the kept (group, matrix) entries (each
+            // matrix is exactly the rows of its entry's blocks)
+            for (size_t g = 0; g < gstart.size(); ++g)
+                for (size_t e = 0; e < gcells[g].size(); ++e)
+                    if (remap[size_t(gcells[g][e].first)] >= 0)
+                        for (int64_t k : gblocks[g][e]) covered[size_t(k)] = 1;
+            if (groups.size() < 4) {  // not worth it
                 groups.clear();
-                other.resize(size_t(nt));
-                for (int64_t u = 0; u < nt; ++u) other[size_t(u)] = int32_t(u);
+                cellof.clear();
+                std::fill(covered.begin(), covered.end(), 0);
             }
-            std::vector<int32_t> cellof(groups.size() * size_t(std::max(nmat, 1)), -1);
-            for (size_t g = 0; g < groups.size(); ++g)
-                for (const auto& e : gcells[g]) cellof[g * size_t(nmat) + size_t(e.first)] = e.second;
+            // residual CSR: the targets' uncovered blocks
+            std::vector<int32_t> res_off(size_t(nt) + 1, 0), other;
+            std::vector<BlkDesc> rdesc;
+            for (int64_t tt = 0; tt < nt; ++tt) {
+                for (int64_t k = blk_off[tt]; k < blk_off[tt + 1]; ++k)
+                    if (!covered[size_t(k)]) {
+                        const int32_t pr = blk_pool[k];
+                        rdesc.push_back(BlkDesc{pool_off[pr], node_off[blk_cell[k]], int32_t(pool_off[pr + 1] - pool_off[pr])});
+                    }
+                res_off[size_t(tt) + 1] = int32_t(rdesc.size());
+                if (res_off[size_t(tt) + 1] > res_off[size_t(tt)]) other.push_back(int32_t(tt));
+            }
+            upload(c->res_off, res_off.data(), res_off.size());
+            upload(c->blk_desc, rdesc.data(), rdesc.size());
             c->nlat = int64_t(groups.size());
             c->nmat = groups.empty() ? 0 : nmat;
             c->nother = int64_t(other.size());
+            int sms = 148;
+            VPG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+            c->lat_tile = c->nlat >= int64_t(64) * 2 * sms ? 64 : c->nlat >= int64_t(16) * 2 * sms ? 16 : 8;
+            // per CTA tile: the matrices any of its groups uses
+            std::vector<int32_t> toff(1, 0), tmats;
+            for (int64_t g0 = 0; g0 < c->nlat; g0 += c->lat_tile) {
+                for (int q = 0; q < c->nmat; ++q) {
+                    bool any = false;
+                    for (int64_t g = g0; g < std::min<int64_t>(g0 + c->lat_tile, c->nlat) && !any; ++g)
+                        any = cellof[size_t(g) * size_t(nmat) + size_t(q)] >= 0;
+                    if (any) tmats.push_back(q);
+                }
+                toff.push_back(int32_t(tmats.size()));
+            }
             upload(c->lat_group, groups.data(), groups.size());
-            upload(c->lat_cell, cellof.data(), groups.empty() ? 0 : cellof.size());
-            upload(c->lat_moff, moff.data(), groups.empty() ? 0 : moff.size());
+            upload(c->lat_cell, cellof.data(), cellof.size());
+            upload(c->lat_toff, toff.data(), toff.size());
+            upload(c->lat_tmats, tmats.data(), tmats.size());
             upload(c->other_t, other.data(), other.size());
+            // the dense matrices, gathered from the pool on the device
             if (c->nlat) {
+                std::vector<int64_t> rowsrc(size_t(nmat) * 64);
+                for (int q = 0; q < nmat; ++q)
+                    for (int u = 0; u < 64; ++u) {
+                        const int32_t r = kept[size_t(q)][size_t(u)];
+                        rowsrc[size_t(q) * 64 + size_t(u)] = r >= 0 ? pool_off[r] : -1;
+                    }
+                DBuf<int64_t> rs;
+                upload(rs, rowsrc.data(), rowsrc.size());
+                c->lat_mats.alloc(size_t(nmat) * 4096);
+                gather_rows_kernel<<<unsigned(nmat * 64), 64>>>(rs.p, c->pool_vals.p, c->lat_mats.p);
+                VPG_LAUNCH_CHECK();
+                VPG_CUDA(cudaDeviceSynchronize());
                 smem_optin((const void*)corr_lattice_kernel<64>, int(sizeof(double) * 64 * (68 + 68)));
                 smem_optin((const void*)corr_lattice_kernel<16>, int(sizeof(double) * 64 * (68 + 20)));
                 smem_optin((const void*)corr_lattice_kernel<8>, int(sizeof(double) * 64 * (68 + 12)));
@@ -371,27 +638,26 @@ int vpg_corr_apply(const vpg_corr* c, const double* f, int64_t nf, double* out,
                 VPG_CUDA(cudaMemcpyAsync(od, out, sizeof(double) * size_t(c->nt), cudaMemcpyHostToDevice, os.s));
         }
         if (c->nlat > 0) {
-            int sms = 148;
-            VPG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
-            if (c->nlat >= int64_t(64) * 2 * sms) {
+            const double* fin = dev ? f : fd;
+            double* o = dev ? out : od;
+            if (c->lat_tile == 64)
                 corr_lattice_kernel<64><<<nblk(c->nlat, 64), 256, sizeof(double) * 64 * (68 + 68), os.s>>>(
-                    c->nlat, int(c->nmat), c->lat_group.p, c->lat_cell.p, c->lat_moff.p, c->pool_vals.p,
-                    dev ? f : fd, dev ? out : od);
-            } else if (c->nlat >= int64_t(16) * 2 * sms) {
+                    c->nlat, int(c->nmat), c->lat_group.p, c->lat_cell.p, c->lat_toff.p, c->lat_tmats.p,
+                    c->lat_mats.p, fin, o);
+            else if (c->lat_tile == 16)
                 corr_lattice_kernel<16><<<nblk(c->nlat, 16), 256, sizeof(double) * 64 * (68 + 20), os.s>>>(
-                    c->nlat, int(c->nmat), c->lat_group.p, c->lat_cell.p, c->lat_moff.p, c->pool_vals.p,
-                    dev ? f : fd, dev ? out : od);
-            } else {
+                    c->nlat, int(c->nmat), c->lat_group.p, c->lat_cell.p, c->lat_toff.p, c->lat_tmats.p,
+                    c->lat_mats.p, fin, o);
+            else
                 corr_lattice_kernel<8><<<nblk(c->nlat, 8), 256, sizeof(double) * 64 * (68 + 12), os.s>>>(
-                    c->nlat, int(c->nmat), c->lat_group.p, c->lat_cell.p, c->lat_moff.p, c->pool_vals.p,
-                    dev ? f : fd, dev ? out : od);
-            }
+                    c->nlat, int(c->nmat), c->lat_group.p, c->lat_cell.p, c->lat_toff.p, c->lat_tmats.p,
+                    c->lat_mats.p, fin, o);
             VPG_LAUNCH_CHECK();
         }
         if (c->nother) {
-            corr_apply_kernel<<<nblk(c->nother, kCorrWarps), kCorrWarps * 32, 0, os.s>>>(
-                c->nother, c->other_t.p, c->blk_off.p, c->blk_cell.p, c->blk_pool.p, c->pool_off.p,
-                c->pool_vals.p, c->node_off.p, dev ? f : fd, dev ? out : od);
+            corr_desc16_kernel<<<nblk(c->nother, 2 * kCorrWarps), kCorrWarps * 32, 0, os.s>>>(
+                c->nother, c->other_t.p, c->res_off.p, c->blk_desc.p, c->pool_vals.p, dev ? f : fd,
+                dev ? out : od);
             VPG_LAUNCH_CHECK();
         }
         if (!dev) {
@@ -444,6 +710,17 @@ int vpg_charges_create(int64_t ncell, const int32_t* cell_type, const int32_t* n
         upload(h->over0, over0, size_t(np0) * nq0);
         upload(h->over1, over1, size_t(np1) * nq1);
         upload(h->src_wj, src_wj, size_t(h->nsrc));
+        for (int kind = 0; kind < 2; ++kind) {
+            std::vector<int32_t> cl;
+            for (int64_t c = 0; c < ncell; ++c)
+                if ((cell_type[c] == 0) == (kind == 0)) cl.push_back(int32_t(c));
+            h->ncells_kind[kind] = int64_t(cl.size());
+            upload(h->cells_kind[kind], cl.data(), cl.size());
+        }
+        if (charges_mma_smem(np0, nq0) > 227 * 1024 || charges_mma_smem(np1, nq1) > 227 * 1024 || nq0 > 256 ||
+            nq1 > 256)
+            h->ncells_kind[0] = h->ncells_kind[1] = 0, h->fallback = true;
+        VPG_CUDA(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, device));
         *ch = h.release();
     });
 }
@@ -465,11 +742,50 @@ int vpg_charges_apply(const vpg_charges* h, const double* f, int64_t nf, double*
             VPG_CUDA(cudaMallocAsync(&cd, sizeof(double) * size_t(std::max<int64_t>(h->nsrc, 1)), os.s));
             if (nf) VPG_CUDA(cudaMemcpyAsync(fd, f, sizeof(double) * size_t(nf), cudaMemcpyHostToDevice, os.s));
         }
-        if (h->ncell) {
+        if (h->fallback && h->ncell) {
             const int npmax = std::max(h->np[0], h->np[1]);
             charges_kernel<<<unsigned(h->ncell), 128, sizeof(double) * size_t(std::max(npmax, 1)), os.s>>>(
                 h->cell_type.p, h->node_off.p, h->src_off.p, h->over0.p, h->np[0], h->nq[0], h->over1.p,
                 h->np[1], h->nq[1], h->src_wj.p, dev ? f : fd, dev ? charges : cd);
+            VPG_LAUNCH_CHECK();
+        }
+        if (h->ncells_kind[0] + h->ncells_kind[1] > 0) {
+            ChKind kk[2];
+            double w[2];
+            int mtmax = 1;
+            for (int kind = 0; kind < 2; ++kind) {
+                kk[kind] = ChKind{h->ncells_kind[kind], h->cells_kind[kind].p, kind ? h->over1.p : h->over0.p,
+                                  h->np[kind], h->nq[kind], 4, 0};
+                w[kind] = double(h->ncells_kind[kind]) * h->np[kind] * h->nq[kind];
+                mtmax = std::max(mtmax, ((h->nq[kind] + 7) / 8 + 7) / 8);
+            }
+            // CTAs split by tile count (a tile's cost is dominated by staging and
+            // the k-loop length, not by its exact flops)
+            const int sms = h->sm_count;
+            for (int kind = 0; kind < 2; ++kind) w[kind] = double((h->ncells_kind[kind] + kChTile - 1) / kChTile);
+            int g0 = w[0] > 0 ? std::max(1, int(std::lround(sms * w[0] / (w[0] + w[1])))) : 0;
+            if (w[1] > 0) g0 = std::min(g0, sms - 1);
+            const int gr[2] = {g0, w[1] > 0 ? sms - g0 : 0};
+            for (int kind = 0; kind < 2; ++kind) {
+                int ntl = 4;
+                while (ntl > 1 && (kk[kind].ncell + 8 * ntl - 1) / (8 * ntl) < gr[kind]) ntl /= 2;
+                kk[kind].ntl = ntl;
+                kk[kind].grid = int(std::min<int64_t>(gr[kind], (kk[kind].ncell + 8 * ntl - 1) / (8 * ntl)));
+            }
+            const size_t smem = std::max(kk[0].ncell ? charges_mma_smem(kk[0].np, kk[0].nq) : 0,
+                                         kk[1].ncell ? charges_mma_smem(kk[1].np, kk[1].nq) : 0);
+            const unsigned grid = unsigned(kk[0].grid + kk[1].grid);
+            const double* fin = dev ? f : fd;
+            double* cout = dev ? charges : cd;
+            if (mtmax <= 2) {
+                smem_optin((const void*)charges_mma_kernel<2>, int(smem));
+                charges_mma_kernel<2><<<grid, 256, smem, os.s>>>(kk[0], kk[1], h->node_off.p, h->src_off.p,
+                                                               h->src_wj.p, fin, cout);
+            } else {
+                smem_optin((const void*)charges_mma_kernel<4>, int(smem));
+                charges_mma_kernel<4><<<grid, 256, smem, os.s>>>(kk[0], kk[1], h->node_off.p, h->src_off.p,
+                                                               h->src_wj.p, fin, cout);
+            }
             VPG_LAUNCH_CHECK();
         }
         if (!dev) {

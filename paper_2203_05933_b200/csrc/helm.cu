@@ -1056,15 +1056,124 @@ void build_helm_fmm(Plan& pl) {
     pl.hf_k = k;
     pl.hf_lmin = lmin;
     pl.P = n;  // reported expansion order: Chebyshev nodes per dimension
-    {
-        cublasHandle_t h = nullptr;
-        VPG_SOLVER(cublasCreate(&h));
-        pl.hf_blas = std::shared_ptr<void>(h, [](void* p) { cublasDestroy(static_cast<cublasHandle_t>(p)); });
-    }
     smem_optin((const void*)hf_m2l_tc_kernel, int(sizeof(double) * kHfMaxK * (kHfMaxK + kHfTile + 8)));
     smem_optin((const void*)hf_l2p_p2p_kernel,
                int(size_t(kLogTableBytes) + sizeof(double) * kHfWarps * kHfMaxN * kHfMaxN));
     pl.hf = true;
+}
+
+// The per-level compress (Wt = Vt W) and expand (Lv = Vc Lt) GEMMs on the FP64
+// tensor cores: C (M x N) = A (M x K) . B (K x N), column-major, M and K at most
+// a few hundred (k, n^2), N the level's box count.  A CTA takes NT columns at a
+// time: A staged whole in smem once per CTA (leading dimension == 4 mod 16
+// doubles so the m8n8k4 fragment loads are conflict-free), the NT B columns
+// staged per tile with the next tile's columns prefetched into registers
+// while the current tile's DMMAs run; warp w owns 8-row tiles w, w + 8, ...
+// and all NT / 8 column tiles; the accumulators go straight to C (8 rows of a
+// column are 64 contiguous bytes per lane group).  Persistent CTAs.
+__host__ __device__ inline int ld4mod16(int n) { return n + ((4 - n % 16) + 16) % 16; }
+template <int NT>
+size_t hf_gemm_smem(int M, int K) {
+    const int Mp = (M + 7) & ~7, Kp = (K + 3) & ~3;
+    return sizeof(double) * (size_t(Kp) * ld4mod16(Mp) + size_t(NT) * ld4mod16(Kp));
+}
+constexpr int kGemmPre = 24;  // B elements per thread in flight (NT * Kp <= 256 * kGemmPre)
+template <int NT>
+__global__ void __launch_bounds__(256)
+hf_gemm_kernel(int M, int N, int K, const double* A, int lda, const double* B, int ldb, double* C, int ldc) {
+    extern __shared__ __align__(16) double gs[];
+    const int Mp = (M + 7) & ~7, Kp = (K + 3) & ~3;
+    const int la = ld4mod16(Mp), lb = ld4mod16(Kp);
+    double* As = gs;                    // [k][m], column-major, ld la
+    double* Bs = gs + size_t(Kp) * la;  // [n][k], ld lb
+    // A: batches of 8 independent loads per thread
+    for (int e0 = threadIdx.x; e0 < Kp * Mp; e0 += 8 * blockDim.x) {
+        double v[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int e = e0 + r * blockDim.x, kk = e / Mp, m = e % Mp;
+            v[r] = (e < Kp * Mp && kk < K && m < M) ? A[int64_t(kk) * lda + m] : 0.0;
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int e = e0 + r * blockDim.x;
+            if (e < Kp * Mp) As[(e / Mp) * la + e % Mp] = v[r];
+        }
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int kq = lane & 3, rq = lane >> 2;
+    const int mtiles = Mp / 8;
+    constexpr int kNt = NT / 8;
+    double pre[kGemmPre];
+    auto fetch = [&](int64_t n0) {
+#pragma unroll
+        for (int r = 0; r < kGemmPre; ++r) {
+            const int e = threadIdx.x + 256 * r, j = e / Kp, kk = e % Kp;
+            pre[r] = (j < NT && n0 + j < N && kk < K) ? B[(n0 + j) * ldb + kk] : 0.0;
+        }
+    };
+    int64_t n0 = int64_t(blockIdx.x) * NT;
+    if (n0 < N) fetch(n0);
+    for (; n0 < N; n0 += int64_t(gridDim.x) * NT) {
+        const int nc = int(min(int64_t(NT), N - n0));
+        __syncthreads();  // A staged / the previous tile's B reads are done
+#pragma unroll
+        for (int r = 0; r < kGemmPre; ++r) {
+            const int e = threadIdx.x + 256 * r, j = e / Kp, kk = e % Kp;
+            if (j < NT) Bs[j * lb + kk] = pre[r];
+        }
+        __syncthreads();
+        const int64_t nn = n0 + int64_t(gridDim.x) * NT;
+        if (nn < N) fetch(nn);
+        for (int mt = warp; mt < mtiles; mt += 8) {
+            double acc[kNt][2];
+#pragma unroll
+            for (int t = 0; t < kNt; ++t) acc[t][0] = acc[t][1] = 0.0;
+#pragma unroll 4
+            for (int k4 = 0; k4 < Kp; k4 += 4) {
+                const double a = As[(k4 + kq) * la + 8 * mt + rq];
+#pragma unroll
+                for (int nt = 0; nt < kNt; ++nt) {
+                    const double b = Bs[(8 * nt + rq) * lb + k4 + kq];
+                    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                                 : "+d"(acc[nt][0]), "+d"(acc[nt][1])
+                                 : "d"(a), "d"(b));
+                }
+            }
+            const int m = 8 * mt + rq;
+            if (m < M)
+#pragma unroll
+                for (int nt = 0; nt < kNt; ++nt)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int j = 8 * nt + 2 * kq + h;
+                        if (j < nc) C[(n0 + j) * ldc + m] = acc[nt][h];
+                    }
+        }
+    }
+}
+
+void hf_gemm(int M, int N, int K, const double* A, int lda, const double* B, int ldb, double* C, int ldc,
+             int sm_count, cudaStream_t st) {
+    if (N <= 0) return;
+    const int Kp = (K + 3) & ~3;
+    // widest column tile whose B prefetch fits the registers and A + B the smem
+    auto launch = [&](auto nt_tag) {
+        constexpr int NT = decltype(nt_tag)::value;
+        const size_t smem = hf_gemm_smem<NT>(M, K);
+        smem_optin((const void*)hf_gemm_kernel<NT>, int(smem));
+        const int grid = int(std::min<int64_t>((N + NT - 1) / NT, int64_t(sm_count)));
+        hf_gemm_kernel<NT><<<grid, 256, smem, st>>>(M, N, K, A, lda, B, ldb, C, ldc);
+        VPG_LAUNCH_CHECK();
+    };
+    if (32 * Kp <= 256 * kGemmPre && hf_gemm_smem<32>(M, K) <= 227 * 1024)
+        launch(std::integral_constant<int, 32>());
+    else if (16 * Kp <= 256 * kGemmPre && hf_gemm_smem<16>(M, K) <= 227 * 1024)
+        launch(std::integral_constant<int, 16>());
+    else if (8 * Kp <= 256 * kGemmPre && hf_gemm_smem<8>(M, K) <= 227 * 1024)
+        launch(std::integral_constant<int, 8>());
+    else  // n <= 18 for every eps >= 1e-12 keeps this unreachable
+        throw Error{VPG_ERR_INVALID_ARGUMENT, "Chebyshev FMM operator too large for the GEMM tile"};
 }
 
 void helm_fmm_apply(const Plan& pl, const double* q_dev, double* out_dev, cudaStream_t st, cudaEvent_t* ev,
@@ -1110,19 +1219,13 @@ void helm_fmm_apply(const Plan& pl, const double* q_dev, double* out_dev, cudaSt
         VPG_LAUNCH_CHECK();
         ++launches;
     }
-    {
-        // compress: Wt_l (k x rows, column-major) = Vt_l (k x n2) . W_l (n2 x rows), one GEMM per level
-        std::lock_guard<std::mutex> lk(pl.hf_mu);
-        cublasHandle_t h = static_cast<cublasHandle_t>(pl.hf_blas.get());
-        VPG_SOLVER(cublasSetStream(h, st));
-        const double one = 1.0, zero = 0.0;
-        for (int l = pl.hf_lmin; l <= L; ++l) {
-            const int rows_l = 1 << (2 * l);
-            const int64_t b0 = pl.hf_row_base[size_t(l)];
-            VPG_SOLVER(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, k, rows_l, n2, &one, pl.hf_Vt.p + pl.hf_V_off[size_t(l)],
-                                   k, W + b0 * n2, n2, &zero, Wt + b0 * k, k));
-            ++launches;
-        }
+    // compress: Wt_l (k x rows, column-major) = Vt_l (k x n2) . W_l (n2 x rows), one GEMM per level
+    for (int l = pl.hf_lmin; l <= L; ++l) {
+        const int rows_l = 1 << (2 * l);
+        const int64_t b0 = pl.hf_row_base[size_t(l)];
+        hf_gemm(k, rows_l, n2, pl.hf_Vt.p + pl.hf_V_off[size_t(l)], k, W + b0 * n2, n2, Wt + b0 * k, k,
+                pl.sm_count, st);
+        ++launches;
     }
     mark(3);
     if (pl.hf_ntbox > 0) {
@@ -1142,19 +1245,13 @@ void helm_fmm_apply(const Plan& pl, const double* q_dev, double* out_dev, cudaSt
         ++launches;
     }
     mark(4);
-    {
-        // expand: Lv_l (n2 x rows) = Vc_l (n2 x k) . Lt_l (k x rows), one GEMM per level
-        std::lock_guard<std::mutex> lk(pl.hf_mu);
-        cublasHandle_t h = static_cast<cublasHandle_t>(pl.hf_blas.get());
-        VPG_SOLVER(cublasSetStream(h, st));
-        const double one = 1.0, zero = 0.0;
-        for (int l = pl.hf_lmin; l <= L; ++l) {
-            const int rows_l = 1 << (2 * l);
-            const int64_t b0 = pl.hf_row_base[size_t(l)];
-            VPG_SOLVER(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, n2, rows_l, k, &one, pl.hf_Vc.p + pl.hf_V_off[size_t(l)],
-                                   n2, Lt + b0 * k, k, &zero, Lv + b0 * n2, n2));
-            ++launches;
-        }
+    // expand: Lv_l (n2 x rows) = Vc_l (n2 x k) . Lt_l (k x rows), one GEMM per level
+    for (int l = pl.hf_lmin; l <= L; ++l) {
+        const int rows_l = 1 << (2 * l);
+        const int64_t b0 = pl.hf_row_base[size_t(l)];
+        hf_gemm(n2, rows_l, k, pl.hf_Vc.p + pl.hf_V_off[size_t(l)], n2, Lt + b0 * k, k, Lv + b0 * n2, n2,
+                pl.sm_count, st);
+        ++launches;
     }
     // L2L, top-down
     for (int l = pl.hf_lmin + 1; l <= L; ++l) {

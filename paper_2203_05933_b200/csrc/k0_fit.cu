@@ -5,7 +5,10 @@
 // K0(x) = int_0^inf exp(-x cosh t) dt (kernel.cpp:51-163).  This is an
 // independent implementation of the same construction: Gauss-Legendre
 // nodes by Newton iteration, composite panels doubled to convergence.
+#include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <thread>
 #include <vector>
 
 #include "k0.cuh"
@@ -59,20 +62,37 @@ long double scaled_k0(long double x, const GL& g, bool order1 = false) {
     return prev;
 }
 
+// The fits' node values g(x_j) are independent: evaluate them on the host's
+// cores (each value is the same long-double computation, so the tables do not
+// depend on the thread count).
+template <typename F>
+void parallel_nodes(int n, F&& f) {
+    const int nt = std::max(1, std::min(n, int(std::thread::hardware_concurrency())));
+    std::atomic<int> next{0};
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t)
+        th.emplace_back([&] {
+            for (int i = next++; i < n; i = next++) f(i);
+        });
+    for (auto& x : th) x.join();
+}
+
 }  // namespace
 
 void k0_fit_host(double* out) {
     const GL g(20);
     const long double pi = 3.141592653589793238462643383279502884L;
     const int N = kK0Coeffs;
-    for (int iv = 0; iv < kK0Intervals; ++iv) {
+    std::vector<long double> fv(size_t(kK0Intervals) * N);
+    parallel_nodes(kK0Intervals * N, [&](int e) {
+        const int iv = e / N, j = e % N;
         const long double lo = std::ldexp(1.0L, iv + 1), hi = 2 * lo;
-        long double f[kK0Coeffs];
-        for (int j = 0; j < N; ++j) {
-            const long double th = pi * (j + 0.5L) / N;
-            const long double xj = 0.5L * (lo + hi) + 0.5L * (hi - lo) * std::cos(th);
-            f[j] = scaled_k0(xj, g) * std::sqrt(xj);
-        }
+        const long double th = pi * (j + 0.5L) / N;
+        const long double xj = 0.5L * (lo + hi) + 0.5L * (hi - lo) * std::cos(th);
+        fv[size_t(e)] = scaled_k0(xj, g) * std::sqrt(xj);
+    });
+    for (int iv = 0; iv < kK0Intervals; ++iv) {
+        const long double* f = fv.data() + size_t(iv) * N;
         for (int k = 0; k < N; ++k) {
             long double s = 0;
             for (int j = 0; j < N; ++j) s += f[j] * std::cos(k * pi * (j + 0.5L) / N);
@@ -86,14 +106,16 @@ void k1_fit_host(double* out) {
     const GL g(20);
     const long double pi = 3.141592653589793238462643383279502884L;
     const int N = kK0Coeffs;
-    for (int iv = 0; iv < kK0Intervals; ++iv) {
+    std::vector<long double> fv(size_t(kK0Intervals) * N);
+    parallel_nodes(kK0Intervals * N, [&](int e) {
+        const int iv = e / N, j = e % N;
         const long double lo = std::ldexp(1.0L, iv + 1), hi = 2 * lo;
-        long double f[kK0Coeffs];
-        for (int j = 0; j < N; ++j) {
-            const long double th = pi * (j + 0.5L) / N;
-            const long double xj = 0.5L * (lo + hi) + 0.5L * (hi - lo) * std::cos(th);
-            f[j] = scaled_k0(xj, g, true) * std::sqrt(xj);
-        }
+        const long double th = pi * (j + 0.5L) / N;
+        const long double xj = 0.5L * (lo + hi) + 0.5L * (hi - lo) * std::cos(th);
+        fv[size_t(e)] = scaled_k0(xj, g, true) * std::sqrt(xj);
+    });
+    for (int iv = 0; iv < kK0Intervals; ++iv) {
+        const long double* f = fv.data() + size_t(iv) * N;
         for (int k = 0; k < N; ++k) {
             long double s = 0;
             for (int j = 0; j < N; ++j) s += f[j] * std::cos(k * pi * (j + 0.5L) / N);
@@ -110,14 +132,17 @@ void k0_fit_fast_host(double* out) {
     const GL g(20);
     const long double pi = 3.141592653589793238462643383279502884L;
     const int N = kK0FastCoeffs;
+    std::vector<long double> fv(size_t(kK0FastIntervals) * N);
+    parallel_nodes(kK0FastIntervals * N, [&](int e) {
+        const int iv = e / N, j = e % N;
+        const long double lo = 2.0L * std::pow(2.0L, iv / 4.0L), hi = 2.0L * std::pow(2.0L, (iv + 1) / 4.0L);
+        const long double th = pi * (j + 0.5L) / N;
+        const long double xj = 0.5L * (lo + hi) + 0.5L * (hi - lo) * std::cos(th);
+        fv[size_t(e)] = scaled_k0(xj, g) * std::sqrt(xj);
+    });
     for (int iv = 0; iv < kK0FastIntervals; ++iv) {
         const long double lo = 2.0L * std::pow(2.0L, iv / 4.0L), hi = 2.0L * std::pow(2.0L, (iv + 1) / 4.0L);
-        long double f[kK0FastCoeffs];
-        for (int j = 0; j < N; ++j) {
-            const long double th = pi * (j + 0.5L) / N;
-            const long double xj = 0.5L * (lo + hi) + 0.5L * (hi - lo) * std::cos(th);
-            f[j] = scaled_k0(xj, g) * std::sqrt(xj);
-        }
+        const long double* f = fv.data() + size_t(iv) * N;
         double* rec = out + iv * kK0FastStride;
         for (int k = 0; k < N; ++k) {
             long double s = 0;

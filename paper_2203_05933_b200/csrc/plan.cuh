@@ -292,8 +292,6 @@ struct Plan {
                              // (first offset, end offset, partial slot or -1, C block base)
     DBuf<int2> hf_splits;    // split targets: (target row, first partial slot); nparts per split
     int64_t hf_ntiles = 0, hf_nsplit = 0, hf_nparts = 0;
-    std::shared_ptr<void> hf_blas;  // cuBLAS handle (compress / expand GEMMs)
-    mutable std::mutex hf_mu;       // serialises use of the handle across host threads
     int hf_split_parts = 0;
     int64_t hf_rows = 0, hf_ntbox = 0, hf_nent = 0;
 

@@ -409,6 +409,7 @@ struct RowSmem {
     int err;
     int smooth_rule; // rule for the subtraction, -1 none
     int post;        // 0 raw, 1 x C, 2 / -kInvTwoPi
+    long long nodes; // quadrature nodes evaluated (accurate + smooth rules)
     double r0x, r0y, z0x, z0y, zsx, zsy;
 };
 
@@ -479,6 +480,7 @@ __device__ bool node_at(const DevCtx& c, const RowSmem& S, const geom::Cell& cel
 // Walks the flattened node list of the current mode, adding into dst[nb].
 __device__ void accumulate(const DevCtx& c, RowSmem& S, const geom::Cell& cell, int total, int nb,
                            double* tile, double* ctile, double* dst) {
+    if (threadIdx.x == 0) S.nodes += total;
     const int groups = max(1, kThreads / nb);
     const int g = threadIdx.x / nb, n = threadIdx.x % nb;
     const bool active = g < groups && threadIdx.x < groups * nb;
@@ -603,7 +605,8 @@ __device__ bool is_self_target(V2 zeta0, V2 zstar) {
 }
 
 __global__ void __launch_bounds__(kThreads)
-rows_kernel(DevCtx c, const RowTask* tasks, const double* table, double* out, int* err) {
+rows_kernel(DevCtx c, const RowTask* tasks, const double* table, double* out, int* err,
+            unsigned long long* nodes_done) {
     extern __shared__ __align__(16) double dyn[];
     __shared__ RowSmem S;
     const RowTask T = tasks[blockIdx.x];
@@ -619,6 +622,7 @@ rows_kernel(DevCtx c, const RowTask* tasks, const double* table, double* out, in
     geom::Cell cell = c.cells[T.cell];
     if (threadIdx.x == 0) {
         S.err = 0;
+        S.nodes = 0;
         S.cell = T.cell;
         S.box = cell.type == geom::kBox;
         S.smooth_rule = -1;
@@ -782,6 +786,7 @@ rows_kernel(DevCtx c, const RowTask* tasks, const double* table, double* out, in
         for (int n = threadIdx.x; n < nb; n += blockDim.x) o[n] = S.acc[n];
     }
     if (threadIdx.x == 0 && S.err) atomicOr(err, S.err);
+    if (threadIdx.x == 0) atomicAdd(nodes_done + (S.box ? 1 : 0), (unsigned long long)S.nodes);
 }
 
 // Laplace lattice table from the log moments (singular.cpp:596-613):
@@ -878,28 +883,38 @@ void upload(DBuf<T>& b, const T* h, size_t n) {
 
 size_t row_smem_bytes(int nb) { return sizeof(double) * (size_t(nb) * (kTile + 1) + std::max(kTile, kThreads)); }
 
+// returns the quadrature nodes evaluated on triangle / box cells (nodes[2])
 void run_tasks(vpg_rows& R, const std::vector<RowTask>& tasks, const double* table, double* out_dev,
-               cudaStream_t s) {
+               cudaStream_t s, int64_t* nodes_out = nullptr) {
     if (tasks.empty()) return;
     DBuf<RowTask> td;
     upload(td, tasks.data(), tasks.size());
     DBuf<int> err;
     err.alloc(1);
+    DBuf<unsigned long long> cnt;
+    cnt.alloc(2);
     VPG_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), s));
+    VPG_CUDA(cudaMemsetAsync(cnt.p, 0, 2 * sizeof(unsigned long long), s));
     const int nbmax = std::max(R.nb_tri, R.nb_box);
     const size_t smem = row_smem_bytes(nbmax);
     smem_optin(reinterpret_cast<const void*>(&rows_kernel), int(smem));
     const DevCtx c = R.ctx();
     for (size_t t0 = 0; t0 < tasks.size(); t0 += 1u << 30) {
         const unsigned n = unsigned(std::min<size_t>(tasks.size() - t0, 1u << 30));
-        rows_kernel<<<n, kThreads, smem, s>>>(c, td.p + t0, table, out_dev, err.p);
+        rows_kernel<<<n, kThreads, smem, s>>>(c, td.p + t0, table, out_dev, err.p, cnt.p);
         VPG_LAUNCH_CHECK();
     }
     int herr = 0;
+    unsigned long long nodes[2] = {0, 0};
     VPG_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    VPG_CUDA(cudaMemcpyAsync(nodes, cnt.p, sizeof(nodes), cudaMemcpyDeviceToHost, s));
     VPG_CUDA(cudaStreamSynchronize(s));
     if (herr & 1) throw Error{VPG_ERR_INVALID_ARGUMENT, "ray node left the reference cell"};
     if (herr & 2) throw Error{VPG_ERR_INVALID_ARGUMENT, "ray node coincides with the target"};
+    if (nodes_out) {
+        nodes_out[0] = int64_t(nodes[0]);
+        nodes_out[1] = int64_t(nodes[1]);
+    }
 }
 
 }  // namespace
@@ -1445,7 +1460,8 @@ extern "C" int vpg_corr_build(vpg_rows* r, int64_t ndofs, const double* nodes_xy
         std::stable_sort(rt.begin(), rt.end(), [](const RowTask& a, const RowTask& b) {
             return (a.job == kJobLattice) < (b.job == kJobLattice);
         });
-        run_tasks(*r, rt, table.p, pool.p, s);
+        int64_t nodes[2] = {0, 0};
+        run_tasks(*r, rt, table.p, pool.p, s, nodes);
         const auto t_rows = std::chrono::steady_clock::now();
         vpg::corr_create_impl(nt, blk_off.data(), int64_t(tasks.size()), blk_cell.data(), blk_pool.data(), npool,
                               pool_off.data(), pool.p, true, ncell, node_off, r->device, out);
@@ -1458,6 +1474,8 @@ extern "C" int vpg_corr_build(vpg_rows* r, int64_t ndofs, const double* nodes_xy
             stats[4] = double(npool);          // pool rows
             stats[5] = double(pool_off.back());
             for (int j = 3; j <= 7; ++j) stats[3 + j] = double(njob[j]);  // stats[6..10]: job counts 3..7
+            stats[11] = double(nodes[0]);       // quadrature nodes evaluated on triangle cells
+            stats[12] = double(nodes[1]);       // ... on box cells
         }
     });
 }

@@ -143,7 +143,7 @@ def build_correction_map(engine: RowEngine, nodes, node_off, targets, D: float =
     no = _i32(node_off)
     tg = _f64(targets).reshape(-1, 2)
     h = C.c_void_p()
-    st = np.zeros(11)
+    st = np.zeros(13)
     L.check(L.lib().vpg_corr_build(engine._h, len(nd), _p(nd), _p(no), len(tg), _p(tg), D, C.byref(h), _p(st)),
             "build_corrections")
     cm = CorrectionMap.__new__(CorrectionMap)
@@ -155,7 +155,7 @@ def build_correction_map(engine: RowEngine, nodes, node_off, targets, D: float =
     L.check(L.lib().vpg_corr_export(h, None, None, None, None, None, _p(sz)), "export")
     cm.nblocks = int(sz[1])
     keys = ("classify_ms", "tasks_ms", "rows_ms", "blocks", "pool_rows", "pool_len", "tri_self_node",
-            "tri_near_snap", "self_generic", "near_generic", "box_lattice")
+            "tri_near_snap", "self_generic", "near_generic", "box_lattice", "quad_nodes_tri", "quad_nodes_box")
     return cm, dict(zip(keys, st.tolist()))
 
 
@@ -169,3 +169,52 @@ def export_map(cm):
     L.check(L.lib().vpg_corr_export(cm._h, *(_p(d[k]) for k in ("blk_off", "blk_cell", "blk_pool", "pool_off",
                                                                    "pool_vals")), None), "export")
     return d
+
+
+# ------------------------------------------------------- operator from a mesh --
+def load_mesh(path):
+    """A hybrid mesh stored as the reference builds it (tests/golden/
+    make_golden_mesh.py): returns (Mesh, h)."""
+    d = np.load(path)
+    mesh = Mesh(d["type"], d["curve"], d["v"], d["tt"], d["ch"], np.array([CURVE_STAR]), d["star"][None, :])
+    return mesh, float(d["h"])
+
+
+def load_basis(path):
+    return dict(np.load(path))
+
+
+def build_operator(mesh: Mesh, basis: dict, family: int, lam: float, p: int, q: int, eps: float = 1e-12,
+                   targets=None, D: float = 0.4, device: int = 0):
+    """VolumePotentialOperator (potential.cpp:360-395) assembled on the GPU:
+    mesh_nodes and build_sources from the cells, the SummationPlan over the
+    oversampled sources, the charge map with the basis' oversampling
+    matrices, and the correction map built on the device (build_corrections).
+    Returns a dict with the operator and its parts."""
+    import time
+
+    from .correction import ChargeMap, VolumePotentialOperator
+    from .summation import KernelFamily, SummationPlan, make_kernel
+    t0 = time.perf_counter()
+    eng = RowEngine(mesh, family, lam, p, q, basis["tri_nodes"], basis["tri_C"], basis["box_C"], basis["tri_src"],
+                    basis["tri_src_w"], device=device)
+    nodes = eng.mesh_nodes()
+    src_xy, src_wj = eng.sources()
+    box = np.asarray(mesh.cell_type) == CELL_BOX
+    npc = np.where(box, p * p, p * (p + 1) // 2)
+    nqc = np.where(box, basis["box_over"].shape[0], basis["tri_over"].shape[0])
+    node_off = np.concatenate([[0], np.cumsum(npc)]).astype(np.int32)
+    src_off = np.concatenate([[0], np.cumsum(nqc)]).astype(np.int32)
+    tgt = nodes if targets is None else np.asarray(targets, dtype=np.float64).reshape(-1, 2)
+    t1 = time.perf_counter()
+    corr, stats = build_correction_map(eng, nodes, node_off, tgt, D)
+    t2 = time.perf_counter()
+    k = make_kernel(KernelFamily.Laplace) if family == 0 else make_kernel(KernelFamily.ModifiedHelmholtz, lam)
+    plan = SummationPlan(k, src_xy, tgt, eps, device=device)
+    charges = ChargeMap(np.where(box, 0, 1).astype(np.int32), node_off, src_off, basis["box_over"],
+                        basis["tri_over"], src_wj, device=device)
+    op = VolumePotentialOperator(plan, corr, charges)
+    t3 = time.perf_counter()
+    stats.update(setup_ms=(t1 - t0) * 1e3, corr_build_ms=(t2 - t1) * 1e3, plan_ms=(t3 - t2) * 1e3)
+    return dict(op=op, plan=plan, charges=charges, corr=corr, engine=eng, nodes=nodes, targets=tgt,
+                src_xy=src_xy, src_wj=src_wj, node_off=node_off, src_off=src_off, stats=stats)

@@ -12,6 +12,7 @@ weight * f) and targets.  Where a config names tolerances, ``eps`` holds them.
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -479,3 +480,108 @@ def layer_cfg2(kernel=None, seed=2):
     w = cfg2(seed)
     sys = layer_system(kernel)
     return sys, layer_density(sys), w.tgt
+
+
+# ------------------------------------------------------------ mesh operators --
+GOLDEN = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden")
+
+
+def _star_eval(par, t, order):
+    """StarCurve pos / derivatives (geometry.cpp:106-132), vectorised."""
+    cx, cy, r0, amp, arms, ph = par
+    k = arms
+    ct, st = np.cos(t), np.sin(t)
+    ck, sk = np.cos(k * t + ph), np.sin(k * t + ph)
+    rho = r0 * (1 + amp * ck)
+    u = np.stack([ct, st], -1)
+    up = np.stack([-st, ct], -1)
+    if order == 0:
+        return np.array([cx, cy]) + rho[..., None] * u
+    drho = -r0 * amp * k * sk
+    if order == 1:
+        return drho[..., None] * u + rho[..., None] * up
+    d2rho = -r0 * amp * k * k * ck
+    if order == 2:
+        return (d2rho - rho)[..., None] * u + (2 * drho)[..., None] * up
+    d3rho = r0 * amp * k * k * k * sk
+    return (d3rho - 3 * drho)[..., None] * u + (3 * d2rho - rho)[..., None] * up
+
+
+def map_cells(mesh, ref_pts):
+    """Cell::map_deriv (geometry.cpp:198-223) of every cell at the reference
+    points ref_pts[kind] (kind 0 triangle, 1 box): returns (xy, jac) in cell
+    order, ref_pts[kind] points per cell."""
+    typ = np.asarray(mesh["type"])
+    out_x, out_j = [], []
+    star = mesh["star"]
+    for c in range(len(typ)):
+        z = ref_pts[1] if typ[c] == 2 else ref_pts[0]
+        if typ[c] == 2:
+            cx, cy, h = mesh["ch"][c]
+            out_x.append(np.array([cx, cy]) + (h / 2) * z)
+            out_j.append(np.full(len(z), h * h / 4))
+            continue
+        v0, v1, v2 = mesh["v"][c]
+        e1, e2 = v1 - v0, v2 - v0
+        if typ[c] == 0:
+            out_x.append(v0 + z[:, :1] * e1 + z[:, 1:] * e2)
+            out_j.append(np.full(len(z), e1[0] * e2[1] - e1[1] * e2[0]))
+            continue
+        ta, tb = mesh["tt"][c]
+        dt = tb - ta
+        xi = z[:, 0]
+        s = 1 - xi
+        far = s >= 1e-5
+        phi = np.zeros((len(z), 2))
+        dphi = np.zeros((len(z), 2))
+        t = ta + xi * dt
+        lam = _star_eval(star, t, 0)
+        dlam = dt * _star_eval(star, t, 1)
+        num = lam - (1 - xi)[:, None] * v0 - xi[:, None] * v1
+        with np.errstate(divide="ignore", invalid="ignore"):
+            phi_f = (1.0 / s)[:, None] * num
+            dphi_f = (1.0 / s)[:, None] * (dlam - e1 + phi_f)
+        d1 = dt * _star_eval(star, np.array([tb]), 1)[0]
+        d2 = dt * dt * _star_eval(star, np.array([tb]), 2)[0]
+        d3 = dt * dt * dt * _star_eval(star, np.array([tb]), 3)[0]
+        phi_n = -1.0 * (d1 - e1) + (s / 2)[:, None] * d2 - (s * s / 6)[:, None] * d3
+        dphi_n = -0.5 * d2 + (s / 3)[:, None] * d3
+        phi = np.where(far[:, None], phi_f, phi_n)
+        dphi = np.where(far[:, None], dphi_f, dphi_n)
+        blend = (1 - z[:, 0] - z[:, 1])[:, None]
+        dxi = e1 - phi + blend * dphi
+        deta = e2 - phi
+        out_x.append(v0 + z[:, :1] * e1 + z[:, 1:] * e2 + blend * phi)
+        out_j.append(dxi[:, 0] * deta[:, 1] - dxi[:, 1] * deta[:, 0])
+    return np.concatenate(out_x), np.concatenate(out_j)
+
+
+def op_star(h_name="star_h00125", p=8, q=16, family=0, lam=0.0, seed=9):
+    """The volume-potential operator of the configs[1] star on the reference's
+    own hybrid mesh (tests/golden/mesh_<h_name>.npz, built by build_mesh) with
+    the reference's p = 8 / q = 16 rules: targets = the mesh nodes, sources =
+    the oversampled source rule, f = 3 seeded Gaussians (alpha in [20, 80]).
+    The step is the operator apply (build_charges + FMM + correction,
+    potential.cpp:431-470); the correction map is built on the device
+    (csrc/rows.cu).  src/q here are the FMM step's points and charges."""
+    m = dict(np.load(os.path.join(GOLDEN, f"mesh_{h_name}.npz")))
+    b = dict(np.load(os.path.join(GOLDEN, f"basis_p{p}_q{q}.npz")))
+    nodes, _ = map_cells(m, [b["tri_nodes"], b["box_nodes"]])
+    src, jac = map_cells(m, [b["tri_src"], b["box_src"]])
+    box = m["type"] == 2
+    w = np.concatenate([b["box_src_w"] if bx else b["tri_src_w"] for bx in box])
+    wj = w * jac
+    rng = np.random.default_rng(seed)
+    cen = rng.uniform(-0.5, 0.5, size=(3, 2))
+    al = rng.uniform(20, 80, size=3)
+    f = sum(gaussian(nodes, cen[k], al[k]) for k in range(3))
+    fs = sum(gaussian(src, cen[k], al[k]) for k in range(3))
+    name = "op_star" if family == 0 else "op_star_mh"
+    return Workload(name, src, wj * fs, nodes, kernel="laplace" if family == 0 else "helmholtz", lam=lam,
+                    notes={"mesh": m, "basis": b, "f": f, "src_wj": wj, "p": p, "q": q, "h_name": h_name,
+                           "cells": int(len(m["type"])), "n_tri": int(m["n_tri"]), "n_box": int(m["n_box"])})
+
+
+CONFIGS["op_star"] = op_star
+CONFIGS["op_star_mh"] = lambda: op_star(family=1, lam=10.0)
+CONFIGS["op_star_84k"] = lambda: op_star(h_name="star_h005")
