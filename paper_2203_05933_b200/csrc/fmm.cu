@@ -1249,7 +1249,16 @@ sym_finalize_kernel(const SymLeaf* leaves, int64_t nleaves, const double* part, 
             const int64_t t = int64_t(lf.tgt) + k;
             const double* pk = part + lf.pbase + k;
             double sum = 0.0;
-            for (int sl = 0; sl < lf.nslot; ++sl) sum += pk[int64_t(sl) * lf.n];
+            int sl = 0;
+            for (; sl + 4 <= lf.nslot; sl += 4) {  // four loads in flight, added in slot order
+                const double a0 = __ldcg(pk + int64_t(sl) * lf.n), a1 = __ldcg(pk + int64_t(sl + 1) * lf.n);
+                const double a2 = __ldcg(pk + int64_t(sl + 2) * lf.n), a3 = __ldcg(pk + int64_t(sl + 3) * lf.n);
+                sum += a0;
+                sum += a1;
+                sum += a2;
+                sum += a3;
+            }
+            for (; sl < lf.nslot; ++sl) sum += __ldcg(pk + int64_t(sl) * lf.n);
             if (add) {  // hybrid: the one-sided kernel wrote this target (coincidences included)
                 out[tids[t]] += -kInv4Pi * sum;
                 continue;
@@ -1787,7 +1796,7 @@ void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const L
             if (pl.sym_hybrid) one_sided(s, pl.hyb_chunks.p, pl.n_hyb_chunks, pl.hyb_ranges.p);
             if (pl.n_sym_leaves > 0) {
                 const unsigned fgrid = unsigned(std::min<int64_t>(nblk(pl.n_sym_leaves, kFinWarps),
-                                                                  int64_t(pl.sm_count) * 2));
+                                                                  int64_t(pl.sm_count) * 3));
                 launch_pdl(sym_finalize_kernel, dim3(fgrid), dim3(kFinWarps * 32), kFinSmem, s,
                            (const SymLeaf*)pl.sym_leaves.p, pl.n_sym_leaves, (const double*)w.sym_part,
                            (const int2*)pl.near_ranges.p, (const double2*)pl.src_sorted.p,
