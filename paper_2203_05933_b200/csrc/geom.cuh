@@ -81,6 +81,32 @@ VPG_HD V2 curve_eval(const Curve& c, double t, int order) {
     return (d3rho - 3 * drho) * u + (3 * d2rho - rho) * up;
 }
 
+// pos and deriv at one t together (one sincos per angle; blend_terms needs both)
+VPG_HD void curve_pos_deriv(const Curve& c, double t, V2& pos, V2& der) {
+    double st, ct;
+    sincos(t, &st, &ct);
+    if (c.kind == kCircle) {
+        pos = V2{c.cx, c.cy} + c.a * V2{ct, st};
+        der = c.a * V2{-st, ct};
+        return;
+    }
+    if (c.kind == kEllipse) {
+        const double u0 = c.a * ct, v0 = c.b * st, u1 = -c.a * st, v1 = c.b * ct;
+        pos = V2{c.cx, c.cy} + V2{c.cs * u0 - c.sn * v0, c.sn * u0 + c.cs * v0};
+        der = V2{c.cs * u1 - c.sn * v1, c.sn * u1 + c.cs * v1};
+        return;
+    }
+    const double k = c.arms;
+    const double r0 = c.a, amp = c.b;
+    double sk, ck;
+    sincos(k * t + c.phase, &sk, &ck);
+    const double rho = r0 * (1 + amp * ck);
+    const V2 u{ct, st}, up{-st, ct};
+    pos = V2{c.cx, c.cy} + rho * u;
+    const double drho = -r0 * amp * k * sk;
+    der = drho * u + rho * up;
+}
+
 // ------------------------------------------------------------------- cells --
 enum CellType : int32_t { kStraightTri = 0, kCurvedTri = 1, kBox = 2 };
 struct Cell {
@@ -100,8 +126,9 @@ VPG_HD void blend_terms(const Cell& c, const Curve* curves, double xi, V2& phi, 
     const V2 base = c.v[1] - c.v[0];
     if (s >= 1e-5) {
         const double t = c.ta + xi * dt;
-        const V2 lam = curve_eval(cu, t, 0);
-        const V2 dlam = dt * curve_eval(cu, t, 1);
+        V2 lam, der;
+        curve_pos_deriv(cu, t, lam, der);
+        const V2 dlam = dt * der;
         const V2 num = lam - (1 - xi) * c.v[0] - xi * c.v[1];
         phi = (1.0 / s) * num;
         dphi = (1.0 / s) * (dlam - base + phi);

@@ -352,9 +352,43 @@ __device__ void i0_and_t(double x, double& i0, double& tser) {
     tser = hsum - kEulerGamma * i0;
 }
 
+// Division-free recurrence coefficients of the basis (built once per CTA):
+// the Jacobi step P_{k+1}^{(0, b)} = (c1 + c2 x) P_k - c3 P_{k-1} with
+// c = (a2, a3, a4) / a1 of jacobi_next (basis.cpp:36-43), and the Q_m step
+// Q_{m+1} = q1 s Q_m - q2 z2 Q_{m-1}, q1 = (2m+1)/(m+1), q2 = m/(m+1)
+// (basis.cpp:24-34).  The reference divides by a1 and (m+1) per call; the
+// reciprocal form differs by rounding only.
+struct BasisCoef {
+    double jc[kMaxP][kMaxP][3];  // [m][k][c1, c2, c3] for P_{k+1} from P_k (k >= 1)
+    double qc[kMaxP][2];         // [m][q1, q2]
+    double gam[kMaxNb];          // sqrt(2 (2m+1)(n+1)) at n(n+1)/2 + m (basis.cpp:222)
+};
+
+__device__ void basis_coef_init(int p, BasisCoef& B) {
+    for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
+        const int m = e / p, k = e % p;
+        const double beta = 2 * m + 1;
+        if (k >= 1) {
+            const double a1 = 2 * (k + 1) * (k + beta + 1) * (2 * k + beta);
+            const double a2 = (2 * k + beta + 1) * (-beta * beta);
+            const double a3 = (2 * k + beta) * (2 * k + beta + 1) * (2 * k + beta + 2);
+            const double a4 = 2 * (k + beta) * k * (2 * k + beta + 2);
+            B.jc[m][k][0] = a2 / a1;
+            B.jc[m][k][1] = a3 / a1;
+            B.jc[m][k][2] = a4 / a1;
+        }
+        if (k == 0) {
+            B.qc[m][0] = double(2 * m + 1) / (m + 1);
+            B.qc[m][1] = double(m) / (m + 1);
+        }
+    }
+    for (int n = 0; n < p; ++n)
+        for (int m = threadIdx.x; m <= n; m += blockDim.x) B.gam[n * (n + 1) / 2 + m] = sqrt(2 * (2 * m + 1) * (n + 1.0));
+}
+
 // basis values at a reference point into out[0..nb) (chebyshev2d_eval,
 // koornwinder_eval: basis.cpp:24-45, 193-228)
-__device__ void eval_basis(bool box, int p, V2 z, const double* gam, double* out, int stride) {
+__device__ void eval_basis(bool box, int p, V2 z, const BasisCoef& B, double* out, int stride) {
     if (box) {
         double tx[kMaxP], ty[kMaxP];
         geom::cheb1d(p, z.x, tx);
@@ -369,7 +403,7 @@ __device__ void eval_basis(bool box, int p, V2 z, const double* gam, double* out
     const double z2 = (1 - eta) * (1 - eta);
     q[0] = 1;
     if (p > 1) q[1] = s;
-    for (int m = 1; m + 1 < p; ++m) q[m + 1] = ((2 * m + 1) * s * q[m] - m * z2 * q[m - 1]) / (m + 1);
+    for (int m = 1; m + 1 < p; ++m) q[m + 1] = B.qc[m][0] * s * q[m] - B.qc[m][1] * z2 * q[m - 1];
     const double x = 1 - 2 * eta;
     for (int m = 0; m < p; ++m) {
         const double beta = 2 * m + 1;
@@ -377,29 +411,80 @@ __device__ void eval_basis(bool box, int p, V2 z, const double* gam, double* out
         for (int n = m; n < p; ++n) {
             const int k = n - m;
             if (k > 0) {
-                const double pk1 = k == 1 ? ((beta + 2) * x - beta) / 2 : geom::jacobi_next(k - 1, beta, x, pk, pkm1);
+                const double pk1 = k == 1 ? 0.5 * ((beta + 2) * x - beta)
+                                          : (B.jc[m][k - 1][0] + B.jc[m][k - 1][1] * x) * pk - B.jc[m][k - 1][2] * pkm1;
                 pkm1 = pk;
                 pk = pk1;
             }
             const int idx = n * (n + 1) / 2 + m;
-            out[idx * stride] = gam[idx] * pk * q[m];
+            out[idx * stride] = B.gam[idx] * pk * q[m];
         }
     }
 }
 
-struct Ray {
-    double zx, zy;   // boundary node zeta
-    double factor;   // per-ray weight factor
-    int rule;        // inner rule id
-    int start;       // first flattened node
-};
+// p = 8 (the reference operator's default order) fully unrolled: the
+// recurrences stay in registers (the runtime-p loops above index local arrays)
+template <int P>
+__device__ __forceinline__ void eval_basis_p(bool box, V2 z, const BasisCoef& B, double* out, int stride) {
+    if (box) {
+        double tx[P], ty[P];
+        tx[0] = 1;
+        ty[0] = 1;
+        if (P > 1) {
+            tx[1] = z.x;
+            ty[1] = z.y;
+        }
+#pragma unroll
+        for (int k = 2; k < P; ++k) {
+            tx[k] = 2 * z.x * tx[k - 1] - tx[k - 2];
+            ty[k] = 2 * z.y * ty[k - 1] - ty[k - 2];
+        }
+#pragma unroll
+        for (int a = 0; a < P; ++a)
+#pragma unroll
+            for (int b = 0; b < P; ++b) out[(a * P + b) * stride] = tx[a] * ty[b];
+        return;
+    }
+    double q[P];
+    const double xi = z.x, eta = z.y;
+    const double s = 2 * xi - (1 - eta);
+    const double z2 = (1 - eta) * (1 - eta);
+    q[0] = 1;
+    if (P > 1) q[1] = s;
+#pragma unroll
+    for (int m = 1; m + 1 < P; ++m) q[m + 1] = B.qc[m][0] * s * q[m] - B.qc[m][1] * z2 * q[m - 1];
+    const double x = 1 - 2 * eta;
+#pragma unroll
+    for (int m = 0; m < P; ++m) {
+        const double beta = 2 * m + 1;
+        double pkm1 = 0, pk = 1;
+#pragma unroll
+        for (int n = m; n < P; ++n) {
+            const int k = n - m;
+            if (k > 0) {
+                const double pk1 = k == 1 ? 0.5 * ((beta + 2) * x - beta)
+                                          : (B.jc[m][k - 1][0] + B.jc[m][k - 1][1] * x) * pk - B.jc[m][k - 1][2] * pkm1;
+                pkm1 = pk;
+                pk = pk1;
+            }
+            const int idx = n * (n + 1) / 2 + m;
+            out[idx * stride] = B.gam[idx] * pk * q[m];
+        }
+    }
+}
+
 
 struct RowSmem {
     double ep[geom::kMaxEndpoints];
-    double gam[kMaxNb];
+    BasisCoef bc;
+    double inv_t[40];  // 1 / t of the split self rule's inner nodes
     double acc[kMaxNb];
     double sm[kMaxNb];
-    Ray rays[kMaxBnodes];
+    // the rays of the current layout, reconstructed per node from their panel
+    // (A, E, mid, half of the kept panels) instead of stored (smem: 4 CTAs/SM)
+    double pan[geom::kMaxEndpoints][6];
+    int rstart[kMaxBnodes + 1];        // first flattened node of each ray
+    unsigned char rrule[kMaxBnodes];  // inner rule of each ray
     int np;          // panel endpoints
     int nrays;
     int total;       // flattened node count
@@ -413,48 +498,70 @@ struct RowSmem {
     double r0x, r0y, z0x, z0y, zsx, zsy;
 };
 
+// Ray b of the layout: its boundary node and per-ray weight factor (the
+// expressions of boundary_discretization, singular.cpp:184-190).
+__device__ __forceinline__ void ray_at(const RowSmem& S, const double2* gl, V2 star, int b, V2& zeta, double& factor) {
+    const double* pn = S.pan[b >> 4];
+    const int l = b & 15;
+    const V2 A{pn[0], pn[1]}, E{pn[2], pn[3]};
+    const double mid = pn[4], half = pn[5];
+    const double s = mid + half * gl[l].x;
+    zeta = A + s * E;
+    factor = geom::cross(zeta - star, E) * (gl[l].y * half);
+}
+
+// the ray owning flattened node i (binary search over the ray starts)
+__device__ __forceinline__ int ray_of(const RowSmem& S, int i) {
+    int lo = 0, hi = S.nrays - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (S.rstart[mid] <= i) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
 // One node of the current task: reference point, weight, kernel factor.
 __device__ bool node_at(const DevCtx& c, const RowSmem& S, const geom::Cell& cell, int i, V2& chi, double& coef) {
     const double2* xw = c.rule_xw;
     const V2 r0{S.r0x, S.r0y};
     if (S.mode == 0) {  // split self rule: 20 -t log t + 20 t nodes per ray
         const int b = i / 40, l = i % 40;
-        const Ray& ray = S.rays[b];
         const V2 z0{S.z0x, S.z0y};
-        const V2 dir = V2{ray.zx, ray.zy} - z0;
+        V2 zeta;
+        double factor;
+        ray_at(S, xw + c.rule_off[kGL16], z0, b, zeta, factor);
+        const V2 dir = zeta - z0;
         const bool log_part = l < 20;
         const double2 tw = log_part ? xw[c.rule_off[kTLog20] + l] : xw[c.rule_off[kT20] + l - 20];
         chi = z0 + tw.x * dir;
-        const double w = tw.y * ray.factor;
+        const double w = tw.y * factor;
         V2 x, dxi, deta;
         double jac;
         geom::map_deriv(cell, c.curves, chi, x, dxi, deta, jac);
         const double r = geom::dist(x, r0);
         double k;
         if (c.family == VPG_LAPLACE) {
-            k = log_part ? kInvTwoPi : -kInvTwoPi * log(r / tw.x);
+            k = log_part ? kInvTwoPi : -kInvTwoPi * log(r * S.inv_t[l]);
         } else {
             double i0, tser;
             i0_and_t(c.lambda * r, i0, tser);
-            k = log_part ? kInvTwoPi * i0 : kInvTwoPi * (tser - i0 * log(c.lambda * r / (2.0 * tw.x)));
+            k = log_part ? kInvTwoPi * i0 : kInvTwoPi * (tser - i0 * log(c.lambda * r * (0.5 * S.inv_t[l])));
         }
         coef = w * jac * k;
         return true;
     }
     if (S.mode == 1) {  // rays: binary search the ray owning flattened node i
-        int lo = 0, hi = S.nrays - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (S.rays[mid].start <= i) lo = mid;
-            else hi = mid - 1;
-        }
-        const Ray& ray = S.rays[lo];
-        const int l = i - ray.start;
-        const double2 tw = xw[c.rule_off[ray.rule] + l];
+        const int b = ray_of(S, i);
+        const int l = i - S.rstart[b];
+        const double2 tw = xw[c.rule_off[S.rrule[b]] + l];
         const V2 zs{S.zsx, S.zsy};
-        const V2 dir = V2{ray.zx, ray.zy} - zs;
+        V2 zeta;
+        double factor;
+        ray_at(S, xw + c.rule_off[kGL16], zs, b, zeta, factor);
+        const V2 dir = zeta - zs;
         chi = V2{zs.x + tw.x * dir.x, zs.y + tw.x * dir.y};
-        const double w = tw.x * tw.y * ray.factor;
+        const double w = tw.x * tw.y * factor;
         V2 x, dxi, deta;
         double jac;
         geom::map_deriv(cell, c.curves, chi, x, dxi, deta, jac);
@@ -495,7 +602,12 @@ __device__ void accumulate(const DevCtx& c, RowSmem& S, const geom::Cell& cell, 
             if (i < total) {
                 V2 chi;
                 if (node_at(c, S, cell, i, chi, coef))
-                    eval_basis(S.box, c.p, chi, S.gam, tile + threadIdx.x, stride);
+                {
+                    if (c.p == 8)
+                        eval_basis_p<8>(S.box, chi, S.bc, tile + threadIdx.x, stride);
+                    else
+                        eval_basis(S.box, c.p, chi, S.bc, tile + threadIdx.x, stride);
+                }
                 else
                     for (int k = 0; k < nb; ++k) tile[k * stride + threadIdx.x] = 0.0;
             }
@@ -562,40 +674,44 @@ __device__ void layout_rays(const DevCtx& c, RowSmem& S, const geom::Cell& cell,
     }
     __syncthreads();
     const double2* gl = c.rule_xw + c.rule_off[kGL16];
+    for (int m = threadIdx.x; m < nkept; m += blockDim.x) {
+        V2 A, E;
+        double sa, sb;
+        geom::boundary_panel(S.box, star, S.ep, S.np, kept[m], A, E, sa, sb);
+        double* pn = S.pan[m];
+        pn[0] = A.x;
+        pn[1] = A.y;
+        pn[2] = E.x;
+        pn[3] = E.y;
+        pn[4] = 0.5 * (sa + sb);
+        pn[5] = 0.5 * (sb - sa);
+    }
+    __syncthreads();
     V2 rstar{0, 0};
     if (mode == 1 && !all_singular) rstar = geom::cell_map(cell, c.curves, star);
     for (int b = threadIdx.x; b < S.nrays; b += blockDim.x) {
-        const int k = kept[b >> 4], l = b & 15;
-        V2 A, E;
-        double sa, sb;
-        geom::boundary_panel(S.box, star, S.ep, S.np, k, A, E, sa, sb);
-        const double half = 0.5 * (sb - sa), mid = 0.5 * (sa + sb);
-        const double s = mid + half * gl[l].x;
-        const V2 zeta = A + s * E;
-        Ray r;
-        r.zx = zeta.x;
-        r.zy = zeta.y;
-        r.factor = geom::cross(zeta - star, E) * (gl[l].y * half);
-        if (mode == 0) {
-            r.rule = -1;
-        } else if (all_singular) {
-            r.rule = kRaySing;
-        } else {
-            const double len = geom::dist(geom::cell_map(cell, c.curves, zeta), rstar);
-            const double deff = fmin(fmax(d / fmax(len, 1e-300), 1e-9), 16.0);
-            const int q = int(floor(-log10(deff)));
-            r.rule = kNear0 + min(max(q, kNearQ0), kNearQ1) - kNearQ0;
+        int rule = 0;
+        if (mode == 1) {
+            if (all_singular) {
+                rule = kRaySing;
+            } else {
+                V2 zeta;
+                double factor;
+                ray_at(S, gl, star, b, zeta, factor);
+                const double len = geom::dist(geom::cell_map(cell, c.curves, zeta), rstar);
+                const double deff = fmin(fmax(d / fmax(len, 1e-300), 1e-9), 16.0);
+                const int q = int(floor(-log10(deff)));
+                rule = kNear0 + min(max(q, kNearQ0), kNearQ1) - kNearQ0;
+            }
         }
-        S.rays[b] = r;
+        S.rrule[b] = (unsigned char)rule;
+        S.rstart[b + 1] = mode == 0 ? 40 : c.rule_off[rule + 1] - c.rule_off[rule];
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        int at = 0;
-        for (int b = 0; b < S.nrays; ++b) {
-            S.rays[b].start = at;
-            at += mode == 0 ? 40 : c.rule_off[S.rays[b].rule + 1] - c.rule_off[S.rays[b].rule];
-        }
-        S.total = at;
+    if (threadIdx.x == 0) {  // ray sizes -> starts
+        S.rstart[0] = 0;
+        for (int b = 0; b < S.nrays; ++b) S.rstart[b + 1] += S.rstart[b];
+        S.total = S.rstart[S.nrays];
     }
     __syncthreads();
 }
@@ -616,8 +732,9 @@ rows_kernel(DevCtx c, const RowTask* tasks, const double* table, double* out, in
         S.sm[i] = 0.0;
     }
     // Koornwinder normalisations sqrt(2 (2m+1)(n+1)) (basis.cpp:222)
-    for (int n = 0; n < p; ++n)
-        for (int m = threadIdx.x; m <= n; m += blockDim.x) S.gam[n * (n + 1) / 2 + m] = sqrt(2 * (2 * m + 1) * (n + 1.0));
+    basis_coef_init(p, S.bc);
+    for (int l = threadIdx.x; l < 40; l += blockDim.x)
+        S.inv_t[l] = 1.0 / c.rule_xw[l < 20 ? c.rule_off[kTLog20] + l : c.rule_off[kT20] + l - 20].x;
     // the task's cell: a mesh cell, or the reference box / the origin box for the tables
     geom::Cell cell = c.cells[T.cell];
     if (threadIdx.x == 0) {
@@ -734,14 +851,12 @@ rows_kernel(DevCtx c, const RowTask* tasks, const double* table, double* out, in
         layout_rays(c, S, cell, zs, 1, all_singular, d);
         // node checks of assemble_rays: inside the closed cell, never on the target
         for (int i = threadIdx.x; i < S.total; i += blockDim.x) {
-            int lo = 0, hi = S.nrays - 1;
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (S.rays[mid].start <= i) lo = mid;
-                else hi = mid - 1;
-            }
-            const double t = c.rule_xw[c.rule_off[S.rays[lo].rule] + i - S.rays[lo].start].x;
-            const V2 chi{zs.x + t * (S.rays[lo].zx - zs.x), zs.y + t * (S.rays[lo].zy - zs.y)};
+            const int b = ray_of(S, i);
+            const double t = c.rule_xw[c.rule_off[S.rrule[b]] + i - S.rstart[b]].x;
+            V2 zeta;
+            double factor;
+            ray_at(S, c.rule_xw + c.rule_off[kGL16], zs, b, zeta, factor);
+            const V2 chi{zs.x + t * (zeta.x - zs.x), zs.y + t * (zeta.y - zs.y)};
             const double pad = 1e-12;
             const bool inside = S.box ? fabs(chi.x) <= 1 + pad && fabs(chi.y) <= 1 + pad
                                       : chi.x >= -pad && chi.y >= -pad && chi.x + chi.y <= 1 + pad;
@@ -887,22 +1002,28 @@ size_t row_smem_bytes(int nb) { return sizeof(double) * (size_t(nb) * (kTile + 1
 void run_tasks(vpg_rows& R, const std::vector<RowTask>& tasks, const double* table, double* out_dev,
                cudaStream_t s, int64_t* nodes_out = nullptr) {
     if (tasks.empty()) return;
-    DBuf<RowTask> td;
-    upload(td, tasks.data(), tasks.size());
     DBuf<int> err;
     err.alloc(1);
     DBuf<unsigned long long> cnt;
     cnt.alloc(2);
     VPG_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), s));
     VPG_CUDA(cudaMemsetAsync(cnt.p, 0, 2 * sizeof(unsigned long long), s));
-    const int nbmax = std::max(R.nb_tri, R.nb_box);
-    const size_t smem = row_smem_bytes(nbmax);
-    smem_optin(reinterpret_cast<const void*>(&rows_kernel), int(smem));
+    // triangle rows (p(p+1)/2 basis) and box rows (p^2) launch separately: the
+    // smem tile is sized by the basis, so triangle rows fit more CTAs per SM
+    std::vector<RowTask> part[2];
+    for (const RowTask& t : tasks) part[R.cells_h[size_t(t.cell)].type == geom::kBox ? 1 : 0].push_back(t);
     const DevCtx c = R.ctx();
-    for (size_t t0 = 0; t0 < tasks.size(); t0 += 1u << 30) {
-        const unsigned n = unsigned(std::min<size_t>(tasks.size() - t0, 1u << 30));
-        rows_kernel<<<n, kThreads, smem, s>>>(c, td.p + t0, table, out_dev, err.p, cnt.p);
-        VPG_LAUNCH_CHECK();
+    DBuf<RowTask> tdk[2];
+    for (int kind = 0; kind < 2; ++kind) {
+        if (part[kind].empty()) continue;
+        upload(tdk[kind], part[kind].data(), part[kind].size());
+        const size_t smem = row_smem_bytes(kind ? R.nb_box : R.nb_tri);
+        smem_optin(reinterpret_cast<const void*>(&rows_kernel), int(row_smem_bytes(std::max(R.nb_tri, R.nb_box))));
+        for (size_t t0 = 0; t0 < part[kind].size(); t0 += 1u << 30) {
+            const unsigned n = unsigned(std::min<size_t>(part[kind].size() - t0, 1u << 30));
+            rows_kernel<<<n, kThreads, smem, s>>>(c, tdk[kind].p + t0, table, out_dev, err.p, cnt.p);
+            VPG_LAUNCH_CHECK();
+        }
     }
     int herr = 0;
     unsigned long long nodes[2] = {0, 0};
