@@ -448,7 +448,7 @@ constexpr int kWSTPW = VPG_M2L_TPW;          // column tiles per MMA warp
 constexpr int kWSMMAWarps = 14 / kWSTPW;     // 14 column tiles
 constexpr int kWSRedThreads = 128;
 constexpr int kWSThreads = 32 * (1 + kWSMMAWarps) + kWSRedThreads;
-constexpr int kWSStages = 5;                 // batch metadata ring (the reduction of batch it - 1 still reads its slot)
+constexpr int kWSStages = 4;                 // batch metadata ring
 #ifndef VPG_M2L_KUNROLL
 #define VPG_M2L_KUNROLL 2
 #endif
@@ -601,10 +601,8 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
                     for (int k4 = 0; k4 < KP; k4 += 4) kstep(k4);
                 }
             }
-            // raw Y to smem: lane holds (re, im) of row l = 8i + rq, entry
-            // p = 4(TPW w + t) + kq; the diagonal epilogue b = d^-l (y - a0/l)
-            // runs in the reduction warps, so the MMA warps go straight on to
-            // the next batch's k-loop
+            // register epilogue: lane holds (re, im) of row l = 8i + rq,
+            // entry p = 4(2w+t) + kq
             if (it >= 2) mbar_wait(&yfree[j], (use - 1u) & 1u);
             double* yb = yb0 + j * n * kM2LXS;
             double2* a0s = a0s0 + j * kM2LPairs;
@@ -612,12 +610,29 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
             for (int t = 0; t < kWSTPW; ++t) {
                 const int p = 4 * (kWSTPW * w + t) + kq;
                 if (p < bt.ecount) {
-                    if (rq == 0) a0s[p] = raw[p * n];
+                    const double2 a0 = raw[p * n];
+                    const int om = sg.omap[p];
+                    const int ci = om & 7, sc = (om >> 3) & 1, m = (om >> 4) & 3;
+                    if (rq == 0) a0s[p] = a0;
 #pragma unroll
                     for (int i = 0; i < MT; ++i) {
                         const int l = 8 * i + rq;
-                        if (l <= P)
-                            *reinterpret_cast<double2*>(yb + l * kM2LXS + 2 * p) = make_double2(acc[i][t][0], acc[i][t][1]);
+                        if (l <= P) {
+                            const double yr = acc[i][t][0], yi = acc[i][t][1];
+                            double br, bim;
+                            if (l == 0) {
+                                const double2 lg = logmd[sg.oidx[p]];
+                                br = yr + (lg.x * a0.x - lg.y * a0.y);
+                                bim = yi + (lg.x * a0.y + lg.y * a0.x);
+                            } else {
+                                const double inv_l = ninv[l];  // -1/l
+                                const double zr = fma(inv_l, a0.x, yr), zi = fma(inv_l, a0.y, yi);
+                                const double2 dl = turn(canon[ci * n + l], (m * l) & 3, sc);
+                                br = dl.x * zr - dl.y * zi;
+                                bim = dl.x * zi + dl.y * zr;
+                            }
+                            *reinterpret_cast<double2*>(yb + l * kM2LXS + 2 * p) = make_double2(br, bim);
+                        }
                     }
                 }
             }
@@ -641,9 +656,7 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
             // per (target t, row l): entries summed in list order, plus the
             // monopole shift (summation.cpp:297-301)
             const double logs = log(side / double(1 << bt.level));
-            const M2LStage& sg = stg[it % kWSStages];
             const int l = rtid & 63;
-            const double inv_l = l > 0 ? ninv[l] : 0.0;  // -1/l
             if (l <= P)
                 for (int t = rtid >> 6; t < bt.tcount; t += kWSRedThreads >> 6) {
                     const int64_t tg = int64_t(bt.tfirst) + t;
@@ -653,26 +666,11 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
                     const int p1 = t + 1 < bt.tcount ? toff[tg + 1] - bt.efirst : bt.ecount;
                     const double* yrow = yb + l * kM2LXS;
                     double sr = 0.0, si = 0.0, qsum = 0.0;
-#pragma unroll 2
+#pragma unroll 4
                     for (int p = p0; p < p1; ++p) {
-                        const double yr = yrow[2 * p], yi = yrow[2 * p + 1];
-                        const double2 a0 = a0s[p];
-                        double br, bim;
-                        if (l == 0) {  // b_0 = y_0 + log(-d) a_0
-                            const double2 lg = logmd[sg.oidx[p]];
-                            br = yr + (lg.x * a0.x - lg.y * a0.y);
-                            bim = yi + (lg.x * a0.y + lg.y * a0.x);
-                            qsum += a0.x;
-                        } else {       // b_l = d^-l (y_l - a_0 / l)
-                            const int om = sg.omap[p];
-                            const int ci = om & 7, sc = (om >> 3) & 1, m = (om >> 4) & 3;
-                            const double zr = fma(inv_l, a0.x, yr), zi = fma(inv_l, a0.y, yi);
-                            const double2 dl = turn(canon[ci * n + l], (m * l) & 3, sc);
-                            br = dl.x * zr - dl.y * zi;
-                            bim = dl.x * zi + dl.y * zr;
-                        }
-                        sr += br;
-                        si += bim;
+                        sr += yrow[2 * p];
+                        si += yrow[2 * p + 1];
+                        if (l == 0) qsum += a0s[p].x;
                     }
                     if (l == 0) sr += qsum * logs;
                     loc[int64_t(tbox[tg]) * n + l] = make_double2(sr, si);
