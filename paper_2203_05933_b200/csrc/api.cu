@@ -243,7 +243,7 @@ static cudaGraph_t capture_apply(const Plan& pl, GraphEntry& e) {
     const double* qd = e.host ? e.qstage : e.q;
     double* od = e.host ? e.ostage : e.out;
     cudaStream_t cap = nullptr, side = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr, far_done = nullptr;
     static const bool prio = [] {  // VPG_PRIO=0: equal priorities (A/B)
         const char* v = std::getenv("VPG_PRIO");
         return !(v && v[0] == '0');
@@ -259,16 +259,18 @@ static cudaGraph_t capture_apply(const Plan& pl, GraphEntry& e) {
     }
     VPG_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
     VPG_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+    VPG_CUDA(cudaEventCreateWithFlags(&far_done, cudaEventDisableTiming));
     struct StreamGuard {
         cudaStream_t s, t;
-        cudaEvent_t f, j;
+        cudaEvent_t f, j, d;
         ~StreamGuard() {
             cudaStreamDestroy(s);
             cudaStreamDestroy(t);
             cudaEventDestroy(f);
             cudaEventDestroy(j);
+            cudaEventDestroy(d);
         }
-    } sg{cap, side, fork, join};
+    } sg{cap, side, fork, join, far_done};
     VPG_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
     cudaGraph_t g = nullptr;
     try {
@@ -280,7 +282,7 @@ static cudaGraph_t capture_apply(const Plan& pl, GraphEntry& e) {
         }();
         int64_t launches = 0;
         laplace_issue(pl, qd, od, laplace_work_at(pl, e.work), cap, nullptr, launches,
-                      no_fork ? nullptr : side, fork, join);
+                      no_fork ? nullptr : side, fork, join, far_done);
         e.launches = launches;
     } catch (...) {
         cudaStreamEndCapture(cap, &g);

@@ -712,7 +712,7 @@ constexpr int kL2PWarps = 8;
 __global__ void __launch_bounds__(kL2PWarps * 32)
 l2p_kernel(const P2PChunk* chunks, int64_t nchunks, const int32_t* lrows, const double2* txy,
            const double2* loc, const int32_t* row_level, const int32_t* row_morton, int P,
-           double x0, double y0, double side, const int32_t* tids, double* out) {
+           double x0, double y0, double side, const int32_t* tids, double* out, int assign) {
     __shared__ double2 rowbuf[kL2PWarps][64];
     pdl_trigger();
     pdl_wait();
@@ -773,8 +773,16 @@ l2p_kernel(const P2PChunk* chunks, int64_t nchunks, const int32_t* lrows, const 
             __syncwarp();
         }
         // the near field is already in out (l2p_p2p_kernel): out += far
-        if (lane < c.tcount) out[tids[c.tbegin + lane]] += -kInv2Pi * s0;
-        if (lane + 32 < c.tcount) out[tids[c.tbegin + lane + 32]] += -kInv2Pi * s1;
+        // assign: the far field goes in first (the symmetric near field adds
+        // on top later); otherwise it adds to the near field already there
+        if (lane < c.tcount) {
+            double& o = out[tids[c.tbegin + lane]];
+            o = assign ? -kInv2Pi * s0 : o + -kInv2Pi * s0;
+        }
+        if (lane + 32 < c.tcount) {
+            double& o = out[tids[c.tbegin + lane + 32]];
+            o = assign ? -kInv2Pi * s1 : o + -kInv2Pi * s1;
+        }
     }
 }
 
@@ -1259,15 +1267,16 @@ sym_finalize_kernel(const SymLeaf* leaves, int64_t nleaves, const double* part, 
                 sum += a3;
             }
             for (; sl < lf.nslot; ++sl) sum += __ldcg(pk + int64_t(sl) * lf.n);
-            if (add) {  // hybrid: the one-sided kernel wrote this target (coincidences included)
+            if (add == 1) {  // hybrid: the one-sided kernel wrote this target (coincidences included)
                 out[tids[t]] += -kInv4Pi * sum;
                 continue;
             }
             const double2 tp = txy[t];
             sum += coin_correction(coin_off, coin_src, t, tp.x, tp.y, sxy, q, tab_lane);
-            out[tids[t]] = -kInv4Pi * sum;
+            double& o = out[tids[t]];
+            o = add == 2 ? o + -kInv4Pi * sum : -kInv4Pi * sum;  // 2: the far field is already there
         }
-        if (add || lf.tgt + lf.n >= lf.t1) continue;
+        if (add == 1 || lf.tgt + lf.n >= lf.t1) continue;
         const NearList nl = near_list(ranges, lf.rfirst, lf.rcount, 0, lane, pre_s, st_s);
         for (int t = lf.tgt + lf.n; t < lf.t1; ++t) {
             const double2 tp = txy[t];
@@ -1287,7 +1296,8 @@ sym_finalize_kernel(const SymLeaf* leaves, int64_t nleaves, const double* part, 
             for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
             if (lane == 0) {
                 v += coin_correction(coin_off, coin_src, t, tp.x, tp.y, sxy, q, tab_lane);
-                out[tids[t]] = -kInv4Pi * v;
+                double& o = out[tids[t]];
+                o = add == 2 ? o + -kInv4Pi * v : -kInv4Pi * v;
             }
         }
     }
@@ -1726,7 +1736,8 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
             if (p) cudaFreeAsync(p, s);
         }
     } fr{base, st};
-    laplace_issue(pl, q_dev, out_dev, laplace_work_at(pl, base), st, ev, launches, nullptr, nullptr, nullptr);
+    laplace_issue(pl, q_dev, out_dev, laplace_work_at(pl, base), st, ev, launches, nullptr, nullptr, nullptr,
+                  nullptr);
 }
 
 // The kernels of one Laplace apply, in stream order, on a given workspace
@@ -1738,7 +1749,7 @@ void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
 // before L2P.  out = near + far either way (one fixed order).
 void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const LaplaceWork& w,
                    cudaStream_t st, cudaEvent_t* ev, int64_t& launches, cudaStream_t side,
-                   cudaEvent_t fork, cudaEvent_t join) {
+                   cudaEvent_t fork, cudaEvent_t join, cudaEvent_t far_done) {
     const int P = pl.P, n = P + 1, L = pl.L;
     auto mark = [&](int i) {
         if (ev) VPG_CUDA(cudaEventRecord(ev[i], st));
@@ -1779,6 +1790,22 @@ void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const L
         ++launches;
     };
 
+    // Symmetric near field on the side stream: the far field's L2P writes out
+    // = far concurrently (main stream) and the finalize adds the near field
+    // after it, so L2P leaves the step's tail (addition order far + near gives
+    // the same bits as near + far)
+    const bool far_first = side && far_done && pl.sym && !pl.sym_hybrid && pl.n_sym_leaves > 0;
+    auto sym_finalize = [&](cudaStream_t s, int mode) {
+        const unsigned fgrid = unsigned(std::min<int64_t>(nblk(pl.n_sym_leaves, kFinWarps),
+                                                          int64_t(pl.sm_count) * 3));
+        launch_pdl(sym_finalize_kernel, dim3(fgrid), dim3(kFinWarps * 32), kFinSmem, s,
+                   (const SymLeaf*)pl.sym_leaves.p, pl.n_sym_leaves, (const double*)w.sym_part,
+                   (const int2*)pl.near_ranges.p, (const double2*)pl.src_sorted.p,
+                   (const double*)qs, (const double2*)pl.tgt_sorted.p, (const int32_t*)pl.tgt_ids.p,
+                   (const int32_t*)pl.coin_off.p, (const int32_t*)pl.coin_src.p, lap_log_table_dev(),
+                   out_dev, mode);
+        ++launches;
+    };
     auto near_field = [&](cudaStream_t s) {
         if (pl.sym) {
             if (pl.n_sym_tasks > 0) {
@@ -1794,17 +1821,7 @@ void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const L
                 ++launches;
             }
             if (pl.sym_hybrid) one_sided(s, pl.hyb_chunks.p, pl.n_hyb_chunks, pl.hyb_ranges.p);
-            if (pl.n_sym_leaves > 0) {
-                const unsigned fgrid = unsigned(std::min<int64_t>(nblk(pl.n_sym_leaves, kFinWarps),
-                                                                  int64_t(pl.sm_count) * 3));
-                launch_pdl(sym_finalize_kernel, dim3(fgrid), dim3(kFinWarps * 32), kFinSmem, s,
-                           (const SymLeaf*)pl.sym_leaves.p, pl.n_sym_leaves, (const double*)w.sym_part,
-                           (const int2*)pl.near_ranges.p, (const double2*)pl.src_sorted.p,
-                           (const double*)qs, (const double2*)pl.tgt_sorted.p, (const int32_t*)pl.tgt_ids.p,
-                           (const int32_t*)pl.coin_off.p, (const int32_t*)pl.coin_src.p, lap_log_table_dev(),
-                           out_dev, pl.sym_hybrid ? 1 : 0);
-                ++launches;
-            }
+            if (pl.n_sym_leaves > 0 && !far_first) sym_finalize(s, pl.sym_hybrid ? 1 : 0);
             return;  // unmatched targets: sym_finalize_kernel (full) or the one-sided pass (hybrid)
         }
         one_sided(s, pl.p2p_chunks.p, pl.n_p2p_chunks, pl.near_ranges.p);
@@ -1818,7 +1835,7 @@ void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const L
         VPG_CUDA(cudaEventRecord(fork, st));
         VPG_CUDA(cudaStreamWaitEvent(side, fork, 0));
         near_field(side);
-        VPG_CUDA(cudaEventRecord(join, side));
+        if (!far_first) VPG_CUDA(cudaEventRecord(join, side));
     }
     mark(1);
 
@@ -1901,16 +1918,25 @@ void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const L
         }
     }
     mark(5);
-    if (side) VPG_CUDA(cudaStreamWaitEvent(st, join, 0));
-    else near_field(st);
+    if (!far_first) {
+        if (side) VPG_CUDA(cudaStreamWaitEvent(st, join, 0));
+        else near_field(st);
+    }
     if (pl.n_p2p_chunks > 0) {
         const int64_t want = (pl.n_p2p_chunks + kL2PWarps - 1) / kL2PWarps;
         const unsigned grid = unsigned(std::min<int64_t>(want, int64_t(pl.sm_count) * 8));
         launch_pdl(l2p_kernel, dim3(grid), dim3(kL2PWarps * 32), 0, st, (const P2PChunk*)pl.p2p_chunks.p,
                    pl.n_p2p_chunks, (const int32_t*)pl.l2p_rows.p, (const double2*)pl.tgt_sorted.p,
                    (const double2*)loc, (const int32_t*)pl.row_level.p, (const int32_t*)pl.row_morton.p, P,
-                   pl.x0, pl.y0, pl.side, (const int32_t*)pl.tgt_ids.p, out_dev);
+                   pl.x0, pl.y0, pl.side, (const int32_t*)pl.tgt_ids.p, out_dev, far_first ? 1 : 0);
         ++launches;
+    }
+    if (far_first) {
+        VPG_CUDA(cudaEventRecord(far_done, st));
+        VPG_CUDA(cudaStreamWaitEvent(side, far_done, 0));
+        sym_finalize(side, 2);
+        VPG_CUDA(cudaEventRecord(join, side));
+        VPG_CUDA(cudaStreamWaitEvent(st, join, 0));
     }
     if (pl.n_m2p_work > 0) {
         launch_pdl(m2p_kernel, dim3(nblk(pl.n_m2p_work, kM2PWarps)), dim3(kM2PWarps * 32),

@@ -353,7 +353,7 @@ size_t laplace_work_bytes(const Plan& pl);
 LaplaceWork laplace_work_at(const Plan& pl, void* base);
 void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const LaplaceWork& w,
                    cudaStream_t st, cudaEvent_t* ev, int64_t& launches, cudaStream_t side,
-                   cudaEvent_t fork, cudaEvent_t join);
+                   cudaEvent_t fork, cudaEvent_t join, cudaEvent_t far_done);
 void laplace_apply(const Plan& pl, const double* q_dev, double* out_dev,
                    cudaStream_t st, cudaEvent_t* ev, int64_t& launches);
 // direct.cu
