@@ -448,7 +448,14 @@ constexpr int kWSTPW = VPG_M2L_TPW;          // column tiles per MMA warp
 constexpr int kWSMMAWarps = 14 / kWSTPW;     // 14 column tiles
 constexpr int kWSRedThreads = 128;
 constexpr int kWSThreads = 32 * (1 + kWSMMAWarps) + kWSRedThreads;
-constexpr int kWSStages = 4;                 // batch metadata ring
+#ifndef VPG_M2L_DEEP
+#define VPG_M2L_DEEP 1
+#endif
+// source-row ring depth and Y buffers: 3 / 1 (rows of two batches ahead in
+// flight, one Y buffer drained by the reduction during the next k-loop) or 2 / 2
+constexpr int kM2LRaw = VPG_M2L_DEEP ? 3 : 2;
+constexpr int kM2LYs = VPG_M2L_DEEP ? 1 : 2;
+constexpr int kWSStages = 5;                 // batch metadata ring (kM2LRaw + 2 live batches)
 #ifndef VPG_M2L_KUNROLL
 #define VPG_M2L_KUNROLL 2
 #endif
@@ -471,23 +478,27 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
     double2* canon = reinterpret_cast<double2*>(hs + KP * kM2LHS);  // [7][n]
     double2* logmd = canon + kM2LCanon * n;                         // [49]
     int32_t* omap_s = reinterpret_cast<int32_t*>(logmd + 49);       // [49] (+pad)
-    double2* raw0 = reinterpret_cast<double2*>(omap_s + 52);        // [2][kM2LPairs][n]
-    double* yb0 = reinterpret_cast<double*>(raw0 + 2 * kM2LPairs * n);  // [2][n][kM2LXS]
-    double2* a0s0 = reinterpret_cast<double2*>(yb0 + 2 * n * kM2LXS);   // [2][kM2LPairs]
-    M2LStage* stg = reinterpret_cast<M2LStage*>(a0s0 + 2 * kM2LPairs);  // [kWSStages]
-    __shared__ __align__(8) uint64_t bars[7];
+    double2* raw0 = reinterpret_cast<double2*>(omap_s + 52);        // [kM2LRaw][kM2LPairs][n]
+    double* yb0 = reinterpret_cast<double*>(raw0 + kM2LRaw * kM2LPairs * n);  // [kM2LYs][n][kM2LXS]
+    double2* a0s0 = reinterpret_cast<double2*>(yb0 + kM2LYs * n * kM2LXS);    // [kM2LYs][kM2LPairs]
+    M2LStage* stg = reinterpret_cast<M2LStage*>(a0s0 + kM2LYs * kM2LPairs);   // [kWSStages]
+    __shared__ __align__(8) uint64_t bars[1 + 2 * kM2LRaw + 2 * kM2LYs];
     __shared__ double ninv[64];    // -1/l (the epilogue's per-lane rows; no divergent LDC)
-    uint64_t* full = bars + 1;     // [2] source rows landed (TMA tx count)
-    uint64_t* mmadone = bars + 3;  // [2] rows consumed, Y written (MMA warps)
-    uint64_t* yfree = bars + 5;    // [2] Y consumed (reduction warps)
+    uint64_t* full = bars + 1;                 // [kM2LRaw] source rows landed (TMA tx count)
+    uint64_t* rawfree = full + kM2LRaw;        // [kM2LRaw] rows consumed (MMA warps)
+    uint64_t* ydone = rawfree + kM2LRaw;       // [kM2LYs] Y written (MMA warps)
+    uint64_t* yfree = ydone + kM2LYs;          // [kM2LYs] Y consumed (reduction warps)
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
         mbar_init(&bars[0], 1);
-        for (int j = 0; j < 2; ++j) {
+        for (int j = 0; j < kM2LRaw; ++j) {
             mbar_init(&full[j], 1);
-            mbar_init(&mmadone[j], 32 * kWSMMAWarps);
+            mbar_init(&rawfree[j], 32 * kWSMMAWarps);
+        }
+        for (int j = 0; j < kM2LYs; ++j) {
+            mbar_init(&ydone[j], 32 * kWSMMAWarps);
             mbar_init(&yfree[j], kWSRedThreads);
         }
     }
@@ -506,26 +517,26 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
     const int64_t stride = gridDim.x;
     if (warp == 0) {
         // ------------------------------------------------- TMA producer
-        // metadata of batches 0..2, rows of batches 0, 1; then per consumed
-        // batch it: rows of it + 2 (metadata already staged), metadata of
-        // it + 3 (its ring slot held batch it - 1, finished before it)
-        for (int j = 0; j < 3; ++j) {
+        // metadata of batches 0..R, rows of batches 0..R-1 (R = kM2LRaw);
+        // then per consumed batch it: rows of it + R into its slot (metadata
+        // already staged), metadata of it + R + 1
+        for (int j = 0; j <= kM2LRaw; ++j) {
             const int64_t bi = blockIdx.x + j * stride;
-            if (bi < nbatch) m2l_stage_meta(batches[bi], esrc, eoidx, omap_s, &stg[j], lane);
+            if (bi < nbatch) m2l_stage_meta(batches[bi], esrc, eoidx, omap_s, &stg[j % kWSStages], lane);
         }
-        for (int j = 0; j < 2; ++j)
+        for (int j = 0; j < kM2LRaw; ++j)
             if (blockIdx.x + j * stride < nbatch)
-                m2l_issue_rows(&stg[j], mult, n, raw0 + j * kM2LPairs * n, &full[j], lane);
+                m2l_issue_rows(&stg[j % kWSStages], mult, n, raw0 + j * kM2LPairs * n, &full[j], lane);
         for (int it = 0;; ++it) {
-            const int64_t bn = blockIdx.x + (it + 2) * stride;
+            const int64_t bn = blockIdx.x + (it + kM2LRaw) * stride;
             if (bn >= nbatch) break;
-            const int j = it & 1;
-            mbar_wait(&mmadone[j], uint32_t(it >> 1) & 1u);
+            const int j = it % kM2LRaw;
+            mbar_wait(&rawfree[j], uint32_t(it / kM2LRaw) & 1u);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            m2l_issue_rows(&stg[(it + 2) % kWSStages], mult, n, raw0 + j * kM2LPairs * n, &full[j], lane);
+            m2l_issue_rows(&stg[(it + kM2LRaw) % kWSStages], mult, n, raw0 + j * kM2LPairs * n, &full[j], lane);
             const int64_t bm = bn + stride;
             if (bm < nbatch)
-                m2l_stage_meta(batches[bm], esrc, eoidx, omap_s, &stg[(it + 3) % kWSStages], lane);
+                m2l_stage_meta(batches[bm], esrc, eoidx, omap_s, &stg[(it + kM2LRaw + 1) % kWSStages], lane);
         }
     } else if (warp <= kWSMMAWarps) {
         // ---------------------------------------------------------- MMA
@@ -538,13 +549,12 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
         for (int it = 0;; ++it) {
             const int64_t bi = blockIdx.x + it * stride;
             if (bi >= nbatch) break;
-            const int j = it & 1;
-            const uint32_t use = uint32_t(it >> 1);
+            const int j = it % kM2LRaw;
             const M2LBatch bt = bt_next;
             if (bi + stride < nbatch) bt_next = batches[bi + stride];
             const M2LStage& sg = stg[it % kWSStages];
             const double2* raw = raw0 + j * kM2LPairs * n;
-            mbar_wait(&full[j], use & 1u);
+            mbar_wait(&full[j], uint32_t(it / kM2LRaw) & 1u);
             // B-fragment sources: tile TPW w + t, column 8(TPW w + t) + rq ->
             // entry 4(TPW w + t) + rq/2, part rq&1; row k4 + kq <-> k = k4 + kq + 1
             const double2* brow[kWSTPW];
@@ -602,15 +612,24 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
                 }
             }
             // register epilogue: lane holds (re, im) of row l = 8i + rq,
-            // entry p = 4(2w+t) + kq
-            if (it >= 2) mbar_wait(&yfree[j], (use - 1u) & 1u);
-            double* yb = yb0 + j * n * kM2LXS;
-            double2* a0s = a0s0 + j * kM2LPairs;
+            // entry p = 4(2w+t) + kq.  The entries' a_0 are read before the
+            // rows' slot is released to the producer.
+            double2 a0r[kWSTPW];
+#pragma unroll
+            for (int t = 0; t < kWSTPW; ++t) {
+                const int p = 4 * (kWSTPW * w + t) + kq;
+                a0r[t] = p < bt.ecount ? raw[p * n] : make_double2(0.0, 0.0);
+            }
+            mbar_arrive(&rawfree[j]);
+            const int ys = it % kM2LYs;
+            if (it >= kM2LYs) mbar_wait(&yfree[ys], uint32_t(it / kM2LYs - 1) & 1u);
+            double* yb = yb0 + ys * n * kM2LXS;
+            double2* a0s = a0s0 + ys * kM2LPairs;
 #pragma unroll
             for (int t = 0; t < kWSTPW; ++t) {
                 const int p = 4 * (kWSTPW * w + t) + kq;
                 if (p < bt.ecount) {
-                    const double2 a0 = raw[p * n];
+                    const double2 a0 = a0r[t];
                     const int om = sg.omap[p];
                     const int ci = om & 7, sc = (om >> 3) & 1, m = (om >> 4) & 3;
                     if (rq == 0) a0s[p] = a0;
@@ -636,7 +655,7 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
                     }
                 }
             }
-            mbar_arrive(&mmadone[j]);
+            mbar_arrive(&ydone[ys]);
         }
     } else {
         // ---------------------------------------------------- reduction
@@ -646,13 +665,12 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
         for (int it = 0;; ++it) {
             const int64_t bi = blockIdx.x + it * stride;
             if (bi >= nbatch) break;
-            const int j = it & 1;
-            const uint32_t use = uint32_t(it >> 1);
+            const int ys = it % kM2LYs;
             const M2LBatch bt = bt_next;
             if (bi + stride < nbatch) bt_next = batches[bi + stride];
-            const double* yb = yb0 + j * n * kM2LXS;
-            const double2* a0s = a0s0 + j * kM2LPairs;
-            mbar_wait(&mmadone[j], use & 1u);
+            const double* yb = yb0 + ys * n * kM2LXS;
+            const double2* a0s = a0s0 + ys * kM2LPairs;
+            mbar_wait(&ydone[ys], uint32_t(it / kM2LYs) & 1u);
             // per (target t, row l): entries summed in list order, plus the
             // monopole shift (summation.cpp:297-301)
             const double logs = log(side / double(1 << bt.level));
@@ -675,7 +693,7 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
                     if (l == 0) sr += qsum * logs;
                     loc[int64_t(tbox[tg]) * n + l] = make_double2(sr, si);
                 }
-            mbar_arrive(&yfree[j]);
+            mbar_arrive(&yfree[ys]);
         }
     }
 }
@@ -1875,8 +1893,8 @@ void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const L
     if (pl.n_m2l_batches > 0) {
         const size_t smem = sizeof(double) * size_t(pl.KP) * kM2LHS +
                             sizeof(double2) * (size_t(kM2LCanon) * n + 49) + sizeof(int32_t) * 52 +
-                            2 * (sizeof(double2) * (size_t(kM2LPairs) * n + kM2LPairs) +
-                                 sizeof(double) * size_t(n) * kM2LXS) +
+                            kM2LRaw * sizeof(double2) * size_t(kM2LPairs) * n +
+                            kM2LYs * (sizeof(double2) * kM2LPairs + sizeof(double) * size_t(n) * kM2LXS) +
                             kWSStages * sizeof(M2LStage);
         const unsigned grid = unsigned(std::min<int64_t>(pl.n_m2l_batches, int64_t(pl.sm_count)));
         void (*kern)(const M2LBatch*, int64_t, const int32_t*, const int32_t*, const int32_t*,
