@@ -332,6 +332,7 @@ class ReferenceOperator:
         h.refop_set_threads.argtypes = [i]
         h.refop_set_threads.restype = None
         h.refop_mesh_star.argtypes = [d, d, d, d, i, d, d, d, C.POINTER(_P)]
+        h.refop_mesh_star_holes.argtypes = [d, d, d, d, i, d, d, d, i, _P, C.POINTER(_P)]
         h.refop_mesh_free.argtypes = [_P]
         h.refop_mesh_free.restype = None
         h.refop_mesh_info.argtypes = [_P, _P, _P, _P, _P]
@@ -374,8 +375,9 @@ class ReferenceOperator:
     def set_threads(self, n):
         self.h.refop_set_threads(int(n))
 
-    def star_mesh(self, h, r0=1.0, amp=0.3, arms=5, phase=0.0, center=(0.0, 0.0), delta=0.8):
-        return RefMesh(self, h, r0, amp, arms, phase, center, delta)
+    def star_mesh(self, h, r0=1.0, amp=0.3, arms=5, phase=0.0, center=(0.0, 0.0), delta=0.8, holes=()):
+        """holes: circles (cx, cy, r) cut out of the star (Domain::holes)."""
+        return RefMesh(self, h, r0, amp, arms, phase, center, delta, holes)
 
     def basis(self, which, p, q=0):
         """0 tri nodes, 1 tri C, 2 box nodes, 3 box C, 4/5 tri source nodes/w,
@@ -483,11 +485,13 @@ class RefLayer:
 
 
 class RefMesh:
-    def __init__(self, ref, h, r0, amp, arms, phase, center, delta):
+    def __init__(self, ref, h, r0, amp, arms, phase, center, delta, holes=()):
         self.ref = ref
         m = C.c_void_p()
-        ref._err(ref.h.refop_mesh_star(center[0], center[1], r0, amp, arms, phase, h, delta, C.byref(m)),
-                 "build_mesh")
+        hl = np.array(holes, float).reshape(-1)
+        ref._err(ref.h.refop_mesh_star_holes(center[0], center[1], r0, amp, arms, phase, h, delta, len(hl) // 3,
+                                             _p(hl) if hl.size else None, C.byref(m)), "build_mesh")
+        self.holes = [tuple(x) for x in np.array(holes, float).reshape(-1, 3)]
         self.handle = m
         nc, nt, nb, hh = C.c_int(), C.c_int(), C.c_int(), C.c_double()
         ref.h.refop_mesh_info(m, C.byref(nc), C.byref(nt), C.byref(nb), C.byref(hh))

@@ -100,6 +100,20 @@ const char* refop_last_error() { return g_err.c_str(); }
 void refop_set_threads(int n) { volpot::set_thread_count(n); }
 
 // ---- mesh ----
+int refop_mesh_star_holes(double cx, double cy, double r0, double amp, int arms, double phase, double h,
+                          double delta, int nholes, const double* holes /*cx, cy, r per circle*/, void** out) {
+    return guarded([&] {
+        auto mb = std::make_unique<MeshBox>();
+        mb->dom.outer = std::make_shared<volpot::StarCurve>(volpot::Vec2{cx, cy}, r0, amp, arms, phase);
+        for (int k = 0; k < nholes; ++k)
+            mb->dom.holes.push_back(std::make_shared<volpot::Circle>(volpot::Vec2{holes[3 * k], holes[3 * k + 1]},
+                                                                     holes[3 * k + 2]));
+        mb->mesh = volpot::build_mesh(mb->dom, h, delta);
+        mb->mesh.domain = &mb->dom;
+        *out = mb.release();
+    });
+}
+
 int refop_mesh_star(double cx, double cy, double r0, double amp, int arms, double phase, double h,
                     double delta, void** out) {
     return guarded([&] {
@@ -139,7 +153,10 @@ int refop_mesh_cells(void* m, int* type, double* v, double* tt, double* ch, int*
         ch[3 * c] = cl.center.x;
         ch[3 * c + 1] = cl.center.y;
         ch[3 * c + 2] = cl.h;
-        curve[c] = cl.curve == mb.dom.outer.get() ? 0 : -1;
+        curve[c] = -1;
+        if (cl.curve == mb.dom.outer.get()) curve[c] = 0;
+        for (size_t k = 0; k < mb.dom.holes.size(); ++k)
+            if (cl.curve == mb.dom.holes[k].get()) curve[c] = int(k) + 1;
     }
     return 0;
 }

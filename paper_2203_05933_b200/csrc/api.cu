@@ -35,7 +35,7 @@ struct DeviceTables {
     double* k1_tab = nullptr;
 };
 std::map<int, DeviceTables> g_tables;
-std::set<std::pair<const void*, int>> g_optin;
+std::map<std::pair<const void*, int>, int> g_optin;  // (kernel, device) -> opted-in dynamic smem
 std::set<int> g_ready;
 }  // namespace
 
@@ -154,9 +154,10 @@ void smem_optin(const void* func, int bytes) {
     int dev = 0;
     VPG_CUDA(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lk(g_mu);
-    if (g_optin.count({func, dev})) return;
+    auto it = g_optin.find({func, dev});
+    if (it != g_optin.end() && it->second >= bytes) return;  // raised only, never lowered
     VPG_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    g_optin.insert({func, dev});
+    g_optin[{func, dev}] = bytes;
 }
 
 int64_t Plan::device_bytes() const {

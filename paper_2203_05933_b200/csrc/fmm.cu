@@ -449,7 +449,7 @@ constexpr int kWSMMAWarps = 14 / kWSTPW;     // 14 column tiles
 constexpr int kWSRedThreads = 128;
 constexpr int kWSThreads = 32 * (1 + kWSMMAWarps) + kWSRedThreads;
 #ifndef VPG_M2L_DEEP
-#define VPG_M2L_DEEP 1
+#define VPG_M2L_DEEP 0
 #endif
 // source-row ring depth and Y buffers: 3 / 1 (rows of two batches ahead in
 // flight, one Y buffer drained by the reduction during the next k-loop) or 2 / 2

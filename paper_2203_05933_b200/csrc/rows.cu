@@ -54,6 +54,12 @@ const double* k0_table_dev();
 
 using vpg::geom::V2;
 
+// Triangle rows at p = 8 accumulate in registers (1) or through the smem
+// basis tile like every other row (0, A/B)
+#ifndef VPG_ROWS_REGACC
+#define VPG_ROWS_REGACC 0  // 1: 192 registers cost occupancy, rows 0.61 -> 0.71 s on 1.34M dofs
+#endif
+
 namespace vpg {
 namespace rows {
 
@@ -585,9 +591,77 @@ __device__ bool node_at(const DevCtx& c, const RowSmem& S, const geom::Cell& cel
 }
 
 // Walks the flattened node list of the current mode, adding into dst[nb].
+// Triangle rows at p = 8: each thread keeps its own 36 row sums in registers
+// (coef * basis added node by node, no smem tile) and the CTA adds the
+// threads' sums once per task (warp butterflies, then the 4 warps in order).
+__device__ void accumulate_tri8(const DevCtx& c, RowSmem& S, const geom::Cell& cell, int total,
+                                double* red, double* dst) {
+    constexpr int NB = 36;
+    double acc[NB];
+#pragma unroll
+    for (int k = 0; k < NB; ++k) acc[k] = 0.0;
+    for (int i = threadIdx.x; i < total; i += blockDim.x) {
+        V2 chi;
+        double coef = 0.0;
+        if (!node_at(c, S, cell, i, chi, coef)) continue;
+        // koornwinder_eval (basis.cpp:193-228) with the coefficient tables, fused
+        // with the accumulation
+        double q[8];
+        const double xi = chi.x, eta = chi.y;
+        const double sv = 2 * xi - (1 - eta);
+        const double z2 = (1 - eta) * (1 - eta);
+        q[0] = 1;
+        q[1] = sv;
+#pragma unroll
+        for (int m = 1; m + 1 < 8; ++m) q[m + 1] = S.bc.qc[m][0] * sv * q[m] - S.bc.qc[m][1] * z2 * q[m - 1];
+        const double x = 1 - 2 * eta;
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const double beta = 2 * m + 1;
+            const double cq = coef * q[m];
+            double pkm1 = 0, pk = 1;
+#pragma unroll
+            for (int n = m; n < 8; ++n) {
+                const int k = n - m;
+                if (k > 0) {
+                    const double pk1 = k == 1 ? 0.5 * ((beta + 2) * x - beta)
+                                              : (S.bc.jc[m][k - 1][0] + S.bc.jc[m][k - 1][1] * x) * pk -
+                                                    S.bc.jc[m][k - 1][2] * pkm1;
+                    pkm1 = pk;
+                    pk = pk1;
+                }
+                const int idx = n * (n + 1) / 2 + m;
+                acc[idx] = fma(cq, S.bc.gam[idx] * pk, acc[idx]);
+            }
+        }
+    }
+    // reduction: butterflies within each warp, then the warps in order
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+        double v = acc[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) red[warp * NB + k] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < NB) {
+        double v = 0.0;
+        for (int w = 0; w < nw; ++w) v += red[w * NB + threadIdx.x];
+        dst[threadIdx.x] += v;
+    }
+    __syncthreads();
+}
+
 __device__ void accumulate(const DevCtx& c, RowSmem& S, const geom::Cell& cell, int total, int nb,
                            double* tile, double* ctile, double* dst) {
     if (threadIdx.x == 0) S.nodes += total;
+#if VPG_ROWS_REGACC
+    if (!S.box && c.p == 8) {
+        accumulate_tri8(c, S, cell, total, tile, dst);
+        return;
+    }
+#endif
     const int groups = max(1, kThreads / nb);
     const int g = threadIdx.x / nb, n = threadIdx.x % nb;
     const bool active = g < groups && threadIdx.x < groups * nb;
@@ -720,7 +794,11 @@ __device__ bool is_self_target(V2 zeta0, V2 zstar) {
     return geom::dist(zstar, zeta0) <= 1e-12 * (1.0 + geom::norm(zeta0));
 }
 
+#if VPG_ROWS_REGACC
+__global__ void __maxnreg__(192)
+#else
 __global__ void __launch_bounds__(kThreads)
+#endif
 rows_kernel(DevCtx c, const RowTask* tasks, const double* table, double* out, int* err,
             unsigned long long* nodes_done) {
     extern __shared__ __align__(16) double dyn[];
