@@ -1062,6 +1062,127 @@ void build_helm_fmm(Plan& pl) {
     pl.hf = true;
 }
 
+// Half a warp per chunk (cfg5's level-8 leaves hold ~16 targets, so a warp per
+// chunk left half its lanes idle): the two halves take independent chunks,
+// broadcast their own sources 16 at a time (width-16 shuffles) and give each
+// lane up to U targets (chunks of <= 16 U targets).  Same arithmetic per pair
+// as hf_l2p_p2p_kernel.
+template <int U>
+__global__ void __launch_bounds__(kHfWarps * 32, 2)
+hf_l2p_p2p16_kernel(HfLevels hl, const P2PChunk* chunks, int64_t nchunks, const int2* ranges,
+                    const int32_t* tgt_row, const double2* sxy, const double* q, const double2* txy,
+                    const int32_t* tids, const double* tab, const double* Lv, double x0, double y0,
+                    double side, double lambda, const double* k0tab, const double2* gtab, double* out) {
+    extern __shared__ double2 hsm[];
+    double2* ltab = hsm;  // log table, 8 copies (common.cuh)
+    const int n = hl.n, n2 = n * n;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, half = lane >> 4, l16 = lane & 15;
+    const unsigned hmask = half ? 0xffff0000u : 0x0000ffffu;
+    double* L = reinterpret_cast<double*>(hsm + kLogTableSize * kLogTableCopies) + (warp * 2 + half) * n2;
+    log_table_to_smem(ltab, gtab);
+    __syncthreads();
+    const uint32_t tab_lane = log_table_lane_addr(ltab, lane & (kLogTableCopies - 1));
+    const double* nodes = tab;
+    const double* bw = tab + 32;
+    const double l2q = 0.25 * lambda * lambda;
+    const double c0 = 0.5 * log(l2q) + 0.57721566490153286061;
+    for (int64_t ci = (int64_t(blockIdx.x) * kHfWarps + warp) * 2 + half; ci < nchunks;
+         ci += int64_t(gridDim.x) * kHfWarps * 2) {
+        const P2PChunk c = chunks[ci];
+        if (c.part != 0) continue;  // split chunks: once, whole
+        const int64_t row = tgt_row[c.tbegin];
+        const int64_t leaf = row - (lvl_base(hl.L) - lvl_base(2));
+        const double s = side / double(1 << hl.L);
+        const double cx = x0 + (squash2(uint32_t(leaf)) + 0.5) * s;
+        const double cy = y0 + (squash2(uint32_t(leaf) >> 1) + 0.5) * s;
+        const int64_t hrow = hl.base[hl.L] + leaf;
+        __syncwarp(hmask);
+        for (int j = l16; j < n2; j += 16) L[j] = Lv[hrow * n2 + j];
+        __syncwarp(hmask);
+        const bool fast = l2q * 18.0 * s * s <= 0.25;
+        // passes of 16 U targets (chunks hold <= 64; most cfg5 leaves <= 32)
+        for (int tb = 0; tb < c.tcount; tb += 16 * U) {
+        const int tcnt = min(16 * U, c.tcount - tb);
+        const int nu = (tcnt + 15) >> 4;  // targets per lane (<= U)
+        double2 t[U];
+        double far[U], near[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            far[u] = near[u] = 0.0;
+            t[u] = txy[c.tbegin + tb + min(l16 + 16 * u, tcnt - 1)];
+            if (u >= nu) continue;
+            double ly[kHfMaxN];
+            hf_bary(nodes, bw, n, (t[u].y - cy) * 2.0 / s, ly);
+            const double x = (t[u].x - cx) * 2.0 / s;
+            int hit = -1;
+            double sx = 0.0;
+            for (int a = 0; a < n; ++a) {
+                const double d = x - nodes[a];
+                if (d == 0.0) hit = a;
+                sx += bw[a] / (d == 0.0 ? 1.0 : d);
+            }
+            const double inv = 1.0 / sx;
+            for (int a = 0; a < n; ++a) {
+                const double d = x - nodes[a];
+                const double lxa = hit >= 0 ? (a == hit ? 1.0 : 0.0) : bw[a] / d * inv;
+                double inner = 0.0;
+#pragma unroll
+                for (int b2 = 0; b2 < kHfMaxN; ++b2)
+                    if (b2 < n) inner = fma(ly[b2], L[a * n + b2], inner);
+                far[u] = fma(lxa, inner, far[u]);
+            }
+        }
+        auto sweep = [&](auto fast_tag) {
+            constexpr bool kFast = decltype(fast_tag)::value;
+            for (int ri = 0; ri < c.rcount; ++ri) {
+                const int2 rg = ranges[c.rfirst + ri];
+                for (int base = rg.x; base < rg.x + rg.y; base += 16) {
+                    const int cnt = min(16, rg.x + rg.y - base);
+                    double2 sp = make_double2(0.0, 0.0);
+                    double qj = 0.0;
+                    if (l16 < cnt) {
+                        sp = sxy[base + l16];
+                        qj = q[base + l16];
+                    }
+#pragma unroll 2
+                    for (int j = 0; j < cnt; ++j) {
+                        const double px = __shfl_sync(hmask, sp.x, j, 16);
+                        const double py = __shfl_sync(hmask, sp.y, j, 16);
+                        const double pq = __shfl_sync(hmask, qj, j, 16);
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            if (u >= nu) continue;
+                            const double dx = t[u].x - px, dy = t[u].y - py;
+                            const double r2 = fma(dy, dy, dx * dx);
+                            const double qq = l2q * r2;
+                            double v;
+                            if (kFast) {
+                                double ed;
+                                const double tl = fast_log_split(r2, tab_lane, ed);
+                                const double lnr2 = fma(ed, kLn2Hi, fma(ed, kLn2Lo, tl));
+                                v = fma(-fma(0.5, lnr2, c0), k0_i0_9(qq), k0_h_9(qq));
+                                if (__double2hiint(r2) < 0x00100000) v = r2 == 0.0 ? 0.0 : k0_small_q(qq);
+                            } else {
+                                v = r2 == 0.0 ? 0.0
+                                              : (qq <= 1.0 ? k0_small_q(qq) : k0_dev(lambda * sqrt(r2), k0tab));
+                            }
+                            near[u] = fma(kInv2Pi * pq, v, near[u]);
+                        }
+                    }
+                }
+            }
+        };
+        if (fast) sweep(std::true_type{});
+        else sweep(std::false_type{});
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int li = l16 + 16 * u;
+            if (u < nu && li < tcnt) out[tids[c.tbegin + tb + li]] = far[u] + near[u];
+        }
+        }
+    }
+}
+
 // The per-level compress (Wt = Vt W) and expand (Lv = Vc Lt) GEMMs on the FP64
 // tensor cores: C (M x N) = A (M x K) . B (K x N), column-major, M and K at most
 // a few hundred (k, n^2), N the level's box count.  A CTA takes NT columns at a
@@ -1265,11 +1386,25 @@ void helm_fmm_apply(const Plan& pl, const double* q_dev, double* out_dev, cudaSt
     if (pl.n_p2p_chunks > 0) {
         const unsigned grid = unsigned(std::min<int64_t>((pl.n_p2p_chunks + kHfWarps - 1) / kHfWarps,
                                                          int64_t(pl.sm_count) * 8));
-        const size_t smem = size_t(kLogTableBytes) + sizeof(double) * kHfWarps * kHfMaxN * kHfMaxN;
-        hf_l2p_p2p_kernel<<<grid, kHfWarps * 32, smem, st>>>(
-            hl, pl.p2p_chunks.p, pl.n_p2p_chunks, pl.near_ranges.p, pl.tgt_row.p, pl.src_sorted.p, qs,
-            pl.tgt_sorted.p, pl.tgt_ids.p, pl.hf_tab.p, Lv, pl.x0, pl.y0, pl.side, pl.lambda,
-            k0_table_dev(), log_table_dev(), out_dev);
+#ifndef VPG_HF_HALF
+#define VPG_HF_HALF 0  // 1: half-warp chunks, slower on cfg5 (K0 near field 2.23 -> 2.98 ms)
+#endif
+        if (VPG_HF_HALF) {  // half a warp per chunk, 32 targets per pass (U = 2)
+            const unsigned grid16 = unsigned(std::min<int64_t>((pl.n_p2p_chunks + 2 * kHfWarps - 1) / (2 * kHfWarps),
+                                                               int64_t(pl.sm_count) * 8));
+            const size_t smem16 = size_t(kLogTableBytes) + sizeof(double) * 2 * kHfWarps * n2;
+            smem_optin((const void*)hf_l2p_p2p16_kernel<2>, int(smem16));
+            hf_l2p_p2p16_kernel<2><<<grid16, kHfWarps * 32, smem16, st>>>(
+                hl, pl.p2p_chunks.p, pl.n_p2p_chunks, pl.near_ranges.p, pl.tgt_row.p, pl.src_sorted.p, qs,
+                pl.tgt_sorted.p, pl.tgt_ids.p, pl.hf_tab.p, Lv, pl.x0, pl.y0, pl.side, pl.lambda,
+                k0_table_dev(), log_table_dev(), out_dev);
+        } else {
+            const size_t smem = size_t(kLogTableBytes) + sizeof(double) * kHfWarps * kHfMaxN * kHfMaxN;
+            hf_l2p_p2p_kernel<<<grid, kHfWarps * 32, smem, st>>>(
+                hl, pl.p2p_chunks.p, pl.n_p2p_chunks, pl.near_ranges.p, pl.tgt_row.p, pl.src_sorted.p, qs,
+                pl.tgt_sorted.p, pl.tgt_ids.p, pl.hf_tab.p, Lv, pl.x0, pl.y0, pl.side, pl.lambda,
+                k0_table_dev(), log_table_dev(), out_dev);
+        }
         VPG_LAUNCH_CHECK();
         ++launches;
     }
