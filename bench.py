@@ -451,9 +451,58 @@ def run_gpu(args):
         e2e_ev[i][1].record(stream)
     torch.cuda.synchronize()
     e2e_serial_ms = float(np.sum([a.elapsed_time(b) for a, b in e2e_ev])) / args.steps
-    two_stream = e2e_ms is not None and e2e_ms < e2e_serial_ms
-    if not two_stream:  # one stream was faster (or the only option): report it
-        e2e_ms = e2e_serial_ms
+    # copy/compute pipeline through the device-pointer API: step i's H2D (own
+    # copy stream) runs under step i-1's apply and its D2H (another copy stream)
+    # under step i+1's, applies themselves back to back on one stream
+    e2e_pipe_ms = None
+    if op is None:
+        q_d2 = [torch.empty(wl.ns, dtype=torch.float64, device="cuda") for _ in range(2)]
+        o_d2 = [torch.empty(wl.nt, dtype=torch.float64, device="cuda") for _ in range(2)]
+        h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
+        ev_h2d = [torch.cuda.Event() for _ in range(2)]
+        ev_app = [torch.cuda.Event() for _ in range(2)]
+        ev_d2h = [torch.cuda.Event() for _ in range(2)]
+
+        def pipe(nsteps, record=None):
+            for i in range(nsteps):
+                k = i & 1
+                with torch.cuda.stream(h2d_s):
+                    if i >= 2:
+                        h2d_s.wait_event(ev_app[k])  # the apply of step i-2 read q_d2[k]
+                    q_d2[k].copy_(q_hs[k], non_blocking=True)
+                    ev_h2d[k].record(h2d_s)
+                stream.wait_event(ev_h2d[k])
+                if i >= 2:
+                    stream.wait_event(ev_d2h[k])     # o_d2[k] of step i-2 copied out
+                with torch.cuda.stream(stream):
+                    flush.zero_()
+                plan.apply_device(q_d2[k].data_ptr(), o_d2[k].data_ptr(), sh)
+                ev_app[k].record(stream)
+                with torch.cuda.stream(d2h_s):
+                    d2h_s.wait_event(ev_app[k])
+                    out_hs[k].copy_(o_d2[k], non_blocking=True)
+                    ev_d2h[k].record(d2h_s)
+
+        pipe(max(2, args.warmup))
+        torch.cuda.synchronize()
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record(stream)
+        h2d_s.wait_event(p0)
+        pipe(args.steps)
+        j1 = torch.cuda.Event()
+        j1.record(d2h_s)
+        stream.wait_event(j1)
+        p1.record(stream)
+        torch.cuda.synchronize()
+        e2e_pipe_ms = p0.elapsed_time(p1) / args.steps
+    cands = {"one stream": e2e_serial_ms}
+    if e2e_ms is not None:
+        cands["applies alternating over two streams"] = e2e_ms
+    if e2e_pipe_ms is not None:
+        cands["copy/compute pipeline (H2D and D2H streams around device-pointer applies)"] = e2e_pipe_ms
+    e2e_mode = min(cands, key=cands.get)
+    e2e_ms = cands[e2e_mode]
+    two_stream = e2e_mode != "one stream"
     if dist:
         t = torch.tensor([e2e_ms, e2e_serial_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -550,8 +599,8 @@ def run_gpu(args):
         "e2e": {"value": inter / (e2e_ms * 1e-3), "unit": "interactions/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": 8 * (wl.ns if op is None else int(f_np.size)), "d2h_bytes_per_step": 8 * wl.nt,
                 "path": ("vpg_operator_apply" if op is not None else "vpg_plan_apply")
-                        + " with pinned host buffers, "
-                        + ("applies alternating over two streams" if two_stream else "one stream"),
+                        + " with pinned host buffers, " + e2e_mode,
+                "candidates_ms": cands,
                 "serial_ms_per_step": e2e_serial_ms,
                 "l2": ("not flushed in the two-stream loop: the plan's working set is > 4x L2" if big and two_stream
                        else "flushed (256 MB write) before every step"),
