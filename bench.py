@@ -153,7 +153,15 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # functional check of the sharded flow on a single-GPU box (VPG_BENCH_BACKEND=gloo):
+    # ranks share device 0; timings from such a run are not scaling numbers
+    if os.environ.get("VPG_BENCH_BACKEND") == "gloo":
+        local = 0
     return world, rank, local
+
+
+def dist_backend():
+    return os.environ.get("VPG_BENCH_BACKEND", "nccl")
 
 
 def interaction_count(wl, levels, p2p_pairs):
@@ -278,16 +286,18 @@ def run_gpu(args):
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group(dist_backend(), **({"device_id": torch.device("cuda", local)}
+                                                   if dist_backend() == "nccl" else {}))
 
     wl = load_workload(args.workload)
     kern = kernel_for(wl)
     eps = args.eps if args.eps else min(wl.eps)
     plan = vp.SummationPlan(kern, wl.src, wl.tgt, eps, mode=args.mode, device=local)
+    info_full = plan.info()  # the whole job's counts (value = all ranks' interactions / max time)
     shard = None
     if world > 1:
         shard = multigpu.shard_plan(plan, rank, world)
-    info = plan.info()
+    info = plan.info()       # this rank's shard (kernel statistics of rank 0)
     # one explicit stream for the L2 flush, the events and every apply: the
     # default stream's handle is 0, which the library would replace by a
     # stream of its own (unordered with the flush, synchronised per call)
@@ -521,7 +531,7 @@ def run_gpu(args):
             dist.destroy_process_group()
         return 0
 
-    ref_pairs = info["p2p_pairs"]
+    ref_pairs = info_full["p2p_pairs"]
     if args.mode == "native" and wl.kernel == "laplace":
         # the workload's count is the reference tree's, whatever tree runs
         with vp.SummationPlan(kern, wl.src, wl.tgt, eps, mode="reference", device=local) as rp:
@@ -808,7 +818,8 @@ def run_layer(args):
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group(dist_backend(), **({"device_id": torch.device("cuda", local)}
+                                                   if dist_backend() == "nccl" else {}))
     sys_, cf, tg_all = W.layer_cfg2(_layer_kernel(args.workload))
     fam, lam = int(sys_.kernel.family), sys_.kernel.lam
     # targets are independent: rank r evaluates a contiguous slice, no collective
