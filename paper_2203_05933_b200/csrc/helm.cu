@@ -16,6 +16,7 @@
 //     order.
 #include <algorithm>
 #include <cmath>
+#include <mutex>
 #include <type_traits>
 #include <vector>
 
@@ -24,6 +25,7 @@
 
 #include "k0.cuh"
 #include "plan.cuh"
+#include "sym.cuh"
 
 namespace vpg {
 namespace {
@@ -271,44 +273,137 @@ __global__ void hf_kmat_kernel(const int2* offs, int noff, int n, const double* 
     A[idx] = kInv2Pi * k0_dev(lambda * sqrt(dx * dx + dy * dy), k0tab);
 }
 
-// W_P = sum_c S_{c&1} W_c S_{c>>1}^T over children with sources (c order):
-// the four children staged together, T_c = S_{c&1} W_c for all c in one
-// pass, then the second products summed in quadrant order.
-__global__ void hf_m2m_kernel(int level, int n, const double* S, const int32_t* scnt_l,
-                              const int32_t* scnt_c, int64_t base_p, int64_t base_c, double* W) {
-    __shared__ double wc[4][kHfMaxN * kHfMaxN], tt[4][kHfMaxN * kHfMaxN];
-    const int64_t b = blockIdx.x;
-    if (scnt_l[b] == 0) return;
-    const int n2 = n * n;
-    const int t = threadIdx.x;
-    const int a = t / n, bb = t % n;
-    bool has[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) has[c] = scnt_c[(b << 2) | c] > 0;
-    for (int i = t; i < 4 * n2; i += blockDim.x) {
-        const int c = i / n2, e = i % n2;
-        wc[c][e] = has[c] ? W[(base_c + ((b << 2) | c)) * n2 + e] : 0.0;
+// Child-to-parent interpolation on the FP64 pipe with the matrix in the
+// constant bank.  S_h[a][a'] = l_a(x_h(a')) (parent basis a at child node a',
+// h = the child half) depends on n only, and the Chebyshev nodes are
+// symmetric, so S_1 = J S_0 J (J = index reversal): every product below uses
+// S_0 with compile-time indices (DFMA with a c[][] operand, no loads) and the
+// child half only reverses which smem element a thread reads or writes.
+constexpr int kHfNMin = 8;
+__host__ __device__ constexpr int hf_s0_off(int n) { return n <= kHfNMin ? 0 : hf_s0_off(n - 1) + (n - 1) * (n - 1); }
+constexpr int kHfS0Total = hf_s0_off(kHfMaxN + 1);
+__constant__ double c_hfS0[kHfS0Total];  // S_0 for n = 8..20, row-major [a][a']
+
+template <int N>
+__device__ __forceinline__ double hf_s0(int a, int ap) {
+    constexpr int kOff = hf_s0_off(N);
+    return c_hfS0[kOff + a * N + ap];
+}
+
+// parents per CTA (4 N threads each) and target boxes per CTA (N threads
+// each), within 48 KB of static smem
+__host__ __device__ constexpr int hf_m2m_parents(int n) { return n <= 18 ? 2 : 1; }
+__host__ __device__ constexpr int hf_l2l_boxes(int n) { return n <= 18 ? 8 : 6; }
+
+// M2M: W_P = sum_c S_{c&1} W_c S_{c>>1}^T over the children with sources.
+// Pass 1: thread (parent, c, column j) forms column j of T_c = S_{c&1} W_c;
+// pass 2: thread (parent, c, row a) forms row a of T_c S_{c>>1}^T; the four
+// partials are then summed in quadrant order.  Empty children contribute
+// zeros; parents without sources are not written (never read downstream).
+template <int N>
+__global__ void __launch_bounds__(4 * N * hf_m2m_parents(N))
+hf_m2m_kernel(int64_t nparents, const int32_t* scnt_l, const int32_t* scnt_c, int64_t base_p, int64_t base_c,
+              double* W) {
+    constexpr int N2 = N * N, RS = N | 1, MS = N * RS;  // odd row stride: conflict-free rows and columns
+    constexpr int P = hf_m2m_parents(N);
+    __shared__ double wc[P][4][MS], tt[P][4][MS];
+    const int64_t b0 = int64_t(blockIdx.x) * P;
+    for (int i = threadIdx.x; i < P * 4 * N2; i += blockDim.x) {
+        const int p = i / (4 * N2), r = i % (4 * N2), c = r / N2, e = r % N2;
+        const int64_t child = ((b0 + p) << 2) | c;
+        wc[p][c][(e / N) * RS + e % N] =
+            (b0 + p < nparents && scnt_c[child] > 0) ? W[(base_c + child) * N2 + e] : 0.0;
     }
     __syncthreads();
-    if (t < n2)
+    const int p = threadIdx.x / (4 * N), c = (threadIdx.x / N) & 3, j = threadIdx.x % N;
+    {
+        const bool rx = c & 1;
+        double w[N];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            if (!has[c]) continue;
-            const double* Sx = S + (c & 1) * n * n;
-            double v = 0.0;
-            for (int q = 0; q < n; ++q) v = fma(Sx[a * n + q], wc[c][q * n + bb], v);
-            tt[c][t] = v;
+        for (int q = 0; q < N; ++q) w[q] = wc[p][c][(rx ? N - 1 - q : q) * RS + j];
+#pragma unroll
+        for (int a = 0; a < N; ++a) {
+            double u = 0.0;
+#pragma unroll
+            for (int q = 0; q < N; ++q) u = fma(hf_s0<N>(a, q), w[q], u);
+            tt[p][c][(rx ? N - 1 - a : a) * RS + j] = u;
         }
+    }
     __syncthreads();
-    if (t < n2) {
-        double acc = 0.0;
+    {
+        const bool ry = c >> 1;
+        double t[N];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            if (!has[c]) continue;
-            const double* Sy = S + (c >> 1) * n * n;
-            for (int q = 0; q < n; ++q) acc = fma(Sy[bb * n + q], tt[c][a * n + q], acc);
+        for (int q = 0; q < N; ++q) t[q] = tt[p][c][j * RS + (ry ? N - 1 - q : q)];
+#pragma unroll
+        for (int bb = 0; bb < N; ++bb) {
+            double v = 0.0;
+#pragma unroll
+            for (int q = 0; q < N; ++q) v = fma(hf_s0<N>(bb, q), t[q], v);
+            wc[p][c][j * RS + (ry ? N - 1 - bb : bb)] = v;
         }
-        W[(base_p + b) * n2 + t] = acc;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < P * N2; i += blockDim.x) {
+        const int pp = i / N2, e = i % N2;
+        const int64_t b = b0 + pp;
+        if (b >= nparents || scnt_l[b] == 0) continue;
+        const int s = (e / N) * RS + e % N;
+        W[(base_p + b) * N2 + e] = ((wc[pp][0][s] + wc[pp][1][s]) + wc[pp][2][s]) + wc[pp][3][s];
+    }
+}
+
+// L2L: Lv[r] += S_{c&1}^T Lp S_{c>>1} (Lp = the parent's Lv, c = r's
+// quadrant).  Pass 1: thread (box, row a') forms row a' of Lp S_{c>>1};
+// pass 2: thread (box, column j) forms column j of S_{c&1}^T (that) and adds
+// it into Lv[r].
+template <int N>
+__global__ void __launch_bounds__(N * hf_l2l_boxes(N))
+hf_l2l_kernel(int64_t nbox, int64_t base_l, int64_t base_p, const int32_t* tbox, double* Lv) {
+    constexpr int N2 = N * N, RS = N | 1, MS = N * RS;
+    constexpr int P = hf_l2l_boxes(N);
+    __shared__ double lp[P][MS], tt[P][MS];
+    const int64_t i0 = int64_t(blockIdx.x) * P;
+    for (int i = threadIdx.x; i < P * N2; i += blockDim.x) {
+        const int p = i / N2, e = i % N2;
+        if (i0 + p < nbox) {
+            const int64_t b = tbox[i0 + p] - base_l;
+            lp[p][(e / N) * RS + e % N] = Lv[(base_p + (b >> 2)) * N2 + e];
+        }
+    }
+    __syncthreads();
+    const int p = threadIdx.x / N, j = threadIdx.x % N;
+    const bool live = i0 + p < nbox;
+    const int64_t r = live ? tbox[i0 + p] : 0;
+    const int c = int((r - base_l) & 3);
+    if (live) {
+        const bool ry = c >> 1;
+        double l[N];
+#pragma unroll
+        for (int q = 0; q < N; ++q) l[q] = lp[p][j * RS + (ry ? N - 1 - q : q)];
+#pragma unroll
+        for (int bb = 0; bb < N; ++bb) {
+            double u = 0.0;
+#pragma unroll
+            for (int q = 0; q < N; ++q) u = fma(hf_s0<N>(q, bb), l[q], u);
+            tt[p][j * RS + (ry ? N - 1 - bb : bb)] = u;
+        }
+    }
+    __syncthreads();
+    if (live) {
+        const bool rx = c & 1;
+        double t[N];
+#pragma unroll
+        for (int q = 0; q < N; ++q) t[q] = tt[p][(rx ? N - 1 - q : q) * RS + j];
+        double* out = Lv + r * N2 + j;
+#pragma unroll
+        for (int a = 0; a < N; ++a) {
+            double v = 0.0;
+#pragma unroll
+            for (int q = 0; q < N; ++q) v = fma(hf_s0<N>(q, a), t[q], v);
+            const int row = rx ? N - 1 - a : a;
+            out[row * N] += v;
+        }
     }
 }
 
@@ -501,41 +596,14 @@ __global__ void hf_m2l_reduce_kernel(const int2* splits, int nparts, const doubl
     Lt[int64_t(sp.x) * kHfMaxK + i] = acc;
 }
 
-// L2L: Lv[r] += the parent's Lv interpolated to r's nodes (Lv[r] = V_l Lt[r]
-// already, one cuBLAS GEMM per level); top-down, one launch per level.
-__global__ void hf_l2l_kernel(HfLevels hl, int level, const int32_t* tbox, const double* S, double* Lv) {
-    __shared__ double lp[kHfMaxN * kHfMaxN], tt[kHfMaxN * kHfMaxN];
-    const int n = hl.n, n2 = n * n;
-    const int64_t r = tbox[blockIdx.x];
-    const int t = threadIdx.x;
-    const int a = t / n, bb = t % n;
-    const int64_t b = r - hl.base[level];
-    if (t < n2) lp[t] = Lv[(hl.base[level - 1] + (b >> 2)) * n2 + t];
-    __syncthreads();
-    const int c = int(b & 3);
-    const double* Sx = S + (c & 1) * n * n;
-    const double* Sy = S + (c >> 1) * n * n;
-    // tt[a'][b] = sum_b' Sy[b'][b] lp[a'][b']; Lv += sum_a' Sx[a'][a] tt[a'][b]
-    if (t < n2) {
-        double u = 0.0;
-        for (int q = 0; q < n; ++q) u = fma(Sy[q * n + bb], lp[a * n + q], u);
-        tt[t] = u;
-    }
-    __syncthreads();
-    if (t < n2) {
-        double v = Lv[r * n2 + t];
-        for (int q = 0; q < n; ++q) v = fma(Sx[q * n + a], tt[q * n + bb], v);
-        Lv[r * n2 + t] = v;
-    }
-}
-
 // Warp per near-field chunk: far field from the leaf's Lv (barycentric) plus
 // the direct 3x3-leaf K0 sum; out = far + near in the original order.
 __global__ void __launch_bounds__(kHfWarps * 32, 2)
 hf_l2p_p2p_kernel(HfLevels hl, const P2PChunk* chunks, int64_t nchunks, const int2* ranges,
                   const int32_t* tgt_row, const double2* sxy, const double* q, const double2* txy,
                   const int32_t* tids, const double* tab, const double* Lv, double x0, double y0,
-                  double side, double lambda, const double* k0tab, const double2* gtab, double* out) {
+                  double side, double lambda, const double* k0tab, const double2* gtab, double* out,
+                  int near_on) {
     extern __shared__ double2 hsm[];
     double2* ltab = hsm;  // log table, 8 copies (common.cuh)
     double (*lvs)[kHfMaxN * kHfMaxN] =
@@ -643,12 +711,94 @@ hf_l2p_p2p_kernel(HfLevels hl, const P2PChunk* chunks, int64_t nchunks, const in
                 }
             }
         };
-        if (fast) sweep(std::true_type{});
+        if (!near_on) {  // symmetric near field: out = far here, the finalize adds the near sums
+        } else if (fast) sweep(std::true_type{});
         else sweep(std::false_type{});
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
             const int li = lane + 32 * u;
             if (li < c.tcount) out[tids[c.tbegin + li]] = far[u] + near[u];
+        }
+    }
+}
+
+// The K0 near field as a pair function of the symmetric kernel (sym.cuh):
+// K0(lambda r) for one unordered pair of nodes, 0 at r = 0 (summation.cpp:486
+// skips coincident pairs).  Fast form (every near pair has lambda r <= 1):
+// the two series of degree D through q = (lambda r / 2)^2 and the table log
+// of r^2; q is clamped at its plan bound so the padding points of partial
+// tiles (1e100 away, zero charge) stay finite.  General form: the series for
+// q <= 1, else the fitted K0 of k0.cuh.
+template <bool kFast, int D>
+struct K0NearK {
+    double l2q, c0, qmax, lambda;
+    const double* k0tab;
+    __device__ __forceinline__ double operator()(double r2, uint32_t tab_lane) const {
+        if (kFast) {
+            const double qq = fmin(l2q * r2, qmax);
+            double ed;
+            const double tl = fast_log_split(r2, tab_lane, ed);
+            const double lnr2 = fma(ed, kLn2Hi, fma(ed, kLn2Lo, tl));
+            double v = fma(-fma(0.5, lnr2, c0), k0_i0_d<D>(qq), k0_h_d<D>(qq));
+            if (__double2hiint(r2) < 0x00100000) v = r2 == 0.0 ? 0.0 : k0_small_q(qq);
+            return v;
+        }
+        const double qq = l2q * r2;
+        return r2 == 0.0 ? 0.0 : (qq <= 1.0 ? k0_small_q(qq) : k0_dev(lambda * sqrt(r2), k0tab));
+    }
+};
+
+// Per leaf (warp per leaf): the matched targets add the leaf's slot partials
+// of the symmetric K0 sweep in slot order; unmatched targets (beyond the
+// leaf's sources) sum their 3x3 near sources one-sided (lanes stride each
+// range, butterfly reduction).  out = far (already written) + near / 2 pi.
+constexpr int kHfFinWarps = 8;
+template <class K>
+__global__ void __launch_bounds__(kHfFinWarps * 32)
+hf_sym_finalize_kernel(K kern, const SymLeaf* leaves, int64_t nleaves, const double* part, const int2* ranges,
+                       const double2* sxy, const double* q, const double2* txy, const int32_t* tids,
+                       const double2* gtab, double* out) {
+    extern __shared__ double2 hfin[];
+    log_table_to_smem(hfin, gtab);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t tab_lane = log_table_lane_addr(hfin, lane & (kLogTableCopies - 1));
+    for (int64_t w = int64_t(blockIdx.x) * kHfFinWarps + warp; w < nleaves;
+         w += int64_t(gridDim.x) * kHfFinWarps) {
+        const SymLeaf lf = leaves[w];
+        for (int k = lane; k < lf.n; k += 32) {
+            const double* pk = part + lf.pbase + k;
+            double sum = 0.0;
+            int sl = 0;
+            for (; sl + 4 <= lf.nslot; sl += 4) {  // four loads in flight, added in slot order
+                const double a0 = __ldcg(pk + int64_t(sl) * lf.n), a1 = __ldcg(pk + int64_t(sl + 1) * lf.n);
+                const double a2 = __ldcg(pk + int64_t(sl + 2) * lf.n), a3 = __ldcg(pk + int64_t(sl + 3) * lf.n);
+                sum += a0;
+                sum += a1;
+                sum += a2;
+                sum += a3;
+            }
+            for (; sl < lf.nslot; ++sl) sum += __ldcg(pk + int64_t(sl) * lf.n);
+            double& o = out[tids[lf.tgt + k]];
+            o = o + kInv2Pi * sum;
+        }
+        for (int t = lf.tgt + lf.n; t < lf.t1; ++t) {
+            const double2 tp = txy[t];
+            double v = 0.0;
+            for (int r = 0; r < lf.rcount; ++r) {
+                const int2 rg = ranges[lf.rfirst + r];
+                for (int j = lane; j < rg.y; j += 32) {
+                    const double2 sp = sxy[rg.x + j];
+                    const double dx = tp.x - sp.x, dy = tp.y - sp.y;
+                    v = fma(q[rg.x + j], kern(fma(dy, dy, dx * dx), tab_lane), v);
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) {
+                double& o = out[tids[t]];
+                o = o + kInv2Pi * v;
+            }
         }
     }
 }
@@ -783,7 +933,58 @@ HfLevels hf_levels(const Plan& pl) {
 // Native-mode plan build for modified Helmholtz (see the block comment at
 // hf_kmat_kernel).  Leaves pl.hf false (treecode fallback) when no level is
 // fine enough for the interpolation (lambda s > 5 at every level).
+// n (Chebyshev nodes per dimension) as a compile-time constant, 8..20
+template <class F>
+void hf_dispatch_n(int n, F&& f) {
+    switch (n) {
+#define VPG_HF_N(v) \
+    case v: f(std::integral_constant<int, v>()); break;
+        VPG_HF_N(8) VPG_HF_N(9) VPG_HF_N(10) VPG_HF_N(11) VPG_HF_N(12) VPG_HF_N(13) VPG_HF_N(14)
+        VPG_HF_N(15) VPG_HF_N(16) VPG_HF_N(17) VPG_HF_N(18) VPG_HF_N(19) VPG_HF_N(20)
+#undef VPG_HF_N
+        default: throw Error{VPG_ERR_INVALID_ARGUMENT, "Chebyshev order outside 8..20"};
+    }
+}
+
+// S_0 (parent basis at the lower child half's nodes) for every n, written to
+// the constant bank once per device; the values depend on n only.
+void hf_const_init() {
+    static std::mutex mu;
+    static uint64_t done = 0;
+    int dev = 0;
+    VPG_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev < 64 && (done >> dev & 1u)) return;
+    const double pi = 3.14159265358979323846;
+    std::vector<double> s0(size_t(kHfS0Total), 0.0);
+    for (int n = kHfNMin; n <= kHfMaxN; ++n) {
+        std::vector<double> t(static_cast<size_t>(n)), bw(static_cast<size_t>(n));
+        for (int a = 0; a < n; ++a) {
+            const double th = (2 * a + 1) * pi / (2 * n);
+            t[size_t(a)] = std::cos(th);
+            bw[size_t(a)] = (a % 2 ? -1.0 : 1.0) * std::sin(th);
+        }
+        for (int ap = 0; ap < n; ++ap) {
+            const double x = -0.5 + 0.5 * t[size_t(ap)];
+            std::vector<double> w(static_cast<size_t>(n));
+            int hit = -1;
+            double sum = 0.0;
+            for (int a = 0; a < n; ++a) {
+                const double d = x - t[size_t(a)];
+                if (d == 0.0) hit = a;
+                w[size_t(a)] = bw[size_t(a)] / (d == 0.0 ? 1.0 : d);
+                sum += w[size_t(a)];
+            }
+            for (int a = 0; a < n; ++a)
+                s0[size_t(hf_s0_off(n)) + size_t(a) * n + ap] = hit >= 0 ? (a == hit ? 1.0 : 0.0) : w[size_t(a)] / sum;
+        }
+    }
+    VPG_CUDA(cudaMemcpyToSymbol(c_hfS0, s0.data(), sizeof(double) * s0.size()));
+    if (dev < 64) done |= uint64_t(1) << dev;
+}
+
 void build_helm_fmm(Plan& pl) {
+    hf_const_init();
     const int L = pl.L;
     int lmin = 2;
     while (lmin <= L && pl.lambda * (pl.side / double(1 << lmin)) > 5.0) ++lmin;
@@ -1060,6 +1261,14 @@ void build_helm_fmm(Plan& pl) {
     smem_optin((const void*)hf_l2p_p2p_kernel,
                int(size_t(kLogTableBytes) + sizeof(double) * kHfWarps * kHfMaxN * kHfMaxN));
     pl.hf = true;
+    // near-field K0 form: every near pair lies within the 3x3 leaves, |r| <= 3 sqrt(2) s
+    {
+        const double s = pl.side / double(1 << L);
+        pl.hf_k0_qmax = 0.25 * pl.lambda * pl.lambda * 18.0 * s * s;
+        pl.hf_k0_fast = pl.hf_k0_qmax <= 0.25;
+        pl.hf_k0_deg = k0_series_degree(pl.hf_k0_qmax);
+    }
+    build_sym_near(pl, pl.shard_lb, pl.shard_le);
 }
 
 // Half a warp per chunk (cfg5's level-8 leaves hold ~16 targets, so a warp per
@@ -1297,6 +1506,25 @@ void hf_gemm(int M, int N, int K, const double* A, int lda, const double* B, int
         throw Error{VPG_ERR_INVALID_ARGUMENT, "Chebyshev FMM operator too large for the GEMM tile"};
 }
 
+// The K0 pair function of the plan's symmetric near field (K0NearK): the
+// fast series form at the plan's degree when every near pair has
+// lambda r <= 1, else the general form.
+template <class F>
+void hf_with_k0(const Plan& pl, F&& f) {
+    const double l2q = 0.25 * pl.lambda * pl.lambda;
+    const double c0 = 0.5 * std::log(l2q) + 0.57721566490153286061;
+    const double qm = pl.hf_k0_qmax;
+    const double* kt = k0_table_dev();
+    if (!pl.hf_k0_fast) return f(K0NearK<false, 9>{l2q, c0, qm, pl.lambda, kt});
+    switch (pl.hf_k0_deg) {
+        case 5: return f(K0NearK<true, 5>{l2q, c0, qm, pl.lambda, kt});
+        case 6: return f(K0NearK<true, 6>{l2q, c0, qm, pl.lambda, kt});
+        case 7: return f(K0NearK<true, 7>{l2q, c0, qm, pl.lambda, kt});
+        case 8: return f(K0NearK<true, 8>{l2q, c0, qm, pl.lambda, kt});
+        default: return f(K0NearK<true, 9>{l2q, c0, qm, pl.lambda, kt});
+    }
+}
+
 void helm_fmm_apply(const Plan& pl, const double* q_dev, double* out_dev, cudaStream_t st, cudaEvent_t* ev,
                     int64_t& launches) {
     auto mark = [&](int i) {
@@ -1306,7 +1534,9 @@ void helm_fmm_apply(const Plan& pl, const double* q_dev, double* out_dev, cudaSt
     const HfLevels hl = hf_levels(pl);
     const size_t rows = size_t(std::max<int64_t>(pl.hf_rows, 1));
     void* base = nullptr;
-    const size_t bytes = sizeof(double) * (size_t(std::max<int64_t>(pl.ns, 1)) + 2 * rows * n2 + 2 * rows * k);
+    const size_t nsym = pl.sym ? size_t(std::max<int64_t>(pl.sym_nparts, 1)) : 0;
+    const size_t bytes =
+        sizeof(double) * (size_t(std::max<int64_t>(pl.ns, 1)) + 2 * rows * n2 + 2 * rows * k + nsym) + 256;
     VPG_CUDA(cudaMallocAsync(&base, bytes, st));
     struct Free {
         void* p;
@@ -1320,6 +1550,8 @@ void helm_fmm_apply(const Plan& pl, const double* q_dev, double* out_dev, cudaSt
     double* Lv = W + rows * n2;
     double* Wt = Lv + rows * n2;
     double* Lt = Wt + rows * k;
+    double* sym_part = Lt + rows * k;
+    int* ticket = reinterpret_cast<int*>(sym_part + nsym);
     mark(0);
     gather_q_h<<<nblk(pl.ns, 256), 256, 0, st>>>(q_dev, pl.src_ids.p, pl.ns, qs);
     VPG_LAUNCH_CHECK();
@@ -1332,11 +1564,15 @@ void helm_fmm_apply(const Plan& pl, const double* q_dev, double* out_dev, cudaSt
     VPG_LAUNCH_CHECK();
     ++launches;
     mark(2);
-    const int tn2 = ((n2 + 31) / 32) * 32;
     for (int l = L - 1; l >= pl.hf_lmin; --l) {
-        hf_m2m_kernel<<<unsigned(int64_t(1) << (2 * l)), tn2, 0, st>>>(
-            l, n, pl.hf_tab.p + 64, pl.src_cnt.p + lvl_base(l), pl.src_cnt.p + lvl_base(l + 1),
-            pl.hf_row_base[size_t(l)], pl.hf_row_base[size_t(l + 1)], W);
+        const int64_t np = int64_t(1) << (2 * l);
+        hf_dispatch_n(n, [&](auto nc) {
+            constexpr int N = decltype(nc)::value;
+            constexpr int P = hf_m2m_parents(N);
+            hf_m2m_kernel<N><<<unsigned((np + P - 1) / P), 4 * N * P, 0, st>>>(
+                np, pl.src_cnt.p + lvl_base(l), pl.src_cnt.p + lvl_base(l + 1), pl.hf_row_base[size_t(l)],
+                pl.hf_row_base[size_t(l + 1)], W);
+        });
         VPG_LAUNCH_CHECK();
         ++launches;
     }
@@ -1378,18 +1614,43 @@ void helm_fmm_apply(const Plan& pl, const double* q_dev, double* out_dev, cudaSt
     for (int l = pl.hf_lmin + 1; l <= L; ++l) {
         const int64_t t0 = pl.hf_lvl_t0[size_t(l)], t1 = pl.hf_lvl_t0[size_t(l + 1)];
         if (t1 == t0) continue;
-        hf_l2l_kernel<<<unsigned(t1 - t0), tn2, 0, st>>>(hl, l, pl.hf_tbox.p + t0, pl.hf_tab.p + 64, Lv);
+        hf_dispatch_n(n, [&](auto nc) {
+            constexpr int N = decltype(nc)::value;
+            constexpr int P = hf_l2l_boxes(N);
+            hf_l2l_kernel<N><<<unsigned((t1 - t0 + P - 1) / P), N * P, 0, st>>>(
+                t1 - t0, pl.hf_row_base[size_t(l)], pl.hf_row_base[size_t(l - 1)], pl.hf_tbox.p + t0, Lv);
+        });
         VPG_LAUNCH_CHECK();
         ++launches;
     }
     mark(5);
+    // symmetric near field (plan.cuh SymTask): the K0 of each unordered node
+    // pair once, into slot partials; L2P below writes out = far, the
+    // finalize adds the near sums
+    if (pl.sym && pl.n_sym_tasks > 0) {
+        VPG_CUDA(cudaMemsetAsync(ticket, 0, 2 * sizeof(int), st));
+        hf_with_k0(pl, [&](auto kern) {
+            using K = decltype(kern);
+            smem_optin((const void*)p2p_sym_kernel<K>, int(kSymSmem));
+            int per_sm = 1;
+            VPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p2p_sym_kernel<K>, kSymWarps * 32,
+                                                                   kSymSmem));
+            const int64_t want = (pl.n_sym_tasks + kSymWarps - 1) / kSymWarps;
+            const unsigned grid = unsigned(std::min<int64_t>(want, int64_t(pl.sm_count) * std::max(per_sm, 1)));
+            p2p_sym_kernel<K><<<grid, kSymWarps * 32, kSymSmem, st>>>(
+                kern, pl.sym_tasks.p, pl.n_sym_tasks, pl.sym_ranges.p, pl.src_sorted.p, qs, log_table_dev(), ticket,
+                sym_part);
+        });
+        VPG_LAUNCH_CHECK();
+        ++launches;
+    }
     if (pl.n_p2p_chunks > 0) {
         const unsigned grid = unsigned(std::min<int64_t>((pl.n_p2p_chunks + kHfWarps - 1) / kHfWarps,
                                                          int64_t(pl.sm_count) * 8));
 #ifndef VPG_HF_HALF
 #define VPG_HF_HALF 0  // 1: half-warp chunks, slower on cfg5 (K0 near field 2.23 -> 2.98 ms)
 #endif
-        if (VPG_HF_HALF) {  // half a warp per chunk, 32 targets per pass (U = 2)
+        if (VPG_HF_HALF && !pl.sym) {  // half a warp per chunk, 32 targets per pass (U = 2)
             const unsigned grid16 = unsigned(std::min<int64_t>((pl.n_p2p_chunks + 2 * kHfWarps - 1) / (2 * kHfWarps),
                                                                int64_t(pl.sm_count) * 8));
             const size_t smem16 = size_t(kLogTableBytes) + sizeof(double) * 2 * kHfWarps * n2;
@@ -1403,8 +1664,21 @@ void helm_fmm_apply(const Plan& pl, const double* q_dev, double* out_dev, cudaSt
             hf_l2p_p2p_kernel<<<grid, kHfWarps * 32, smem, st>>>(
                 hl, pl.p2p_chunks.p, pl.n_p2p_chunks, pl.near_ranges.p, pl.tgt_row.p, pl.src_sorted.p, qs,
                 pl.tgt_sorted.p, pl.tgt_ids.p, pl.hf_tab.p, Lv, pl.x0, pl.y0, pl.side, pl.lambda,
-                k0_table_dev(), log_table_dev(), out_dev);
+                k0_table_dev(), log_table_dev(), out_dev, pl.sym ? 0 : 1);
         }
+        VPG_LAUNCH_CHECK();
+        ++launches;
+    }
+    if (pl.sym && pl.n_sym_leaves > 0) {
+        hf_with_k0(pl, [&](auto kern) {
+            using K = decltype(kern);
+            smem_optin((const void*)hf_sym_finalize_kernel<K>, kLogTableBytes);
+            const unsigned grid = unsigned(std::min<int64_t>(nblk(pl.n_sym_leaves, kHfFinWarps),
+                                                             int64_t(pl.sm_count) * 3));
+            hf_sym_finalize_kernel<K><<<grid, kHfFinWarps * 32, kLogTableBytes, st>>>(
+                kern, pl.sym_leaves.p, pl.n_sym_leaves, sym_part, pl.near_ranges.p, pl.src_sorted.p, qs,
+                pl.tgt_sorted.p, pl.tgt_ids.p, log_table_dev(), out_dev);
+        });
         VPG_LAUNCH_CHECK();
         ++launches;
     }

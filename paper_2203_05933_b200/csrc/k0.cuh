@@ -14,6 +14,8 @@
 //   exp(-x) underflow (x > ~745) returns 0 like kernel.cpp:158-161.
 #pragma once
 
+#include <cmath>
+
 #include "common.cuh"
 
 namespace vpg {
@@ -66,19 +68,38 @@ __device__ __forceinline__ double k0_small_q(double q) {
     return -(0.5 * log(q) + kGamma) * i0 + s;
 }
 
-// Degree-9 truncations of the two series for q <= 1/4 (the dropped tail is
-// below q^10 / (10!)^2 ~ 7e-20 relative).
-__device__ __forceinline__ double k0_i0_9(double q) {
-    double v = c_k0_i0[9];
+// Degree-D truncations of the two series; D = 9 for q <= 1/4 (the dropped
+// tail is below q^10 / (10!)^2 ~ 7e-20 relative), lower when the plan bounds
+// q further (k0_series_degree).
+template <int D>
+__device__ __forceinline__ double k0_i0_d(double q) {
+    double v = c_k0_i0[D];
 #pragma unroll
-    for (int k = 8; k >= 0; --k) v = fma(v, q, c_k0_i0[k]);
+    for (int k = D - 1; k >= 0; --k) v = fma(v, q, c_k0_i0[k]);
     return v;
 }
-__device__ __forceinline__ double k0_h_9(double q) {
-    double v = c_k0_h[9];
+template <int D>
+__device__ __forceinline__ double k0_h_d(double q) {
+    double v = c_k0_h[D];
 #pragma unroll
-    for (int k = 8; k >= 0; --k) v = fma(v, q, c_k0_h[k]);
+    for (int k = D - 1; k >= 0; --k) v = fma(v, q, c_k0_h[k]);
     return v;
+}
+__device__ __forceinline__ double k0_i0_9(double q) { return k0_i0_d<9>(q); }
+__device__ __forceinline__ double k0_h_9(double q) { return k0_h_d<9>(q); }
+
+// Smallest degree D in [5, 9] whose dropped tail at q <= qmax stays below
+// 1e-17 of K0 there (K0 >= K0(1) = 0.42 for q <= 1/4; |ln(x/2) + gamma| <= 2).
+inline int k0_series_degree(double qmax) {
+    static const double i0[11] = {1.0, 1.0, 0.25, 0.027777777777777776, 0.001736111111111111,
+                                  6.944444444444444e-05, 1.9290123456790124e-06, 3.936759889140842e-08,
+                                  6.151187326782565e-10, 7.594058428126624e-12, 7.594058428126623e-14};
+    static const double h[11] = {0.0, 1.0, 0.375, 0.05092592592592592, 0.003616898148148148,
+                                 0.0001585648148148148, 4.72608024691358e-06, 1.0207455998272325e-07,
+                                 1.6718048413148328e-09, 2.1483350211950277e-11, 2.224275605476294e-13};
+    for (int d = 5; d < 9; ++d)
+        if (std::pow(qmax, d + 1) * (2.0 * i0[d + 1] + h[d + 1]) <= 4e-18) return d;
+    return 9;
 }
 
 __device__ __forceinline__ double k0_large(double x, const double* tab) {

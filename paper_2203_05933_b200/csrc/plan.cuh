@@ -80,7 +80,7 @@ struct P2PChunk {
 };
 constexpr int kMaxNearRanges = 64;
 
-// Symmetric near field (uniform Laplace trees whose first ns targets are the
+// Symmetric near field (uniform Laplace or Chebyshev-FMM Helmholtz trees whose first ns targets are the
 // sources, the volume-potential case "targets = nodes"): every unordered pair
 // of near points is evaluated ONCE -- log r^2 feeds target i (with q_j) and
 // target j (with q_i).  Leaf A owns the pairs {A, B} with its neighbours B
@@ -281,6 +281,9 @@ struct Plan {
     // hf_lmin..L, M2L through a rank-k SVD basis per level.
     bool hf = false;
     int hf_n = 0, hf_k = 0, hf_lmin = 0;
+    bool hf_k0_fast = false;   // near-field K0 by the series (every near pair has lambda r <= 1)
+    int hf_k0_deg = 9;         // series degree of that form (k0_series_degree)
+    double hf_k0_qmax = 0.25;  // bound of q = (lambda r / 2)^2 over the near pairs
     DBuf<double> hf_tab;            // nodes[n], bw[n], S[2][n][n]
     DBuf<double> hf_Vt, hf_Vc;      // per level: V as [n2][k] (row-major) and [k][n2]
     DBuf<double> hf_C;              // per level and offset: C [k][k], C[j*k + i] = C_ij

@@ -665,7 +665,7 @@ void build_schedules(Plan& pl, int64_t lb, int64_t le) {
         }
         pl.shard_m2l = m2l;
     }
-    if (pl.coin_ready) build_sym_near(pl, lb, le);
+    if (pl.coin_ready || pl.hf) build_sym_near(pl, lb, le);  // Laplace ops / Chebyshev FMM built
 }
 
 // The symmetric near-field schedule (SymTask, plan.cuh) for the targets of
@@ -675,12 +675,13 @@ void build_schedules(Plan& pl, int64_t lb, int64_t le) {
 // leaf's first n_src targets) one-sided.  Taken when the first ns
 // targets are the sources (so leaf A's first n_src sorted targets are its
 // sorted sources, both sorts being stable), the tree is uniform, the
-// kernel Laplace and no leaf holds more than kSymMaxN sources.
+// kernel Laplace (or modified Helmholtz with the Chebyshev FMM: every pair
+// symmetric, no hybrid) and no leaf holds more than kSymMaxN sources.
 void build_sym_near(Plan& pl, int64_t lb, int64_t le) {
     pl.sym = false;
     const char* fv = std::getenv("VPG_SYM");  // 0: never, 1: always (when applicable), unset: by cost
     const int force = fv ? std::atoi(fv) : -1;
-    if (force == 0 || !pl.matched || pl.adaptive || pl.direct || pl.family != VPG_LAPLACE) return;
+    if (force == 0 || !pl.matched || pl.adaptive || pl.direct || (pl.family != VPG_LAPLACE && !pl.hf)) return;
     const int L = pl.L;
     const int nb = 1 << L;
     const int64_t nleaf = int64_t(1) << (2 * L);
@@ -733,7 +734,8 @@ void build_sym_near(Plan& pl, int64_t lb, int64_t le) {
         // with 82% / 79% / 54% of the pairs symmetric), so it is opt-in only.
         (void)big_pairs;
         (void)all_pairs;
-        if (tmin >= 0) pl.sym_min = tmin;
+        if (pl.family != VPG_LAPLACE) pl.sym_min = 0;  // K0 pairs (~40 FP64 instructions) dwarf the tile overheads
+        else if (tmin >= 0) pl.sym_min = tmin;
         else if (cost_sym < 0.6 * cost_one) pl.sym_min = 0;
         else pl.sym_min = -1;
         // subtasks of about half one warp's fair share (16 warps per SM)

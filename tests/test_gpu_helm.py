@@ -74,3 +74,28 @@ def test_native_helmholtz_random_clusters(vp, rest):
     idx = np.random.default_rng(5).choice(len(tgt), 1500, replace=False)
     ld = rest.pairwise_ld(1, 4.0, src, q, tgt[idx])
     assert rel_l2(gpu[idx], ld) <= 1e-12
+
+
+def test_native_helmholtz_symmetric_near_field(vp, rest, monkeypatch):
+    """The Chebyshev FMM's near field by unordered node pairs (sym.cuh with
+    the K0 pair function, hf_sym_finalize_kernel) against the one-sided
+    kernel (VPG_SYM=0) and long-double direct sums; 3,000 extra targets that
+    are not nodes take the finalize's one-sided branch."""
+    w = W.cfg5(n_side=96, ntri=1000)
+    src, q = w.src, w.q
+    extra = np.random.default_rng(8).uniform(src.min(0), src.max(0), (3000, 2))
+    tgt = np.concatenate([src, extra])
+    with vp.SummationPlan(mh(vp), src, tgt, 1e-12, mode="native") as plan:
+        assert plan.info()["near_symmetric"] == 1
+        sym = plan.apply(q)
+        assert np.array_equal(sym, plan.apply(q))
+    monkeypatch.setenv("VPG_SYM", "0")
+    with vp.SummationPlan(mh(vp), src, tgt, 1e-12, mode="native") as plan:
+        assert plan.info()["near_symmetric"] == 0
+        one = plan.apply(q)
+    assert rel_l2(sym, one) <= 1e-14
+    idx = np.concatenate([np.random.default_rng(9).choice(len(src), 1000, replace=False),
+                          len(src) + np.arange(500)])
+    ld = rest.pairwise_ld(1, 10.0, src, q, tgt[idx])
+    assert rel_l2(sym[idx], ld) <= 1e-12
+    assert rel_l2(sym[len(src):len(src) + 500], ld[1000:]) <= 1e-12
