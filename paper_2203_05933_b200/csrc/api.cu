@@ -238,8 +238,8 @@ bool plan_is_sharded(const Plan& pl) {
     return pl.shard_lb != 0 || pl.shard_le != (int64_t(1) << (2 * pl.L));
 }
 
-// Captures laplace_issue for e's pointers; nullptr when capture is not
-// supported here (the caller falls back to plain launches).
+// Captures laplace_issue (or helm_fmm_issue) for e's pointers; nullptr when
+// capture is not supported here (the caller falls back to plain launches).
 static cudaGraph_t capture_apply(const Plan& pl, GraphEntry& e) {
     const double* qd = e.host ? e.qstage : e.q;
     double* od = e.host ? e.ostage : e.out;
@@ -282,8 +282,12 @@ static cudaGraph_t capture_apply(const Plan& pl, GraphEntry& e) {
             return v && v[0] == '1';
         }();
         int64_t launches = 0;
-        laplace_issue(pl, qd, od, laplace_work_at(pl, e.work), cap, nullptr, launches,
-                      no_fork ? nullptr : side, fork, join, far_done);
+        if (pl.family == VPG_LAPLACE)
+            laplace_issue(pl, qd, od, laplace_work_at(pl, e.work), cap, nullptr, launches,
+                          no_fork ? nullptr : side, fork, join, far_done);
+        else
+            helm_fmm_issue(pl, qd, od, e.work, cap, nullptr, launches, no_fork ? nullptr : side, fork, join,
+                           far_done);
         e.launches = launches;
     } catch (...) {
         cudaStreamEndCapture(cap, &g);
@@ -337,7 +341,7 @@ GraphEntry* graph_entry(const Plan& pl, const double* q, double* out, bool host)
     e->q = q;
     e->out = out;
     e->host = host;
-    VPG_CUDA(cudaMalloc(&e->work, laplace_work_bytes(pl)));
+    VPG_CUDA(cudaMalloc(&e->work, pl.family == VPG_LAPLACE ? laplace_work_bytes(pl) : helm_work_bytes(pl)));
     if (host) {
         VPG_CUDA(cudaMalloc(&e->qstage, sizeof(double) * size_t(std::max<int64_t>(pl.ns, 1))));
         VPG_CUDA(cudaMalloc(&e->ostage, sizeof(double) * size_t(std::max<int64_t>(pl.nt, 1))));
@@ -453,7 +457,7 @@ int vpg_plan_apply(const vpg_plan* plan, const double* q, int64_t nq, double* ou
         CallStream cs(stream);
         cudaStream_t st = cs.s;
         const bool dev = flags & VPG_DEVICE_POINTERS;
-        if (!pl.direct && pl.family == VPG_LAPLACE && !pl.profiling && graphs_enabled()) {
+        if (!pl.direct && (pl.family == VPG_LAPLACE || pl.hf) && !pl.profiling && graphs_enabled()) {
             std::unique_lock<std::mutex> lk(pl.graph_mu);
             // host pointers: two staged graphs used in turn, so applies issued on
             // two streams overlap one's copies with the other's kernels

@@ -1525,19 +1525,49 @@ void hf_with_k0(const Plan& pl, F&& f) {
     }
 }
 
+// Per-apply scratch of the Chebyshev FMM, carved from one block: sorted
+// charges, W / Lv rows (n^2 each), Wt / Lt rows (k each), the split-M2L
+// partials, the symmetric near field's slot partials and its ticket.
+namespace {
+size_t hf_al(size_t b) { return (b + 255) & ~size_t(255); }
+struct HfWork {
+    double *qs, *W, *Lv, *Wt, *Lt, *Lpart, *sym_part;
+    int* ticket;
+};
+HfWork hf_work_at(const Plan& pl, void* base, size_t* total) {
+    const size_t rows = size_t(std::max<int64_t>(pl.hf_rows, 1));
+    const size_t n2 = size_t(pl.hf_n) * pl.hf_n, k = size_t(pl.hf_k);
+    char* p = static_cast<char*>(base);
+    size_t used = 0;
+    auto take = [&](size_t bytes) {
+        char* r = p ? p + used : nullptr;
+        used += hf_al(bytes);
+        return r;
+    };
+    HfWork w;
+    w.qs = reinterpret_cast<double*>(take(sizeof(double) * size_t(std::max<int64_t>(pl.ns, 1))));
+    w.W = reinterpret_cast<double*>(take(sizeof(double) * rows * n2));
+    w.Lv = reinterpret_cast<double*>(take(sizeof(double) * rows * n2));
+    w.Wt = reinterpret_cast<double*>(take(sizeof(double) * rows * k));
+    w.Lt = reinterpret_cast<double*>(take(sizeof(double) * rows * k));
+    w.Lpart = reinterpret_cast<double*>(take(sizeof(double) * size_t(std::max<int64_t>(pl.hf_nparts, 1)) * kHfMaxK));
+    w.sym_part = reinterpret_cast<double*>(take(sizeof(double) * size_t(pl.sym ? std::max<int64_t>(pl.sym_nparts, 1) : 1)));
+    w.ticket = reinterpret_cast<int*>(take(sizeof(int) * 32));
+    if (total) *total = used;
+    return w;
+}
+}  // namespace
+
+size_t helm_work_bytes(const Plan& pl) {
+    size_t total = 0;
+    (void)hf_work_at(pl, nullptr, &total);
+    return total;
+}
+
 void helm_fmm_apply(const Plan& pl, const double* q_dev, double* out_dev, cudaStream_t st, cudaEvent_t* ev,
                     int64_t& launches) {
-    auto mark = [&](int i) {
-        if (ev) VPG_CUDA(cudaEventRecord(ev[i], st));
-    };
-    const int L = pl.L, n = pl.hf_n, n2 = n * n, k = pl.hf_k;
-    const HfLevels hl = hf_levels(pl);
-    const size_t rows = size_t(std::max<int64_t>(pl.hf_rows, 1));
     void* base = nullptr;
-    const size_t nsym = pl.sym ? size_t(std::max<int64_t>(pl.sym_nparts, 1)) : 0;
-    const size_t bytes =
-        sizeof(double) * (size_t(std::max<int64_t>(pl.ns, 1)) + 2 * rows * n2 + 2 * rows * k + nsym) + 256;
-    VPG_CUDA(cudaMallocAsync(&base, bytes, st));
+    VPG_CUDA(cudaMallocAsync(&base, helm_work_bytes(pl), st));
     struct Free {
         void* p;
         cudaStream_t s;
@@ -1545,17 +1575,72 @@ void helm_fmm_apply(const Plan& pl, const double* q_dev, double* out_dev, cudaSt
             if (p) cudaFreeAsync(p, s);
         }
     } fr{base, st};
-    double* qs = static_cast<double*>(base);
-    double* W = qs + std::max<int64_t>(pl.ns, 1);
-    double* Lv = W + rows * n2;
-    double* Wt = Lv + rows * n2;
-    double* Lt = Wt + rows * k;
-    double* sym_part = Lt + rows * k;
-    int* ticket = reinterpret_cast<int*>(sym_part + nsym);
+    helm_fmm_issue(pl, q_dev, out_dev, base, st, ev, launches, nullptr, nullptr, nullptr, nullptr);
+}
+
+// The kernels of one Chebyshev-FMM apply in stream order on a given
+// workspace (no allocation: capturable into a CUDA graph).  With a side
+// stream the symmetric near field runs concurrently with the far-field
+// chain; L2P writes out = far on the main stream and the finalize (side)
+// adds the near sums after it.
+void helm_fmm_issue(const Plan& pl, const double* q_dev, double* out_dev, void* work, cudaStream_t st,
+                    cudaEvent_t* ev, int64_t& launches, cudaStream_t side, cudaEvent_t fork, cudaEvent_t join,
+                    cudaEvent_t far_done) {
+    auto mark = [&](int i) {
+        if (ev) VPG_CUDA(cudaEventRecord(ev[i], st));
+    };
+    const int L = pl.L, n = pl.hf_n, n2 = n * n, k = pl.hf_k;
+    const HfLevels hl = hf_levels(pl);
+    const HfWork w = hf_work_at(pl, work, nullptr);
+    double* qs = w.qs;
+    double* W = w.W;
+    double* Lv = w.Lv;
+    double* Wt = w.Wt;
+    double* Lt = w.Lt;
+    double* sym_part = w.sym_part;
+    int* ticket = w.ticket;
+    const bool sym_side = side && pl.sym;
+    auto sym_sweep = [&](cudaStream_t s) {
+        if (!pl.sym || pl.n_sym_tasks == 0) return;
+        VPG_CUDA(cudaMemsetAsync(ticket, 0, 2 * sizeof(int), s));
+        hf_with_k0(pl, [&](auto kern) {
+            using K = decltype(kern);
+            smem_optin((const void*)p2p_sym_kernel<K>, int(kSymSmem));
+            int per_sm = 1;
+            VPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p2p_sym_kernel<K>, kSymWarps * 32,
+                                                                   kSymSmem));
+            const int64_t want = (pl.n_sym_tasks + kSymWarps - 1) / kSymWarps;
+            const unsigned grid = unsigned(std::min<int64_t>(want, int64_t(pl.sm_count) * std::max(per_sm, 1)));
+            p2p_sym_kernel<K><<<grid, kSymWarps * 32, kSymSmem, s>>>(kern, pl.sym_tasks.p, pl.n_sym_tasks,
+                                                                     pl.sym_ranges.p, pl.src_sorted.p, qs,
+                                                                     log_table_dev(), ticket, sym_part);
+        });
+        VPG_LAUNCH_CHECK();
+        ++launches;
+    };
+    auto sym_finalize = [&](cudaStream_t s) {
+        if (!pl.sym || pl.n_sym_leaves == 0) return;
+        hf_with_k0(pl, [&](auto kern) {
+            using K = decltype(kern);
+            smem_optin((const void*)hf_sym_finalize_kernel<K>, kLogTableBytes);
+            const unsigned grid = unsigned(std::min<int64_t>(nblk(pl.n_sym_leaves, kHfFinWarps),
+                                                             int64_t(pl.sm_count) * 3));
+            hf_sym_finalize_kernel<K><<<grid, kHfFinWarps * 32, kLogTableBytes, s>>>(
+                kern, pl.sym_leaves.p, pl.n_sym_leaves, sym_part, pl.near_ranges.p, pl.src_sorted.p, qs,
+                pl.tgt_sorted.p, pl.tgt_ids.p, log_table_dev(), out_dev);
+        });
+        VPG_LAUNCH_CHECK();
+        ++launches;
+    };
     mark(0);
     gather_q_h<<<nblk(pl.ns, 256), 256, 0, st>>>(q_dev, pl.src_ids.p, pl.ns, qs);
     VPG_LAUNCH_CHECK();
     ++launches;
+    if (sym_side) {
+        VPG_CUDA(cudaEventRecord(fork, st));
+        VPG_CUDA(cudaStreamWaitEvent(side, fork, 0));
+        sym_sweep(side);
+    }
     mark(1);
     // P2M at the leaves (warp per leaf)
     hf_anterp_leaf_kernel<<<unsigned(((int64_t(1) << (2 * L)) + kAntWarps - 1) / kAntWarps), kAntWarps * 32, 0, st>>>(
@@ -1586,9 +1671,7 @@ void helm_fmm_apply(const Plan& pl, const double* q_dev, double* out_dev, cudaSt
     }
     mark(3);
     if (pl.hf_ntbox > 0) {
-        double* Lpart = nullptr;
-        if (pl.hf_nparts > 0)
-            VPG_CUDA(cudaMallocAsync(&Lpart, sizeof(double) * size_t(pl.hf_nparts) * kHfMaxK, st));
+        double* Lpart = w.Lpart;
         hf_m2l_tc_kernel<<<unsigned(pl.hf_ntiles), 256, sizeof(double) * kHfMaxK * (kHfMaxK + kHfTile + 8), st>>>(
             pl.hf_tiles.p, pl.hf_tbox.p, pl.hf_srcof.p, pl.hf_C.p, Wt, Lt, Lpart);
         VPG_LAUNCH_CHECK();
@@ -1597,7 +1680,6 @@ void helm_fmm_apply(const Plan& pl, const double* q_dev, double* out_dev, cudaSt
             hf_m2l_reduce_kernel<<<unsigned(pl.hf_nsplit), kHfMaxK, 0, st>>>(pl.hf_splits.p, pl.hf_split_parts,
                                                                             Lpart, Lt);
         }
-        if (Lpart) VPG_CUDA(cudaFreeAsync(Lpart, st));
         VPG_LAUNCH_CHECK();
         ++launches;
     }
@@ -1627,23 +1709,7 @@ void helm_fmm_apply(const Plan& pl, const double* q_dev, double* out_dev, cudaSt
     // symmetric near field (plan.cuh SymTask): the K0 of each unordered node
     // pair once, into slot partials; L2P below writes out = far, the
     // finalize adds the near sums
-    if (pl.sym && pl.n_sym_tasks > 0) {
-        VPG_CUDA(cudaMemsetAsync(ticket, 0, 2 * sizeof(int), st));
-        hf_with_k0(pl, [&](auto kern) {
-            using K = decltype(kern);
-            smem_optin((const void*)p2p_sym_kernel<K>, int(kSymSmem));
-            int per_sm = 1;
-            VPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p2p_sym_kernel<K>, kSymWarps * 32,
-                                                                   kSymSmem));
-            const int64_t want = (pl.n_sym_tasks + kSymWarps - 1) / kSymWarps;
-            const unsigned grid = unsigned(std::min<int64_t>(want, int64_t(pl.sm_count) * std::max(per_sm, 1)));
-            p2p_sym_kernel<K><<<grid, kSymWarps * 32, kSymSmem, st>>>(
-                kern, pl.sym_tasks.p, pl.n_sym_tasks, pl.sym_ranges.p, pl.src_sorted.p, qs, log_table_dev(), ticket,
-                sym_part);
-        });
-        VPG_LAUNCH_CHECK();
-        ++launches;
-    }
+    if (!sym_side) sym_sweep(st);
     if (pl.n_p2p_chunks > 0) {
         const unsigned grid = unsigned(std::min<int64_t>((pl.n_p2p_chunks + kHfWarps - 1) / kHfWarps,
                                                          int64_t(pl.sm_count) * 8));
@@ -1669,18 +1735,14 @@ void helm_fmm_apply(const Plan& pl, const double* q_dev, double* out_dev, cudaSt
         VPG_LAUNCH_CHECK();
         ++launches;
     }
-    if (pl.sym && pl.n_sym_leaves > 0) {
-        hf_with_k0(pl, [&](auto kern) {
-            using K = decltype(kern);
-            smem_optin((const void*)hf_sym_finalize_kernel<K>, kLogTableBytes);
-            const unsigned grid = unsigned(std::min<int64_t>(nblk(pl.n_sym_leaves, kHfFinWarps),
-                                                             int64_t(pl.sm_count) * 3));
-            hf_sym_finalize_kernel<K><<<grid, kHfFinWarps * 32, kLogTableBytes, st>>>(
-                kern, pl.sym_leaves.p, pl.n_sym_leaves, sym_part, pl.near_ranges.p, pl.src_sorted.p, qs,
-                pl.tgt_sorted.p, pl.tgt_ids.p, log_table_dev(), out_dev);
-        });
-        VPG_LAUNCH_CHECK();
-        ++launches;
+    if (sym_side) {
+        VPG_CUDA(cudaEventRecord(far_done, st));
+        VPG_CUDA(cudaStreamWaitEvent(side, far_done, 0));
+        sym_finalize(side);
+        VPG_CUDA(cudaEventRecord(join, side));
+        VPG_CUDA(cudaStreamWaitEvent(st, join, 0));
+    } else {
+        sym_finalize(st);
     }
     mark(6);
 }

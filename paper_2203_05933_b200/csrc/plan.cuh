@@ -369,6 +369,10 @@ void direct_sum_device(int family, double lambda, const double2* src,
 // helm.cu
 void build_helm_ops(Plan& pl);
 void build_helm_fmm(Plan& pl);  // native mode (helm.cu)
+size_t helm_work_bytes(const Plan& pl);  // Chebyshev FMM apply scratch (helm.cu)
+void helm_fmm_issue(const Plan& pl, const double* q_dev, double* out_dev, void* work, cudaStream_t st,
+                    cudaEvent_t* ev, int64_t& launches, cudaStream_t side, cudaEvent_t fork, cudaEvent_t join,
+                    cudaEvent_t far_done);
 void helm_apply(const Plan& pl, const double* q_dev, double* out_dev,
                 cudaStream_t st, cudaEvent_t* ev, int64_t& launches);
 void k0_device(const double* x, int64_t n, double* out, cudaStream_t st);

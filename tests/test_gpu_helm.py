@@ -99,3 +99,44 @@ def test_native_helmholtz_symmetric_near_field(vp, rest, monkeypatch):
     ld = rest.pairwise_ld(1, 10.0, src, q, tgt[idx])
     assert rel_l2(sym[idx], ld) <= 1e-12
     assert rel_l2(sym[len(src):len(src) + 500], ld[1000:]) <= 1e-12
+
+
+def test_native_helmholtz_graph_paths_agree(vp):
+    """Chebyshev-FMM applies are replayed from CUDA graphs (near field on a
+    concurrent branch): device-pointer pairs, host-pointer applies, the
+    profiled plain-launch path and applies from several host threads all give
+    bit-identical potentials."""
+    import threading
+    torch = pytest.importorskip("torch")
+    w = W.cfg5(n_side=96, ntri=1000)
+    src, q = w.src, w.q
+    with vp.SummationPlan(mh(vp), src, src, 1e-12, mode="native") as plan:
+        plan.set_profiling(True)
+        ref = plan.apply(q)
+        plan.set_profiling(False)
+        assert np.array_equal(plan.apply(q), ref)
+        s = torch.cuda.current_stream()
+        qd = torch.tensor(q, device="cuda")
+        outs = [torch.empty(len(src), dtype=torch.float64, device="cuda") for _ in range(5)]
+        for o in outs:
+            o.fill_(float("nan"))
+            plan.apply_device(qd.data_ptr(), o.data_ptr(), s.cuda_stream)
+        torch.cuda.synchronize()
+        for o in outs:
+            assert np.array_equal(o.cpu().numpy(), ref)
+        rng = np.random.default_rng(12)
+        qs = [rng.standard_normal(len(src)) for _ in range(4)]
+        want = [plan.apply(x) for x in qs]
+        got = [None] * len(qs)
+
+        def run(i):
+            for _ in range(2):
+                got[i] = plan.apply(qs[i])
+
+        th = [threading.Thread(target=run, args=(i,)) for i in range(len(qs))]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+    for a, b in zip(got, want):
+        assert np.array_equal(a, b)
