@@ -212,6 +212,28 @@ __device__ __forceinline__ double fast_log(double x, uint32_t tab_lane) {
 }
 static_assert(kLogTableBits == 9 && kLogTableCopies == 8, "fast_log assumes the 9-bit, 8-copy layout");
 
+// fast_log with the table read from global memory (lap_log_table_dev, one
+// copy): the same arithmetic on the same table values, so it returns the
+// same bits as the smem form -- for rare paths (coincidence fix-ups) in
+// kernels that do not stage the 66 KB table.
+__device__ __forceinline__ double fast_log(double x, const double2* gtab) {
+    constexpr int kHalf = 1 << (19 - kLogTableBits);
+    const int hi = __double2hiint(x);
+    const int lo = __double2loint(x);
+    const double g = __int2double_rn(((hi + kHalf) >> 11) - (0x3FF << 9));
+    int mhi;
+    asm("lop3.b32 %0, %1, 0x000FFFFF, %2, 0xEA;" : "=r"(mhi) : "r"(hi), "r"(0x3FF00000));
+    const uint32_t idx = (uint32_t(mhi + kHalf) >> 11) - uint32_t(0x3FF << kLogTableBits);
+    const double m = __hiloint2double(mhi, lo);
+    const double2 tc = __ldg(gtab + idx);
+    const double r = fma(m, tc.x, -1.0);
+    const double w = fma(g, c_flog[1], tc.y);
+    double p = fma(r, c_flog[2], c_flog[0]);
+    p = fma(r, p, -0.5);
+    p = fma(r, p, c_flog[3]);
+    return fma(r, p, w);
+}
+
 // ----------------------------------------------- programmatic launches --
 // Kernels of one apply are chained with programmatic dependent launch: the
 // next grid may start (and stage its constant operators / tables) while the

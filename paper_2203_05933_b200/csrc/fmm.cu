@@ -960,9 +960,10 @@ __device__ __forceinline__ void near_range(const NearList& nl, int f0, int f1, i
 // The coincidence correction of one target (sorted index ti): the listed
 // pairs undone and redone with the reference rule (lap_pair_fixup), as a
 // separate sum added to the target's total.
+template <class Tab>
 __device__ __forceinline__ double coin_correction(const int32_t* coin_off, const int32_t* coin_src,
                                                   int64_t ti, double tx, double ty, const double2* sxy,
-                                                  const double* q, uint32_t tab_lane) {
+                                                  const double* q, Tab tab_lane) {
     const int k0 = coin_off[ti], k1 = coin_off[ti + 1];
     if (k0 == k1) return 0.0;
     LapAcc fix;
@@ -1097,6 +1098,11 @@ constexpr size_t kFinScratch = size_t(kFinWarps) * 2 * kMaxNearRanges * sizeof(i
                                    ? size_t(kFinWarps) * 2 * kMaxNearRanges * sizeof(int)
                                    : size_t(kLogTableSize) * 16;  // range slots, or the table's staging copy
 constexpr size_t kFinSmem = size_t(kLogTableBytes) + kFinScratch;
+// kTable = false (no unmatched targets, or the hybrid form): no smem table;
+// the coincidence fix-ups read the global table (same bits), so the kernel
+// runs at full occupancy -- the slot sums are latency-bound loads, and the
+// kernel sits on the step's tail.
+template <bool kTable>
 __global__ void __launch_bounds__(kFinWarps * 32)
 sym_finalize_kernel(const SymLeaf* leaves, int64_t nleaves, const double* part, const int2* ranges,
                     const double2* sxy, const double* q, const double2* txy, const int32_t* tids,
@@ -1104,18 +1110,19 @@ sym_finalize_kernel(const SymLeaf* leaves, int64_t nleaves, const double* part, 
     extern __shared__ double2 smp[];
     double2* tab = smp;
     int* rbuf = reinterpret_cast<int*>(smp + kLogTableSize * kLogTableCopies);  // [warps][2][64]
-    __shared__ __align__(8) uint64_t bar;
-    if (threadIdx.x == 0) mbar_init(&bar, 1);
-    __syncthreads();
-    bulk_stage(rbuf, gtab, uint32_t(kLogTableSize) * 16u, &bar, 0);
-    log_table_to_smem(tab, reinterpret_cast<const double2*>(rbuf));
+    uint32_t tab_lane = 0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if constexpr (kTable) {
+        __shared__ __align__(8) uint64_t bar;
+        if (threadIdx.x == 0) mbar_init(&bar, 1);
+        __syncthreads();
+        bulk_stage(rbuf, gtab, uint32_t(kLogTableSize) * 16u, &bar, 0);
+        log_table_to_smem(tab, reinterpret_cast<const double2*>(rbuf));
+        tab_lane = log_table_lane_addr(tab, lane & (kLogTableCopies - 1));
+    }
     pdl_trigger();
     pdl_wait();
-    __syncthreads();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t tab_lane = log_table_lane_addr(tab, lane & (kLogTableCopies - 1));
-    int* pre_s = rbuf + warp * 2 * kMaxNearRanges;
-    int* st_s = pre_s + kMaxNearRanges;
+    if constexpr (kTable) __syncthreads();
     for (int64_t w = int64_t(blockIdx.x) * kFinWarps + warp; w < nleaves; w += int64_t(gridDim.x) * kFinWarps) {
         const SymLeaf lf = leaves[w];
         for (int k = lane; k < lf.n; k += 32) {
@@ -1123,13 +1130,20 @@ sym_finalize_kernel(const SymLeaf* leaves, int64_t nleaves, const double* part, 
             const double* pk = part + lf.pbase + k;
             double sum = 0.0;
             int sl = 0;
-            for (; sl + 4 <= lf.nslot; sl += 4) {  // four loads in flight, added in slot order
-                const double a0 = __ldcg(pk + int64_t(sl) * lf.n), a1 = __ldcg(pk + int64_t(sl + 1) * lf.n);
-                const double a2 = __ldcg(pk + int64_t(sl + 2) * lf.n), a3 = __ldcg(pk + int64_t(sl + 3) * lf.n);
-                sum += a0;
-                sum += a1;
-                sum += a2;
-                sum += a3;
+            for (; sl + 8 <= lf.nslot; sl += 8) {  // eight loads in flight, added in slot order
+                double a[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) a[u] = __ldcg(pk + int64_t(sl + u) * lf.n);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) sum += a[u];
+            }
+            if (sl + 4 <= lf.nslot) {
+                double a[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) a[u] = __ldcg(pk + int64_t(sl + u) * lf.n);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) sum += a[u];
+                sl += 4;
             }
             for (; sl < lf.nslot; ++sl) sum += __ldcg(pk + int64_t(sl) * lf.n);
             if (add == 1) {  // hybrid: the one-sided kernel wrote this target (coincidences included)
@@ -1137,32 +1151,37 @@ sym_finalize_kernel(const SymLeaf* leaves, int64_t nleaves, const double* part, 
                 continue;
             }
             const double2 tp = txy[t];
-            sum += coin_correction(coin_off, coin_src, t, tp.x, tp.y, sxy, q, tab_lane);
+            if constexpr (kTable) sum += coin_correction(coin_off, coin_src, t, tp.x, tp.y, sxy, q, tab_lane);
+            else sum += coin_correction(coin_off, coin_src, t, tp.x, tp.y, sxy, q, gtab);
             double& o = out[tids[t]];
             o = add == 2 ? o + -kInv4Pi * sum : -kInv4Pi * sum;  // 2: the far field is already there
         }
-        if (add == 1 || lf.tgt + lf.n >= lf.t1) continue;
-        const NearList nl = near_list(ranges, lf.rfirst, lf.rcount, 0, lane, pre_s, st_s);
-        for (int t = lf.tgt + lf.n; t < lf.t1; ++t) {
-            const double2 tp = txy[t];
-            LapAcc acc;
-            for (int ff = lane; ff < nl.total; ff += 32) {
-                int lo = 0, hi = nl.nr - 1;
-                while (lo < hi) {
-                    const int mid = (lo + hi + 1) >> 1;
-                    if (nl.pre[mid] <= ff) lo = mid; else hi = mid - 1;
+        if constexpr (kTable) {
+            if (add == 1 || lf.tgt + lf.n >= lf.t1) continue;
+            int* pre_s = rbuf + warp * 2 * kMaxNearRanges;
+            int* st_s = pre_s + kMaxNearRanges;
+            const NearList nl = near_list(ranges, lf.rfirst, lf.rcount, 0, lane, pre_s, st_s);
+            for (int t = lf.tgt + lf.n; t < lf.t1; ++t) {
+                const double2 tp = txy[t];
+                LapAcc acc;
+                for (int ff = lane; ff < nl.total; ff += 32) {
+                    int lo = 0, hi = nl.nr - 1;
+                    while (lo < hi) {
+                        const int mid = (lo + hi + 1) >> 1;
+                        if (nl.pre[mid] <= ff) lo = mid; else hi = mid - 1;
+                    }
+                    const int src = nl.st[lo] + (ff - nl.pre[lo]);
+                    const double2 sp = sxy[src];
+                    lap_pair_fast(tp.x, tp.y, sp.x, sp.y, q[src], tab_lane, acc);
                 }
-                const int src = nl.st[lo] + (ff - nl.pre[lo]);
-                const double2 sp = sxy[src];
-                lap_pair_fast(tp.x, tp.y, sp.x, sp.y, q[src], tab_lane, acc);
-            }
-            double v = lap_total(acc);
+                double v = lap_total(acc);
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            if (lane == 0) {
-                v += coin_correction(coin_off, coin_src, t, tp.x, tp.y, sxy, q, tab_lane);
-                double& o = out[tids[t]];
-                o = add == 2 ? o + -kInv4Pi * v : -kInv4Pi * v;
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0) {
+                    v += coin_correction(coin_off, coin_src, t, tp.x, tp.y, sxy, q, tab_lane);
+                    double& o = out[tids[t]];
+                    o = add == 2 ? o + -kInv4Pi * v : -kInv4Pi * v;
+                }
             }
         }
     }
@@ -1543,7 +1562,7 @@ void build_laplace_ops(Plan& pl) {
     }
     smem_optin((const void*)l2p_p2p_kernel, kLogTableBytes + 32 * 1024);
     smem_optin((const void*)p2p_sym_kernel<LapLogK>, int(kSymSmem));
-    smem_optin((const void*)sym_finalize_kernel, int(kFinSmem));
+    smem_optin((const void*)sym_finalize_kernel<true>, int(kFinSmem));
     build_coincidences(pl);
     pl.coin_ready = true;
     if (!pl.adaptive) build_sym_near(pl, pl.shard_lb, pl.shard_le);
@@ -1661,9 +1680,15 @@ void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const L
     // the same bits as near + far)
     const bool far_first = side && far_done && pl.sym && !pl.sym_hybrid && pl.n_sym_leaves > 0;
     auto sym_finalize = [&](cudaStream_t s, int mode) {
+        // the table variant only for unmatched targets summed one-sided here
+        const bool table = pl.sym_unmatched && mode != 1;
+        const auto fk = table ? sym_finalize_kernel<true> : sym_finalize_kernel<false>;
+        const size_t fsmem = table ? kFinSmem : 0;
+        int per_sm = 1;
+        VPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fk, kFinWarps * 32, fsmem));
         const unsigned fgrid = unsigned(std::min<int64_t>(nblk(pl.n_sym_leaves, kFinWarps),
-                                                          int64_t(pl.sm_count) * 3));
-        launch_pdl(sym_finalize_kernel, dim3(fgrid), dim3(kFinWarps * 32), kFinSmem, s,
+                                                          int64_t(pl.sm_count) * std::max(per_sm, 1)));
+        launch_pdl(fk, dim3(fgrid), dim3(kFinWarps * 32), fsmem, s,
                    (const SymLeaf*)pl.sym_leaves.p, pl.n_sym_leaves, (const double*)w.sym_part,
                    (const int2*)pl.near_ranges.p, (const double2*)pl.src_sorted.p,
                    (const double*)qs, (const double2*)pl.tgt_sorted.p, (const int32_t*)pl.tgt_ids.p,

@@ -41,11 +41,20 @@ __device__ __forceinline__ void lap_pair_fast(double tx, double ty, double sx,
     lap_acc(r2, q, tab_lane, acc);
 }
 
+#if VPG_LOG_FOLD
+// The global-table twin (same bits; fast_log(double, const double2*)).
+__device__ __forceinline__ void lap_acc(double r2, double q, const double2* gtab, LapAcc& acc) {
+    acc.a = fma(q, fast_log(r2, gtab), acc.a);
+}
+#endif
+
 // Undoes lap_pair_fast for r^2 below the normal range and applies the
 // reference semantics instead: skip r^2 == 0 (summation.cpp:340), exact
-// log for subnormal r^2.
+// log for subnormal r^2.  Tab: the lane's smem table address (uint32_t) or
+// the global table (const double2*).
+template <class Tab>
 __device__ __forceinline__ void lap_pair_fixup(double tx, double ty, double sx,
-                                               double sy, double q, uint32_t tab_lane,
+                                               double sy, double q, Tab tab_lane,
                                                LapAcc& acc) {
     const double dx = tx - sx, dy = ty - sy;
     const double r2 = fma(dy, dy, dx * dx);

@@ -101,7 +101,7 @@ struct SymTask {
     int32_t c0, c1;        // flat column chunk [c0, c1) (multiples of 32, c1 may be ncol)
     int32_t rfirst, rcount;  // column ranges sym_ranges[rfirst, +rcount), the first is A
     int64_t a_part;        // row partial of row i: part[a_part + i]
-    int32_t rg, rows2;     // row group index (column slots: b_part + rg * nb); R = 1 + rows2
+    int32_t rg, rows2;     // row group index (column slots: b_part + rg * nb); R = 1 << rows2
 };
 struct SymRange {
     int32_t b_src, coff, nb, pad;  // sorted source of the range, flat offset, leaf size
@@ -214,6 +214,7 @@ struct Plan {
     DBuf<SymRange> sym_ranges;
     DBuf<SymLeaf> sym_leaves;
     int64_t n_sym_tasks = 0, n_sym_leaves = 0;
+    bool sym_unmatched = false;  // some leaf has targets beyond its sources (summed one-sided in the finalize)
     int64_t sym_nparts = 0;   // partial doubles per apply
     int32_t sym_chunk = 0;    // column chunk (whole-tree decision, shards reuse it)
     double sym_fair = 0.0;    // pairs per subtask (whole-tree decision)

@@ -40,10 +40,10 @@ constexpr size_t kSymSmem = size_t(kLogTableBytes) + size_t(kSymWarps) * (64 * 1
 
 template <int R, bool kDiag, class K>
 __device__ __forceinline__ void sym_block(const K& kern, const double2* cxy, const double* cq, int lane, int i0,
-                                          int j0, const double (&rx)[2], const double (&ry)[2],
-                                          const double (&rq)[2], uint32_t tab_lane, double (&racc)[2],
+                                          int j0, const double (&rx)[R], const double (&ry)[R],
+                                          const double (&rq)[R], uint32_t tab_lane, double (&racc)[R],
                                           double& cacc) {
-#pragma unroll 4
+#pragma unroll(R > 2 ? 2 : 4)
     for (int st = 0; st < 32; ++st) {
         const int c = lane + st;
         const double2 sp = cxy[c];
@@ -92,10 +92,12 @@ __device__ __forceinline__ void sym_task(const K& kern, const SymTask& T, const 
         }
     }
     for (int r0 = T.r0; r0 < T.r1; r0 += 32 * R) {
-        double rx[2] = {kFar, kFar}, ry[2] = {kFar, kFar}, rq[2] = {0.0, 0.0}, racc[2] = {0.0, 0.0};
+        double rx[R], ry[R], rq[R], racc[R];
 #pragma unroll
         for (int u = 0; u < R; ++u) {
             const int i = r0 + lane + 32 * u;
+            rx[u] = ry[u] = kFar;
+            rq[u] = racc[u] = 0.0;
             if (i < T.r1) {
                 const double2 p = sxy[T.a_src + i];
                 rx[u] = p.x;
@@ -167,7 +169,8 @@ p2p_sym_kernel(K kern, const SymTask* tasks, int64_t ntask, const SymRange* rang
         __syncwarp();
         if (lane < T.rcount) rng[lane] = ranges[T.rfirst + lane];
         __syncwarp();
-        if (T.rows2) sym_task<2>(kern, T, rng, sxy, q, cxy, cq, tab_lane, lane, part);
+        if (T.rows2 == 2) sym_task<4>(kern, T, rng, sxy, q, cxy, cq, tab_lane, lane, part);
+        else if (T.rows2) sym_task<2>(kern, T, rng, sxy, q, cxy, cq, tab_lane, lane, part);
         else sym_task<1>(kern, T, rng, sxy, q, cxy, cq, tab_lane, lane, part);
     }
 }

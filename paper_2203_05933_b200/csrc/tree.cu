@@ -697,8 +697,14 @@ void build_sym_near(Plan& pl, int64_t lb, int64_t le) {
         if (bx < 0 || by < 0 || bx >= nb || by >= nb) return -1;
         return int64_t(mort(uint32_t(bx), uint32_t(by)));
     };
+    // rows per lane R = 1 << rsel: 1 for leaves of <= 32 sources, 2 up to
+    // 64, 4 above for Laplace (cfg4: near field 5.57 -> 5.31 ms, the column
+    // tile's smem loads and shuffles amortised over 4 rows; VPG_SYM_R4=0: 2)
+    const char* r4v = std::getenv("VPG_SYM_R4");
+    const bool r4 = !(r4v && std::atoi(r4v) == 0) && pl.family == VPG_LAPLACE;
     auto rows2_of = [&](int32_t n) { return n > 32 ? 1 : 0; };
-    auto nrt_of = [&](int32_t n) { return (n + (rows2_of(n) ? 63 : 31)) / (rows2_of(n) ? 64 : 32); };
+    auto rsel_of = [&](int32_t n) { return r4 && n > 64 ? 2 : rows2_of(n); };
+    auto nrt_of = [&](int32_t n) { return (n + (32 << rsel_of(n)) - 1) / (32 << rsel_of(n)); };
     // Which pairs go symmetric: all of them (T = 0), or in the hybrid form only
     // pairs of "big" leaves (>= T sources each); the other pairs of a target
     // stay one-sided.  Decided once on the whole tree.
@@ -724,7 +730,7 @@ void build_sym_near(Plan& pl, int64_t lb, int64_t le) {
             }
             cost_one += double(na) * na * 31.0 / 32.0;
             total += double(na) * nc;
-            cost_sym += double(nrt_of(na)) * ((nc + 31) / 32) * 32.0 * (rows2_of(na) ? 56.0 : 31.0) + 150.0;
+            cost_sym += double((na + (rows2_of(na) ? 63 : 31)) / (rows2_of(na) ? 64 : 32)) * ((nc + 31) / 32) * 32.0 * (rows2_of(na) ? 56.0 : 31.0) + 150.0;
         }
         // measured: cfg4 (256 per leaf) model 0.50 -> near field 0.64x; cfg2
         // (16..337 per leaf) model 0.76 -> 1.37x when every pair goes
@@ -766,7 +772,7 @@ void build_sym_near(Plan& pl, int64_t lb, int64_t le) {
     // row tiles per group: as many as keep group rows x chunk columns near the share
     auto gsz_of = [&](int64_t a) {
         const int32_t na = nsrc(a);
-        const double tile = (rows2_of(na) ? 64.0 : 32.0) * std::min(C, ncol[size_t(a)]);
+        const double tile = double(32 << rsel_of(na)) * std::min(C, ncol[size_t(a)]);
         return std::clamp(int32_t(pl.sym_fair / tile), 1, nrt_of(na));
     };
     auto nrg_of = [&](int64_t a) { return (nrt_of(nsrc(a)) + gsz_of(a) - 1) / gsz_of(a); };
@@ -816,8 +822,8 @@ void build_sym_near(Plan& pl, int64_t lb, int64_t le) {
             touches = touches || in(b);
         }
         if (!touches) continue;
-        const int r2 = rows2_of(na);
-        const int32_t rows = (r2 ? 64 : 32) * gsz_of(a);
+        const int r2 = rsel_of(na);
+        const int32_t rows = (32 << r2) * gsz_of(a);
         const int32_t rfirst = int32_t(ranges.size());
         ranges.insert(ranges.end(), mine.begin(), mine.end());
         for (int32_t rg = 0; rg < nrg_of(a); ++rg)
@@ -834,9 +840,11 @@ void build_sym_near(Plan& pl, int64_t lb, int64_t le) {
     // of them (small leaves, unmatched targets).
     std::vector<P2PChunk> hyb;
     std::vector<int2> hranges;
+    pl.sym_unmatched = false;
     for (const LeafNear& ln : pl.h_leafnear) {
         const int64_t x = ln.leaf;
         const int32_t na = nsrc(x);
+        if (!hybrid && ln.t0 + na < ln.t1) pl.sym_unmatched = true;
         if (!hybrid || big(x))
             leaves.push_back(SymLeaf{pbase[size_t(x)], ln.t0, hybrid ? na : na, nslot[size_t(x)], ln.t1, ln.rfirst,
                                      ln.rcount});

@@ -307,16 +307,17 @@ def test_symmetric_near_field(vp, rest, monkeypatch, sym, smin):
     assert rel_l2(gpu, cpu) <= 1e-13
 
 
-@pytest.mark.parametrize("sym", ["0", "1"])
-def test_symmetric_near_field_duplicates_and_subnormal(vp, rest, monkeypatch, sym):
+@pytest.mark.parametrize("sym,extra", [("0", True), ("1", True), ("1", False)])
+def test_symmetric_near_field_duplicates_and_subnormal(vp, rest, monkeypatch, sym, extra):
     """Coincident distinct sources and subnormal r^2 with targets = sources
     (+ extras): the symmetric path feeds each pair to both targets and the
-    coincidence list undoes exactly what the hot loop added."""
+    coincidence list undoes exactly what the hot loop added.  Without extras
+    the finalize runs without the smem table (global-table fix-ups)."""
     monkeypatch.setenv("VPG_SYM", sym)
     rng = np.random.default_rng(43)
     base = rng.uniform(-1, 1, (30_000, 2))
     src = np.concatenate([base, base[:500], [[0.0, 0.0], [0.0, 3e-160], [1e-160, 0.0]]])
-    tgt = np.concatenate([src, rng.uniform(-1, 1, (2000, 2)), [[-2e-161, 1e-161]]])
+    tgt = np.concatenate([src, rng.uniform(-1, 1, (2000, 2)), [[-2e-161, 1e-161]]]) if extra else src.copy()
     q = rng.standard_normal(len(src))
     with vp.SummationPlan(lap(vp), src, tgt, 1e-12) as plan:
         gpu = plan.apply(q)
