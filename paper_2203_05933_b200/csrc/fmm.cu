@@ -461,6 +461,12 @@ constexpr int kWSStages = 5;                 // batch metadata ring (kM2LRaw + 2
 #define VPG_M2L_KUNROLL 2
 #endif
 constexpr int kM2LKUnroll = VPG_M2L_KUNROLL;  // k-loop unroll of the MMA warps
+// Timing ablations (tools/ab_m2l_abl.sh; wrong results, never in a shipped
+// build): 1 no DMMA, 2 no B-fragment build, 4 no A-fragment loads, 8 no
+// reduction sums, 16 no epilogue, 32 source rows fetched once only.
+#ifndef VPG_M2L_ABL
+#define VPG_M2L_ABL 0
+#endif
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -534,6 +540,10 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
             const int j = it % kM2LRaw;
             mbar_wait(&rawfree[j], uint32_t(it / kM2LRaw) & 1u);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if (VPG_M2L_ABL & 32) {
+                if (lane == 0) mbar_arrive(&full[j]);
+                continue;
+            }
             m2l_issue_rows(&stg[(it + kM2LRaw) % kWSStages], mult, n, raw0 + j * kM2LPairs * n, &full[j], lane);
             const int64_t bm = bn + stride;
             if (bm < nbatch)
@@ -584,13 +594,18 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
                 auto kstep = [&](int k4) {
                     double afr[MT];
 #pragma unroll
-                    for (int i = 0; i < MT; ++i) afr[i] = hcol[k4 * kM2LHS + 8 * i];
+                    for (int i = 0; i < MT; ++i)
+                        afr[i] = (VPG_M2L_ABL & 4) ? double(k4 + i) : hcol[k4 * kM2LHS + 8 * i];
                     // branch-free B fragments (mma.sync needs a converged warp)
                     const int k = k4 + kq + 1;
                     const int kc = min(k, P);
                     double bfr[kWSTPW];
 #pragma unroll
                     for (int t = 0; t < kWSTPW; ++t) {
+                        if (VPG_M2L_ABL & 2) {
+                            bfr[t] = double(kc);
+                            continue;
+                        }
                         const double2 a = brow[t][kc];
                         const double2 d = turn(bcan[t][kc], (bm2[t] * kc) & 3, bsc[t]);
                         const double v = im ? fma(a.x, d.y, a.y * d.x) : fma(a.x, d.x, -(a.y * d.y));
@@ -599,8 +614,12 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
 #pragma unroll
                     for (int i = 0; i < MT; ++i)
 #pragma unroll
-                        for (int t = 0; t < kWSTPW; ++t)
-                            dmma_884(acc[i][t][0], acc[i][t][1], afr[i], bfr[t]);
+                        for (int t = 0; t < kWSTPW; ++t) {
+                            if (VPG_M2L_ABL & 1)
+                                asm volatile("" : "+d"(acc[i][t][0]) : "d"(afr[i]), "d"(bfr[t]));
+                            else
+                                dmma_884(acc[i][t][0], acc[i][t][1], afr[i], bfr[t]);
+                        }
                 };
                 if constexpr (NK > 0) {
                     // the plan's k-step count is known at compile time: the
@@ -629,6 +648,7 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
 #pragma unroll
             for (int t = 0; t < kWSTPW; ++t) {
                 const int p = 4 * (kWSTPW * w + t) + kq;
+                if ((VPG_M2L_ABL & 16) && acc[0][t][0] != 1.2345) continue;
                 if (p < bt.ecount) {
                     const double2 a0 = a0r[t];
                     const int om = sg.omap[p];
@@ -676,7 +696,7 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
             // monopole shift (summation.cpp:297-301)
             const double logs = log(side / double(1 << bt.level));
             const int l = rtid & 63;
-            if (l <= P)
+            if (l <= P && !((VPG_M2L_ABL & 8) && it > 0))
                 for (int t = rtid >> 6; t < bt.tcount; t += kWSRedThreads >> 6) {
                     const int64_t tg = int64_t(bt.tfirst) + t;
                     // the batch's entries are contiguous; its last box ends at the
