@@ -29,7 +29,8 @@ thread_local std::string t_err;
 std::mutex g_mu;
 struct DeviceTables {
     double2* log_tab = nullptr;
-    double2* log_tab2 = nullptr;  // fast_log's truncation table
+    double2* log_tab2 = nullptr;  // fast_log's table (round-to-nearest centres)
+    double2* log_tab3 = nullptr;  // trunc_log's table (mid-point centres)
     double* k0_tab = nullptr;
     double* k0f_tab = nullptr;
     double* k1_tab = nullptr;
@@ -94,6 +95,19 @@ static DeviceTables& tables_locked(int dev) {
         VPG_CUDA(cudaMalloc(&t.log_tab2, sizeof(double2) * h.size()));
         VPG_CUDA(cudaMemcpy(t.log_tab2, h.data(), sizeof(double2) * h.size(), cudaMemcpyHostToDevice));
     }
+    if (!t.log_tab3) {
+        // centres c = 1 + (i + 1/2)/512 (trunc_log): (RN(1/c), -ln RN(1/c) - i ln2/512);
+        // entry 512 is never indexed (the index is the truncated mantissa)
+        std::vector<double2> h(kLogTableSize);
+        const long double ln2_512 = (long double)kLn2Over512;
+        for (int i = 0; i < kLogTableSize; ++i) {
+            const long double c = 1.0L + ((long double)i + 0.5L) / (kLogTableSize - 1);
+            const double inv = double(1.0L / c);
+            h[size_t(i)] = make_double2(inv, double(-std::log((long double)inv) - (long double)i * ln2_512));
+        }
+        VPG_CUDA(cudaMalloc(&t.log_tab3, sizeof(double2) * h.size()));
+        VPG_CUDA(cudaMemcpy(t.log_tab3, h.data(), sizeof(double2) * h.size(), cudaMemcpyHostToDevice));
+    }
     if (!t.k0_tab) {
         std::vector<double> h(size_t(kK0Intervals) * kK0Coeffs);
         k0_fit_host(h.data());
@@ -121,7 +135,7 @@ const double2* log_table_dev() {
     std::lock_guard<std::mutex> lk(g_mu);
     return tables_locked(dev).log_tab;
 }
-const double2* lap_log_table_dev() {
+const double2* lap_log_table_rn_dev() {
 #if VPG_LOG_FOLD
     int dev = 0;
     VPG_CUDA(cudaGetDevice(&dev));
@@ -129,6 +143,16 @@ const double2* lap_log_table_dev() {
     return tables_locked(dev).log_tab2;
 #else
     return log_table_dev();
+#endif
+}
+const double2* lap_log_table_dev() {
+#if VPG_LOG_FOLD && VPG_LOG_TRUNC
+    int dev = 0;
+    VPG_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_mu);
+    return tables_locked(dev).log_tab3;
+#else
+    return lap_log_table_rn_dev();
 #endif
 }
 const double* k0_fast_table_dev() {

@@ -234,6 +234,63 @@ __device__ __forceinline__ double fast_log(double x, const double2* gtab) {
     return fma(r, p, w);
 }
 
+// The near-field form of fast_log (VPG_LOG_TRUNC, default): the mantissa's
+// top 9 bits TRUNCATED select the centre c = 1 + (i + 1/2)/512 (i = 0..511,
+// again |m/c - 1| <= 2^-10), so the exponent-and-index word g = e 512 + i
+// is (hi >> 11) - bias without the rounding add and the mantissa word
+// indexes the table as it is: two integer instructions fewer per pair
+// (logvar_bench: +4% pairs/s), same six DFMAs, same error bound.  No centre
+// is exactly 1, so ln 1 comes out as a rounding error (1.1e-17) instead of
+// 0: the all-pairs kernel, which has to return the SPEC's exact zeros, keeps
+// fast_log.  Table lap_log_table_dev(): (RN(1/c), -ln RN(1/c) - i ln2/512).
+#ifndef VPG_LOG_TRUNC
+#define VPG_LOG_TRUNC 1
+#endif
+__device__ __forceinline__ double trunc_log(double x, uint32_t tab_lane) {
+    const int hi = __double2hiint(x);
+    const int lo = __double2loint(x);
+    const double g = __int2double_rn((hi >> 11) - (0x3FF << 9));
+    int mhi;
+    asm("lop3.b32 %0, %1, 0x000FFFFF, %2, 0xEA;" : "=r"(mhi) : "r"(hi), "r"(0x3FF00000));
+    uint32_t idx, addr;
+    asm("shr.b32 %0, %1, 11;" : "=r"(idx) : "r"(mhi));
+    asm("mad.lo.u32 %0, %1, 128, %2;" : "=r"(addr) : "r"(idx), "r"(tab_lane));
+    const double m = __hiloint2double(mhi, lo);
+    const double2 tc = lds_f64x2(addr);
+    const double r = fma(m, tc.x, -1.0);
+    const double w = fma(g, c_flog[1], tc.y);
+    double p = fma(r, c_flog[2], c_flog[0]);
+    p = fma(r, p, -0.5);
+    p = fma(r, p, c_flog[3]);
+    return fma(r, p, w);
+}
+__device__ __forceinline__ double trunc_log(double x, const double2* gtab) {
+    const int hi = __double2hiint(x);
+    const int lo = __double2loint(x);
+    const double g = __int2double_rn((hi >> 11) - (0x3FF << 9));
+    int mhi;
+    asm("lop3.b32 %0, %1, 0x000FFFFF, %2, 0xEA;" : "=r"(mhi) : "r"(hi), "r"(0x3FF00000));
+    const uint32_t idx = (uint32_t(mhi) >> 11) - uint32_t(0x3FF << kLogTableBits);
+    const double m = __hiloint2double(mhi, lo);
+    const double2 tc = __ldg(gtab + idx);
+    const double r = fma(m, tc.x, -1.0);
+    const double w = fma(g, c_flog[1], tc.y);
+    double p = fma(r, c_flog[2], c_flog[0]);
+    p = fma(r, p, -0.5);
+    p = fma(r, p, c_flog[3]);
+    return fma(r, p, w);
+}
+// ln x of the near-field kernels (one function, so every kernel of a plan
+// returns the same bits for the same pair)
+template <class Tab>
+__device__ __forceinline__ double near_log(double x, Tab tab) {
+#if VPG_LOG_TRUNC
+    return trunc_log(x, tab);
+#else
+    return fast_log(x, tab);
+#endif
+}
+
 // ----------------------------------------------- programmatic launches --
 // Kernels of one apply are chained with programmatic dependent launch: the
 // next grid may start (and stage its constant operators / tables) while the
@@ -331,7 +388,8 @@ void launch_coop(void (*kern)(KArgs...), int grid, dim3 block, size_t smem, cuda
 
 // Per-device constant tables, built on first use (api.cu).
 const double2* log_table_dev();  // kLogTableSize entries (inv_c, -ln inv_c): fast_log_split
-const double2* lap_log_table_dev();  // the near-field table: fast_log's (VPG_LOG_FOLD=0: log_table_dev)
+const double2* lap_log_table_dev();  // the near-field table: near_log's (VPG_LOG_FOLD=0: log_table_dev)
+const double2* lap_log_table_rn_dev();  // fast_log's table (all-pairs kernel)
 const double* k0_table_dev();    // K0 Chebyshev fits, see k0.cuh
 const double* k1_table_dev();    // K1 Chebyshev fits (same layout)
 const double* k0_fast_table_dev();  // quarter-octave K0 fits (k0_fast)

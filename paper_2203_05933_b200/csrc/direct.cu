@@ -124,7 +124,7 @@ void launch_allpairs(const double2* src, const double* q, int64_t ns,
     const dim3 grid{unsigned(gx), unsigned(nslice), 1u};
     allpairs_kernel<kFamily, kSkip><<<grid, kDirThreads, smem, st>>>(
         src, q, ns, tgt, nt, std::max<int64_t>(slice, 1), lambda,
-        kFamily == VPG_LAPLACE ? lap_log_table_dev() : nullptr,
+        kFamily == VPG_LAPLACE ? lap_log_table_rn_dev() : nullptr,
         kFamily == VPG_LAPLACE ? nullptr : k0_table_dev(), out, partial, clash);
     VPG_LAUNCH_CHECK();
     if (nslice > 1) {

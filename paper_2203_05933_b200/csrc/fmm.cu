@@ -1104,7 +1104,14 @@ l2p_p2p_kernel(const P2PChunk* chunks, int64_t nchunks, const int2* ranges,
 
 // ------------------------------------------------- symmetric near field --
 // (sym.cuh) with ln r^2 as the pair function
+#ifndef VPG_SYM_LAP_WARPS
+#define VPG_SYM_LAP_WARPS 12
+#endif
+#ifndef VPG_SYM_LAP_MINB
+#define VPG_SYM_LAP_MINB 1
+#endif
 struct LapLogK {
+    static constexpr int kSymWarps = VPG_SYM_LAP_WARPS, kSymMinB = VPG_SYM_LAP_MINB, kSymMaxR = kSymLapMaxR;
     __device__ __forceinline__ double operator()(double r2, uint32_t tab_lane) const { return lap_log(r2, tab_lane); }
 };
 
@@ -1581,7 +1588,7 @@ void build_laplace_ops(Plan& pl) {
         pl.shift_grid = std::max(1, std::min(pu, pd)) * pl.sm_count;
     }
     smem_optin((const void*)l2p_p2p_kernel, kLogTableBytes + 32 * 1024);
-    smem_optin((const void*)p2p_sym_kernel<LapLogK>, int(kSymSmem));
+    smem_optin((const void*)p2p_sym_kernel<LapLogK>, int(sym_smem<LapLogK>()));
     smem_optin((const void*)sym_finalize_kernel<true>, int(kFinSmem));
     build_coincidences(pl);
     pl.coin_ready = true;
@@ -1720,6 +1727,8 @@ void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const L
         if (pl.sym) {
             if (pl.n_sym_tasks > 0) {
                 int per_sm = 1;
+                constexpr int kSymWarps = SymShape<LapLogK>::kWarps;
+                constexpr size_t kSymSmem = sym_smem<LapLogK>();
                 VPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p2p_sym_kernel<LapLogK>, kSymWarps * 32,
                                                                        kSymSmem));
                 const int64_t want = (pl.n_sym_tasks + kSymWarps - 1) / kSymWarps;

@@ -731,6 +731,7 @@ hf_l2p_p2p_kernel(HfLevels hl, const P2PChunk* chunks, int64_t nchunks, const in
 // q <= 1, else the fitted K0 of k0.cuh.
 template <bool kFast, int D>
 struct K0NearK {
+    static constexpr int kSymMaxR = 2;
     double l2q, c0, qmax, lambda;
     const double* k0tab;
     __device__ __forceinline__ double operator()(double r2, uint32_t tab_lane) const {
@@ -1605,6 +1606,8 @@ void helm_fmm_issue(const Plan& pl, const double* q_dev, double* out_dev, void* 
         VPG_CUDA(cudaMemsetAsync(ticket, 0, 2 * sizeof(int), s));
         hf_with_k0(pl, [&](auto kern) {
             using K = decltype(kern);
+            constexpr int kSymWarps = SymShape<K>::kWarps;
+            constexpr size_t kSymSmem = sym_smem<K>();
             smem_optin((const void*)p2p_sym_kernel<K>, int(kSymSmem));
             int per_sm = 1;
             VPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p2p_sym_kernel<K>, kSymWarps * 32,

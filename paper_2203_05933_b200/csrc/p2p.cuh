@@ -20,7 +20,7 @@ struct LapAcc {
 // One pair's contribution to the accumulators (the hot-loop form).
 __device__ __forceinline__ void lap_acc(double r2, double q, uint32_t tab_lane, LapAcc& acc) {
 #if VPG_LOG_FOLD
-    acc.a = fma(q, fast_log(r2, tab_lane), acc.a);
+    acc.a = fma(q, near_log(r2, tab_lane), acc.a);
 #else
     double ed;
     const double t = fast_log_split(r2, tab_lane, ed);
@@ -44,7 +44,7 @@ __device__ __forceinline__ void lap_pair_fast(double tx, double ty, double sx,
 #if VPG_LOG_FOLD
 // The global-table twin (same bits; fast_log(double, const double2*)).
 __device__ __forceinline__ void lap_acc(double r2, double q, const double2* gtab, LapAcc& acc) {
-    acc.a = fma(q, fast_log(r2, gtab), acc.a);
+    acc.a = fma(q, near_log(r2, gtab), acc.a);
 }
 #endif
 
@@ -76,7 +76,11 @@ __device__ __forceinline__ void lap_pair(double tx, double ty, double sx,
         if ((hi | __double2loint(r2)) != 0) acc.c = fma(q, log(r2), acc.c);
         qe = 0.0;
     }
+#if VPG_LOG_FOLD
+    acc.a = fma(qe, fast_log(r2, tab_lane), acc.a);  // round-to-nearest centres: ln 1 = 0 exactly
+#else
     lap_acc(r2, qe, tab_lane, acc);
+#endif
 }
 
 // sum_j q_j log(r2_j) from the accumulators.
@@ -91,7 +95,7 @@ __device__ __forceinline__ double lap_total(const LapAcc& acc) {
 // ln(r2) of the symmetric kernel: one double feeding both targets.
 __device__ __forceinline__ double lap_log(double r2, uint32_t tab_lane) {
 #if VPG_LOG_FOLD
-    return fast_log(r2, tab_lane);
+    return near_log(r2, tab_lane);
 #else
     double ed;
     const double t = fast_log_split(r2, tab_lane, ed);

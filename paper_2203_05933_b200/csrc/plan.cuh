@@ -116,6 +116,14 @@ struct SymLeaf {
 };
 constexpr int kSymMaxN = 4096;    // largest leaf (sources) the symmetric path takes
 constexpr int kSymMaxRanges = 9;
+// most rows per lane of the Laplace symmetric kernel (sym.cuh; tree.cu picks R per leaf
+// size up to this).  8 is built on request only: on cfg4 it measured slower than 4 (5.20 vs
+// 4.71 ms: three warps per scheduler leave fixed-latency waits exposed and the eight extra
+// diagonal-tile instances cost instruction fetches), on cfg3's 4,096-point leaves 3% faster.
+#ifndef VPG_SYM_MAXR
+#define VPG_SYM_MAXR 4
+#endif
+constexpr int kSymLapMaxR = VPG_SYM_MAXR;
 struct LeafNear {  // per-leaf near-field data of the last schedule (host)
     int32_t leaf, t0, t1, rfirst, rcount, rself, lfirst, lcount;
 };

@@ -19,7 +19,7 @@ namespace {
 // one shuffle per step hands lane l + 1's accumulator to lane l, so after 32
 // steps lane c holds column c again and adds it to the column's partial
 // (global, .cg, this warp is its only writer; one read-modify-write per row
-// tile).  v = ln r^2 as one double (t + e ln2 with the split constant: the
+// tile).  R = 1, 2, 4 or 8 rows per lane (SymTask::rows2 = log2 R).  v = ln r^2 as one double (t + e ln2 with the split constant: the
 // reference's own log is a single rounded double); r^2 of (i, j) and (j, i)
 // are bitwise equal, so each ordered pair sees the value the one-sided
 // kernel computes.  The pair function K is the kernel: K(r2, tab_lane) =
@@ -29,21 +29,40 @@ namespace {
 // undoes it as in the one-sided kernel, K0 is 0 at r = 0; neighbour columns
 // have j >= na > i).  Row sums are added to slot 4 of A's targets at the end
 // of each row tile, after the self-column sums of the earlier tiles.
+// Launch shape per pair function (K::kSymWarps warps per CTA, K::kSymMinB
+// CTAs per SM; default 8 x 2).  ln r^2 runs 12 warps x 1 CTA so that R = 8
+// rows per lane fit (160 registers): tools/pairloop_sweep.cu measured the
+// pair loop at 1118 G pairs/s for R = 8 / unroll 2 / 12 x 1 against 1073
+// for R = 4 / unroll 4 / 8 x 2 and 1025 for R = 4 / unroll 2 / 8 x 2 --
+// instruction-level parallelism inside a warp beats warps per scheduler.
 #ifndef VPG_SYM_WARPS
 #define VPG_SYM_WARPS 8
 #endif
 #ifndef VPG_SYM_MINB
 #define VPG_SYM_MINB 2
 #endif
-constexpr int kSymWarps = VPG_SYM_WARPS;
-constexpr size_t kSymSmem = size_t(kLogTableBytes) + size_t(kSymWarps) * (64 * 16 + 64 * 8 + kSymMaxRanges * sizeof(SymRange));
+#ifndef VPG_SYM_UNROLL
+#define VPG_SYM_UNROLL 4
+#endif
+constexpr int kSymUnroll4 = VPG_SYM_UNROLL;  // step unroll at R = 4
+template <class K, class = void>
+struct SymShape {
+    static constexpr int kWarps = VPG_SYM_WARPS, kMinB = VPG_SYM_MINB;
+};
+template <class K>
+struct SymShape<K, decltype(void(K::kSymWarps))> {
+    static constexpr int kWarps = K::kSymWarps, kMinB = K::kSymMinB;
+};
+template <class K>
+constexpr size_t sym_smem() {
+    return size_t(kLogTableBytes) + size_t(SymShape<K>::kWarps) * (64 * 16 + 64 * 8 + kSymMaxRanges * sizeof(SymRange));
+}
 
-template <int R, bool kDiag, class K>
-__device__ __forceinline__ void sym_block(const K& kern, const double2* cxy, const double* cq, int lane, int i0,
-                                          int j0, const double (&rx)[R], const double (&ry)[R],
-                                          const double (&rq)[R], uint32_t tab_lane, double (&racc)[R],
-                                          double& cacc) {
-#pragma unroll(R > 2 ? 2 : 4)
+template <int R, class K>
+__device__ __forceinline__ void sym_block(const K& kern, const double2* cxy, const double* cq, int lane,
+                                          const double (&rx)[R], const double (&ry)[R], const double (&rq)[R],
+                                          uint32_t tab_lane, double (&racc)[R], double& cacc) {
+#pragma unroll(R > 4 ? 2 : R > 2 ? kSymUnroll4 : 4)
     for (int st = 0; st < 32; ++st) {
         const int c = lane + st;
         const double2 sp = cxy[c];
@@ -53,17 +72,56 @@ __device__ __forceinline__ void sym_block(const K& kern, const double2* cxy, con
             const double dx = rx[u] - sp.x, dy = ry[u] - sp.y;
             const double r2 = fma(dy, dy, dx * dx);
             const double v = kern(r2, tab_lane);
-            double qr = qc, qcol = rq[u];
-            if (kDiag) {
-                const int i = i0 + lane + 32 * u, j = j0 + (c & 31);
-                qr = i <= j ? qc : 0.0;
-                qcol = i < j ? rq[u] : 0.0;
-            }
-            racc[u] = fma(qr, v, racc[u]);
-            cacc = fma(qcol, v, cacc);
+            racc[u] = fma(qc, v, racc[u]);
+            cacc = fma(rq[u], v, cacc);
         }
         cacc = __shfl_sync(0xffffffffu, cacc, (lane + 1) & 31);
     }
+}
+
+// A column tile of A itself that meets the row tile's diagonal: the 32
+// columns start at row sub-tile N - 1 of the R (j0 = i0 + 32 (N - 1)).
+// Sub-tiles below N - 1 lie wholly above the diagonal (i < j: plain pairs),
+// sub-tile N - 1 is the diagonal one -- row i0' + lane against column
+// i0' + (lane + st) mod 32, so i <= j exactly when lane + st does not wrap
+// and i < j when also st > 0 -- and the sub-tiles after it lie below the
+// diagonal and are skipped (their pairs belong to the transposed tile).
+template <int R, int N, class K>
+__device__ __forceinline__ void sym_block_diag(const K& kern, const double2* cxy, const double* cq, int lane,
+                                               const double (&rx)[R], const double (&ry)[R],
+                                               const double (&rq)[R], uint32_t tab_lane, double (&racc)[R],
+                                               double& cacc) {
+#pragma unroll(N > 4 ? 2 : N > 2 ? kSymUnroll4 : 4)
+    for (int st = 0; st < 32; ++st) {
+        const int c = lane + st;
+        const double2 sp = cxy[c];
+        const double qc = cq[c];
+#pragma unroll
+        for (int u = 0; u < N - 1; ++u) {
+            const double dx = rx[u] - sp.x, dy = ry[u] - sp.y;
+            const double r2 = fma(dy, dy, dx * dx);
+            const double v = kern(r2, tab_lane);
+            racc[u] = fma(qc, v, racc[u]);
+            cacc = fma(rq[u], v, cacc);
+        }
+        {
+            const double dx = rx[N - 1] - sp.x, dy = ry[N - 1] - sp.y;
+            const double r2 = fma(dy, dy, dx * dx);
+            const double v = kern(r2, tab_lane);
+            const bool upper = c < 32;
+            racc[N - 1] = fma(upper ? qc : 0.0, v, racc[N - 1]);
+            cacc = fma(upper && st > 0 ? rq[N - 1] : 0.0, v, cacc);
+        }
+        cacc = __shfl_sync(0xffffffffu, cacc, (lane + 1) & 31);
+    }
+}
+template <int R, int N, class K>
+__device__ __forceinline__ void sym_diag_dispatch(int ud, const K& kern, const double2* cxy, const double* cq,
+                                                  int lane, const double (&rx)[R], const double (&ry)[R],
+                                                  const double (&rq)[R], uint32_t tab_lane, double (&racc)[R],
+                                                  double& cacc) {
+    if (ud == N - 1) sym_block_diag<R, N>(kern, cxy, cq, lane, rx, ry, rq, tab_lane, racc, cacc);
+    else if constexpr (N < R) sym_diag_dispatch<R, N + 1>(ud, kern, cxy, cq, lane, rx, ry, rq, tab_lane, racc, cacc);
 }
 
 // flat column j -> (range index) by a linear scan of the task's ranges
@@ -106,29 +164,40 @@ __device__ __forceinline__ void sym_task(const K& kern, const SymTask& T, const 
             }
         }
         const bool first = r0 == T.r0;
-        for (int ct = max(T.c0 >> 5, r0 >> 5); ct < ct_end; ++ct) {
+        // column tile ct + 1 is fetched into registers while tile ct is summed
+        double2 p = make_double2(-kFar, -kFar);
+        double qj = 0.0;
+        int64_t dst = -1;
+        auto fetch = [&](int ct) {
             const int j = ct * 32 + lane;
-            double2 p = make_double2(-kFar, -kFar);
-            double qj = 0.0;
-            int64_t dst = -1;
-            if (j < T.c1) {
+            p = make_double2(-kFar, -kFar);
+            qj = 0.0;
+            dst = -1;
+            if (ct < ct_end && j < T.c1) {
                 const SymRange& g = rng[sym_range_of(rng, T.rcount, j)];
                 p = sxy[g.b_src + (j - g.coff)];
                 qj = q[g.b_src + (j - g.coff)];
                 dst = g.b_part + int64_t(T.rg) * g.nb + (j - g.coff);
             }
+        };
+        const int ct_begin = max(T.c0 >> 5, r0 >> 5);
+        fetch(ct_begin);
+        for (int ct = ct_begin; ct < ct_end; ++ct) {
             __syncwarp();
             cxy[lane] = p;
             cxy[lane + 32] = p;
             cq[lane] = qj;
             cq[lane + 32] = qj;
             __syncwarp();
-            double cacc = 0.0;
-            if (ct * 32 < T.na)
-                sym_block<R, true>(kern, cxy, cq, lane, r0, ct * 32, rx, ry, rq, tab_lane, racc, cacc);
+            const int64_t dcur = dst;
+            double cacc = !first && dcur >= 0 ? part[dcur] : 0.0;  // the earlier row tiles' sum, in flight under the tile
+            fetch(ct + 1);
+            const int ud = (ct * 32 - r0) >> 5;  // >= 0: self columns below the row tile are never visited
+            if (ct * 32 < T.na && ud < R)
+                sym_diag_dispatch<R, 1>(ud, kern, cxy, cq, lane, rx, ry, rq, tab_lane, racc, cacc);
             else
-                sym_block<R, false>(kern, cxy, cq, lane, r0, ct * 32, rx, ry, rq, tab_lane, racc, cacc);
-            if (dst >= 0) part[dst] = first ? cacc : part[dst] + cacc;
+                sym_block<R>(kern, cxy, cq, lane, rx, ry, rq, tab_lane, racc, cacc);
+            if (dcur >= 0) part[dcur] = cacc;
         }
 #pragma unroll
         for (int u = 0; u < R; ++u) {
@@ -139,9 +208,10 @@ __device__ __forceinline__ void sym_task(const K& kern, const SymTask& T, const 
 }
 
 template <class K>
-__global__ void __launch_bounds__(kSymWarps * 32, VPG_SYM_MINB)
+__global__ void __launch_bounds__(SymShape<K>::kWarps * 32, SymShape<K>::kMinB)
 p2p_sym_kernel(K kern, const SymTask* tasks, int64_t ntask, const SymRange* ranges, const double2* sxy,
                const double* q, const double2* gtab, int* ticket, double* part) {
+    constexpr int kSymWarps = SymShape<K>::kWarps;
     extern __shared__ double2 smp[];
     double2* tab = smp;                                                   // log table
     double2* cbuf = smp + kLogTableSize * kLogTableCopies;                // [warps][64] xy
@@ -169,7 +239,8 @@ p2p_sym_kernel(K kern, const SymTask* tasks, int64_t ntask, const SymRange* rang
         __syncwarp();
         if (lane < T.rcount) rng[lane] = ranges[T.rfirst + lane];
         __syncwarp();
-        if (T.rows2 == 2) sym_task<4>(kern, T, rng, sxy, q, cxy, cq, tab_lane, lane, part);
+        if (K::kSymMaxR >= 8 && T.rows2 == 3) sym_task<K::kSymMaxR >= 8 ? 8 : 2>(kern, T, rng, sxy, q, cxy, cq, tab_lane, lane, part);
+        else if (K::kSymMaxR >= 4 && T.rows2 == 2) sym_task<K::kSymMaxR >= 4 ? 4 : 2>(kern, T, rng, sxy, q, cxy, cq, tab_lane, lane, part);
         else if (T.rows2) sym_task<2>(kern, T, rng, sxy, q, cxy, cq, tab_lane, lane, part);
         else sym_task<1>(kern, T, rng, sxy, q, cxy, cq, tab_lane, lane, part);
     }

@@ -698,12 +698,16 @@ void build_sym_near(Plan& pl, int64_t lb, int64_t le) {
         return int64_t(mort(uint32_t(bx), uint32_t(by)));
     };
     // rows per lane R = 1 << rsel: 1 for leaves of <= 32 sources, 2 up to
-    // 64, 4 above for Laplace (cfg4: near field 5.57 -> 5.31 ms, the column
-    // tile's smem loads and shuffles amortised over 4 rows; VPG_SYM_R4=0: 2)
+    // 64, for Laplace 4 up to 128 and 8 above (cfg4: near field 5.57 -> 5.31
+    // ms at R = 4, the column tile's smem loads and shuffles amortised over
+    // the rows and more independent pair chains per warp; VPG_SYM_R4=0: 2,
+    // VPG_SYM_R8=0: at most 4; 8 needs a -DVPG_SYM_MAXR=8 build, plan.cuh)
     const char* r4v = std::getenv("VPG_SYM_R4");
     const bool r4 = !(r4v && std::atoi(r4v) == 0) && pl.family == VPG_LAPLACE;
+    const char* r8v = std::getenv("VPG_SYM_R8");
+    const bool r8 = r4 && kSymLapMaxR >= 8 && !(r8v && std::atoi(r8v) == 0);
     auto rows2_of = [&](int32_t n) { return n > 32 ? 1 : 0; };
-    auto rsel_of = [&](int32_t n) { return r4 && n > 64 ? 2 : rows2_of(n); };
+    auto rsel_of = [&](int32_t n) { return r8 && n > 128 ? 3 : r4 && n > 64 ? 2 : rows2_of(n); };
     auto nrt_of = [&](int32_t n) { return (n + (32 << rsel_of(n)) - 1) / (32 << rsel_of(n)); };
     // Which pairs go symmetric: all of them (T = 0), or in the hybrid form only
     // pairs of "big" leaves (>= T sources each); the other pairs of a target
