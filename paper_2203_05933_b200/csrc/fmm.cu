@@ -468,6 +468,39 @@ constexpr int kM2LKUnroll = VPG_M2L_KUNROLL;  // k-loop unroll of the MMA warps
 #define VPG_M2L_ABL 0
 #endif
 
+// Ping-pong of the MMA warps' k-loops (VPG_M2L_PINGPONG, measured and left
+// off: cfg2 M2L 0.203 -> 0.213 ms, cfg4 0.353 -> 0.364 ms).  The
+// 14 MMA warps of a batch all run k-loop, register epilogue, k-loop, ... in
+// lock step (the batch barriers keep them together), so the FP64 tensor pipe
+// idles through every epilogue and every wait for the next rows: the timing
+// ablations give 0.126 ms for the kernel without its DMMAs and 0.110 ms for
+// the DMMAs alone against 0.203 ms together (cfg2).  With the token the
+// warps of column tiles 0-6 and 7-13 take turns: one half runs its k-loop at
+// the pipe's full rate (7 warps saturate it, tools/dmma_sweep.cu) while the
+// other half does its epilogue, hands its rows back and waits for the next
+// batch's.  Two named barriers pass the token (the CUTLASS ordered-sequence
+// form): a half syncs on its own barrier before the k-loop and arrives on
+// the other half's after it.  It did not pay: a half's 7 warps sit 2/2/2/1 on
+// the four schedulers, each of which owns a quarter of the DMMA rate
+// (tools/dmma_sweep.cu: 1 warp per SM 9.0 TFLOP/s, 4 warps 36.3, 7 warps
+// 32.1, 14 warps 32.3), so a half's k-loop takes as long as half of the
+// lock-step one and the hand-offs come on top.
+// VPG_M2L_PREBUILD (also off: 0.203 -> 0.210 ms) builds all B fragments of a
+// batch before a DMMA-only k-loop, after tools/dmma_with_dfma.cu showed that
+// an FP64 CUDA-core instruction issued among DMMAs costs ~9 pipe cycles.
+#ifndef VPG_M2L_PINGPONG
+#define VPG_M2L_PINGPONG 0
+#endif
+#ifndef VPG_M2L_PREBUILD
+#define VPG_M2L_PREBUILD 0
+#endif
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int count) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -557,6 +590,10 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
         // latency otherwise sits in front of every batch)
         M2LBatch bt_next{};
         if (blockIdx.x < nbatch) bt_next = batches[blockIdx.x];
+        constexpr bool kPing = VPG_M2L_PINGPONG && kWSMMAWarps % 2 == 0;
+        constexpr int kTokThreads = 32 * kWSMMAWarps;
+        const int half = w >= kWSMMAWarps / 2;  // named barrier 1 + half: this half may run its k-loop
+        if (kPing && half == 1 && blockIdx.x < nbatch) named_bar_arrive(1, kTokThreads);  // half 0 goes first
         for (int it = 0;; ++it) {
             const int64_t bi = blockIdx.x + it * stride;
             if (bi >= nbatch) break;
@@ -566,6 +603,7 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
             const M2LStage& sg = stg[it % kWSStages];
             const double2* raw = raw0 + j * kM2LPairs * n;
             mbar_wait(&full[j], uint32_t(it / kM2LRaw) & 1u);
+            if (kPing) named_bar_sync(1 + half, kTokThreads);
             // B-fragment sources: tile TPW w + t, column 8(TPW w + t) + rq ->
             // entry 4(TPW w + t) + rq/2, part rq&1; row k4 + kq <-> k = k4 + kq + 1
             const double2* brow[kWSTPW];
@@ -621,7 +659,35 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
                                 dmma_884(acc[i][t][0], acc[i][t][1], afr[i], bfr[t]);
                         }
                 };
-                if constexpr (NK > 0) {
+                if constexpr (NK > 0 && VPG_M2L_PREBUILD && kWSTPW == 1) {
+                    // All B fragments of the batch first, then a k-loop of
+                    // DMMAs only.  An FP64 CUDA-core instruction issued among
+                    // DMMAs costs ~9 cycles of the shared FP64 pipe, not 2
+                    // (tools/dmma_with_dfma.cu); the MMA warps wake together
+                    // on the rows' barrier, so their builds coincide and the
+                    // pipe then sees DMMAs only.  The empty volatile asm pins
+                    // every fragment ahead of the first (volatile) DMMA.
+                    double ball[NK];
+#pragma unroll
+                    for (int s4 = 0; s4 < NK; ++s4) {
+                        const int k = 4 * s4 + kq + 1;
+                        const int kc = min(k, P);
+                        const double2 a = brow[0][kc];
+                        const double2 d = turn(bcan[0][kc], (bm2[0] * kc) & 3, bsc[0]);
+                        const double v = im ? fma(a.x, d.y, a.y * d.x) : fma(a.x, d.x, -(a.y * d.y));
+                        ball[s4] = (blive[0] && k <= P) ? v : 0.0;
+                    }
+#pragma unroll
+                    for (int s4 = 0; s4 < NK; ++s4) asm volatile("" : "+d"(ball[s4]));
+#pragma unroll
+                    for (int s4 = 0; s4 < NK; ++s4) {
+                        double afr[MT];
+#pragma unroll
+                        for (int i = 0; i < MT; ++i) afr[i] = hcol[4 * s4 * kM2LHS + 8 * i];
+#pragma unroll
+                        for (int i = 0; i < MT; ++i) dmma_884(acc[i][0][0], acc[i][0][1], afr[i], ball[s4]);
+                    }
+                } else if constexpr (NK > 0) {
                     // the plan's k-step count is known at compile time: the
                     // whole k-loop unrolls (13 steps at P = 50: M2L -7%)
 #pragma unroll
@@ -631,6 +697,8 @@ m2l_kernel(const M2LBatch* batches, int64_t nbatch, const int32_t* tbox,
                     for (int k4 = 0; k4 < KP; k4 += 4) kstep(k4);
                 }
             }
+            // the token goes to the other half (the last batch's second half keeps it)
+            if (kPing && (half == 0 || bi + stride < nbatch)) named_bar_arrive(2 - half, kTokThreads);
             // register epilogue: lane holds (re, im) of row l = 8i + rq,
             // entry p = 4(2w+t) + kq.  The entries' a_0 are read before the
             // rows' slot is released to the producer.

@@ -4,7 +4,7 @@
 O=gpurun_out/abl; mkdir -p $O
 for v in main "$@"; do
   if [ $v = main ]; then unset VPG_LIB_PATH; else export VPG_LIB_PATH=$PWD/variants/$v/libvolpot_b200.so; fi
-  timeout 300 python bench.py --workload ${AB_WL:-cfg2} --steps 10 --warmup 3 --no-cpu-baseline > $O/$v.json 2> $O/$v.err
+  VPG_BENCH_ABLATION=1 timeout 300 python bench.py --workload ${AB_WL:-cfg2} --steps 10 --warmup 3 --no-cpu-baseline > $O/$v.json 2> $O/$v.err
   python -c "
 import json
 d=json.load(open('$O/$v.json'))
