@@ -32,99 +32,145 @@ __device__ inline void box_center(double x0, double y0, double s, uint32_t id,
 }
 
 // ------------------------------------------------------------------ P2M --
-// One warp per work item = (level, box, source range): two lanes per source,
-// lane (j, h) forms the running powers q w^k of source j
-// (summation.cpp:247-254) for the half k in (h*kh, (h+1)*kh], the upper half
-// starting from w^kh by binary powering, so the dependent multiply chain is
-// half as long.  The scaled powers -q w^k / k land in a per-warp [16][P+1]
-// smem panel; lane k then sums column k in source order.  Leaf items cover
-// the reference P2M; in the multilevel upward pass (small problems, see
+// One warp per work item = (level, box, source range).  Lane 4 j + h:
+// source stream j (0..7: the item's sources j, j + 8, ...) and quarter h of
+// the powers, k in (h KQ, (h + 1) KQ].  Every lane keeps the sums of q w^k
+// over its stream's sources for its KQ powers IN REGISTERS (summation.cpp:
+// 247-254 with the sums reassociated: per stream, then across the 8 streams
+// by shuffles, once per item); quarter h of a source runs one step after
+// quarter h - 1 and takes over its running power q w^(h KQ) and w by a
+// shuffle from the neighbouring lane, so no power is formed twice and
+// nothing goes through shared memory -- the per-source smem panel of the
+// first version (25 STS.128 + 32 LDS.128 per 16 sources and warp) capped
+// P2M at the shared-memory pipe: cfg4 0.276 ms against 0.08 ms of FP64 work.
+// The factors -1/k are applied to the sums, not to the powers.  Leaf items
+// cover the reference P2M; in the multilevel upward pass (small problems, see
 // laplace_apply) every level's boxes are items too and boxes split into
 // several items are summed in item order by p2m_reduce_kernel.
 constexpr int kP2MWarps = 4;
-constexpr int kP2MSrc = 16;
-
-#ifndef VPG_P2M_SRC
-#define VPG_P2M_SRC 16
+constexpr int kP2MSrc = 16;  // p2l_kernel's panel rows
+#ifndef VPG_P2M_ILP
+#define VPG_P2M_ILP 1
 #endif
-constexpr int kP2MSrcRound = VPG_P2M_SRC;        // sources per round: 16 (2 lanes each) or 8 (4 lanes each)
-constexpr int kP2MLanes = 32 / kP2MSrcRound;     // lanes per source, each a contiguous share of k
 
+template <int KQ>
 __global__ void __launch_bounds__(kP2MWarps * 32)
-p2m_kernel(const P2MItem* items, int64_t nitems, const int32_t* sorted_unused,
-           const double2* sxy, const double* q, int P, double x0, double y0, double side,
-           double2* mult, double2* partial) {
-    extern __shared__ double2 panels[];
+p2m_kernel(const P2MItem* items, int64_t nitems, const double2* sxy, const double* q, int P, double x0,
+           double y0, double side, double2* mult, double2* partial) {
     pdl_trigger();
     pdl_wait();
-    (void)sorted_unused;
     const int n = P + 1;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t li = int64_t(blockIdx.x) * kP2MWarps + warp;
     if (li >= nitems) return;
-    const int ps = n | 1;  // panel row stride: odd in double2 (an even n puts every row in one bank group)
-    double2* panel = panels + warp * kP2MSrcRound * ps;
     const P2MItem it = items[li];
     const double s = side / double(1 << it.level);
     double cx, cy;
     box_center(x0, y0, s, uint32_t(it.box), cx, cy);
     const double inv_s = 1.0 / s;
     const int e0 = it.e0, e1 = it.e1;
-    const int j = lane & (kP2MSrcRound - 1), h = lane / kP2MSrcRound;
-    const int kq = (P + kP2MLanes - 1) / kP2MLanes;  // powers per lane share
-    double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
-    for (int base = e0; base < e1; base += kP2MSrcRound) {
-        const int cnt = min(kP2MSrcRound, e1 - base);
-        if (j < cnt) {
-            const double2 p = sxy[base + j];
-            const double wr = (p.x - cx) * inv_s, wi = (p.y - cy) * inv_s;
-            const double qj = q[base + j];
-            double2* row = panel + j * ps;
-            double pr = qj, pi = 0.0;
-            const int k0 = h * kq + 1, k1 = min((h + 1) * kq, P);
+    const int j = lane >> 2, h = lane & 3;
+    // S sources of the stream per step (2 S independent multiply chains per lane; S = 2
+    // measured slower: cfg4 0.140 -> 0.177 ms, one more fill/drain step in three and 118 registers)
+    constexpr int S = VPG_P2M_ILP;
+    const int nstep = (e1 - e0 + 8 * S - 1) / (8 * S) + 3;  // + 3: the last sources' upper quarters
+    double ar[KQ], ai[KQ];
+#pragma unroll
+    for (int t = 0; t < KQ; ++t) ar[t] = ai[t] = 0.0;
+    double a0 = 0.0;  // sum q (lanes h = 0)
+    double pr[S], pi[S], wr[S], wi[S];  // running powers q w^k and w of the lane's current sources
+    double2 pn[S];                      // quarter 0 loads one step ahead
+    double qn[S];
+#pragma unroll
+    for (int u = 0; u < S; ++u) {
+        pr[u] = pi[u] = wr[u] = wi[u] = 0.0;
+        pn[u] = make_double2(cx, cy);
+        qn[u] = 0.0;
+        const int i0 = e0 + j + 8 * u;
+        if (h == 0 && i0 < e1) {
+            pn[u] = sxy[i0];
+            qn[u] = q[i0];
+        }
+    }
+    for (int st = 0; st < nstep; ++st) {
+#pragma unroll
+        for (int u = 0; u < S; ++u) {
+            // the neighbouring quarter's state after its previous step
+            const double tpr = __shfl_up_sync(0xffffffffu, pr[u], 1), tpi = __shfl_up_sync(0xffffffffu, pi[u], 1);
+            const double twr = __shfl_up_sync(0xffffffffu, wr[u], 1), twi = __shfl_up_sync(0xffffffffu, wi[u], 1);
             if (h == 0) {
-                row[0] = make_double2(qj, 0.0);
-            } else {
-                // q w^(k0 - 1) by binary powering
-                double br = wr, bi = wi;
-                for (int e = k0 - 1; e; e >>= 1) {
-                    if (e & 1) {
-                        const double nr = pr * br - pi * bi;
-                        pi = pr * bi + pi * br;
-                        pr = nr;
-                    }
-                    const double sr = br * br - bi * bi;
-                    bi = 2.0 * br * bi;
-                    br = sr;
+                wr[u] = (pn[u].x - cx) * inv_s;
+                wi[u] = (pn[u].y - cy) * inv_s;
+                pr[u] = qn[u];
+                pi[u] = 0.0;
+                a0 += qn[u];
+                const int nx = e0 + j + 8 * (S * (st + 1) + u);
+                pn[u] = make_double2(cx, cy);
+                qn[u] = 0.0;
+                if (nx < e1) {
+                    pn[u] = sxy[nx];
+                    qn[u] = q[nx];
                 }
-            }
-            for (int k = k0; k <= k1; ++k) {
-                const double nr = pr * wr - pi * wi;
-                const double ni = pr * wi + pi * wr;
-                pr = nr;
-                pi = ni;
-                const double f = c_neg_inv_k[k];
-                row[k] = make_double2(f * pr, f * pi);
+            } else {
+                pr[u] = tpr;
+                pi[u] = tpi;
+                wr[u] = twr;
+                wi[u] = twi;
             }
         }
-        __syncwarp();
-        for (int t = 0; t < cnt; ++t) {
-            if (lane <= P) {
-                const double2 v0 = panel[t * ps + lane];
-                acc0.x += v0.x;
-                acc0.y += v0.y;
+#pragma unroll
+        for (int t = 0; t < KQ; ++t) {
+#pragma unroll
+            for (int u = 0; u < S; ++u) {
+                const double nr = fma(pr[u], wr[u], -(pi[u] * wi[u]));
+                const double ni = fma(pr[u], wi[u], pi[u] * wr[u]);
+                pr[u] = nr;
+                pi[u] = ni;
             }
-            if (lane + 32 <= P) {
-                const double2 v1 = panel[t * ps + lane + 32];
-                acc1.x += v1.x;
-                acc1.y += v1.y;
+            if (S == 2) {
+                ar[t] += pr[0] + pr[S - 1];
+                ai[t] += pi[0] + pi[S - 1];
+            } else {
+                ar[t] += pr[0];
+                ai[t] += pi[0];
             }
         }
-        __syncwarp();
+    }
+    // the 8 streams' sums (lane bits 2..4) by recursive halving: at each of
+    // the three stages a lane keeps one half of its slots and receives the
+    // partner's copy of that half, so 14 + 14 values cross the warp instead
+    // of 3 x 2 KQ; stream j ends with the slots 8 j0 + 4 j1 + 2 j2 + {0, 1}
+    constexpr int KH = 16;
+    double vr[KH], vi[KH];
+#pragma unroll
+    for (int t = 0; t < KH; ++t) {
+        vr[t] = t < KQ ? ar[t] : 0.0;
+        vi[t] = t < KQ ? ai[t] : 0.0;
+    }
+#pragma unroll
+    for (int stage = 0; stage < 3; ++stage) {
+        const int off = 4 << stage, half = KH >> (stage + 1);
+        const bool up = lane & off;
+        a0 += __shfl_xor_sync(0xffffffffu, a0, off);
+#pragma unroll
+        for (int t = 0; t < half; ++t) {
+            const double sr = up ? vr[t] : vr[t + half], si = up ? vi[t] : vi[t + half];
+            const double kr = up ? vr[t + half] : vr[t], ki = up ? vi[t + half] : vi[t];
+            vr[t] = kr + __shfl_xor_sync(0xffffffffu, sr, off);
+            vi[t] = ki + __shfl_xor_sync(0xffffffffu, si, off);
+        }
     }
     double2* dst = it.direct ? mult + int64_t(it.row) * n : partial + li * n;
-    if (lane <= P) dst[lane] = acc0;
-    if (lane + 32 <= P) dst[lane + 32] = acc1;
+    if (lane == 0) dst[0] = make_double2(a0, 0.0);
+    const int slot0 = 8 * (j & 1) + 4 * ((j >> 1) & 1) + 2 * (j >> 2);
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+        const int slot = slot0 + t, k = h * KQ + slot + 1;
+        if (slot < KQ && k <= P) {
+            const double f = c_neg_inv_k[k];
+            dst[k] = make_double2(f * vr[t], f * vi[t]);
+        }
+    }
 }
 
 // Boxes split over several P2M items: sum the item partials in item order.
@@ -1642,7 +1688,6 @@ void build_laplace_ops(Plan& pl) {
 
     for (int mt = 2; mt <= kM2LMaxMT; ++mt) smem_optin((const void*)m2l_kernel_for(mt, 0), 225 * 1024);
     smem_optin((const void*)m2l_kernel_for(pl.RP / 8, pl.KP), 225 * 1024);
-    smem_optin((const void*)p2m_kernel, 100 * 1024);
     smem_optin((const void*)p2l_kernel, 100 * 1024);
     {
         // co-resident CTAs for the cooperative shift passes
@@ -1828,10 +1873,16 @@ void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const L
 
     double2* partial = w.p2m_partial;
     if (pl.n_p2m_items > 0) {
-        launch_pdl(p2m_kernel, dim3(nblk(pl.n_p2m_items, kP2MWarps)), dim3(kP2MWarps * 32),
-                   size_t(kP2MWarps) * kP2MSrcRound * (n | 1) * sizeof(double2), st, (const P2MItem*)pl.p2m_items.p,
-                   pl.n_p2m_items, (const int32_t*)nullptr, (const double2*)pl.src_sorted.p, (const double*)qs,
-                   P, pl.x0, pl.y0, pl.side, mult, partial);
+        auto p2m = [&](auto kern) {
+            launch_pdl(kern, dim3(nblk(pl.n_p2m_items, kP2MWarps)), dim3(kP2MWarps * 32), 0, st,
+                       (const P2MItem*)pl.p2m_items.p, pl.n_p2m_items, (const double2*)pl.src_sorted.p,
+                       (const double*)qs, P, pl.x0, pl.y0, pl.side, mult, partial);
+        };
+        const int kq = (P + 3) / 4;  // powers per lane quarter
+        if (kq <= 7) p2m(p2m_kernel<7>);
+        else if (kq <= 10) p2m(p2m_kernel<10>);
+        else if (kq <= 13) p2m(p2m_kernel<13>);
+        else p2m(p2m_kernel<16>);
         ++launches;
     }
     if (pl.n_p2m_splits > 0) {
