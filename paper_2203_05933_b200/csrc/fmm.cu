@@ -1243,12 +1243,28 @@ constexpr size_t kFinSmem = size_t(kLogTableBytes) + kFinScratch;
 // the coincidence fix-ups read the global table (same bits), so the kernel
 // runs at full occupancy -- the slot sums are latency-bound loads, and the
 // kernel sits on the step's tail.
-template <bool kTable>
+// kFar: the far field too -- the leaf's local expansion (plans whose leaves
+// evaluate one row: the classical downward pass) is staged per warp and
+// every target's Horner (l2p_kernel's arithmetic, same bits) runs under its
+// slot loads, so the far field never makes the round trip through `out`
+// (cfg4: l2p_kernel 0.10 ms + finalize 0.13 ms, one scattered write and one
+// scattered read-modify-write of 4.2M doubles, become one kernel).
+struct FarArgs {
+    const int32_t* lrows;
+    const double2* loc;
+    const int32_t* row_level;
+    const int32_t* row_morton;
+    int P;
+    double x0, y0, side;
+};
+template <bool kTable, bool kFar>
 __global__ void __launch_bounds__(kFinWarps * 32)
 sym_finalize_kernel(const SymLeaf* leaves, int64_t nleaves, const double* part, const int2* ranges,
                     const double2* sxy, const double* q, const double2* txy, const int32_t* tids,
-                    const int32_t* coin_off, const int32_t* coin_src, const double2* gtab, double* out, int add) {
+                    const int32_t* coin_off, const int32_t* coin_src, const double2* gtab, double* out, int add,
+                    FarArgs far) {
     extern __shared__ double2 smp[];
+    __shared__ double2 rowbuf[kFar ? kFinWarps : 1][64];
     double2* tab = smp;
     int* rbuf = reinterpret_cast<int*>(smp + kLogTableSize * kLogTableCopies);  // [warps][2][64]
     uint32_t tab_lane = 0;
@@ -1266,11 +1282,38 @@ sym_finalize_kernel(const SymLeaf* leaves, int64_t nleaves, const double* part, 
     if constexpr (kTable) __syncthreads();
     for (int64_t w = int64_t(blockIdx.x) * kFinWarps + warp; w < nleaves; w += int64_t(gridDim.x) * kFinWarps) {
         const SymLeaf lf = leaves[w];
+        double fcx = 0.0, fcy = 0.0, finv = 0.0;
+        if constexpr (kFar) {
+            const int n = far.P + 1;
+            const int r = far.lrows[lf.lfirst];
+            __syncwarp();
+            rowbuf[warp][lane] = lane < n ? far.loc[int64_t(r) * n + lane] : make_double2(0.0, 0.0);
+            rowbuf[warp][lane + 32] = lane + 32 < n ? far.loc[int64_t(r) * n + lane + 32] : make_double2(0.0, 0.0);
+            __syncwarp();
+            const double s = far.side / double(1 << far.row_level[r]);
+            box_center(far.x0, far.y0, s, uint32_t(far.row_morton[r]), fcx, fcy);
+            finv = 1.0 / s;
+        }
         for (int k = lane; k < lf.n; k += 32) {
             const int64_t t = int64_t(lf.tgt) + k;
             const double* pk = part + lf.pbase + k;
             double sum = 0.0;
             int sl = 0;
+            double farv = 0.0;
+            if constexpr (kFar) {  // issued ahead of the slot loads' use: the Horner chain hides them
+                const double2 tp = txy[t];
+                const double2* buf = rowbuf[warp];
+                const double ur = (tp.x - fcx) * finv, ui = (tp.y - fcy) * finv;
+                double ar = buf[far.P].x, ai = buf[far.P].y;
+                for (int kk = far.P - 1; kk >= 0; --kk) {
+                    const double2 a = buf[kk];
+                    const double nar = fma(ar, ur, fma(-ai, ui, a.x));
+                    const double nai = fma(ar, ui, fma(ai, ur, a.y));
+                    ar = nar;
+                    ai = nai;
+                }
+                farv = -kInv2Pi * (0.0 + ar);
+            }
             for (; sl + 8 <= lf.nslot; sl += 8) {  // eight loads in flight, added in slot order
                 double a[8];
 #pragma unroll
@@ -1295,7 +1338,12 @@ sym_finalize_kernel(const SymLeaf* leaves, int64_t nleaves, const double* part, 
             if constexpr (kTable) sum += coin_correction(coin_off, coin_src, t, tp.x, tp.y, sxy, q, tab_lane);
             else sum += coin_correction(coin_off, coin_src, t, tp.x, tp.y, sxy, q, gtab);
             double& o = out[tids[t]];
-            o = add == 2 ? o + -kInv4Pi * sum : -kInv4Pi * sum;  // 2: the far field is already there
+            if constexpr (kFar) {
+                const double o0 = farv;
+                o = o0 + -kInv4Pi * sum;
+            } else {
+                o = add == 2 ? o + -kInv4Pi * sum : -kInv4Pi * sum;  // 2: the far field is already there
+            }
         }
         if constexpr (kTable) {
             if (add == 1 || lf.tgt + lf.n >= lf.t1) continue;
@@ -1702,7 +1750,7 @@ void build_laplace_ops(Plan& pl) {
     }
     smem_optin((const void*)l2p_p2p_kernel, kLogTableBytes + 32 * 1024);
     smem_optin((const void*)p2p_sym_kernel<LapLogK>, int(sym_smem<LapLogK>()));
-    smem_optin((const void*)sym_finalize_kernel<true>, int(kFinSmem));
+    smem_optin((const void*)sym_finalize_kernel<true, false>, int(kFinSmem));
     build_coincidences(pl);
     pl.coin_ready = true;
     if (!pl.adaptive) build_sym_near(pl, pl.shard_lb, pl.shard_le);
@@ -1822,7 +1870,8 @@ void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const L
     auto sym_finalize = [&](cudaStream_t s, int mode) {
         // the table variant only for unmatched targets summed one-sided here
         const bool table = pl.sym_unmatched && mode != 1;
-        const auto fk = table ? sym_finalize_kernel<true> : sym_finalize_kernel<false>;
+        const auto fk = mode == 3 ? sym_finalize_kernel<false, true>
+                                  : table ? sym_finalize_kernel<true, false> : sym_finalize_kernel<false, false>;
         const size_t fsmem = table ? kFinSmem : 0;
         int per_sm = 1;
         VPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fk, kFinWarps * 32, fsmem));
@@ -1833,7 +1882,9 @@ void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const L
                    (const int2*)pl.near_ranges.p, (const double2*)pl.src_sorted.p,
                    (const double*)qs, (const double2*)pl.tgt_sorted.p, (const int32_t*)pl.tgt_ids.p,
                    (const int32_t*)pl.coin_off.p, (const int32_t*)pl.coin_src.p, lap_log_table_dev(),
-                   out_dev, mode);
+                   out_dev, mode,
+                   FarArgs{(const int32_t*)pl.l2p_rows.p, (const double2*)loc, (const int32_t*)pl.row_level.p,
+                           (const int32_t*)pl.row_morton.p, P, pl.x0, pl.y0, pl.side});
         ++launches;
     };
     auto near_field = [&](cudaStream_t s) {
@@ -1960,7 +2011,10 @@ void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const L
         if (side) VPG_CUDA(cudaStreamWaitEvent(st, join, 0));
         else near_field(st);
     }
-    if (pl.n_p2p_chunks > 0) {
+    // symmetric plans whose leaves evaluate one local expansion: the finalize does the L2P too
+    static const bool fuse_env = !(std::getenv("VPG_FUSE_L2P") && std::atoi(std::getenv("VPG_FUSE_L2P")) == 0);
+    const bool fused_far = far_first && fuse_env && pl.sym_l2p_single && !pl.sym_unmatched;
+    if (pl.n_p2p_chunks > 0 && !fused_far) {
         const int64_t want = (pl.n_p2p_chunks + kL2PWarps - 1) / kL2PWarps;
         const unsigned grid = unsigned(std::min<int64_t>(want, int64_t(pl.sm_count) * 8));
         launch_pdl(l2p_kernel, dim3(grid), dim3(kL2PWarps * 32), 0, st, (const P2PChunk*)pl.p2p_chunks.p,
@@ -1972,7 +2026,7 @@ void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const L
     if (far_first) {
         VPG_CUDA(cudaEventRecord(far_done, st));
         VPG_CUDA(cudaStreamWaitEvent(side, far_done, 0));
-        sym_finalize(side, 2);
+        sym_finalize(side, fused_far ? 3 : 2);
         VPG_CUDA(cudaEventRecord(join, side));
         VPG_CUDA(cudaStreamWaitEvent(st, join, 0));
     }

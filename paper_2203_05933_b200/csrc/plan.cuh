@@ -113,6 +113,7 @@ struct SymLeaf {
     int32_t nslot;
     int32_t t1;      // end of the leaf's targets: [tgt + n, t1) are unmatched
     int32_t rfirst, rcount;  // the leaf's 3x3 source ranges in near_ranges (unmatched targets)
+    int32_t lfirst, lcount;  // the leaf's L2P chain in l2p_rows (the fused far field of sym_finalize_kernel)
 };
 constexpr int kSymMaxN = 4096;    // largest leaf (sources) the symmetric path takes
 constexpr int kSymMaxRanges = 9;
@@ -225,6 +226,7 @@ struct Plan {
     bool sym_unmatched = false;  // some leaf has targets beyond its sources (summed one-sided in the finalize)
     int64_t sym_nparts = 0;   // partial doubles per apply
     int32_t sym_chunk = 0;    // column chunk (whole-tree decision, shards reuse it)
+    bool sym_l2p_single = false;  // every symmetric leaf evaluates one local expansion (its own)
     double sym_fair = 0.0;    // pairs per subtask (whole-tree decision)
     std::vector<LeafNear> h_leafnear;
     int64_t n_p2p_chunks = 0;

@@ -751,6 +751,7 @@ void build_sym_near(Plan& pl, int64_t lb, int64_t le) {
         // subtasks of about half one warp's fair share (16 warps per SM)
         pl.sym_fair = std::max(4096.0, total / (double(pl.sm_count) * 16.0 * 2.0));
         pl.sym_chunk = int32_t(std::clamp(std::floor(pl.sym_fair / 64.0 / 32.0) * 32.0, 32.0, 8192.0));
+        if (const char* cv = std::getenv("VPG_SYM_CHUNK")) pl.sym_chunk = std::max(32, std::atoi(cv) / 32 * 32);
     }
     if (pl.sym_min < 0 && force != 1) return;
     const int32_t T = std::max(0, pl.sym_min);
@@ -773,6 +774,12 @@ void build_sym_near(Plan& pl, int64_t lb, int64_t le) {
     }
     const int32_t C = std::max(32, pl.sym_chunk);
     auto ncc_of = [&](int64_t a) { return (ncol[size_t(a)] + C - 1) / C; };
+    // a leaf's chunks are balanced: ncc chunks of ceil(ncol / ncc) columns rounded up to tiles
+    // (cfg4: 1280 columns as 448 + 448 + 384, not 544 + 544 + 192: near field 4.89 -> 4.83 ms)
+    auto cw_of = [&](int64_t a) {
+        const int32_t k = std::max(1, ncc_of(a));
+        return std::min(C, ((ncol[size_t(a)] + k - 1) / k + 31) / 32 * 32);
+    };
     // row tiles per group: as many as keep group rows x chunk columns near the share
     auto gsz_of = [&](int64_t a) {
         const int32_t na = nsrc(a);
@@ -832,8 +839,8 @@ void build_sym_near(Plan& pl, int64_t lb, int64_t le) {
         ranges.insert(ranges.end(), mine.begin(), mine.end());
         for (int32_t rg = 0; rg < nrg_of(a); ++rg)
             for (int32_t cc = 0; cc < ncc_of(a); ++cc)
-                tasks.push_back(SymTask{so[size_t(a)], na, rg * rows, std::min(na, (rg + 1) * rows), cc * C,
-                                        std::min(ncol[size_t(a)], (cc + 1) * C), rfirst, int32_t(mine.size()),
+                tasks.push_back(SymTask{so[size_t(a)], na, rg * rows, std::min(na, (rg + 1) * rows), cc * cw_of(a),
+                                        std::min(ncol[size_t(a)], (cc + 1) * cw_of(a)), rfirst, int32_t(mine.size()),
                                         pbase[size_t(a)] + int64_t(cc) * na, rg, r2});
     }
     // full form: every leaf of the range with targets -- matched ones from
@@ -851,7 +858,7 @@ void build_sym_near(Plan& pl, int64_t lb, int64_t le) {
         if (!hybrid && ln.t0 + na < ln.t1) pl.sym_unmatched = true;
         if (!hybrid || big(x))
             leaves.push_back(SymLeaf{pbase[size_t(x)], ln.t0, hybrid ? na : na, nslot[size_t(x)], ln.t1, ln.rfirst,
-                                     ln.rcount});
+                                     ln.rcount, ln.lfirst, ln.lcount});
         if (!hybrid) continue;
         for (int part = 0; part < 2; ++part) {  // 0: matched targets, 1: unmatched
             const int32_t t0 = part == 0 ? ln.t0 : ln.t0 + na, t1 = part == 0 ? ln.t0 + na : ln.t1;
@@ -893,6 +900,10 @@ void build_sym_near(Plan& pl, int64_t lb, int64_t le) {
     to_device(pl.sym_leaves, leaves, st);
     pl.n_sym_tasks = int64_t(tasks.size());
     pl.n_sym_leaves = int64_t(leaves.size());
+    pl.sym_l2p_single = true;
+    // (and no leaf so large that a warp per leaf unbalances the Horner work: cfg3's 4,096-point
+    // leaves measured 20.2 -> 20.5 ms fused)
+    for (const SymLeaf& lf : leaves) pl.sym_l2p_single = pl.sym_l2p_single && lf.lcount == 1 && lf.n <= 512;
     pl.sym = true;
 }
 
