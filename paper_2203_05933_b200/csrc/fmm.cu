@@ -964,15 +964,20 @@ l2p_kernel(const P2PChunk* chunks, int64_t nchunks, const int32_t* lrows, const 
 // Every sum has a fixed order, so results are run-to-run identical.  Output:
 // far field (l2p_kernel) + near field, scattered to the original target
 // order (summation.cpp:345).
-constexpr int kP2PWarps = 8;
+// 16 warps x 1 CTA per SM, 4 sources per hot-loop trip (A/B with the truncated-index log:
+// 8 x 2 / unroll 2 -> 16 x 1 / unroll 4: op_star near field 7.39 -> 7.13 ms, cfg2 0.195 -> 0.192 ms)
+#ifndef VPG_P2P_WARPS
+#define VPG_P2P_WARPS 16
+#endif
+constexpr int kP2PWarps = VPG_P2P_WARPS;
 constexpr int kP2PBatch = 64;
 constexpr int kP2PChunk = 64;
 #ifndef VPG_P2P_MIN_BLOCKS
-#define VPG_P2P_MIN_BLOCKS 2
+#define VPG_P2P_MIN_BLOCKS 1
 #endif
 constexpr int kP2PMinBlocks = VPG_P2P_MIN_BLOCKS;
 #ifndef VPG_P2P_UNROLL
-#define VPG_P2P_UNROLL 2
+#define VPG_P2P_UNROLL 4
 #endif
 constexpr int kP2PUnroll = VPG_P2P_UNROLL;  // sources per hot-loop iteration
 
@@ -1748,7 +1753,7 @@ void build_laplace_ops(Plan& pl) {
                                                                kShiftWarps * 32, sm_dn));
         pl.shift_grid = std::max(1, std::min(pu, pd)) * pl.sm_count;
     }
-    smem_optin((const void*)l2p_p2p_kernel, kLogTableBytes + 32 * 1024);
+    smem_optin((const void*)l2p_p2p_kernel, kLogTableBytes + 48 * 1024);
     smem_optin((const void*)p2p_sym_kernel<LapLogK>, int(sym_smem<LapLogK>()));
     smem_optin((const void*)sym_finalize_kernel<true, false>, int(kFinSmem));
     build_coincidences(pl);

@@ -984,6 +984,128 @@ void hf_const_init() {
     if (dev < 64) done |= uint64_t(1) << dev;
 }
 
+// The M2L schedule of a Chebyshev-FMM plan for the targets of the leaf range
+// [lb, le) (vpg_plan_set_shard; the whole tree by default): target rows CSR
+// over all levels, the dense (target, offset) -> source row table and the
+// 16-target tiles.  A shard keeps the target boxes that lie over its leaves,
+// so M2L, the expansion back to node values and L2L shrink with the shard
+// (the upward pass stays whole on every rank, as for the Laplace plans).
+void hf_build_m2l(Plan& pl, int64_t lb, int64_t le) {
+    const int L = pl.L, lmin = pl.hf_lmin, k = pl.hf_k;
+    // M2L lists (target rows CSR over all levels; entries: source row, C block)
+    std::vector<int32_t> tbox, toff{0}, esrc, eop;
+    pl.hf_lvl_t0.assign(size_t(L + 2), 0);
+    for (int l = lmin; l <= L; ++l) {
+        pl.hf_lvl_t0[size_t(l)] = int64_t(tbox.size());
+        const int nb = 1 << l;
+        const auto& of = pl.hf_offs[size_t(l)];
+        auto oidx = [&](int dx, int dy) {
+            for (size_t i = 0; i < of.size(); ++i)
+                if (of[i].x == dx && of[i].y == dy) return int(i);
+            return -1;
+        };
+        const int64_t cblk0 = pl.hf_C_off[size_t(l)] / (int64_t(k) * k);
+        for (int64_t tb = 0; tb < (int64_t(1) << (2 * l)); ++tb) {
+            if (pl.h_tcnt[size_t(lvl_base(l) + tb)] == 0) continue;
+            // shards: only the boxes over the shard's leaves (their locals are all the shard's
+            // L2L chain and L2P read)
+            const int sh = 2 * (L - l);
+            if (((tb + 1) << sh) <= lb || (tb << sh) >= le) continue;
+            const int tx = int(squash2(uint32_t(tb))), ty = int(squash2(uint32_t(tb) >> 1));
+            auto add = [&](int sx, int sy) {
+                if (sx < 0 || sy < 0 || sx >= nb || sy >= nb) return;
+                if (std::max(std::abs(tx - sx), std::abs(ty - sy)) < 2) return;
+                const uint32_t sb = mort(uint32_t(sx), uint32_t(sy));
+                if (pl.h_scnt[size_t(lvl_base(l) + sb)] == 0) return;
+                const int o = oidx(tx - sx, ty - sy);
+                if (o < 0) return;  // beyond the decay cutoff
+                esrc.push_back(int32_t(pl.hf_row_base[size_t(l)] + sb));
+                eop.push_back(int32_t(cblk0 + o));
+            };
+            if (l == lmin) {
+                for (int sy = 0; sy < nb; ++sy)
+                    for (int sx = 0; sx < nb; ++sx) add(sx, sy);
+            } else {
+                const int px = tx >> 1, py = ty >> 1;
+                for (int qy = std::max(0, py - 1); qy <= std::min((nb >> 1) - 1, py + 1); ++qy)
+                    for (int qx = std::max(0, px - 1); qx <= std::min((nb >> 1) - 1, px + 1); ++qx)
+                        for (int c = 0; c < 4; ++c) add(2 * qx + (c & 1), 2 * qy + (c >> 1));
+            }
+            tbox.push_back(int32_t(pl.hf_row_base[size_t(l)] + tb));
+            toff.push_back(int32_t(esrc.size()));
+        }
+    }
+    pl.hf_lvl_t0[size_t(L + 1)] = int64_t(tbox.size());
+    pl.hf_ntbox = int64_t(tbox.size());
+    // dense (target, offset) -> source row table and 16-target tiles per level
+    {
+        std::vector<int32_t> srcof;
+        std::vector<int4> tiles;
+        std::vector<int2> splits;
+        constexpr int kSplitOffsets = 48;  // offsets per tile above which targets are split
+        int parts_per_split = 0;           // one part count for every split level
+        for (int l = lmin; l <= L; ++l) {
+            const int noff = int(pl.hf_offs[size_t(l)].size());
+            if (noff > kSplitOffsets)
+                parts_per_split = std::max(parts_per_split, (noff + kSplitOffsets - 1) / kSplitOffsets);
+        }
+        int64_t slot = 0;
+        for (int l = lmin; l <= L; ++l) {
+            const int64_t a0 = pl.hf_lvl_t0[size_t(l)], a1 = pl.hf_lvl_t0[size_t(l + 1)];
+            const int noff = int(pl.hf_offs[size_t(l)].size());
+            const int64_t cblk0 = pl.hf_C_off[size_t(l)] / (int64_t(k) * k);
+            const int64_t sbase = int64_t(srcof.size()) - a0 * noff;
+            for (int64_t ti = a0; ti < a1; ++ti) {
+                const size_t row0 = srcof.size();
+                srcof.resize(row0 + size_t(noff), -1);
+                for (int e = toff[size_t(ti)]; e < toff[size_t(ti + 1)]; ++e)
+                    srcof[row0 + size_t(eop[size_t(e)] - cblk0)] = esrc[size_t(e)];
+            }
+            if (noff > kSplitOffsets) {
+                // target tiles x offset ranges -> partial sums (slot + p * kHfTile + t),
+                // reduced per target in range order
+                const int np = parts_per_split;
+                for (int64_t ti = a0; ti < a1; ti += kHfTile) {
+                    const int cnt = int(std::min<int64_t>(kHfTile, a1 - ti));
+                    for (int t = 0; t < cnt; ++t) splits.push_back(make_int2(tbox[size_t(ti + t)], int(slot + t)));
+                    for (int p = 0; p < np; ++p) {
+                        const int o0 = int(int64_t(noff) * p / np), o1 = int(int64_t(noff) * (p + 1) / np);
+                        tiles.push_back(make_int4(int(ti), cnt, int(sbase), noff));
+                        tiles.push_back(make_int4(o0, o1, int(slot + p * kHfTile), int(cblk0)));
+                    }
+                    slot += int64_t(np) * kHfTile;
+                }
+            } else {
+                for (int64_t ti = a0; ti < a1; ti += kHfTile) {
+                    tiles.push_back(make_int4(int(ti), int(std::min<int64_t>(kHfTile, a1 - ti)), int(sbase), noff));
+                    tiles.push_back(make_int4(0, noff, -1, int(cblk0)));
+                }
+            }
+        }
+        // every split level uses the same part count (ranges of equal count)
+        pl.hf_split_parts = parts_per_split;
+        pl.hf_nsplit = int64_t(splits.size());
+        pl.hf_nparts = slot;
+        pl.hf_ntiles = int64_t(tiles.size()) / 2;
+        auto up2 = [](auto& d, const auto& h) {
+            d.alloc(std::max<size_t>(h.size(), 1));
+            if (!h.empty()) VPG_CUDA(cudaMemcpy(d.p, h.data(), h.size() * sizeof(h[0]), cudaMemcpyHostToDevice));
+        };
+        up2(pl.hf_srcof, srcof);
+        up2(pl.hf_tiles, tiles);
+        up2(pl.hf_splits, splits);
+    }
+    pl.hf_nent = int64_t(esrc.size());
+    auto up = [](auto& d, const auto& h) {
+        d.alloc(std::max<size_t>(h.size(), 1));
+        if (!h.empty()) VPG_CUDA(cudaMemcpy(d.p, h.data(), h.size() * sizeof(h[0]), cudaMemcpyHostToDevice));
+    };
+    up(pl.hf_tbox, tbox);
+    up(pl.hf_toff, toff);
+    up(pl.hf_esrc, esrc);
+    up(pl.hf_eop, eop);
+}
+
 void build_helm_fmm(Plan& pl) {
     hf_const_init();
     const int L = pl.L;
@@ -1133,114 +1255,11 @@ void build_helm_fmm(Plan& pl) {
     }
     VPG_CUDA(cudaDeviceSynchronize());
 
-    // M2L lists (target rows CSR over all levels; entries: source row, C block)
-    std::vector<int32_t> tbox, toff{0}, esrc, eop;
-    pl.hf_lvl_t0.assign(size_t(L + 2), 0);
-    for (int l = lmin; l <= L; ++l) {
-        pl.hf_lvl_t0[size_t(l)] = int64_t(tbox.size());
-        const int nb = 1 << l;
-        const auto& of = offs[size_t(l)];
-        auto oidx = [&](int dx, int dy) {
-            for (size_t i = 0; i < of.size(); ++i)
-                if (of[i].x == dx && of[i].y == dy) return int(i);
-            return -1;
-        };
-        const int64_t cblk0 = pl.hf_C_off[size_t(l)] / (int64_t(k) * k);
-        for (int64_t tb = 0; tb < (int64_t(1) << (2 * l)); ++tb) {
-            if (pl.h_tcnt[size_t(lvl_base(l) + tb)] == 0) continue;
-            const int tx = int(squash2(uint32_t(tb))), ty = int(squash2(uint32_t(tb) >> 1));
-            auto add = [&](int sx, int sy) {
-                if (sx < 0 || sy < 0 || sx >= nb || sy >= nb) return;
-                if (std::max(std::abs(tx - sx), std::abs(ty - sy)) < 2) return;
-                const uint32_t sb = mort(uint32_t(sx), uint32_t(sy));
-                if (pl.h_scnt[size_t(lvl_base(l) + sb)] == 0) return;
-                const int o = oidx(tx - sx, ty - sy);
-                if (o < 0) return;  // beyond the decay cutoff
-                esrc.push_back(int32_t(pl.hf_row_base[size_t(l)] + sb));
-                eop.push_back(int32_t(cblk0 + o));
-            };
-            if (l == lmin) {
-                for (int sy = 0; sy < nb; ++sy)
-                    for (int sx = 0; sx < nb; ++sx) add(sx, sy);
-            } else {
-                const int px = tx >> 1, py = ty >> 1;
-                for (int qy = std::max(0, py - 1); qy <= std::min((nb >> 1) - 1, py + 1); ++qy)
-                    for (int qx = std::max(0, px - 1); qx <= std::min((nb >> 1) - 1, px + 1); ++qx)
-                        for (int c = 0; c < 4; ++c) add(2 * qx + (c & 1), 2 * qy + (c >> 1));
-            }
-            tbox.push_back(int32_t(pl.hf_row_base[size_t(l)] + tb));
-            toff.push_back(int32_t(esrc.size()));
-        }
-    }
-    pl.hf_lvl_t0[size_t(L + 1)] = int64_t(tbox.size());
-    pl.hf_ntbox = int64_t(tbox.size());
-    // dense (target, offset) -> source row table and 16-target tiles per level
-    {
-        std::vector<int32_t> srcof;
-        std::vector<int4> tiles;
-        std::vector<int2> splits;
-        constexpr int kSplitOffsets = 48;  // offsets per tile above which targets are split
-        int parts_per_split = 0;           // one part count for every split level
-        for (int l = lmin; l <= L; ++l) {
-            const int noff = int(offs[size_t(l)].size());
-            if (noff > kSplitOffsets)
-                parts_per_split = std::max(parts_per_split, (noff + kSplitOffsets - 1) / kSplitOffsets);
-        }
-        int64_t slot = 0;
-        for (int l = lmin; l <= L; ++l) {
-            const int64_t a0 = pl.hf_lvl_t0[size_t(l)], a1 = pl.hf_lvl_t0[size_t(l + 1)];
-            const int noff = int(offs[size_t(l)].size());
-            const int64_t cblk0 = pl.hf_C_off[size_t(l)] / (int64_t(k) * k);
-            const int64_t sbase = int64_t(srcof.size()) - a0 * noff;
-            for (int64_t ti = a0; ti < a1; ++ti) {
-                const size_t row0 = srcof.size();
-                srcof.resize(row0 + size_t(noff), -1);
-                for (int e = toff[size_t(ti)]; e < toff[size_t(ti + 1)]; ++e)
-                    srcof[row0 + size_t(eop[size_t(e)] - cblk0)] = esrc[size_t(e)];
-            }
-            if (noff > kSplitOffsets) {
-                // target tiles x offset ranges -> partial sums (slot + p * kHfTile + t),
-                // reduced per target in range order
-                const int np = parts_per_split;
-                for (int64_t ti = a0; ti < a1; ti += kHfTile) {
-                    const int cnt = int(std::min<int64_t>(kHfTile, a1 - ti));
-                    for (int t = 0; t < cnt; ++t) splits.push_back(make_int2(tbox[size_t(ti + t)], int(slot + t)));
-                    for (int p = 0; p < np; ++p) {
-                        const int o0 = int(int64_t(noff) * p / np), o1 = int(int64_t(noff) * (p + 1) / np);
-                        tiles.push_back(make_int4(int(ti), cnt, int(sbase), noff));
-                        tiles.push_back(make_int4(o0, o1, int(slot + p * kHfTile), int(cblk0)));
-                    }
-                    slot += int64_t(np) * kHfTile;
-                }
-            } else {
-                for (int64_t ti = a0; ti < a1; ti += kHfTile) {
-                    tiles.push_back(make_int4(int(ti), int(std::min<int64_t>(kHfTile, a1 - ti)), int(sbase), noff));
-                    tiles.push_back(make_int4(0, noff, -1, int(cblk0)));
-                }
-            }
-        }
-        // every split level uses the same part count (ranges of equal count)
-        pl.hf_split_parts = parts_per_split;
-        pl.hf_nsplit = int64_t(splits.size());
-        pl.hf_nparts = slot;
-        pl.hf_ntiles = int64_t(tiles.size()) / 2;
-        auto up2 = [](auto& d, const auto& h) {
-            d.alloc(std::max<size_t>(h.size(), 1));
-            if (!h.empty()) VPG_CUDA(cudaMemcpy(d.p, h.data(), h.size() * sizeof(h[0]), cudaMemcpyHostToDevice));
-        };
-        up2(pl.hf_srcof, srcof);
-        up2(pl.hf_tiles, tiles);
-        up2(pl.hf_splits, splits);
-    }
-    pl.hf_nent = int64_t(esrc.size());
-    auto up = [](auto& d, const auto& h) {
-        d.alloc(std::max<size_t>(h.size(), 1));
-        if (!h.empty()) VPG_CUDA(cudaMemcpy(d.p, h.data(), h.size() * sizeof(h[0]), cudaMemcpyHostToDevice));
-    };
-    up(pl.hf_tbox, tbox);
-    up(pl.hf_toff, toff);
-    up(pl.hf_esrc, esrc);
-    up(pl.hf_eop, eop);
+    pl.hf_offs = offs;
+    pl.hf_n = n;
+    pl.hf_k = k;
+    pl.hf_lmin = lmin;
+    hf_build_m2l(pl, pl.shard_lb, pl.shard_le);
     // anterp_kernel layout: nodes / bw per level (32 slots) -> the same n nodes at every level
     std::vector<double> nl(size_t(L + 1) * 32, 0.0), bl(size_t(L + 1) * 32, 0.0);
     for (int l = 0; l <= L; ++l)
@@ -1687,11 +1706,14 @@ void helm_fmm_issue(const Plan& pl, const double* q_dev, double* out_dev, void* 
         ++launches;
     }
     mark(4);
-    // expand: Lv_l (n2 x rows) = Vc_l (n2 x k) . Lt_l (k x rows), one GEMM per level
+    // expand: Lv_l (n2 x rows) = Vc_l (n2 x k) . Lt_l (k x rows), one GEMM per level over the rows
+    // of the boxes above the shard's leaves (Morton-contiguous; the whole level without shards)
     for (int l = pl.hf_lmin; l <= L; ++l) {
-        const int rows_l = 1 << (2 * l);
-        const int64_t b0 = pl.hf_row_base[size_t(l)];
-        hf_gemm(n2, rows_l, k, pl.hf_Vc.p + pl.hf_V_off[size_t(l)], n2, Lt + b0 * k, k, Lv + b0 * n2, n2,
+        const int sh = 2 * (L - l);
+        const int64_t r0 = pl.shard_lb >> sh, r1 = pl.shard_le > pl.shard_lb ? ((pl.shard_le - 1) >> sh) + 1 : r0;
+        if (r1 <= r0) continue;
+        const int64_t b0 = pl.hf_row_base[size_t(l)] + r0;
+        hf_gemm(n2, int(r1 - r0), k, pl.hf_Vc.p + pl.hf_V_off[size_t(l)], n2, Lt + b0 * k, k, Lv + b0 * n2, n2,
                 pl.sm_count, st);
         ++launches;
     }

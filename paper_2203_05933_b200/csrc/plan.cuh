@@ -301,6 +301,7 @@ struct Plan {
     std::vector<int64_t> hf_V_off, hf_C_off, hf_row_base;  // per level
     DBuf<int32_t> hf_tbox, hf_toff, hf_esrc, hf_eop;       // M2L target rows CSR; entries (src row, C block)
     std::vector<int64_t> hf_lvl_t0;                        // per level first index into hf_tbox
+    std::vector<std::vector<int2>> hf_offs;                // per level: the M2L offsets (T - S in box units)
     DBuf<int32_t> hf_srcof;  // per level [targets][offsets]: source row or -1
     DBuf<int4> hf_tiles;     // M2L tiles, 2 x int4: (first target, count, srcof base, noff),
                              // (first offset, end offset, partial slot or -1, C block base)
@@ -380,6 +381,7 @@ void direct_sum_device(int family, double lambda, const double2* src,
 // helm.cu
 void build_helm_ops(Plan& pl);
 void build_helm_fmm(Plan& pl);  // native mode (helm.cu)
+void hf_build_m2l(Plan& pl, int64_t lb, int64_t le);  // its M2L schedule for the targets of a leaf range
 size_t helm_work_bytes(const Plan& pl);  // Chebyshev FMM apply scratch (helm.cu)
 void helm_fmm_issue(const Plan& pl, const double* q_dev, double* out_dev, void* work, cudaStream_t st,
                     cudaEvent_t* ev, int64_t& launches, cudaStream_t side, cudaEvent_t fork, cudaEvent_t join,

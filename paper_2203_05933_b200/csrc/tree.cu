@@ -665,6 +665,7 @@ void build_schedules(Plan& pl, int64_t lb, int64_t le) {
         }
         pl.shard_m2l = m2l;
     }
+    if (pl.hf) hf_build_m2l(pl, lb, le);                     // the Chebyshev FMM's far field follows the shard
     if (pl.coin_ready || pl.hf) build_sym_near(pl, lb, le);  // Laplace ops / Chebyshev FMM built
 }
 

@@ -167,8 +167,9 @@ def test_native_target_shards_assemble_bit_exact(vp, world):
 @pytest.mark.parametrize("mode", ["reference", "native"])
 def test_helmholtz_target_shards_assemble_bit_exact(vp, mode):
     """Modified Helmholtz shards: the treecode traverses only the shard's
-    targets; the Chebyshev FMM evaluates L2P + near field only for them (its
-    far field stays whole on every rank).  Bit-exact assembly."""
+    targets; the Chebyshev FMM keeps the upward pass whole and restricts M2L,
+    the expansion, L2L, L2P and the near field to the boxes over the shard's
+    leaves (hf_build_m2l).  Bit-exact assembly."""
     from paper_2203_05933_b200 import multigpu
     rng = np.random.default_rng(39)
     src = rng.uniform(-1, 1, (30_000, 2))
