@@ -128,13 +128,17 @@ class ClockSampler:
 
 def measured_traffic(workload, kernel):
     """DRAM bytes per launch of `kernel` from the committed ncu capture
-    (profiles/traffic_r01.json), or None when that workload was not captured."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic_r01.json")
-    try:
-        with open(path) as f:
-            return json.load(f).get(workload, {}).get(kernel)
-    except (OSError, ValueError):
-        return None
+    (profiles/traffic_r02.json, else traffic_r01.json), or None when that workload was not captured."""
+    for name in ("traffic_r02.json", "traffic_r01.json"):  # the latest capture that has the kernel
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", name)
+        try:
+            with open(path) as f:
+                v = json.load(f).get(workload, {}).get(kernel)
+        except (OSError, ValueError):
+            v = None
+        if v is not None:
+            return v
+    return None
 
 
 def load_workload(name):
