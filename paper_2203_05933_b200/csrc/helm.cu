@@ -407,37 +407,49 @@ hf_l2l_kernel(int64_t nbox, int64_t base_l, int64_t base_p, const int32_t* tbox,
     }
 }
 
-// barycentric weights of x in [-1, 1] on the n Chebyshev nodes (exact node -> delta)
+// Lagrange weights l_a(x) of x in [-1, 1] on the n Chebyshev nodes, in the product form
+// l_a = bw_a prod_{c != a} (x - x_c) / sum, the products by a forward and a backward running
+// product and ONE division for the normalisation (the barycentric quotients bw_a / (x - x_a)
+// cost n FP64 divisions, ~30 instructions each: 36 per point dominated the leaf P2M and the
+// L2P).  At a node every other weight is an exact 0 and the node's own weight 1 to an ulp.
 __device__ __forceinline__ void hf_bary(const double* nodes, const double* bw, int n, double x, double* w) {
-    int hit = -1;
-    double sum = 0.0;
+    double run = 1.0;
 #pragma unroll
     for (int a = 0; a < kHfMaxN; ++a) {
         if (a < n) {
-            const double d = x - nodes[a];
-            if (d == 0.0) hit = a;
-            w[a] = bw[a] / (d == 0.0 ? 1.0 : d);
+            w[a] = run;
+            run *= x - nodes[a];
+        }
+    }
+    run = 1.0;
+    double sum = 0.0;
+#pragma unroll
+    for (int a = kHfMaxN - 1; a >= 0; --a) {
+        if (a < n) {
+            w[a] *= run * bw[a];
             sum += w[a];
+            run *= x - nodes[a];
         }
     }
     const double inv = 1.0 / sum;
 #pragma unroll
     for (int a = 0; a < kHfMaxN; ++a)
-        if (a < n) w[a] = hit >= 0 ? (a == hit ? 1.0 : 0.0) : w[a] * inv;
+        if (a < n) w[a] *= inv;
 }
 
 // P2M at the leaves of the Chebyshev FMM: a warp per leaf (leaves hold
-// ~16 points), sources 32 at a time: lane j builds the barycentric rows
-// l_a(x_j), l_b(y_j) in smem, then each lane accumulates its ~n^2/32 of
-// W[a][b] = sum_j q_j l_a(x_j) l_b(y_j) in source order.
+// ~16 points), sources 32 at a time: lane j builds the rows q_j l_a(x_j),
+// l_b(y_j) in smem, then the lanes, as a 4 x 8 grid, accumulate register
+// tiles of 5 x 3 entries of W[a][b] = sum_j q_j l_a(x_j) l_b(y_j) in source
+// order (8 smem loads per 15 DFMAs; one entry per (lane, round) took 3 per 2).
 constexpr int kAntWarps = 4;  // 41 KB of static smem
+constexpr int kAntTA = (kHfMaxN + 3) / 4, kAntTB = (kHfMaxN + 7) / 8;
 
 __global__ void __launch_bounds__(kAntWarps * 32)
 hf_anterp_leaf_kernel(int L, int n, double x0, double y0, double side, const int32_t* scnt_leaf,
                       const int32_t* soff, const double2* sxy, const double* q, const double* tab,
                       int64_t base_leaf, double* W) {
     __shared__ double rows[kAntWarps][2][32][kHfMaxN];
-    __shared__ double qsh[kAntWarps][32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t b = int64_t(blockIdx.x) * kAntWarps + warp;
     if (b >= (int64_t(1) << (2 * L)) || scnt_leaf[b] == 0) return;
@@ -448,42 +460,44 @@ hf_anterp_leaf_kernel(int L, int n, double x0, double y0, double side, const int
     const double cx = x0 + (squash2(uint32_t(b)) + 0.5) * s;
     const double cy = y0 + (squash2(uint32_t(b) >> 1) + 0.5) * s;
     const int e0 = soff[b], e1 = soff[b + 1];
-    double acc[(kHfMaxN * kHfMaxN + 31) / 32];
+    const int a0 = (lane >> 3) * kAntTA, b0 = (lane & 7) * kAntTB;  // the lane's tile of W
+    double acc[kAntTA][kAntTB];
 #pragma unroll
-    for (int r = 0; r < (kHfMaxN * kHfMaxN + 31) / 32; ++r) acc[r] = 0.0;
+    for (int i = 0; i < kAntTA; ++i)
+#pragma unroll
+        for (int k = 0; k < kAntTB; ++k) acc[i][k] = 0.0;
     for (int base = e0; base < e1; base += 32) {
         const int cnt = min(32, e1 - base);
         __syncwarp();
         if (lane < cnt) {
             const double2 p = sxy[base + lane];
+            const double qj = q[base + lane];
             double w[kHfMaxN];
             hf_bary(nodes, bw, n, (p.x - cx) * 2.0 / s, w);
 #pragma unroll
-            for (int a = 0; a < kHfMaxN; ++a)
-                if (a < n) rows[warp][0][lane][a] = w[a];
+            for (int a = 0; a < kHfMaxN; ++a) rows[warp][0][lane][a] = a < n ? qj * w[a] : 0.0;
             hf_bary(nodes, bw, n, (p.y - cy) * 2.0 / s, w);
 #pragma unroll
-            for (int a = 0; a < kHfMaxN; ++a)
-                if (a < n) rows[warp][1][lane][a] = w[a];
-            qsh[warp][lane] = q[base + lane];
+            for (int a = 0; a < kHfMaxN; ++a) rows[warp][1][lane][a] = a < n ? w[a] : 0.0;
         }
         __syncwarp();
+        for (int j = 0; j < cnt; ++j) {
+            double ra[kAntTA], rb[kAntTB];
 #pragma unroll
-        for (int r = 0; r < (kHfMaxN * kHfMaxN + 31) / 32; ++r) {
-            const int e = lane + 32 * r;
-            if (e < n2) {
-                const int a = e / n, bb = e % n;
-                double v = acc[r];
-                for (int j = 0; j < cnt; ++j) v = fma(qsh[warp][j] * rows[warp][0][j][a], rows[warp][1][j][bb], v);
-                acc[r] = v;
-            }
+            for (int i = 0; i < kAntTA; ++i) ra[i] = rows[warp][0][j][a0 + i];
+#pragma unroll
+            for (int k = 0; k < kAntTB; ++k) rb[k] = b0 + k < kHfMaxN ? rows[warp][1][j][b0 + k] : 0.0;
+#pragma unroll
+            for (int i = 0; i < kAntTA; ++i)
+#pragma unroll
+                for (int k = 0; k < kAntTB; ++k) acc[i][k] = fma(ra[i], rb[k], acc[i][k]);
         }
     }
 #pragma unroll
-    for (int r = 0; r < (kHfMaxN * kHfMaxN + 31) / 32; ++r) {
-        const int e = lane + 32 * r;
-        if (e < n2) W[(base_leaf + b) * n2 + e] = acc[r];
-    }
+    for (int i = 0; i < kAntTA; ++i)
+#pragma unroll
+        for (int k = 0; k < kAntTB; ++k)
+            if (a0 + i < n && b0 + k < n) W[(base_leaf + b) * n2 + (a0 + i) * n + b0 + k] = acc[i][k];
 }
 
 struct HfLevels {
