@@ -39,8 +39,11 @@ def test_cfg2_fmm_vs_reference(vp, rest):
     assert rel_l2(gpu[idx], ld) <= 1e-12
 
 
-@pytest.mark.parametrize("eps", [1e-6, 1e-9])
+@pytest.mark.parametrize("eps", [1e-3, 1e-4, 1e-6, 1e-7, 1e-9, 1e-11])
 def test_tolerances(vp, rest, eps):
+    """Every order between the clamps (P = 16 at 1e-3 ... 50 at 1e-12): the P2M
+    quarters (ceil(P/4) = 4 ... 13 powers per lane), the M2L instances with a
+    compile-time k-step count (P = 27, 39, 50) and the generic ones."""
     w = W.cfg1()
     with vp.SummationPlan(lap(vp), w.src, w.tgt, eps) as plan:
         gpu = plan.apply(w.q)
