@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define VPG_ABI_VERSION 2  /* 2: vpg_plan_info_t.near_symmetric, vpg_layer_* */
+#define VPG_ABI_VERSION 3  /* 2: vpg_plan_info_t.near_symmetric, vpg_layer_*; 3: near_lattice (was reserved) */
 
 typedef enum {
     VPG_OK = 0,
@@ -99,7 +99,7 @@ typedef struct {
     int64_t m2m_children, l2l_children;
     int64_t device_bytes;    /* resident plan footprint */
     int32_t near_symmetric;  /* 1: near field by unordered pairs (fmm.cu p2p_sym_kernel) */
-    int32_t reserved;
+    int32_t near_lattice;    /* 1: near field as dense K_o q products of translation-invariant leaves (lattice.cu) */
 } vpg_plan_info_t;
 
 /* Phase timings of the most recent apply on a plan with profiling on, in

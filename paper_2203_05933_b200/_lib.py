@@ -79,7 +79,7 @@ class PlanInfo(C.Structure):
         ("epsilon", C.c_double), ("x0", C.c_double), ("y0", C.c_double),
         ("side", C.c_double), ("m2l_pairs", C.c_int64), ("p2p_pairs", C.c_int64),
         ("m2m_children", C.c_int64), ("l2l_children", C.c_int64),
-        ("device_bytes", C.c_int64), ("near_symmetric", C.c_int32), ("reserved", C.c_int32),
+        ("device_bytes", C.c_int64), ("near_symmetric", C.c_int32), ("near_lattice", C.c_int32),
     ]
 
 

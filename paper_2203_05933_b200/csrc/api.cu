@@ -573,6 +573,7 @@ int vpg_plan_info(const vpg_plan* plan, vpg_plan_info_t* info) {
         r.l2l_children = pl.l2l_children;
         r.device_bytes = pl.device_bytes();
         r.near_symmetric = pl.sym ? 1 : 0;
+        r.near_lattice = pl.lat ? 1 : 0;
         *info = r;
     });
 }

@@ -1270,6 +1270,8 @@ sym_finalize_kernel(const SymLeaf* leaves, int64_t nleaves, const double* part, 
                     FarArgs far) {
     extern __shared__ double2 smp[];
     __shared__ double2 rowbuf[kFar ? kFinWarps : 1][64];
+    const bool coin = !(add & 4);  // 4: the slots hold exact sums (lattice.cu skips r^2 == 0 itself)
+    add &= 3;
     double2* tab = smp;
     int* rbuf = reinterpret_cast<int*>(smp + kLogTableSize * kLogTableCopies);  // [warps][2][64]
     uint32_t tab_lane = 0;
@@ -1340,8 +1342,10 @@ sym_finalize_kernel(const SymLeaf* leaves, int64_t nleaves, const double* part, 
                 continue;
             }
             const double2 tp = txy[t];
-            if constexpr (kTable) sum += coin_correction(coin_off, coin_src, t, tp.x, tp.y, sxy, q, tab_lane);
-            else sum += coin_correction(coin_off, coin_src, t, tp.x, tp.y, sxy, q, gtab);
+            if (coin) {
+                if constexpr (kTable) sum += coin_correction(coin_off, coin_src, t, tp.x, tp.y, sxy, q, tab_lane);
+                else sum += coin_correction(coin_off, coin_src, t, tp.x, tp.y, sxy, q, gtab);
+            }
             double& o = out[tids[t]];
             if constexpr (kFar) {
                 const double o0 = farv;
@@ -1875,6 +1879,7 @@ void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const L
     auto sym_finalize = [&](cudaStream_t s, int mode) {
         // the table variant only for unmatched targets summed one-sided here
         const bool table = pl.sym_unmatched && mode != 1;
+        const int kmode = mode | (pl.lat ? 4 : 0);
         const auto fk = mode == 3 ? sym_finalize_kernel<false, true>
                                   : table ? sym_finalize_kernel<true, false> : sym_finalize_kernel<false, false>;
         const size_t fsmem = table ? kFinSmem : 0;
@@ -1887,13 +1892,17 @@ void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const L
                    (const int2*)pl.near_ranges.p, (const double2*)pl.src_sorted.p,
                    (const double*)qs, (const double2*)pl.tgt_sorted.p, (const int32_t*)pl.tgt_ids.p,
                    (const int32_t*)pl.coin_off.p, (const int32_t*)pl.coin_src.p, lap_log_table_dev(),
-                   out_dev, mode,
+                   out_dev, kmode,
                    FarArgs{(const int32_t*)pl.l2p_rows.p, (const double2*)loc, (const int32_t*)pl.row_level.p,
                            (const int32_t*)pl.row_morton.p, P, pl.x0, pl.y0, pl.side});
         ++launches;
     };
     auto near_field = [&](cudaStream_t s) {
         if (pl.sym) {
+            if (pl.lat) {  // translation-invariant leaves: dense GEMMs on the tensor cores (lattice.cu)
+                lattice_near_issue(pl, qs, w.sym_part, s);
+                ++launches;
+            }
             if (pl.n_sym_tasks > 0) {
                 int per_sm = 1;
                 constexpr int kSymWarps = SymShape<LapLogK>::kWarps;

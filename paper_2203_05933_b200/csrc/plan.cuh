@@ -228,6 +228,14 @@ struct Plan {
     int32_t sym_chunk = 0;    // column chunk (whole-tree decision, shards reuse it)
     bool sym_l2p_single = false;  // every symmetric leaf evaluates one local expansion (its own)
     double sym_fair = 0.0;    // pairs per subtask (whole-tree decision)
+    // translation-invariant leaves (lattice.cu): the near field as dense GEMMs K_o . q on the
+    // FP64 tensor cores; sym_leaves then holds one-slot leaves for the finalize
+    bool lat = false;
+    int lat_m = 0, lat_nt = 64;   // points per leaf, column tile of the kernel
+    int64_t lat_ncol = 0;         // target leaves of the schedule
+    double lat_pairs_exec = 0.0;  // m^2 x 9 x leaves: multiply-adds per apply (boundary zeros included)
+    DBuf<double> lat_K;           // [9][m / 32][32][m + 4]
+    DBuf<int32_t> lat_nbr;        // [leaf][9]: first sorted charge of the neighbour leaf, -1 outside
     std::vector<LeafNear> h_leafnear;
     int64_t n_p2p_chunks = 0;
     int64_t n_p2p_heavy = 0;  // split chunks (counters)
@@ -380,6 +388,8 @@ void direct_sum_device(int family, double lambda, const double2* src,
                        unsigned long long* clash, cudaStream_t st);
 // helm.cu
 void build_helm_ops(Plan& pl);
+bool build_lattice_near(Plan& pl, int64_t lb, int64_t le);  // lattice.cu
+void lattice_near_issue(const Plan& pl, const double* qs, double* near, cudaStream_t st);
 void build_helm_fmm(Plan& pl);  // native mode (helm.cu)
 void hf_build_m2l(Plan& pl, int64_t lb, int64_t le);  // its M2L schedule for the targets of a leaf range
 size_t helm_work_bytes(const Plan& pl);  // Chebyshev FMM apply scratch (helm.cu)

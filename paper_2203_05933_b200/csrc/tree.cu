@@ -683,6 +683,8 @@ void build_sym_near(Plan& pl, int64_t lb, int64_t le) {
     const char* fv = std::getenv("VPG_SYM");  // 0: never, 1: always (when applicable), unset: by cost
     const int force = fv ? std::atoi(fv) : -1;
     if (force == 0 || !pl.matched || pl.adaptive || pl.direct || (pl.family != VPG_LAPLACE && !pl.hf)) return;
+    pl.lat = false;
+    if (pl.family == VPG_LAPLACE && pl.coin_ready && build_lattice_near(pl, lb, le)) return;  // leaves are translates of one pattern
     const int L = pl.L;
     const int nb = 1 << L;
     const int64_t nleaf = int64_t(1) << (2 * L);
