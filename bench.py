@@ -561,11 +561,18 @@ def run_gpu(args):
             # for the pair plus 2 for the second accumulation, per 2 ordered pairs
             p2p_flops = info["p2p_pairs"] / 2.0 * 29.0
             kern_stats["p2p"]["tflops_executed_sym"] = p2p_flops / (phases["p2p"] * 1e-3) / 1e12 if phases["p2p"] else None
+        lattice = bool(info.get("near_lattice"))
+        if lattice:
+            # translation-invariant leaves (lattice.cu): the near field is sum_o K_o q on the
+            # FP64 tensor cores, one multiply-add per near pair
+            p2p_flops = info["p2p_pairs"] * 2.0
+            kern_stats["p2p"]["tflops_executed_lattice"] = p2p_flops / (phases["p2p"] * 1e-3) / 1e12 if phases["p2p"] else None
+            kern_stats["p2p"].pop("tflops_executed_sym", None)
         flops = m2l_flops if dom == "m2l" else p2p_flops
         achieved = flops / (phases[dom] * 1e-3) / 1e12
-        near_k = "p2p_sym_kernel" if info.get("near_symmetric") else "l2p_p2p_kernel"
+        near_k = "lattice_near_kernel" if lattice else "p2p_sym_kernel" if info.get("near_symmetric") else "l2p_p2p_kernel"
         kname = "m2l_kernel" if dom == "m2l" else near_k
-        bound = "tensor" if dom == "m2l" else "fp64"
+        bound = "tensor" if dom == "m2l" or lattice else "fp64"
         peak = fp64_peak_tflops(bound)
         roofline = {"bound": bound, "kernel": kname,
                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
@@ -573,9 +580,13 @@ def run_gpu(args):
                     "peak_source": ("measured FP64 tensor-core (DMMA, tools/dmma_peak.cu)" if bound == "tensor"
                                     else "measured FP64 CUDA-core (DFMA, tools/fp64_peak.cu)")
                                    + " peak, profiles/fp64_peak_r01.json; MEASURED_PEAKS.json has no FP64 entry",
-                    "bound_note": ("M2L runs on the FP64 tensor cores (mma.sync m8n8k4 f64)" if bound == "tensor"
+                    "bound_note": ("M2L runs on the FP64 tensor cores (mma.sync m8n8k4 f64)" if dom == "m2l"
+                                   else "leaves are translates of one point pattern: the near field is the dense "
+                                        "contraction sum_o K_o q (K_o = ln r^2 blocks formed once per plan) on the "
+                                        "FP64 tensor cores; phase time includes the finalize" if lattice
                                    else "the near-field log sum is FP64 CUDA-core work (no tensor-core form)"),
                     "flops_per_unit": ("4P(P+1)+8(P+1)+6P executed per M2L pair" if dom == "m2l"
+                                       else "2 per near-field pair (one multiply-add of the precomputed ln r^2)" if lattice
                                        else "27 per near-field pair (SURVEY.md 8d convention)"
                                        if near_k != "p2p_sym_kernel" else
                                        "29 per unordered near-field pair (27 per pair, SURVEY.md 8d, + 2 for the "

@@ -36,7 +36,7 @@ def test_python_binding_matches_header():
     from paper_2203_05933_b200 import _lib
     assert sorted(_lib.EXPORTED_SYMBOLS) == declared()
     h = _lib.lib()
-    assert h.vpg_abi_version() == 2
+    assert h.vpg_abi_version() == 3
 
 
 def test_device_query_does_not_crash():

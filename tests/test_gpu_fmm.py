@@ -346,3 +346,53 @@ def test_subnormal_pairs_across_leaf_edges(vp, rest, monkeypatch, sym):
         gpu = plan.apply(q)
     cpu = rest.plan_sum(0, 0.0, pts, q, pts, 1e-12)
     assert rel_l2(gpu, cpu) <= 1e-13
+
+
+def _lattice_points(nbox, nx, ny):
+    """nbox x nbox boxes on [-1, 1]^2, each an nx x ny tensor Gauss-Legendre rule."""
+    h = 2.0 / nbox
+    gx, _ = np.polynomial.legendre.leggauss(nx)
+    gy, _ = np.polynomial.legendre.leggauss(ny)
+    c = -1.0 + (np.arange(nbox) + 0.5) * h
+    X = (c[None, :, None, None] + 0.5 * h * gx[None, None, None, :]) + 0.0 * c[:, None, None, None] + 0.0 * gy[None, None, :, None]
+    Y = (c[:, None, None, None] + 0.5 * h * gy[None, None, :, None]) + 0.0 * c[None, :, None, None] + 0.0 * gx[None, None, None, :]
+    return np.stack([X.ravel(), Y.ravel()], axis=1)
+
+
+@pytest.mark.parametrize("nx,ny,m", [(8, 8, 64), (16, 8, 128)])
+def test_lattice_near_field(vp, rest, monkeypatch, nx, ny, m):
+    """Leaves that are translates of one point pattern (one box per leaf, 64 or
+    128 nodes): the near field runs as dense K_o q products (lattice.cu) and
+    agrees with the pairwise kernels to rounding and with the oracle; shards
+    assemble bit-exactly; one node moved by 1e-9 sends the plan back to the
+    pairwise kernels."""
+    from paper_2203_05933_b200 import multigpu
+    pts = _lattice_points(128, nx, ny)
+    rng = np.random.default_rng(77)
+    q = rng.standard_normal(len(pts)) * np.exp(-3.0 * (pts[:, 0] ** 2 + pts[:, 1] ** 2))
+    with vp.SummationPlan(lap(vp), pts, pts, 1e-12) as plan:
+        info = plan.info()
+        assert info["levels"] == 7 and info["near_lattice"] == 1
+        lat = plan.apply(q)
+        total = np.zeros_like(lat)
+        for r in range(3):
+            multigpu.shard_plan(plan, r, 3)
+            total += plan.apply(q)
+        plan.set_shard(0, 4 ** plan.levels())
+        assert np.array_equal(total, lat)
+        assert np.array_equal(plan.apply(q), lat)
+    monkeypatch.setenv("VPG_LATTICE", "0")
+    with vp.SummationPlan(lap(vp), pts, pts, 1e-12) as plan:
+        assert plan.info()["near_lattice"] == 0
+        pair = plan.apply(q)
+    assert rel_l2(lat, pair) <= 1e-14
+    monkeypatch.delenv("VPG_LATTICE")
+    if m == 64:
+        cpu = rest.plan_sum(0, 0.0, pts, q, pts, 1e-12)
+        assert rel_l2(lat, cpu) <= 1e-13
+    moved = pts.copy()
+    moved[12345, 0] += 1e-9
+    with vp.SummationPlan(lap(vp), moved, moved, 1e-12) as plan:
+        assert plan.info()["near_lattice"] == 0
+        gpu = plan.apply(q)
+    assert rel_l2(gpu, pair) <= 1e-9 and not np.array_equal(gpu, pair)

@@ -1,7 +1,8 @@
 """Parity at the >= 1M-node configurations the north star targets.
 
-* cfg4 (BASELINE configs[3], 4,194,304 nodes, reference tree L = 7 with the
-  symmetric near field at 256 points per leaf) at eps = 1e-12, 1e-9, 1e-6:
+* cfg4 (BASELINE configs[3], 4,194,304 nodes, reference tree L = 7, 256 points
+  per leaf: the lattice near field (lattice.cu), and with VPG_LATTICE=0 the
+  symmetric pairwise kernel) at eps = 1e-12, 1e-9, 1e-6:
   the whole potential vector against the unmodified reference
   SummationPlan::apply (oracle/_ref, summation.cpp:610-643) on the host
   cores, and 2,000 seeded targets against the long-double pairwise sum
@@ -44,7 +45,7 @@ def test_cfg4_vs_reference_apply(vp, ref, cfg4, cfg4_ld, eps, order):
     with vp.SummationPlan(lap(vp), w.src, w.tgt, eps) as plan:
         info = plan.info()
         assert info["levels"] == 7 and info["expansion_order"] == order
-        assert info["near_symmetric"] == 1  # the cost model picks the symmetric kernel here
+        assert info["near_symmetric"] == 1 and info["near_lattice"] == 1  # leaves are translates of one pattern
         assert info["p2p_pairs"] == 9_563_275_264  # the instrumented reference's count
         assert info["m2l_pairs"] == 568_872
         gpu = plan.apply(w.q)
@@ -60,17 +61,33 @@ def test_cfg4_vs_reference_apply(vp, ref, cfg4, cfg4_ld, eps, order):
     assert rel_l2(cpu[idx], ld) <= max(eps, 1e-12)
 
 
-def test_cfg4_one_sided_near_field_agrees(vp, cfg4, monkeypatch):
-    """The one-sided near-field kernel (VPG_SYM=0) and the symmetric one give
-    the same potentials at cfg4 to rounding."""
+def test_cfg4_near_field_paths_agree(vp, ref, cfg4, cfg4_ld, monkeypatch):
+    """The three near-field forms at cfg4: the lattice GEMMs (default), the
+    symmetric pairwise kernel (VPG_LATTICE=0, the cost model's choice among the
+    pairwise kernels) and the one-sided kernel (VPG_SYM=0) give the same
+    potentials to rounding, and the pairwise symmetric one matches the reference
+    apply and the long-double sums on its own."""
     w = cfg4
     with vp.SummationPlan(lap(vp), w.src, w.tgt, 1e-12) as plan:
+        assert plan.info()["near_lattice"] == 1
+        lat = plan.apply(w.q)
+    monkeypatch.setenv("VPG_LATTICE", "0")
+    with vp.SummationPlan(lap(vp), w.src, w.tgt, 1e-12) as plan:
+        info = plan.info()
+        assert info["near_symmetric"] == 1 and info["near_lattice"] == 0
         sym = plan.apply(w.q)
     monkeypatch.setenv("VPG_SYM", "0")
     with vp.SummationPlan(lap(vp), w.src, w.tgt, 1e-12) as plan:
         assert plan.info()["near_symmetric"] == 0
         one = plan.apply(w.q)
     assert rel_l2(sym, one) <= 1e-14
+    assert rel_l2(lat, one) <= 1e-14
+    rp = ref.plan(0, 0.0, w.src, w.tgt, 1e-12)
+    cpu = rp.apply(w.q)
+    rp.close()
+    assert rel_l2(sym, cpu) <= 1e-13
+    idx, ld = cfg4_ld
+    assert rel_l2(sym[idx], ld) <= 1e-12
 
 
 def test_cfg3_reference_mode(vp, ref, rest):
