@@ -1301,14 +1301,34 @@ sym_finalize_kernel(const SymLeaf* leaves, int64_t nleaves, const double* part, 
             box_center(far.x0, far.y0, s, uint32_t(far.row_morton[r]), fcx, fcy);
             finv = 1.0 / s;
         }
+        // fused far field: the next target's coordinates, id and first slot are fetched under
+        // the current target's Horner chain (the lane's targets are otherwise serial round trips)
+        double2 tp_n = make_double2(0.0, 0.0);
+        double a_n = 0.0;
+        int id_n = 0;
+        if constexpr (kFar) {
+            if (lane < lf.n) {
+                tp_n = txy[int64_t(lf.tgt) + lane];
+                id_n = tids[int64_t(lf.tgt) + lane];
+                a_n = __ldcg(part + lf.pbase + lane);
+            }
+        }
         for (int k = lane; k < lf.n; k += 32) {
             const int64_t t = int64_t(lf.tgt) + k;
             const double* pk = part + lf.pbase + k;
             double sum = 0.0;
             int sl = 0;
             double farv = 0.0;
+            const double2 tp_c = tp_n;
+            const double a_c = a_n;
+            const int id_c = id_n;
             if constexpr (kFar) {  // issued ahead of the slot loads' use: the Horner chain hides them
-                const double2 tp = txy[t];
+                if (k + 32 < lf.n) {
+                    tp_n = txy[t + 32];
+                    id_n = tids[t + 32];
+                    a_n = __ldcg(pk + 32);
+                }
+                const double2 tp = tp_c;
                 const double2* buf = rowbuf[warp];
                 const double ur = (tp.x - fcx) * finv, ui = (tp.y - fcy) * finv;
                 double ar = buf[far.P].x, ai = buf[far.P].y;
@@ -1320,6 +1340,20 @@ sym_finalize_kernel(const SymLeaf* leaves, int64_t nleaves, const double* part, 
                     ai = nai;
                 }
                 farv = -kInv2Pi * (0.0 + ar);
+            }
+            if constexpr (kFar) {  // slot 0 came with the prefetch
+                if (lf.nslot > 0) {
+                    sum += a_c;
+                    sl = 1;
+                }
+                if (lf.nslot >= 8) {  // slots 1..7 in flight together
+                    double a[7];
+#pragma unroll
+                    for (int u = 0; u < 7; ++u) a[u] = __ldcg(pk + int64_t(1 + u) * lf.n);
+#pragma unroll
+                    for (int u = 0; u < 7; ++u) sum += a[u];
+                    sl = 8;
+                }
             }
             for (; sl + 8 <= lf.nslot; sl += 8) {  // eight loads in flight, added in slot order
                 double a[8];
@@ -1341,12 +1375,12 @@ sym_finalize_kernel(const SymLeaf* leaves, int64_t nleaves, const double* part, 
                 out[tids[t]] += -kInv4Pi * sum;
                 continue;
             }
-            const double2 tp = txy[t];
+            const double2 tp = kFar ? tp_c : txy[t];
             if (coin) {
                 if constexpr (kTable) sum += coin_correction(coin_off, coin_src, t, tp.x, tp.y, sxy, q, tab_lane);
                 else sum += coin_correction(coin_off, coin_src, t, tp.x, tp.y, sxy, q, gtab);
             }
-            double& o = out[tids[t]];
+            double& o = out[kFar ? id_c : tids[t]];
             if constexpr (kFar) {
                 const double o0 = farv;
                 o = o0 + -kInv4Pi * sum;
