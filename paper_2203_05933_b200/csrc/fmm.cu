@@ -2009,7 +2009,10 @@ void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const L
         }
     }
     mark(3);
-    if (pl.n_m2l_batches > 0) {
+    if (pl.n_gt_tiles > 0 && pl.n_m2l_batches > 0) {  // uniform tree: by offset (m2lgrid.cu), same bits
+        m2l_grid_issue(pl, (const double2*)mult, loc, st);
+        ++launches;
+    } else if (pl.n_m2l_batches > 0) {
         const size_t smem = sizeof(double) * size_t(pl.KP) * kM2LHS +
                             sizeof(double2) * (size_t(kM2LCanon) * n + 49) + sizeof(int32_t) * 52 +
                             kM2LRaw * sizeof(double2) * size_t(kM2LPairs) * n +

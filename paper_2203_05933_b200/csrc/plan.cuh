@@ -125,6 +125,11 @@ constexpr int kSymMaxRanges = 9;
 #define VPG_SYM_MAXR 4
 #endif
 constexpr int kSymLapMaxR = VPG_SYM_MAXR;
+// M2L by offset (m2lgrid.cu): up to 32 target boxes of one level and one position in the parent
+struct GridTile {
+    int32_t level, cls, first, count;  // first: index into gt_rows / gt_nbr rows
+};
+
 struct LeafNear {  // per-leaf near-field data of the last schedule (host)
     int32_t leaf, t0, t1, rfirst, rcount, rself, lfirst, lcount;
 };
@@ -186,6 +191,10 @@ struct Plan {
     int64_t n_tbox = 0, n_m2l = 0;
     DBuf<M2LBatch> m2l_batches;
     int64_t n_m2l_batches = 0;
+    // uniform trees: the by-offset M2L schedule (m2lgrid.cu); 0 tiles: m2l_kernel runs the batches
+    DBuf<GridTile> gt_tiles;
+    DBuf<int32_t> gt_rows, gt_nbr, gt_oidx;  // target rows; [row][27] source rows or -1; [4][27] offset ids
+    int64_t n_gt_tiles = 0;
 
     // Laplace operators (summation.cpp:150-222), uploaded once.
     DBuf<double> m2m_ops, l2l_ops;  // binomial triangles of the factorised M2M / L2L
@@ -388,6 +397,8 @@ void direct_sum_device(int family, double lambda, const double2* src,
                        unsigned long long* clash, cudaStream_t st);
 // helm.cu
 void build_helm_ops(Plan& pl);
+void build_m2l_grid(Plan& pl, int64_t lb, int64_t le);  // m2lgrid.cu
+void m2l_grid_issue(const Plan& pl, const double2* mult, double2* loc, cudaStream_t st);
 bool build_lattice_near(Plan& pl, int64_t lb, int64_t le);  // lattice.cu
 void lattice_near_issue(const Plan& pl, const double* qs, double* near, cudaStream_t st);
 void build_helm_fmm(Plan& pl);  // native mode (helm.cu)

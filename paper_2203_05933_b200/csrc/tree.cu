@@ -563,6 +563,7 @@ void build_schedules(Plan& pl, int64_t lb, int64_t le) {
         pl.n_m2l_batches = int64_t(batches.size());
         to_device(pl.m2l_batches, batches, st);
     }
+    build_m2l_grid(pl, lb, le);  // the same entries batched by offset (uniform Laplace trees)
     {
         std::vector<int32_t> boxes;  // parent rows
         std::vector<int4> kids;      // child rows per quadrant, -1 = none

@@ -396,3 +396,25 @@ def test_lattice_near_field(vp, rest, monkeypatch, nx, ny, m):
         assert plan.info()["near_lattice"] == 0
         gpu = plan.apply(q)
     assert rel_l2(gpu, pair) <= 1e-9 and not np.array_equal(gpu, pair)
+
+
+@pytest.mark.parametrize("eps", [1e-12, 1e-6, 1e-4])
+def test_m2l_by_offset_agrees(vp, monkeypatch, eps):
+    """The opt-in M2L batched by offset (m2lgrid.cu, VPG_M2L_GRID=1): same
+    factorisation, same arithmetic per list entry and same order of the entry
+    sums as the per-target-box kernel, so the potentials agree to rounding -- on
+    cfg2 (irregular occupancy, empty boxes, domain edges) and on a shard."""
+    from paper_2203_05933_b200 import multigpu
+    w = W.cfg2()
+    with vp.SummationPlan(lap(vp), w.src, w.tgt, eps) as plan:
+        box = plan.apply(w.q)
+        multigpu.shard_plan(plan, 1, 3)
+        box_shard = plan.apply(w.q)
+    monkeypatch.setenv("VPG_M2L_GRID", "1")
+    with vp.SummationPlan(lap(vp), w.src, w.tgt, eps) as plan:
+        grid = plan.apply(w.q)
+        multigpu.shard_plan(plan, 1, 3)
+        grid_shard = plan.apply(w.q)
+    assert rel_l2(grid, box) <= 1e-14
+    assert rel_l2(grid_shard, box_shard) <= 1e-14
+    assert np.array_equal(grid_shard != 0.0, box_shard != 0.0)
