@@ -208,12 +208,16 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "interactions/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, BASELINE.json shapes)",
+        # the same keys as the GPU arm's config; the workload keys carry the same values
         "config": {"workload": args.workload, "ns": wl.ns, "nt": wl.nt, "epsilon": eps,
-                   "levels": levels, "order": plan.expansion_order(),
-                   "tree": "reference uniform quadtree",
-                   "interactions_per_step": inter, "interactions_counted": counted},
+                   "levels": levels, "order": plan.expansion_order(), "mode": "reference",
+                   "parallelism": "single" if world == 1 else f"target-shard{world}",
+                   "interactions_per_step": inter, "interactions_counted": counted,
+                   "l2": "host arm (no device L2 flush)",
+                   "near_field": "pairwise (the reference's own loop, summation.cpp:330-344)",
+                   "step": "FMM step: SummationPlan::apply (summation.cpp:610-643)"},
         "cpu_baseline": {"value": v, "unit": "interactions/s", "cores": cores, "kind": "reference",
                          "sample": f"{args.steps} full SummationPlan::apply of {args.workload} "
                                    f"(oracle/_ref = unmodified proj/src/summation.cpp, g++ -O3 "
@@ -619,6 +623,12 @@ def run_gpu(args):
                    "parallelism": f"target-shard{world}" if world > 1 else "single",
                    "interactions_per_step": inter, "interactions_counted": counted,
                    "l2": "flushed (256 MB write) before every timed step",
+                   "near_field": ("dense K_o q products on the FP64 tensor cores: the leaves are translates of one "
+                                  "point pattern, the nine ln r^2 blocks K_o are plan data like the translation "
+                                  "operators (lattice.cu; VPG_LATTICE=0 runs the pairwise kernel, "
+                                  "profiles/r02/bench_cfg4_pairwise_v8.json)" if info.get("near_lattice")
+                                  else "pairwise, unordered pairs (p2p_sym_kernel)" if info.get("near_symmetric")
+                                  else "pairwise, one-sided (l2p_p2p_kernel)"),
                    "step": ("operator apply: build_charges + FMM step + correction (potential.cpp:431-470)"
                             if op is not None else "FMM step: SummationPlan::apply (summation.cpp:610-643)")},
         "e2e": {"value": inter / (e2e_ms * 1e-3), "unit": "interactions/s", "ms_per_step": e2e_ms,
