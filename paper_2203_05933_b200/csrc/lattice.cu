@@ -40,6 +40,10 @@
 namespace vpg {
 namespace {
 
+#ifndef VPG_LAT_UNROLL
+#define VPG_LAT_UNROLL 8
+#endif
+constexpr int kLatUnroll = VPG_LAT_UNROLL;  // k-steps unrolled
 constexpr int kLatKC = 32;        // k per chunk
 constexpr int kLatThreads = 256;  // 8 warps
 constexpr int kLatLB = kLatKC + 4;
@@ -145,7 +149,7 @@ lattice_near_kernel(const double* K, const int32_t* nbr, const double* qs, int n
             else mbar_wait(&bar[0], use0++ & 1u);
             __syncthreads();  // Bs written
             const double* Ab = As + size_t(c & 1) * kLatKC * la;
-#pragma unroll 2
+#pragma unroll(kLatUnroll)
             for (int k4 = 0; k4 < kLatKC; k4 += 4) {
                 double a[MTW], b[kNt];
 #pragma unroll
