@@ -1971,7 +1971,10 @@ void laplace_issue(const Plan& pl, const double* q_dev, double* out_dev, const L
     mark(1);
 
     double2* partial = w.p2m_partial;
-    if (pl.n_p2m_items > 0) {
+    if (pl.lat && pl.lat_p2m && pl.n_p2m_items > 0) {  // lattice plans: power sums by one GEMM + per-leaf shift
+        lattice_p2m_issue(pl, qs, w.sym_part + pl.lat_near_parts, mult, st);
+        launches += 2;
+    } else if (pl.n_p2m_items > 0) {
         auto p2m = [&](auto kern) {
             launch_pdl(kern, dim3(nblk(pl.n_p2m_items, kP2MWarps)), dim3(kP2MWarps * 32), 0, st,
                        (const P2MItem*)pl.p2m_items.p, pl.n_p2m_items, (const double2*)pl.src_sorted.p,

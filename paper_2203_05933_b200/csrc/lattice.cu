@@ -77,10 +77,12 @@ __device__ __forceinline__ void lat_dmma(double& c0, double& c1, double a, doubl
                  : "d"(a), "d"(b));
 }
 
-template <int MTW, int NT>
+// KB: k extent of a block (the pattern's point count), NBLK: blocks per column (9 neighbour leaves
+// for the near field; 1 for the pattern's power sums, lattice_p2m_issue)
+template <int MTW, int NT, int KB, int NBLK>
 __global__ void __launch_bounds__(kLatThreads, 1)
 lattice_near_kernel(const double* K, const int32_t* nbr, const double* qs, int ncol, double* near) {
-    constexpr int m = 64 * MTW, la = lat_la(m), kNt = NT / 8, kChunks = 9 * (m / kLatKC);
+    constexpr int m = 64 * MTW, la = lat_la(m), kNt = NT / 8, kChunks = NBLK * (KB / kLatKC);
     constexpr uint32_t kChunkBytes = uint32_t(kLatKC) * la * 8u;
     extern __shared__ __align__(16) double ls[];
     double* As = ls;                                // [2][kLatKC][la]
@@ -117,11 +119,11 @@ lattice_near_kernel(const double* K, const int32_t* nbr, const double* qs, int n
             }
         };
         auto fetch_b = [&](int c) {
-            const int o = c / (m / kLatKC), kc = c % (m / kLatKC);
+            const int o = c / (KB / kLatKC), kc = c % (KB / kLatKC);
 #pragma unroll
             for (int r = 0; r < 4; ++r) breg[r] = make_double2(0.0, 0.0);
             if (bj < nc) {
-                const int src = nbr[int64_t(n0 + bj) * 9 + o];
+                const int src = nbr[int64_t(n0 + bj) * NBLK + o];
                 if (src >= 0) {
                     const double2* p = reinterpret_cast<const double2*>(qs + src + kc * kLatKC + bpart * 8);
 #pragma unroll
@@ -177,7 +179,7 @@ lattice_near_kernel(const double* K, const int32_t* nbr, const double* qs, int n
 }
 
 template <int MTW, int NT>
-size_t lat_smem() {
+size_t lat_smem() {  // (independent of KB / NBLK)
     constexpr int m = 64 * MTW;
     return sizeof(double) * (2 * size_t(kLatKC) * lat_la(m) + size_t(NT) * kLatLB);
 }
@@ -185,10 +187,11 @@ size_t lat_smem() {
 template <int MTW, int NT>
 void lat_launch(const Plan& pl, const double* qs, double* near, cudaStream_t st) {
     const size_t smem = lat_smem<MTW, NT>();
-    smem_optin((const void*)lattice_near_kernel<MTW, NT>, int(smem));
+    smem_optin((const void*)lattice_near_kernel<MTW, NT, 64 * MTW, 9>, int(smem));
     const int ntiles = int((pl.lat_ncol + NT - 1) / NT);
-    launch_pdl(lattice_near_kernel<MTW, NT>, dim3(unsigned(std::min(ntiles, pl.sm_count))), dim3(kLatThreads), smem,
-               st, (const double*)pl.lat_K.p, (const int32_t*)pl.lat_nbr.p, qs, int(pl.lat_ncol), near);
+    launch_pdl(lattice_near_kernel<MTW, NT, 64 * MTW, 9>, dim3(unsigned(std::min(ntiles, pl.sm_count))),
+               dim3(kLatThreads), smem, st, (const double*)pl.lat_K.p, (const int32_t*)pl.lat_nbr.p, qs,
+               int(pl.lat_ncol), near);
 }
 
 template <int MTW>
@@ -201,6 +204,81 @@ void lat_launch_nt(const Plan& pl, const double* qs, double* near, cudaStream_t 
     }
 }
 
+
+// ---- P2M of lattice plans.  Every leaf is the pattern shifted by its translation, and the
+// tree's box centres drift against the lattice by d_A = (translation - centre offset) / s
+// (the bounding box is not a multiple of the pitch: |d| <= ~2% of a box on cfg4), so with
+// w0_j the pattern's points about the pattern leaf's centre,
+//   sum_j q_j (w0_j + d_A)^k = sum_{i <= k} C(k, i) d_A^(k - i) S_i(A),   S_i(A) = sum_j q_j w0_j^i:
+// the power sums S (re, im rows of the fixed matrix V = w0^i, 2 (P + 1) <= 128 rows) are ONE
+// GEMM V . q for all leaves on the tensor cores (the kernel above, one block per column), and a
+// warp per leaf applies the binomial shift and the -1/k (summation.cpp:247-254's multipoles
+// to rounding; the coordinates enter through the pattern as in the near field).
+constexpr int kLatSRows = 128;
+
+__global__ void __launch_bounds__(128)
+lat_p2m_shift_kernel(const double* S, const double2* drift, const int32_t* rows, const double* binom, int ncol,
+                     int P, double2* mult) {
+    __shared__ double2 sp[4][64], dp[4][64];
+    __shared__ double bsm[51 * 51];  // C(k, i): lanes differ in k, so not the constant bank
+    for (int i = threadIdx.x; i < 51 * 51; i += blockDim.x) bsm[i] = binom[i];
+    __syncthreads();
+    pdl_trigger();
+    pdl_wait();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int n = P + 1;
+    for (int col = blockIdx.x * 4 + warp; col < ncol; col += gridDim.x * 4) {
+        const double2 d = drift[col];
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int i = lane + 32 * h;
+            if (i <= P) {
+                sp[warp][i] = make_double2(S[int64_t(col) * kLatSRows + 2 * i], S[int64_t(col) * kLatSRows + 2 * i + 1]);
+                double2 r = make_double2(1.0, 0.0), b = d;  // d^i by binary powering
+                for (int e = i; e; e >>= 1) {
+                    if (e & 1) r = make_double2(r.x * b.x - r.y * b.y, r.x * b.y + r.y * b.x);
+                    b = make_double2(b.x * b.x - b.y * b.y, 2.0 * b.x * b.y);
+                }
+                dp[warp][i] = r;
+            }
+        }
+        __syncwarp();
+        double2* dst = mult + int64_t(rows[col]) * n;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int k = lane + 32 * h;
+            const int kk = min(k, P);             // idle lanes shadow k = P (result dropped)
+            const int kmax = min(31 + 32 * h, P);  // the warp's longest sum: one trip count for every lane
+            const double* brow = bsm + kk * 51;
+            double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;  // two interleaved partial sums (even / odd i)
+            for (int i = 0; i <= kmax; i += 2) {
+                const int j0 = kk - i, j1 = kk - i - 1;
+                const double c0 = i <= kk ? brow[i] : 0.0, c1 = i + 1 <= kk ? brow[i + 1] : 0.0;
+                const double2 s0 = sp[warp][i], s1 = sp[warp][min(i + 1, P)];
+                const double2 t0 = dp[warp][max(j0, 0)], t1 = dp[warp][max(j1, 0)];
+                ar = fma(c0, s0.x * t0.x - s0.y * t0.y, ar);
+                ai = fma(c0, s0.x * t0.y + s0.y * t0.x, ai);
+                br = fma(c1, s1.x * t1.x - s1.y * t1.y, br);
+                bi = fma(c1, s1.x * t1.y + s1.y * t1.x, bi);
+            }
+            if (k <= P) {
+                const double f = k ? -1.0 / double(k) : 1.0;
+                dst[k] = make_double2(f * (ar + br), k ? f * (ai + bi) : 0.0);
+            }
+        }
+    }
+}
+
+template <int NT, int KB>
+void lat_p2m_launch(const Plan& pl, const double* qs, double* S, cudaStream_t st) {
+    const size_t smem = lat_smem<2, NT>();
+    smem_optin((const void*)lattice_near_kernel<2, NT, KB, 1>, int(smem));
+    const int ntiles = int((pl.lat_p2m_ncol + NT - 1) / NT);
+    launch_pdl(lattice_near_kernel<2, NT, KB, 1>, dim3(unsigned(std::min(ntiles, pl.sm_count))), dim3(kLatThreads),
+               smem, st, (const double*)pl.lat_V.p, (const int32_t*)pl.lat_p2m_src.p, qs, int(pl.lat_p2m_ncol), S);
+}
+
 }  // namespace
 
 // The apply's near field: near[col m + i] = sum over the 3 x 3 leaves of K_o q.
@@ -210,6 +288,79 @@ void lattice_near_issue(const Plan& pl, const double* qs, double* near, cudaStre
         case 128: return lat_launch_nt<2>(pl, qs, near, st);
         default: return lat_launch_nt<4>(pl, qs, near, st);
     }
+}
+
+// P2M of a lattice plan: S = V q for every non-empty leaf, then the per-leaf shift into the
+// multipole rows.  S: scratch of lat_p2m_ncol x 128 doubles.
+void lattice_p2m_issue(const Plan& pl, const double* qs, double* S, double2* mult, cudaStream_t st) {
+    switch (pl.lat_m) {
+        case 64: lat_p2m_launch<64, 64>(pl, qs, S, st); break;
+        case 128: lat_p2m_launch<64, 128>(pl, qs, S, st); break;
+        default: lat_p2m_launch<64, 256>(pl, qs, S, st); break;
+    }
+    const unsigned grid = unsigned(std::min<int64_t>((pl.lat_p2m_ncol + 3) / 4, int64_t(pl.sm_count) * 8));
+    launch_pdl(lat_p2m_shift_kernel, dim3(grid), dim3(128), 0, st, (const double*)S, (const double2*)pl.lat_drift.p,
+               (const int32_t*)pl.lat_p2m_rows.p, (const double*)pl.lat_binom.p, int(pl.lat_p2m_ncol), pl.P, mult);
+}
+
+// Host side of the lattice P2M (called by build_lattice_near once the pattern is verified).
+static void build_lattice_p2m(Plan& pl, const double2* pat, int64_t first, double px, double py) {
+    pl.lat_p2m = false;
+    const char* ev = std::getenv("VPG_LATTICE_P2M");
+    if (ev && std::atoi(ev) == 0) return;
+    const int P = pl.P, L = pl.L, m = pl.lat_m;
+    if (P > 50 || 2 * (P + 1) > kLatSRows || pl.up_cap != 0 || pl.multilevel_up || pl.n_p2m_splits > 0) return;
+    const int64_t nleaf = int64_t(1) << (2 * L);
+    const std::vector<int32_t>& so = pl.h_soff;
+    const double s = pl.side / double(1 << L);
+    const int fx = int(squash2(uint32_t(first))), fy = int(squash2(uint32_t(first) >> 1));
+    const double c0x = pl.x0 + (fx + 0.5) * s, c0y = pl.y0 + (fy + 0.5) * s;
+    // V in the kernel's chunk order: [kc][kk][la], element (kk, r) = V[r][32 kc + kk], rows r = 2 i + part
+    const int la = lat_la(kLatSRows);
+    std::vector<double> V(size_t(m) * la, 0.0);
+    for (int j = 0; j < m; ++j) {
+        const long double wr = ((long double)pat[j].x - c0x) / s, wi = ((long double)pat[j].y - c0y) / s;
+        long double pr = 1.0L, pi = 0.0L;
+        for (int i = 0; i <= P; ++i) {
+            V[size_t(j) * la + 2 * i] = double(pr);
+            V[size_t(j) * la + 2 * i + 1] = double(pi);
+            const long double nr = pr * wr - pi * wi;
+            pi = pr * wi + pi * wr;
+            pr = nr;
+        }
+    }
+    std::vector<int32_t> src, rows;
+    std::vector<double2> drift;
+    int64_t items = 0;
+    for (int64_t b = 0; b < nleaf; ++b) {
+        if (so[size_t(b) + 1] == so[size_t(b)]) continue;
+        const int ix = int(squash2(uint32_t(b))), iy = int(squash2(uint32_t(b) >> 1));
+        src.push_back(so[size_t(b)]);
+        rows.push_back(int32_t(lvl_base(L) - lvl_base(2) + b));
+        // translation of the leaf's points minus the offset of its box centre, in box units
+        const long double tx = (long double)(ix - fx) * px, ty = (long double)(iy - fy) * py;
+        const long double cx = (long double)pl.x0 + (ix + 0.5L) * s, cy = (long double)pl.y0 + (iy + 0.5L) * s;
+        drift.push_back(make_double2(double((tx - (cx - c0x)) / s), double((ty - (cy - c0y)) / s)));
+        ++items;
+    }
+    if (items != pl.n_p2m_items) return;  // the P2M items are exactly the non-empty leaves
+    std::vector<double> binom(51 * 51, 0.0);
+    for (int k = 0; k <= 50; ++k) {
+        binom[size_t(k) * 51] = 1.0;
+        for (int i = 1; i <= k; ++i)
+            binom[size_t(k) * 51 + i] = binom[size_t(k - 1) * 51 + i - 1] + (i <= k - 1 ? binom[size_t(k - 1) * 51 + i] : 0.0);
+    }
+    auto up = [](auto& d, const auto& h) {
+        d.alloc(std::max<size_t>(h.size(), 1));
+        VPG_CUDA(cudaMemcpy(d.p, h.data(), h.size() * sizeof(h[0]), cudaMemcpyHostToDevice));
+    };
+    up(pl.lat_V, V);
+    up(pl.lat_binom, binom);
+    up(pl.lat_p2m_src, src);
+    up(pl.lat_p2m_rows, rows);
+    up(pl.lat_drift, drift);
+    pl.lat_p2m_ncol = items;
+    pl.lat_p2m = true;
 }
 
 // Decides whether the plan's leaves are translates of one pattern and, if
@@ -333,6 +484,9 @@ bool build_lattice_near(Plan& pl, int64_t lb, int64_t le) {
     pl.sym_l2p_single = true;
     for (const SymLeaf& lf : leaves) pl.sym_l2p_single = pl.sym_l2p_single && lf.lcount == 1;
     pl.lat_pairs_exec = double(pl.lat_ncol) * 9.0 * double(m) * double(m);
+    pl.lat_near_parts = pl.sym_nparts;
+    build_lattice_p2m(pl, pat, first, px, py);
+    if (pl.lat_p2m) pl.sym_nparts += pl.lat_p2m_ncol * kLatSRows;  // S scratch behind the near-field slots
     pl.sym = true;
     pl.lat = true;
     return true;

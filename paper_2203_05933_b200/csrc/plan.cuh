@@ -245,6 +245,13 @@ struct Plan {
     double lat_pairs_exec = 0.0;  // m^2 x 9 x leaves: multiply-adds per apply (boundary zeros included)
     DBuf<double> lat_K;           // [9][m / 32][32][m + 4]
     DBuf<int32_t> lat_nbr;        // [leaf][9]: first sorted charge of the neighbour leaf, -1 outside
+    // lattice P2M: power sums of the pattern by one GEMM, per-leaf binomial shift (lattice.cu)
+    bool lat_p2m = false;
+    int64_t lat_p2m_ncol = 0, lat_near_parts = 0;
+    DBuf<double> lat_V;           // [m / 32][32][128 + 4]: re / im rows of w0^i
+    DBuf<double> lat_binom;       // [51][51] binomial coefficients of the shift
+    DBuf<int32_t> lat_p2m_src, lat_p2m_rows;  // per non-empty leaf: first sorted charge, multipole row
+    DBuf<double2> lat_drift;      // per non-empty leaf: (translation - box-centre offset) / box side
     std::vector<LeafNear> h_leafnear;
     int64_t n_p2p_chunks = 0;
     int64_t n_p2p_heavy = 0;  // split chunks (counters)
@@ -401,6 +408,7 @@ void build_m2l_grid(Plan& pl, int64_t lb, int64_t le);  // m2lgrid.cu
 void m2l_grid_issue(const Plan& pl, const double2* mult, double2* loc, cudaStream_t st);
 bool build_lattice_near(Plan& pl, int64_t lb, int64_t le);  // lattice.cu
 void lattice_near_issue(const Plan& pl, const double* qs, double* near, cudaStream_t st);
+void lattice_p2m_issue(const Plan& pl, const double* qs, double* S, double2* mult, cudaStream_t st);
 void build_helm_fmm(Plan& pl);  // native mode (helm.cu)
 void hf_build_m2l(Plan& pl, int64_t lb, int64_t le);  // its M2L schedule for the targets of a leaf range
 size_t helm_work_bytes(const Plan& pl);  // Chebyshev FMM apply scratch (helm.cu)
