@@ -218,7 +218,7 @@ constexpr int kLatSRows = 128;
 
 __global__ void __launch_bounds__(128)
 lat_p2m_shift_kernel(const double* S, const double2* drift, const int32_t* rows, const double* binom, int ncol,
-                     int P, double2* mult) {
+                     int P, int J, double2* mult) {
     __shared__ double2 sp[4][64], dp[4][64];
     __shared__ double bsm[51 * 51];  // C(k, i): lanes differ in k, so not the constant bank
     for (int i = threadIdx.x; i < 51 * 51; i += blockDim.x) bsm[i] = binom[i];
@@ -252,9 +252,12 @@ lat_p2m_shift_kernel(const double* S, const double2* drift, const int32_t* rows,
             const int kmax = min(31 + 32 * h, P);  // the warp's longest sum: one trip count for every lane
             const double* brow = bsm + kk * 51;
             double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;  // two interleaved partial sums (even / odd i)
-            for (int i = 0; i <= kmax; i += 2) {
+            // terms with k - i > J are below 1e-17 of the coefficient's scale (J from the plan's
+            // largest drift, build_lattice_p2m): the warp starts at its smallest useful i
+            const int ilo = max(0, (32 * h - J) & ~1);
+            for (int i = ilo; i <= kmax; i += 2) {
                 const int j0 = kk - i, j1 = kk - i - 1;
-                const double c0 = i <= kk ? brow[i] : 0.0, c1 = i + 1 <= kk ? brow[i + 1] : 0.0;
+                const double c0 = (i <= kk && j0 <= J) ? brow[i] : 0.0, c1 = (i + 1 <= kk && j1 <= J) ? brow[i + 1] : 0.0;
                 const double2 s0 = sp[warp][i], s1 = sp[warp][min(i + 1, P)];
                 const double2 t0 = dp[warp][max(j0, 0)], t1 = dp[warp][max(j1, 0)];
                 ar = fma(c0, s0.x * t0.x - s0.y * t0.y, ar);
@@ -300,7 +303,8 @@ void lattice_p2m_issue(const Plan& pl, const double* qs, double* S, double2* mul
     }
     const unsigned grid = unsigned(std::min<int64_t>((pl.lat_p2m_ncol + 3) / 4, int64_t(pl.sm_count) * 8));
     launch_pdl(lat_p2m_shift_kernel, dim3(grid), dim3(128), 0, st, (const double*)S, (const double2*)pl.lat_drift.p,
-               (const int32_t*)pl.lat_p2m_rows.p, (const double*)pl.lat_binom.p, int(pl.lat_p2m_ncol), pl.P, mult);
+               (const int32_t*)pl.lat_p2m_rows.p, (const double*)pl.lat_binom.p, int(pl.lat_p2m_ncol), pl.P,
+               pl.lat_shift_terms, mult);
 }
 
 // Host side of the lattice P2M (called by build_lattice_near once the pattern is verified).
@@ -344,6 +348,20 @@ static void build_lattice_p2m(Plan& pl, const double2* pat, int64_t first, doubl
         ++items;
     }
     if (items != pl.n_p2m_items) return;  // the P2M items are exactly the non-empty leaves
+    // shift series cut: C(P, J) (dmax / 0.7)^J < 1e-17 of the coefficient's scale sum |q| 0.7^k
+    // (|w0| <= sqrt(2)/2); cfg4: dmax = 0.02, J = 20
+    double dmax = 0.0;
+    for (const double2& d : drift) dmax = std::max(dmax, std::hypot(d.x, d.y));
+    int J = P;
+    for (int j = 1; j <= P; ++j) {
+        double c = 1.0;
+        for (int t = 1; t <= j; ++t) c *= double(P - j + t) / t;  // C(P, j)
+        if (c * std::pow(dmax / 0.7, j) < 1e-17) {
+            J = j;
+            break;
+        }
+    }
+    pl.lat_shift_terms = J;
     std::vector<double> binom(51 * 51, 0.0);
     for (int k = 0; k <= 50; ++k) {
         binom[size_t(k) * 51] = 1.0;

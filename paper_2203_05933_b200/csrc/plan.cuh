@@ -248,6 +248,7 @@ struct Plan {
     // lattice P2M: power sums of the pattern by one GEMM, per-leaf binomial shift (lattice.cu)
     bool lat_p2m = false;
     int64_t lat_p2m_ncol = 0, lat_near_parts = 0;
+    int lat_shift_terms = 0;      // the shift series keeps k - i <= this
     DBuf<double> lat_V;           // [m / 32][32][128 + 4]: re / im rows of w0^i
     DBuf<double> lat_binom;       // [51][51] binomial coefficients of the shift
     DBuf<int32_t> lat_p2m_src, lat_p2m_rows;  // per non-empty leaf: first sorted charge, multipole row
