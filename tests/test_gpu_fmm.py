@@ -381,6 +381,12 @@ def test_lattice_near_field(vp, rest, monkeypatch, nx, ny, m):
         plan.set_shard(0, 4 ** plan.levels())
         assert np.array_equal(total, lat)
         assert np.array_equal(plan.apply(q), lat)
+    monkeypatch.setenv("VPG_LATTICE_P2M", "0")  # the lattice near field with the pairwise P2M kernel
+    with vp.SummationPlan(lap(vp), pts, pts, 1e-12) as plan:
+        assert plan.info()["near_lattice"] == 1
+        lat_p2m0 = plan.apply(q)
+    monkeypatch.delenv("VPG_LATTICE_P2M")
+    assert rel_l2(lat, lat_p2m0) <= 1e-14
     monkeypatch.setenv("VPG_LATTICE", "0")
     with vp.SummationPlan(lap(vp), pts, pts, 1e-12) as plan:
         assert plan.info()["near_lattice"] == 0
