@@ -192,7 +192,10 @@ int64_t Plan::device_bytes() const {
                    l2l_ops.bytes() + h_t.bytes() + dpow.bytes() + logmd.bytes() +
                    p2p_chunks.bytes() + near_ranges.bytes() + row_level.bytes() + row_morton.bytes() +
                    row_parent.bytes() + tgt_row.bytes() + p2m_items.bytes() + p2m_splits.bytes() + updown_boxes.bytes() + updown_kids.bytes() + row_chain.bytes() +
-                   helm_nodes.bytes() + helm_bw.bytes() + exp_off_dev.bytes());
+                   helm_nodes.bytes() + helm_bw.bytes() + exp_off_dev.bytes() + sym_tasks.bytes() + sym_ranges.bytes() +
+                   sym_leaves.bytes() + lat_K.bytes() + lat_nbr.bytes() + lat_V.bytes() + lat_binom.bytes() +
+                   lat_p2m_src.bytes() + lat_p2m_rows.bytes() + lat_drift.bytes() + gt_tiles.bytes() + gt_rows.bytes() +
+                   gt_nbr.bytes() + gt_oidx.bytes());
 }
 
 // Runs f, mapping exceptions to status codes + thread-local message.
